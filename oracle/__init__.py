@@ -1,0 +1,287 @@
+"""ctypes front-end of the fp64 CPU oracle (oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: import this from tests/, __graft_entry__.smoke() or
+bench.py's cpu_baseline / ``--impl reference`` legs, never from the product
+package.  It shares no code with the CUDA path.
+
+Every function takes plain numpy arrays (float32 inputs exactly as the CUDA
+path receives them) and returns float64 results.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with g++ (fp64, no -ffast-math)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC",
+                               _SRC, "-o", _SO + ".tmp"])
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+class or_params(C.Structure):
+    _fields_ = [("k", C.c_int32), ("n_nbr", C.c_int32),
+                ("w_data", C.c_double), ("w_pt", C.c_double), ("w_reg", C.c_double), ("w_corr", C.c_double),
+                ("eps_d", C.c_double), ("eps_n_deg", C.c_double),
+                ("tau_z", C.c_double), ("delta_deg", C.c_double), ("trunc", C.c_double), ("omega_max", C.c_double),
+                ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_double),
+                ("solve_mode", C.c_int32)]
+
+
+class or_frame(C.Structure):
+    _fields_ = [("W", C.c_int32), ("H", C.c_int32),
+                ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("depth", C.c_void_p), ("pose", C.c_double * 12)]
+
+
+class or_problem(C.Structure):
+    _fields_ = [("n", C.c_int64), ("xyz", C.c_void_p), ("nrm", C.c_void_p),
+                ("idx", C.c_void_p), ("w", C.c_void_p),
+                ("m", C.c_int32), ("g", C.c_void_p), ("nbr", C.c_void_p),
+                ("nf", C.c_int32), ("fsrc", C.c_void_p), ("fdst", C.c_void_p)]
+
+
+class or_model(C.Structure):
+    _fields_ = [("n", C.c_int64), ("xyz", C.c_void_p), ("nrm", C.c_void_p), ("rgb", C.c_void_p),
+                ("weight", C.c_void_p), ("stamp", C.c_void_p)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_SO)
+            P = C.POINTER
+            L.or_frame_prep.argtypes = [P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_skin.argtypes = [C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                  C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_exp.argtypes = [C.c_void_p, C.c_void_p]
+            L.or_warp.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_associate.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_system.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_int64,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_system.restype = C.c_int64
+            L.or_residuals.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+            L.or_residuals.restype = C.c_int64
+            L.or_solve.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_double, C.c_int32, C.c_int32, C.c_void_p]
+            L.or_solve.restype = C.c_int32
+            L.or_register.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_warp_model.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_fuse.argtypes = [P(or_params), P(or_model), P(or_frame), C.c_void_p, C.c_int32, C.c_int32,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]
+            L.or_fuse.restype = C.c_int64
+            _lib = L
+    return _lib
+
+
+# ---------------------------------------------------------------- marshalling
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+PAPER_DEFAULTS = dict(k=4, n_nbr=4, w_data=1.0, w_pt=1.0, w_reg=1e4, w_corr=10.0,
+                      eps_d=15.0, eps_n_deg=10.0, tau_z=10.0, delta_deg=10.0, trunc=40.0, omega_max=10.0,
+                      gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1)
+
+
+def params(**kw) -> or_params:
+    d = dict(PAPER_DEFAULTS)
+    d.update(kw)
+    return or_params(**d)
+
+
+class Frame:
+    """Owns the arrays an or_frame points to."""
+
+    def __init__(self, depth, intr, pose):
+        self.depth = _f32(depth)
+        H, W = self.depth.shape
+        self.s = or_frame(W, H, intr["fx"], intr["fy"], intr["cx"], intr["cy"], _p(self.depth),
+                          (C.c_double * 12)(*[float(x) for x in np.asarray(pose, np.float64).ravel()]))
+
+
+class Problem:
+    def __init__(self, xyz, nrm, idx, w, g, nbr, fsrc=None, fdst=None):
+        self.xyz, self.nrm = _f32(xyz), _f32(nrm)
+        self.idx, self.w = _i32(idx), _f32(w)
+        self.g, self.nbr = _f32(g), _i32(nbr)
+        self.k = self.idx.shape[1]
+        self.n_nbr = self.nbr.shape[1]
+        self.fsrc = _f32(fsrc if fsrc is not None else np.zeros((0, 3)))
+        self.fdst = _f32(fdst if fdst is not None else np.zeros((0, 3)))
+        self.s = or_problem(self.xyz.shape[0], _p(self.xyz), _p(self.nrm), _p(self.idx), _p(self.w),
+                            self.g.shape[0], _p(self.g), _p(self.nbr),
+                            self.fsrc.shape[0], _p(self.fsrc), _p(self.fdst))
+
+
+def identity_state(m):
+    Rt = np.zeros((m, 12))
+    Rt[:, 0] = Rt[:, 4] = Rt[:, 8] = 1.0
+    return Rt
+
+
+def frame_prep(fr: Frame):
+    H, W = fr.depth.shape
+    q = np.zeros((H, W, 3)); N = np.zeros((H, W, 3))
+    dv = np.zeros((H, W), np.uint8); nv = np.zeros((H, W), np.uint8)
+    lib().or_frame_prep(C.byref(fr.s), _p(q), _p(N), _p(dv), _p(nv))
+    return q, N, dv.astype(bool), nv.astype(bool)
+
+
+def skin(points, g, k):
+    points, g = _f32(points), _f32(g)
+    n = points.shape[0]
+    idx = np.zeros((n, k), np.int32); w = np.zeros((n, k)); mg = np.zeros(n)
+    lib().or_skin(n, _p(points), g.shape[0], _p(g), k, _p(idx), _p(w), _p(mg))
+    return idx, w, mg
+
+
+def exp_so3(w):
+    w = np.ascontiguousarray(w, np.float64); R = np.zeros(9)
+    lib().or_exp(_p(w), _p(R))
+    return R.reshape(3, 3)
+
+
+def warp(pb: Problem, Rt, pose):
+    n = pb.xyz.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64); pose = np.ascontiguousarray(pose, np.float64)
+    xh = np.zeros((n, 3)); nh = np.zeros((n, 3)); vt = np.zeros((n, 3)); nt = np.zeros((n, 3))
+    ok = np.zeros(n, np.uint8)
+    lib().or_warp(C.byref(pb.s), pb.k, _p(Rt), _p(pose), _p(xh), _p(nh), _p(vt), _p(nt), _p(ok))
+    return xh, nh, vt, nt, ok.astype(bool)
+
+
+def associate(prm: or_params, pb: Problem, fr: Frame, Rt):
+    n = pb.xyz.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    pix = np.zeros(n, np.int32); why = np.zeros(n, np.uint8); mg = np.zeros(n)
+    lib().or_associate(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pix), _p(why), _p(mg))
+    return pix, why, mg
+
+
+def feature_skin(pb: Problem):
+    if pb.fsrc.shape[0] == 0:
+        return np.zeros((0, pb.k), np.int32), np.zeros((0, pb.k)), np.zeros(0)
+    return skin(pb.fsrc, pb.g, pb.k)
+
+
+def system(prm: or_params, pb: Problem, fr: Frame, Rt, fskin=None):
+    """Returns dict(blocks={(j,l): 6x6}, rows, cols, vals, rhs, energy, n_assoc)."""
+    m = pb.g.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    rhs = np.zeros(6 * m); E = np.zeros(5); na = np.zeros(1, np.int64)
+    cap = 0
+    z = np.zeros(1, np.int32); zd = np.zeros(36)
+    nb = lib().or_system(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(fidx), _p(fw), cap,
+                         _p(z), _p(z), _p(zd), _p(rhs), _p(E), _p(na))
+    rows = np.zeros(nb, np.int32); cols = np.zeros(nb, np.int32); vals = np.zeros((nb, 36))
+    lib().or_system(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(fidx), _p(fw), nb,
+                    _p(rows), _p(cols), _p(vals), _p(rhs), _p(E), _p(na))
+    return dict(rows=rows, cols=cols, vals=vals.reshape(nb, 6, 6), rhs=rhs, energy=E, n_assoc=int(na[0]))
+
+
+def dense_H(sysd, m):
+    H = np.zeros((6 * m, 6 * m))
+    for r, c, B in zip(sysd["rows"], sysd["cols"], sysd["vals"]):
+        H[6 * r:6 * r + 6, 6 * c:6 * c + 6] += B
+        if r != c:
+            H[6 * c:6 * c + 6, 6 * r:6 * r + 6] += B.T
+    return H
+
+
+def residuals(prm: or_params, pb: Problem, fr: Frame, Rt, pix_frozen, fskin=None):
+    m = pb.g.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    pix_frozen = _i32(pix_frozen)
+    cap = 4 * pb.xyz.shape[0] + 3 * m * pb.n_nbr + 3 * pb.fsrc.shape[0]
+    r = np.zeros(cap); J = np.zeros((cap, 6 * m))
+    nr = lib().or_residuals(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pix_frozen), _p(fidx), _p(fw),
+                            cap, _p(r), _p(J))
+    assert nr >= 0
+    return r[:nr], J[:nr]
+
+
+def solve(sysd, m, lam, mode, pcg_iters):
+    x = np.zeros(6 * m)
+    nb = len(sysd["rows"])
+    vals = np.ascontiguousarray(sysd["vals"].reshape(nb, 36), np.float64)
+    it = lib().or_solve(m, nb, _p(_i32(sysd["rows"])), _p(_i32(sysd["cols"])), _p(vals),
+                        _p(np.ascontiguousarray(sysd["rhs"], np.float64)), lam, mode, pcg_iters, _p(x))
+    return x, it
+
+
+def register(prm: or_params, pb: Problem, fr: Frame, Rt0=None):
+    m = pb.g.shape[0]
+    Rt = identity_state(m) if Rt0 is None else np.array(Rt0, np.float64, copy=True)
+    G = prm.gn_iters
+    E = np.zeros((G + 1, 5)); na = np.zeros(G + 1, np.int64)
+    lib().or_register(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(E), _p(na))
+    return Rt, E, na
+
+
+def warp_model(pb: Problem, Rt):
+    n, m = pb.xyz.shape[0], pb.g.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    xyz = np.zeros((n, 3)); nrm = np.zeros((n, 3)); g = np.zeros((m, 3))
+    lib().or_warp_model(C.byref(pb.s), pb.k, _p(Rt), _p(xyz), _p(nrm), _p(g))
+    return xyz, nrm, g
+
+
+def fuse(prm: or_params, xyz, nrm, rgb, weight, stamp, fr: Frame, rgb_obs, frame_index, g):
+    xyz, nrm, rgb, weight = _f32(xyz), _f32(nrm), _f32(rgb), _f32(weight)
+    stamp = _i32(stamp); g = _f32(g)
+    n = xyz.shape[0]
+    H, W = fr.depth.shape
+    cap = n + H * W
+    k = prm.k
+    md = or_model(n, _p(xyz), _p(nrm), _p(rgb), _p(weight), _p(stamp))
+    ro = None if rgb_obs is None else _f32(rgb_obs)
+    out = dict(xyz=np.zeros((cap, 3)), nrm=np.zeros((cap, 3)), rgb=np.zeros((cap, 3)),
+               weight=np.zeros(cap), stamp=np.zeros(cap, np.int32),
+               lift_idx=np.zeros((H * W, k), np.int32), lift_w=np.zeros((H * W, k)), lift_margin=np.zeros(H * W),
+               owner=np.zeros(H * W, np.int64), key_margin=np.zeros(H * W), why=np.zeros(n, np.uint8),
+               gate_margin=np.zeros(n))
+    nl = lib().or_fuse(C.byref(prm), C.byref(md), C.byref(fr.s), _p(ro), frame_index, g.shape[0], _p(g),
+                       _p(out["xyz"]), _p(out["nrm"]), _p(out["rgb"]), _p(out["weight"]), _p(out["stamp"]),
+                       _p(out["lift_idx"]), _p(out["lift_w"]), _p(out["lift_margin"]),
+                       _p(out["owner"]), _p(out["key_margin"]), _p(out["why"]), _p(out["gate_margin"]))
+    for key in ("xyz", "nrm", "rgb", "weight", "stamp"):
+        out[key] = out[key][:n + nl]
+    for key in ("lift_idx", "lift_w", "lift_margin"):
+        out[key] = out[key][:nl]
+    out["n_lift"] = int(nl)
+    return out

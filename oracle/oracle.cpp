@@ -1,0 +1,856 @@
+// oracle.cpp -- plain fp64 CPU oracle of the MIS-SLAM registration hot path.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle.h).  Written from PAPER.md and the
+// readings in DESIGN.md §3 in the paper's order and notation; no blocking,
+// fusion or reordering beyond what the definitions state.  Shares no code with
+// the CUDA path.
+//
+// Citations: P:n = PAPER.md line n (section / equation / algorithm named
+// beside it); S:n = SPEC.md line n; R-An = DESIGN.md reading An.
+#include "oracle.h"
+
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <utility>
+#include <vector>
+#include <algorithm>
+
+namespace {
+
+typedef std::array<double, 3> V3;
+typedef std::array<double, 9> M3;     // row-major
+typedef std::array<double, 36> B6;    // 6x6 row-major
+
+const double kInf = std::numeric_limits<double>::infinity();
+
+V3 v3(double a, double b, double c) { V3 r = {a, b, c}; return r; }
+V3 load3(const float* p) { return v3((double)p[0], (double)p[1], (double)p[2]); }
+V3 add(const V3& a, const V3& b) { return v3(a[0] + b[0], a[1] + b[1], a[2] + b[2]); }
+V3 sub(const V3& a, const V3& b) { return v3(a[0] - b[0], a[1] - b[1], a[2] - b[2]); }
+V3 scale(const V3& a, double s) { return v3(a[0] * s, a[1] * s, a[2] * s); }
+double dot(const V3& a, const V3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+double norm(const V3& a) { return std::sqrt(dot(a, a)); }
+V3 cross(const V3& a, const V3& b) {
+  return v3(a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]);
+}
+V3 mul(const M3& R, const V3& x) {
+  return v3(R[0] * x[0] + R[1] * x[1] + R[2] * x[2],
+            R[3] * x[0] + R[4] * x[1] + R[5] * x[2],
+            R[6] * x[0] + R[7] * x[1] + R[8] * x[2]);
+}
+V3 mulT(const M3& R, const V3& x) {   // R^T x
+  return v3(R[0] * x[0] + R[3] * x[1] + R[6] * x[2],
+            R[1] * x[0] + R[4] * x[1] + R[7] * x[2],
+            R[2] * x[0] + R[5] * x[1] + R[8] * x[2]);
+}
+M3 matmul(const M3& A, const M3& B) {
+  M3 C;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int l = 0; l < 3; ++l) s += A[3 * i + l] * B[3 * l + j];
+      C[3 * i + j] = s;
+    }
+  return C;
+}
+M3 node_R(const double* Rt, int j) { M3 R; for (int a = 0; a < 9; ++a) R[a] = Rt[12 * j + a]; return R; }
+V3 node_t(const double* Rt, int j) { return v3(Rt[12 * j + 9], Rt[12 * j + 10], Rt[12 * j + 11]); }
+M3 pose_R(const double* pose) { M3 R; for (int a = 0; a < 9; ++a) R[a] = pose[a]; return R; }
+V3 pose_T(const double* pose) { return v3(pose[9], pose[10], pose[11]); }
+
+bool depth_ok(float d) { return std::isfinite(d) && d > 0.0f; }
+
+// ---- O0: back-projection Pi(u, D) ("back-projection function")
+V3 back_project(const or_frame* f, int x, int y, double D) {
+  return v3(((double)x - f->cx) * D / f->fx, ((double)y - f->cy) * D / f->fy, D);
+}
+
+// Central-difference normal, R-A11 (paper silent on the estimator):
+// N = normalize((q(x+1,y)-q(x-1,y)) x (q(x,y+1)-q(x,y-1))), flipped so N.q < 0.
+bool pixel_normal(const or_frame* f, int x, int y, V3* N) {
+  const int W = f->W, H = f->H;
+  if (x <= 0 || y <= 0 || x >= W - 1 || y >= H - 1) return false;
+  const float* D = f->depth;
+  float c = D[y * W + x], l = D[y * W + x - 1], r = D[y * W + x + 1];
+  float u = D[(y - 1) * W + x], d = D[(y + 1) * W + x];
+  if (!depth_ok(c) || !depth_ok(l) || !depth_ok(r) || !depth_ok(u) || !depth_ok(d)) return false;
+  V3 dx = sub(back_project(f, x + 1, y, r), back_project(f, x - 1, y, l));
+  V3 dy = sub(back_project(f, x, y + 1, d), back_project(f, x, y - 1, u));
+  V3 n = cross(dx, dy);
+  double len = norm(n);
+  if (len < 1e-12) return false;
+  n = scale(n, 1.0 / len);
+  if (dot(n, back_project(f, x, y, c)) > 0) n = scale(n, -1.0);
+  *N = n;
+  return true;
+}
+
+// ---- Eq. 2 skinning, normalised (R-A6); ties -> lower id
+void skin_one(const V3& v, int m, const float* g, int k, int32_t* idx, double* w, double* margin) {
+  // the k+1 smallest (distance, id) pairs in lexicographic order, by insertion
+  std::vector<std::pair<double, int> > d;
+  for (int j = 0; j < m; ++j) {
+    std::pair<double, int> c = std::make_pair(norm(sub(v, load3(g + 3 * j))), j);
+    if ((int)d.size() == k + 1 && !(c < d.back())) continue;
+    if ((int)d.size() == k + 1) d.pop_back();
+    d.insert(std::upper_bound(d.begin(), d.end(), c), c);   // equal distances -> lower id first
+  }
+  double dmax = d[k].first;        // distance to the (k+1)-th nearest node
+  double sum = 0;
+  for (int s = 0; s < k; ++s) {
+    idx[s] = d[s].second;
+    w[s] = (dmax > 0) ? 1.0 - d[s].first / dmax : 1.0 / k;   // d_max = 0 -> 1/k
+    sum += w[s];
+  }
+  for (int s = 0; s < k; ++s) w[s] = (sum > 0) ? w[s] / sum : 1.0 / k;
+  if (margin) *margin = (d[k].first > 0) ? (d[k].first - d[k - 1].first) / d[k].first : 0.0;
+}
+
+// ---- O3a: Eq. 1 warp with A_j = R_j (R-A1) and normalised weights (R-A6)
+// x_hat = sum_j w_j (R_j (v - g_j) + g_j + t_j);  v~ = R x_hat + T;
+// m_hat = sum_j w_j R_j n;  n~ = R m_hat / |m_hat|.
+struct Warped {
+  bool ok;
+  double wn[8];      // normalised weights
+  V3 a[8];           // a_j = R_j (v - g_j)
+  V3 x_hat, m_hat, vt, nt;
+};
+
+Warped warp_point(const V3& v, const V3& n, int k, const int32_t* idx, const double* wraw,
+                  const float* g, const double* Rt, const double* pose) {
+  Warped o;
+  o.ok = false;
+  double W = 0;
+  for (int s = 0; s < k; ++s) W += wraw[s];
+  if (!(W > 0)) return o;
+  o.x_hat = v3(0, 0, 0);
+  o.m_hat = v3(0, 0, 0);
+  for (int s = 0; s < k; ++s) {
+    int j = idx[s];
+    o.wn[s] = wraw[s] / W;
+    M3 Rj = node_R(Rt, j);
+    V3 gj = load3(g + 3 * j);
+    o.a[s] = mul(Rj, sub(v, gj));
+    o.x_hat = add(o.x_hat, scale(add(add(o.a[s], gj), node_t(Rt, j)), o.wn[s]));
+    o.m_hat = add(o.m_hat, scale(mul(Rj, n), o.wn[s]));
+  }
+  M3 R = pose_R(pose);
+  o.vt = add(mul(R, o.x_hat), pose_T(pose));
+  double ml = norm(o.m_hat);
+  if (ml < 1e-12) return o;
+  o.nt = mul(R, scale(o.m_hat, 1.0 / ml));
+  o.ok = true;
+  return o;
+}
+
+// ---- Projection P and pixel rounding floor(u + 0.5) (R-A10)
+struct Proj { bool z_ok, in_frame; int px, py; double margin; };
+Proj project(const or_frame* f, const V3& p) {
+  Proj r;
+  r.z_ok = p[2] > 0;
+  r.in_frame = false;
+  r.px = r.py = -1;
+  r.margin = std::fabs(p[2]);
+  if (!r.z_ok) return r;
+  double u = f->fx * p[0] / p[2] + f->cx;
+  double v = f->fy * p[1] / p[2] + f->cy;
+  double fu = std::floor(u + 0.5), fv = std::floor(v + 0.5);
+  double mu = std::min(u + 0.5 - fu, fu + 1.0 - (u + 0.5));   // distance of u+0.5 to an integer
+  double mv = std::min(v + 0.5 - fv, fv + 1.0 - (v + 0.5));
+  r.margin = std::min(r.margin, std::min(mu, mv));
+  if (fu < 0 || fv < 0 || fu >= f->W || fv >= f->H) return r;
+  r.px = (int)fu;
+  r.py = (int)fv;
+  r.in_frame = true;
+  return r;
+}
+
+// ---- O3b: Eq. 7 gates with the warped point (R-A7), angle < eps_n (R-A8)
+struct Assoc { int32_t pix; uint8_t why; double margin; V3 q, N; };
+Assoc associate_point(const or_params* prm, const or_frame* f, const Warped& w) {
+  Assoc a;
+  a.pix = -1;
+  a.why = 0;
+  a.margin = kInf;
+  if (!w.ok) return a;
+  Proj pr = project(f, w.vt);
+  a.margin = pr.margin;
+  if (!pr.z_ok) return a;
+  a.why |= OR_Z;
+  if (!pr.in_frame) return a;
+  a.why |= OR_FRAME;
+  float D = f->depth[pr.py * f->W + pr.px];
+  if (!depth_ok(D)) return a;
+  a.why |= OR_DEPTH;
+  if (!pixel_normal(f, pr.px, pr.py, &a.N)) return a;
+  a.why |= OR_NORMAL;
+  a.q = back_project(f, pr.px, pr.py, (double)D);
+  double d = norm(sub(w.vt, a.q));
+  a.margin = std::min(a.margin, std::fabs(d - prm->eps_d) / prm->eps_d);
+  if (!(d < prm->eps_d)) return a;
+  a.why |= OR_DIST;
+  double c = dot(w.nt, a.N), ce = std::cos(prm->eps_n_deg * M_PI / 180.0);
+  a.margin = std::min(a.margin, std::fabs(c - ce));
+  if (!(c > ce)) return a;
+  a.why |= OR_ANGLE;
+  a.pix = pr.py * f->W + pr.px;
+  return a;
+}
+
+// ---- block-sparse normal equations: upper blocks (j <= l), full 6x6 each
+struct System {
+  int m;
+  std::map<std::pair<int, int>, B6> blk;
+  std::vector<double> rhs;
+  double E[4];
+  int64_t n_assoc;
+  explicit System(int m_) : m(m_), rhs(6 * m_, 0.0), n_assoc(0) { E[0] = E[1] = E[2] = E[3] = 0; }
+  // H += w * Ja^T Jb for rows r (Ja: rows x 6 for node a, Jb for node b)
+  void add_pair(int a, const double* Ja, int b, const double* Jb, int rows, double w) {
+    if (a <= b) {
+      B6& B = blk[std::make_pair(a, b)];
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+          double s = 0;
+          for (int r = 0; r < rows; ++r) s += Ja[6 * r + i] * Jb[6 * r + j];
+          B[6 * i + j] += w * s;
+        }
+    } else {
+      B6& B = blk[std::make_pair(b, a)];
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+          double s = 0;
+          for (int r = 0; r < rows; ++r) s += Jb[6 * r + i] * Ja[6 * r + j];
+          B[6 * i + j] += w * s;
+        }
+    }
+  }
+  // rhs_a -= w * Ja^T r
+  void add_rhs(int a, const double* Ja, const double* r, int rows, double w) {
+    for (int i = 0; i < 6; ++i) {
+      double s = 0;
+      for (int q = 0; q < rows; ++q) s += Ja[6 * q + i] * r[q];
+      rhs[6 * a + i] -= w * s;
+    }
+  }
+};
+
+// J_pt,j = w_j R [-[a_j]x, I]  (3x6), from dv~/d(dtheta_j) = -w_j R [a_j]x (left update, R-A18)
+void jac_point(const M3& R, double wj, const V3& a, double* J) {
+  // -[a]x = [[0, a2, -a1], [-a2, 0, a0], [a1, -a0, 0]]
+  double S[9] = {0, a[2], -a[1], -a[2], 0, a[0], a[1], -a[0], 0};
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) {
+      double s = 0, t = 0;
+      for (int l = 0; l < 3; ++l) { s += R[3 * r + l] * S[3 * l + c]; }
+      t = R[3 * r + c];
+      J[6 * r + c] = wj * s;
+      J[6 * r + 3 + c] = wj * t;
+    }
+  }
+}
+
+// Point term rows for one associated point: plane (1 row) and point (3 rows)
+void point_rows(const M3& R, const Warped& w, const Assoc& as, int k,
+                double* Jpl /*k x 6*/, double* Jpt /*k x 18*/, double* rpl, double* rpt) {
+  // Eq. 8: r_pl = N^T (v~ - q); north_star point-to-point: r_pt = v~ - q
+  V3 d = sub(w.vt, as.q);
+  *rpl = dot(as.N, d);
+  rpt[0] = d[0]; rpt[1] = d[1]; rpt[2] = d[2];
+  V3 np = mulT(R, as.N);   // n' = R^T N
+  for (int s = 0; s < k; ++s) {
+    V3 c = cross(w.a[s], np);   // d r_pl / d dtheta_j = w_j (a_j x n')^T
+    for (int i = 0; i < 3; ++i) {
+      Jpl[6 * s + i] = w.wn[s] * c[i];
+      Jpl[6 * s + 3 + i] = w.wn[s] * np[i];
+    }
+    jac_point(R, w.wn[s], w.a[s], Jpt + 18 * s);
+  }
+}
+
+// Eq. 6, alpha = 1, directed edges (R-A14):
+// e = R_j (g_l - g_j) + g_j + t_j - g_l - t_l; J_j = [-[b]x, I], J_l = [0, -I], b = R_j (g_l - g_j)
+void reg_edge(const or_problem* p, const double* Rt, int j, int l, double* e, double* Jj, double* Jl) {
+  V3 gj = load3(p->g + 3 * j), gl = load3(p->g + 3 * l);
+  V3 b = mul(node_R(Rt, j), sub(gl, gj));
+  V3 ev = sub(add(add(b, gj), node_t(Rt, j)), add(gl, node_t(Rt, l)));
+  e[0] = ev[0]; e[1] = ev[1]; e[2] = ev[2];
+  double S[9] = {0, b[2], -b[1], -b[2], 0, b[0], b[1], -b[0], 0};   // -[b]x
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      Jj[6 * r + c] = S[3 * r + c];
+      Jj[6 * r + 3 + c] = (r == c) ? 1.0 : 0.0;
+      Jl[6 * r + c] = 0.0;
+      Jl[6 * r + 3 + c] = (r == c) ? -1.0 : 0.0;
+    }
+}
+
+// Eq. 9, squared 3-vector residual (R-A12): e_f = warp(V_f) - V'_f
+bool feature_rows(const or_problem* p, int k, const double* Rt, const double* pose, int f,
+                  const int32_t* fidx, const double* fw, Warped* w, double* e, double* J) {
+  V3 v = load3(p->fsrc + 3 * f);
+  *w = warp_point(v, v3(0, 0, 1), k, fidx + k * f, fw + k * f, p->g, Rt, pose);
+  double W = 0;
+  for (int s = 0; s < k; ++s) W += fw[k * f + s];
+  if (!(W > 0)) return false;
+  V3 d = sub(w->vt, load3(p->fdst + 3 * f));
+  e[0] = d[0]; e[1] = d[1]; e[2] = d[2];
+  M3 R = pose_R(pose);
+  for (int s = 0; s < k; ++s) jac_point(R, w->wn[s], w->a[s], J + 18 * s);
+  return true;
+}
+
+void wraw_of(const or_problem* p, int k, int64_t i, double* wr) {
+  for (int s = 0; s < k; ++s) wr[s] = (double)p->w[k * i + s];
+}
+
+void assemble(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+              const int32_t* fidx, const double* fw, System* S) {
+  const int k = prm->k;
+  M3 R = pose_R(f->pose);
+  double Jpl[8 * 6], Jpt[8 * 18], rpl, rpt[3];
+  // O3a-d, O3g: data (Eq. 8) and dense point-to-point terms
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
+    Assoc as = associate_point(prm, f, w);
+    if (as.pix < 0) continue;
+    S->n_assoc++;
+    point_rows(R, w, as, k, Jpl, Jpt, &rpl, rpt);
+    S->E[0] += rpl * rpl;
+    S->E[1] += rpt[0] * rpt[0] + rpt[1] * rpt[1] + rpt[2] * rpt[2];
+    for (int a = 0; a < k; ++a) {
+      int ja = p->idx[k * i + a];
+      for (int b = 0; b < k; ++b) {
+        int jb = p->idx[k * i + b];
+        if (ja > jb || (ja == jb && a > b)) continue;   // each unordered slot pair once
+        S->add_pair(ja, Jpl + 6 * a, jb, Jpl + 6 * b, 1, prm->w_data);
+        S->add_pair(ja, Jpt + 18 * a, jb, Jpt + 18 * b, 3, prm->w_pt);
+        if (ja == jb && a != b) {   // same node in two slots: add the mirrored product too
+          S->add_pair(jb, Jpl + 6 * b, ja, Jpl + 6 * a, 1, prm->w_data);
+          S->add_pair(jb, Jpt + 18 * b, ja, Jpt + 18 * a, 3, prm->w_pt);
+        }
+      }
+      S->add_rhs(ja, Jpl + 6 * a, &rpl, 1, prm->w_data);
+      S->add_rhs(ja, Jpt + 18 * a, rpt, 3, prm->w_pt);
+    }
+  }
+  // O3e: regulariser
+  double e[3], Jj[18], Jl[18];
+  for (int j = 0; j < p->m; ++j)
+    for (int s = 0; s < prm->n_nbr; ++s) {
+      int l = p->nbr[prm->n_nbr * j + s];
+      if (l < 0) continue;
+      reg_edge(p, Rt, j, l, e, Jj, Jl);
+      S->E[2] += e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+      S->add_pair(j, Jj, j, Jj, 3, prm->w_reg);
+      S->add_pair(l, Jl, l, Jl, 3, prm->w_reg);
+      S->add_pair(j, Jj, l, Jl, 3, prm->w_reg);
+      S->add_rhs(j, Jj, e, 3, prm->w_reg);
+      S->add_rhs(l, Jl, e, 3, prm->w_reg);
+    }
+  // O3f: features
+  double Jf[8 * 18];
+  for (int q = 0; q < p->nf; ++q) {
+    Warped w;
+    if (!feature_rows(p, k, Rt, f->pose, q, fidx, fw, &w, e, Jf)) continue;
+    S->E[3] += e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+    for (int a = 0; a < k; ++a) {
+      int ja = fidx[k * q + a];
+      for (int b = 0; b < k; ++b) {
+        int jb = fidx[k * q + b];
+        if (ja > jb || (ja == jb && a > b)) continue;
+        S->add_pair(ja, Jf + 18 * a, jb, Jf + 18 * b, 3, prm->w_corr);
+        if (ja == jb && a != b) S->add_pair(jb, Jf + 18 * b, ja, Jf + 18 * a, 3, prm->w_corr);
+      }
+      S->add_rhs(ja, Jf + 18 * a, e, 3, prm->w_corr);
+    }
+  }
+}
+
+double total_energy(const or_params* prm, const double* E) {
+  return prm->w_data * E[0] + prm->w_pt * E[1] + prm->w_reg * E[2] + prm->w_corr * E[3];
+}
+
+// ---- linear algebra for O3h
+// y = (H + lambda I) x with H given by its upper blocks
+void spmv(const System& S, double lambda, const std::vector<double>& x, std::vector<double>& y) {
+  std::fill(y.begin(), y.end(), 0.0);
+  for (std::map<std::pair<int, int>, B6>::const_iterator it = S.blk.begin(); it != S.blk.end(); ++it) {
+    int j = it->first.first, l = it->first.second;
+    const B6& B = it->second;
+    for (int a = 0; a < 6; ++a)
+      for (int b = 0; b < 6; ++b) {
+        y[6 * j + a] += B[6 * a + b] * x[6 * l + b];
+        if (j != l) y[6 * l + b] += B[6 * a + b] * x[6 * j + a];
+      }
+  }
+  for (size_t i = 0; i < y.size(); ++i) y[i] += lambda * x[i];
+}
+
+// in-place Cholesky A = L L^T (n x n, row-major); false if not positive definite
+bool cholesky(std::vector<double>& A, int n) {
+  for (int j = 0; j < n; ++j) {
+    double s = A[j * n + j];
+    for (int l = 0; l < j; ++l) s -= A[j * n + l] * A[j * n + l];
+    if (!(s > 0)) return false;
+    double d = std::sqrt(s);
+    A[j * n + j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double t = A[i * n + j];
+      for (int l = 0; l < j; ++l) t -= A[i * n + l] * A[j * n + l];
+      A[i * n + j] = t / d;
+    }
+  }
+  return true;
+}
+void chol_solve(const std::vector<double>& L, int n, const double* b, double* x) {
+  std::vector<double> y(n);
+  for (int i = 0; i < n; ++i) {
+    double s = b[i];
+    for (int l = 0; l < i; ++l) s -= L[i * n + l] * y[l];
+    y[i] = s / L[i * n + i];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int l = i + 1; l < n; ++l) s -= L[l * n + i] * x[l];
+    x[i] = s / L[i * n + i];
+  }
+}
+
+// Block-Jacobi preconditioner M_j = (H_jj + lambda I + mu_j I)^-1, mu_j = 1e-9 tr(H_jj)/6 (R-A17)
+void block_jacobi(const System& S, double lambda, std::vector<double>& Minv) {
+  Minv.assign(36 * S.m, 0.0);
+  for (int j = 0; j < S.m; ++j) {
+    std::vector<double> A(36, 0.0);
+    std::map<std::pair<int, int>, B6>::const_iterator it = S.blk.find(std::make_pair(j, j));
+    if (it != S.blk.end()) for (int a = 0; a < 36; ++a) A[a] = it->second[a];
+    double tr = A[0] + A[7] + A[14] + A[21] + A[28] + A[35];
+    double mu = 1e-9 * tr / 6.0;
+    for (int a = 0; a < 6; ++a) A[7 * a] += lambda + mu;
+    std::vector<double> L = A;
+    if (!cholesky(L, 6)) continue;   // leaves M_j = 0 (never happens with lambda > 0)
+    for (int c = 0; c < 6; ++c) {
+      double e[6] = {0, 0, 0, 0, 0, 0}, col[6];
+      e[c] = 1.0;
+      chol_solve(L, 6, e, col);
+      for (int r = 0; r < 6; ++r) Minv[36 * j + 6 * r + c] = col[r];
+    }
+  }
+}
+
+void apply_M(const std::vector<double>& Minv, int m, const std::vector<double>& r, std::vector<double>& z) {
+  for (int j = 0; j < m; ++j)
+    for (int a = 0; a < 6; ++a) {
+      double s = 0;
+      for (int b = 0; b < 6; ++b) s += Minv[36 * j + 6 * a + b] * r[6 * j + b];
+      z[6 * j + a] = s;
+    }
+}
+double vdot(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+// PCG from x0 = 0: fixed P iterations (MIRROR) or to a
+// relative residual of 1e-12 (EXACT for large systems).  Early stop if
+// r.z == 0 or p.Ap <= 0.
+int pcg(const System& S, double lambda, const std::vector<double>& b, int max_it, double rel_tol,
+        std::vector<double>& x) {
+  const int n = 6 * S.m;
+  std::vector<double> Minv, r(b), z(n), p(n), Ap(n);
+  block_jacobi(S, lambda, Minv);
+  x.assign(n, 0.0);
+  apply_M(Minv, S.m, r, z);
+  p = z;
+  double rz = vdot(r, z), b2 = vdot(b, b);
+  int it = 0;
+  for (; it < max_it; ++it) {
+    if (rel_tol > 0 && vdot(r, r) <= rel_tol * rel_tol * b2) break;
+    if (rz == 0) break;
+    spmv(S, lambda, p, Ap);
+    double pAp = vdot(p, Ap);
+    if (!(pAp > 0)) break;
+    double alpha = rz / pAp;
+    for (int i = 0; i < n; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * Ap[i]; }
+    apply_M(Minv, S.m, r, z);
+    double rz_new = vdot(r, z);
+    double beta = rz_new / rz;
+    rz = rz_new;
+    for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+  return it;
+}
+
+int solve_system(const System& S, double lambda, int mode, int pcg_iters, std::vector<double>& x) {
+  const int n = 6 * S.m;
+  if (mode == 1) return pcg(S, lambda, S.rhs, pcg_iters, 0.0, x);
+  if (n <= 600) {   // EXACT, small: dense Cholesky of H + lambda I
+    std::vector<double> A((size_t)n * n, 0.0);
+    for (std::map<std::pair<int, int>, B6>::const_iterator it = S.blk.begin(); it != S.blk.end(); ++it) {
+      int j = it->first.first, l = it->first.second;
+      for (int a = 0; a < 6; ++a)
+        for (int b = 0; b < 6; ++b) {
+          A[(size_t)(6 * j + a) * n + 6 * l + b] += it->second[6 * a + b];
+          if (j != l) A[(size_t)(6 * l + b) * n + 6 * j + a] += it->second[6 * a + b];
+        }
+    }
+    for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += lambda;
+    x.assign(n, 0.0);
+    if (!cholesky(A, n)) return -1;
+    chol_solve(A, n, S.rhs.data(), x.data());
+    return 0;
+  }
+  return pcg(S, lambda, S.rhs, 20 * n, 1e-12, x);
+}
+
+// O3i: R_j <- Exp(dtheta_j) R_j, t_j += dt_j (R-A18)
+void update_nodes(int m, const std::vector<double>& x, double* Rt) {
+  for (int j = 0; j < m; ++j) {
+    double w[3] = {x[6 * j], x[6 * j + 1], x[6 * j + 2]}, E[9];
+    or_exp(w, E);
+    M3 Em, Rj = node_R(Rt, j);
+    for (int a = 0; a < 9; ++a) Em[a] = E[a];
+    M3 Rn = matmul(Em, Rj);
+    for (int a = 0; a < 9; ++a) Rt[12 * j + a] = Rn[a];
+    for (int a = 0; a < 3; ++a) Rt[12 * j + 9 + a] += x[6 * j + 3 + a];
+  }
+}
+
+void feature_skin(const or_problem* p, int k, std::vector<int32_t>& fidx, std::vector<double>& fw) {
+  fidx.assign((size_t)k * p->nf, 0);
+  fw.assign((size_t)k * p->nf, 0.0);
+  for (int q = 0; q < p->nf; ++q)
+    skin_one(load3(p->fsrc + 3 * q), p->m, p->g, k, &fidx[k * q], &fw[k * q], nullptr);
+}
+
+}  // namespace
+
+extern "C" {
+
+void or_frame_prep(const or_frame* f, double* q, double* N, uint8_t* dvalid, uint8_t* nvalid) {
+  for (int y = 0; y < f->H; ++y)
+    for (int x = 0; x < f->W; ++x) {
+      int i = y * f->W + x;
+      float D = f->depth[i];
+      dvalid[i] = depth_ok(D) ? 1 : 0;
+      V3 qq = dvalid[i] ? back_project(f, x, y, (double)D) : v3(0, 0, 0);
+      V3 nn = v3(0, 0, 0);
+      nvalid[i] = pixel_normal(f, x, y, &nn) ? 1 : 0;
+      for (int a = 0; a < 3; ++a) { q[3 * i + a] = qq[a]; N[3 * i + a] = nn[a]; }
+    }
+}
+
+void or_skin(int64_t nq, const float* p, int32_t m, const float* g, int32_t k,
+             int32_t* idx, double* w, double* margin) {
+  for (int64_t i = 0; i < nq; ++i)
+    skin_one(load3(p + 3 * i), m, g, k, idx + k * i, w + k * i, margin ? margin + i : nullptr);
+}
+
+void or_exp(const double w[3], double R[9]) {
+  double th = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};   // [w]x
+  double K2[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int l = 0; l < 3; ++l) s += K[3 * i + l] * K[3 * l + j];
+      K2[3 * i + j] = s;
+    }
+  double A, B;
+  if (th < 1e-12) { A = 1.0; B = 0.0; }                 // first order
+  else { A = std::sin(th) / th; B = (1.0 - std::cos(th)) / (th * th); }
+  for (int i = 0; i < 9; ++i) R[i] = ((i % 4) == 0 ? 1.0 : 0.0) + A * K[i] + B * K2[i];
+}
+
+void or_warp(const or_problem* p, int32_t k, const double* Rt, const double pose[12],
+             double* x_hat, double* n_hat, double* vt, double* nt, uint8_t* ok) {
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, pose);
+    ok[i] = w.ok ? 1 : 0;
+    for (int a = 0; a < 3; ++a) {
+      x_hat[3 * i + a] = w.ok ? w.x_hat[a] : 0.0;
+      n_hat[3 * i + a] = w.ok ? w.m_hat[a] / norm(w.m_hat) : 0.0;
+      vt[3 * i + a] = w.ok ? w.vt[a] : 0.0;
+      nt[3 * i + a] = w.ok ? w.nt[a] : 0.0;
+    }
+  }
+}
+
+void or_associate(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                  int32_t* pix, uint8_t* why, double* margin) {
+  const int k = prm->k;
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
+    Assoc a = associate_point(prm, f, w);
+    pix[i] = a.pix;
+    why[i] = a.why;
+    margin[i] = a.margin;
+  }
+}
+
+int64_t or_system(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                  const int32_t* fidx, const double* fw, int64_t cap,
+                  int32_t* brow, int32_t* bcol, double* bval, double* rhs, double energy[5],
+                  int64_t* n_assoc) {
+  System S(p->m);
+  assemble(prm, p, f, Rt, fidx, fw, &S);
+  int64_t nb = 0;
+  for (std::map<std::pair<int, int>, B6>::const_iterator it = S.blk.begin(); it != S.blk.end(); ++it, ++nb) {
+    if (nb >= cap) continue;
+    brow[nb] = it->first.first;
+    bcol[nb] = it->first.second;
+    for (int a = 0; a < 36; ++a) bval[36 * nb + a] = it->second[a];
+  }
+  for (int i = 0; i < 6 * p->m; ++i) rhs[i] = S.rhs[i];
+  for (int a = 0; a < 4; ++a) energy[a] = S.E[a];
+  energy[4] = total_energy(prm, S.E);
+  *n_assoc = S.n_assoc;
+  return nb;
+}
+
+int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                     const int32_t* pix_frozen, const int32_t* fidx, const double* fw,
+                     int64_t cap_rows, double* r, double* J) {
+  const int k = prm->k, ncol = 6 * p->m;
+  M3 R = pose_R(f->pose);
+  int64_t row = 0;
+  double Jpl[8 * 6], Jpt[8 * 18], rpl, rpt[3];
+  const double sd = std::sqrt(prm->w_data), sp = std::sqrt(prm->w_pt);
+  const double sr = std::sqrt(prm->w_reg), sc = std::sqrt(prm->w_corr);
+  for (int64_t i = 0; i < p->n; ++i) {
+    if (pix_frozen[i] < 0) continue;
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
+    if (!w.ok) continue;
+    Assoc as;
+    int px = pix_frozen[i] % f->W, py = pix_frozen[i] / f->W;
+    as.q = back_project(f, px, py, (double)f->depth[pix_frozen[i]]);
+    if (!pixel_normal(f, px, py, &as.N)) continue;
+    point_rows(R, w, as, k, Jpl, Jpt, &rpl, rpt);
+    if (row + 4 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 4 * ncol);
+    r[row] = sd * rpl;
+    for (int c = 0; c < 3; ++c) r[row + 1 + c] = sp * rpt[c];
+    for (int s = 0; s < k; ++s) {
+      int j = p->idx[k * i + s];
+      for (int c = 0; c < 6; ++c) {
+        J0[6 * j + c] += sd * Jpl[6 * s + c];
+        for (int q = 0; q < 3; ++q) J0[(size_t)(1 + q) * ncol + 6 * j + c] += sp * Jpt[18 * s + 6 * q + c];
+      }
+    }
+    row += 4;
+  }
+  double e[3], Jj[18], Jl[18];
+  for (int j = 0; j < p->m; ++j)
+    for (int s = 0; s < prm->n_nbr; ++s) {
+      int l = p->nbr[prm->n_nbr * j + s];
+      if (l < 0) continue;
+      reg_edge(p, Rt, j, l, e, Jj, Jl);
+      if (row + 3 > cap_rows) return -1;
+      double* J0 = J + (size_t)row * ncol;
+      std::memset(J0, 0, sizeof(double) * 3 * ncol);
+      for (int q = 0; q < 3; ++q) {
+        r[row + q] = sr * e[q];
+        for (int c = 0; c < 6; ++c) {
+          J0[(size_t)q * ncol + 6 * j + c] += sr * Jj[6 * q + c];
+          J0[(size_t)q * ncol + 6 * l + c] += sr * Jl[6 * q + c];
+        }
+      }
+      row += 3;
+    }
+  double Jf[8 * 18];
+  for (int q = 0; q < p->nf; ++q) {
+    Warped w;
+    if (!feature_rows(p, k, Rt, f->pose, q, fidx, fw, &w, e, Jf)) continue;
+    if (row + 3 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 3 * ncol);
+    for (int a = 0; a < 3; ++a) {
+      r[row + a] = sc * e[a];
+      for (int s = 0; s < k; ++s) {
+        int j = fidx[k * q + s];
+        for (int c = 0; c < 6; ++c) J0[(size_t)a * ncol + 6 * j + c] += sc * Jf[18 * s + 6 * a + c];
+      }
+    }
+    row += 3;
+  }
+  return row;
+}
+
+int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
+                 const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x) {
+  System S(m);
+  for (int64_t b = 0; b < nblk; ++b) {
+    B6& B = S.blk[std::make_pair(brow[b], bcol[b])];
+    for (int a = 0; a < 36; ++a) B[a] = bval[36 * b + a];
+  }
+  for (int i = 0; i < 6 * m; ++i) S.rhs[i] = rhs[i];
+  std::vector<double> xs;
+  int32_t it = solve_system(S, lambda, mode, pcg_iters, xs);
+  for (int i = 0; i < 6 * m; ++i) x[i] = xs[i];
+  return it;
+}
+
+void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
+                 double* energy, int64_t* n_assoc) {
+  std::vector<int32_t> fidx;
+  std::vector<double> fw;
+  feature_skin(p, prm->k, fidx, fw);   // O1 on the (fixed) node positions
+  for (int it = 0; it <= prm->gn_iters; ++it) {
+    System S(p->m);
+    assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);
+    for (int a = 0; a < 4; ++a) energy[5 * it + a] = S.E[a];
+    energy[5 * it + 4] = total_energy(prm, S.E);
+    n_assoc[it] = S.n_assoc;
+    if (it == prm->gn_iters) break;   // final energy only
+    std::vector<double> x;
+    solve_system(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+    update_nodes(p->m, x, Rt);
+  }
+}
+
+void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
+                   double* g_out) {
+  double pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, pose);
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * i + a] = w.ok ? w.x_hat[a] : (double)p->xyz[3 * i + a];
+      nrm_out[3 * i + a] = w.ok ? w.nt[a] : (double)p->nrm[3 * i + a];
+    }
+  }
+  for (int j = 0; j < p->m; ++j)   // A26: g_j <- g_j + t_j (then R_j = I, t_j = 0)
+    for (int a = 0; a < 3; ++a) g_out[3 * j + a] = (double)p->g[3 * j + a] + Rt[12 * j + 9 + a];
+}
+
+int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, const float* rgb_obs,
+                int32_t frame_index, int32_t m, const float* g,
+                double* xyz_out, double* nrm_out, double* rgb_out, double* weight_out, int32_t* stamp_out,
+                int32_t* lift_idx, double* lift_w, double* lift_margin,
+                int64_t* owner, double* key_margin, uint8_t* why, double* gate_margin) {
+  const int W = f->W, H = f->H, k = prm->k;
+  const M3 R = pose_R(f->pose);
+  const V3 T = pose_T(f->pose);
+  const double cd = std::cos(prm->delta_deg * M_PI / 180.0);
+  std::vector<double> best(W * H, kInf), second(W * H, kInf);
+  for (int i = 0; i < W * H; ++i) owner[i] = -1;
+  std::vector<int32_t> pix(mdl->n, -1);
+  std::vector<double> dz(mdl->n, 0.0);
+  // O5 / Alg. 1: v~ = R v + T, gates, exclusive per pixel with key (|dz|, i)
+  for (int64_t i = 0; i < mdl->n; ++i) {
+    V3 vt = add(mul(R, load3(mdl->xyz + 3 * i)), T);
+    V3 nt = mul(R, load3(mdl->nrm + 3 * i));
+    Proj pr = project(f, vt);
+    uint8_t wb = 0;
+    double mg = pr.margin;
+    if (pr.z_ok) {
+      wb |= OR_Z;
+      if (pr.in_frame) {
+        wb |= OR_FRAME;
+        int q = pr.py * W + pr.px;
+        float D = f->depth[q];
+        V3 N;
+        if (depth_ok(D)) {
+          wb |= OR_DEPTH;
+          if (pixel_normal(f, pr.px, pr.py, &N)) {
+            wb |= OR_NORMAL;
+            double d = std::fabs(vt[2] - (double)D);
+            double tz = std::min(prm->tau_z, prm->trunc);   // Alg. 1 gate and Eq. 11 truncation (R-A20)
+            mg = std::min(mg, std::fabs(d - tz) / tz);
+            if (d < tz) {
+              wb |= OR_DIST;
+              double c = dot(nt, N);
+              mg = std::min(mg, std::fabs(c - cd));
+              if (c > cd) {
+                wb |= OR_ANGLE;
+                pix[i] = q;
+                dz[i] = d;
+              }
+            }
+          }
+        }
+      }
+    }
+    why[i] = wb;
+    gate_margin[i] = mg;
+  }
+  for (int64_t i = 0; i < mdl->n; ++i) {   // lexicographic (|dz|, i) minimum per pixel (R-A19)
+    if (pix[i] < 0) continue;
+    int q = pix[i];
+    if (dz[i] < best[q]) { second[q] = best[q]; best[q] = dz[i]; owner[q] = i; }
+    else if (dz[i] < second[q]) second[q] = dz[i];
+    else if (dz[i] == best[q]) second[q] = dz[i];
+  }
+  for (int q = 0; q < W * H; ++q) key_margin[q] = second[q] - best[q];
+  // copy, then Eq. 12-15 on each pixel's winner (R-A21: 3-D weighted average)
+  for (int64_t i = 0; i < mdl->n; ++i) {
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * i + a] = mdl->xyz[3 * i + a];
+      nrm_out[3 * i + a] = mdl->nrm[3 * i + a];
+      rgb_out[3 * i + a] = mdl->rgb[3 * i + a];
+    }
+    weight_out[i] = mdl->weight[i];
+    stamp_out[i] = mdl->stamp[i];
+  }
+  for (int q = 0; q < W * H; ++q) {
+    int64_t i = owner[q];
+    if (i < 0) continue;
+    int px = q % W, py = q / W;
+    V3 Q = back_project(f, px, py, (double)f->depth[q]);
+    V3 N;
+    pixel_normal(f, px, py, &N);
+    double om = mdl->weight[i];
+    V3 vt = add(mul(R, load3(mdl->xyz + 3 * i)), T);
+    V3 nt = mul(R, load3(mdl->nrm + 3 * i));
+    V3 pf = scale(add(scale(vt, om), Q), 1.0 / (om + 1.0));                  // Eq. 12 (3-D)
+    V3 nf = scale(add(scale(nt, om), N), 1.0 / (om + 1.0));                  // Eq. 14
+    nf = scale(nf, 1.0 / norm(nf));
+    V3 vw = mulT(R, sub(pf, T)), nw = mulT(R, nf);
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * i + a] = vw[a];
+      nrm_out[3 * i + a] = nw[a];
+      if (rgb_obs) rgb_out[3 * i + a] = (om * mdl->rgb[3 * i + a] + (double)rgb_obs[3 * q + a]) / (om + 1.0);  // Eq. 13
+    }
+    weight_out[i] = std::min(om + 1.0, prm->omega_max);                       // Eq. 15
+    stamp_out[i] = frame_index;
+  }
+  // O6: Alg. 2 Step 3 "else" branch: lift valid, unregistered pixels, row-major
+  int64_t nl = 0;
+  for (int q = 0; q < W * H; ++q) {
+    if (owner[q] >= 0) continue;
+    int px = q % W, py = q / W;
+    if (!depth_ok(f->depth[q])) continue;
+    V3 N;
+    if (!pixel_normal(f, px, py, &N)) continue;
+    V3 Q = back_project(f, px, py, (double)f->depth[q]);
+    V3 vw = mulT(R, sub(Q, T)), nw = mulT(R, N);
+    int64_t o = mdl->n + nl;
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * o + a] = vw[a];
+      nrm_out[3 * o + a] = nw[a];
+      rgb_out[3 * o + a] = rgb_obs ? (double)rgb_obs[3 * q + a] : 0.0;
+    }
+    weight_out[o] = 1.0;
+    stamp_out[o] = frame_index;
+    float pf[3] = {(float)vw[0], (float)vw[1], (float)vw[2]};   // skinning input as the GPU stores it
+    skin_one(load3(pf), m, g, k, lift_idx + k * nl, lift_w + k * nl, lift_margin + nl);
+    ++nl;
+  }
+  return nl;
+}
+
+}  // extern "C"

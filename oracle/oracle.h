@@ -1,0 +1,117 @@
+/* oracle.h -- plain, slow, fp64 CPU oracle of the MIS-SLAM (arXiv 1803.02009)
+ * non-rigid registration + fusion hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load or call it.  It
+ * shares no code, header, table or helper with the CUDA path
+ * (paper_1803_02009_b200/csrc, include/mis.h); neither side includes the other.
+ *
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n, "R-An" = the
+ * reading An of DESIGN.md §3.  Units are mm throughout.
+ * All arithmetic is fp64; fp32 inputs are upcast exactly.
+ */
+#ifndef MIS_ORACLE_H
+#define MIS_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t k;            /* nodes per point (Eq. 1 "k"), R-A5                         */
+  int32_t n_nbr;        /* regulariser neighbours per node (Eq. 6 N(j)), R-A15       */
+  double w_data, w_pt, w_reg, w_corr;   /* P:598 (w_pt: R-A13)                      */
+  double eps_d, eps_n_deg;              /* Eq. 7 thresholds                   */
+  double tau_z, delta_deg, trunc, omega_max; /* Alg. 1 / Eq. 11 / Eq. 15 */
+  int32_t gn_iters, pcg_iters;
+  double lambda;                        /* GN damping, R-A16                         */
+  int32_t solve_mode;                   /* 0 = EXACT, 1 = MIRROR (same P as GPU)     */
+} or_params;
+
+typedef struct {
+  int32_t W, H;
+  double fx, fy, cx, cy;
+  const float* depth;   /* H*W, mm; <=0 or non-finite = invalid                     */
+  double pose[12];      /* world->camera: R row-major (9), T (3); Eq. 1 R_i, T_i      */
+} or_frame;
+
+typedef struct {
+  int64_t n;
+  const float* xyz;     /* n*3 model points v_i (world)                              */
+  const float* nrm;     /* n*3 model normals                                        */
+  const int32_t* idx;   /* n*k node ids per point (Eq. 1 "k nearest")               */
+  const float* w;       /* n*k skinning weights (Eq. 2), normalised in the warp     */
+  int32_t m;
+  const float* g;       /* m*3 node positions g_j                                   */
+  const int32_t* nbr;   /* m*n_nbr neighbour ids, -1 = none                         */
+  int32_t nf;
+  const float* fsrc;    /* nf*3 feature model positions V_i (world, frame n-1)      */
+  const float* fdst;    /* nf*3 feature observed positions (camera, frame n)        */
+} or_problem;
+
+/* why-bits of one association (Eq. 7 / Alg. 1 gates), evaluated in order and
+ * short-circuited at the first failure. */
+enum { OR_Z = 1, OR_FRAME = 2, OR_DEPTH = 4, OR_NORMAL = 8, OR_DIST = 16, OR_ANGLE = 32, OR_ALL = 63 };
+
+/* O0: back-projection and central-difference normals of a depth map. */
+void or_frame_prep(const or_frame* f, double* q, double* N, uint8_t* dvalid, uint8_t* nvalid);
+/* O1: Eq. 2 skinning of nq query points against m nodes. idx/w: nq*k, nearest
+ * first; margin[i] = relative gap deciding the k-set (for tie exclusion). */
+void or_skin(int64_t nq, const float* p, int32_t m, const float* g, int32_t k,
+             int32_t* idx, double* w, double* margin);
+/* A18: Rodrigues exponential. */
+void or_exp(const double w[3], double R[9]);
+/* O3a: warp every point (Eq. 1).  x_hat: world (before the pose), vt/nt:
+ * camera frame.  ok[i]=0 when the weights sum to <= 0 or the normal vanishes. */
+void or_warp(const or_problem* p, int32_t k, const double* Rt, const double pose[12],
+             double* x_hat, double* n_hat, double* vt, double* nt, uint8_t* ok);
+/* O3b: projective association (Eq. 7). */
+void or_associate(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                  int32_t* pix, uint8_t* why, double* margin);
+/* O3c-g: normal equations in 6x6 node blocks (upper triangle j<=l, full 6x6
+ * each, sorted by (row, col)).  Returns the number of blocks; writes at most
+ * cap of them.  energy[5] = E_data, E_pt, E_reg, E_corr, weighted total.
+ * fidx/fw: feature skinning (nf*k) from or_skin. */
+int64_t or_system(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                  const int32_t* fidx, const double* fw, int64_t cap,
+                  int32_t* brow, int32_t* bcol, double* bval, double* rhs, double energy[5],
+                  int64_t* n_assoc);
+/* Dense Jacobian / residual stack for small problems (pins P6, P7).  Rows:
+ * per associated point 1 (plane) + 3 (point), per directed edge 3, per feature
+ * 3, each scaled by sqrt(weight).  pix_frozen (n) fixes the association (-1 =
+ * none) so that finite differences see a smooth function.  J: rows*6m. */
+int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                     const int32_t* pix_frozen, const int32_t* fidx, const double* fw,
+                     int64_t cap_rows, double* r, double* J);
+/* O3h: solve (H + lambda I) x = rhs from or_system's blocks. mode 0 EXACT, 1 MIRROR. */
+int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
+                 const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x);
+/* O3: fixed-iteration Gauss-Newton registration.  Rt (m*12, R row-major + t)
+ * is the initial state on entry and the result on exit.  energy: (G+1)*5 (start
+ * of each iteration, then final), n_assoc: G+1. */
+void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
+                 double* energy, int64_t* n_assoc);
+/* O4: apply the field: live world state x_hat, unit normals; advanced nodes g+t. */
+void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
+                   double* g_out);
+
+typedef struct {
+  int64_t n;
+  const float* xyz; const float* nrm; const float* rgb; const float* weight; const int32_t* stamp;
+} or_model;
+
+/* O5 + O6: Alg. 1 registration, Eq. 12-15 fusion, Alg. 2 Step 3 lift.
+ * Outputs for the n existing points (fused in place of the copies) and the
+ * lifted points appended after them (capacity n + W*H).  owner: W*H point id
+ * or -1; key_margin: W*H gap between the two best keys (mm, +inf if < 2).
+ * Returns the number of lifted points. */
+int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, const float* rgb_obs,
+                int32_t frame_index, int32_t m, const float* g,
+                double* xyz_out, double* nrm_out, double* rgb_out, double* weight_out, int32_t* stamp_out,
+                int32_t* lift_idx, double* lift_w, double* lift_margin,
+                int64_t* owner, double* key_margin, uint8_t* why, double* gate_margin);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

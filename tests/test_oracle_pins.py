@@ -1,0 +1,649 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix.
+
+Every test here checks the oracle against something other than itself: the
+worked examples of tests/golden/spec_examples.json (hand-derived values, each
+cited), closed forms, invariants (identity / rigid fields), brute force on tiny
+inputs, finite differences, dense linear algebra (numpy) and textbook special
+cases.  SURVEY §8(c) "Pins" P1-P16; DESIGN.md §4.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1803_02009_b200 import synth
+from tests.common import apply_perturbation, pose12, random_state, rot, scene_problem
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ------------------------------------------------------------------ helpers
+def plane_frame(W=64, H=48, z=50.0, f=40.0, tilt=None):
+    """Depth map of a plane seen by the identity camera (analytic ray/plane)."""
+    intr = dict(fx=f, fy=f, cx=W / 2.0, cy=H / 2.0, W=W, H=H)
+    u, v = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    if tilt is None:
+        D = np.full((H, W), z)
+    else:   # plane z = z0 + tan(tilt) * y (about the x axis)
+        s = np.tan(np.deg2rad(tilt))
+        D = z / (1.0 - s * (v - intr["cy"]) / f)
+    return D.astype(np.float32), intr
+
+
+def single_node_problem(pts, nrms):
+    """Every point bound to node 0 (k=1); nodes: 0 at origin and 1 far away."""
+    n = len(pts)
+    g = np.array([[0, 0, 50.0], [1000, 0, 50.0]], np.float32)
+    return O.Problem(np.asarray(pts, np.float32), np.asarray(nrms, np.float32),
+                     np.zeros((n, 1), np.int32), np.ones((n, 1), np.float32),
+                     g, np.array([[1], [0]], np.int32))
+
+
+# ------------------------------------------------------------------ P5 projection
+def test_p5_projection_golden():
+    gp = GOLD["projection"]
+    it = gp["intr"]
+    D = np.full((it["H"], it["W"]), 50.0, np.float32)
+    fr = O.Frame(D, it, pose12())
+    pts = np.array([c["point"] for c in gp["cases"]])
+    pb = single_node_problem(pts, [[0, 0, -1]] * len(pts))
+    prm = O.params(k=1, n_nbr=1)
+    pix, why, _ = O.associate(prm, pb, fr, O.identity_state(2))
+    for c, p, wb in zip(gp["cases"], pix, why):
+        assert wb == 63
+        assert p == c["pixel"][1] * it["W"] + c["pixel"][0]
+    # back-projection inverse: q at (420, 240) with D=50 is (10, 0, 50)
+    q, N, dv, nv = O.frame_prep(fr)
+    assert np.allclose(q[240, 420], [10, 0, 50], atol=1e-12)
+    assert np.allclose(q[240, 320], [0, 0, 50], atol=1e-12)
+
+
+def test_p5_roundtrip_random_pixels():
+    rng = np.random.default_rng(5)
+    D, it = plane_frame(W=97, H=61, f=73.0)
+    D = rng.uniform(40, 70, D.shape).astype(np.float32)
+    fr = O.Frame(D, it, pose12())
+    q, _, _, _ = O.frame_prep(fr)
+    ys, xs = rng.integers(0, 61, 100), rng.integers(0, 97, 100)
+    Q = q[ys, xs]
+    u = it["fx"] * Q[:, 0] / Q[:, 2] + it["cx"]
+    v = it["fy"] * Q[:, 1] / Q[:, 2] + it["cy"]
+    assert np.max(np.abs(u - xs)) < 1e-9 and np.max(np.abs(v - ys)) < 1e-9
+
+
+# ------------------------------------------------------------------ P11 normals
+def test_p11_normals_plane_and_45deg():
+    D, it = plane_frame()
+    _, N, dv, nv = O.frame_prep(O.Frame(D, it, pose12()))
+    assert nv[1:-1, 1:-1].all() and not nv[0].any() and not nv[:, -1].any()
+    assert np.allclose(N[nv], [0, 0, -1], atol=1e-12)
+    D45, it = plane_frame(tilt=45.0, z=50.0, f=60.0)
+    _, N, _, nv = O.frame_prep(O.Frame(D45, it, pose12()))
+    expect = np.array([0.0, 1.0, -1.0]) / np.sqrt(2)   # plane z - y = 50, facing the camera
+    err = np.abs(N[nv] - expect).max()
+    assert err < GOLD["normals"]["tol_45"], err
+
+
+def test_p11_hole_neighbour_invalid():
+    D, it = plane_frame()
+    D[10, 10] = 0.0
+    _, _, dv, nv = O.frame_prep(O.Frame(D, it, pose12()))
+    assert not dv[10, 10]
+    for y, x in [(10, 10), (9, 10), (11, 10), (10, 9), (10, 11)]:
+        assert not nv[y, x]
+    assert nv[8, 10] and nv[10, 12]
+
+
+# ------------------------------------------------------------------ P4 skinning
+def test_p4_skinning_golden():
+    for c in GOLD["skinning"]["cases"]:
+        idx, w, _ = O.skin(np.array([c["v"]]), np.array(c["nodes"]), c["k"])
+        got = {int(i): float(x) for i, x in zip(idx[0], w[0])}
+        exp = {int(a): b for a, b in c["weights"].items()}
+        assert set(got) == set(exp)
+        for a in exp:
+            assert abs(got[a] - exp[a]) < 1e-9
+
+
+def test_p4_skinning_sum_and_brute_force():
+    rng = np.random.default_rng(4)
+    g = rng.uniform(-20, 20, (37, 3)).astype(np.float32)
+    p = rng.uniform(-20, 20, (200, 3)).astype(np.float32)
+    for k in (1, 4, 8):
+        idx, w, _ = O.skin(p, g, k)
+        assert np.allclose(w.sum(1), 1.0, atol=1e-12)
+        assert (w >= 0).all()
+        d = np.linalg.norm(p[:, None, :].astype(np.float64) - g[None].astype(np.float64), axis=-1)
+        order = np.argsort(d, axis=1, kind="stable")
+        assert (np.sort(idx, 1) == np.sort(order[:, :k], 1)).all()
+        dk = np.take_along_axis(d, order[:, k:k + 1], 1)
+        raw = 1 - np.take_along_axis(d, idx, 1) / dk
+        assert np.allclose(w, raw / raw.sum(1, keepdims=True), atol=1e-12)
+
+
+# ------------------------------------------------------------------ P13 exponential map
+def test_p13_exp():
+    assert np.array_equal(O.exp_so3([0, 0, 0]), np.eye(3))
+    R = O.exp_so3([0, 0, np.pi / 2])
+    assert np.allclose(R, [[0, -1, 0], [1, 0, 0], [0, 0, 1]], atol=1e-15)
+    rng = np.random.default_rng(13)
+    for _ in range(50):
+        R = O.exp_so3(rng.normal(0, 1, 3))
+        assert np.allclose(R @ R.T, np.eye(3), atol=1e-12)
+        assert abs(np.linalg.det(R) - 1) < 1e-12
+    w = np.array([3e-13, -1e-13, 2e-13])     # below the first-order switch
+    assert np.allclose(O.exp_so3(w), np.eye(3) + np.array(
+        [[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]]), atol=1e-24)
+
+
+# ------------------------------------------------------------------ P1 identity / warp golden
+def test_p1_identity_field_leaves_model_unchanged():
+    sc, pb, fr, _ = scene_problem("c1")
+    xh, nh, vt, nt, ok = O.warp(pb, O.identity_state(pb.g.shape[0]), pose12())
+    assert ok.all()
+    assert np.abs(vt - pb.xyz).max() < 1e-12
+    n64 = pb.nrm.astype(np.float64)
+    assert np.abs(nt - n64 / np.linalg.norm(n64, axis=1, keepdims=True)).max() < 1e-12
+
+
+def test_warp_golden():
+    for c in GOLD["warp"]["cases"]:
+        pb = single_node_problem([c["v"]], [[1, 0, 0]])
+        Rt = O.identity_state(2)
+        Rt[0, 9:] = c["t_node"]
+        pb.g[0] = 0.0   # node at the origin
+        pb = O.Problem(pb.xyz, pb.nrm, pb.idx, pb.w, np.array([[0, 0, 0], [1000, 0, 0]], np.float32), pb.nbr)
+        _, _, vt, _, _ = O.warp(pb, Rt, pose12(c["pose_R"], c["pose_T"]))
+        assert np.allclose(vt[0], c["out"], atol=1e-12)
+    for c in GOLD["normal_warp"]["cases"]:
+        pb = single_node_problem([[1, 2, 3]], [c["n"]])
+        _, _, _, nt, _ = O.warp(pb, O.identity_state(2), pose12(c["pose_R"]))
+        assert np.allclose(nt[0], c["out"], atol=1e-12)
+
+
+def test_rigid_consistent_field_is_rigid_map():
+    """A_j = Q, t_j = (Q-I) g_j + c for all j  =>  warp(v) = R (Q v + c) + T."""
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    Q = rot([1, 2, 3], 7.0)
+    c = np.array([1.0, -2.0, 0.5])
+    Rt = np.zeros((m, 12))
+    for j in range(m):
+        Rt[j, :9] = Q.ravel()
+        Rt[j, 9:] = (Q - np.eye(3)) @ pb.g[j].astype(np.float64) + c
+    R, T = rot([0, 1, 1], 20.0), np.array([3.0, 1.0, -2.0])
+    _, _, vt, nt, ok = O.warp(pb, Rt, pose12(R, T))
+    v = pb.xyz.astype(np.float64)
+    assert np.abs(vt - ((v @ Q.T + c) @ R.T + T)).max() < 1e-9
+    n = pb.nrm.astype(np.float64)
+    n = n / np.linalg.norm(n, axis=1, keepdims=True)
+    assert np.abs(nt - n @ Q.T @ R.T).max() < 1e-9
+
+
+# ------------------------------------------------------------------ P3 regulariser
+def _reg_only_system(g, nbr, Rt, w_reg=1.0):
+    g = np.asarray(g, np.float32)
+    pb = O.Problem(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 1), np.int32), np.zeros((0, 1)),
+                   g, np.asarray(nbr, np.int32))
+    D, it = plane_frame()
+    prm = O.params(k=1, n_nbr=np.asarray(nbr).shape[1], w_reg=w_reg)
+    return O.system(prm, pb, O.Frame(D, it, pose12()), Rt)
+
+
+def test_p3_two_node_golden():
+    gr = GOLD["regulariser"]
+    Rt = O.identity_state(2)
+    Rt[:, 9:] = gr["t"]
+    s = _reg_only_system(gr["nodes"], [[1], [0]], Rt)
+    assert abs(s["energy"][2] - gr["E_reg"]) < 1e-12
+
+
+def test_p3_rigid_consistent_reg_is_zero():
+    rng = np.random.default_rng(3)
+    g = rng.uniform(-30, 30, (40, 3))
+    nbr = synth.node_graph(g.astype(np.float32), 4)
+    Q = rot([0.3, -1, 2], 25.0)
+    c = np.array([4.0, 5.0, -6.0])
+    Rt = np.zeros((40, 12))
+    for j in range(40):
+        Rt[j, :9] = Q.ravel()
+        Rt[j, 9:] = (Q - np.eye(3)) @ g[j].astype(np.float32).astype(np.float64) + c
+    s = _reg_only_system(g, nbr, Rt)
+    assert s["energy"][2] < 1e-18
+    assert np.abs(s["rhs"]).max() < 1e-8
+
+
+# ------------------------------------------------------------------ P8 data term
+def test_p8_plane_residual_and_tangential_invariance():
+    gd = GOLD["data_term"]
+    D, it = plane_frame(z=gd["plane_z"])
+    fr = O.Frame(D, it, pose12())
+    prm = O.params(k=1, n_nbr=1, w_pt=0.0, w_reg=0.0)
+    for x in (0.0, 1.0, 0.37):   # 1 mm tangential shift
+        pb = single_node_problem([[x, 0, gd["point_z"]]], [[0, 0, -1]])
+        s = O.system(prm, pb, fr, O.identity_state(2))
+        assert s["n_assoc"] == 1
+        assert abs(np.sqrt(s["energy"][0]) - gd["abs_residual"]) < 1e-9
+
+
+def test_visibility_golden():
+    gv = GOLD["visibility"]
+    D, it = plane_frame(z=50.0)
+    fr = O.Frame(D, it, pose12())
+    prm = O.params(k=1, n_nbr=1, eps_d=gv["eps_d"], eps_n_deg=gv["eps_n_deg"])
+    n_tilt = rot([1, 0, 0], gv["tilt_deg"]) @ np.array([0, 0, -1.0])
+    n_ok = rot([1, 0, 0], 5.0) @ np.array([0, 0, -1.0])
+    pts = [[0, 0, 50 + gv["offset_mm"]], [0, 0, 50 + 10.0], [0, 0, 50.0], [0, 0, 50.0]]
+    nrm = [[0, 0, -1], [0, 0, -1], n_tilt, n_ok]
+    pb = single_node_problem(pts, nrm)
+    pix, why, _ = O.associate(prm, pb, fr, O.identity_state(2))
+    assert why[0] == 15 and pix[0] == -1          # 20 mm > eps_d: distance gate fails
+    assert why[1] == 63 and pix[1] >= 0
+    assert why[2] == 31 and pix[2] == -1          # 15 deg > eps_n: angle gate fails
+    assert why[3] == 63
+
+
+# ------------------------------------------------------------------ P9 association brute force
+def _brute_force_association(prm, pb, fr, Rt, intr):
+    """Every point against every pixel: the pixel whose unit square (centred on
+    the integer coordinate) contains the projection, then the Eq. 7 gates."""
+    _, _, vt, nt, ok = O.warp(pb, Rt, np.array(fr.s.pose[:]))
+    q, N, dv, nv = O.frame_prep(fr)
+    H, W = fr.depth.shape
+    xs, ys = np.meshgrid(np.arange(W), np.arange(H))
+    out = np.full(len(vt), -1)
+    ce = np.cos(np.deg2rad(prm.eps_n_deg))
+    for i in range(len(vt)):
+        if not ok[i] or vt[i, 2] <= 0:
+            continue
+        u = intr["fx"] * vt[i, 0] / vt[i, 2] + intr["cx"]
+        v = intr["fy"] * vt[i, 1] / vt[i, 2] + intr["cy"]
+        hit = (xs - 0.5 <= u) & (u < xs + 0.5) & (ys - 0.5 <= v) & (v < ys + 0.5)
+        hit &= dv & nv
+        hit &= np.linalg.norm(q - vt[i], axis=-1) < prm.eps_d
+        hit &= (N @ nt[i]) > ce
+        cand = np.flatnonzero(hit.ravel())
+        assert len(cand) <= 1
+        if len(cand):
+            out[i] = cand[0]
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_p9_association_equals_brute_force(seed):
+    rng = np.random.default_rng(900 + seed)
+    W, H = int(rng.integers(12, 33)), int(rng.integers(12, 33))
+    f = float(rng.uniform(15, 30))
+    intr = dict(fx=f, fy=f * rng.uniform(0.9, 1.1), cx=W / 2 + rng.uniform(-1, 1), cy=H / 2 + rng.uniform(-1, 1), W=W, H=H)
+    u, v = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    D = (50 + 3 * np.sin(0.3 * u) * np.cos(0.2 * v) + rng.normal(0, 0.3, u.shape)).astype(np.float32)
+    D[rng.uniform(size=D.shape) < 0.05] = 0.0
+    fr = O.Frame(D, intr, pose12(rot(rng.normal(size=3), 2.0), rng.normal(0, 0.5, 3)))
+    n = 300
+    pts = np.stack([rng.uniform(-15, 15, n), rng.uniform(-15, 15, n), rng.uniform(45, 56, n)], -1)
+    nrm = rng.normal(0, 0.15, (n, 3)) + [0, 0, -1]
+    g = rng.uniform(-15, 15, (9, 3)) + [0, 0, 50]
+    idx, w, _ = O.skin(pts, g, 3)
+    pb = O.Problem(pts, nrm, idx, w, g, synth.node_graph(g.astype(np.float32), 3))
+    Rt = random_state(9, rng, 0.02, 0.3)
+    prm = O.params(k=3, n_nbr=3)
+    pix, why, mg = O.associate(prm, pb, fr, Rt)
+    bf = _brute_force_association(prm, pb, fr, Rt, intr)
+    keep = mg > 1e-6
+    assert (pix[keep] == bf[keep]).all()
+    assert (pix >= 0).sum() > 20
+
+
+# ------------------------------------------------------------------ P6 finite differences
+def _small_problem(seed):
+    """10 points bound to 4 nodes (k=3) + 2 features on the C1 scene."""
+    rng = np.random.default_rng(600 + seed)
+    sc = synth.make_scene("c1", 1)
+    g_all = sc["g"].astype(np.float64)
+    c0 = np.argsort(np.linalg.norm(g_all[:, :2], axis=1))[:4]
+    g = sc["g"][c0]
+    centre = g.astype(np.float64).mean(0)
+    d = np.linalg.norm(sc["xyz"][:, :2] - centre[:2], axis=1)
+    near = np.argsort(d)[:400]
+    sel = rng.choice(near, 10, replace=False)
+    fs = rng.choice(near, 2, replace=False)
+    idx, w, _ = O.skin(sc["xyz"][sel], g, 3)
+    nbr = synth.node_graph(g, 3)
+    fdst = sc["xyz"][fs] @ sc["pose"][:9].reshape(3, 3).T.astype(np.float32) + sc["pose"][9:] + rng.normal(0, 1, (2, 3))
+    pb = O.Problem(sc["xyz"][sel], sc["nrm"][sel], idx, w, g, nbr, sc["xyz"][fs], fdst)
+    fr = O.Frame(sc["depth"], sc["intr"], sc["pose"])
+    prm = O.params(k=3, n_nbr=3, w_pt=1.0)
+    return prm, pb, fr, random_state(4, rng, 0.02, 0.3)
+
+
+def _fd_check(prm, pb, fr, Rt, h=1e-5):
+    pix, _, _ = O.associate(prm, pb, fr, Rt)
+    fsk = O.feature_skin(pb)[:2]
+    r0, J = O.residuals(prm, pb, fr, Rt, pix, fsk)
+    m = pb.g.shape[0]
+    Jfd = np.zeros_like(J)
+    for j in range(m):
+        for c in range(6):
+            rp, _ = O.residuals(prm, pb, fr, apply_perturbation(Rt, j, c, h), pix, fsk)
+            rm, _ = O.residuals(prm, pb, fr, apply_perturbation(Rt, j, c, -h), pix, fsk)
+            Jfd[:, 6 * j + c] = (rp - rm) / (2 * h)
+    return J, Jfd, pix
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_p6_finite_difference_jacobians_small(seed):
+    prm, pb, fr, Rt = _small_problem(seed)
+    J, Jfd, pix = _fd_check(prm, pb, fr, Rt)
+    assert (pix >= 0).sum() >= 5
+    rel = np.abs(J - Jfd).max() / np.abs(J).max()
+    assert rel < 1e-4, rel
+
+
+def test_p6_finite_difference_jacobians_c1():
+    sc, pb, fr, _ = scene_problem("c1")
+    sub = np.random.default_rng(61).choice(pb.xyz.shape[0], 300, replace=False)
+    pb = O.Problem(pb.xyz[sub], pb.nrm[sub], pb.idx[sub], pb.w[sub], pb.g, pb.nbr, pb.fsrc, pb.fdst)
+    Rt = random_state(pb.g.shape[0], np.random.default_rng(62), 0.01, 0.3)
+    prm = O.params()
+    J, Jfd, pix = _fd_check(prm, pb, fr, Rt)
+    rel = np.abs(J - Jfd).max() / np.abs(J).max()
+    assert rel < 1e-4, rel
+
+
+# ------------------------------------------------------------------ P7 / P14 assembly and solves
+def test_p7_assembly_equals_dense_jtj_c1():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    Rt = random_state(m, np.random.default_rng(70), 0.01, 0.3)
+    prm = O.params()
+    s = O.system(prm, pb, fr, Rt)
+    pix, _, _ = O.associate(prm, pb, fr, Rt)
+    r, J = O.residuals(prm, pb, fr, Rt, pix)
+    Hd = J.T @ J
+    H = O.dense_H(s, m)
+    scale = np.abs(Hd).max()
+    assert np.abs(H - Hd).max() < 1e-10 * scale
+    assert np.abs(s["rhs"] + J.T @ r).max() < 1e-10 * np.abs(J.T @ r).max()
+    assert abs(s["energy"][4] - r @ r) < 1e-10 * (r @ r)
+    # P14: symmetric positive semi-definite
+    ev = np.linalg.eigvalsh(0.5 * (H + H.T))
+    assert ev.min() > -1e-10 * ev.max()
+    assert s["n_assoc"] == int((pix >= 0).sum())
+
+
+def test_p7_solves_match_dense():
+    sc, pb, fr, _ = scene_problem("c2", with_features=True)
+    m = pb.g.shape[0]
+    prm = O.params()
+    s = O.system(prm, pb, fr, O.identity_state(m))
+    A = O.dense_H(s, m) + prm.lambda_ * np.eye(6 * m)
+    x_ref = np.linalg.solve(A, s["rhs"])
+    x, _ = O.solve(s, m, prm.lambda_, 0, 0)          # EXACT (PCG to 1e-12 at this size)
+    assert np.abs(A @ x - s["rhs"]).max() < 1e-9 * np.abs(s["rhs"]).max()
+    assert np.abs(x - x_ref).max() < 1e-6 * np.abs(x_ref).max()
+    # MIRROR, one iteration = preconditioned steepest descent from 0: x = (b.z)/(z.A z) z, z = M b
+    Minv = np.zeros((6 * m, 6 * m))
+    Hd = O.dense_H(s, m)
+    for j in range(m):
+        B = Hd[6 * j:6 * j + 6, 6 * j:6 * j + 6]
+        mu = 1e-9 * np.trace(B) / 6
+        Minv[6 * j:6 * j + 6, 6 * j:6 * j + 6] = np.linalg.inv(B + (prm.lambda_ + mu) * np.eye(6))
+    z = Minv @ s["rhs"]
+    x1_ref = (s["rhs"] @ z) / (z @ A @ z) * z
+    x1, _ = O.solve(s, m, prm.lambda_, 1, 1)
+    assert np.abs(x1 - x1_ref).max() < 1e-9 * np.abs(x1_ref).max()
+
+
+def test_p7_exact_small_is_cholesky():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    prm = O.params()
+    s = O.system(prm, pb, fr, O.identity_state(m))
+    A = O.dense_H(s, m) + prm.lambda_ * np.eye(6 * m)
+    x, _ = O.solve(s, m, prm.lambda_, 0, 0)
+    assert np.abs(x - np.linalg.solve(A, s["rhs"])).max() < 1e-9 * np.abs(x).max()
+
+
+# ------------------------------------------------------------------ P15 shard invariance
+def test_p15_shard_sum_equals_full_system():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    Rt = random_state(m, np.random.default_rng(150), 0.01, 0.2)
+    prm = O.params()
+    full = O.system(prm, pb, fr, Rt)
+    n = pb.xyz.shape[0]
+    cuts = [0, n // 3, 2 * n // 3, n]
+    Hs = np.zeros((6 * m, 6 * m)); rhs = np.zeros(6 * m); E = np.zeros(5)
+    for s_ in range(3):
+        a, b = cuts[s_], cuts[s_ + 1]
+        nbr = pb.nbr if s_ == 0 else np.full_like(pb.nbr, -1)   # graph terms on shard 0 only
+        fs = (pb.fsrc, pb.fdst) if s_ == 0 else (None, None)
+        sb = O.Problem(pb.xyz[a:b], pb.nrm[a:b], pb.idx[a:b], pb.w[a:b], pb.g, nbr, *fs)
+        ss = O.system(prm, sb, fr, Rt)
+        Hs += O.dense_H(ss, m); rhs += ss["rhs"]; E += ss["energy"]
+    Hf = O.dense_H(full, m)
+    assert np.abs(Hs - Hf).max() < 1e-10 * np.abs(Hf).max()
+    assert np.abs(rhs - full["rhs"]).max() < 1e-10 * np.abs(full["rhs"]).max()
+    assert np.allclose(E, full["energy"], rtol=1e-12)
+
+
+# ------------------------------------------------------------------ P2 / P12 rigid recovery
+def _rigid_scene(Q, c, cfg="c1", n_feat=24, bump=True):
+    """Noise-free observation of the frame-0 surface after a rigid tissue motion
+    (Q, c), seen by the identity camera (PAPER.md:616 protocol without noise)."""
+    cfgo = synth.CONFIGS[cfg]
+    rng = np.random.default_rng(20)
+    bumps = [(3.0, -2.0, 2.5, synth.BUMP_SIGMA)] if bump else []
+    surf = synth.Surface(0.0, bumps)
+    mdl = synth.sample_model(cfgo, surf, rng, 0)
+    # tissue motion (Q, c) in world == camera pose (Q, c) on the unmoved tissue
+    depth = synth.render_depth(cfgo, surf, Q, c, rng, noise=False, holes=False)
+    idx, w, _ = O.skin(mdl["xyz"], mdl["g"], cfgo.k)
+    fsel = rng.choice(len(mdl["xyz"]), n_feat, replace=False)
+    fsrc = mdl["xyz"][fsel]
+    fdst = fsrc.astype(np.float64) @ Q.T + c
+    pb = O.Problem(mdl["xyz"], mdl["nrm"], idx, w, mdl["g"], mdl["nbr"], fsrc, fdst)
+    fr = O.Frame(depth, synth.intrinsics(cfgo), pose12())
+    return pb, fr
+
+
+@pytest.mark.parametrize("Qc", [
+    (rot([0, 0, 1], 0.0), np.array([2.0, 0.0, 0.0])),          # S:294 pure translation (2,0,0)
+    (rot([1, -2, 0.5], 1.5), np.array([0.8, -0.5, 0.6])),      # general rigid motion
+])
+def test_p2_rigid_motion_recovered(Qc):
+    Q, c = Qc
+    pb, fr = _rigid_scene(Q, c)
+    m = pb.g.shape[0]
+    prm = O.params(w_pt=0.0, gn_iters=8, solve_mode=0)
+    Rt, E, na = O.register(prm, pb, fr)
+    g = pb.g.astype(np.float64)
+    t_exp = g @ (Q - np.eye(3)).T + c
+    terr = np.linalg.norm(Rt[:, 9:] - t_exp, axis=1)
+    rerr = np.array([np.linalg.norm(_log(Rt[j, :9].reshape(3, 3) @ Q.T)) for j in range(m)])
+    assert terr.max() < 0.01, terr.max()
+    assert rerr.max() < 1e-4, rerr.max()
+    assert E[-1, 4] < 1e-3 * E[0, 4]
+
+
+def _log(R):
+    c = np.clip((np.trace(R) - 1) / 2, -1, 1)
+    th = np.arccos(c)
+    if th < 1e-9:
+        return np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]]) / 2
+    return th / (2 * np.sin(th)) * np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+
+
+def test_p12_fixed_point():
+    pb, fr = _rigid_scene(np.eye(3), np.zeros(3))
+    prm = O.params(w_pt=0.0, gn_iters=6, solve_mode=0)
+    Rt, E, _ = O.register(prm, pb, fr)
+    prm1 = O.params(w_pt=0.0, gn_iters=1, solve_mode=0)
+    Rt2, E2, _ = O.register(prm1, pb, fr, Rt)
+    assert abs(E2[1, 4] - E2[0, 4]) < 1e-10 * max(1.0, E2[0, 4])
+    assert np.abs(Rt2 - Rt).max() < 1e-6
+
+
+def test_p16_energy_non_increasing_noiseless():
+    """Sanity (not a gate): fixed-P (MIRROR) GN on a noise-free, exactly
+    representable deformation (a rigid tissue motion) lowers the energy every
+    iteration.  (A 2-3 mm bump is NOT representable by C1's 16 nodes, and
+    point-to-plane alone leaves near-null modes on the bowl, so those are not
+    used here.)"""
+    pb, fr = _rigid_scene(rot([0.2, 1, -0.4], 1.0), np.array([0.5, 0.3, -0.4]))
+    Rt, E, na = O.register(O.params(w_pt=0.0, gn_iters=5, pcg_iters=10, solve_mode=1), pb, fr)
+    tot = E[:, 4]
+    assert (np.diff(tot) <= 1e-9 * tot[0]).all(), tot
+    assert tot[-1] < 0.25 * tot[0]   # 10 PCG iterations do not fully converge
+
+
+# ------------------------------------------------------------------ P10 fusion
+def test_p10_fusion_golden_and_cap():
+    gf = GOLD["fusion"]
+    D, it = plane_frame(z=gf["depth"], f=40.0)
+    fr = O.Frame(D, it, pose12())
+    prm = O.params(k=1, n_nbr=1, tau_z=10.0, trunc=40.0)
+    xyz = np.array([[0, 0, gf["model_z"]], [0.3, 0.0, gf["model_z"] + 0.5]], np.float32)
+    # second point lands on another pixel; give it omega = omega_max
+    xyz[1] = [12.0 / 40 * 10.0 * 2, 0, gf["model_z"]]
+    nrm = np.array([[0, 0, -1], [0, 0, -1]], np.float32)
+    rgb = np.zeros((2, 3), np.float32)
+    out = O.fuse(prm, xyz, nrm, rgb, np.array([gf["omega"], prm.omega_max], np.float32),
+                 np.zeros(2, np.int32), fr, None, 7, np.array([[0, 0, 0], [100, 0, 0]], np.float32))
+    assert abs(out["xyz"][0, 2] - gf["fused_z"]) < 1e-12
+    assert out["weight"][0] == 2.0 and out["stamp"][0] == 7
+    assert out["weight"][1] == prm.omega_max
+    assert (out["weight"] <= prm.omega_max).all()
+
+
+def _fusion_scene(seed, W=32, H=24):
+    rng = np.random.default_rng(1000 + seed)
+    f = 30.0
+    intr = dict(fx=f, fy=f, cx=W / 2, cy=H / 2, W=W, H=H)
+    u, v = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    D = (50 + 2 * np.sin(0.25 * u + 0.1 * v)).astype(np.float32)
+    D[rng.uniform(size=D.shape) < 0.04] = 0.0
+    fr = O.Frame(D, intr, pose12(rot(rng.normal(size=3), 1.0), rng.normal(0, 0.3, 3)))
+    n = 900
+    pts = np.stack([rng.uniform(-25, 25, n), rng.uniform(-19, 19, n), rng.uniform(45, 57, n)], -1).astype(np.float32)
+    nrm = (rng.normal(0, 0.1, (n, 3)) + [0, 0, -1]).astype(np.float32)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    return fr, intr, pts, nrm, rng
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_p10_registration_brute_force_and_accounting(seed):
+    fr, intr, pts, nrm, rng = _fusion_scene(seed)
+    n = len(pts)
+    prm = O.params(k=2, n_nbr=1)
+    g = rng.uniform(-20, 20, (6, 3)).astype(np.float32) + np.float32([0, 0, 50])
+    out = O.fuse(prm, pts, nrm, rng.uniform(0, 1, (n, 3)), rng.integers(1, 11, n).astype(np.float32),
+                 np.zeros(n, np.int32), fr, rng.uniform(0, 1, (intr["H"], intr["W"], 3)), 3, g)
+    # brute force: every point against every pixel, same gates, lexicographic (|dz|, i) min
+    q, N, dv, nv = O.frame_prep(fr)
+    pose = np.array(fr.s.pose[:])
+    R, T = pose[:9].reshape(3, 3), pose[9:]
+    vt = pts.astype(np.float64) @ R.T + T
+    nt = nrm.astype(np.float64) @ R.T
+    H, W = fr.depth.shape
+    xs, ys = np.meshgrid(np.arange(W), np.arange(H))
+    best = {}
+    cd = np.cos(np.deg2rad(prm.delta_deg))
+    for i in range(n):
+        if vt[i, 2] <= 0:
+            continue
+        u = intr["fx"] * vt[i, 0] / vt[i, 2] + intr["cx"]
+        v = intr["fy"] * vt[i, 1] / vt[i, 2] + intr["cy"]
+        hit = (xs - 0.5 <= u) & (u < xs + 0.5) & (ys - 0.5 <= v) & (v < ys + 0.5) & dv & nv
+        dz = np.abs(vt[i, 2] - fr.depth.astype(np.float64))
+        hit &= (dz < min(prm.tau_z, prm.trunc)) & ((N @ nt[i]) > cd)
+        for p in np.flatnonzero(hit.ravel()):
+            key = (dz.ravel()[p], i)
+            if p not in best or key < best[p]:
+                best[p] = key
+    owner = out["owner"]
+    for p in range(H * W):
+        if out["key_margin"][p] <= 1e-6:
+            continue
+        assert owner[p] == (best[p][1] if p in best else -1)
+    # pixel accounting: every valid pixel is registered once or lifted once
+    valid = (dv & nv).ravel()
+    assert (owner >= 0).sum() + out["n_lift"] == valid.sum()
+    assert len(set(owner[owner >= 0])) == (owner >= 0).sum()
+    assert (out["weight"] <= prm.omega_max).all()
+    assert out["lift_w"].shape[0] == out["n_lift"] and np.allclose(out["lift_w"].sum(1), 1.0)
+
+
+def test_p10_refuse_contracts():
+    """Fusing the identical scan twice moves points less the second time."""
+    fr, intr, pts, nrm, rng = _fusion_scene(7)
+    n = len(pts)
+    prm = O.params(k=2, n_nbr=1)
+    g = np.array([[0, 0, 50], [10, 0, 50], [0, 10, 50]], np.float32)
+    w0 = np.ones(n, np.float32)
+    o1 = O.fuse(prm, pts, nrm, np.zeros((n, 3)), w0, np.zeros(n, np.int32), fr, None, 1, g)
+    x1 = o1["xyz"][:n].astype(np.float32)
+    o2 = O.fuse(prm, x1, o1["nrm"][:n], np.zeros((n, 3)), o1["weight"][:n], np.zeros(n, np.int32), fr, None, 2, g)
+    d1 = np.linalg.norm(o1["xyz"][:n] - pts, axis=1)
+    d2 = np.linalg.norm(o2["xyz"][:n] - x1, axis=1)
+    moved = d1 > 1e-9
+    assert moved.sum() > 50
+    assert d2[moved].sum() < d1[moved].sum()
+
+
+# ------------------------------------------------------------------ more closed forms
+def test_point_to_point_and_feature_residuals_golden():
+    """r_pt = v~ - q (north_star point-to-point) on the S:214 plane example; E_corr
+    (Eq. 9): identity field and V = V' -> 0, global T = (1,0,0) -> (1,0,0) per pair."""
+    gd = GOLD["data_term"]
+    D, it = plane_frame(z=gd["plane_z"])
+    fr = O.Frame(D, it, pose12())
+    pb = single_node_problem([[0, 0, gd["point_z"]]], [[0, 0, -1]])
+    s = O.system(O.params(k=1, n_nbr=1, w_reg=0.0), pb, fr, O.identity_state(2))
+    assert abs(s["energy"][1] - 4.0) < 1e-12     # |(0,0,2)|^2
+    src = np.array([[1.0, 2.0, 50.0], [-3.0, 0.5, 48.0]], np.float32)
+    g = np.array([[0, 0, 50], [5, 0, 50], [0, 5, 50]], np.float32)
+    for T, e in [(np.zeros(3), 0.0), (np.array([1.0, 0, 0]), 2.0)]:
+        pb = O.Problem(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 2), np.int32), np.zeros((0, 2)),
+                       g, np.array([[1], [0], [0]], np.int32), src, src)
+        s = O.system(O.params(k=2, n_nbr=1, w_reg=0.0), pb, O.Frame(D, it, pose12(None, T)), O.identity_state(3))
+        assert abs(s["energy"][3] - e) < 1e-12
+
+
+def test_warp_model_closed_forms():
+    """O4: identity field -> unchanged model; rigid-consistent field -> rigid map;
+    nodes advance by t_j (R-A26)."""
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    xyz, nrm, g = O.warp_model(pb, O.identity_state(m))
+    assert np.abs(xyz - pb.xyz).max() < 1e-12 and np.abs(g - pb.g).max() < 1e-12
+    Q, c = rot([1, 0, 1], 5.0), np.array([0.5, -1.0, 2.0])
+    Rt = np.zeros((m, 12))
+    Rt[:, :9] = Q.ravel()
+    Rt[:, 9:] = pb.g.astype(np.float64) @ (Q - np.eye(3)).T + c
+    xyz, nrm, g = O.warp_model(pb, Rt)
+    assert np.abs(xyz - (pb.xyz.astype(np.float64) @ Q.T + c)).max() < 1e-9
+    n64 = pb.nrm.astype(np.float64)
+    assert np.abs(nrm - (n64 / np.linalg.norm(n64, axis=1, keepdims=True)) @ Q.T).max() < 1e-9
+    assert np.abs(g - (pb.g.astype(np.float64) + Rt[:, 9:])).max() < 1e-12
+
+
+def test_fusion_colour_normal_golden():
+    """Eq. 13: omega=1, C=0, C_obs=1 -> 0.5; Eq. 14: equal normals stay; lifted
+    point = back-projected pixel with omega=1, stamp=frame (Alg. 2 Step 3)."""
+    D, it = plane_frame(z=12.0, f=40.0)
+    fr = O.Frame(D, it, pose12())
+    prm = O.params(k=1, n_nbr=1)
+    xyz = np.array([[0, 0, 10.0]], np.float32)
+    out = O.fuse(prm, xyz, np.array([[0, 0, -1]], np.float32), np.zeros((1, 3), np.float32),
+                 np.ones(1, np.float32), np.zeros(1, np.int32), fr,
+                 np.ones((it["H"], it["W"], 3), np.float32), 4, np.array([[0, 0, 0], [9, 9, 9]], np.float32))
+    assert np.allclose(out["rgb"][0], 0.5, atol=1e-12)
+    assert np.allclose(out["nrm"][0], [0, 0, -1], atol=1e-12)
+    valid = (it["W"] - 2) * (it["H"] - 2)
+    assert out["n_lift"] == valid - 1
+    p = 1 + 0   # first lifted point = pixel (1, 1) in row-major order
+    assert np.allclose(out["xyz"][p], [(1 - it["cx"]) * 12 / 40, (1 - it["cy"]) * 12 / 40, 12], atol=1e-12)
+    assert out["weight"][p] == 1.0 and out["stamp"][p] == 4 and np.allclose(out["rgb"][p], 1.0)
