@@ -1,0 +1,214 @@
+/* mis.h -- C-ABI of the B200 (sm_100a) MIS-SLAM registration + fusion hot path.
+ *
+ * MIS-SLAM: "MIS-SLAM: Real-time Large Scale Dense Deformable SLAM System in
+ * Minimal Invasive Surgery Based on Heterogeneous Computing", arXiv 1803.02009.
+ * Citations: P:n = PAPER.md line n (equation / algorithm named), S:n = SPEC.md
+ * line n, "reading An" = DESIGN.md §3.
+ *
+ * Conventions (all calls):
+ *  - Units: millimetres; angles in degrees in mis_params, radians elsewhere.
+ *  - mis_mem says where every pointer argument of the call lives:
+ *    MIS_MEM_HOST (pageable or pinned host memory) or MIS_MEM_DEVICE (device
+ *    memory of the context's GPU, e.g. a torch tensor's data_ptr()).  Device
+ *    inputs are read in stream order on the context stream.
+ *  - Ownership: the library copies every input into context-owned device
+ *    memory (allocated with cudaMalloc on the context's device) and never
+ *    retains a caller pointer after the call returns.  Outputs are written
+ *    into caller buffers.  Calls with host outputs synchronise the context
+ *    stream before returning; calls with device outputs do not.
+ *  - Errors: every call returns a mis_status; no exception crosses the
+ *    boundary.  mis_last_error() gives a human-readable message for the last
+ *    failing call on that context.  Per-point degeneracies (z <= 0, invalid
+ *    depth, vanishing warped normal) are masked, never errors.
+ *  - Threading: a context is not re-entrant; distinct contexts are independent.
+ *  - Layouts: xyz-like arrays are n x 3 row-major float32 (x, y, z), node
+ *    states are m x 12 float32 (R row-major 9, t 3), pose[12] is the
+ *    world->camera transform (R row-major 9, T 3) of Eq. 1.
+ *  - Internal point order: points are kept sorted by their canonical kNN
+ *    tuple (the K13 sort); every per-point output is in that internal order
+ *    and mis_get_model returns the caller ids that map it back.
+ */
+#ifndef MIS_H
+#define MIS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MIS_ABI_VERSION 1
+#define MIS_MAX_GN 32
+#define MIS_MAX_K 8
+
+typedef struct mis_ctx mis_ctx;
+
+typedef enum {
+  MIS_OK = 0,
+  MIS_E_ARG = 1,       /* invalid argument (value, size, range)                     */
+  MIS_E_STATE = 2,     /* call out of order (e.g. register before set_graph)        */
+  MIS_E_CUDA = 3,      /* CUDA runtime error (message in mis_last_error)            */
+  MIS_E_NCCL = 4,      /* NCCL error or NCCL unavailable with world > 1             */
+  MIS_E_NOMEM = 5,     /* device allocation failed                                  */
+  MIS_E_CAPACITY = 6,  /* Group-2 growth would exceed the model capacity            */
+  MIS_E_NUMERIC = 7    /* non-finite GN step; the node state is rolled back         */
+} mis_status;
+
+typedef enum { MIS_MEM_HOST = 0, MIS_MEM_DEVICE = 1 } mis_mem;
+
+/* Pinhole intrinsics: fx, fy > 0; 0 <= cx < width; 0 <= cy < height. */
+typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
+
+/* Flags */
+#define MIS_F_FINAL_ENERGY 1u   /* mis_register also evaluates the energy after the last update */
+#define MIS_F_NO_GRAPH     2u   /* do not capture the GN loop in a CUDA graph                    */
+
+/* Method parameters; defaults (mis_default_params) are the paper's. */
+typedef struct {
+  int32_t k;            /* nodes per point, Eq. 1 (reading A5), 1..8                       */
+  int32_t n_nbr;        /* regulariser neighbours per node, Eq. 6 N(j) (reading A15)       */
+  float w_data;         /* Eq. 8 weight, 1                                         */
+  float w_point;        /* dense point-to-point weight, 1 (reading A13)                    */
+  float w_reg;          /* Eq. 6 weight, 1e4                                       */
+  float w_corr;         /* Eq. 9 weight, 10                                        */
+  float eps_d_mm;       /* Eq. 7 distance gate, 15 mm                              */
+  float eps_n_deg;      /* Eq. 7 angle gate, 10 deg (reading A8)                    */
+  float tau_z_mm;       /* Alg. 1 depth gate, 10 mm                                */
+  float delta_deg;      /* Alg. 1 angle gate, 10 deg                               */
+  float trunc_mm;       /* Eq. 11 truncation, 40 mm (reading A20)                   */
+  float omega_max;      /* Eq. 15 weight cap, 10 (reading A22)                      */
+  int32_t gn_iters;     /* Gauss-Newton iterations G, 1..MIS_MAX_GN (reading A3)           */
+  int32_t pcg_iters;    /* PCG iterations P per GN iteration, >= 1                         */
+  float lambda;         /* GN damping, 1e-4 (reading A16)                                  */
+  uint32_t flags;       /* MIS_F_*                                                         */
+} mis_params;
+
+/* Per-registration report (all host memory). */
+typedef struct {
+  int32_t iters;                       /* GN iterations run                                  */
+  int32_t status;                      /* mis_status of the registration                    */
+  double energy[MIS_MAX_GN + 1][5];    /* per iteration (state before its update): E_data,
+                                          E_point, E_reg, E_corr, weighted total; row
+                                          [iters] = after the last update (MIS_F_FINAL_ENERGY) */
+  int64_t n_assoc[MIS_MAX_GN + 1];     /* associated points per iteration                   */
+  float pcg_rel_res[MIS_MAX_GN];       /* sqrt(r.z / r0.z0) after the last PCG iteration    */
+  int64_t nnzb;                        /* nonzero 6x6 blocks of H (both triangles)           */
+  int64_t n_segments;                  /* distinct kNN tuples in the model                  */
+} mis_report;
+
+int32_t mis_abi_version(void);
+void mis_default_params(mis_params* out);
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to
+ * adopt (e.g. torch.cuda.current_stream().cuda_stream) or NULL to create one.
+ * rank/world: this process' place in a data-parallel job (world >= 1);
+ * nccl_unique_id: 128 bytes from mis_nccl_unique_id on rank 0 (broadcast by
+ * the caller), NULL when world == 1.  With world > 1 every rank must pass its
+ * own point shard to mis_set_model and the same node graph to mis_set_graph;
+ * the node-block system is all-reduced over NCCL each GN iteration. */
+mis_status mis_create(const mis_params* params, int device, void* cuda_stream, int rank, int world,
+                      const void* nccl_unique_id, mis_ctx** out);
+mis_status mis_destroy(mis_ctx* ctx);
+const char* mis_last_error(const mis_ctx* ctx);
+/* 128-byte NCCL unique id (rank 0 only).  MIS_E_NCCL if libnccl cannot be loaded. */
+mis_status mis_nccl_unique_id(void* out128);
+mis_status mis_set_params(mis_ctx* ctx, const mis_params* params);
+
+/* Model points, Sec. II-A "five domains" + normal.  n >= 0 points,
+ * capacity >= n bounds Group-2 growth in mis_fuse.  xyz: world positions v_i;
+ * nrm: unit normals; rgb (n x 3, [0,1], NULL = 0); weight: fusion weights
+ * omega (NULL = 1); stamp: frame stamps t_i (NULL = 0); ids: caller ids
+ * (NULL = 0..n-1).  Invalidates the graph binding (call mis_set_graph next). */
+mis_status mis_set_model(mis_ctx* ctx, int64_t n, mis_mem mem, const float* xyz, const float* nrm,
+                         const float* rgb, const float* weight, const int32_t* stamp, const int64_t* ids,
+                         int64_t capacity);
+
+/* ED graph (Sec. II-D).  node_pos: m x 3 positions g_j; node_nbr:
+ * m x n_nbr neighbour ids of Eq. 6, -1 padded, never self (MIS_E_ARG);
+ * knn_idx / knn_w: n x k skinning of the model points in the caller's point
+ * order (distinct ids per point, weights >= 0, normalised in the warp,
+ * reading A6).  knn_idx == NULL: the skinning is computed on the device by
+ * Eq. 2 (k+1 nearest nodes, ties to the lower id; requires m >= k+1).
+ * Resets every node transform to the identity (R_j = I, t_j = 0).  Sorts the
+ * points by their canonical kNN tuple (internal order). */
+mis_status mis_set_graph(mis_ctx* ctx, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
+                         const int32_t* knn_idx, const float* knn_w);
+
+/* Current observation: depth (H x W mm, <= 0 or non-finite = invalid),
+ * intrinsics and the world->camera pose (the ORB-SLAM input of P:85, fixed
+ * during registration, reading A2).  Computes the normal map (K1). */
+mis_status mis_set_frame(mis_ctx* ctx, mis_mem mem, const float* depth_mm, const mis_intrinsics* intr,
+                         const float pose[12]);
+/* Sparse ORB feature pairs (Eq. 9): feat_src n_feat x 3 model-side
+ * positions V_i (world, frame n-1), feat_dst n_feat x 3 observed positions
+ * (camera frame, frame n).  Skinned on the device by Eq. 2. */
+mis_status mis_set_features(mis_ctx* ctx, mis_mem mem, int32_t n_feat, const float* feat_src,
+                            const float* feat_dst);
+
+/* One registration (Sec. II-E/F): mis_set_frame + mis_set_features + G
+ * Gauss-Newton iterations of warp (Eq. 1), association (Eq. 7), residuals
+ * (Eq. 6, 8, 9, point-to-point), 6x6 block normal equations, block-Jacobi PCG
+ * (P iterations, x0 = 0) and the node update R_j <- Exp(dtheta) R_j, t_j += dt
+ * (reading A18), starting from the current node state.  depth_mm == NULL
+ * keeps the frame of the last mis_set_frame; n_feat < 0 keeps the features.
+ * rep (host, nullable) receives the report (synchronises). */
+mis_status mis_register(mis_ctx* ctx, mis_mem mem, const float* depth_mm, const mis_intrinsics* intr,
+                        const float pose[12], int32_t n_feat, const float* feat_src, const float* feat_dst,
+                        mis_report* rep);
+
+/* Node transforms: R9_t3 m x 12 float32 (mem) or fp64 master copy (host). */
+mis_status mis_get_nodes(mis_ctx* ctx, mis_mem mem, float* R9_t3);
+mis_status mis_get_nodes_f64(mis_ctx* ctx, double* R9_t3_host);
+/* Current node positions g_j (m x 3). */
+mis_status mis_get_graph(mis_ctx* ctx, mis_mem mem, float* node_pos);
+
+/* Alg. 2 Step 2: apply the converged field to every point and
+ * normal; the model becomes the live world-frame state x_hat_i; the nodes
+ * advance g_j += t_j and reset (reading A26).  xyz_cam / nrm_cam (n x 3,
+ * nullable, internal order) receive R x_hat + T and the camera-frame normals. */
+mis_status mis_warp(mis_ctx* ctx, mis_mem mem, float* xyz_cam, float* nrm_cam);
+
+/* Alg. 1 + Alg. 2 Step 3 on the current frame: exclusive
+ * point-to-pixel registration (gates |z - D| < tau_z, < trunc, angle < delta;
+ * smallest |dz| then lower internal index wins, reading A19), Eq. 12-15
+ * weighted-average fusion of the winners, and lifting of every valid,
+ * unregistered pixel into a new point (row-major order, omega = 1, stamp =
+ * frame_index, skinned by Eq. 2).  rgb: H x W x 3 observed colour (mem;
+ * NULL = no colour fusion, lifted colour 0).  n_out (host): new model size;
+ * stats (host, nullable): [registered, lifted, valid pixels, model size].
+ * MIS_E_CAPACITY (model unchanged) if the lift exceeds the capacity. */
+mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out,
+                    int64_t stats[4]);
+
+/* Read the model (internal order).  Any output may be NULL.  knn_idx/knn_w:
+ * n x k in the canonical per-point order (ids ascending). */
+mis_status mis_get_model(mis_ctx* ctx, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight,
+                         int32_t* stamp, int64_t* ids, int32_t* knn_idx, float* knn_w, int64_t* n_host);
+
+/* Eq. 2 skinning (k+1 nearest of the current nodes, ties to the lower id,
+ * d_max = 0 -> 1/k) of nq query points: idx / w n x k, ids ascending. */
+mis_status mis_skin(mis_ctx* ctx, mis_mem mem, int64_t nq, const float* pts, int32_t* idx, float* w);
+
+/* ---- stage outputs for parity tests (same kernels as the hot path) ---- */
+/* Inject a node state (m x 12 float32: R row-major, t); fp64 master = upcast. */
+mis_status mis_dbg_set_nodes(mis_ctx* ctx, mis_mem mem, const float* R9_t3);
+/* Normal map of the current frame: H x W x 4 (nx, ny, nz, D); n = 0 when the
+ * normal is invalid, D = 0 when the depth is invalid. */
+mis_status mis_dbg_frame(mis_ctx* ctx, mis_mem mem, float* nmap);
+/* Association of every point under the current node state (Eq. 7): pix =
+ * py*W + px or -1; why = passed gates, bit0 z>0, bit1 in frame, bit2 depth
+ * valid, bit3 normal valid, bit4 distance, bit5 angle (short-circuit). */
+mis_status mis_dbg_associate(mis_ctx* ctx, mis_mem mem, int32_t* pix, uint8_t* why);
+/* The normal equations at the current state: full BSR (both triangles,
+ * rows sorted by column): row_ptr (m+1), col (nnzb), val (nnzb x 36,
+ * row-major 6x6, unknowns [dtheta, dt] per node), rhs (6m) = -J^T r, energy[5].
+ * With val == NULL only *nnzb is returned.  Host memory only. */
+mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* val, float* rhs,
+                          double energy[5], int64_t* nnzb);
+/* The fusion registration of the current frame without applying it: owner
+ * (H*W, internal point index or -1), why (n). Host memory only. */
+mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIS_H */

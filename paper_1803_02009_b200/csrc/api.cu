@@ -1,0 +1,910 @@
+// api.cu -- the C-ABI of libmis (include/mis.h): context, argument checking,
+// uploads, orchestration of the kernels of one frame, NCCL plumbing.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "ctx.cuh"
+
+struct mis_ctx : public mis::Ctx {};
+
+namespace mis {
+
+// ------------------------------------------------------------ buffers
+cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.p && b.bytes >= bytes) return cudaSuccess;
+  if (b.p) {
+    cudaError_t e = cudaStreamSynchronize(c->st);   // the old buffer may still be in use
+    if (e != cudaSuccess) return e;
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  size_t alloc = bytes + bytes / 4 + 256;
+  cudaError_t e = cudaMalloc(&b.p, alloc);
+  if (e != cudaSuccess) { b.p = nullptr; return e; }
+  b.bytes = alloc;
+  return cudaSuccess;
+}
+
+void free_buf(DBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+ModelView model_view(Ctx* c) {
+  ModelBufs& B = c->mb[c->cur];
+  ModelView v;
+  v.n = c->n; v.cap = c->cap;
+  v.px = B.px.as<float>(); v.py = B.py.as<float>(); v.pz = B.pz.as<float>();
+  v.nx = B.nx.as<float>(); v.ny = B.ny.as<float>(); v.nz = B.nz.as<float>();
+  v.cr = B.cr.as<float>(); v.cg = B.cg.as<float>(); v.cb = B.cb.as<float>(); v.w = B.w.as<float>();
+  v.stamp = B.stamp.as<int32_t>(); v.ids = B.ids.as<int64_t>();
+  v.kidx = B.kidx.as<int32_t>(); v.kw = B.kw.as<float>();
+  return v;
+}
+
+NodeView node_view(Ctx* c) {
+  NodeView v;
+  v.m = c->m; v.g = c->g.as<float>(); v.node32 = c->node32.as<float>(); v.Rt64 = c->Rt64.as<double>();
+  return v;
+}
+
+FrameView frame_view(Ctx* c) {
+  FrameView f;
+  f.W = c->W; f.H = c->H;
+  f.fx = c->intr.fx; f.fy = c->intr.fy; f.cx = c->intr.cx; f.cy = c->intr.cy;
+  f.fxd = c->intr.fx; f.fyd = c->intr.fy; f.cxd = c->intr.cx; f.cyd = c->intr.cy;
+  f.depth = c->depth.as<float>();
+  f.nmap = c->nmap.as<float4>();
+  for (int i = 0; i < 9; ++i) { f.R[i] = c->pose[i]; f.Rd[i] = c->pose[i]; }
+  for (int i = 0; i < 3; ++i) { f.T[i] = c->pose[9 + i]; f.Td[i] = c->pose[9 + i]; }
+  return f;
+}
+
+AccView acc_view(Ctx* c) {
+  AccView a;
+  float* base = c->acc.as<float>();
+  const size_t nz = (size_t)c->nnzb, m = (size_t)c->m;
+  a.data = base;
+  a.mom = a.data + nz * 36;
+  a.graph = a.mom + nz * 16;
+  a.rhs_data = a.graph + nz * 36;
+  a.node_mom = a.rhs_data + 6 * m;
+  a.rhs_graph = a.node_mom + 12 * m;
+  a.energy = c->energy.as<double>();
+  return a;
+}
+
+// ------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(void**, int, char[128], int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+// ncclDataType_t / ncclRedOp_t values (nccl.h, NCCL 2.x)
+enum { kNcclInt64 = 4, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8 };
+enum { kNcclSum = 0, kNcclMax = 2 };
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { api.why = "libnccl.so.2 not found"; return; }
+    api.GetUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (int (*)(void**, int, char[128], int))dlsym(h, "ncclCommInitRank");
+    api.AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+    api.AllGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(h, "ncclAllGather");
+    api.CommDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    api.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy;
+    if (!api.ok) api.why = "libnccl symbols missing";
+  });
+  return api;
+}
+
+static cudaError_t nccl_ret(Ctx* c, int r) {
+  if (r == 0) return cudaSuccess;
+  c->err = std::string("NCCL error: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+  return cudaErrorUnknown;
+}
+cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count) {
+  return nccl_ret(c, nccl().AllReduce(buf, buf, count, kNcclFloat32, kNcclSum, c->nccl_comm, c->st));
+}
+cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count) {
+  return nccl_ret(c, nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->nccl_comm, c->st));
+}
+cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count) {
+  return nccl_ret(c, nccl().AllReduce(buf, buf, count, kNcclInt64, kNcclMax, c->nccl_comm, c->st));
+}
+cudaError_t nccl_allgather_u64(Ctx* c, const uint64_t* send, uint64_t* recv, size_t count) {
+  return nccl_ret(c, nccl().AllGather(send, recv, count, kNcclUint64, c->nccl_comm, c->st));
+}
+
+// ------------------------------------------------------------ small kernels
+__global__ void k_deinterleave3(int64_t n, const float* aos, float* x, float* y, float* z, float dflt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (aos) { x[i] = aos[3 * i]; y[i] = aos[3 * i + 1]; z[i] = aos[3 * i + 2]; }
+  else { x[i] = dflt; y[i] = dflt; z[i] = dflt; }
+}
+__global__ void k_interleave3(int64_t n, const float* x, const float* y, const float* z, float* aos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  aos[3 * i] = x[i]; aos[3 * i + 1] = y[i]; aos[3 * i + 2] = z[i];
+}
+__global__ void k_fill_defaults(int64_t n, int64_t id0, float* w, int32_t* stamp, int64_t* ids, bool fw, bool fs,
+                                bool fi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (fw) w[i] = 1.0f;
+  if (fs) stamp[i] = 0;
+  if (fi) ids[i] = id0 + i;
+}
+// point-major (n x K) caller skinning -> slot-major, ids ascending; validation flags
+__global__ void k_canon_knn(int64_t n, int K, int m, const int32_t* idx_pm, const float* w_pm, int64_t cap,
+                            int32_t* kidx, float* kw, int* flag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int id[MIS_MAX_K];
+  float w[MIS_MAX_K];
+  for (int s = 0; s < K; ++s) { id[s] = idx_pm[i * K + s]; w[s] = w_pm[i * K + s]; }
+  for (int a = 1; a < K; ++a)
+    for (int b = a; b > 0 && id[b] < id[b - 1]; --b) {
+      int t = id[b]; id[b] = id[b - 1]; id[b - 1] = t;
+      float tw = w[b]; w[b] = w[b - 1]; w[b - 1] = tw;
+    }
+  int f = 0;
+  for (int s = 0; s < K; ++s) {
+    if (id[s] < 0 || id[s] >= m) f |= 1;
+    if (s > 0 && id[s] == id[s - 1]) f |= 2;
+    if (!(w[s] >= 0.f) || !isfinite(w[s])) f |= 4;
+    kidx[s * cap + i] = id[s] < 0 ? 0 : (id[s] >= m ? m - 1 : id[s]);
+    kw[s * cap + i] = w[s];
+  }
+  if (f) atomicOr(flag, f);
+}
+__global__ void k_to_point_major(int64_t n, int K, int64_t cap, const int32_t* kidx, const float* kw, int32_t* idx_pm,
+                                 float* w_pm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int s = 0; s < K; ++s) {
+    if (idx_pm) idx_pm[i * K + s] = kidx[s * cap + i];
+    if (w_pm) w_pm[i * K + s] = kw[s * cap + i];
+  }
+}
+__global__ void k_check_nbr(int m, int n_nbr, const int32_t* nbr, int* flag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * n_nbr) return;
+  const int l = nbr[t];
+  if (l < -1 || l >= m || l == t / n_nbr) atomicOr(flag, 8);
+}
+__global__ void k_init_nodes(int m, const float* g, double* Rt64, float* node32) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (int i = 0; i < 12; ++i) Rt64[12 * j + i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
+  for (int i = 0; i < 12; ++i) node32[16 * j + i] = (float)Rt64[12 * j + i];
+  for (int c = 0; c < 3; ++c) node32[16 * j + 12 + c] = g[3 * j + c];
+  node32[16 * j + 15] = 0.f;
+}
+__global__ void k_set_nodes(int m, const float* Rt, double* Rt64, float* node32) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (int i = 0; i < 12; ++i) {
+    Rt64[12 * j + i] = (double)Rt[12 * j + i];
+    node32[16 * j + i] = Rt[12 * j + i];
+  }
+}
+__global__ void k_get_nodes(int m, const float* node32, float* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  for (int i = 0; i < 12; ++i) out[12 * j + i] = node32[16 * j + i];
+}
+__global__ void k_count_winners(int n, const unsigned long long* key, unsigned long long* cnt) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = __syncthreads_count(p < n && key[p] != ~0ull);
+  if (threadIdx.x == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+
+static inline int nb(int64_t n, int t = 256) { return (int)((n + t - 1) / t); }
+
+}  // namespace mis
+
+using namespace mis;
+
+// ------------------------------------------------------------ error helpers
+static mis_status fail(Ctx* c, mis_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+static mis_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
+  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e) + (c->err.empty() ? "" : "");
+  return MIS_E_CUDA;
+}
+#define TRY(c, call)                                              \
+  do {                                                            \
+    cudaError_t e__ = (call);                                     \
+    if (e__ != cudaSuccess) return cuda_fail((c), e__, #call);    \
+  } while (0)
+
+static cudaMemcpyKind kind_in(mis_mem mem) { return mem == MIS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice; }
+static cudaMemcpyKind kind_out(mis_mem mem) { return mem == MIS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice; }
+
+static mis_status check_params(const mis_params* p) {
+  if (!p) return MIS_E_ARG;
+  if (p->k < 1 || p->k > MIS_MAX_K || p->n_nbr < 0 || p->gn_iters < 1 || p->gn_iters > MIS_MAX_GN ||
+      p->pcg_iters < 0 || !(p->eps_d_mm > 0) || !(p->eps_n_deg > 0) || !(p->tau_z_mm > 0) || !(p->trunc_mm > 0) ||
+      !(p->omega_max >= 1) || !(p->lambda >= 0))
+    return MIS_E_ARG;
+  return MIS_OK;
+}
+
+// ------------------------------------------------------------ C-ABI
+extern "C" {
+
+int32_t mis_abi_version(void) { return MIS_ABI_VERSION; }
+
+void mis_default_params(mis_params* o) {
+  if (!o) return;
+  o->k = 4; o->n_nbr = 4;
+  o->w_data = 1.0f; o->w_point = 1.0f; o->w_reg = 1e4f; o->w_corr = 10.0f;
+  o->eps_d_mm = 15.0f; o->eps_n_deg = 10.0f;
+  o->tau_z_mm = 10.0f; o->delta_deg = 10.0f; o->trunc_mm = 40.0f; o->omega_max = 10.0f;
+  o->gn_iters = 5; o->pcg_iters = 10; o->lambda = 1e-4f; o->flags = 0;
+}
+
+const char* mis_last_error(const mis_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+mis_status mis_nccl_unique_id(void* out128) {
+  if (!out128) return MIS_E_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return MIS_E_NCCL;
+  return api.GetUniqueId(out128) == 0 ? MIS_OK : MIS_E_NCCL;
+}
+
+mis_status mis_create(const mis_params* params, int device, void* cuda_stream, int rank, int world,
+                      const void* nccl_unique_id, mis_ctx** out) {
+  if (!out) return MIS_E_ARG;
+  *out = nullptr;
+  if (check_params(params) != MIS_OK || world < 1 || rank < 0 || rank >= world) return MIS_E_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return MIS_E_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return MIS_E_CUDA;
+  mis_ctx* c = new mis_ctx();
+  c->prm = *params;
+  c->K = params->k;
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    c->st = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) { delete c; return MIS_E_CUDA; }
+    c->own_stream = true;
+  }
+  if (world > 1) {
+    NcclApi& api = nccl();
+    if (!api.ok || !nccl_unique_id) { delete c; return MIS_E_NCCL; }
+    char id[128];
+    memcpy(id, nccl_unique_id, 128);
+    if (api.CommInitRank(&c->nccl_comm, world, id, rank) != 0) { delete c; return MIS_E_NCCL; }
+  }
+  if (ensure(c, c->rep_energy, (MIS_MAX_GN + 1) * 5 * 8) != cudaSuccess ||
+      ensure(c, c->rep_nassoc, (MIS_MAX_GN + 1) * 8) != cudaSuccess ||
+      ensure(c, c->rep_res, MIS_MAX_GN * 4) != cudaSuccess || ensure(c, c->numeric_flag, 16) != cudaSuccess ||
+      ensure(c, c->counter, 64) != cudaSuccess) {
+    delete c;
+    return MIS_E_NOMEM;
+  }
+  *out = c;
+  return MIS_OK;
+}
+
+mis_status mis_destroy(mis_ctx* c) {
+  if (!c) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  DBuf* all[] = {&c->g, &c->nbr, &c->node32, &c->Rt64, &c->keys, &c->keys2, &c->vals, &c->vals2, &c->flags,
+                 &c->scan, &c->seg_start, &c->seg_nodes, &c->chunks, &c->chunk_off, &c->ckeys, &c->ckeys2,
+                 &c->uflag, &c->upos, &c->ukeys, &c->row_ptr, &c->col, &c->diag_pos, &c->upper_of, &c->seg_slot,
+                 &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->acc, &c->energy, &c->Hval, &c->rhs, &c->Minv,
+                 &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots, &c->numeric_flag, &c->depth, &c->nmap,
+                 &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey, &c->pix, &c->why,
+                 &c->lift_counts, &c->counter, &c->rep_energy, &c->rep_nassoc, &c->rep_res, &c->cub_tmp};
+  for (DBuf* b : all) free_buf(*b);
+  for (int s = 0; s < 2; ++s) {
+    ModelBufs& B = c->mb[s];
+    DBuf* mbv[] = {&B.px, &B.py, &B.pz, &B.nx, &B.ny, &B.nz, &B.cr, &B.cg, &B.cb, &B.w, &B.stamp, &B.ids, &B.kidx, &B.kw};
+    for (DBuf* b : mbv) free_buf(*b);
+  }
+  if (c->nccl_comm && nccl().ok) nccl().CommDestroy(c->nccl_comm);
+  if (c->own_stream) cudaStreamDestroy(c->st);
+  delete c;
+  return MIS_OK;
+}
+
+mis_status mis_set_params(mis_ctx* c, const mis_params* p) {
+  if (!c) return MIS_E_ARG;
+  if (check_params(p) != MIS_OK) return fail(c, MIS_E_ARG, "invalid parameters");
+  if (p->k != c->prm.k && c->have_graph) return fail(c, MIS_E_STATE, "k cannot change after mis_set_graph");
+  if (p->n_nbr != c->prm.n_nbr && c->have_graph) return fail(c, MIS_E_STATE, "n_nbr cannot change after mis_set_graph");
+  c->prm = *p;
+  c->K = p->k;
+  c->pattern_valid = false;
+  return MIS_OK;
+}
+
+mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, const float* nrm, const float* rgb,
+                         const float* weight, const int32_t* stamp, const int64_t* ids, int64_t capacity) {
+  if (!c) return MIS_E_ARG;
+  if (n < 0 || capacity < n || (n > 0 && (!xyz || !nrm)) || capacity > (int64_t)0x7fffffff)
+    return fail(c, MIS_E_ARG, "set_model: bad sizes or null xyz/nrm");
+  cudaSetDevice(c->device);
+  const int K = c->K;
+  if (capacity < 1) capacity = 1;
+  for (int s = 0; s < 2; ++s) {
+    ModelBufs& B = c->mb[s];
+    DBuf* f[] = {&B.px, &B.py, &B.pz, &B.nx, &B.ny, &B.nz, &B.cr, &B.cg, &B.cb, &B.w};
+    for (DBuf* b : f) TRY(c, ensure(c, *b, capacity * 4));
+    TRY(c, ensure(c, B.stamp, capacity * 4));
+    TRY(c, ensure(c, B.ids, capacity * 8));
+    TRY(c, ensure(c, B.kidx, capacity * 4 * MIS_MAX_K));
+    TRY(c, ensure(c, B.kw, capacity * 4 * MIS_MAX_K));
+  }
+  c->cur = 0;
+  c->cap = capacity;
+  c->n = n;
+  ModelView md = model_view(c);
+  if (n > 0) {
+    TRY(c, ensure(c, c->stage, n * 12));
+    float* st = c->stage.as<float>();
+    TRY(c, cudaMemcpyAsync(st, xyz, n * 12, kind_in(mem), c->st));
+    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, st, md.px, md.py, md.pz, 0.f);
+    TRY(c, cudaMemcpyAsync(st, nrm, n * 12, kind_in(mem), c->st));
+    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, st, md.nx, md.ny, md.nz, 0.f);
+    if (rgb) TRY(c, cudaMemcpyAsync(st, rgb, n * 12, kind_in(mem), c->st));
+    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, rgb ? st : nullptr, md.cr, md.cg, md.cb, 0.f);
+    if (weight) TRY(c, cudaMemcpyAsync(md.w, weight, n * 4, kind_in(mem), c->st));
+    if (stamp) TRY(c, cudaMemcpyAsync(md.stamp, stamp, n * 4, kind_in(mem), c->st));
+    if (ids) TRY(c, cudaMemcpyAsync(md.ids, ids, n * 8, kind_in(mem), c->st));
+    k_fill_defaults<<<nb(n), 256, 0, c->st>>>(n, 0, md.w, md.stamp, md.ids, !weight, !stamp, !ids);
+    TRY(c, cudaGetLastError());
+  }
+  c->next_id = n;
+  if (ids && n > 0) {   // next fresh id = max(ids) + 1 (host read)
+    std::vector<int64_t> h(n);
+    TRY(c, cudaMemcpyAsync(h.data(), md.ids, n * 8, cudaMemcpyDeviceToHost, c->st));
+    TRY(c, cudaStreamSynchronize(c->st));
+    int64_t mx = -1;
+    for (int64_t v : h) mx = v > mx ? v : mx;
+    c->next_id = mx + 1;
+  }
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  c->have_model = true;
+  c->have_graph = false;
+  c->pattern_valid = false;
+  return MIS_OK;
+}
+
+mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
+                         const int32_t* knn_idx, const float* knn_w) {
+  if (!c) return MIS_E_ARG;
+  if (!c->have_model) return fail(c, MIS_E_STATE, "set_graph before set_model");
+  const int K = c->K, nn = c->prm.n_nbr;
+  if (m < 1 || !node_pos || (nn > 0 && !node_nbr) || (knn_idx && !knn_w))
+    return fail(c, MIS_E_ARG, "set_graph: bad arguments");
+  if (!knn_idx && m < K + 1) return fail(c, MIS_E_ARG, "device skinning needs m >= k+1 (Eq. 2)");
+  if (knn_idx && m < K) return fail(c, MIS_E_ARG, "k distinct nodes per point need m >= k");
+  cudaSetDevice(c->device);
+  c->m = m;
+  TRY(c, ensure(c, c->g, (size_t)m * 12));
+  TRY(c, ensure(c, c->nbr, (size_t)m * (nn > 0 ? nn : 1) * 4));
+  TRY(c, ensure(c, c->node32, (size_t)m * 64));
+  TRY(c, ensure(c, c->Rt64, (size_t)m * 96));
+  TRY(c, cudaMemcpyAsync(c->g.p, node_pos, (size_t)m * 12, kind_in(mem), c->st));
+  if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, kind_in(mem), c->st));
+  int* flag = c->counter.as<int>();
+  TRY(c, cudaMemsetAsync(flag, 0, 4, c->st));
+  if (nn > 0) k_check_nbr<<<nb((int64_t)m * nn), 256, 0, c->st>>>(m, nn, c->nbr.as<int32_t>(), flag);
+  ModelView md = model_view(c);
+  const int64_t n = c->n;
+  if (n > 0) {
+    if (knn_idx) {
+      TRY(c, ensure(c, c->stage, n * K * 8));
+      int32_t* si = c->stage.as<int32_t>();
+      float* sw = reinterpret_cast<float*>(si + n * K);
+      TRY(c, cudaMemcpyAsync(si, knn_idx, n * K * 4, kind_in(mem), c->st));
+      TRY(c, cudaMemcpyAsync(sw, knn_w, n * K * 4, kind_in(mem), c->st));
+      k_canon_knn<<<nb(n), 256, 0, c->st>>>(n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
+    } else {
+      launch_skin(n, md.px, md.py, md.pz, 1, c->g.as<float>(), m, K, md.kidx, md.kw, c->cap, c->st);
+    }
+  }
+  int hflag = 0;
+  TRY(c, cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  if (hflag) {
+    c->have_graph = false;
+    return fail(c, MIS_E_ARG, std::string("set_graph: invalid") + ((hflag & 1) ? " node id" : "") +
+                                  ((hflag & 2) ? " duplicate id" : "") + ((hflag & 4) ? " weight" : "") +
+                                  ((hflag & 8) ? " neighbour list" : ""));
+  }
+  k_init_nodes<<<nb(m), 256, 0, c->st>>>(m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
+  TRY(c, cudaGetLastError());
+  TRY(c, build_order(c));
+  c->have_graph = true;
+  return MIS_OK;
+}
+
+mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it, const float pose[12]) {
+  if (!c) return MIS_E_ARG;
+  if (!depth_mm || !it || !pose) return fail(c, MIS_E_ARG, "set_frame: null argument");
+  if (!(it->fx > 0) || !(it->fy > 0) || it->width < 3 || it->height < 3 || !(it->cx >= 0) || !(it->cx < it->width) ||
+      !(it->cy >= 0) || !(it->cy < it->height))
+    return fail(c, MIS_E_ARG, "set_frame: invalid intrinsics (S:24)");
+  cudaSetDevice(c->device);
+  c->intr = *it;
+  c->W = it->width;
+  c->H = it->height;
+  memcpy(c->pose, pose, 48);   // pose is host memory (12 floats) in every mode
+  const size_t px = (size_t)c->W * c->H;
+  TRY(c, ensure(c, c->depth, px * 4));
+  TRY(c, ensure(c, c->nmap, px * 16));
+  TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, kind_in(mem), c->st));
+  launch_frame_prep(frame_view(c), c->nmap.as<float4>(), c->st);
+  TRY(c, cudaGetLastError());
+  c->have_frame = true;
+  return MIS_OK;
+}
+
+mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float* src, const float* dst) {
+  if (!c) return MIS_E_ARG;
+  if (n_feat < 0 || (n_feat > 0 && (!src || !dst))) return fail(c, MIS_E_ARG, "set_features: bad arguments");
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "set_features before set_graph");
+  if (n_feat > 0 && c->m < c->K + 1) return fail(c, MIS_E_ARG, "feature skinning needs m >= k+1");
+  cudaSetDevice(c->device);
+  c->nf = n_feat;
+  const int K = c->K;
+  TRY(c, ensure(c, c->fsrc, (size_t)n_feat * 12 + 16));
+  TRY(c, ensure(c, c->fdst, (size_t)n_feat * 12 + 16));
+  TRY(c, ensure(c, c->fidx, (size_t)n_feat * K * 4 + 16));
+  TRY(c, ensure(c, c->fw, (size_t)n_feat * K * 4 + 16));
+  if (n_feat > 0) {
+    TRY(c, cudaMemcpyAsync(c->fsrc.p, src, (size_t)n_feat * 12, kind_in(mem), c->st));
+    TRY(c, cudaMemcpyAsync(c->fdst.p, dst, (size_t)n_feat * 12, kind_in(mem), c->st));
+    const float* s = c->fsrc.as<float>();
+    launch_skin(n_feat, s, s + 1, s + 2, 3, c->g.as<float>(), c->m, K, c->fidx.as<int32_t>(), c->fw.as<float>(),
+                n_feat, c->st);
+    TRY(c, cudaGetLastError());
+  }
+  c->pattern_valid = false;
+  return MIS_OK;
+}
+
+// zero the accumulators, run K3 (+ K4/K5 on rank 0), all-reduce across ranks
+static mis_status assemble(Ctx* c, bool dbg) {
+  AccView acc = acc_view(c);
+  TRY(c, cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));
+  TRY(c, cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
+  const double d2r = M_PI / 180.0;
+  AsmPointsArgs a;
+  a.md = model_view(c);
+  a.seg_nodes = c->seg_nodes.as<int32_t>();
+  a.chunks = c->chunks.as<int4>();
+  a.nchunk = c->nchunk;
+  a.seg_slot = c->seg_slot.as<int32_t>();
+  a.nd = node_view(c);
+  a.fr = frame_view(c);
+  a.eps_d = c->prm.eps_d_mm;
+  a.eps_dd = c->prm.eps_d_mm;
+  a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
+  a.cos_eps_n = (float)a.cos_eps_nd;
+  a.acc = acc;
+  a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
+  a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
+  launch_assemble_points(c->K, a, c->num_sms, c->st);
+  TRY(c, cudaGetLastError());
+  if (c->rank == 0) {
+    AsmGraphArgs gA;
+    gA.nd = node_view(c);
+    gA.n_nbr = c->prm.n_nbr;
+    gA.nbr = c->nbr.as<int32_t>();
+    gA.edge_slot = c->edge_slot.as<int32_t>();
+    gA.diag_slot = c->diag_pos.as<int32_t>();
+    gA.nf = c->nf;
+    gA.fsrc = c->fsrc.as<float>();
+    gA.fdst = c->fdst.as<float>();
+    gA.fidx = c->fidx.as<int32_t>();
+    gA.fw = c->fw.as<float>();
+    gA.feat_slot = c->feat_slot.as<int32_t>();
+    gA.fr = frame_view(c);
+    gA.w_reg = c->prm.w_reg;
+    gA.w_corr = c->prm.w_corr;
+    gA.acc = acc;
+    gA.K = c->K;
+    launch_assemble_graph(gA, c->st);
+    TRY(c, cudaGetLastError());
+  }
+  if (c->world > 1) {
+    if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
+    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 8) != cudaSuccess) return MIS_E_NCCL;
+  }
+  return MIS_OK;
+}
+
+static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
+  SolveArgs s;
+  s.m = c->m;
+  s.K = c->K;
+  s.nnzb = c->nnzb;
+  s.row_ptr = c->row_ptr.as<int32_t>();
+  s.col = c->col.as<int32_t>();
+  s.upper_of = c->upper_of.as<int32_t>();
+  s.diag_pos = c->diag_pos.as<int32_t>();
+  s.acc = acc_view(c);
+  s.w_data = c->prm.w_data;
+  s.w_pt = c->prm.w_point;
+  s.lambda = c->prm.lambda;
+  s.pcg_iters = pcg_iters;
+  s.Hval = c->Hval.as<float>();
+  s.rhs = c->rhs.as<float>();
+  s.Minv = c->Minv.as<float>();
+  s.x = c->x.as<float>(); s.r = c->r.as<float>(); s.z = c->z.as<float>(); s.p = c->p.as<float>(); s.Ap = c->Ap.as<float>();
+  s.dots = c->dots.as<double>();
+  s.nd = node_view(c);
+  s.do_update = update ? 1 : 0;
+  s.gn_it = it;
+  s.rep_energy = c->rep_energy.as<double>();
+  s.rep_nassoc = c->rep_nassoc.as<double>();
+  s.rep_res = c->rep_res.as<float>();
+  s.numeric_flag = c->numeric_flag.as<int>();
+  return s;
+}
+
+static mis_status prepare(Ctx* c) {
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph (mis_set_graph)");
+  if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
+  if (c->dirty) TRY(c, build_order(c));
+  if (!c->pattern_valid) TRY(c, build_pattern(c));
+  if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
+  return MIS_OK;
+}
+
+static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
+  memset(rep, 0, sizeof(*rep));
+  double e[(MIS_MAX_GN + 1) * 5], na[MIS_MAX_GN + 1];
+  TRY(c, cudaMemcpyAsync(e, c->rep_energy.p, sizeof(e), cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaMemcpyAsync(na, c->rep_nassoc.p, sizeof(na), cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaMemcpyAsync(rep->pcg_rel_res, c->rep_res.p, sizeof(rep->pcg_rel_res), cudaMemcpyDeviceToHost, c->st));
+  int flag = 0;
+  TRY(c, cudaMemcpyAsync(&flag, c->numeric_flag.p, 4, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  rep->iters = iters;
+  rep->status = flag ? MIS_E_NUMERIC : MIS_OK;
+  for (int i = 0; i <= MIS_MAX_GN; ++i) {
+    for (int q = 0; q < 5; ++q) rep->energy[i][q] = e[5 * i + q];
+    rep->n_assoc[i] = (int64_t)llround(na[i]);
+  }
+  rep->nnzb = c->nnzb;
+  rep->n_segments = c->nseg;
+  return flag ? MIS_E_NUMERIC : MIS_OK;
+}
+
+mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* intr,
+                        const float pose[12], int32_t n_feat, const float* feat_src, const float* feat_dst,
+                        mis_report* rep) {
+  if (!c) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  mis_status s;
+  if (depth_mm) {
+    if ((s = mis_set_frame(c, mem, depth_mm, intr, pose)) != MIS_OK) return s;
+  } else if (pose) {
+    memcpy(c->pose, pose, 48);
+  }
+  if (n_feat >= 0)
+    if ((s = mis_set_features(c, mem, n_feat, feat_src, feat_dst)) != MIS_OK) return s;
+  if ((s = prepare(c)) != MIS_OK) return s;
+  const int G = c->prm.gn_iters;
+  TRY(c, cudaMemsetAsync(c->numeric_flag.p, 0, 4, c->st));
+  TRY(c, cudaMemsetAsync(c->rep_energy.p, 0, (MIS_MAX_GN + 1) * 5 * 8, c->st));
+  TRY(c, cudaMemsetAsync(c->rep_nassoc.p, 0, (MIS_MAX_GN + 1) * 8, c->st));
+  for (int it = 0; it < G; ++it) {
+    if ((s = assemble(c, false)) != MIS_OK) return s;
+    launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, it,
+                         c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
+    TRY(c, launch_solve(solve_args(c, it, true, c->prm.pcg_iters), c->num_sms, c->st));
+  }
+  if (c->prm.flags & MIS_F_FINAL_ENERGY) {
+    if ((s = assemble(c, false)) != MIS_OK) return s;
+    launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, G,
+                         c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
+  }
+  TRY(c, cudaGetLastError());
+  if (rep) return fill_report(c, rep, G);
+  return MIS_OK;
+}
+
+mis_status mis_get_nodes(mis_ctx* c, mis_mem mem, float* out) {
+  if (!c || !out) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  cudaSetDevice(c->device);
+  TRY(c, ensure(c, c->stage, (size_t)c->m * 48));
+  k_get_nodes<<<nb(c->m), 256, 0, c->st>>>(c->m, c->node32.as<float>(), c->stage.as<float>());
+  TRY(c, cudaMemcpyAsync(out, c->stage.p, (size_t)c->m * 48, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_get_nodes_f64(mis_ctx* c, double* out) {
+  if (!c || !out) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  cudaSetDevice(c->device);
+  TRY(c, cudaMemcpyAsync(out, c->Rt64.p, (size_t)c->m * 96, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_get_graph(mis_ctx* c, mis_mem mem, float* node_pos) {
+  if (!c || !node_pos) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  cudaSetDevice(c->device);
+  TRY(c, cudaMemcpyAsync(node_pos, c->g.p, (size_t)c->m * 12, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_dbg_set_nodes(mis_ctx* c, mis_mem mem, const float* Rt) {
+  if (!c || !Rt) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  cudaSetDevice(c->device);
+  TRY(c, ensure(c, c->stage, (size_t)c->m * 48));
+  TRY(c, cudaMemcpyAsync(c->stage.p, Rt, (size_t)c->m * 48, kind_in(mem), c->st));
+  k_set_nodes<<<nb(c->m), 256, 0, c->st>>>(c->m, c->stage.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
+  TRY(c, cudaGetLastError());
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_dbg_frame(mis_ctx* c, mis_mem mem, float* nmap) {
+  if (!c || !nmap) return MIS_E_ARG;
+  if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame");
+  cudaSetDevice(c->device);
+  TRY(c, cudaMemcpyAsync(nmap, c->nmap.p, (size_t)c->W * c->H * 16, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_dbg_associate(mis_ctx* c, mis_mem mem, int32_t* pix, uint8_t* why) {
+  if (!c || !pix || !why) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  mis_status s;
+  if ((s = prepare(c)) != MIS_OK) return s;
+  TRY(c, ensure(c, c->pix, c->cap * 4));
+  TRY(c, ensure(c, c->why, c->cap));
+  if ((s = assemble(c, true)) != MIS_OK) return s;
+  TRY(c, cudaMemcpyAsync(pix, c->pix.p, c->n * 4, kind_out(mem), c->st));
+  TRY(c, cudaMemcpyAsync(why, c->why.p, c->n, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val, float* rhs, double energy[5],
+                          int64_t* nnzb) {
+  if (!c || !nnzb) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  mis_status s;
+  if ((s = prepare(c)) != MIS_OK) return s;
+  *nnzb = c->nnzb;
+  if (!val) return MIS_OK;
+  if ((s = assemble(c, false)) != MIS_OK) return s;
+  launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, 0,
+                       c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
+  TRY(c, launch_solve(solve_args(c, 0, false, 0), c->num_sms, c->st));
+  if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
+  if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
+  if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)c->m * 24, cudaMemcpyDeviceToHost, c->st));
+  if (energy) TRY(c, cudaMemcpyAsync(energy, c->rep_energy.p, 40, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_warp(mis_ctx* c, mis_mem mem, float* xyz_cam, float* nrm_cam) {
+  if (!c) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  cudaSetDevice(c->device);
+  if (c->dirty) TRY(c, build_order(c));
+  float* xc = nullptr;
+  float* nc = nullptr;
+  if (xyz_cam || nrm_cam) {
+    TRY(c, ensure(c, c->stage, (size_t)c->n * 24 + 16));
+    xc = c->stage.as<float>();
+    nc = xc + 3 * c->n;
+  }
+  launch_warp_model(c->K, model_view(c), node_view(c), frame_view(c), xyz_cam ? xc : nullptr,
+                    nrm_cam ? nc : nullptr, c->st);
+  launch_advance_nodes(node_view(c), c->g.as<float>(), c->st);
+  TRY(c, cudaGetLastError());
+  if (xyz_cam) TRY(c, cudaMemcpyAsync(xyz_cam, xc, (size_t)c->n * 12, kind_out(mem), c->st));
+  if (nrm_cam) TRY(c, cudaMemcpyAsync(nrm_cam, nc, (size_t)c->n * 12, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST && (xyz_cam || nrm_cam)) TRY(c, cudaStreamSynchronize(c->st));
+  c->pattern_valid = false;   // feature skinning refers to the old node positions
+  return MIS_OK;
+}
+
+static FuseArgs fuse_args(Ctx* c, const float* rgb, int32_t frame) {
+  FuseArgs a;
+  a.md = model_view(c);
+  a.fr = frame_view(c);
+  a.tz = fmin((double)c->prm.tau_z_mm, (double)c->prm.trunc_mm);
+  a.cos_delta = cos(c->prm.delta_deg * M_PI / 180.0);
+  a.omega_max = c->prm.omega_max;
+  a.rgb_obs = rgb;
+  a.frame_index = frame;
+  a.pixkey = c->pixkey.as<unsigned long long>();
+  a.pix = c->pix.as<int32_t>();
+  a.why = c->why.as<uint8_t>();
+  return a;
+}
+
+static mis_status fuse_register(Ctx* c, const float* rgb, int32_t frame) {
+  const size_t px = (size_t)c->W * c->H;
+  TRY(c, ensure(c, c->pixkey, px * 8));
+  TRY(c, ensure(c, c->pix, c->cap * 4));
+  TRY(c, ensure(c, c->why, c->cap));
+  TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
+  launch_fuse_register(fuse_args(c, rgb, frame), c->st);
+  TRY(c, cudaGetLastError());
+  return MIS_OK;
+}
+
+mis_status mis_dbg_fuse_register(mis_ctx* c, int64_t* owner, uint8_t* why) {
+  if (!c || !owner) return MIS_E_ARG;
+  if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
+  cudaSetDevice(c->device);
+  if (c->dirty) TRY(c, build_order(c));
+  mis_status s;
+  if ((s = fuse_register(c, nullptr, 0)) != MIS_OK) return s;
+  const size_t px = (size_t)c->W * c->H;
+  std::vector<unsigned long long> k(px);
+  TRY(c, cudaMemcpyAsync(k.data(), c->pixkey.p, px * 8, cudaMemcpyDeviceToHost, c->st));
+  if (why) TRY(c, cudaMemcpyAsync(why, c->why.p, c->n, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  for (size_t p = 0; p < px; ++p) owner[p] = (k[p] == ~0ull) ? -1 : (int64_t)(k[p] & 0xffffffffull);
+  return MIS_OK;
+}
+
+mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out, int64_t stats[4]) {
+  if (!c || !n_out) return MIS_E_ARG;
+  if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
+  cudaSetDevice(c->device);
+  if (c->dirty) TRY(c, build_order(c));
+  const size_t px = (size_t)c->W * c->H;
+  const float* rgb_dev = nullptr;
+  if (rgb) {
+    TRY(c, ensure(c, c->rgb_obs, px * 12));
+    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, kind_in(mem), c->st));
+    rgb_dev = c->rgb_obs.as<float>();
+  }
+  mis_status s;
+  if ((s = fuse_register(c, rgb_dev, frame_index)) != MIS_OK) return s;
+  FuseArgs a = fuse_args(c, rgb_dev, frame_index);
+  launch_fuse_apply(a, c->st);
+  const int nbk = lift_blocks(c->W, c->H);
+  TRY(c, ensure(c, c->lift_counts, (size_t)(2 * nbk + 4) * 4));
+  int32_t* counts = c->lift_counts.as<int32_t>();
+  launch_lift_count(a, counts, nbk, c->st);
+  unsigned long long* cnt = c->counter.as<unsigned long long>();
+  TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
+  k_count_winners<<<nb((int64_t)px), 256, 0, c->st>>>((int)px, c->pixkey.as<unsigned long long>(), cnt);
+  int32_t n_lift = 0;
+  unsigned long long n_reg = 0;
+  TRY(c, cudaMemcpyAsync(&n_lift, counts + 2 * nbk + 1, 4, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaMemcpyAsync(&n_reg, cnt, 8, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  if (c->n + n_lift > c->cap) {
+    *n_out = c->n;
+    return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
+  }
+  const int64_t base = c->n;
+  launch_lift_write(a, counts + nbk + 1, nbk, base, c->next_id, c->st);
+  ModelView md = model_view(c);
+  if (n_lift > 0) {
+    launch_skin(n_lift, md.px + base, md.py + base, md.pz + base, 1, c->g.as<float>(), c->m, c->K, md.kidx + base,
+                md.kw + base, c->cap, c->st);
+    c->dirty = true;
+  }
+  TRY(c, cudaGetLastError());
+  c->n += n_lift;
+  c->next_id += n_lift;
+  *n_out = c->n;
+  if (stats) {
+    stats[0] = (int64_t)n_reg;
+    stats[1] = n_lift;
+    stats[2] = (int64_t)n_reg + n_lift;
+    stats[3] = c->n;
+  }
+  c->pattern_valid = false;
+  return MIS_OK;
+}
+
+mis_status mis_get_model(mis_ctx* c, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight, int32_t* stamp,
+                         int64_t* ids, int32_t* knn_idx, float* knn_w, int64_t* n_host) {
+  if (!c) return MIS_E_ARG;
+  if (!c->have_model) return fail(c, MIS_E_STATE, "no model");
+  cudaSetDevice(c->device);
+  const int64_t n = c->n;
+  if (n_host) *n_host = n;
+  if (n == 0) return MIS_OK;
+  ModelView md = model_view(c);
+  TRY(c, ensure(c, c->stage, (size_t)n * 8 * MIS_MAX_K + 64));
+  float* st = c->stage.as<float>();
+  if (xyz) {
+    k_interleave3<<<nb(n), 256, 0, c->st>>>(n, md.px, md.py, md.pz, st);
+    TRY(c, cudaMemcpyAsync(xyz, st, n * 12, kind_out(mem), c->st));
+    if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  }
+  if (nrm) {
+    k_interleave3<<<nb(n), 256, 0, c->st>>>(n, md.nx, md.ny, md.nz, st);
+    TRY(c, cudaMemcpyAsync(nrm, st, n * 12, kind_out(mem), c->st));
+    if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  }
+  if (rgb) {
+    k_interleave3<<<nb(n), 256, 0, c->st>>>(n, md.cr, md.cg, md.cb, st);
+    TRY(c, cudaMemcpyAsync(rgb, st, n * 12, kind_out(mem), c->st));
+    if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  }
+  if (weight) TRY(c, cudaMemcpyAsync(weight, md.w, n * 4, kind_out(mem), c->st));
+  if (stamp) TRY(c, cudaMemcpyAsync(stamp, md.stamp, n * 4, kind_out(mem), c->st));
+  if (ids) TRY(c, cudaMemcpyAsync(ids, md.ids, n * 8, kind_out(mem), c->st));
+  if (knn_idx || knn_w) {
+    if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+    int32_t* si = reinterpret_cast<int32_t*>(st);
+    float* sw = reinterpret_cast<float*>(si + n * c->K);
+    k_to_point_major<<<nb(n), 256, 0, c->st>>>(n, c->K, c->cap, md.kidx, md.kw, si, sw);
+    if (knn_idx) TRY(c, cudaMemcpyAsync(knn_idx, si, n * c->K * 4, kind_out(mem), c->st));
+    if (knn_w) TRY(c, cudaMemcpyAsync(knn_w, sw, n * c->K * 4, kind_out(mem), c->st));
+  }
+  TRY(c, cudaGetLastError());
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32_t* idx, float* w) {
+  if (!c || nq < 0 || (nq > 0 && (!pts || !idx || !w))) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  if (c->m < c->K + 1) return fail(c, MIS_E_ARG, "skinning needs m >= k+1");
+  if (nq == 0) return MIS_OK;
+  cudaSetDevice(c->device);
+  const int K = c->K;
+  TRY(c, ensure(c, c->stage, (size_t)nq * (12 + 16 * K) + 64));
+  float* sp = c->stage.as<float>();
+  int32_t* si = reinterpret_cast<int32_t*>(sp + 3 * nq);
+  float* sw = reinterpret_cast<float*>(si + nq * K);
+  int32_t* pi = reinterpret_cast<int32_t*>(sw + nq * K);
+  float* pw = reinterpret_cast<float*>(pi + nq * K);
+  TRY(c, cudaMemcpyAsync(sp, pts, nq * 12, kind_in(mem), c->st));
+  launch_skin(nq, sp, sp + 1, sp + 2, 3, c->g.as<float>(), c->m, K, si, sw, nq, c->st);
+  k_to_point_major<<<nb(nq), 256, 0, c->st>>>(nq, K, nq, si, sw, pi, pw);
+  TRY(c, cudaGetLastError());
+  TRY(c, cudaMemcpyAsync(idx, pi, nq * K * 4, kind_out(mem), c->st));
+  TRY(c, cudaMemcpyAsync(w, pw, nq * K * 4, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,514 @@
+// assemble.cu -- K3 (per-point warp + association + residuals + J^T J) and
+// K4/K5 (regulariser and feature terms) of one Gauss-Newton iteration.
+//
+// K3 design: points are sorted by their canonical kNN tuple
+// (K13), so a "chunk" (<= 256 consecutive points of one tuple segment) shares
+// all K nodes.  One warp owns a chunk: each lane warps one point (Eq. 1),
+// associates it (Eq. 7, with an fp64 guard band at every decision boundary)
+// and writes one row f of per-point factors to shared memory:
+//   c' = [w_1 u_1, ..., w_K u_K, r_pl]      u_j = [a_j x n', n'] (Eq. 8 Jacobian row / w_j)
+//   e' = [w_1 a_1, w_1, ..., w_K a_K, w_K, r']   (point-to-point moments, r' = R^T (v~ - q))
+// Every per-chunk sum the normal equations need is an entry of sum_i c'c'^T or
+// sum_i e'e'^T (upper triangles), i.e. two tiny SYRKs.  Lanes own 4x4 tiles of
+// those triangles and accumulate them from shared memory in registers over the
+// chunk's points (16 FFMA per 2 LDS.128), then commit each entry once per
+// chunk with a global atomic add.  K_finalize (solve.cu) turns the moments
+// into 6x6 point-to-point blocks: sum of w_j w_l [-[a_j]x[a_l]x, [a_j]x; -[a_l]x, I].
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace mis {
+
+template <int K>
+struct Lay {
+  static constexpr int CD = 6 * K + 1;
+  static constexpr int CDP = (CD + 3) & ~3;
+  static constexpr int CE = 4 * K + 3;
+  static constexpr int CEP = (CE + 3) & ~3;
+  static constexpr int FS = CDP + CEP;
+  static constexpr int FSP = FS + 4;                 // padded smem row stride (bank spread)
+  static constexpr int ND = CDP / 4, NE = CEP / 4;   // tile grid sizes
+  static constexpr int TD = ND * (ND + 1) / 2;
+  static constexpr int TE = NE * (NE + 1) / 2;
+  static constexpr int NT = TD + TE;
+  static constexpr int R = (NT + 31) / 32;           // tiles per lane
+  static constexpr int P = K * (K + 1) / 2;
+};
+
+constexpr int kWarps = 8;
+constexpr float kGuardPx = 2e-3f;     // fp32 rounding guard (pixels)
+constexpr float kGuardRel = 1e-3f;    // distance gate guard (relative)
+constexpr float kGuardCos = 1e-4f;    // angle gate guard (cosine)
+
+__device__ __forceinline__ bool depth_ok_d(float d) { return isfinite(d) && d > 0.0f; }
+
+// fp64 re-evaluation of one point's warp and Eq. 7 gates (the oracle's
+// arithmetic order is irrelevant here; only decisions within ~1e-12 of a
+// threshold can differ).  Used for the rare points whose fp32 quantities lie
+// inside a guard band.
+template <int K>
+__device__ __noinline__ void assoc_fp64(const AsmPointsArgs& a, int64_t i, const int32_t* nodes, float* vt_out,
+                                        float* q_out, float* N_out, int* pix_out, uint8_t* why_out) {
+  const ModelView& md = a.md;
+  const FrameView& f = a.fr;
+  double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
+  double W = 0, wr[K];
+  for (int s = 0; s < K; ++s) { wr[s] = md.kw[s * md.cap + i]; W += wr[s]; }
+  *pix_out = -1;
+  *why_out = 0;
+  if (!(W > 0)) return;
+  double xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
+  for (int s = 0; s < K; ++s) {
+    const double* Rt = a.nd.Rt64 + 12 * nodes[s];
+    const float* g = a.nd.g + 3 * nodes[s];
+    const double wn = wr[s] / W;
+    double d[3] = {v[0] - g[0], v[1] - g[1], v[2] - g[2]};
+    for (int r = 0; r < 3; ++r) {
+      double ar = Rt[3 * r] * d[0] + Rt[3 * r + 1] * d[1] + Rt[3 * r + 2] * d[2];
+      xh[r] += wn * (ar + (double)g[r] + Rt[9 + r]);
+      mh[r] += wn * (Rt[3 * r] * n[0] + Rt[3 * r + 1] * n[1] + Rt[3 * r + 2] * n[2]);
+    }
+  }
+  double vt[3], nt[3];
+  for (int r = 0; r < 3; ++r) {
+    vt[r] = f.Rd[3 * r] * xh[0] + f.Rd[3 * r + 1] * xh[1] + f.Rd[3 * r + 2] * xh[2] + f.Td[r];
+    nt[r] = f.Rd[3 * r] * mh[0] + f.Rd[3 * r + 1] * mh[1] + f.Rd[3 * r + 2] * mh[2];
+  }
+  const double ml = sqrt(mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2]);
+  if (ml < 1e-12) return;
+  for (int r = 0; r < 3; ++r) { nt[r] /= ml; vt_out[r] = (float)vt[r]; }
+  uint8_t why = 0;
+  if (!(vt[2] > 0)) { *why_out = why; return; }
+  why |= 1;
+  const double u = f.fxd * vt[0] / vt[2] + f.cxd, vv = f.fyd * vt[1] / vt[2] + f.cyd;
+  const double fu = floor(u + 0.5), fv = floor(vv + 0.5);
+  if (fu < 0 || fv < 0 || fu >= f.W || fv >= f.H) { *why_out = why; return; }
+  why |= 2;
+  const int px = (int)fu, py = (int)fv, W_ = f.W;
+  const float D = f.depth[py * W_ + px];
+  if (!depth_ok_d(D)) { *why_out = why; return; }
+  why |= 4;
+  // normal in fp64 from the five depths (reading A11)
+  if (px <= 0 || py <= 0 || px >= W_ - 1 || py >= f.H - 1) { *why_out = why; return; }
+  const float l = f.depth[py * W_ + px - 1], r = f.depth[py * W_ + px + 1];
+  const float up = f.depth[(py - 1) * W_ + px], dn = f.depth[(py + 1) * W_ + px];
+  if (!depth_ok_d(l) || !depth_ok_d(r) || !depth_ok_d(up) || !depth_ok_d(dn)) { *why_out = why; return; }
+  const double ax = ((px + 1) - f.cxd) * r / f.fxd - ((px - 1) - f.cxd) * l / f.fxd;
+  const double ay = (py - f.cyd) * (double)r / f.fyd - (py - f.cyd) * (double)l / f.fyd;
+  const double az = (double)r - (double)l;
+  const double bx = (px - f.cxd) * (double)dn / f.fxd - (px - f.cxd) * (double)up / f.fxd;
+  const double by = ((py + 1) - f.cyd) * dn / f.fyd - ((py - 1) - f.cyd) * up / f.fyd;
+  const double bz = (double)dn - (double)up;
+  double N[3] = {ay * bz - az * by, az * bx - ax * bz, ax * by - ay * bx};
+  const double len = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
+  if (len < 1e-12) { *why_out = why; return; }
+  const double q[3] = {(px - f.cxd) * D / f.fxd, (py - f.cyd) * D / f.fyd, (double)D};
+  for (int c = 0; c < 3; ++c) N[c] /= len;
+  if (N[0] * q[0] + N[1] * q[1] + N[2] * q[2] > 0) for (int c = 0; c < 3; ++c) N[c] = -N[c];
+  why |= 8;
+  const double dd = sqrt((vt[0] - q[0]) * (vt[0] - q[0]) + (vt[1] - q[1]) * (vt[1] - q[1]) + (vt[2] - q[2]) * (vt[2] - q[2]));
+  for (int c = 0; c < 3; ++c) { q_out[c] = (float)q[c]; N_out[c] = (float)N[c]; }
+  if (!(dd < a.eps_dd)) { *why_out = why; return; }
+  why |= 16;
+  const double cs = nt[0] * N[0] + nt[1] * N[1] + nt[2] * N[2];
+  if (!(cs > a.cos_eps_nd)) { *why_out = why; return; }
+  why |= 32;
+  *why_out = why;
+  *pix_out = py * W_ + px;
+}
+
+// One lane, one point: warp, associate, write the factor row (zeros if not associated).
+template <int K, bool DBG>
+__device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, bool act, const float* __restrict__ ND,
+                                          const int32_t* nodes, float* __restrict__ row) {
+  using L = Lay<K>;
+  float f[L::FS];
+#pragma unroll
+  for (int c = 0; c < L::FS; ++c) f[c] = 0.f;
+  bool assoc = false;
+  int pix = -1;
+  uint8_t why = 0;
+  if (act) {
+    const ModelView& md = a.md;
+    const FrameView& fr = a.fr;
+    const float v0 = md.px[i], v1 = md.py[i], v2 = md.pz[i];
+    const float n0 = md.nx[i], n1 = md.ny[i], n2 = md.nz[i];
+    float wn[K], ax[K], ay[K], az[K];
+    float W = 0.f;
+#pragma unroll
+    for (int s = 0; s < K; ++s) { wn[s] = md.kw[s * md.cap + i]; W += wn[s]; }
+    if (W > 0.f) {
+      const float iW = 1.0f / W;
+      float x0 = 0, x1 = 0, x2 = 0, m0 = 0, m1 = 0, m2 = 0;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const float* nd = ND + 16 * s;   // R(9) t(3) g(3)
+        wn[s] *= iW;
+        const float d0 = v0 - nd[12], d1 = v1 - nd[13], d2 = v2 - nd[14];
+        ax[s] = nd[0] * d0 + nd[1] * d1 + nd[2] * d2;
+        ay[s] = nd[3] * d0 + nd[4] * d1 + nd[5] * d2;
+        az[s] = nd[6] * d0 + nd[7] * d1 + nd[8] * d2;
+        x0 += wn[s] * (ax[s] + nd[12] + nd[9]);
+        x1 += wn[s] * (ay[s] + nd[13] + nd[10]);
+        x2 += wn[s] * (az[s] + nd[14] + nd[11]);
+        m0 += wn[s] * (nd[0] * n0 + nd[1] * n1 + nd[2] * n2);
+        m1 += wn[s] * (nd[3] * n0 + nd[4] * n1 + nd[5] * n2);
+        m2 += wn[s] * (nd[6] * n0 + nd[7] * n1 + nd[8] * n2);
+      }
+      const float* R = fr.R;
+      float vt[3] = {R[0] * x0 + R[1] * x1 + R[2] * x2 + fr.T[0], R[3] * x0 + R[4] * x1 + R[5] * x2 + fr.T[1],
+                     R[6] * x0 + R[7] * x1 + R[8] * x2 + fr.T[2]};
+      const float ml = sqrtf(m0 * m0 + m1 * m1 + m2 * m2);
+      float q[3] = {0, 0, 0}, N[3] = {0, 0, 0};
+      bool guard = !(ml > 1e-6f) || fabsf(vt[2]) < 1e-3f;
+      if (!guard && vt[2] > 0.f) {
+        why = 1;
+        const float iz = 1.0f / vt[2];
+        const float uu = fr.fx * vt[0] * iz + fr.cx + 0.5f, vv = fr.fy * vt[1] * iz + fr.cy + 0.5f;
+        const float fu = floorf(uu), fv = floorf(vv);
+        if (fminf(uu - fu, fu + 1.f - uu) < kGuardPx || fminf(vv - fv, fv + 1.f - vv) < kGuardPx) {
+          guard = true;
+        } else if (fu >= 0.f && fv >= 0.f && fu < (float)fr.W && fv < (float)fr.H) {
+          why |= 2;
+          const int px = (int)fu, py = (int)fv;
+          const float4 nm = fr.nmap[py * fr.W + px];
+          if (nm.w > 0.f) {
+            why |= 4;
+            if (nm.x != 0.f || nm.y != 0.f || nm.z != 0.f) {
+              why |= 8;
+              N[0] = nm.x; N[1] = nm.y; N[2] = nm.z;
+              q[0] = (px - fr.cx) * nm.w / fr.fx;
+              q[1] = (py - fr.cy) * nm.w / fr.fy;
+              q[2] = nm.w;
+              const float e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
+              const float dd = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
+              if (fabsf(dd - a.eps_d) < kGuardRel * a.eps_d) {
+                guard = true;
+              } else if (dd < a.eps_d) {
+                why |= 16;
+                const float im = 1.0f / ml;
+                const float nt0 = (R[0] * m0 + R[1] * m1 + R[2] * m2) * im;
+                const float nt1 = (R[3] * m0 + R[4] * m1 + R[5] * m2) * im;
+                const float nt2 = (R[6] * m0 + R[7] * m1 + R[8] * m2) * im;
+                const float cs = nt0 * N[0] + nt1 * N[1] + nt2 * N[2];
+                if (fabsf(cs - a.cos_eps_n) < kGuardCos) guard = true;
+                else if (cs > a.cos_eps_n) { why |= 32; pix = py * fr.W + px; }
+              }
+            }
+          }
+        }
+      }
+      if (guard) assoc_fp64<K>(a, i, nodes, vt, q, N, &pix, &why);
+      assoc = (pix >= 0);
+      if (assoc) {
+        const float e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
+        const float rpl = N[0] * e0 + N[1] * e1 + N[2] * e2;                 // Eq. 8
+        const float np0 = R[0] * N[0] + R[3] * N[1] + R[6] * N[2];         // n' = R^T N
+        const float np1 = R[1] * N[0] + R[4] * N[1] + R[7] * N[2];
+        const float np2 = R[2] * N[0] + R[5] * N[1] + R[8] * N[2];
+        const float rp0 = R[0] * e0 + R[3] * e1 + R[6] * e2;               // r' = R^T (v~ - q)
+        const float rp1 = R[1] * e0 + R[4] * e1 + R[7] * e2;
+        const float rp2 = R[2] * e0 + R[5] * e1 + R[8] * e2;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          f[6 * s + 0] = wn[s] * (ay[s] * np2 - az[s] * np1);   // w_j (a_j x n')
+          f[6 * s + 1] = wn[s] * (az[s] * np0 - ax[s] * np2);
+          f[6 * s + 2] = wn[s] * (ax[s] * np1 - ay[s] * np0);
+          f[6 * s + 3] = wn[s] * np0;
+          f[6 * s + 4] = wn[s] * np1;
+          f[6 * s + 5] = wn[s] * np2;
+          f[L::CDP + 4 * s + 0] = wn[s] * ax[s];
+          f[L::CDP + 4 * s + 1] = wn[s] * ay[s];
+          f[L::CDP + 4 * s + 2] = wn[s] * az[s];
+          f[L::CDP + 4 * s + 3] = wn[s];
+        }
+        f[6 * K] = rpl;
+        f[L::CDP + 4 * K + 0] = rp0;
+        f[L::CDP + 4 * K + 1] = rp1;
+        f[L::CDP + 4 * K + 2] = rp2;
+      }
+    }
+    if (DBG) { a.dbg_pix[i] = pix; a.dbg_why[i] = why; }
+  }
+  float4* r4 = reinterpret_cast<float4*>(row);
+#pragma unroll
+  for (int c = 0; c < L::FS / 4; ++c) r4[c] = make_float4(f[4 * c], f[4 * c + 1], f[4 * c + 2], f[4 * c + 3]);
+  return assoc;
+}
+
+template <int K, bool DBG>
+__global__ void __launch_bounds__(kWarps * 32) k_assemble_points(AsmPointsArgs a) {
+  using L = Lay<K>;
+  extern __shared__ float4 smem4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* F = reinterpret_cast<float*>(smem4) + warp * (32 * L::FSP + 16 * K);
+  float* ND = F + 32 * L::FSP;
+
+  // static ownership of 4x4 tiles of the two upper triangles
+  int offA[L::R], offB[L::R], tI[L::R], tJ[L::R];
+  bool tE[L::R], tV[L::R];
+#pragma unroll
+  for (int r = 0; r < L::R; ++r) {
+    int t = lane + 32 * r;
+    tV[r] = t < L::NT;
+    tE[r] = t >= L::TD;
+    int nb = tE[r] ? L::NE : L::ND;
+    int u = tE[r] ? t - L::TD : t;
+    int I = 0;
+    if (tV[r]) {
+      while (u >= nb - I) { u -= nb - I; ++I; }
+    }
+    tI[r] = I;
+    tJ[r] = I + u;
+    const int base = tE[r] ? L::CDP : 0;
+    offA[r] = tV[r] ? base + 4 * tI[r] : 0;
+    offB[r] = tV[r] ? base + 4 * tJ[r] : 0;
+  }
+
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < a.nchunk; c += nw) {
+    const int4 ch = a.chunks[c];
+    const int seg = ch.x;
+    const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
+    __syncwarp();
+    for (int t = lane; t < 16 * K; t += 32) ND[t] = a.nd.node32[16 * nodes[t >> 4] + (t & 15)];
+    __syncwarp();
+    float acc[L::R][16];
+#pragma unroll
+    for (int r = 0; r < L::R; ++r)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[r][e] = 0.f;
+    unsigned n_assoc = 0;
+    for (int base = ch.y; base < ch.z; base += 32) {
+      const int64_t i = base + lane;
+      const bool as = point_row<K, DBG>(a, i, i < ch.z, ND, nodes, F + lane * L::FSP);
+      n_assoc += __popc(__ballot_sync(0xffffffffu, as));
+      __syncwarp();
+      const int np = min(32, ch.z - base);
+#pragma unroll
+      for (int r = 0; r < L::R; ++r) {
+        if (!tV[r]) continue;
+        const float* pa = F + offA[r];
+        const float* pb = F + offB[r];
+        for (int p = 0; p < np; ++p) {
+          const float4 A = *reinterpret_cast<const float4*>(pa + p * L::FSP);
+          const float4 B = *reinterpret_cast<const float4*>(pb + p * L::FSP);
+          const float Av[4] = {A.x, A.y, A.z, A.w}, Bv[4] = {B.x, B.y, B.z, B.w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[r][4 * x + y] = fmaf(Av[x], Bv[y], acc[r][4 * x + y]);
+        }
+      }
+      __syncwarp();
+    }
+    // ---- commit: one atomic per triangle entry per chunk
+    const int32_t* slots = a.seg_slot + (int64_t)seg * L::P;
+    float eD = 0.f, eP = 0.f;
+#pragma unroll
+    for (int r = 0; r < L::R; ++r) {
+      if (!tV[r]) continue;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int A = 4 * tI[r] + x, B = 4 * tJ[r] + y;
+          if (A > B) continue;
+          const float val = acc[r][4 * x + y];
+          if (!tE[r]) {
+            if (B < 6 * K) {
+              if (val != 0.f) {
+                const int slot = slots[pair_index(A / 6, B / 6, K)];
+                atomicAdd(a.acc.data + (int64_t)slot * 36 + (A % 6) * 6 + (B % 6), val);
+              }
+            } else if (B == 6 * K) {
+              if (A < 6 * K) {
+                if (val != 0.f) atomicAdd(a.acc.rhs_data + 6 * nodes[A / 6] + (A % 6), val);
+              } else {
+                eD += val;
+              }
+            }
+          } else {
+            if (B < 4 * K) {
+              if (val != 0.f) {
+                const int slot = slots[pair_index(A / 4, B / 4, K)];
+                atomicAdd(a.acc.mom + (int64_t)slot * 16 + (A % 4) * 4 + (B % 4), val);
+              }
+            } else if (B < 4 * K + 3) {
+              if (A < 4 * K) {
+                if (val != 0.f) atomicAdd(a.acc.node_mom + 12 * nodes[A / 4] + (A % 4) * 3 + (B - 4 * K), val);
+              } else if (A == B) {
+                eP += val;
+              }
+            }
+          }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      eD += __shfl_xor_sync(0xffffffffu, eD, o);
+      eP += __shfl_xor_sync(0xffffffffu, eP, o);
+    }
+    if (lane == 0) {
+      atomicAdd(a.acc.energy + 0, (double)eD);
+      atomicAdd(a.acc.energy + 1, (double)eP);
+      atomicAdd(a.acc.energy + 4, (double)n_assoc);
+    }
+  }
+}
+
+template <int K>
+static void launch_points_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+  using L = Lay<K>;
+  const size_t smem = sizeof(float) * kWarps * (32 * L::FSP + 16 * K);
+  const bool dbg = a.dbg_pix != nullptr;
+  auto kern = dbg ? k_assemble_points<K, true> : k_assemble_points<K, false>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[dbg]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set[dbg] = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t want = (a.nchunk + kWarps - 1) / kWarps;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (want < grid) grid = want;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, kWarps * 32, smem, s>>>(a);
+}
+
+void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+  if (a.nchunk <= 0) return;
+  switch (K) {
+    case 1: launch_points_k<1>(a, num_sms, s); break;
+    case 2: launch_points_k<2>(a, num_sms, s); break;
+    case 3: launch_points_k<3>(a, num_sms, s); break;
+    case 4: launch_points_k<4>(a, num_sms, s); break;
+    case 5: launch_points_k<5>(a, num_sms, s); break;
+    case 6: launch_points_k<6>(a, num_sms, s); break;
+    case 7: launch_points_k<7>(a, num_sms, s); break;
+    case 8: launch_points_k<8>(a, num_sms, s); break;
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------- K4 / K5
+__device__ __forceinline__ void add_block(float* B, const float (&M)[36], float w) {
+#pragma unroll
+  for (int e = 0; e < 36; ++e)
+    if (M[e] != 0.f) atomicAdd(B + e, w * M[e]);
+}
+
+// [ (a.b) I - b a^T , [a]x ; -[b]x , I ]  = [[a]x ; I] [-[b]x , I]
+__device__ __forceinline__ void pt_block(const float* a, const float* b, float (&M)[36]) {
+  const float ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) M[6 * r + c] = (r == c ? ab : 0.f) - b[r] * a[c];
+  const float Ax[9] = {0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0};
+  const float Bx[9] = {0, -b[2], b[1], b[2], 0, -b[0], -b[1], b[0], 0};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      M[6 * r + 3 + c] = Ax[3 * r + c];
+      M[6 * (r + 3) + c] = -Bx[3 * r + c];
+      M[6 * (r + 3) + 3 + c] = (r == c) ? 1.f : 0.f;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_assemble_graph(AsmGraphArgs a) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ne = a.nd.m * a.n_nbr;
+  float eR = 0.f, eC = 0.f;
+  if (tid < ne) {
+    // Eq. 6, alpha = 1, directed edge j -> l (reading A14)
+    const int j = tid / a.n_nbr, l = a.nbr[tid];
+    if (l >= 0) {
+      const float* Nj = a.nd.node32 + 16 * j;
+      const float* Nl = a.nd.node32 + 16 * l;
+      const float d[3] = {Nl[12] - Nj[12], Nl[13] - Nj[13], Nl[14] - Nj[14]};
+      float b[3], e[3];
+      for (int r = 0; r < 3; ++r) b[r] = Nj[3 * r] * d[0] + Nj[3 * r + 1] * d[1] + Nj[3 * r + 2] * d[2];
+      for (int r = 0; r < 3; ++r) e[r] = b[r] + Nj[12 + r] + Nj[9 + r] - Nl[12 + r] - Nl[9 + r];
+      eR = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+      float M[36];
+      pt_block(b, b, M);                        // J_j^T J_j, J_j = [-[b]x, I]
+      add_block(a.acc.graph + 36 * (int64_t)a.diag_slot[j], M, a.w_reg);
+      for (int x = 0; x < 36; ++x) M[x] = 0.f;  // J_l^T J_l = diag(0, I)
+      M[21] = M[28] = M[35] = 1.f;
+      add_block(a.acc.graph + 36 * (int64_t)a.diag_slot[l], M, a.w_reg);
+      // J_j^T J_l = [0, -[b]x ; 0, -I]  (stored transposed when l < j)
+      const float Bx[9] = {0, -b[2], b[1], b[2], 0, -b[0], -b[1], b[0], 0};
+      for (int x = 0; x < 36; ++x) M[x] = 0.f;
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+          if (j < l) { M[6 * r + 3 + c] = -Bx[3 * r + c]; }
+          else { M[6 * (r + 3) + c] = -Bx[3 * c + r]; }
+          M[6 * (r + 3) + 3 + c] = (r == c) ? -1.f : 0.f;
+        }
+      add_block(a.acc.graph + 36 * (int64_t)a.edge_slot[tid], M, a.w_reg);
+      // rhs: -J^T e
+      const float bxe[3] = {b[1] * e[2] - b[2] * e[1], b[2] * e[0] - b[0] * e[2], b[0] * e[1] - b[1] * e[0]};
+      for (int r = 0; r < 3; ++r) {
+        atomicAdd(a.acc.rhs_graph + 6 * j + r, -a.w_reg * bxe[r]);
+        atomicAdd(a.acc.rhs_graph + 6 * j + 3 + r, -a.w_reg * e[r]);
+        atomicAdd(a.acc.rhs_graph + 6 * l + 3 + r, a.w_reg * e[r]);
+      }
+    }
+  } else if (tid < ne + a.nf) {
+    // Eq. 9, squared (reading A12)
+    const int fi = tid - ne, K = a.K;
+    const float V[3] = {a.fsrc[3 * fi], a.fsrc[3 * fi + 1], a.fsrc[3 * fi + 2]};
+    float W = 0.f;
+    for (int s = 0; s < K; ++s) W += a.fw[(int64_t)s * a.nf + fi];
+    if (W > 0.f) {
+      float am[MIS_MAX_K][3], wn[MIS_MAX_K], xh[3] = {0, 0, 0};
+      for (int s = 0; s < K; ++s) {
+        const float* Nd = a.nd.node32 + 16 * a.fidx[(int64_t)s * a.nf + fi];
+        wn[s] = a.fw[(int64_t)s * a.nf + fi] / W;
+        const float d[3] = {V[0] - Nd[12], V[1] - Nd[13], V[2] - Nd[14]};
+        for (int r = 0; r < 3; ++r) {
+          am[s][r] = Nd[3 * r] * d[0] + Nd[3 * r + 1] * d[1] + Nd[3 * r + 2] * d[2];
+          xh[r] += wn[s] * (am[s][r] + Nd[12 + r] + Nd[9 + r]);
+        }
+      }
+      const float* R = a.fr.R;
+      float e[3], rp[3];
+      for (int r = 0; r < 3; ++r) e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.T[r] - a.fdst[3 * fi + r];
+      for (int r = 0; r < 3; ++r) rp[r] = R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2];
+      eC = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+      const int32_t* slots = a.feat_slot + (int64_t)fi * (K * (K + 1) / 2);
+      float M[36];
+      for (int s = 0; s < K; ++s) {
+        for (int s2 = s; s2 < K; ++s2) {
+          pt_block(am[s], am[s2], M);
+          add_block(a.acc.graph + 36 * (int64_t)slots[pair_index(s, s2, K)], M, a.w_corr * wn[s] * wn[s2]);
+        }
+        const int node = a.fidx[(int64_t)s * a.nf + fi];
+        const float axr[3] = {am[s][1] * rp[2] - am[s][2] * rp[1], am[s][2] * rp[0] - am[s][0] * rp[2],
+                              am[s][0] * rp[1] - am[s][1] * rp[0]};
+        for (int r = 0; r < 3; ++r) {
+          atomicAdd(a.acc.rhs_graph + 6 * node + r, -a.w_corr * wn[s] * axr[r]);
+          atomicAdd(a.acc.rhs_graph + 6 * node + 3 + r, -a.w_corr * wn[s] * rp[r]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    eR += __shfl_xor_sync(0xffffffffu, eR, o);
+    eC += __shfl_xor_sync(0xffffffffu, eC, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (eR != 0.f) atomicAdd(a.acc.energy + 2, (double)eR);
+    if (eC != 0.f) atomicAdd(a.acc.energy + 3, (double)eC);
+  }
+}
+
+void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s) {
+  const int n = a.nd.m * a.n_nbr + a.nf;
+  if (n <= 0) return;
+  k_assemble_graph<<<(n + 127) / 128, 128, 0, s>>>(a);
+}
+
+}  // namespace mis

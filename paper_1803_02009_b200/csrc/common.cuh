@@ -1,0 +1,150 @@
+// common.cuh -- internal declarations of libmis (B200 / sm_100a).
+// Device-side structs, small vector helpers and the kernel launchers shared
+// between the .cu files of the library.  Nothing here is visible through the
+// C-ABI (include/mis.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mis.h"
+
+namespace mis {
+
+// ------------------------------------------------------------- device views
+struct FrameView {
+  int W, H;
+  float fx, fy, cx, cy;
+  double fxd, fyd, cxd, cyd;
+  const float* depth;    // H*W
+  const float4* nmap;    // H*W: (nx, ny, nz, D); n = 0 invalid normal, D = 0 invalid depth
+  float R[9], T[3];      // world -> camera (fp32 copy)
+  double Rd[9], Td[3];   // fp64 copy (guard-band recompute)
+};
+
+struct ModelView {
+  int64_t n, cap;
+  float *px, *py, *pz, *nx, *ny, *nz;   // SoA, internal (tuple-sorted) order
+  float *cr, *cg, *cb, *w;              // colour, fusion weight omega
+  int32_t* stamp;
+  int64_t* ids;
+  int32_t* kidx;                        // slot-major [s*cap + i], ids ascending per point
+  float* kw;                            // slot-major raw skinning weights
+};
+
+struct NodeView {
+  int m;
+  const float* g;        // m*3 node positions
+  float* node32;         // m*16: R (9) t (3) g (3) pad -- what the kernels read
+  double* Rt64;          // m*12 fp64 master state (R row-major, t)
+};
+
+// pair index of slot positions (j <= l) within a k-tuple
+__host__ __device__ inline int pair_index(int j, int l, int K) { return j * K - (j * (j - 1)) / 2 + (l - j); }
+__host__ __device__ inline int n_pairs(int K) { return K * (K + 1) / 2; }
+
+// ------------------------------------------------------------- accumulator layout
+// acc region (float), zeroed every GN iteration, all-reduced across ranks:
+//   data[nnzu*36] | mom[nnzu*16] | graph[nnzu*36] | rhs_data[m*6] | node_mom[m*12] | rhs_graph[m*6]
+// energy region (double): E_data, E_pt, E_reg, E_corr ; n_assoc (u64 as double slot 4)
+struct AccView {
+  float* data;
+  float* mom;
+  float* graph;
+  float* rhs_data;
+  float* node_mom;
+  float* rhs_graph;
+  double* energy;              // [0..3] energies, [4] n_assoc (as double)
+};
+
+// ------------------------------------------------------------- host-side launchers
+struct Ctx;   // defined in api.cu
+
+void launch_frame_prep(const FrameView& f, float4* nmap, cudaStream_t s);
+void launch_skin(int64_t nq, const float* px, const float* py, const float* pz, int64_t stride_xyz,
+                 const float* g, int m, int K, int32_t* idx, float* w, int64_t out_stride, cudaStream_t s);
+
+struct AsmPointsArgs {
+  ModelView md;
+  const int32_t* seg_nodes;   // nseg*K
+  const int4* chunks;         // (seg, start, end, -)
+  int64_t nchunk;
+  const int32_t* seg_slot;    // nseg*P
+  NodeView nd;
+  FrameView fr;
+  float eps_d, cos_eps_n;
+  double eps_dd, cos_eps_nd;
+  AccView acc;
+  int32_t* dbg_pix;           // nullable: per point association outputs
+  uint8_t* dbg_why;
+};
+void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
+
+struct AsmGraphArgs {
+  NodeView nd;
+  int n_nbr;
+  const int32_t* nbr;         // m*n_nbr
+  const int32_t* edge_slot;   // m*n_nbr (slot of (min, max)), -1 if none
+  const int32_t* diag_slot;   // m
+  int nf;
+  const float* fsrc; const float* fdst;
+  const int32_t* fidx; const float* fw;   // K*nf (slot-major: [s*nf + f]), ids ascending
+  const int32_t* feat_slot;   // nf*P
+  FrameView fr;
+  float w_reg, w_corr;
+  AccView acc;
+  int K;
+};
+void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s);
+
+struct SolveArgs {
+  int m, K;
+  int64_t nnzb;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const int32_t* upper_of;    // nnzb: index of the (min, max) entry
+  const int32_t* diag_pos;    // m
+  AccView acc;
+  float w_data, w_pt, lambda;
+  int pcg_iters;
+  float* Hval;                // nnzb*36
+  float* rhs;                 // 6m
+  float* Minv;                // m*36
+  float *x, *r, *z, *p, *Ap;  // 6m
+  double* dots;               // 2*pcg_iters + 4
+  NodeView nd;
+  int do_update;              // 0: only build the system (debug)
+  int gn_it;                  // report slot
+  double* rep_energy;         // (MIS_MAX_GN+1)*5
+  double* rep_nassoc;         // MIS_MAX_GN+1
+  float* rep_res;             // MIS_MAX_GN
+  int* numeric_flag;
+};
+cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
+void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr,
+                          int slot, double* rep_energy, double* rep_nassoc, cudaStream_t s);
+
+// ---- fusion (fuse.cu)
+void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const FrameView& fr, float* xyz_cam,
+                       float* nrm_cam, cudaStream_t s);
+void launch_advance_nodes(const NodeView& nd, float* g_mut, cudaStream_t s);
+struct FuseArgs {
+  ModelView md;
+  FrameView fr;
+  double tz, cos_delta, omega_max;
+  const float* rgb_obs;       // H*W*3 or null
+  int32_t frame_index;
+  unsigned long long* pixkey; // H*W
+  int32_t* pix;               // n
+  uint8_t* why;               // n (nullable)
+};
+void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
+void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);
+// lift: count pass (per-block counts) then write pass; returns via device counters
+void launch_lift_count(const FuseArgs& a, int32_t* block_counts, int nblocks, cudaStream_t s);
+void launch_lift_write(const FuseArgs& a, const int32_t* block_offsets, int nblocks, int64_t base,
+                       int64_t next_id, cudaStream_t s);
+int lift_blocks(int W, int H);
+
+// ---- model order / pattern (sort.cu)
+struct SortWork;   // temp storage owner (in api.cu)
+}  // namespace mis

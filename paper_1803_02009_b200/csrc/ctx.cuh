@@ -1,0 +1,100 @@
+// ctx.cuh -- the library context (host side) shared by api.cu and sort.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct mis_ctx;   // opaque in mis.h; defined as mis::Ctx below
+
+namespace mis {
+
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct ModelBufs {
+  DBuf px, py, pz, nx, ny, nz, cr, cg, cb, w, stamp, ids, kidx, kw;
+};
+
+struct NcclApi;   // dlopen'ed NCCL entry points (api.cu)
+
+struct Ctx {
+  mis_params prm{};
+  int device = 0, num_sms = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  void* nccl_comm = nullptr;
+  std::string err;
+
+  // ---- model (internal, tuple-sorted order); two buffer sets for the sort gather
+  int64_t n = 0, cap = 0, next_id = 0;
+  int K = 4;
+  ModelBufs mb[2];
+  int cur = 0;
+  bool have_model = false, have_graph = false, dirty = false;
+
+  // ---- graph
+  int m = 0;
+  DBuf g, nbr, node32, Rt64;
+
+  // ---- order: segments and chunks (K13)
+  int64_t nseg = 0, nchunk = 0;
+  DBuf keys, keys2, vals, vals2, flags, scan, seg_start, seg_nodes, chunks, chunk_off;
+
+  // ---- pattern
+  int64_t nnzb = 0, ncand = 0;
+  bool pattern_valid = false;
+  DBuf ckeys, ckeys2, uflag, upos, ukeys, row_ptr, col, diag_pos, upper_of, seg_slot, edge_slot, feat_slot, nnz_dev;
+
+  // ---- system and solver
+  size_t acc_floats = 0;
+  DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots, numeric_flag;
+
+  // ---- frame
+  bool have_frame = false;
+  int W = 0, H = 0;
+  mis_intrinsics intr{};
+  float pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+  DBuf depth, nmap, rgb_obs, stage;
+
+  // ---- features
+  int nf = 0;
+  DBuf fsrc, fdst, fidx, fw;
+
+  // ---- fuse
+  DBuf pixkey, pix, why, lift_counts, counter;
+
+  // ---- report
+  DBuf rep_energy, rep_nassoc, rep_res;
+
+  DBuf cub_tmp;
+  // host staging for small uploads
+  DBuf pinned_small;
+};
+
+// buffer management (api.cu)
+cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes);
+void free_buf(DBuf& b);
+
+// views
+ModelView model_view(Ctx* c);
+NodeView node_view(Ctx* c);
+FrameView frame_view(Ctx* c);
+AccView acc_view(Ctx* c);
+
+// sort.cu
+cudaError_t build_order(Ctx* c);      // K13: tuple sort, gather, segments, chunks
+cudaError_t build_pattern(Ctx* c);    // BSR pattern + slot tables (incl. features)
+cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
+cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
+cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count);
+cudaError_t nccl_allgather_u64(Ctx* c, const uint64_t* send, uint64_t* recv, size_t count);
+
+constexpr int kChunk = 256;   // max points per K3 chunk
+}  // namespace mis

@@ -1,0 +1,132 @@
+// frame.cu -- K1 frame prep and K2 Eq. 2 skinning.
+#include "common.cuh"
+
+namespace mis {
+
+__device__ __forceinline__ bool depth_ok(float d) { return isfinite(d) && d > 0.0f; }
+
+// K1: per pixel (nx, ny, nz, D).  Back-projection Pi and the
+// central-difference normal (reading A11):
+//   N = normalize((q(x+1,y) - q(x-1,y)) x (q(x,y+1) - q(x,y-1))), flipped so N.q < 0;
+// invalid on the border or next to an invalid depth.  HBM-bound: 4 B read
+// (+ neighbours from L1/L2), 16 B written per pixel.
+__global__ void __launch_bounds__(256) k_frame_prep(FrameView f, float4* __restrict__ nmap) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= f.W || y >= f.H) return;
+  const int W = f.W;
+  const float* D = f.depth;
+  const float c = __ldg(D + y * W + x);
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (depth_ok(c)) {
+    out.w = c;
+    if (x > 0 && y > 0 && x < W - 1 && y < f.H - 1) {
+      const float l = __ldg(D + y * W + x - 1), r = __ldg(D + y * W + x + 1);
+      const float u = __ldg(D + (y - 1) * W + x), d = __ldg(D + (y + 1) * W + x);
+      if (depth_ok(l) && depth_ok(r) && depth_ok(u) && depth_ok(d)) {
+        const float ifx = 1.0f / f.fx, ify = 1.0f / f.fy;
+        // q(x+1,y) - q(x-1,y), q(x,y+1) - q(x,y-1)
+        const float ax = ((x + 1) - f.cx) * r * ifx - ((x - 1) - f.cx) * l * ifx;
+        const float ay = (y - f.cy) * (r - l) * ify;
+        const float az = r - l;
+        const float bx = (x - f.cx) * (d - u) * ifx;
+        const float by = ((y + 1) - f.cy) * d * ify - ((y - 1) - f.cy) * u * ify;
+        const float bz = d - u;
+        float nx = ay * bz - az * by, ny = az * bx - ax * bz, nz = ax * by - ay * bx;
+        const float len = sqrtf(nx * nx + ny * ny + nz * nz);
+        if (len > 1e-12f) {
+          const float s = 1.0f / len;
+          nx *= s; ny *= s; nz *= s;
+          const float qx = (x - f.cx) * c * ifx, qy = (y - f.cy) * c * ify;
+          if (nx * qx + ny * qy + nz * c > 0.f) { nx = -nx; ny = -ny; nz = -nz; }
+          out.x = nx; out.y = ny; out.z = nz;
+        }
+      }
+    }
+  }
+  nmap[y * W + x] = out;
+}
+
+void launch_frame_prep(const FrameView& f, float4* nmap, cudaStream_t s) {
+  dim3 blk(32, 8), grd((f.W + 31) / 32, (f.H + 7) / 8);
+  k_frame_prep<<<grd, blk, 0, s>>>(f, nmap);
+}
+
+// K2: Eq. 2 -- the k+1 nearest nodes of each query (ties to the
+// lower id), w_j = 1 - |v - g_j| / d_max with d_max the distance to the
+// (k+1)-th, normalised (d_max = 0 -> 1/k).  Output ids
+// ascending (the canonical tuple order used by the K13 sort).  Brute force
+// over all nodes staged through shared memory.
+template <int K>
+__global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restrict__ px, const float* __restrict__ py,
+                                              const float* __restrict__ pz, int64_t sxyz, const float* __restrict__ g,
+                                              int m, int32_t* __restrict__ idx, float* __restrict__ w, int64_t os) {
+  __shared__ float4 sg[1024];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = i < nq;
+  float vx = 0, vy = 0, vz = 0;
+  if (act) { vx = px[i * sxyz]; vy = py[i * sxyz]; vz = pz[i * sxyz]; }
+  float bd[K + 1];
+  int bi[K + 1];
+#pragma unroll
+  for (int s = 0; s <= K; ++s) { bd[s] = INFINITY; bi[s] = 0x7fffffff; }
+  for (int base = 0; base < m; base += 1024) {
+    const int cnt = min(1024, m - base);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x)
+      sg[t] = make_float4(g[3 * (base + t)], g[3 * (base + t) + 1], g[3 * (base + t) + 2], 0.f);
+    __syncthreads();
+    if (act) {
+      for (int t = 0; t < cnt; ++t) {
+        const float4 q = sg[t];
+        const float dx = vx - q.x, dy = vy - q.y, dz = vz - q.z;
+        const float d2 = dx * dx + dy * dy + dz * dz;
+        const int id = base + t;
+        if (d2 < bd[K]) {   // ids arrive ascending: equal distance keeps the lower id
+          float cd = d2;
+          int ci = id;
+#pragma unroll
+          for (int s = 0; s <= K; ++s) {
+            if (cd < bd[s]) { float td = bd[s]; int ti = bi[s]; bd[s] = cd; bi[s] = ci; cd = td; ci = ti; }
+          }
+        }
+      }
+    }
+  }
+  if (!act) return;
+  const float dmax = sqrtf(bd[K]);
+  float ww[K];
+  float sum = 0.f;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    ww[s] = dmax > 0.f ? 1.0f - sqrtf(bd[s]) / dmax : 1.0f / K;
+    sum += ww[s];
+  }
+#pragma unroll
+  for (int s = 0; s < K; ++s) ww[s] = sum > 0.f ? ww[s] / sum : 1.0f / K;
+  // canonical order: ids ascending (insertion sort of K pairs)
+#pragma unroll
+  for (int a = 1; a < K; ++a)
+#pragma unroll
+    for (int b = a; b > 0; --b)
+      if (bi[b] < bi[b - 1]) {
+        int ti = bi[b]; bi[b] = bi[b - 1]; bi[b - 1] = ti;
+        float tw = ww[b]; ww[b] = ww[b - 1]; ww[b - 1] = tw;
+      }
+#pragma unroll
+  for (int s = 0; s < K; ++s) { idx[s * os + i] = bi[s]; w[s * os + i] = ww[s]; }
+}
+
+void launch_skin(int64_t nq, const float* px, const float* py, const float* pz, int64_t sxyz, const float* g, int m,
+                 int K, int32_t* idx, float* w, int64_t os, cudaStream_t s) {
+  if (nq <= 0) return;
+  const int blocks = (int)((nq + 255) / 256);
+  switch (K) {
+#define SK(KK) case KK: k_skin<KK><<<blocks, 256, 0, s>>>(nq, px, py, pz, sxyz, g, m, idx, w, os); break;
+    SK(1) SK(2) SK(3) SK(4) SK(5) SK(6) SK(7) SK(8)
+#undef SK
+    default: break;
+  }
+}
+
+}  // namespace mis

@@ -1,0 +1,282 @@
+// fuse.cu -- K9 final warp (Alg. 2 Step 2), K10/K11 point-to-depth registration
+// and weighted-average fusion (Alg. 1, Eq. 12-15), K12 Group-2 lift (Alg. 2 Step 3).
+// All per-point / per-pixel, HBM-bound; decisions in fp64 (cheap here) so the
+// exclusive per-pixel winner matches the oracle outside 1e-8 mm key ties.
+#include "common.cuh"
+
+namespace mis {
+
+__device__ __forceinline__ bool dok(float d) { return isfinite(d) && d > 0.0f; }
+
+// K9: x_hat = sum_j w_j (R_j (v - g_j) + g_j + t_j), n = normalize(sum_j w_j R_j n) (Eq. 1, A_j = R_j)
+template <int K>
+__global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, FrameView fr, float* xyz_cam,
+                                                   float* nrm_cam) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= md.n) return;
+  float v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
+  float w[K], W = 0.f;
+#pragma unroll
+  for (int s = 0; s < K; ++s) { w[s] = md.kw[s * md.cap + i]; W += w[s]; }
+  if (W > 0.f) {
+    float xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const float* N = nd.node32 + 16 * md.kidx[s * md.cap + i];
+      const float wn = w[s] / W;
+      const float d[3] = {v[0] - N[12], v[1] - N[13], v[2] - N[14]};
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        xh[r] += wn * (N[3 * r] * d[0] + N[3 * r + 1] * d[1] + N[3 * r + 2] * d[2] + N[12 + r] + N[9 + r]);
+        mh[r] += wn * (N[3 * r] * n[0] + N[3 * r + 1] * n[1] + N[3 * r + 2] * n[2]);
+      }
+    }
+    const float ml = sqrtf(mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2]);
+    if (ml >= 1e-12f) {
+      for (int r = 0; r < 3; ++r) { v[r] = xh[r]; n[r] = mh[r] / ml; }
+      md.px[i] = v[0]; md.py[i] = v[1]; md.pz[i] = v[2];
+      md.nx[i] = n[0]; md.ny[i] = n[1]; md.nz[i] = n[2];
+    }
+  }
+  if (xyz_cam) {
+    for (int r = 0; r < 3; ++r)
+      xyz_cam[3 * i + r] = fr.R[3 * r] * v[0] + fr.R[3 * r + 1] * v[1] + fr.R[3 * r + 2] * v[2] + fr.T[r];
+  }
+  if (nrm_cam) {
+    for (int r = 0; r < 3; ++r) nrm_cam[3 * i + r] = fr.R[3 * r] * n[0] + fr.R[3 * r + 1] * n[1] + fr.R[3 * r + 2] * n[2];
+  }
+}
+
+void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const FrameView& fr, float* xyz_cam,
+                       float* nrm_cam, cudaStream_t s) {
+  if (md.n <= 0) return;
+  const int b = (int)((md.n + 255) / 256);
+  switch (K) {
+#define WK(KK) case KK: k_warp_model<KK><<<b, 256, 0, s>>>(md, nd, fr, xyz_cam, nrm_cam); break;
+    WK(1) WK(2) WK(3) WK(4) WK(5) WK(6) WK(7) WK(8)
+#undef WK
+    default: break;
+  }
+}
+
+// Reading A26: g_j += t_j, then R_j = I, t_j = 0.
+__global__ void k_advance_nodes(NodeView nd, float* g) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nd.m) return;
+  double* Rt = nd.Rt64 + 12 * j;
+  float* n32 = nd.node32 + 16 * j;
+  for (int c = 0; c < 3; ++c) {
+    const float gn = (float)((double)g[3 * j + c] + Rt[9 + c]);
+    g[3 * j + c] = gn;
+    n32[12 + c] = gn;
+  }
+  for (int i = 0; i < 12; ++i) Rt[i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
+  for (int i = 0; i < 12; ++i) n32[i] = (float)Rt[i];
+}
+
+void launch_advance_nodes(const NodeView& nd, float* g, cudaStream_t s) {
+  if (nd.m <= 0) return;
+  k_advance_nodes<<<(nd.m + 255) / 256, 256, 0, s>>>(nd, g);
+}
+
+// fp64 normal at a pixel from the five depths (reading A11); false if invalid
+__device__ bool normal64(const FrameView& f, int px, int py, double* N, double* q) {
+  const int W = f.W;
+  const float D = f.depth[py * W + px];
+  if (!dok(D)) return false;
+  q[0] = (px - f.cxd) * D / f.fxd; q[1] = (py - f.cyd) * D / f.fyd; q[2] = D;
+  if (px <= 0 || py <= 0 || px >= W - 1 || py >= f.H - 1) return false;
+  const float l = f.depth[py * W + px - 1], r = f.depth[py * W + px + 1];
+  const float u = f.depth[(py - 1) * W + px], d = f.depth[(py + 1) * W + px];
+  if (!dok(l) || !dok(r) || !dok(u) || !dok(d)) return false;
+  const double ax = ((px + 1) - f.cxd) * r / f.fxd - ((px - 1) - f.cxd) * l / f.fxd;
+  const double ay = (py - f.cyd) * (double)r / f.fyd - (py - f.cyd) * (double)l / f.fyd;
+  const double az = (double)r - (double)l;
+  const double bx = (px - f.cxd) * (double)d / f.fxd - (px - f.cxd) * (double)u / f.fxd;
+  const double by = ((py + 1) - f.cyd) * d / f.fyd - ((py - 1) - f.cyd) * u / f.fyd;
+  const double bz = (double)d - (double)u;
+  N[0] = ay * bz - az * by; N[1] = az * bx - ax * bz; N[2] = ax * by - ay * bx;
+  const double len = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
+  if (len < 1e-12) return false;
+  for (int c = 0; c < 3; ++c) N[c] /= len;
+  if (N[0] * q[0] + N[1] * q[1] + N[2] * q[2] > 0) for (int c = 0; c < 3; ++c) N[c] = -N[c];
+  return true;
+}
+
+// K10: Alg. 1 gates + exclusive registration by 64-bit atomicMin
+// of ((|dz| in 1e-8 mm units) << 32 | point index) per pixel (reading A19).
+__global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.md.n) return;
+  const FrameView& f = a.fr;
+  const double v[3] = {a.md.px[i], a.md.py[i], a.md.pz[i]}, n[3] = {a.md.nx[i], a.md.ny[i], a.md.nz[i]};
+  double vt[3], nt[3];
+  for (int r = 0; r < 3; ++r) {
+    vt[r] = f.Rd[3 * r] * v[0] + f.Rd[3 * r + 1] * v[1] + f.Rd[3 * r + 2] * v[2] + f.Td[r];
+    nt[r] = f.Rd[3 * r] * n[0] + f.Rd[3 * r + 1] * n[1] + f.Rd[3 * r + 2] * n[2];
+  }
+  uint8_t why = 0;
+  int32_t pix = -1;
+  if (vt[2] > 0) {
+    why |= 1;
+    const double fu = floor(f.fxd * vt[0] / vt[2] + f.cxd + 0.5), fv = floor(f.fyd * vt[1] / vt[2] + f.cyd + 0.5);
+    if (fu >= 0 && fv >= 0 && fu < f.W && fv < f.H) {
+      why |= 2;
+      const int px = (int)fu, py = (int)fv;
+      const float D = f.depth[py * f.W + px];
+      double N[3], q[3];
+      if (dok(D)) {
+        why |= 4;
+        if (normal64(f, px, py, N, q)) {
+          why |= 8;
+          const double dz = fabs(vt[2] - (double)D);
+          if (dz < a.tz) {
+            why |= 16;
+            if (nt[0] * N[0] + nt[1] * N[1] + nt[2] * N[2] > a.cos_delta) {
+              why |= 32;
+              pix = py * f.W + px;
+              const unsigned long long key =
+                  ((unsigned long long)(dz * 1e8) << 32) | (unsigned long long)(uint32_t)i;
+              atomicMin(a.pixkey + pix, key);
+            }
+          }
+        }
+      }
+    }
+  }
+  a.pix[i] = pix;
+  if (a.why) a.why[i] = why;
+}
+
+void launch_fuse_register(const FuseArgs& a, cudaStream_t s) {
+  if (a.md.n <= 0) return;
+  k_fuse_register<<<(int)((a.md.n + 255) / 256), 256, 0, s>>>(a);
+}
+
+// K11: Eq. 12-15 on each pixel's winner; 3-D weighted average (reading A21)
+__global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.md.n) return;
+  const int32_t pix = a.pix[i];
+  if (pix < 0) return;
+  if ((uint32_t)(a.pixkey[pix] & 0xffffffffull) != (uint32_t)i) return;
+  const FrameView& f = a.fr;
+  const int px = pix % f.W, py = pix / f.W;
+  double N[3], q[3];
+  normal64(f, px, py, N, q);
+  const double v[3] = {a.md.px[i], a.md.py[i], a.md.pz[i]}, n[3] = {a.md.nx[i], a.md.ny[i], a.md.nz[i]};
+  const double om = a.md.w[i];
+  double pf[3], nf[3];
+  for (int r = 0; r < 3; ++r) {
+    const double vt = f.Rd[3 * r] * v[0] + f.Rd[3 * r + 1] * v[1] + f.Rd[3 * r + 2] * v[2] + f.Td[r];
+    const double nt = f.Rd[3 * r] * n[0] + f.Rd[3 * r + 1] * n[1] + f.Rd[3 * r + 2] * n[2];
+    pf[r] = (om * vt + q[r]) / (om + 1.0);      // Eq. 12 (its z) lifted to 3-D
+    nf[r] = (om * nt + N[r]) / (om + 1.0);      // Eq. 14
+  }
+  const double nl = sqrt(nf[0] * nf[0] + nf[1] * nf[1] + nf[2] * nf[2]);
+  for (int r = 0; r < 3; ++r) { nf[r] /= nl; pf[r] -= f.Td[r]; }
+  float vo[3], no[3];
+  for (int c = 0; c < 3; ++c) {   // back to world: R^T (p - T), R^T n
+    vo[c] = (float)(f.Rd[c] * pf[0] + f.Rd[3 + c] * pf[1] + f.Rd[6 + c] * pf[2]);
+    no[c] = (float)(f.Rd[c] * nf[0] + f.Rd[3 + c] * nf[1] + f.Rd[6 + c] * nf[2]);
+  }
+  a.md.px[i] = vo[0]; a.md.py[i] = vo[1]; a.md.pz[i] = vo[2];
+  a.md.nx[i] = no[0]; a.md.ny[i] = no[1]; a.md.nz[i] = no[2];
+  if (a.rgb_obs) {   // Eq. 13
+    const float* c = a.rgb_obs + 3 * (int64_t)pix;
+    a.md.cr[i] = (float)((om * a.md.cr[i] + c[0]) / (om + 1.0));
+    a.md.cg[i] = (float)((om * a.md.cg[i] + c[1]) / (om + 1.0));
+    a.md.cb[i] = (float)((om * a.md.cb[i] + c[2]) / (om + 1.0));
+  }
+  a.md.w[i] = (float)fmin(om + 1.0, a.omega_max);   // Eq. 15
+  a.md.stamp[i] = a.frame_index;
+}
+
+void launch_fuse_apply(const FuseArgs& a, cudaStream_t s) {
+  if (a.md.n <= 0) return;
+  k_fuse_apply<<<(int)((a.md.n + 255) / 256), 256, 0, s>>>(a);
+}
+
+// K12: valid (depth and normal), unregistered pixels -> new points, row-major.
+constexpr int kLiftBlock = 256;
+int lift_blocks(int W, int H) { return (W * H + kLiftBlock - 1) / kLiftBlock; }
+
+__device__ __forceinline__ bool lift_pixel(const FuseArgs& a, int p) {
+  const FrameView& f = a.fr;
+  if (p >= f.W * f.H) return false;
+  const float4 nm = f.nmap[p];
+  return nm.w > 0.f && (nm.x != 0.f || nm.y != 0.f || nm.z != 0.f) && a.pixkey[p] == ~0ull;
+}
+
+__global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts) {
+  const int p = blockIdx.x * kLiftBlock + threadIdx.x;
+  const int c = __syncthreads_count(lift_pixel(a, p));
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+
+// exclusive scan of the per-block counts (single block; counts[nb] = total)
+__global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb) {
+  __shared__ int32_t part[1024];
+  const int per = (nb + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  int32_t s = 0;
+  for (int b = b0; b < min(nb, b0 + per); ++b) s += counts[b];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int t = 0; t < 1024; ++t) { int32_t v = part[t]; part[t] = run; run += v; }
+    offs[nb] = run;
+  }
+  __syncthreads();
+  int32_t run = part[threadIdx.x];
+  for (int b = b0; b < min(nb, b0 + per); ++b) { offs[b] = run; run += counts[b]; }
+}
+
+__global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int32_t* offs, int64_t base,
+                                                           int64_t next_id) {
+  __shared__ int wsum[kLiftBlock / 32];
+  const int p = blockIdx.x * kLiftBlock + threadIdx.x;
+  const bool on = lift_pixel(a, p);
+  const unsigned bal = __ballot_sync(0xffffffffu, on);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) wsum[w] = __popc(bal);
+  __syncthreads();
+  int before = 0;
+  for (int i = 0; i < w; ++i) before += wsum[i];
+  if (!on) return;
+  const int64_t o = base + offs[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
+  const FrameView& f = a.fr;
+  const int px = p % f.W, py = p / f.W;
+  double N[3], q[3];
+  normal64(f, px, py, N, q);
+  for (int c = 0; c < 3; ++c) q[c] -= f.Td[c];
+  float vo[3], no[3];
+  for (int c = 0; c < 3; ++c) {
+    vo[c] = (float)(f.Rd[c] * q[0] + f.Rd[3 + c] * q[1] + f.Rd[6 + c] * q[2]);
+    no[c] = (float)(f.Rd[c] * N[0] + f.Rd[3 + c] * N[1] + f.Rd[6 + c] * N[2]);
+  }
+  ModelView md = a.md;
+  md.px[o] = vo[0]; md.py[o] = vo[1]; md.pz[o] = vo[2];
+  md.nx[o] = no[0]; md.ny[o] = no[1]; md.nz[o] = no[2];
+  if (a.rgb_obs) {
+    md.cr[o] = a.rgb_obs[3 * (int64_t)p]; md.cg[o] = a.rgb_obs[3 * (int64_t)p + 1]; md.cb[o] = a.rgb_obs[3 * (int64_t)p + 2];
+  } else {
+    md.cr[o] = md.cg[o] = md.cb[o] = 0.f;
+  }
+  md.w[o] = 1.0f;
+  md.stamp[o] = a.frame_index;
+  md.ids[o] = next_id + (o - base);
+}
+
+void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, cudaStream_t s) {
+  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts);
+  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks);
+}
+
+void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, int64_t next_id,
+                       cudaStream_t s) {
+  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, next_id);
+}
+
+}  // namespace mis
