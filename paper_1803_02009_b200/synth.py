@@ -66,6 +66,8 @@ RESP_HZ = 0.25       # respiration frequency (Hz)
 FPS = 30.0           # PAPER.md:523 (30 fps porcine data)
 BUMP_SIGMA = 8.0     # mm
 DEPTH_SIGMA = 0.1    # mm
+NOISE_CORR_MM = 1.0  # correlation length of the depth noise on the tissue (mm)
+WHITE_SIGMA = 0.005  # mm, uncorrelated part
 FEAT_SIGMA = 0.2     # mm
 HOLE_FRAC = 0.03
 
@@ -76,7 +78,7 @@ def rng_for(cfg: SceneConfig, frame: int) -> np.random.Generator:
 
 def intrinsics(cfg: SceneConfig):
     """Pinhole, fx = fy = 0.714 W (~70 deg horizontal FOV), centre at W/2, H/2."""
-    f = 0.714 * cfg.W
+    f = float(np.float32(0.714 * cfg.W))   # float32-representable: both sides see the same value
     return dict(fx=f, fy=f, cx=cfg.W / 2.0, cy=cfg.H / 2.0, W=cfg.W, H=cfg.H)
 
 
@@ -157,7 +159,16 @@ def render_depth(cfg, surf: Surface, R, T, rng, noise=True, holes=True):
     # the camera-frame z of o + s*dw equals s (dc has unit z)
     depth = s.copy()
     if noise:
-        depth += rng.normal(0.0, DEPTH_SIGMA, depth.shape)
+        # stereo (ELAS-like) depth noise is spatially correlated: a smooth field of
+        # std DEPTH_SIGMA (correlation ~NOISE_CORR_MM on the tissue) plus a small
+        # white part.  i.i.d. 0.1 mm noise at 0.1-0.2 mm pixels would make
+        # central-difference normals ~15-20 deg noisy, failing every 10 deg gate.
+        from scipy.ndimage import gaussian_filter
+        pix_mm = Z0 / it["fx"]
+        sig_px = max(0.5, NOISE_CORR_MM / pix_mm)
+        field_ = gaussian_filter(rng.normal(0.0, 1.0, depth.shape), sig_px, mode="reflect")
+        field_ *= DEPTH_SIGMA / max(field_.std(), 1e-12)
+        depth += field_ + rng.normal(0.0, WHITE_SIGMA, depth.shape)
     if holes:
         target = HOLE_FRAC * H * W
         r = max(1.5, 0.02 * W)
