@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark of the MIS-SLAM registration hot path on B200 (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl mis|reference]
+
+A step = one pass of the whole hot path over one frame of the C3 workload
+(BASELINE.json configs[2]: 640x480 depth, ~300k model points, ~1000 nodes,
+k=4, sparse ORB feature term, 5 GN x 10 PCG): rebuild of the model order
+(mis_set_model + mis_set_graph: K13 tuple sort), frame prep, feature skinning,
+BSR pattern, 5 Gauss-Newton iterations (K3 + K4/K5 + K6-K8), final warp (K9)
+and fusion + lift (K10-K12).  Inputs are resident in HBM when the timed region
+starts (`value`); `e2e` repeats the step through the C-ABI with pinned HOST
+buffers (H2D of the model, graph, depth, features, colour and D2H of the
+report inside the timed region).  Metric: GN registrations per second
+(whole job, all ranks).  With N > 1 each rank runs an independent replica
+(the C3 path does not shard: DESIGN.md §7, "replicas only"), scaling "weak".
+
+--impl reference times the fp64 CPU oracle (oracle/, the reference arm of this
+tier) on the same workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GN registrations/sec"
+UNIT = "registrations/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks (NVML, sampled in a thread)
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def load_workload(cfg_name, seed_offset):
+    from paper_1803_02009_b200 import synth
+    sc = synth.make_scene(cfg_name, 1, seed_offset)
+    return sc
+
+
+def params_for(cfg, M):
+    return M.mis_default_params(k=cfg.k, n_nbr=cfg.n_nbr, gn_iters=cfg.gn_iters, pcg_iters=cfg.pcg_iters)
+
+
+def run_mis(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1803_02009_b200 import mis as M
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sc = load_workload(args.config, seed_offset=rank)
+    cfg = sc["cfg"]
+    it = sc["intr"]
+    intr = M.intrinsics(it["fx"], it["fy"], it["cx"], it["cy"], it["W"], it["H"])
+    stream = torch.cuda.current_stream()
+    ctx = M.Context(params_for(cfg, M), device=local_rank, stream=stream.cuda_stream)
+    n = sc["xyz"].shape[0]
+    cap = n + cfg.H * cfg.W + 16
+    td = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    # one-time setup: device skinning (Eq. 2) of the initial model, then keep the
+    # tuple-sorted model + skinning as the per-step restore state
+    M.mis_set_model(ctx.ptr, td(sc["xyz"]), td(sc["nrm"]), td(sc["rgb"]), td(sc["weight"]), td(sc["stamp"]),
+                    capacity=cap)
+    M.mis_set_graph(ctx.ptr, td(sc["g"]), td(sc["nbr"]))
+    st = M.mis_get_model(ctx.ptr, cfg.k, device=True)
+    g_d, nbr_d = td(sc["g"]), td(sc["nbr"])
+    depth_d, rgb_d = td(sc["depth"]), td(sc["rgb_obs"])
+    fs_d, fd_d = td(sc["feat_src"]), td(sc["feat_dst"])
+    pose = sc["pose"]
+
+    def step():
+        M.mis_set_model(ctx.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
+        M.mis_set_graph(ctx.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+        M.mis_register(ctx.ptr, depth_d, intr, pose, fs_d, fd_d, report=False)
+        M.mis_warp(ctx.ptr)
+        return M.mis_fuse(ctx.ptr, rgb_d, 1)
+
+    # pinned host copies for the end-to-end leg
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h = {k: pin(v) for k, v in st.items()}
+    g_h, nbr_h = pin(g_d), pin(nbr_d)
+    depth_h, rgb_h, fs_h, fd_h = pin(depth_d), pin(rgb_d), pin(fs_d), pin(fd_d)
+    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in
+                    [h["xyz"], h["nrm"], h["rgb"], h["weight"], h["stamp"], h["ids"], h["knn_idx"], h["knn_w"],
+                     g_h, nbr_h, depth_h, rgb_h, fs_h, fd_h])
+    rep_bytes = M.C.sizeof(M.mis_report)
+
+    def step_e2e():
+        M.mis_set_model(ctx.ptr, h["xyz"], h["nrm"], h["rgb"], h["weight"], h["stamp"], h["ids"], capacity=cap)
+        M.mis_set_graph(ctx.ptr, g_h, nbr_h, h["knn_idx"], h["knn_w"])
+        rep = M.mis_register(ctx.ptr, depth_h, intr, pose, fs_h, fd_h, report=True)   # D2H of the report
+        M.mis_warp(ctx.ptr)
+        n_out, _ = M.mis_fuse(ctx.ptr, rgb_h, 1)
+        return rep, n_out
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        step()
+    for _ in range(min(args.warmup, 3)):
+        step_e2e()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device): per-step CUDA events, L2 flushed between steps
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    M.mis_prof_read(ctx.ptr, reset=True)
+    M.mis_prof_enable(ctx.ptr, True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = M.mis_launch_count()
+    t0 = time.perf_counter()
+    with ClockSampler(local_rank) as clk:
+        for k in range(K):
+            flush.zero_()
+            evs[k][0].record(stream)
+            stats_last = step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    launches = M.mis_launch_count() - l0
+    M.mis_prof_enable(ctx.ptr, False)
+    prof = M.mis_prof_read(ctx.ptr, reset=True)
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    dev_ms_max = float(t.item())
+
+    # ---------------- end-to-end leg (host buffers through the C-ABI)
+    Ke = max(1, min(K, args.e2e_steps))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(Ke):
+        rep, n_out = step_e2e()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(t.item())
+    rep = M.report_dict(rep)
+
+    # ---------------- roofline of the dominant kernel group
+    hbm, _, peak_kind = peaks()
+    groups = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(groups, key=lambda k: groups[k][0])
+    nnzb, m = rep["nnzb"], sc["g"].shape[0]
+    P, G = cfg.pcg_iters, cfg.gn_iters
+    n_assoc = float(np.mean(rep["n_assoc"][:G]))
+    # algorithmic bytes per launch
+    algo = {
+        "assemble_points": n * (24 + 4 * cfg.k) + 16 * n_assoc,
+        "solve": P * (nnzb * 144 + 6 * m * 4 * 11) + nnzb * (36 + 16 + 36) * 4 + m * 36 * 4,
+        "frame_prep": cfg.H * cfg.W * 20,
+        "warp_model": n * (24 + 8 * cfg.k) * 2 // 2 + n * 24,
+        "fuse_register": n * 24 + cfg.H * cfg.W * 8,
+        "fuse_apply": n * 64,
+        "lift": cfg.H * cfg.W * 28,
+    }
+    ms_dom, n_dom = groups[dom]
+    per_launch_ms = ms_dom / max(1, n_dom if dom not in ("solve",) else n_dom / 2)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    bytes_dom = algo.get(dom)
+    roof = None
+    if bytes_dom is not None:
+        ach = bytes_dom / (per_launch_ms * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": int(bytes_dom), "launch_ms": round(per_launch_ms, 5),
+                "share_of_step": round(ms_dom / max(dev_ms, 1e-9), 3)}
+
+    value = world * K / (dev_ms_max / 1e3)
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(dev_ms_max / K, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.W}x{cfg.H} depth, {n} model points, {m} nodes, k={cfg.k}, "
+                               f"{cfg.gn_iters} GN x {cfg.pcg_iters} PCG, {sc['feat_src'].shape[0]} ORB features; "
+                               "step = order + register + warp + fuse",
+                   "l2": "flushed between steps (256 MiB write outside the per-step events)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "gn_iters_per_s": round(value * cfg.gn_iters, 2),
+        "e2e": {"value": round(world * Ke / (e2e_ms_max / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": rep_bytes + 8, "steps": Ke},
+        "roofline": roof,
+        "kernels_ms_per_step": {k: round(v[0] / K, 5) for k, v in groups.items()},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "wall_s_timed": round(wall, 4),
+        "registration": {"E_first": rep["energy"][0, 4], "E_last_iter": rep["energy"][G - 1, 4],
+                         "n_assoc": int(rep["n_assoc"][0]), "nnzb": int(nnzb), "segments": int(rep["n_segments"]),
+                         "fuse_stats": [int(x) for x in stats_last[1]]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, sc)
+    ctx.close()
+    return out
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_step(O, sc, prm, pb, fr, rgb_obs):
+    Rt, E, na = O.register(prm, pb, fr)
+    xyz, nrm, g = O.warp_model(pb, Rt)
+    o = O.fuse(prm, xyz.astype(np.float32), nrm.astype(np.float32), sc["rgb"], sc["weight"], sc["stamp"], fr,
+               rgb_obs, 1, g.astype(np.float32))
+    return E, o["n_lift"]
+
+
+def oracle_setup(sc):
+    import oracle as O
+    cfg = sc["cfg"]
+    idx, w, _ = O.skin(sc["xyz"], sc["g"], cfg.k)
+    pb = O.Problem(sc["xyz"], sc["nrm"], idx, w.astype(np.float32), sc["g"], sc["nbr"], sc["feat_src"], sc["feat_dst"])
+    fr = O.Frame(sc["depth"], sc["intr"], sc["pose"])
+    prm = O.params(k=cfg.k, n_nbr=cfg.n_nbr, gn_iters=cfg.gn_iters, pcg_iters=cfg.pcg_iters, solve_mode=1)
+    return O, pb, fr, prm
+
+
+def cpu_baseline(args, sc, steps=2):
+    O, pb, fr, prm = oracle_setup(sc)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle_step(O, sc, prm, pb, fr, sc["rgb_obs"])
+    dt = time.perf_counter() - t0
+    return {"value": round(steps / dt, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full steps of the same {args.config} workload (register {sc['cfg'].gn_iters} GN x "
+                      f"{sc['cfg'].pcg_iters} PCG MIRROR + warp + fuse/lift), fp64 C++ oracle, single thread; "
+                      "initial skinning precomputed (as on the GPU)"}
+
+
+def run_reference(args):
+    sc = load_workload(args.config, 0)
+    O, pb, fr, prm = oracle_setup(sc)
+    for _ in range(args.warmup):
+        oracle_step(O, sc, prm, pb, fr, sc["rgb_obs"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(O, sc, prm, pb, fr, sc["rgb_obs"])
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    cfg = sc["cfg"]
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg.W}x{cfg.H} depth, {sc['xyz'].shape[0]} model points, "
+                               f"{sc['g'].shape[0]} nodes, k={cfg.k}, {cfg.gn_iters} GN x {cfg.pcg_iters} PCG; "
+                               "step = register + warp + fuse"},
+        "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": "each step = one full frame of the workload on the fp64 C++ oracle, 1 thread"},
+        "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="mis", choices=["mis", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3   # timing rule: W >= 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_mis(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out, default=float), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

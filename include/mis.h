@@ -208,6 +208,23 @@ mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* v
  * (H*W, internal point index or -1), why (n). Host memory only. */
 mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
 
+/* ---- instrumentation (bench / profiling) ---- */
+#define MIS_PROF_NCAT 12
+/* Kernel groups: 0 frame_prep (K1), 1 skin (K2), 2 sort_order (K13), 3 pattern,
+ * 4 assemble_points (K3), 5 assemble_graph (K4/K5), 6 solve (K6-K8),
+ * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),
+ * 11 io (uploads, layout conversion). */
+const char* mis_prof_name(int cat);
+/* on != 0: record a CUDA event pair on the context stream around every kernel
+ * group launched by this context (adds no synchronisation). */
+mis_status mis_prof_enable(mis_ctx* ctx, int on);
+/* Accumulated device milliseconds and launches per group since the last reset
+ * (synchronises the context stream).  ms / launches: MIS_PROF_NCAT entries. */
+mis_status mis_prof_read(mis_ctx* ctx, double* ms, int64_t* launches, int reset);
+/* Kernels of this library launched so far in this process (all contexts;
+ * CUB library kernels of the setup sort are not counted). */
+int64_t mis_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,6 +2,7 @@
 // uploads, orchestration of the kernels of one frame, NCCL plumbing.
 #include <dlfcn.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -221,6 +222,42 @@ __global__ void k_count_winners(int n, const unsigned long long* key, unsigned l
 
 static inline int nb(int64_t n, int t = 256) { return (int)((n + t - 1) / t); }
 
+// ------------------------------------------------------------ instrumentation
+static std::atomic<int64_t> g_launches{0};
+void count_launches(int64_t k) { g_launches += k; }
+
+static cudaEvent_t pool_get(Ctx* c) {
+  if (!c->pool.empty()) { cudaEvent_t e = c->pool.back(); c->pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(Ctx* c_, int cat_, int nk) : c(c_), cat(cat_) {
+  g_launches += nk;
+  c->prof_n[cat] += nk;
+  if (c->prof) {
+    cudaEvent_t a = pool_get(c);
+    b = pool_get(c);
+    cudaEventRecord(a, c->st);
+    c->pev.push_back({cat, a, b});
+  }
+}
+ProfScope::~ProfScope() {
+  if (b) cudaEventRecord(b, c->st);
+}
+
+static void prof_collect(Ctx* c) {
+  cudaStreamSynchronize(c->st);
+  for (auto& e : c->pev) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) c->prof_ms[e.cat] += ms;
+    c->pool.push_back(e.a);
+    c->pool.push_back(e.b);
+  }
+  c->pev.clear();
+}
+
 }  // namespace mis
 
 using namespace mis;
@@ -239,6 +276,11 @@ static mis_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
     cudaError_t e__ = (call);                                     \
     if (e__ != cudaSuccess) return cuda_fail((c), e__, #call);    \
   } while (0)
+
+static cudaError_t run_build_order(Ctx* c) {
+  ProfScope ps(c, P_ORDER, c->n > 0 ? 17 + 2 * c->K : 0);
+  return build_order(c);
+}
 
 static cudaMemcpyKind kind_in(mis_mem mem) { return mem == MIS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice; }
 static cudaMemcpyKind kind_out(mis_mem mem) { return mem == MIS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice; }
@@ -371,6 +413,7 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
   ModelView md = model_view(c);
   if (n > 0) {
     TRY(c, ensure(c, c->stage, n * 12));
+    ProfScope ps(c, P_IO, 4);
     float* st = c->stage.as<float>();
     TRY(c, cudaMemcpyAsync(st, xyz, n * 12, kind_in(mem), c->st));
     k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, st, md.px, md.py, md.pz, 0.f);
@@ -419,10 +462,14 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, kind_in(mem), c->st));
   int* flag = c->counter.as<int>();
   TRY(c, cudaMemsetAsync(flag, 0, 4, c->st));
-  if (nn > 0) k_check_nbr<<<nb((int64_t)m * nn), 256, 0, c->st>>>(m, nn, c->nbr.as<int32_t>(), flag);
+  if (nn > 0) {
+    ProfScope ps(c, P_IO, 1);
+    k_check_nbr<<<nb((int64_t)m * nn), 256, 0, c->st>>>(m, nn, c->nbr.as<int32_t>(), flag);
+  }
   ModelView md = model_view(c);
   const int64_t n = c->n;
   if (n > 0) {
+    ProfScope ps(c, knn_idx ? P_IO : P_SKIN, 1);
     if (knn_idx) {
       TRY(c, ensure(c, c->stage, n * K * 8));
       int32_t* si = c->stage.as<int32_t>();
@@ -443,9 +490,12 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
                                   ((hflag & 2) ? " duplicate id" : "") + ((hflag & 4) ? " weight" : "") +
                                   ((hflag & 8) ? " neighbour list" : ""));
   }
-  k_init_nodes<<<nb(m), 256, 0, c->st>>>(m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
+  {
+    ProfScope ps(c, P_IO, 1);
+    k_init_nodes<<<nb(m), 256, 0, c->st>>>(m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
+  }
   TRY(c, cudaGetLastError());
-  TRY(c, build_order(c));
+  TRY(c, run_build_order(c));
   c->have_graph = true;
   return MIS_OK;
 }
@@ -465,6 +515,7 @@ mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const m
   TRY(c, ensure(c, c->depth, px * 4));
   TRY(c, ensure(c, c->nmap, px * 16));
   TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, kind_in(mem), c->st));
+  ProfScope ps(c, P_FRAME, 1);
   launch_frame_prep(frame_view(c), c->nmap.as<float4>(), c->st);
   TRY(c, cudaGetLastError());
   c->have_frame = true;
@@ -487,6 +538,7 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
     TRY(c, cudaMemcpyAsync(c->fsrc.p, src, (size_t)n_feat * 12, kind_in(mem), c->st));
     TRY(c, cudaMemcpyAsync(c->fdst.p, dst, (size_t)n_feat * 12, kind_in(mem), c->st));
     const float* s = c->fsrc.as<float>();
+    ProfScope ps(c, P_SKIN, 1);
     launch_skin(n_feat, s, s + 1, s + 2, 3, c->g.as<float>(), c->m, K, c->fidx.as<int32_t>(), c->fw.as<float>(),
                 n_feat, c->st);
     TRY(c, cudaGetLastError());
@@ -516,9 +568,13 @@ static mis_status assemble(Ctx* c, bool dbg) {
   a.acc = acc;
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
-  launch_assemble_points(c->K, a, c->num_sms, c->st);
+  if (a.nchunk > 0) {
+    ProfScope ps(c, P_POINTS, 1);
+    launch_assemble_points(c->K, a, c->num_sms, c->st);
+  }
   TRY(c, cudaGetLastError());
-  if (c->rank == 0) {
+  if (c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0) {
+    ProfScope ps(c, P_GRAPH, 1);
     AsmGraphArgs gA;
     gA.nd = node_view(c);
     gA.n_nbr = c->prm.n_nbr;
@@ -578,8 +634,11 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
 static mis_status prepare(Ctx* c) {
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph (mis_set_graph)");
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
-  if (c->dirty) TRY(c, build_order(c));
-  if (!c->pattern_valid) TRY(c, build_pattern(c));
+  if (c->dirty) TRY(c, run_build_order(c));
+  if (!c->pattern_valid) {
+    ProfScope ps(c, P_PATTERN, c->world > 1 ? 8 : 5);
+    TRY(c, build_pattern(c));
+  }
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
   return MIS_OK;
 }
@@ -624,12 +683,14 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
   TRY(c, cudaMemsetAsync(c->rep_nassoc.p, 0, (MIS_MAX_GN + 1) * 8, c->st));
   for (int it = 0; it < G; ++it) {
     if ((s = assemble(c, false)) != MIS_OK) return s;
+    ProfScope ps(c, P_SOLVE, 2);
     launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, it,
                          c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
     TRY(c, launch_solve(solve_args(c, it, true, c->prm.pcg_iters), c->num_sms, c->st));
   }
   if (c->prm.flags & MIS_F_FINAL_ENERGY) {
     if ((s = assemble(c, false)) != MIS_OK) return s;
+    ProfScope ps(c, P_SOLVE, 1);
     launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, G,
                          c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
   }
@@ -643,6 +704,7 @@ mis_status mis_get_nodes(mis_ctx* c, mis_mem mem, float* out) {
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
   cudaSetDevice(c->device);
   TRY(c, ensure(c, c->stage, (size_t)c->m * 48));
+  ProfScope ps(c, P_IO, 1);
   k_get_nodes<<<nb(c->m), 256, 0, c->st>>>(c->m, c->node32.as<float>(), c->stage.as<float>());
   TRY(c, cudaMemcpyAsync(out, c->stage.p, (size_t)c->m * 48, kind_out(mem), c->st));
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
@@ -673,6 +735,7 @@ mis_status mis_dbg_set_nodes(mis_ctx* c, mis_mem mem, const float* Rt) {
   cudaSetDevice(c->device);
   TRY(c, ensure(c, c->stage, (size_t)c->m * 48));
   TRY(c, cudaMemcpyAsync(c->stage.p, Rt, (size_t)c->m * 48, kind_in(mem), c->st));
+  ProfScope ps(c, P_IO, 1);
   k_set_nodes<<<nb(c->m), 256, 0, c->st>>>(c->m, c->stage.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
   TRY(c, cudaGetLastError());
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
@@ -727,7 +790,7 @@ mis_status mis_warp(mis_ctx* c, mis_mem mem, float* xyz_cam, float* nrm_cam) {
   if (!c) return MIS_E_ARG;
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
   cudaSetDevice(c->device);
-  if (c->dirty) TRY(c, build_order(c));
+  if (c->dirty) TRY(c, run_build_order(c));
   float* xc = nullptr;
   float* nc = nullptr;
   if (xyz_cam || nrm_cam) {
@@ -735,9 +798,12 @@ mis_status mis_warp(mis_ctx* c, mis_mem mem, float* xyz_cam, float* nrm_cam) {
     xc = c->stage.as<float>();
     nc = xc + 3 * c->n;
   }
-  launch_warp_model(c->K, model_view(c), node_view(c), frame_view(c), xyz_cam ? xc : nullptr,
-                    nrm_cam ? nc : nullptr, c->st);
-  launch_advance_nodes(node_view(c), c->g.as<float>(), c->st);
+  {
+    ProfScope ps(c, P_WARP, (c->n > 0) + 1);
+    launch_warp_model(c->K, model_view(c), node_view(c), frame_view(c), xyz_cam ? xc : nullptr,
+                      nrm_cam ? nc : nullptr, c->st);
+    launch_advance_nodes(node_view(c), c->g.as<float>(), c->st);
+  }
   TRY(c, cudaGetLastError());
   if (xyz_cam) TRY(c, cudaMemcpyAsync(xyz_cam, xc, (size_t)c->n * 12, kind_out(mem), c->st));
   if (nrm_cam) TRY(c, cudaMemcpyAsync(nrm_cam, nc, (size_t)c->n * 12, kind_out(mem), c->st));
@@ -767,6 +833,7 @@ static mis_status fuse_register(Ctx* c, const float* rgb, int32_t frame) {
   TRY(c, ensure(c, c->pix, c->cap * 4));
   TRY(c, ensure(c, c->why, c->cap));
   TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
+  ProfScope ps(c, P_FREG, c->n > 0 ? 1 : 0);
   launch_fuse_register(fuse_args(c, rgb, frame), c->st);
   TRY(c, cudaGetLastError());
   return MIS_OK;
@@ -776,7 +843,7 @@ mis_status mis_dbg_fuse_register(mis_ctx* c, int64_t* owner, uint8_t* why) {
   if (!c || !owner) return MIS_E_ARG;
   if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
   cudaSetDevice(c->device);
-  if (c->dirty) TRY(c, build_order(c));
+  if (c->dirty) TRY(c, run_build_order(c));
   mis_status s;
   if ((s = fuse_register(c, nullptr, 0)) != MIS_OK) return s;
   const size_t px = (size_t)c->W * c->H;
@@ -792,7 +859,7 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   if (!c || !n_out) return MIS_E_ARG;
   if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
   cudaSetDevice(c->device);
-  if (c->dirty) TRY(c, build_order(c));
+  if (c->dirty) TRY(c, run_build_order(c));
   const size_t px = (size_t)c->W * c->H;
   const float* rgb_dev = nullptr;
   if (rgb) {
@@ -803,14 +870,20 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   mis_status s;
   if ((s = fuse_register(c, rgb_dev, frame_index)) != MIS_OK) return s;
   FuseArgs a = fuse_args(c, rgb_dev, frame_index);
-  launch_fuse_apply(a, c->st);
+  {
+    ProfScope ps(c, P_FAPPLY, c->n > 0 ? 1 : 0);
+    launch_fuse_apply(a, c->st);
+  }
   const int nbk = lift_blocks(c->W, c->H);
   TRY(c, ensure(c, c->lift_counts, (size_t)(2 * nbk + 4) * 4));
   int32_t* counts = c->lift_counts.as<int32_t>();
-  launch_lift_count(a, counts, nbk, c->st);
   unsigned long long* cnt = c->counter.as<unsigned long long>();
   TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
-  k_count_winners<<<nb((int64_t)px), 256, 0, c->st>>>((int)px, c->pixkey.as<unsigned long long>(), cnt);
+  {
+    ProfScope ps(c, P_LIFT, 3);
+    launch_lift_count(a, counts, nbk, c->st);
+    k_count_winners<<<nb((int64_t)px), 256, 0, c->st>>>((int)px, c->pixkey.as<unsigned long long>(), cnt);
+  }
   int32_t n_lift = 0;
   unsigned long long n_reg = 0;
   TRY(c, cudaMemcpyAsync(&n_lift, counts + 2 * nbk + 1, 4, cudaMemcpyDeviceToHost, c->st));
@@ -821,6 +894,7 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
     return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
   }
   const int64_t base = c->n;
+  ProfScope ps(c, P_LIFT, 1 + (n_lift > 0));
   launch_lift_write(a, counts + nbk + 1, nbk, base, c->next_id, c->st);
   ModelView md = model_view(c);
   if (n_lift > 0) {
@@ -852,6 +926,7 @@ mis_status mis_get_model(mis_ctx* c, mis_mem mem, float* xyz, float* nrm, float*
   if (n == 0) return MIS_OK;
   ModelView md = model_view(c);
   TRY(c, ensure(c, c->stage, (size_t)n * 8 * MIS_MAX_K + 64));
+  ProfScope ps(c, P_IO, (xyz != nullptr) + (nrm != nullptr) + (rgb != nullptr) + (knn_idx || knn_w));
   float* st = c->stage.as<float>();
   if (xyz) {
     k_interleave3<<<nb(n), 256, 0, c->st>>>(n, md.px, md.py, md.pz, st);
@@ -898,6 +973,7 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
   int32_t* pi = reinterpret_cast<int32_t*>(sw + nq * K);
   float* pw = reinterpret_cast<float*>(pi + nq * K);
   TRY(c, cudaMemcpyAsync(sp, pts, nq * 12, kind_in(mem), c->st));
+  ProfScope ps(c, P_SKIN, 2);
   launch_skin(nq, sp, sp + 1, sp + 2, 3, c->g.as<float>(), c->m, K, si, sw, nq, c->st);
   k_to_point_major<<<nb(nq), 256, 0, c->st>>>(nq, K, nq, si, sw, pi, pw);
   TRY(c, cudaGetLastError());
@@ -906,5 +982,32 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
   return MIS_OK;
 }
+
+const char* mis_prof_name(int cat) {
+  static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assemble_points",
+                                             "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
+                                             "lift", "io"};
+  return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
+}
+
+mis_status mis_prof_enable(mis_ctx* c, int on) {
+  if (!c) return MIS_E_ARG;
+  c->prof = on != 0;
+  return MIS_OK;
+}
+
+mis_status mis_prof_read(mis_ctx* c, double* ms, int64_t* launches, int reset) {
+  if (!c) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  prof_collect(c);
+  for (int i = 0; i < MIS_PROF_NCAT; ++i) {
+    if (ms) ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_n[i];
+    if (reset) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+  }
+  return MIS_OK;
+}
+
+int64_t mis_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"

@@ -76,6 +76,27 @@ struct Ctx {
   DBuf cub_tmp;
   // host staging for small uploads
   DBuf pinned_small;
+
+  // ---- instrumentation
+  bool prof = false;
+  struct PEv { int cat; cudaEvent_t a, b; };
+  std::vector<PEv> pev;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[MIS_PROF_NCAT] = {0};
+  int64_t prof_n[MIS_PROF_NCAT] = {0};
+};
+
+enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO };
+void count_launches(int64_t k);
+
+// Records an event pair around a group of `nk` kernel launches on the context
+// stream when profiling is on; always adds nk to the launch counter.
+struct ProfScope {
+  Ctx* c;
+  int cat;
+  cudaEvent_t b = nullptr;
+  ProfScope(Ctx* c_, int cat_, int nk);
+  ~ProfScope();
 };
 
 // buffer management (api.cu)

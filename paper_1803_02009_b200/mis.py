@@ -80,7 +80,12 @@ _sig = {
     "mis_dbg_associate": ([_V, C.c_int, _V, _V], C.c_int),
     "mis_dbg_system": ([_V, _V, _V, _V, _V, _V, _P(C.c_int64)], C.c_int),
     "mis_dbg_fuse_register": ([_V, _V, _V], C.c_int),
+    "mis_prof_name": ([C.c_int], C.c_char_p),
+    "mis_prof_enable": ([_V, C.c_int], C.c_int),
+    "mis_prof_read": ([_V, _V, _V, C.c_int], C.c_int),
+    "mis_launch_count": ([], C.c_int64),
 }
+MIS_PROF_NCAT = 12
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -94,9 +99,9 @@ def _is_torch(x):
 
 
 def _mem_of(*arrays):
-    kinds = {MIS_MEM_DEVICE if _is_torch(a) else MIS_MEM_HOST for a in arrays if a is not None}
+    kinds = {MIS_MEM_DEVICE if (_is_torch(a) and a.is_cuda) else MIS_MEM_HOST for a in arrays if a is not None}
     if len(kinds) > 1:
-        raise ValueError("all array arguments of one call must be host (numpy) or device (torch) alike")
+        raise ValueError("all array arguments of one call must be host (numpy / CPU tensor) or device alike")
     return kinds.pop() if kinds else MIS_MEM_HOST
 
 
@@ -104,8 +109,8 @@ def _ptr(x, dtype=None):
     if x is None:
         return None
     if _is_torch(x):
-        if not x.is_cuda or not x.is_contiguous():
-            raise ValueError("device arguments must be contiguous CUDA tensors")
+        if not x.is_contiguous():
+            raise ValueError("tensor arguments must be contiguous")
         return C.c_void_p(x.data_ptr())
     if dtype is not None and x.dtype != dtype:
         raise TypeError(f"expected {dtype}, got {x.dtype}")
@@ -307,6 +312,25 @@ def mis_dbg_fuse_register(ctx, H, W, n):
     why = np.zeros(n, np.uint8)
     _check(ctx, _lib.mis_dbg_fuse_register(ctx, _ptr(owner), _ptr(why)))
     return owner, why
+
+
+def mis_prof_name(cat):
+    return _lib.mis_prof_name(cat).decode()
+
+
+def mis_prof_enable(ctx, on=True):
+    _check(ctx, _lib.mis_prof_enable(ctx, 1 if on else 0))
+
+
+def mis_prof_read(ctx, reset=False):
+    ms = np.zeros(MIS_PROF_NCAT, np.float64)
+    n = np.zeros(MIS_PROF_NCAT, np.int64)
+    _check(ctx, _lib.mis_prof_read(ctx, _ptr(ms), _ptr(n), 1 if reset else 0))
+    return {mis_prof_name(i): (float(ms[i]), int(n[i])) for i in range(MIS_PROF_NCAT)}
+
+
+def mis_launch_count():
+    return int(_lib.mis_launch_count())
 
 
 class Context:
