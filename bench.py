@@ -185,6 +185,7 @@ def run_mis(args, rank, world, local_rank):
     launches = M.mis_launch_count() - l0
     M.mis_prof_enable(ctx.ptr, False)
     prof = M.mis_prof_read(ctx.ptr, reset=True)
+    pcg_phases = M.mis_dbg_solver_phases(ctx.ptr)
     dev_ms = sum(a.elapsed_time(b) for a, b in evs)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -258,11 +259,13 @@ def run_mis(args, rank, world, local_rank):
                 "d2h_bytes_per_step": rep_bytes + 8, "steps": Ke},
         "roofline": roof,
         "kernels_ms_per_step": {k: round(v[0] / K, 5) for k, v in groups.items()},
+        "pcg_phases_us_last_launch": pcg_phases,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
         "registration": {"E_first": rep["energy"][0, 4], "E_last_iter": rep["energy"][G - 1, 4],
                          "n_assoc": int(rep["n_assoc"][0]), "nnzb": int(nnzb), "segments": int(rep["n_segments"]),
+                         "pcg_cluster_ctas": int(rep["solver_cluster"]),
                          "fuse_stats": [int(x) for x in stats_last[1]]},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

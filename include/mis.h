@@ -61,6 +61,8 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
 /* Flags */
 #define MIS_F_FINAL_ENERGY 1u   /* mis_register also evaluates the energy after the last update */
 #define MIS_F_NO_GRAPH     2u   /* do not capture the GN loop in a CUDA graph                    */
+#define MIS_F_GRID_SOLVER  4u   /* force the grid-wide PCG kernel (else the cluster-resident one
+                                   whenever the system fits in one cluster's shared memory)       */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {
@@ -93,6 +95,8 @@ typedef struct {
   float pcg_rel_res[MIS_MAX_GN];       /* sqrt(r.z / r0.z0) after the last PCG iteration    */
   int64_t nnzb;                        /* nonzero 6x6 blocks of H (both triangles)           */
   int64_t n_segments;                  /* distinct kNN tuples in the model                  */
+  int32_t solver_cluster;              /* CTAs of the cluster-resident PCG (0: grid kernel)  */
+  int32_t reserved;
 } mis_report;
 
 int32_t mis_abi_version(void);
@@ -209,11 +213,11 @@ mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* v
 mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
 
 /* ---- instrumentation (bench / profiling) ---- */
-#define MIS_PROF_NCAT 12
+#define MIS_PROF_NCAT 13
 /* Kernel groups: 0 frame_prep (K1), 1 skin (K2), 2 sort_order (K13), 3 pattern,
  * 4 assemble_points (K3), 5 assemble_graph (K4/K5), 6 solve (K6-K8),
  * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),
- * 11 io (uploads, layout conversion). */
+ * 11 io (uploads, layout conversion), 12 reduce_records (K3 chunk records -> blocks). */
 const char* mis_prof_name(int cat);
 /* on != 0: record a CUDA event pair on the context stream around every kernel
  * group launched by this context (adds no synchronisation). */
@@ -224,6 +228,10 @@ mis_status mis_prof_read(mis_ctx* ctx, double* ms, int64_t* launches, int reset)
 /* Kernels of this library launched so far in this process (all contexts;
  * CUB library kernels of the setup sort are not counted). */
 int64_t mis_launch_count(void);
+/* %globaltimer stamps (ns) of the last cluster-PCG launch, 8 per CTA (16 CTAs):
+ * start, system built, preconditioner built, PCG start, PCG end, nodes updated,
+ * z replicated, partial published (host memory, 128 entries). */
+mis_status mis_dbg_solver_phases(mis_ctx* ctx, uint64_t* out128);
 
 #ifdef __cplusplus
 }

@@ -73,12 +73,14 @@ AccView acc_view(Ctx* c) {
   AccView a;
   float* base = c->acc.as<float>();
   const size_t nz = (size_t)c->nnzb, m = (size_t)c->m;
+  // written whole by the record reduction: data | mom | rhs_data | node_mom
+  // accumulated by K4/K5 atomics (zeroed each iteration): graph | rhs_graph
   a.data = base;
   a.mom = a.data + nz * 36;
-  a.graph = a.mom + nz * 16;
-  a.rhs_data = a.graph + nz * 36;
+  a.rhs_data = a.mom + nz * 16;
   a.node_mom = a.rhs_data + 6 * m;
-  a.rhs_graph = a.node_mom + 12 * m;
+  a.graph = a.node_mom + 12 * m;
+  a.rhs_graph = a.graph + nz * 36;
   a.energy = c->energy.as<double>();
   return a;
 }
@@ -348,6 +350,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
   if (ensure(c, c->rep_energy, (MIS_MAX_GN + 1) * 5 * 8) != cudaSuccess ||
       ensure(c, c->rep_nassoc, (MIS_MAX_GN + 1) * 8) != cudaSuccess ||
       ensure(c, c->rep_res, MIS_MAX_GN * 4) != cudaSuccess || ensure(c, c->numeric_flag, 16) != cudaSuccess ||
+      ensure(c, c->tstamp, 2048) != cudaSuccess || cudaMemset(c->tstamp.p, 0, 2048) != cudaSuccess ||
       ensure(c, c->counter, 64) != cudaSuccess) {
     delete c;
     return MIS_E_NOMEM;
@@ -550,7 +553,10 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
 // zero the accumulators, run K3 (+ K4/K5 on rank 0), all-reduce across ranks
 static mis_status assemble(Ctx* c, bool dbg) {
   AccView acc = acc_view(c);
-  TRY(c, cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));
+  {   // only the atomically accumulated graph part needs zeroing; the record reduction writes the rest
+    const size_t head = (size_t)c->nnzb * 52 + 18 * (size_t)c->m;
+    TRY(c, cudaMemsetAsync(c->acc.as<float>() + head, 0, (c->acc_floats - head) * 4, c->st));
+  }
   TRY(c, cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
   const double d2r = M_PI / 180.0;
   AsmPointsArgs a;
@@ -565,12 +571,30 @@ static mis_status assemble(Ctx* c, bool dbg) {
   a.eps_dd = c->prm.eps_d_mm;
   a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
   a.cos_eps_n = (float)a.cos_eps_nd;
-  a.acc = acc;
+  a.records = c->records.as<float>();
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
   if (a.nchunk > 0) {
     ProfScope ps(c, P_POINTS, 1);
     launch_assemble_points(c->K, a, c->num_sms, c->st);
+  }
+  TRY(c, cudaGetLastError());
+  {
+    ProfScope ps(c, P_REDUCE, 1);
+    ReduceArgs r;
+    r.records = c->records.as<float>();
+    r.rec_stride = rec_stride(c->K);
+    r.K = c->K;
+    r.nchunk = c->nchunk;
+    r.nnzb = c->nnzb;
+    r.m = c->m;
+    r.upper_of = c->upper_of.as<int32_t>();
+    r.slot_ptr = c->slot_ptr.as<int32_t>();
+    r.slot_src = c->slot_src.as<int32_t>();
+    r.node_ptr = c->node_ptr.as<int32_t>();
+    r.node_src = c->node_src.as<int32_t>();
+    r.acc = acc;
+    launch_reduce_records(r, c->st);
   }
   TRY(c, cudaGetLastError());
   if (c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0) {
@@ -628,7 +652,32 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.rep_nassoc = c->rep_nassoc.as<double>();
   s.rep_res = c->rep_res.as<float>();
   s.numeric_flag = c->numeric_flag.as<int>();
+  const bool cl = c->cl_size > 0 && c->cluster_ok && !(c->prm.flags & MIS_F_GRID_SOLVER);
+  s.cluster_size = cl ? c->cl_size : 0;
+  s.part = c->part.as<int32_t>();
+  s.max_rows = c->cl_max_rows;
+  s.max_nnz = c->cl_max_nnz;
+  s.smem_bytes = c->cl_smem;
+  s.write_global = update ? 0 : 1;
+  s.tstamp = c->tstamp.as<unsigned long long>();
   return s;
+}
+
+// cluster launch first; fall back to the grid-wide kernel if the device refuses it
+static cudaError_t run_solve(Ctx* c, const SolveArgs& s) {
+  cudaError_t e = launch_solve(s, c->num_sms, c->st);
+  if (e != cudaSuccess && s.cluster_size > 0) {
+    cudaGetLastError();
+    c->cluster_ok = false;
+    c->solver_note = std::string("cluster PCG unavailable (") + cudaGetErrorString(e) + "), using the grid kernel";
+    SolveArgs g = s;
+    g.cluster_size = 0;
+    e = launch_solve(g, c->num_sms, c->st);
+    c->last_solver = 0;
+  } else {
+    c->last_solver = s.cluster_size;
+  }
+  return e;
 }
 
 static mis_status prepare(Ctx* c) {
@@ -636,7 +685,7 @@ static mis_status prepare(Ctx* c) {
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
   if (c->dirty) TRY(c, run_build_order(c));
   if (!c->pattern_valid) {
-    ProfScope ps(c, P_PATTERN, c->world > 1 ? 8 : 5);
+    ProfScope ps(c, P_PATTERN, (c->world > 1 ? 8 : 5) + (c->nchunk > 0 ? 4 : 0));
     TRY(c, build_pattern(c));
   }
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
@@ -660,6 +709,7 @@ static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
   }
   rep->nnzb = c->nnzb;
   rep->n_segments = c->nseg;
+  rep->solver_cluster = c->last_solver;
   return flag ? MIS_E_NUMERIC : MIS_OK;
 }
 
@@ -686,7 +736,7 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
     ProfScope ps(c, P_SOLVE, 2);
     launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, it,
                          c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
-    TRY(c, launch_solve(solve_args(c, it, true, c->prm.pcg_iters), c->num_sms, c->st));
+    TRY(c, run_solve(c, solve_args(c, it, true, c->prm.pcg_iters)));
   }
   if (c->prm.flags & MIS_F_FINAL_ENERGY) {
     if ((s = assemble(c, false)) != MIS_OK) return s;
@@ -776,7 +826,7 @@ mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val
   if ((s = assemble(c, false)) != MIS_OK) return s;
   launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, 0,
                        c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
-  TRY(c, launch_solve(solve_args(c, 0, false, 0), c->num_sms, c->st));
+  TRY(c, run_solve(c, solve_args(c, 0, false, 0)));
   if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
   if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
@@ -986,7 +1036,7 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
 const char* mis_prof_name(int cat) {
   static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assemble_points",
                                              "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
-                                             "lift", "io"};
+                                             "lift", "io", "reduce_records"};
   return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
 }
 
@@ -1009,5 +1059,13 @@ mis_status mis_prof_read(mis_ctx* c, double* ms, int64_t* launches, int reset) {
 }
 
 int64_t mis_launch_count(void) { return g_launches.load(); }
+
+mis_status mis_dbg_solver_phases(mis_ctx* c, uint64_t* out128) {
+  if (!c || !out128) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  TRY(c, cudaMemcpyAsync(out128, c->tstamp.p, 2048, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
 
 }  // extern "C"

@@ -47,11 +47,29 @@ __device__ __forceinline__ bool depth_ok_d(float d) { return isfinite(d) && d > 
 // arithmetic order is irrelevant here; only decisions within ~1e-12 of a
 // threshold can differ).  Used for the rare points whose fp32 quantities lie
 // inside a guard band.
+// Arguments by value / pointer-to-global only: a reference to the kernel's
+// parameter struct would force an addressable (local-memory) copy of it.
+struct Fp64Args {
+  const float *px, *py, *pz, *nx, *ny, *nz, *kw;
+  int64_t cap;
+  const double* Rt64;
+  const float* g;
+  const float* depth;
+  int W, H;
+  double fxd, fyd, cxd, cyd;
+  double Rd[9], Td[3];
+  double eps_dd, cos_eps_nd;
+};
+
 template <int K>
-__device__ __noinline__ void assoc_fp64(const AsmPointsArgs& a, int64_t i, const int32_t* nodes, float* vt_out,
+__device__ __noinline__ void assoc_fp64(const Fp64Args* __restrict__ pa, int64_t i, const int32_t* nodes, float* vt_out,
                                         float* q_out, float* N_out, int* pix_out, uint8_t* why_out) {
-  const ModelView& md = a.md;
-  const FrameView& f = a.fr;
+  const Fp64Args& a = *pa;
+  struct MV { const float *px, *py, *pz, *nx, *ny, *nz, *kw; int64_t cap; } md = {a.px, a.py, a.pz, a.nx, a.ny, a.nz,
+                                                                                 a.kw, a.cap};
+  struct FV { int W, H; double fxd, fyd, cxd, cyd; const double *Rd, *Td; const float* depth; } f = {
+      a.W, a.H, a.fxd, a.fyd, a.cxd, a.cyd, a.Rd, a.Td, a.depth};
+  struct ND { const double* Rt64; const float* g; } ndv = {a.Rt64, a.g};
   double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
   double W = 0, wr[K];
   for (int s = 0; s < K; ++s) { wr[s] = md.kw[s * md.cap + i]; W += wr[s]; }
@@ -60,8 +78,8 @@ __device__ __noinline__ void assoc_fp64(const AsmPointsArgs& a, int64_t i, const
   if (!(W > 0)) return;
   double xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
   for (int s = 0; s < K; ++s) {
-    const double* Rt = a.nd.Rt64 + 12 * nodes[s];
-    const float* g = a.nd.g + 3 * nodes[s];
+    const double* Rt = ndv.Rt64 + 12 * nodes[s];
+    const float* g = ndv.g + 3 * nodes[s];
     const double wn = wr[s] / W;
     double d[3] = {v[0] - g[0], v[1] - g[1], v[2] - g[2]};
     for (int r = 0; r < 3; ++r) {
@@ -123,9 +141,6 @@ template <int K, bool DBG>
 __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, bool act, const float* __restrict__ ND,
                                           const int32_t* nodes, float* __restrict__ row) {
   using L = Lay<K>;
-  float f[L::FS];
-#pragma unroll
-  for (int c = 0; c < L::FS; ++c) f[c] = 0.f;
   bool assoc = false;
   int pix = -1;
   uint8_t why = 0;
@@ -199,7 +214,23 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
           }
         }
       }
-      if (guard) assoc_fp64<K>(a, i, nodes, vt, q, N, &pix, &why);
+      if (guard) {
+        Fp64Args fa;
+        fa.px = md.px; fa.py = md.py; fa.pz = md.pz; fa.nx = md.nx; fa.ny = md.ny; fa.nz = md.nz; fa.kw = md.kw;
+        fa.cap = md.cap;
+        fa.Rt64 = a.nd.Rt64;
+        fa.g = a.nd.g;
+        fa.depth = fr.depth;
+        fa.W = fr.W; fa.H = fr.H;
+        fa.fxd = fr.fxd; fa.fyd = fr.fyd; fa.cxd = fr.cxd; fa.cyd = fr.cyd;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) fa.Rd[k] = fr.Rd[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) fa.Td[k] = fr.Td[k];
+        fa.eps_dd = a.eps_dd;
+        fa.cos_eps_nd = a.cos_eps_nd;
+        assoc_fp64<K>(&fa, i, nodes, vt, q, N, &pix, &why);
+      }
       assoc = (pix >= 0);
       if (assoc) {
         const float e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
@@ -210,60 +241,85 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
         const float rp0 = R[0] * e0 + R[3] * e1 + R[6] * e2;               // r' = R^T (v~ - q)
         const float rp1 = R[1] * e0 + R[4] * e1 + R[7] * e2;
         const float rp2 = R[2] * e0 + R[5] * e1 + R[8] * e2;
+        // the factor row, straight to shared memory (8-byte / 16-byte stores)
 #pragma unroll
         for (int s = 0; s < K; ++s) {
-          f[6 * s + 0] = wn[s] * (ay[s] * np2 - az[s] * np1);   // w_j (a_j x n')
-          f[6 * s + 1] = wn[s] * (az[s] * np0 - ax[s] * np2);
-          f[6 * s + 2] = wn[s] * (ax[s] * np1 - ay[s] * np0);
-          f[6 * s + 3] = wn[s] * np0;
-          f[6 * s + 4] = wn[s] * np1;
-          f[6 * s + 5] = wn[s] * np2;
-          f[L::CDP + 4 * s + 0] = wn[s] * ax[s];
-          f[L::CDP + 4 * s + 1] = wn[s] * ay[s];
-          f[L::CDP + 4 * s + 2] = wn[s] * az[s];
-          f[L::CDP + 4 * s + 3] = wn[s];
+          float2* c2 = reinterpret_cast<float2*>(row + 6 * s);
+          c2[0] = make_float2(wn[s] * (ay[s] * np2 - az[s] * np1), wn[s] * (az[s] * np0 - ax[s] * np2));  // w_j (a_j x n')
+          c2[1] = make_float2(wn[s] * (ax[s] * np1 - ay[s] * np0), wn[s] * np0);
+          c2[2] = make_float2(wn[s] * np1, wn[s] * np2);
+          *reinterpret_cast<float4*>(row + L::CDP + 4 * s) = make_float4(wn[s] * ax[s], wn[s] * ay[s], wn[s] * az[s], wn[s]);
         }
-        f[6 * K] = rpl;
-        f[L::CDP + 4 * K + 0] = rp0;
-        f[L::CDP + 4 * K + 1] = rp1;
-        f[L::CDP + 4 * K + 2] = rp2;
+        row[6 * K] = rpl;
+#pragma unroll
+        for (int c = 6 * K + 1; c < L::CDP; ++c) row[c] = 0.f;
+        row[L::CDP + 4 * K + 0] = rp0;
+        row[L::CDP + 4 * K + 1] = rp1;
+        row[L::CDP + 4 * K + 2] = rp2;
+#pragma unroll
+        for (int c = L::CDP + 4 * K + 3; c < L::FS; ++c) row[c] = 0.f;
       }
     }
     if (DBG) { a.dbg_pix[i] = pix; a.dbg_why[i] = why; }
   }
-  float4* r4 = reinterpret_cast<float4*>(row);
+  if (!assoc) {
+    float4* r4 = reinterpret_cast<float4*>(row);
 #pragma unroll
-  for (int c = 0; c < L::FS / 4; ++c) r4[c] = make_float4(f[4 * c], f[4 * c + 1], f[4 * c + 2], f[4 * c + 3]);
+    for (int c = 0; c < L::FS / 4; ++c) r4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   return assoc;
 }
 
 template <int K, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32) k_assemble_points(AsmPointsArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 2) k_assemble_points(AsmPointsArgs a) {
   using L = Lay<K>;
+  constexpr int P = L::P;
+  constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
   extern __shared__ float4 smem4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* F = reinterpret_cast<float*>(smem4) + warp * (32 * L::FSP + 16 * K);
   float* ND = F + 32 * L::FSP;
 
-  // static ownership of 4x4 tiles of the two upper triangles
-  int offA[L::R], offB[L::R], tI[L::R], tJ[L::R];
-  bool tE[L::R], tV[L::R];
+  // tile table of the two upper triangles: (I, J) in units of 4 entries
+  __shared__ uint8_t tabI[L::NT], tabJ[L::NT];
+  // record permutation: perm[d] = tile-dump index feeding record float d (-1: zero)
+  __shared__ int16_t perm[RS];
+  for (int t = threadIdx.x; t < L::NT; t += blockDim.x) {
+    const bool e = t >= L::TD;
+    const int nb = e ? L::NE : L::ND;
+    int u = e ? t - L::TD : t, I = 0;
+    while (u >= nb - I) { u -= nb - I; ++I; }
+    tabI[t] = (uint8_t)I;
+    tabJ[t] = (uint8_t)(I + u);
+  }
+  for (int d = threadIdx.x; d < RS; d += blockDim.x) perm[d] = -1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < 16 * L::NT; q += blockDim.x) {
+    const int t = q >> 4, A = 4 * tabI[t] + ((q >> 2) & 3), B = 4 * tabJ[t] + (q & 3);
+    if (A > B) continue;
+    int d = -1;
+    if (t < L::TD) {             // c' = [w_j u_j ..., r_pl]
+      if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
+      else if (B == 6 * K && A < 6 * K) d = 52 * P + 18 * (A / 6) + (A % 6);
+      else if (B == 6 * K && A == 6 * K) d = 52 * P + 18 * K;
+    } else {                     // e' = [w_j a_j, w_j ..., r']
+      if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
+      else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 18 * (A / 4) + 6 + 3 * (A % 4) + (B - 4 * K);
+      else if (B < 4 * K + 3 && A == B) d = 52 * P + 18 * K + 1 + (A - 4 * K);
+    }
+    if (d >= 0) perm[d] = (int16_t)q;
+  }
+  __syncthreads();
+  // static ownership: lane owns tiles lane, lane + 32, ...
+  int offA[L::R], offB[L::R];
+  bool tV[L::R];
 #pragma unroll
   for (int r = 0; r < L::R; ++r) {
-    int t = lane + 32 * r;
+    const int t = lane + 32 * r;
     tV[r] = t < L::NT;
-    tE[r] = t >= L::TD;
-    int nb = tE[r] ? L::NE : L::ND;
-    int u = tE[r] ? t - L::TD : t;
-    int I = 0;
-    if (tV[r]) {
-      while (u >= nb - I) { u -= nb - I; ++I; }
-    }
-    tI[r] = I;
-    tJ[r] = I + u;
-    const int base = tE[r] ? L::CDP : 0;
-    offA[r] = tV[r] ? base + 4 * tI[r] : 0;
-    offB[r] = tV[r] ? base + 4 * tJ[r] : 0;
+    const int base = (t >= L::TD) ? L::CDP : 0;
+    offA[r] = tV[r] ? base + 4 * tabI[t] : 0;
+    offB[r] = tV[r] ? base + 4 * tabJ[t] : 0;
   }
 
   const int64_t nw = (int64_t)gridDim.x * kWarps;
@@ -291,6 +347,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_assemble_points(AsmPointsArgs a
         if (!tV[r]) continue;
         const float* pa = F + offA[r];
         const float* pb = F + offB[r];
+#pragma unroll 4
         for (int p = 0; p < np; ++p) {
           const float4 A = *reinterpret_cast<const float4*>(pa + p * L::FSP);
           const float4 B = *reinterpret_cast<const float4*>(pb + p * L::FSP);
@@ -303,59 +360,93 @@ __global__ void __launch_bounds__(kWarps * 32) k_assemble_points(AsmPointsArgs a
       }
       __syncwarp();
     }
-    // ---- commit: one atomic per triangle entry per chunk
-    const int32_t* slots = a.seg_slot + (int64_t)seg * L::P;
-    float eD = 0.f, eP = 0.f;
+    // ---- commit: tiles -> shared memory -> the chunk's record (coalesced, no atomics)
 #pragma unroll
     for (int r = 0; r < L::R; ++r) {
       if (!tV[r]) continue;
+      float4* d4 = reinterpret_cast<float4*>(F + 16 * (lane + 32 * r));
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          const int A = 4 * tI[r] + x, B = 4 * tJ[r] + y;
-          if (A > B) continue;
-          const float val = acc[r][4 * x + y];
-          if (!tE[r]) {
-            if (B < 6 * K) {
-              if (val != 0.f) {
-                const int slot = slots[pair_index(A / 6, B / 6, K)];
-                atomicAdd(a.acc.data + (int64_t)slot * 36 + (A % 6) * 6 + (B % 6), val);
-              }
-            } else if (B == 6 * K) {
-              if (A < 6 * K) {
-                if (val != 0.f) atomicAdd(a.acc.rhs_data + 6 * nodes[A / 6] + (A % 6), val);
-              } else {
-                eD += val;
-              }
-            }
-          } else {
-            if (B < 4 * K) {
-              if (val != 0.f) {
-                const int slot = slots[pair_index(A / 4, B / 4, K)];
-                atomicAdd(a.acc.mom + (int64_t)slot * 16 + (A % 4) * 4 + (B % 4), val);
-              }
-            } else if (B < 4 * K + 3) {
-              if (A < 4 * K) {
-                if (val != 0.f) atomicAdd(a.acc.node_mom + 12 * nodes[A / 4] + (A % 4) * 3 + (B - 4 * K), val);
-              } else if (A == B) {
-                eP += val;
-              }
-            }
-          }
-        }
+      for (int x = 0; x < 4; ++x) d4[x] = make_float4(acc[r][4 * x], acc[r][4 * x + 1], acc[r][4 * x + 2], acc[r][4 * x + 3]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      eD += __shfl_xor_sync(0xffffffffu, eD, o);
-      eP += __shfl_xor_sync(0xffffffffu, eP, o);
+    __syncwarp();
+    float* rec = a.records + c * (int64_t)RS;
+    for (int d = lane; d < RS; d += 32) {
+      const int q = perm[d];
+      rec[d] = q >= 0 ? F[q] : 0.f;
     }
-    if (lane == 0) {
-      atomicAdd(a.acc.energy + 0, (double)eD);
-      atomicAdd(a.acc.energy + 1, (double)eP);
-      atomicAdd(a.acc.energy + 4, (double)n_assoc);
-    }
+    if (lane == 0) rec[52 * P + 18 * K + 4] = (float)n_assoc;
   }
+}
+
+// Deterministic slot-major reduction of the chunk records into the
+// accumulator layout read by the solvers: one warp per BSR entry (upper
+// entries gather their (chunk, pair) contributions in sorted order), one warp
+// per node (rhs and node moments), then energies.
+__global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int P = r.K * (r.K + 1) / 2;
+  const int RS = r.rec_stride;
+  if (gw < r.nnzb) {
+    const int64_t e = gw;
+    if (r.upper_of[e] != e) return;   // lower-triangle entries mirror their upper partner
+    float v0 = 0.f, v1 = 0.f;         // lane owns record floats lane and lane + 32 (< 52)
+    for (int k = r.slot_ptr[e]; k < r.slot_ptr[e + 1]; ++k) {
+      const int src = r.slot_src[k];
+      const float* rec = r.records + (int64_t)(src / P) * RS + 52 * (src % P);
+      v0 += rec[lane];
+      if (lane < 20) v1 += rec[32 + lane];
+    }
+    // floats 0..35 -> data, 36..51 -> moments
+    if (lane < 32) {
+      if (lane < 36) r.acc.data[36 * e + lane] = v0;
+    }
+    if (lane < 20) {
+      const int f = 32 + lane;
+      if (f < 36) r.acc.data[36 * e + f] = v1;
+      else r.acc.mom[16 * e + (f - 36)] = v1;
+    }
+    return;
+  }
+  const int64_t gn = gw - r.nnzb;
+  if (gn < r.m) {
+    const int n = (int)gn;
+    float v = 0.f;   // lanes 0..17: 6 rhs_data + 12 node moments
+    if (lane < 18)
+      for (int k = r.node_ptr[n]; k < r.node_ptr[n + 1]; ++k) {
+        const int src = r.node_src[k];
+        v += r.records[(int64_t)(src / r.K) * RS + 52 * P + 18 * (src % r.K) + lane];
+      }
+    if (lane < 6) r.acc.rhs_data[6 * n + lane] = v;
+    else if (lane < 18) r.acc.node_mom[12 * n + (lane - 6)] = v;
+    return;
+  }
+  const int64_t c0 = (gn - r.m) * 32;
+  if (c0 >= r.nchunk) return;
+  const int64_t c = c0 + lane;
+  double eD = 0, eP = 0, na = 0;
+  if (c < r.nchunk) {
+    const float* t = r.records + c * RS + 52 * P + 18 * r.K;
+    eD = t[0];
+    eP = (double)t[1] + t[2] + t[3];
+    na = t[4];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    eD += __shfl_xor_sync(0xffffffffu, eD, o);
+    eP += __shfl_xor_sync(0xffffffffu, eP, o);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+  }
+  if (lane == 0) {
+    atomicAdd(r.acc.energy + 0, eD);
+    atomicAdd(r.acc.energy + 1, eP);
+    atomicAdd(r.acc.energy + 4, na);
+  }
+}
+
+void launch_reduce_records(const ReduceArgs& r, cudaStream_t s) {
+  const int64_t warps = r.nnzb + r.m + (r.nchunk + 31) / 32;
+  const int64_t blocks = (warps * 32 + 255) / 256;
+  if (blocks > 0) k_reduce_records<<<(unsigned)blocks, 256, 0, s>>>(r);
 }
 
 template <int K>

@@ -73,11 +73,30 @@ struct AsmPointsArgs {
   FrameView fr;
   float eps_d, cos_eps_n;
   double eps_dd, cos_eps_nd;
-  AccView acc;
+  float* records;             // nchunk x rec_stride per-chunk partial sums (pair-major)
   int32_t* dbg_pix;           // nullable: per point association outputs
   uint8_t* dbg_why;
 };
 void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
+
+// Per-chunk record layout (floats): P pairs x [36 data (6x6, upper for the
+// diagonal pair) | 16 point-to-point moments], K slots x [6 rhs_data | 12
+// node moments], tail [E_data, E_pt x, E_pt y, E_pt z, n_assoc]; padded to 4.
+__host__ __device__ inline int rec_stride(int K) { return (52 * (K * (K + 1) / 2) + 18 * K + 5 + 3) & ~3; }
+
+struct ReduceArgs {
+  const float* records;
+  int rec_stride, K;
+  int64_t nchunk, nnzb;
+  int m;
+  const int32_t* upper_of;
+  const int32_t* slot_ptr;    // nnzb+1: contributions to each entry (upper entries only)
+  const int32_t* slot_src;    // (chunk * P + pair)
+  const int32_t* node_ptr;    // m+1
+  const int32_t* node_src;    // (chunk * K + slot)
+  AccView acc;
+};
+void launch_reduce_records(const ReduceArgs& r, cudaStream_t s);
 
 struct AsmGraphArgs {
   NodeView nd;
@@ -118,8 +137,25 @@ struct SolveArgs {
   double* rep_nassoc;         // MIS_MAX_GN+1
   float* rep_res;             // MIS_MAX_GN
   int* numeric_flag;
+  // cluster-resident variant (pcg_cluster.cu); cluster_size == 0 -> grid variant
+  int cluster_size;
+  const int32_t* part;        // cluster_size+1 row boundaries (balanced by nnz)
+  int max_rows, max_nnz;      // per-CTA maxima (uniform smem layout)
+  size_t smem_bytes;
+  int write_global;           // also write Hval / rhs to global memory (debug)
+  unsigned long long* tstamp; // 8 %globaltimer stamps of the phases (rank 0, thread 0)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
+// host: pick the cluster partition; returns 0 if the system does not fit
+int plan_cluster(const int32_t* row_ptr_host, int m, int max_cluster, int32_t* part_host, int* max_rows,
+                 int* max_nnz, size_t* smem_bytes);
 void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr,
                           int slot, double* rep_energy, double* rep_nassoc, cudaStream_t s);
 

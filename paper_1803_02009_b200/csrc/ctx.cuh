@@ -51,8 +51,16 @@ struct Ctx {
   int64_t nnzb = 0, ncand = 0;
   bool pattern_valid = false;
   DBuf ckeys, ckeys2, uflag, upos, ukeys, row_ptr, col, diag_pos, upper_of, seg_slot, edge_slot, feat_slot, nnz_dev;
+  // per-chunk records and their contribution lists (deterministic reduction)
+  DBuf records, ck_key, ck_val, ck_key2, ck_val2, slot_ptr, slot_src, node_ptr, node_src;
 
   // ---- system and solver
+  int cl_size = 0, cl_max_rows = 0, cl_max_nnz = 0;   // cluster-resident PCG plan (0: grid variant)
+  size_t cl_smem = 0;
+  bool cluster_ok = true;
+  std::string solver_note;
+  int last_solver = 0;   // cluster size of the last PCG launch (0: grid kernel)
+  DBuf part, tstamp;
   size_t acc_floats = 0;
   DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots, numeric_flag;
 
@@ -86,7 +94,8 @@ struct Ctx {
   int64_t prof_n[MIS_PROF_NCAT] = {0};
 };
 
-enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO };
+enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO,
+       P_REDUCE };
 void count_launches(int64_t k);
 
 // Records an event pair around a group of `nk` kernel launches on the context

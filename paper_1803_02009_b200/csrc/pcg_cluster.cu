@@ -1,0 +1,317 @@
+// pcg_cluster.cu -- K6-K8, cluster-resident variant.  One thread-block
+// cluster (up to 16 CTAs, one per SM, 1024 threads each) owns the whole
+// normal-equation system of a Gauss-Newton iteration: every CTA finalises the
+// 6x6 blocks of its node rows straight from the K3/K4/K5 accumulators into its
+// shared memory (the matrix never round-trips through global memory), builds
+// its block-Jacobi preconditioner, and runs the P PCG iterations with
+//   * the SpMV reading z of other CTAs through distributed shared memory,
+//   * 2 cluster barriers per iteration (A p_{k+1} = A z_{k+1} + beta A p_k),
+//   * dot products reduced per CTA and published to every CTA (DSMEM), summed
+//     in rank order so every CTA sees bit-identical scalars,
+// then updates its nodes (Exp(dtheta) R_j, t_j += dt, fp64).  Used whenever
+// the system fits in the cluster's shared memory (C1-C3); the grid-wide
+// cooperative kernel (solve.cu) handles larger ones.
+#include <cooperative_groups.h>
+
+#include <vector>
+
+#include "solve_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mis {
+
+constexpr int kCT = 1024;          // threads per CTA
+constexpr int kMaxCluster = 16;
+
+struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
+  size_t dots, vec, zf, mi, col, own, h, total;
+  __host__ __device__ CLay(int max_rows, int max_nnz, int m) {
+    dots = 0;                                        // double partA[16], partB[16], partF[16], red[32]
+    vec = dots + sizeof(double) * (3 * kMaxCluster + 32);
+    const size_t nv = (size_t)max_rows * 6;
+    zf = vec + sizeof(float) * 6 * nv;               // x r z p Ap Az, then the replicated full z
+    mi = zf + sizeof(float) * 6 * (size_t)m;
+    col = mi + sizeof(float) * 36 * max_rows;
+    own = col + sizeof(int) * max_nnz;
+    h = (own + sizeof(int) * (max_nnz + 1) + 15) & ~(size_t)15;
+    total = h + sizeof(float) * 36 * (size_t)max_nnz;
+  }
+};
+
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kCT / 32; ++i) s += red[i];
+  return s;   // thread 0
+}
+
+// thread 0 of every CTA writes its partial into slot [rank] of `slot` in all CTAs
+__device__ __forceinline__ void publish(cg::cluster_group& cl, double* slot, double v, int rank, int cs) {
+  if (threadIdx.x == 0)
+    for (int c = 0; c < cs; ++c) cl.map_shared_rank(slot, c)[rank] = v;
+}
+
+// push this CTA's z slice into every CTA's full-length copy (remote stores,
+// made visible by the following cluster barrier)
+__device__ __forceinline__ void replicate(cg::cluster_group& cl, float* zf, const float* z, int r0, int nr, int cs) {
+  const int n = 3 * nr;   // float2 units (6 r0 floats = 24 r0 bytes: 8-byte aligned)
+  const float2* z2 = reinterpret_cast<const float2*>(z);
+  for (int w = threadIdx.x; w < n * cs; w += kCT) {
+    const int d = w / n, q = w - d * n;
+    reinterpret_cast<float2*>(cl.map_shared_rank(zf, d) + 6 * r0)[q] = z2[q];
+  }
+}
+
+__device__ __forceinline__ double gather_sum(const double* slot, int cs) {
+  double s = 0;
+  for (int c = 0; c < cs; ++c) s += slot[c];
+  return s;
+}
+
+__global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char sm[];
+  const CLay L(a.max_rows, a.max_nnz, a.m);
+  double* partA = reinterpret_cast<double*>(sm + L.dots);
+  double* partB = partA + kMaxCluster;
+  double* partF = partB + kMaxCluster;
+  double* red = partF + kMaxCluster;
+  const int nv = a.max_rows * 6;
+  float* x = reinterpret_cast<float*>(sm + L.vec);
+  float* r = x + nv;
+  float* z = r + nv;
+  float* p = z + nv;
+  float* Ap = p + nv;
+  float* Az = Ap + nv;
+  float* zf = reinterpret_cast<float*>(sm + L.zf);   // every CTA's copy of the full z
+  float* Mi = reinterpret_cast<float*>(sm + L.mi);
+  int* col = reinterpret_cast<int*>(sm + L.col);
+  int* lrp = reinterpret_cast<int*>(sm + L.own);   // local row pointers (nr + 1)
+  float* H = reinterpret_cast<float*>(sm + L.h);
+
+  const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  const int r0 = a.part[rank], r1 = a.part[rank + 1], nr = r1 - r0;
+  const int e0 = a.row_ptr[r0], e1 = a.row_ptr[r1], ne = e1 - e0;
+  const int t = threadIdx.x;
+  const bool stamp = a.tstamp && t == 0;
+  unsigned long long* ts = a.tstamp + 16 * rank;
+  if (stamp) ts[0] = gtimer();
+
+  // ---- phase 0: local rows of H (from the accumulators), b, column owners
+  __shared__ int spart[kMaxCluster + 1];
+  if (t <= cs) spart[t] = a.part[t];
+  for (int i = t; i <= nr; i += kCT) lrp[i] = a.row_ptr[r0 + i] - e0;
+  __syncthreads();
+  for (int k = t; k < ne; k += kCT) {
+    const int e = e0 + k;
+    const int c = a.col[e];
+    col[k] = c;
+    const int64_t u = a.upper_of[e];
+    float B[36];
+    upper_block(a.acc, a.w_data, a.w_pt, u, a.diag_pos[c] == e, B);
+    float* out = H + 36 * (size_t)k;
+    if (u == e) {
+      for (int i = 0; i < 36; ++i) out[i] = B[i];
+    } else {
+      for (int rr = 0; rr < 6; ++rr)
+        for (int cc = 0; cc < 6; ++cc) out[6 * rr + cc] = B[6 * cc + rr];
+    }
+    if (a.write_global)
+      for (int i = 0; i < 36; ++i) a.Hval[36 * (int64_t)e + i] = out[i];
+  }
+  for (int i = t; i < 6 * nr; i += kCT) {
+    const float b = rhs_entry(a.acc, a.w_data, a.w_pt, 6 * (int64_t)r0 + i);
+    r[i] = b;
+    x[i] = 0.f;
+    p[i] = 0.f;
+    Ap[i] = 0.f;
+    if (a.write_global) a.rhs[6 * (int64_t)r0 + i] = b;
+  }
+  __syncthreads();
+  if (stamp) ts[1] = gtimer();
+  if (a.pcg_iters <= 0 && !a.do_update) return;
+
+  // ---- phase 1: block-Jacobi preconditioner, z = M r, r.z
+  for (int i = t; i < nr; i += kCT) precond_block(H + 36 * (size_t)(a.diag_pos[r0 + i] - e0), a.lambda, Mi + 36 * i);
+  __syncthreads();
+  if (stamp) ts[2] = gtimer();
+  double my = 0.0;
+  for (int q = t; q < 6 * nr; q += kCT) {
+    const int i = q / 6, c = q % 6;
+    float zz = 0.f;
+    for (int b = 0; b < 6; ++b) zz = fmaf(Mi[36 * i + 6 * c + b], r[6 * i + b], zz);
+    z[q] = zz;
+    my += (double)r[q] * (double)zz;
+  }
+  __syncthreads();
+  replicate(cl, zf, z, r0, nr, cs);
+  if (stamp) ts[6] = gtimer();
+  double s = cta_sum(my, red);
+  publish(cl, partA, s, rank, cs);
+  if (stamp) ts[7] = gtimer();
+  cl.sync();
+  double rz = gather_sum(partA, cs), rz_prev = 1.0;
+  const double rz0 = rz;
+  if (stamp) ts[3] = gtimer();
+  int done = 0;
+  const int n_items = 12 * nr, passes = (n_items + kCT - 1) / kCT;
+  for (int it = 0; it < a.pcg_iters && !done; ++it) {
+    if (rz == 0.0) break;
+    const bool st1 = stamp && it == 1;
+    if (st1) ts[8] = gtimer();
+    const float beta = it == 0 ? 0.f : (float)(rz / rz_prev);
+    // Az = (H + lambda I) z: two threads per (row, component) split the row's blocks,
+    // reading the replicated z from local shared memory, pair-reduced by shuffle
+    for (int ps = 0; ps < passes; ++ps) {
+      const int item = t + ps * kCT;
+      const bool act = item < n_items;
+      const int i = item / 12, c = (item % 12) >> 1, hf = item & 1;
+      float v = 0.f;
+      if (act) {
+        for (int k = lrp[i] + hf; k < lrp[i + 1]; k += 2) {
+          const float* zr = zf + 6 * col[k];
+          const float* h = H + 36 * (size_t)k + 6 * c;
+#pragma unroll
+          for (int b = 0; b < 6; ++b) v = fmaf(h[b], zr[b], v);
+        }
+      }
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      if (act && hf == 0) Az[6 * i + c] = fmaf(a.lambda, z[6 * i + c], v);
+    }
+    __syncthreads();
+    if (st1) ts[9] = gtimer();
+    my = 0.0;
+    for (int q = t; q < 6 * nr; q += kCT) {
+      const float pn = fmaf(beta, p[q], z[q]);
+      const float apn = fmaf(beta, Ap[q], Az[q]);
+      p[q] = pn;
+      Ap[q] = apn;
+      my += (double)pn * (double)apn;
+    }
+    s = cta_sum(my, red);
+    publish(cl, partB, s, rank, cs);
+    if (st1) ts[10] = gtimer();
+    cl.sync();   // (B) p.Ap known everywhere; every CTA is done reading z
+    if (st1) ts[11] = gtimer();
+    const double pAp = gather_sum(partB, cs);
+    if (!(pAp > 0.0)) { done = 1; break; }
+    const float alpha = (float)(rz / pAp);
+    for (int q = t; q < 6 * nr; q += kCT) {
+      x[q] = fmaf(alpha, p[q], x[q]);
+      r[q] = fmaf(-alpha, Ap[q], r[q]);
+    }
+    __syncthreads();
+    my = 0.0;
+    for (int q = t; q < 6 * nr; q += kCT) {
+      const int i = q / 6, c = q % 6;
+      float zz = 0.f;
+      for (int b = 0; b < 6; ++b) zz = fmaf(Mi[36 * i + 6 * c + b], r[6 * i + b], zz);
+      z[q] = zz;
+      my += (double)r[q] * (double)zz;
+    }
+    __syncthreads();
+    if (st1) ts[12] = gtimer();
+    replicate(cl, zf, z, r0, nr, cs);
+    s = cta_sum(my, red);
+    publish(cl, partA, s, rank, cs);
+    if (st1) ts[13] = gtimer();
+    cl.sync();   // (A) r.z known everywhere; z complete and replicated
+    if (st1) ts[14] = gtimer();
+    rz_prev = rz;
+    rz = gather_sum(partA, cs);
+  }
+  if (stamp) ts[4] = gtimer();
+  if (rank == 0 && t == 0) a.rep_res[a.gn_it] = (float)(rz0 > 0 ? sqrt(fabs(rz / rz0)) : 0.0);
+  if (a.write_global)
+    for (int q = t; q < 6 * nr; q += kCT) a.x[6 * (int64_t)r0 + q] = x[q];
+  if (!a.do_update) {
+    cl.sync();   // no CTA may exit while others still read its shared memory
+    return;
+  }
+  // ---- node update; a non-finite step anywhere rolls the whole update back
+  my = 0.0;
+  for (int q = t; q < 6 * nr; q += kCT)
+    if (!isfinite(x[q])) my = 1.0;
+  s = cta_sum(my, red);
+  publish(cl, partF, s, rank, cs);
+  cl.sync();
+  if (gather_sum(partF, cs) != 0.0) {
+    if (rank == 0 && t == 0) atomicOr(a.numeric_flag, 1);
+    return;
+  }
+  if (*a.numeric_flag) return;   // sticky from an earlier iteration
+  for (int i = t; i < nr; i += kCT) {
+    const int j = r0 + i;
+    node_update(x + 6 * i, a.nd.Rt64 + 12 * (int64_t)j, a.nd.node32 + 16 * (int64_t)j);
+  }
+  if (stamp) ts[5] = gtimer();
+}
+
+int plan_cluster(const int32_t* row_ptr, int m, int max_cluster, int32_t* part, int* max_rows, int* max_nnz,
+                 size_t* smem_bytes) {
+  int cs = max_cluster < m ? max_cluster : m;
+  if (cs > kMaxCluster) cs = kMaxCluster;
+  if (cs < 1) return 0;
+  const int64_t nnz = row_ptr[m];
+  part[0] = 0;
+  int row = 0;
+  for (int c = 1; c < cs; ++c) {   // boundaries balancing nnz + rows
+    const int64_t target = (nnz * c) / cs;
+    while (row < m && row_ptr[row] < target) ++row;
+    if (row <= part[c - 1]) row = part[c - 1] + 1;
+    if (row > m - (cs - c)) row = m - (cs - c);
+    part[c] = row;
+  }
+  part[cs] = m;
+  int mr = 0, mn = 0;
+  for (int c = 0; c < cs; ++c) {
+    const int nr = part[c + 1] - part[c];
+    const int nz = row_ptr[part[c + 1]] - row_ptr[part[c]];
+    mr = nr > mr ? nr : mr;
+    mn = nz > mn ? nz : mn;
+  }
+  CLay L(mr, mn, m);
+  *max_rows = mr;
+  *max_nnz = mn;
+  *smem_bytes = L.total;
+  if (L.total > 226 * 1024) return 0;   // 227 KB per CTA minus the static shared memory
+  return cs;
+}
+
+cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {
+  static size_t smem_set = 0;
+  static bool nonportable = false;
+  cudaError_t e;
+  if (!nonportable) {
+    if ((e = cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return e;
+    nonportable = true;
+  }
+  if (a.smem_bytes > smem_set) {
+    if ((e = cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem_bytes)) !=
+        cudaSuccess)
+      return e;
+    smem_set = a.smem_bytes;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.cluster_size);
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = a.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)a.cluster_size;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_pcg_cluster, a);
+}
+
+}  // namespace mis

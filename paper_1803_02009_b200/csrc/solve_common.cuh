@@ -1,0 +1,129 @@
+// solve_common.cuh -- device helpers shared by the two PCG kernels (solve.cu:
+// grid-wide cooperative variant; pcg_cluster.cu: thread-block-cluster variant
+// with the system resident in shared memory).
+#pragma once
+#include "common.cuh"
+
+namespace mis {
+
+__device__ __forceinline__ void skew_into(float* M, int r0, int c0, const float* v, float s) {
+  // M[r0.., c0..] += s [v]x   (6x6 row-major)
+  M[6 * (r0 + 0) + c0 + 1] += -s * v[2];
+  M[6 * (r0 + 0) + c0 + 2] += s * v[1];
+  M[6 * (r0 + 1) + c0 + 0] += s * v[2];
+  M[6 * (r0 + 1) + c0 + 2] += -s * v[0];
+  M[6 * (r0 + 2) + c0 + 0] += -s * v[1];
+  M[6 * (r0 + 2) + c0 + 1] += s * v[0];
+}
+
+// Block (j, l), j <= l, of H from the accumulators of upper slot u:
+//   H = w_data sum c c^T + w_pt PT(moments) + graph (K4/K5, already weighted),
+//   PT = [tr(S) I - S^T, [s_j]x ; -[s_l]x, s0 I]  with S = sum s a_j a_l^T,
+//   s_j = sum s a_j, s_l = sum s a_l, s0 = sum s, s = w_j w_l (point-to-point).
+__device__ __forceinline__ void upper_block(const AccView& acc, float w_data, float w_pt, int64_t u, bool diag,
+                                            float* B) {
+  const float* D = acc.data + 36 * u;
+  const float* Mo = acc.mom + 16 * u;
+  const float* G = acc.graph + 36 * u;
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      const float d = diag ? D[6 * min(r, c) + max(r, c)] : D[6 * r + c];
+      B[6 * r + c] = w_data * d + G[6 * r + c];
+    }
+  float S[9], sj[3], sl[3];
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) S[3 * p + q] = diag ? Mo[4 * min(p, q) + max(p, q)] : Mo[4 * p + q];
+  for (int p = 0; p < 3; ++p) { sj[p] = Mo[4 * p + 3]; sl[p] = diag ? Mo[4 * p + 3] : Mo[12 + p]; }
+  const float s0 = Mo[15];
+  const float tr = S[0] + S[4] + S[8];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) B[6 * r + c] += w_pt * ((r == c ? tr : 0.f) - S[3 * c + r]);
+  skew_into(B, 0, 3, sj, w_pt);
+  skew_into(B, 3, 0, sl, -w_pt);
+  for (int r = 0; r < 3; ++r) B[6 * (3 + r) + 3 + r] += w_pt * s0;
+}
+
+// b_i = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs
+__device__ __forceinline__ float rhs_entry(const AccView& acc, float w_data, float w_pt, int64_t i) {
+  const int64_t j = i / 6;
+  const int c = (int)(i % 6);
+  const float* Nm = acc.node_mom + 12 * j;
+  float pt;
+  if (c < 3) {
+    const int c1 = (c + 1) % 3, c2 = (c + 2) % 3;   // (sum w a x r')_c = Nm[c1][c2] - Nm[c2][c1]
+    pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
+  } else {
+    pt = Nm[9 + (c - 3)];
+  }
+  return -w_data * acc.rhs_data[i] - w_pt * pt + acc.rhs_graph[i];
+}
+
+// 6x6 SPD inverse in fp64 via Cholesky; false if not positive definite
+__device__ inline bool inv6(const double* A, double* Ai) {
+  double L[36];
+  for (int i = 0; i < 36; ++i) L[i] = A[i];
+  for (int j = 0; j < 6; ++j) {
+    double s = L[6 * j + j];
+    for (int k = 0; k < j; ++k) s -= L[6 * j + k] * L[6 * j + k];
+    if (!(s > 0)) return false;
+    const double d = sqrt(s);
+    L[6 * j + j] = d;
+    for (int i = j + 1; i < 6; ++i) {
+      double t = L[6 * i + j];
+      for (int k = 0; k < j; ++k) t -= L[6 * i + k] * L[6 * j + k];
+      L[6 * i + j] = t / d;
+    }
+  }
+  for (int c = 0; c < 6; ++c) {
+    double y[6], x[6];
+    for (int i = 0; i < 6; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[6 * i + k] * y[k];
+      y[i] = s / L[6 * i + i];
+    }
+    for (int i = 5; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < 6; ++k) s -= L[6 * k + i] * x[k];
+      x[i] = s / L[6 * i + i];
+    }
+    for (int r = 0; r < 6; ++r) Ai[6 * r + c] = x[r];
+  }
+  return true;
+}
+
+// M_j = (H_jj + lambda I + mu_j I)^-1, mu_j = 1e-9 tr(H_jj)/6 (reading A17); 0 if not PD
+__device__ inline void precond_block(const float* Hjj, float lambda, float* Mi) {
+  double A[36], Ai[36], tr = 0;
+  for (int i = 0; i < 36; ++i) A[i] = Hjj[i];
+  for (int i = 0; i < 6; ++i) tr += A[7 * i];
+  const double mu = 1e-9 * tr / 6.0;
+  for (int i = 0; i < 6; ++i) A[7 * i] += (double)lambda + mu;
+  if (!inv6(A, Ai))
+    for (int i = 0; i < 36; ++i) Ai[i] = 0.0;
+  for (int i = 0; i < 36; ++i) Mi[i] = (float)Ai[i];
+}
+
+// R_j <- Exp(dtheta) R_j (Rodrigues, theta < 1e-12 first order), t_j += dt (reading A18)
+__device__ inline void node_update(const float* dx, double* Rt, float* n32) {
+  const double w0 = dx[0], w1 = dx[1], w2 = dx[2];
+  const double th = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+  const double K[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+  double K2[9];
+  for (int i = 0; i < 3; ++i)
+    for (int jj = 0; jj < 3; ++jj) K2[3 * i + jj] = K[3 * i] * K[jj] + K[3 * i + 1] * K[3 + jj] + K[3 * i + 2] * K[6 + jj];
+  double A, Bc;
+  if (th < 1e-12) { A = 1.0; Bc = 0.0; }
+  else { A = sin(th) / th; Bc = (1.0 - cos(th)) / (th * th); }
+  double E[9];
+  for (int i = 0; i < 9; ++i) E[i] = ((i % 4) == 0 ? 1.0 : 0.0) + A * K[i] + Bc * K2[i];
+  double Rn[9];
+  for (int i = 0; i < 3; ++i)
+    for (int jj = 0; jj < 3; ++jj) Rn[3 * i + jj] = E[3 * i] * Rt[jj] + E[3 * i + 1] * Rt[3 + jj] + E[3 * i + 2] * Rt[6 + jj];
+  for (int i = 0; i < 9; ++i) { Rt[i] = Rn[i]; n32[i] = (float)Rn[i]; }
+  for (int c = 0; c < 3; ++c) {
+    Rt[9 + c] += (double)dx[3 + c];
+    n32[9 + c] = (float)Rt[9 + c];
+  }
+}
+
+}  // namespace mis

@@ -268,6 +268,48 @@ __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, in
   }
 }
 
+// contributions of the chunk records: (key = BSR slot or node, value = chunk * W + position)
+__global__ void k_contrib(int64_t nchunk, const int4* chunks, const int32_t* table, int W, int32_t* key,
+                          int32_t* val) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nchunk * W) return;
+  const int64_t c = t / W;
+  const int p = (int)(t % W);
+  key[t] = table[(int64_t)chunks[c].x * W + p];
+  val[t] = (int32_t)t;
+}
+
+// CSR row pointers over nbins from sorted keys
+__global__ void k_csr_ptr(int64_t n, const int32_t* key, int nbins, int32_t* ptr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = key[i];
+  const int kp = (i == 0) ? -1 : key[i - 1];
+  for (int b = kp + 1; b <= k; ++b) ptr[b] = (int32_t)i;
+  if (i == n - 1)
+    for (int b = k + 1; b <= nbins; ++b) ptr[b] = (int32_t)n;
+}
+
+static cudaError_t build_contrib(Ctx* c, const int32_t* table, int W, int nbins, DBuf& ptr, DBuf& src) {
+  const int64_t n = c->nchunk * W;
+  CK(ensure(c, ptr, (size_t)(nbins + 1) * 4));
+  CK(ensure(c, src, (size_t)n * 4 + 16));
+  if (n == 0) return cudaMemsetAsync(ptr.p, 0, (size_t)(nbins + 1) * 4, c->st);
+  CK(ensure(c, c->ck_key, n * 4)); CK(ensure(c, c->ck_val, n * 4));
+  CK(ensure(c, c->ck_key2, n * 4));
+  const int b = (int)((n + 255) / 256);
+  k_contrib<<<b, 256, 0, c->st>>>(c->nchunk, c->chunks.as<int4>(), table, W, c->ck_key.as<int32_t>(),
+                                  c->ck_val.as<int32_t>());
+  int bits = 1;
+  while ((1ll << bits) <= (int64_t)nbins) ++bits;
+  CK(cub_call(c, [&](void* t, size_t& s) {
+    return cub::DeviceRadixSort::SortPairs(t, s, c->ck_key.as<int32_t>(), c->ck_key2.as<int32_t>(),
+                                           c->ck_val.as<int32_t>(), src.as<int32_t>(), (int)n, 0, bits, c->st);
+  }));
+  k_csr_ptr<<<b, 256, 0, c->st>>>(n, c->ck_key2.as<int32_t>(), nbins, ptr.as<int32_t>());
+  return cudaGetLastError();
+}
+
 cudaError_t build_pattern(Ctx* c) {
   const int K = c->K, P = K * (K + 1) / 2;
   const int64_t total = c->nseg * P + (int64_t)c->m * c->prm.n_nbr + (int64_t)c->nf * P + c->m;
@@ -328,6 +370,18 @@ cudaError_t build_pattern(Ctx* c) {
   const int bn = (int)((nnz + 255) / 256);
   k_rows<<<bn, 256, 0, c->st>>>(nnz, c->ukeys.as<uint64_t>(), c->m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
                                 c->upper_of.as<int32_t>(), c->diag_pos.as<int32_t>());
+  {   // plan of the cluster-resident PCG (host needs the row structure once per pattern)
+    std::vector<int32_t> rp(c->m + 1);
+    CK(cudaMemcpyAsync(rp.data(), c->row_ptr.p, (c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int32_t part[17];
+    c->cl_size = plan_cluster(rp.data(), c->m, 16, part, &c->cl_max_rows, &c->cl_max_nnz, &c->cl_smem);
+    if (c->cl_size) {
+      CK(ensure(c, c->part, 17 * 4));
+      CK(cudaMemcpyAsync(c->part.p, part, (c->cl_size + 1) * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaStreamSynchronize(c->st));   // `part` is a host stack array
+    }
+  }
   CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
   CK(ensure(c, c->edge_slot, ((int64_t)c->m * c->prm.n_nbr + 1) * 4));
   CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
@@ -335,6 +389,10 @@ cudaError_t build_pattern(Ctx* c) {
                                  c->nf, c->fidx.as<int32_t>(), c->ukeys.as<uint64_t>(), nnz, c->seg_slot.as<int32_t>(),
                                  c->edge_slot.as<int32_t>(), c->feat_slot.as<int32_t>(), total);
   CK(cudaGetLastError());
+  // chunk records and their (deterministic, sorted) contribution lists
+  CK(ensure(c, c->records, (size_t)c->nchunk * rec_stride(K) * 4 + 16));
+  CK(build_contrib(c, c->seg_slot.as<int32_t>(), P, (int)nnz, c->slot_ptr, c->slot_src));
+  CK(build_contrib(c, c->seg_nodes.as<int32_t>(), K, c->m, c->node_ptr, c->node_src));
   // accumulators and solver buffers
   const size_t m6 = 6 * (size_t)c->m;
   c->acc_floats = (size_t)nnz * (36 + 16 + 36) + m6 + 12 * (size_t)c->m + m6;

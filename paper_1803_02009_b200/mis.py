@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libmis.so")
 
 MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
-MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH = 1, 2
+MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH, MIS_F_GRID_SOLVER = 1, 2, 4
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
 
@@ -47,7 +47,8 @@ class mis_report(C.Structure):
                 ("energy", (C.c_double * 5) * (MIS_MAX_GN + 1)),
                 ("n_assoc", C.c_int64 * (MIS_MAX_GN + 1)),
                 ("pcg_rel_res", C.c_float * MIS_MAX_GN),
-                ("nnzb", C.c_int64), ("n_segments", C.c_int64)]
+                ("nnzb", C.c_int64), ("n_segments", C.c_int64), ("solver_cluster", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -84,8 +85,9 @@ _sig = {
     "mis_prof_enable": ([_V, C.c_int], C.c_int),
     "mis_prof_read": ([_V, _V, _V, C.c_int], C.c_int),
     "mis_launch_count": ([], C.c_int64),
+    "mis_dbg_solver_phases": ([_V, _V], C.c_int),
 }
-MIS_PROF_NCAT = 12
+MIS_PROF_NCAT = 13
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -211,7 +213,7 @@ def report_dict(rep: mis_report):
                 energy=np.array([[rep.energy[i][q] for q in range(5)] for i in range(it + 1)]),
                 n_assoc=np.array([rep.n_assoc[i] for i in range(it + 1)]),
                 pcg_rel_res=np.array([rep.pcg_rel_res[i] for i in range(it)]),
-                nnzb=rep.nnzb, n_segments=rep.n_segments)
+                nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster)
 
 
 def mis_get_nodes(ctx, out):
@@ -331,6 +333,37 @@ def mis_prof_read(ctx, reset=False):
 
 def mis_launch_count():
     return int(_lib.mis_launch_count())
+
+
+def mis_dbg_solver_phases(ctx):
+    """Microseconds spent in the phases of the last cluster-PCG launch."""
+    t = np.zeros(256, np.uint64)
+    _check(ctx, _lib.mis_dbg_solver_phases(ctx, _ptr(t)))
+    t = t.astype(np.int64).reshape(16, 16)
+    t = t[t[:, 0] > 0]
+    it1 = None
+    if len(t) and (t[:, 14] > 0).all():
+        it1 = {}
+        for n, a_, b_ in [("spmv", 8, 9), ("pAp_sum", 9, 10), ("syncB", 10, 11), ("xr_z", 11, 12),
+                          ("replicate_sum", 12, 13), ("syncA", 13, 14)]:
+            d = (t[:, b_] - t[:, a_]) / 1e3
+            it1[n] = (round(float(d.min()), 2), round(float(d.max()), 2))
+    if len(t) == 0:
+        return {}
+    t0 = t[:, 0].min()
+    names = ["build_system", "precond", "init", "pcg", "update"]
+    out = {}
+    for i, n in enumerate(names):
+        d = (t[:, i + 1] - t[:, i]) / 1e3
+        out[n] = round(float(d.max()), 2)
+        out[n + "_min_cta"] = round(float(d.min()), 2)
+    out["precond_done_spread"] = round(float((t[:, 2].max() - t[:, 2].min()) / 1e3), 2)
+    out["build_done_spread"] = round(float((t[:, 1].max() - t[:, 1].min()) / 1e3), 2)
+    out["start_spread"] = round(float((t[:, 0].max() - t0) / 1e3), 2)
+    out["total"] = round(float((t[:, 5].max() - t0) / 1e3), 2)
+    if it1:
+        out["pcg_iteration_1_us_min_max"] = it1
+    return out
 
 
 class Context:

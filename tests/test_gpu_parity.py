@@ -178,10 +178,13 @@ def rot_err(Ra, Rb):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
-def test_register_parity_mirror(cfg):
+@pytest.mark.parametrize("solver", ["cluster", "grid"])
+def test_register_parity_mirror(cfg, solver):
     sc, pb, fr, _ = scene_problem(cfg)
-    ctx = make_ctx(sc, pb, flags=M.MIS_F_FINAL_ENERGY)
+    flags = M.MIS_F_FINAL_ENERGY | (M.MIS_F_GRID_SOLVER if solver == "grid" else 0)
+    ctx = make_ctx(sc, pb, flags=flags)
     rep = M.report_dict(M.mis_register(ctx.ptr))
+    assert (rep["solver_cluster"] > 0) == (solver == "cluster")
     m = pb.g.shape[0]
     Rg = M.mis_get_nodes_f64(ctx.ptr, m)
     Ro, Eo, nao = O.register(oracle_params(ctx.params), pb, fr)
