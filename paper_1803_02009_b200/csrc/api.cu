@@ -348,7 +348,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
     if (api.CommInitRank(&c->nccl_comm, world, id, rank) != 0) { delete c; return MIS_E_NCCL; }
   }
   if (ensure(c, c->rep_energy, (MIS_MAX_GN + 1) * 5 * 8) != cudaSuccess ||
-      ensure(c, c->rep_nassoc, (MIS_MAX_GN + 1) * 8) != cudaSuccess ||
+      ensure(c, c->rep_nassoc, 2 * (MIS_MAX_GN + 1) * 8) != cudaSuccess ||
       ensure(c, c->rep_res, MIS_MAX_GN * 4) != cudaSuccess || ensure(c, c->numeric_flag, 16) != cudaSuccess ||
       ensure(c, c->tstamp, 2048) != cudaSuccess || cudaMemset(c->tstamp.p, 0, 2048) != cudaSuccess ||
       ensure(c, c->counter, 64) != cudaSuccess) {
@@ -572,6 +572,8 @@ static mis_status assemble(Ctx* c, bool dbg) {
   a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
   a.cos_eps_n = (float)a.cos_eps_nd;
   a.records = c->records.as<float>();
+  a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
+  a.guard_counter = c->energy.as<double>() + 5;
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
   if (a.nchunk > 0) {
@@ -694,7 +696,7 @@ static mis_status prepare(Ctx* c) {
 
 static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
   memset(rep, 0, sizeof(*rep));
-  double e[(MIS_MAX_GN + 1) * 5], na[MIS_MAX_GN + 1];
+  double e[(MIS_MAX_GN + 1) * 5], na[2 * (MIS_MAX_GN + 1)];
   TRY(c, cudaMemcpyAsync(e, c->rep_energy.p, sizeof(e), cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(na, c->rep_nassoc.p, sizeof(na), cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(rep->pcg_rel_res, c->rep_res.p, sizeof(rep->pcg_rel_res), cudaMemcpyDeviceToHost, c->st));
@@ -706,6 +708,7 @@ static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
   for (int i = 0; i <= MIS_MAX_GN; ++i) {
     for (int q = 0; q < 5; ++q) rep->energy[i][q] = e[5 * i + q];
     rep->n_assoc[i] = (int64_t)llround(na[i]);
+    rep->n_guard[i] = (int64_t)llround(na[MIS_MAX_GN + 1 + i]);
   }
   rep->nnzb = c->nnzb;
   rep->n_segments = c->nseg;
@@ -730,7 +733,7 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
   const int G = c->prm.gn_iters;
   TRY(c, cudaMemsetAsync(c->numeric_flag.p, 0, 4, c->st));
   TRY(c, cudaMemsetAsync(c->rep_energy.p, 0, (MIS_MAX_GN + 1) * 5 * 8, c->st));
-  TRY(c, cudaMemsetAsync(c->rep_nassoc.p, 0, (MIS_MAX_GN + 1) * 8, c->st));
+  TRY(c, cudaMemsetAsync(c->rep_nassoc.p, 0, 2 * (MIS_MAX_GN + 1) * 8, c->st));
   for (int it = 0; it < G; ++it) {
     if ((s = assemble(c, false)) != MIS_OK) return s;
     ProfScope ps(c, P_SOLVE, 2);

@@ -37,9 +37,14 @@ struct Lay {
 };
 
 constexpr int kWarps = 8;
-constexpr float kGuardPx = 2e-3f;     // fp32 rounding guard (pixels)
-constexpr float kGuardRel = 1e-3f;    // distance gate guard (relative)
-constexpr float kGuardCos = 1e-4f;    // angle gate guard (cosine)
+#ifndef MIS_GUARD_SCALE
+#define MIS_GUARD_SCALE 1.0f
+#endif
+// Guard bands around every fp32 decision, each ~3-10x the fp32
+// error bound: u, v <= ~3.5e-4 px at 640 px; |v~ - q| <= ~3e-5 mm; n~.N <= ~1e-6.
+constexpr float kGuardPx = 1e-3f * MIS_GUARD_SCALE;     // rounding of u, v (pixels)
+constexpr float kGuardRel = 2e-5f * MIS_GUARD_SCALE;    // distance gate (relative to eps_d)
+constexpr float kGuardCos = 1e-5f * MIS_GUARD_SCALE;    // angle gate (cosine)
 
 __device__ __forceinline__ bool depth_ok_d(float d) { return isfinite(d) && d > 0.0f; }
 
@@ -215,6 +220,7 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
         }
       }
       if (guard) {
+        atomicAdd(a.guard_counter, 1.0);
         Fp64Args fa;
         fa.px = md.px; fa.py = md.py; fa.pz = md.pz; fa.nx = md.nx; fa.ny = md.ny; fa.nz = md.nz; fa.kw = md.kw;
         fa.cap = md.cap;
@@ -271,7 +277,7 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
 }
 
 template <int K, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_assemble_points(AsmPointsArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_points(AsmPointsArgs a) {
   using L = Lay<K>;
   constexpr int P = L::P;
   constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
@@ -322,8 +328,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_assemble_points(AsmPointsArg
     offB[r] = tV[r] ? base + 4 * tabJ[t] : 0;
   }
 
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t c = (int64_t)blockIdx.x * kWarps + warp; c < a.nchunk; c += nw) {
+  // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
+  int64_t c = 0;
+  if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  for (; c < a.nchunk;) {
     const int4 ch = a.chunks[c];
     const int seg = ch.x;
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
@@ -370,11 +379,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_assemble_points(AsmPointsArg
     }
     __syncwarp();
     float* rec = a.records + c * (int64_t)RS;
+    int64_t nxt = 0;
+    if (lane == 0) nxt = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
     for (int d = lane; d < RS; d += 32) {
       const int q = perm[d];
       rec[d] = q >= 0 ? F[q] : 0.f;
     }
     if (lane == 0) rec[52 * P + 18 * K + 4] = (float)n_assoc;
+    c = __shfl_sync(0xffffffffu, nxt, 0);
   }
 }
 

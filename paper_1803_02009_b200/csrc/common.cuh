@@ -74,6 +74,8 @@ struct AsmPointsArgs {
   float eps_d, cos_eps_n;
   double eps_dd, cos_eps_nd;
   float* records;             // nchunk x rec_stride per-chunk partial sums (pair-major)
+  unsigned long long* work_counter;   // zeroed before the launch (dynamic chunk scheduling)
+  double* guard_counter;              // fp64 guard-band re-evaluations (energy slot 5)
   int32_t* dbg_pix;           // nullable: per point association outputs
   uint8_t* dbg_why;
 };

@@ -161,6 +161,7 @@ __global__ void k_energy_report(AccView acc, float w_data, float w_pt, float w_r
   rep[0] = E[0]; rep[1] = E[1]; rep[2] = E[2]; rep[3] = E[3];
   rep[4] = (double)w_data * E[0] + (double)w_pt * E[1] + (double)w_reg * E[2] + (double)w_corr * E[3];
   rep_nassoc[slot] = E[4];
+  rep_nassoc[MIS_MAX_GN + 1 + slot] = E[5];   // fp64 guard-band re-evaluations
 }
 
 void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr, int slot,

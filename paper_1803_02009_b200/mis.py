@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmis.so")
+LIB_PATH = os.environ.get("MIS_LIB_PATH", os.path.join(_HERE, "libmis.so"))   # override: experiments only
 
 MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
@@ -48,7 +48,7 @@ class mis_report(C.Structure):
                 ("n_assoc", C.c_int64 * (MIS_MAX_GN + 1)),
                 ("pcg_rel_res", C.c_float * MIS_MAX_GN),
                 ("nnzb", C.c_int64), ("n_segments", C.c_int64), ("solver_cluster", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("reserved", C.c_int32), ("n_guard", C.c_int64 * (MIS_MAX_GN + 1))]
 
 
 if not os.path.exists(LIB_PATH):
@@ -213,7 +213,8 @@ def report_dict(rep: mis_report):
                 energy=np.array([[rep.energy[i][q] for q in range(5)] for i in range(it + 1)]),
                 n_assoc=np.array([rep.n_assoc[i] for i in range(it + 1)]),
                 pcg_rel_res=np.array([rep.pcg_rel_res[i] for i in range(it)]),
-                nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster)
+                nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster,
+                n_guard=np.array([rep.n_guard[i] for i in range(it + 1)]))
 
 
 def mis_get_nodes(ctx, out):
