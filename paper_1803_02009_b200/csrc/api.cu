@@ -39,8 +39,9 @@ void free_buf(DBuf& b) {
   b.bytes = 0;
 }
 
-ModelView model_view(Ctx* c) {
-  ModelBufs& B = c->mb[c->cur];
+ModelView model_view(Ctx* c) { return model_view_of(c, c->mb[c->cur]); }
+
+ModelView model_view_of(Ctx* c, ModelBufs& B) {
   ModelView v;
   v.n = c->n; v.cap = c->cap;
   v.px = B.px.as<float>(); v.py = B.py.as<float>(); v.pz = B.pz.as<float>();
@@ -216,6 +217,19 @@ __global__ void k_get_nodes(int m, const float* node32, float* out) {
   if (j >= m) return;
   for (int i = 0; i < 12; ++i) out[12 * j + i] = node32[16 * j + i];
 }
+// ids_dev[0] = max(ids) + 1 (ids == null: n); grid-wide max by atomicMax after a block max
+__global__ void k_next_id(int64_t n, const int64_t* ids, long long* ids_dev) {
+  __shared__ long long bm;
+  if (threadIdx.x == 0) bm = -1;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !ids) ids_dev[0] = n;
+  __syncthreads();
+  if (!ids) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicMax(&bm, (long long)ids[i]);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(ids_dev, bm + 1);
+}
+
 __global__ void k_count_winners(int n, const unsigned long long* key, unsigned long long* cnt) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = __syncthreads_count(p < n && key[p] != ~0ull);
@@ -280,7 +294,7 @@ static mis_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
   } while (0)
 
 static cudaError_t run_build_order(Ctx* c) {
-  ProfScope ps(c, P_ORDER, c->n > 0 ? 17 + 2 * c->K : 0);
+  ProfScope ps(c, P_ORDER, c->n > 0 ? 6 : 0);
   return build_order(c);
 }
 
@@ -430,15 +444,14 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
     k_fill_defaults<<<nb(n), 256, 0, c->st>>>(n, 0, md.w, md.stamp, md.ids, !weight, !stamp, !ids);
     TRY(c, cudaGetLastError());
   }
-  c->next_id = n;
-  if (ids && n > 0) {   // next fresh id = max(ids) + 1 (host read)
-    std::vector<int64_t> h(n);
-    TRY(c, cudaMemcpyAsync(h.data(), md.ids, n * 8, cudaMemcpyDeviceToHost, c->st));
-    TRY(c, cudaStreamSynchronize(c->st));
-    int64_t mx = -1;
-    for (int64_t v : h) mx = v > mx ? v : mx;
-    c->next_id = mx + 1;
+  // next fresh id = max(ids) + 1, kept on the device (no host synchronisation)
+  TRY(c, ensure(c, c->ids_dev, 16));
+  TRY(c, cudaMemsetAsync(c->ids_dev.p, 0, 16, c->st));
+  {
+    ProfScope ps(c, P_IO, 1);
+    k_next_id<<<n > 0 ? nb(n) : 1, 256, 0, c->st>>>(n, ids ? md.ids : nullptr, c->ids_dev.as<long long>());
   }
+  TRY(c, cudaGetLastError());
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
   c->have_model = true;
   c->have_graph = false;
@@ -934,7 +947,7 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
   {
     ProfScope ps(c, P_LIFT, 3);
-    launch_lift_count(a, counts, nbk, c->st);
+    launch_lift_count(a, counts, nbk, c->ids_dev.as<long long>(), c->st);
     k_count_winners<<<nb((int64_t)px), 256, 0, c->st>>>((int)px, c->pixkey.as<unsigned long long>(), cnt);
   }
   int32_t n_lift = 0;
@@ -948,7 +961,7 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   }
   const int64_t base = c->n;
   ProfScope ps(c, P_LIFT, 1 + (n_lift > 0));
-  launch_lift_write(a, counts + nbk + 1, nbk, base, c->next_id, c->st);
+  launch_lift_write(a, counts + nbk + 1, nbk, base, c->ids_dev.as<long long>(), c->st);
   ModelView md = model_view(c);
   if (n_lift > 0) {
     launch_skin(n_lift, md.px + base, md.py + base, md.pz + base, 1, c->g.as<float>(), c->m, c->K, md.kidx + base,
@@ -957,7 +970,6 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   }
   TRY(c, cudaGetLastError());
   c->n += n_lift;
-  c->next_id += n_lift;
   *n_out = c->n;
   if (stats) {
     stats[0] = (int64_t)n_reg;

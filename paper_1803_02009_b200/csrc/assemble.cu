@@ -498,101 +498,123 @@ void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStre
 }
 
 // ---------------------------------------------------------------- K4 / K5
-__device__ __forceinline__ void add_block(float* B, const float (&M)[36], float w) {
-#pragma unroll
-  for (int e = 0; e < 36; ++e)
-    if (M[e] != 0.f) atomicAdd(B + e, w * M[e]);
+// One thread per (edge, block row), (feature, node pair, block row) and
+// (feature, node): ~50k independent items at C3 instead of 4.5k serial
+// atomic chains (the regulariser and feature blocks are few: latency-bound).
+__device__ __forceinline__ void feature_warp(const AsmGraphArgs& a, int fi, float (*am)[3], float* wn, float* e,
+                                             float* rp, bool* ok) {
+  const int K = a.K;
+  const float V[3] = {a.fsrc[3 * fi], a.fsrc[3 * fi + 1], a.fsrc[3 * fi + 2]};
+  float W = 0.f;
+  for (int s = 0; s < K; ++s) W += a.fw[(int64_t)s * a.nf + fi];
+  *ok = W > 0.f;
+  if (!*ok) return;
+  float xh[3] = {0, 0, 0};
+  for (int s = 0; s < K; ++s) {
+    const float* Nd = a.nd.node32 + 16 * a.fidx[(int64_t)s * a.nf + fi];
+    wn[s] = a.fw[(int64_t)s * a.nf + fi] / W;
+    const float d[3] = {V[0] - Nd[12], V[1] - Nd[13], V[2] - Nd[14]};
+    for (int r = 0; r < 3; ++r) {
+      am[s][r] = Nd[3 * r] * d[0] + Nd[3 * r + 1] * d[1] + Nd[3 * r + 2] * d[2];
+      xh[r] += wn[s] * (am[s][r] + Nd[12 + r] + Nd[9 + r]);
+    }
+  }
+  const float* R = a.fr.R;
+  for (int r = 0; r < 3; ++r)
+    e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.T[r] - a.fdst[3 * fi + r];
+  for (int r = 0; r < 3; ++r) rp[r] = R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2];
 }
 
-// [ (a.b) I - b a^T , [a]x ; -[b]x , I ]  = [[a]x ; I] [-[b]x , I]
-__device__ __forceinline__ void pt_block(const float* a, const float* b, float (&M)[36]) {
-  const float ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) M[6 * r + c] = (r == c ? ab : 0.f) - b[r] * a[c];
+// row r of [ (a.b) I - b a^T , [a]x ; -[b]x , I ]
+__device__ __forceinline__ void pt_row(const float* a, const float* b, int r, float* row) {
   const float Ax[9] = {0, -a[2], a[1], a[2], 0, -a[0], -a[1], a[0], 0};
   const float Bx[9] = {0, -b[2], b[1], b[2], 0, -b[0], -b[1], b[0], 0};
-  for (int r = 0; r < 3; ++r)
+  if (r < 3) {
+    const float ab = a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
     for (int c = 0; c < 3; ++c) {
-      M[6 * r + 3 + c] = Ax[3 * r + c];
-      M[6 * (r + 3) + c] = -Bx[3 * r + c];
-      M[6 * (r + 3) + 3 + c] = (r == c) ? 1.f : 0.f;
+      row[c] = (r == c ? ab : 0.f) - b[r] * a[c];
+      row[3 + c] = Ax[3 * r + c];
     }
+  } else {
+    const int rr = r - 3;
+    for (int c = 0; c < 3; ++c) {
+      row[c] = -Bx[3 * rr + c];
+      row[3 + c] = (rr == c) ? 1.f : 0.f;
+    }
+  }
 }
 
-__global__ void __launch_bounds__(128) k_assemble_graph(AsmGraphArgs a) {
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ne = a.nd.m * a.n_nbr;
+__device__ __forceinline__ void add_row(float* B, int r, const float* row, float w) {
+  for (int c = 0; c < 6; ++c)
+    if (row[c] != 0.f) atomicAdd(B + 6 * r + c, w * row[c]);
+}
+
+__global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = a.K, P = K * (K + 1) / 2;
+  const int64_t n_edge = (int64_t)a.nd.m * a.n_nbr * 6, n_fp = (int64_t)a.nf * P * 6, n_fr = (int64_t)a.nf * K;
   float eR = 0.f, eC = 0.f;
-  if (tid < ne) {
-    // Eq. 6, alpha = 1, directed edge j -> l (reading A14)
-    const int j = tid / a.n_nbr, l = a.nbr[tid];
+  if (tid < n_edge) {
+    // Eq. 6, alpha = 1, directed edge j -> l (reading A14):
+    // J_j = [-[b]x, I], J_l = [0, -I], b = R_j (g_l - g_j)
+    const int64_t ei = tid / 6;
+    const int r = (int)(tid % 6);
+    const int j = (int)(ei / a.n_nbr), l = a.nbr[ei];
     if (l >= 0) {
       const float* Nj = a.nd.node32 + 16 * j;
       const float* Nl = a.nd.node32 + 16 * l;
       const float d[3] = {Nl[12] - Nj[12], Nl[13] - Nj[13], Nl[14] - Nj[14]};
-      float b[3], e[3];
-      for (int r = 0; r < 3; ++r) b[r] = Nj[3 * r] * d[0] + Nj[3 * r + 1] * d[1] + Nj[3 * r + 2] * d[2];
-      for (int r = 0; r < 3; ++r) e[r] = b[r] + Nj[12 + r] + Nj[9 + r] - Nl[12 + r] - Nl[9 + r];
-      eR = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
-      float M[36];
-      pt_block(b, b, M);                        // J_j^T J_j, J_j = [-[b]x, I]
-      add_block(a.acc.graph + 36 * (int64_t)a.diag_slot[j], M, a.w_reg);
-      for (int x = 0; x < 36; ++x) M[x] = 0.f;  // J_l^T J_l = diag(0, I)
-      M[21] = M[28] = M[35] = 1.f;
-      add_block(a.acc.graph + 36 * (int64_t)a.diag_slot[l], M, a.w_reg);
-      // J_j^T J_l = [0, -[b]x ; 0, -I]  (stored transposed when l < j)
+      float b[3], e[3], row[6];
+      for (int q = 0; q < 3; ++q) b[q] = Nj[3 * q] * d[0] + Nj[3 * q + 1] * d[1] + Nj[3 * q + 2] * d[2];
+      for (int q = 0; q < 3; ++q) e[q] = b[q] + Nj[12 + q] + Nj[9 + q] - Nl[12 + q] - Nl[9 + q];
+      if (r == 0) eR = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+      pt_row(b, b, r, row);                                           // J_j^T J_j
+      add_row(a.acc.graph + 36 * (int64_t)a.diag_slot[j], r, row, a.w_reg);
+      if (r >= 3) atomicAdd(a.acc.graph + 36 * (int64_t)a.diag_slot[l] + 7 * r, a.w_reg);   // J_l^T J_l
       const float Bx[9] = {0, -b[2], b[1], b[2], 0, -b[0], -b[1], b[0], 0};
-      for (int x = 0; x < 36; ++x) M[x] = 0.f;
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) {
-          if (j < l) { M[6 * r + 3 + c] = -Bx[3 * r + c]; }
-          else { M[6 * (r + 3) + c] = -Bx[3 * c + r]; }
-          M[6 * (r + 3) + 3 + c] = (r == c) ? -1.f : 0.f;
-        }
-      add_block(a.acc.graph + 36 * (int64_t)a.edge_slot[tid], M, a.w_reg);
-      // rhs: -J^T e
-      const float bxe[3] = {b[1] * e[2] - b[2] * e[1], b[2] * e[0] - b[0] * e[2], b[0] * e[1] - b[1] * e[0]};
-      for (int r = 0; r < 3; ++r) {
-        atomicAdd(a.acc.rhs_graph + 6 * j + r, -a.w_reg * bxe[r]);
-        atomicAdd(a.acc.rhs_graph + 6 * j + 3 + r, -a.w_reg * e[r]);
-        atomicAdd(a.acc.rhs_graph + 6 * l + 3 + r, a.w_reg * e[r]);
+      for (int c = 0; c < 6; ++c) row[c] = 0.f;
+      if (j < l) {                                                    // J_j^T J_l = [0, -[b]x ; 0, -I]
+        if (r < 3) for (int c = 0; c < 3; ++c) row[3 + c] = -Bx[3 * r + c];
+        else row[r] = -1.f;
+      } else if (r >= 3) {                                            // its transpose [0, 0 ; -[b]x^T, -I]
+        for (int c = 0; c < 3; ++c) row[c] = -Bx[3 * c + (r - 3)];
+        row[r] = -1.f;
+      }
+      add_row(a.acc.graph + 36 * (int64_t)a.edge_slot[ei], r, row, a.w_reg);
+      if (r < 3) {                                                    // rhs = -J^T e
+        const float bxe = b[(r + 1) % 3] * e[(r + 2) % 3] - b[(r + 2) % 3] * e[(r + 1) % 3];
+        atomicAdd(a.acc.rhs_graph + 6 * j + r, -a.w_reg * bxe);
+      } else {
+        atomicAdd(a.acc.rhs_graph + 6 * j + r, -a.w_reg * e[r - 3]);
+        atomicAdd(a.acc.rhs_graph + 6 * l + r, a.w_reg * e[r - 3]);
       }
     }
-  } else if (tid < ne + a.nf) {
-    // Eq. 9, squared (reading A12)
-    const int fi = tid - ne, K = a.K;
-    const float V[3] = {a.fsrc[3 * fi], a.fsrc[3 * fi + 1], a.fsrc[3 * fi + 2]};
-    float W = 0.f;
-    for (int s = 0; s < K; ++s) W += a.fw[(int64_t)s * a.nf + fi];
-    if (W > 0.f) {
-      float am[MIS_MAX_K][3], wn[MIS_MAX_K], xh[3] = {0, 0, 0};
-      for (int s = 0; s < K; ++s) {
-        const float* Nd = a.nd.node32 + 16 * a.fidx[(int64_t)s * a.nf + fi];
-        wn[s] = a.fw[(int64_t)s * a.nf + fi] / W;
-        const float d[3] = {V[0] - Nd[12], V[1] - Nd[13], V[2] - Nd[14]};
-        for (int r = 0; r < 3; ++r) {
-          am[s][r] = Nd[3 * r] * d[0] + Nd[3 * r + 1] * d[1] + Nd[3 * r + 2] * d[2];
-          xh[r] += wn[s] * (am[s][r] + Nd[12 + r] + Nd[9 + r]);
-        }
-      }
-      const float* R = a.fr.R;
-      float e[3], rp[3];
-      for (int r = 0; r < 3; ++r) e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.T[r] - a.fdst[3 * fi + r];
-      for (int r = 0; r < 3; ++r) rp[r] = R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2];
-      eC = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
-      const int32_t* slots = a.feat_slot + (int64_t)fi * (K * (K + 1) / 2);
-      float M[36];
-      for (int s = 0; s < K; ++s) {
-        for (int s2 = s; s2 < K; ++s2) {
-          pt_block(am[s], am[s2], M);
-          add_block(a.acc.graph + 36 * (int64_t)slots[pair_index(s, s2, K)], M, a.w_corr * wn[s] * wn[s2]);
-        }
+  } else if (tid < n_edge + n_fp + n_fr) {
+    // Eq. 9, squared 3-vector residual (reading A12): J_j = w_j R [-[a_j]x, I]
+    const bool is_rhs = tid >= n_edge + n_fp;
+    const int64_t t2 = is_rhs ? tid - n_edge - n_fp : tid - n_edge;
+    const int fi = is_rhs ? (int)(t2 / K) : (int)(t2 / (6 * P));
+    float am[MIS_MAX_K][3], wn[MIS_MAX_K], e[3], rp[3];
+    bool ok;
+    feature_warp(a, fi, am, wn, e, rp, &ok);
+    if (ok) {
+      if (!is_rhs) {
+        const int pr = (int)((t2 / 6) % P), r = (int)(t2 % 6);
+        int s = 0, q = pr;
+        while (q >= K - s) { q -= K - s; ++s; }
+        const int s2 = s + q;
+        float row[6];
+        pt_row(am[s], am[s2], r, row);
+        add_row(a.acc.graph + 36 * (int64_t)a.feat_slot[(int64_t)fi * P + pr], r, row, a.w_corr * wn[s] * wn[s2]);
+      } else {
+        const int s = (int)(t2 % K);
+        if (s == 0) eC = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
         const int node = a.fidx[(int64_t)s * a.nf + fi];
         const float axr[3] = {am[s][1] * rp[2] - am[s][2] * rp[1], am[s][2] * rp[0] - am[s][0] * rp[2],
                               am[s][0] * rp[1] - am[s][1] * rp[0]};
-        for (int r = 0; r < 3; ++r) {
-          atomicAdd(a.acc.rhs_graph + 6 * node + r, -a.w_corr * wn[s] * axr[r]);
-          atomicAdd(a.acc.rhs_graph + 6 * node + 3 + r, -a.w_corr * wn[s] * rp[r]);
+        for (int q = 0; q < 3; ++q) {
+          atomicAdd(a.acc.rhs_graph + 6 * node + q, -a.w_corr * wn[s] * axr[q]);
+          atomicAdd(a.acc.rhs_graph + 6 * node + 3 + q, -a.w_corr * wn[s] * rp[q]);
         }
       }
     }
@@ -609,9 +631,11 @@ __global__ void __launch_bounds__(128) k_assemble_graph(AsmGraphArgs a) {
 }
 
 void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s) {
-  const int n = a.nd.m * a.n_nbr + a.nf;
+  const int P = a.K * (a.K + 1) / 2;
+  const int64_t n = (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.K;
   if (n <= 0) return;
-  k_assemble_graph<<<(n + 127) / 128, 128, 0, s>>>(a);
+  k_assemble_graph<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
 }
+
 
 }  // namespace mis

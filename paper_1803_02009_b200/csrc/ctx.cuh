@@ -77,6 +77,7 @@ struct Ctx {
 
   // ---- fuse
   DBuf pixkey, pix, why, lift_counts, counter;
+  DBuf ids_dev;   // int64 [0] next fresh point id, [1] id base of the last lift (device-resident: no host sync)
 
   // ---- report
   DBuf rep_energy, rep_nassoc, rep_res;
@@ -114,6 +115,7 @@ void free_buf(DBuf& b);
 
 // views
 ModelView model_view(Ctx* c);
+ModelView model_view_of(Ctx* c, ModelBufs& B);
 NodeView node_view(Ctx* c);
 FrameView frame_view(Ctx* c);
 AccView acc_view(Ctx* c);

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restric
       sg[t] = make_float4(g[3 * (base + t)], g[3 * (base + t) + 1], g[3 * (base + t) + 2], 0.f);
     __syncthreads();
     if (act) {
+#pragma unroll 8
       for (int t = 0; t < cnt; ++t) {
         const float4 q = sg[t];
         const float dx = vx - q.x, dy = vy - q.y, dz = vz - q.z;

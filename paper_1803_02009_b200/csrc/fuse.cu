@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* 
 }
 
 // exclusive scan of the per-block counts (single block; counts[nb] = total)
-__global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb) {
+__global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb,
+                                                      long long* ids_dev) {
   __shared__ int32_t part[1024];
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
@@ -227,6 +228,8 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
     int32_t run = 0;
     for (int t = 0; t < 1024; ++t) { int32_t v = part[t]; part[t] = run; run += v; }
     offs[nb] = run;
+    ids_dev[1] = ids_dev[0];   // ids of the lifted points: ids_dev[1] + rank
+    ids_dev[0] += run;
   }
   __syncthreads();
   int32_t run = part[threadIdx.x];
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
 }
 
 __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int32_t* offs, int64_t base,
-                                                           int64_t next_id) {
+                                                           const long long* ids_dev) {
   __shared__ int wsum[kLiftBlock / 32];
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const bool on = lift_pixel(a, p);
@@ -266,17 +269,17 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   }
   md.w[o] = 1.0f;
   md.stamp[o] = a.frame_index;
-  md.ids[o] = next_id + (o - base);
+  md.ids[o] = ids_dev[1] + (o - base);
 }
 
-void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, cudaStream_t s) {
+void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long long* ids_dev, cudaStream_t s) {
   k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts);
-  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks);
+  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks, ids_dev);
 }
 
-void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, int64_t next_id,
+void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, const long long* ids_dev,
                        cudaStream_t s) {
-  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, next_id);
+  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, ids_dev);
 }
 
 }  // namespace mis

@@ -108,22 +108,20 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (t <= cs) spart[t] = a.part[t];
   for (int i = t; i <= nr; i += kCT) lrp[i] = a.row_ptr[r0 + i] - e0;
   __syncthreads();
-  for (int k = t; k < ne; k += kCT) {
+  for (int w = t; w < 6 * ne; w += kCT) {   // one thread per (entry, row)
+    const int k = w / 6, rr = w - 6 * k;
     const int e = e0 + k;
     const int c = a.col[e];
-    col[k] = c;
+    if (rr == 0) col[k] = c;
     const int64_t u = a.upper_of[e];
-    float B[36];
-    upper_block(a.acc, a.w_data, a.w_pt, u, a.diag_pos[c] == e, B);
-    float* out = H + 36 * (size_t)k;
-    if (u == e) {
-      for (int i = 0; i < 36; ++i) out[i] = B[i];
-    } else {
-      for (int rr = 0; rr < 6; ++rr)
-        for (int cc = 0; cc < 6; ++cc) out[6 * rr + cc] = B[6 * cc + rr];
-    }
+    float row[6];
+    block_row(a.acc, a.w_data, a.w_pt, u, a.diag_pos[c] == e, u != e, rr, row);
+    float* out = H + 36 * (size_t)k + 6 * rr;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[q] = row[q];
     if (a.write_global)
-      for (int i = 0; i < 36; ++i) a.Hval[36 * (int64_t)e + i] = out[i];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) a.Hval[36 * (int64_t)e + 6 * rr + q] = row[q];
   }
   for (int i = t; i < 6 * nr; i += kCT) {
     const float b = rhs_entry(a.acc, a.w_data, a.w_pt, 6 * (int64_t)r0 + i);
@@ -138,7 +136,43 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (a.pcg_iters <= 0 && !a.do_update) return;
 
   // ---- phase 1: block-Jacobi preconditioner, z = M r, r.z
-  for (int i = t; i < nr; i += kCT) precond_block(H + 36 * (size_t)(a.diag_pos[r0 + i] - e0), a.lambda, Mi + 36 * i);
+  // M_j = (H_jj + (lambda + mu_j) I)^-1 in fp64 by Gauss-Jordan, 6 lanes per node
+  // (one row each, pivot rows broadcast by shuffles), 5 nodes per warp.
+  {
+    const int wid = t >> 5, ln = t & 31, slot = ln / 6, rr = ln - 6 * slot;
+    for (int base = 0; base < nr; base += 5 * (kCT / 32)) {
+      const int i = base + 5 * wid + slot;
+      const bool act = slot < 5 && i < nr;
+      const float* Hd = H + 36 * (size_t)(act ? a.diag_pos[r0 + i] - e0 : 0);
+      double row[12];
+      double trc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) trc += act ? (double)Hd[7 * q] : 0.0;
+      const double mu = 1e-9 * trc / 6.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        row[q] = act ? (double)Hd[6 * rr + q] + (q == rr ? (double)a.lambda + mu : 0.0) : (q == rr ? 1.0 : 0.0);
+        row[6 + q] = (q == rr) ? 1.0 : 0.0;
+      }
+      bool pd = true;
+      const int src0 = slot < 5 ? 6 * slot : 0;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const double pv = __shfl_sync(0xffffffffu, row[p], src0 + p);
+        if (!(pv > 0.0)) pd = false;
+        const double ipv = 1.0 / pv;
+        const double f = row[p] * ipv;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+          const double pq = __shfl_sync(0xffffffffu, row[q], src0 + p);
+          row[q] = (rr == p) ? pq * ipv : row[q] - f * pq;
+        }
+      }
+      if (act)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) Mi[36 * i + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
+    }
+  }
   __syncthreads();
   if (stamp) ts[2] = gtimer();
   double my = 0.0;

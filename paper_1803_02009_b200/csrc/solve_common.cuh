@@ -43,6 +43,43 @@ __device__ __forceinline__ void upper_block(const AccView& acc, float w_data, fl
   for (int r = 0; r < 3; ++r) B[6 * (3 + r) + 3 + r] += w_pt * s0;
 }
 
+// Row r of the block B(j,l) of upper slot u (tr: row r of B^T), same formula as
+// upper_block; one thread per (entry, row) keeps the loads parallel.
+__device__ __forceinline__ void block_row(const AccView& acc, float w_data, float w_pt, int64_t u, bool diag, bool tr,
+                                          int r, float* out) {
+  const float* D = acc.data + 36 * u;
+  const float* G = acc.graph + 36 * u;
+  float Mo[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) Mo[q] = acc.mom[16 * u + q];
+  float S[9], sj[3], sl[3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) S[3 * p + q] = diag ? Mo[4 * min(p, q) + max(p, q)] : Mo[4 * p + q];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) { sj[p] = Mo[4 * p + 3]; sl[p] = diag ? Mo[4 * p + 3] : Mo[12 + p]; }
+  const float s0 = Mo[15], trS = S[0] + S[4] + S[8];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int i = tr ? k : r, j = tr ? r : k;   // entry (i, j) of B
+    const float d = diag ? D[6 * min(i, j) + max(i, j)] : D[6 * i + j];
+    float pt;
+    if (i < 3 && j < 3) {
+      pt = (i == j ? trS : 0.f) - S[3 * j + i];
+    } else if (i < 3) {            // [s_j]x (i, j-3)
+      const int c = j - 3;
+      pt = (i == c) ? 0.f : ((c == (i + 1) % 3) ? -sj[(i + 2) % 3] : sj[(i + 1) % 3]);
+    } else if (j < 3) {            // -[s_l]x (i-3, j)
+      const int rr = i - 3;
+      pt = (rr == j) ? 0.f : ((j == (rr + 1) % 3) ? sl[(rr + 2) % 3] : -sl[(rr + 1) % 3]);
+    } else {
+      pt = (i == j) ? s0 : 0.f;
+    }
+    out[k] = w_data * d + G[6 * i + j] + w_pt * pt;
+  }
+}
+
 // b_i = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs
 __device__ __forceinline__ float rhs_entry(const AccView& acc, float w_data, float w_pt, int64_t i) {
   const int64_t j = i / 6;

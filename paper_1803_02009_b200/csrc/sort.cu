@@ -44,6 +44,21 @@ __global__ void k_tuple_keys(int64_t n, int64_t cap, const int32_t* kidx, int K,
   vals[i] = (uint32_t)i;
 }
 
+// all model arrays in one launch: dst[i] = src[perm[i]]
+__global__ void k_gather_model(int64_t n, const uint32_t* perm, ModelView a, ModelView b, int K) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+  b.px[i] = a.px[j]; b.py[i] = a.py[j]; b.pz[i] = a.pz[j];
+  b.nx[i] = a.nx[j]; b.ny[i] = a.ny[j]; b.nz[i] = a.nz[j];
+  b.cr[i] = a.cr[j]; b.cg[i] = a.cg[j]; b.cb[i] = a.cb[j]; b.w[i] = a.w[j];
+  b.stamp[i] = a.stamp[j]; b.ids[i] = a.ids[j];
+  for (int s = 0; s < K; ++s) {
+    b.kidx[s * a.cap + i] = a.kidx[s * a.cap + j];
+    b.kw[s * a.cap + i] = a.kw[s * a.cap + j];
+  }
+}
+
 template <class T>
 __global__ void k_gather(int64_t n, const uint32_t* perm, const T* src, T* dst) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -79,16 +94,18 @@ __global__ void k_seg_write(int64_t n, int64_t cap, const int32_t* kidx, int K, 
   if (i == 0) seg_start[scan[n - 1]] = (int32_t)n;   // sentinel
 }
 
-__global__ void k_chunk_count(int64_t nseg, const int32_t* seg_start, int32_t* cnt) {
+__global__ void k_chunk_count(int64_t n, const int32_t* nseg_dev, const int32_t* seg_start, int32_t* cnt) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
+  if (s >= n) return;
+  if (s >= *nseg_dev) { cnt[s] = 0; return; }
   const int32_t len = seg_start[s + 1] - seg_start[s];
   cnt[s] = (len + kChunk - 1) / kChunk;
 }
 
-__global__ void k_chunk_write(int64_t nseg, const int32_t* seg_start, const int32_t* off, int4* chunks) {
+__global__ void k_chunk_write(int64_t n, const int32_t* nseg_dev, const int32_t* seg_start, const int32_t* off,
+                              int4* chunks) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
+  if (s >= n || s >= *nseg_dev) return;
   const int32_t a = seg_start[s], b = seg_start[s + 1];
   int32_t o = off[s] - (b - a + kChunk - 1) / kChunk;   // inclusive scan -> start
   for (int32_t p = a; p < b; p += kChunk) chunks[o++] = make_int4((int)s, p, min(b, p + kChunk), 0);
@@ -119,49 +136,40 @@ cudaError_t build_order(Ctx* c) {
       return cub::DeviceRadixSort::SortPairs(t, s, c->keys.as<uint64_t>(), c->keys2.as<uint64_t>(),
                                              c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, 64, c->st);
     }));
-    const uint32_t* perm = c->vals2.as<uint32_t>();
-    gather<float>(c, perm, A.px, B.px, n, 1); gather<float>(c, perm, A.py, B.py, n, 1);
-    gather<float>(c, perm, A.pz, B.pz, n, 1); gather<float>(c, perm, A.nx, B.nx, n, 1);
-    gather<float>(c, perm, A.ny, B.ny, n, 1); gather<float>(c, perm, A.nz, B.nz, n, 1);
-    gather<float>(c, perm, A.cr, B.cr, n, 1); gather<float>(c, perm, A.cg, B.cg, n, 1);
-    gather<float>(c, perm, A.cb, B.cb, n, 1); gather<float>(c, perm, A.w, B.w, n, 1);
-    gather<int32_t>(c, perm, A.stamp, B.stamp, n, 1); gather<int64_t>(c, perm, A.ids, B.ids, n, 1);
-    gather<int32_t>(c, perm, A.kidx, B.kidx, n, K); gather<float>(c, perm, A.kw, B.kw, n, K);
+    k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
     CK(cudaGetLastError());
     c->cur = 1 - c->cur;
   }
   ModelBufs& S = c->mb[c->cur];
-  // segments
+  // segments and chunks, sized by the upper bound n: one host readback at the end
   c->nseg = 0;
   c->nchunk = 0;
   if (n > 0) {
     CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
+    CK(ensure(c, c->seg_start, (n + 1) * 4));
+    CK(ensure(c, c->seg_nodes, (size_t)n * K * 4));
+    CK(ensure(c, c->chunk_off, (n + 1) * 4));
+    CK(ensure(c, c->chunks, (size_t)n * 16));
     const int b = (int)((n + 255) / 256);
     k_seg_flags<<<b, 256, 0, c->st>>>(n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->scan.as<int32_t>(), (int)n, c->st);
     }));
-    int32_t nseg = 0;
-    CK(cudaMemcpyAsync(&nseg, c->scan.as<int32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    c->nseg = nseg;
-    CK(ensure(c, c->seg_start, (nseg + 1) * 4));
-    CK(ensure(c, c->seg_nodes, (size_t)nseg * K * 4));
+    const int32_t* nseg_dev = c->scan.as<int32_t>() + n - 1;
     k_seg_write<<<b, 256, 0, c->st>>>(n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>(),
                                       c->scan.as<int32_t>(), c->seg_start.as<int32_t>(), c->seg_nodes.as<int32_t>());
-    CK(ensure(c, c->chunk_off, (nseg + 1) * 4));   // flags (n entries >= nseg) is reused for the counts
-    const int bs = (nseg + 255) / 256;
-    k_chunk_count<<<bs, 256, 0, c->st>>>(nseg, c->seg_start.as<int32_t>(), c->flags.as<int32_t>());
+    k_chunk_count<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->flags.as<int32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
-      return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->chunk_off.as<int32_t>(), (int)nseg, c->st);
+      return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->chunk_off.as<int32_t>(), (int)n, c->st);
     }));
-    int32_t nch = 0;
-    CK(cudaMemcpyAsync(&nch, c->chunk_off.as<int32_t>() + nseg - 1, 4, cudaMemcpyDeviceToHost, c->st));
+    k_chunk_write<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
+                                        c->chunks.as<int4>());
+    int32_t cnt[2] = {0, 0};
+    CK(cudaMemcpyAsync(&cnt[0], nseg_dev, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&cnt[1], c->chunk_off.as<int32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    c->nchunk = nch;
-    CK(ensure(c, c->chunks, (size_t)nch * 16));
-    k_chunk_write<<<bs, 256, 0, c->st>>>(nseg, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
-                                         c->chunks.as<int4>());
+    c->nseg = cnt[0];
+    c->nchunk = cnt[1];
     CK(cudaGetLastError());
   }
   c->dirty = false;
