@@ -155,9 +155,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
-// host: pick the cluster partition; returns 0 if the system does not fit
-int plan_cluster(const int32_t* row_ptr_host, int m, int max_cluster, int32_t* part_host, int* max_rows,
-                 int* max_nnz, size_t* smem_bytes);
+// cluster partition (row boundaries balancing nnz) computed on the device; cl_size 0 = does not fit
+struct PlanOut { int32_t cl_size, max_rows, max_nnz, pad; int64_t smem; };
+void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, cudaStream_t s);
 void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr,
                           int slot, double* rep_energy, double* rep_nassoc, cudaStream_t s);
 

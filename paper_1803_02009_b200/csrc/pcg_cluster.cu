@@ -287,35 +287,51 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[5] = gtimer();
 }
 
-int plan_cluster(const int32_t* row_ptr, int m, int max_cluster, int32_t* part, int* max_rows, int* max_nnz,
-                 size_t* smem_bytes) {
+// The plan on the device (one warp; lane c binary-searches boundary c), so the
+// host never reads the row structure back.  Same rule as plan_cluster.
+__global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part) {
+  __shared__ int32_t b[kMaxCluster + 1];
   int cs = max_cluster < m ? max_cluster : m;
   if (cs > kMaxCluster) cs = kMaxCluster;
-  if (cs < 1) return 0;
+  const int lane = threadIdx.x;
   const int64_t nnz = row_ptr[m];
-  part[0] = 0;
-  int row = 0;
-  for (int c = 1; c < cs; ++c) {   // boundaries balancing nnz + rows
-    const int64_t target = (nnz * c) / cs;
-    while (row < m && row_ptr[row] < target) ++row;
-    if (row <= part[c - 1]) row = part[c - 1] + 1;
-    if (row > m - (cs - c)) row = m - (cs - c);
-    part[c] = row;
+  if (lane > 0 && lane < cs) {
+    const int64_t target = (nnz * lane) / cs;
+    int lo = 0, hi = m;   // first row with row_ptr[row] >= target
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (row_ptr[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    b[lane] = lo;
   }
-  part[cs] = m;
+  __syncwarp();
+  if (lane != 0) return;
+  b[0] = 0;
+  for (int c = 1; c < cs; ++c) {
+    int row = b[c];
+    if (row <= b[c - 1]) row = b[c - 1] + 1;
+    if (row > m - (cs - c)) row = m - (cs - c);
+    b[c] = row;
+  }
+  b[cs] = m;
   int mr = 0, mn = 0;
   for (int c = 0; c < cs; ++c) {
-    const int nr = part[c + 1] - part[c];
-    const int nz = row_ptr[part[c + 1]] - row_ptr[part[c]];
+    const int nr = b[c + 1] - b[c];
+    const int nz = row_ptr[b[c + 1]] - row_ptr[b[c]];
     mr = nr > mr ? nr : mr;
     mn = nz > mn ? nz : mn;
   }
-  CLay L(mr, mn, m);
-  *max_rows = mr;
-  *max_nnz = mn;
-  *smem_bytes = L.total;
-  if (L.total > 226 * 1024) return 0;   // 227 KB per CTA minus the static shared memory
-  return cs;
+  const CLay L(mr, mn, m);
+  const bool fits = cs >= 1 && L.total <= 226 * 1024;   // 227 KB per CTA minus the static shared memory
+  out->cl_size = fits ? cs : 0;
+  out->max_rows = mr;
+  out->max_nnz = mn;
+  out->smem = (int64_t)L.total;
+  for (int c = 0; c <= cs; ++c) part[c] = b[c];
+}
+
+void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, cudaStream_t s) {
+  k_plan_cluster<<<1, 32, 0, s>>>(row_ptr, m, max_cluster, out, part);
 }
 
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {

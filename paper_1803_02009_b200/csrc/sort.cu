@@ -134,7 +134,7 @@ cudaError_t build_order(Ctx* c) {
                                         c->vals.as<uint32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceRadixSort::SortPairs(t, s, c->keys.as<uint64_t>(), c->keys2.as<uint64_t>(),
-                                             c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, 64, c->st);
+                                             c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, K * bits <= 64 ? K * bits : 64, c->st);
     }));
     k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
     CK(cudaGetLastError());
@@ -178,12 +178,13 @@ cudaError_t build_order(Ctx* c) {
 }
 
 // ---------------------------------------------------------------- pattern
-__device__ __forceinline__ uint64_t pkey(int r, int col) { return ((uint64_t)(uint32_t)r << 32) | (uint32_t)col; }
+// (row, col) key with sb = bits_for(m) bits per index: radix sorts need only 2 sb + 1 bits
+__device__ __forceinline__ uint64_t pkey(int r, int col, int sb) { return ((uint64_t)(uint32_t)r << sb) | (uint32_t)col; }
 constexpr uint64_t kNoKey = ~0ull;
 
 // candidates: [segment pairs nseg*P][edges m*n_nbr][feature pairs nf*P][diagonal m]; 2 keys each
 __global__ void k_candidates(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr,
-                             int nf, const int32_t* fidx, uint64_t* keys, int64_t total) {
+                             int nf, const int32_t* fidx, uint64_t* keys, int64_t total, int sb) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   const int P = K * (K + 1) / 2;
@@ -210,8 +211,8 @@ __global__ void k_candidates(int64_t nseg, const int32_t* seg_nodes, int K, int 
     a = b = (int)(t - ns - ne - nfp);
   }
   if (a < 0) { keys[2 * t] = kNoKey; keys[2 * t + 1] = kNoKey; return; }
-  keys[2 * t] = pkey(a, b);
-  keys[2 * t + 1] = (a != b) ? pkey(b, a) : kNoKey;
+  keys[2 * t] = pkey(a, b, sb);
+  keys[2 * t + 1] = (a != b) ? pkey(b, a, sb) : kNoKey;
 }
 
 __global__ void k_unique_flags(int64_t n, const uint64_t* k, int32_t* f) {
@@ -237,24 +238,26 @@ __device__ __forceinline__ int64_t find_key(const uint64_t* u, int64_t nnz, uint
   return (lo < nnz && u[lo] == key) ? lo : -1;
 }
 
-__global__ void k_rows(int64_t nnz, const uint64_t* u, int m, int32_t* row_ptr, int32_t* col, int32_t* upper_of,
-                       int32_t* diag_pos) {
+__global__ void k_rows(int64_t cap, const int64_t* nnz_dev, const uint64_t* u, int m, int32_t* row_ptr, int32_t* col,
+                       int32_t* upper_of, int32_t* diag_pos, int sb) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nnz) return;
-  const int r = (int)(u[e] >> 32), cc = (int)(u[e] & 0xffffffffu);
+  const int64_t nnz = *nnz_dev;
+  if (e >= nnz || e >= cap) return;
+  const int r = (int)(u[e] >> sb), cc = (int)(u[e] & ((1ull << sb) - 1));
   col[e] = cc;
-  const int rp = (e == 0) ? -1 : (int)(u[e - 1] >> 32);
+  const int rp = (e == 0) ? -1 : (int)(u[e - 1] >> sb);
   for (int q = rp + 1; q <= r; ++q) row_ptr[q] = (int32_t)e;
   if (e == nnz - 1)
     for (int q = r + 1; q <= m; ++q) row_ptr[q] = (int32_t)nnz;
   if (r == cc) diag_pos[r] = (int32_t)e;
-  upper_of[e] = (r <= cc) ? (int32_t)e : (int32_t)find_key(u, nnz, pkey(cc, r));
+  upper_of[e] = (r <= cc) ? (int32_t)e : (int32_t)find_key(u, nnz, pkey(cc, r, sb));
 }
 
 __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr, int nf,
-                        const int32_t* fidx, const uint64_t* u, int64_t nnz, int32_t* seg_slot, int32_t* edge_slot,
-                        int32_t* feat_slot, int64_t total) {
+                        const int32_t* fidx, const uint64_t* u, const int64_t* nnz_dev, int32_t* seg_slot, int32_t* edge_slot,
+                        int32_t* feat_slot, int64_t total, int sb) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nnz = *nnz_dev;
   if (t >= total) return;
   const int P = K * (K + 1) / 2;
   const int64_t ns = nseg * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P;
@@ -262,17 +265,17 @@ __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, in
     const int64_t s = t / P;
     int p = (int)(t % P), j = 0;
     while (p >= K - j) { p -= K - j; ++j; }
-    seg_slot[t] = (int32_t)find_key(u, nnz, pkey(seg_nodes[s * K + j], seg_nodes[s * K + j + p]));
+    seg_slot[t] = (int32_t)find_key(u, nnz, pkey(seg_nodes[s * K + j], seg_nodes[s * K + j + p], sb));
   } else if (t < ns + ne) {
     const int64_t e = t - ns;
     const int l = nbr[e], j = (int)(e / n_nbr);
-    edge_slot[e] = (l >= 0) ? (int32_t)find_key(u, nnz, pkey(min(j, l), max(j, l))) : -1;
+    edge_slot[e] = (l >= 0) ? (int32_t)find_key(u, nnz, pkey(min(j, l), max(j, l), sb)) : -1;
   } else if (t < ns + ne + nfp) {
     const int64_t e = t - ns - ne;
     const int64_t f = e / P;
     int p = (int)(e % P), j = 0;
     while (p >= K - j) { p -= K - j; ++j; }
-    feat_slot[e] = (int32_t)find_key(u, nnz, pkey(fidx[(int64_t)j * nf + f], fidx[(int64_t)(j + p) * nf + f]));
+    feat_slot[e] = (int32_t)find_key(u, nnz, pkey(fidx[(int64_t)j * nf + f], fidx[(int64_t)(j + p) * nf + f], sb));
   }
 }
 
@@ -288,9 +291,10 @@ __global__ void k_contrib(int64_t nchunk, const int4* chunks, const int32_t* tab
 }
 
 // CSR row pointers over nbins from sorted keys
-__global__ void k_csr_ptr(int64_t n, const int32_t* key, int nbins, int32_t* ptr) {
+__global__ void k_csr_ptr(int64_t n, const int32_t* key, const int64_t* nbins_dev, int nbins_host, int32_t* ptr) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int nbins = nbins_dev ? (int)*nbins_dev : nbins_host;
   const int k = key[i];
   const int kp = (i == 0) ? -1 : key[i - 1];
   for (int b = kp + 1; b <= k; ++b) ptr[b] = (int32_t)i;
@@ -298,7 +302,9 @@ __global__ void k_csr_ptr(int64_t n, const int32_t* key, int nbins, int32_t* ptr
     for (int b = k + 1; b <= nbins; ++b) ptr[b] = (int32_t)n;
 }
 
-static cudaError_t build_contrib(Ctx* c, const int32_t* table, int W, int nbins, DBuf& ptr, DBuf& src) {
+// nbins: upper bound (host); nbins_dev: exact count on the device (or null: nbins is exact)
+static cudaError_t build_contrib(Ctx* c, const int32_t* table, int W, int nbins, const int64_t* nbins_dev, DBuf& ptr,
+                                 DBuf& src) {
   const int64_t n = c->nchunk * W;
   CK(ensure(c, ptr, (size_t)(nbins + 1) * 4));
   CK(ensure(c, src, (size_t)n * 4 + 16));
@@ -314,7 +320,7 @@ static cudaError_t build_contrib(Ctx* c, const int32_t* table, int W, int nbins,
     return cub::DeviceRadixSort::SortPairs(t, s, c->ck_key.as<int32_t>(), c->ck_key2.as<int32_t>(),
                                            c->ck_val.as<int32_t>(), src.as<int32_t>(), (int)n, 0, bits, c->st);
   }));
-  k_csr_ptr<<<b, 256, 0, c->st>>>(n, c->ck_key2.as<int32_t>(), nbins, ptr.as<int32_t>());
+  k_csr_ptr<<<b, 256, 0, c->st>>>(n, c->ck_key2.as<int32_t>(), nbins_dev, nbins, ptr.as<int32_t>());
   return cudaGetLastError();
 }
 
@@ -322,14 +328,15 @@ cudaError_t build_pattern(Ctx* c) {
   const int K = c->K, P = K * (K + 1) / 2;
   const int64_t total = c->nseg * P + (int64_t)c->m * c->prm.n_nbr + (int64_t)c->nf * P + c->m;
   const int64_t nk = 2 * total;
+  const int sb = bits_for(c->m);
   CK(ensure(c, c->ckeys, nk * 8)); CK(ensure(c, c->ckeys2, nk * 8));
   CK(ensure(c, c->uflag, nk * 4)); CK(ensure(c, c->upos, nk * 4));
-  CK(ensure(c, c->nnz_dev, 16));
+  CK(ensure(c, c->nnz_dev, 64));
   const int bt = (int)((total + 255) / 256), bk = (int)((nk + 255) / 256);
   k_candidates<<<bt, 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, c->m, c->prm.n_nbr,
-                                      c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(), c->ckeys.as<uint64_t>(), total);
+                                      c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(), c->ckeys.as<uint64_t>(), total, sb);
   CK(cub_call(c, [&](void* t, size_t& s) {
-    return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)nk, 0, 64, c->st);
+    return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)nk, 0, 2 * sb + 1, c->st);
   }));
   k_unique_flags<<<bk, 256, 0, c->st>>>(nk, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>());
   CK(cub_call(c, [&](void* t, size_t& s) {
@@ -338,11 +345,11 @@ cudaError_t build_pattern(Ctx* c) {
   CK(ensure(c, c->ukeys, nk * 8));
   k_unique_write<<<bk, 256, 0, c->st>>>(nk, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>(), c->upos.as<int32_t>(),
                                         c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>());
-  int64_t nnz = 0;
-  CK(cudaMemcpyAsync(&nnz, c->nnz_dev.p, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  int64_t nnz = nk;   // upper bound until the single readback below
   if (c->world > 1) {
     // union of the ranks' patterns: every rank ends with the same sorted unique keys
+    CK(cudaMemcpyAsync(&nnz, c->nnz_dev.p, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
     int64_t mx = nnz;
     int64_t* dmx = c->nnz_dev.as<int64_t>() + 1;
     CK(cudaMemcpyAsync(dmx, &mx, 8, cudaMemcpyHostToDevice, c->st));
@@ -359,7 +366,7 @@ cudaError_t build_pattern(Ctx* c) {
     CK(ensure(c, c->ckeys2, all * 8));
     CK(ensure(c, c->uflag, all * 4)); CK(ensure(c, c->upos, all * 4)); CK(ensure(c, c->ukeys, all * 8));
     CK(cub_call(c, [&](void* t, size_t& s) {
-      return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)all, 0, 64, c->st);
+      return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)all, 0, 2 * sb + 1, c->st);
     }));
     const int ba = (int)((all + 255) / 256);
     k_unique_flags<<<ba, 256, 0, c->st>>>(all, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>());
@@ -368,39 +375,40 @@ cudaError_t build_pattern(Ctx* c) {
     }));
     k_unique_write<<<ba, 256, 0, c->st>>>(all, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>(),
                                           c->upos.as<int32_t>(), c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>());
-    CK(cudaMemcpyAsync(&nnz, c->nnz_dev.p, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    nnz = all;
   }
-  c->nnzb = nnz;
+  const int64_t cap = nnz;   // upper bound of the unique count
   CK(ensure(c, c->row_ptr, (c->m + 1) * 4));
-  CK(ensure(c, c->col, nnz * 4)); CK(ensure(c, c->upper_of, nnz * 4));
+  CK(ensure(c, c->col, cap * 4)); CK(ensure(c, c->upper_of, cap * 4));
   CK(ensure(c, c->diag_pos, c->m * 4));
-  const int bn = (int)((nnz + 255) / 256);
-  k_rows<<<bn, 256, 0, c->st>>>(nnz, c->ukeys.as<uint64_t>(), c->m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
-                                c->upper_of.as<int32_t>(), c->diag_pos.as<int32_t>());
-  {   // plan of the cluster-resident PCG (host needs the row structure once per pattern)
-    std::vector<int32_t> rp(c->m + 1);
-    CK(cudaMemcpyAsync(rp.data(), c->row_ptr.p, (c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    int32_t part[17];
-    c->cl_size = plan_cluster(rp.data(), c->m, 16, part, &c->cl_max_rows, &c->cl_max_nnz, &c->cl_smem);
-    if (c->cl_size) {
-      CK(ensure(c, c->part, 17 * 4));
-      CK(cudaMemcpyAsync(c->part.p, part, (c->cl_size + 1) * 4, cudaMemcpyHostToDevice, c->st));
-      CK(cudaStreamSynchronize(c->st));   // `part` is a host stack array
-    }
-  }
+  CK(ensure(c, c->part, 32 * 4));
+  PlanOut* plan = reinterpret_cast<PlanOut*>(c->nnz_dev.as<int64_t>() + 2);
+  const int bn = (int)((cap + 255) / 256);
+  k_rows<<<bn, 256, 0, c->st>>>(cap, c->nnz_dev.as<int64_t>(), c->ukeys.as<uint64_t>(), c->m, c->row_ptr.as<int32_t>(),
+                                c->col.as<int32_t>(), c->upper_of.as<int32_t>(), c->diag_pos.as<int32_t>(), sb);
+  launch_plan_cluster(c->row_ptr.as<int32_t>(), c->m, 16, plan, c->part.as<int32_t>(), c->st);
   CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
   CK(ensure(c, c->edge_slot, ((int64_t)c->m * c->prm.n_nbr + 1) * 4));
   CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
   k_slots<<<bt, 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, c->m, c->prm.n_nbr, c->nbr.as<int32_t>(),
-                                 c->nf, c->fidx.as<int32_t>(), c->ukeys.as<uint64_t>(), nnz, c->seg_slot.as<int32_t>(),
-                                 c->edge_slot.as<int32_t>(), c->feat_slot.as<int32_t>(), total);
+                                 c->nf, c->fidx.as<int32_t>(), c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>(),
+                                 c->seg_slot.as<int32_t>(), c->edge_slot.as<int32_t>(), c->feat_slot.as<int32_t>(), total,
+                                 sb);
   CK(cudaGetLastError());
   // chunk records and their (deterministic, sorted) contribution lists
   CK(ensure(c, c->records, (size_t)c->nchunk * rec_stride(K) * 4 + 16));
-  CK(build_contrib(c, c->seg_slot.as<int32_t>(), P, (int)nnz, c->slot_ptr, c->slot_src));
-  CK(build_contrib(c, c->seg_nodes.as<int32_t>(), K, c->m, c->node_ptr, c->node_src));
+  CK(build_contrib(c, c->seg_slot.as<int32_t>(), P, (int)cap, c->nnz_dev.as<int64_t>(), c->slot_ptr, c->slot_src));
+  CK(build_contrib(c, c->seg_nodes.as<int32_t>(), K, c->m, nullptr, c->node_ptr, c->node_src));
+  // the single host readback of the pattern build: nnz and the cluster plan
+  struct { int64_t nnz, pad; PlanOut plan; } info;
+  CK(cudaMemcpyAsync(&info, c->nnz_dev.p, sizeof(info), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  nnz = info.nnz;
+  c->nnzb = nnz;
+  c->cl_size = info.plan.cl_size;
+  c->cl_max_rows = info.plan.max_rows;
+  c->cl_max_nnz = info.plan.max_nnz;
+  c->cl_smem = (size_t)info.plan.smem;
   // accumulators and solver buffers
   const size_t m6 = 6 * (size_t)c->m;
   c->acc_floats = (size_t)nnz * (36 + 16 + 36) + m6 + 12 * (size_t)c->m + m6;
