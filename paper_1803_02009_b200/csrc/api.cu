@@ -594,24 +594,6 @@ static mis_status assemble(Ctx* c, bool dbg) {
     launch_assemble_points(c->K, a, c->num_sms, c->st);
   }
   TRY(c, cudaGetLastError());
-  {
-    ProfScope ps(c, P_REDUCE, 1);
-    ReduceArgs r;
-    r.records = c->records.as<float>();
-    r.rec_stride = rec_stride(c->K);
-    r.K = c->K;
-    r.nchunk = c->nchunk;
-    r.nnzb = c->nnzb;
-    r.m = c->m;
-    r.upper_of = c->upper_of.as<int32_t>();
-    r.slot_ptr = c->slot_ptr.as<int32_t>();
-    r.slot_src = c->slot_src.as<int32_t>();
-    r.node_ptr = c->node_ptr.as<int32_t>();
-    r.node_src = c->node_src.as<int32_t>();
-    r.acc = acc;
-    launch_reduce_records(r, c->st);
-  }
-  TRY(c, cudaGetLastError());
   if (c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0) {
     ProfScope ps(c, P_GRAPH, 1);
     AsmGraphArgs gA;
@@ -634,9 +616,33 @@ static mis_status assemble(Ctx* c, bool dbg) {
     launch_assemble_graph(gA, c->st);
     TRY(c, cudaGetLastError());
   }
-  if (c->world > 1) {
-    if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
-    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 8) != cudaSuccess) return MIS_E_NCCL;
+  {   // records (+ graph part) -> final H, b and energies
+    ProfScope ps(c, P_REDUCE, 1);
+    ReduceArgs r;
+    r.records = c->records.as<float>();
+    r.rec_stride = rec_stride(c->K);
+    r.K = c->K;
+    r.nchunk = c->nchunk;
+    r.nnzb = c->nnzb;
+    r.m = c->m;
+    r.upper_of = c->upper_of.as<int32_t>();
+    r.slot_ptr = c->slot_ptr.as<int32_t>();
+    r.slot_src = c->slot_src.as<int32_t>();
+    r.node_ptr = c->node_ptr.as<int32_t>();
+    r.node_src = c->node_src.as<int32_t>();
+    r.lower_of = c->lower_of.as<int32_t>();
+    r.w_data = c->prm.w_data;
+    r.w_pt = c->prm.w_point;
+    r.acc = acc;
+    r.Hval = c->Hval.as<float>();
+    r.rhs = c->rhs.as<float>();
+    launch_reduce_records(r, c->st);
+  }
+  TRY(c, cudaGetLastError());
+  if (c->world > 1) {   // H, b and the energies are linear in the per-rank sums: all-reduce them
+    if (nccl_allreduce_sum_f32(c, c->Hval.as<float>(), (size_t)c->nnzb * 36) != cudaSuccess) return MIS_E_NCCL;
+    if (nccl_allreduce_sum_f32(c, c->rhs.as<float>(), (size_t)c->m * 6) != cudaSuccess) return MIS_E_NCCL;
+    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 6) != cudaSuccess) return MIS_E_NCCL;
   }
   return MIS_OK;
 }

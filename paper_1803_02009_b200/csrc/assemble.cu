@@ -16,7 +16,7 @@
 // into 6x6 point-to-point blocks: sum of w_j w_l [-[a_j]x[a_l]x, [a_j]x; -[a_l]x, I].
 #include <cuda_runtime.h>
 
-#include "common.cuh"
+#include "solve_common.cuh"
 
 namespace mis {
 
@@ -390,18 +390,22 @@ __global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_poin
   }
 }
 
-// Deterministic slot-major reduction of the chunk records into the
-// accumulator layout read by the solvers: one warp per BSR entry (upper
-// entries gather their (chunk, pair) contributions in sorted order), one warp
-// per node (rhs and node moments), then energies.
+// Deterministic slot-major reduction of the chunk records, fused with the
+// finalisation of the normal equations (so the latency-bound solver only
+// streams its rows): one warp per upper BSR entry gathers its (chunk, pair)
+// contributions in sorted order, adds the K4/K5 graph block and writes
+//   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j));
+// one warp per node writes b_j; then the energies.
 __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
+  __shared__ float stage[8][88];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int P = r.K * (r.K + 1) / 2;
   const int RS = r.rec_stride;
+  float* st = stage[wib];
   if (gw < r.nnzb) {
     const int64_t e = gw;
-    if (r.upper_of[e] != e) return;   // lower-triangle entries mirror their upper partner
+    if (r.upper_of[e] != e) return;   // lower-triangle entries are written as mirrors
     float v0 = 0.f, v1 = 0.f;         // lane owns record floats lane and lane + 32 (< 52)
     for (int k = r.slot_ptr[e]; k < r.slot_ptr[e + 1]; ++k) {
       const int src = r.slot_src[k];
@@ -409,14 +413,18 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
       v0 += rec[lane];
       if (lane < 20) v1 += rec[32 + lane];
     }
-    // floats 0..35 -> data, 36..51 -> moments
-    if (lane < 32) {
-      if (lane < 36) r.acc.data[36 * e + lane] = v0;
-    }
-    if (lane < 20) {
-      const int f = 32 + lane;
-      if (f < 36) r.acc.data[36 * e + f] = v1;
-      else r.acc.mom[16 * e + (f - 36)] = v1;
+    st[lane] = v0;                                    // D (36) | Mo (16) | G (36)
+    if (lane < 20) st[32 + lane] = v1;
+    st[52 + lane] = r.acc.graph[36 * e + lane];
+    if (lane < 4) st[84 + lane] = r.acc.graph[36 * e + 32 + lane];
+    __syncwarp();
+    const int lo = r.lower_of[e];
+    const bool diag = lo < 0;
+    for (int l = lane; l < 36; l += 32) {
+      const int i = l / 6, j = l - 6 * (l / 6);
+      const float h = block_entry(st, st + 36, st + 52, diag, i, j, r.w_data, r.w_pt);
+      r.Hval[36 * e + l] = h;
+      if (!diag) r.Hval[36 * (int64_t)lo + 6 * j + i] = h;
     }
     return;
   }
@@ -429,8 +437,19 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
         const int src = r.node_src[k];
         v += r.records[(int64_t)(src / r.K) * RS + 52 * P + 18 * (src % r.K) + lane];
       }
-    if (lane < 6) r.acc.rhs_data[6 * n + lane] = v;
-    else if (lane < 18) r.acc.node_mom[12 * n + (lane - 6)] = v;
+    st[lane] = v;
+    __syncwarp();
+    if (lane < 6) {   // b = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs
+      const float* Nm = st + 6;
+      float pt;
+      if (lane < 3) {
+        const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
+        pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
+      } else {
+        pt = Nm[9 + (lane - 3)];
+      }
+      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + r.acc.rhs_graph[6 * n + lane];
+    }
     return;
   }
   const int64_t c0 = (gn - r.m) * 32;

@@ -96,7 +96,11 @@ struct ReduceArgs {
   const int32_t* slot_src;    // (chunk * P + pair)
   const int32_t* node_ptr;    // m+1
   const int32_t* node_src;    // (chunk * K + slot)
-  AccView acc;
+  const int32_t* lower_of;    // upper entry -> its mirror (-1 on the diagonal)
+  float w_data, w_pt;
+  AccView acc;                // graph / rhs_graph (K4/K5) in, energies out
+  float* Hval;                // nnzb*36 final blocks (both triangles)
+  float* rhs;                 // 6m final right-hand side
 };
 void launch_reduce_records(const ReduceArgs& r, cudaStream_t s);
 

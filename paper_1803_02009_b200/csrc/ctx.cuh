@@ -50,7 +50,8 @@ struct Ctx {
   // ---- pattern
   int64_t nnzb = 0, ncand = 0;
   bool pattern_valid = false;
-  DBuf ckeys, ckeys2, uflag, upos, ukeys, row_ptr, col, diag_pos, upper_of, seg_slot, edge_slot, feat_slot, nnz_dev;
+  DBuf ckeys, ckeys2, uflag, upos, ukeys, row_ptr, col, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot,
+      nnz_dev;
   // per-chunk records and their contribution lists (deterministic reduction)
   DBuf records, ck_key, ck_val, ck_key2, ck_val2, slot_ptr, slot_src, node_ptr, node_src;
 

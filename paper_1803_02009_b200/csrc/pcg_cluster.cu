@@ -108,28 +108,17 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (t <= cs) spart[t] = a.part[t];
   for (int i = t; i <= nr; i += kCT) lrp[i] = a.row_ptr[r0 + i] - e0;
   __syncthreads();
-  for (int w = t; w < 6 * ne; w += kCT) {   // one thread per (entry, row)
-    const int k = w / 6, rr = w - 6 * k;
-    const int e = e0 + k;
-    const int c = a.col[e];
-    if (rr == 0) col[k] = c;
-    const int64_t u = a.upper_of[e];
-    float row[6];
-    block_row(a.acc, a.w_data, a.w_pt, u, a.diag_pos[c] == e, u != e, rr, row);
-    float* out = H + 36 * (size_t)k + 6 * rr;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) out[q] = row[q];
-    if (a.write_global)
-#pragma unroll
-      for (int q = 0; q < 6; ++q) a.Hval[36 * (int64_t)e + 6 * rr + q] = row[q];
+  {   // stream this CTA's rows of the final H (built by the record reduction) into shared memory
+    const float4* src = reinterpret_cast<const float4*>(a.Hval + 36 * (int64_t)e0);
+    float4* dst = reinterpret_cast<float4*>(H);
+    for (int q = t; q < 9 * ne; q += kCT) dst[q] = src[q];
+    for (int k = t; k < ne; k += kCT) col[k] = a.col[e0 + k];
   }
   for (int i = t; i < 6 * nr; i += kCT) {
-    const float b = rhs_entry(a.acc, a.w_data, a.w_pt, 6 * (int64_t)r0 + i);
-    r[i] = b;
+    r[i] = a.rhs[6 * (int64_t)r0 + i];
     x[i] = 0.f;
     p[i] = 0.f;
     Ap[i] = 0.f;
-    if (a.write_global) a.rhs[6 * (int64_t)r0 + i] = b;
   }
   __syncthreads();
   if (stamp) ts[1] = gtimer();

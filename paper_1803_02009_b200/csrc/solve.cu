@@ -36,21 +36,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int m = a.m, n6 = 6 * m;
 
-  // ---- phase 0: H (both triangles) and b
-  for (int64_t e = tid; e < a.nnzb; e += nth) {
-    const int64_t u = a.upper_of[e];
-    const int c = a.col[e];
-    float B[36];
-    upper_block(a.acc, a.w_data, a.w_pt, u, a.diag_pos[c] == e, B);
-    float* out = a.Hval + 36 * e;
-    if (u == e) {
-      for (int i = 0; i < 36; ++i) out[i] = B[i];
-    } else {
-      for (int r = 0; r < 6; ++r)
-        for (int cc = 0; cc < 6; ++cc) out[6 * r + cc] = B[6 * cc + r];
-    }
-  }
-  for (int64_t i = tid; i < n6; i += nth) a.rhs[i] = rhs_entry(a.acc, a.w_data, a.w_pt, i);
+  // ---- phase 0: H (both triangles) and b are final (record reduction); clear the dot slots
   if (tid < 2 * a.pcg_iters + 4) a.dots[tid] = 0.0;
   grid.sync();
   if (a.pcg_iters <= 0 && !a.do_update) return;

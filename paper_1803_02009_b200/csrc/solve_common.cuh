@@ -43,6 +43,30 @@ __device__ __forceinline__ void upper_block(const AccView& acc, float w_data, fl
   for (int r = 0; r < 3; ++r) B[6 * (3 + r) + 3 + r] += w_pt * s0;
 }
 
+// Entry (i, j) of the block B(j, l), j <= l, from its summed data D (36; upper
+// triangle only when diag), moments Mo (16) and graph part G (36).
+__device__ __forceinline__ float block_entry(const float* D, const float* Mo, const float* G, bool diag, int i, int j,
+                                             float w_data, float w_pt) {
+  const float d = diag ? D[6 * min(i, j) + max(i, j)] : D[6 * i + j];
+  float pt;
+  if (i < 3 && j < 3) {   // tr(S) I - S^T, S = sum s a_j a_l^T
+    const float trS = diag ? Mo[0] + Mo[5] + Mo[10] : Mo[0] + Mo[5] + Mo[10];
+    const float Sji = diag ? Mo[4 * min(i, j) + max(i, j)] : Mo[4 * j + i];
+    pt = (i == j ? trS : 0.f) - Sji;
+  } else if (i < 3) {     // [s_j]x (i, j-3), s_j = Mo[p][3]
+    const int c = j - 3;
+    pt = (i == c) ? 0.f : ((c == (i + 1) % 3) ? -Mo[4 * ((i + 2) % 3) + 3] : Mo[4 * ((i + 1) % 3) + 3]);
+  } else if (j < 3) {     // -[s_l]x (i-3, j), s_l = Mo[3][q] (= Mo[q][3] on the diagonal)
+    const int rr = i - 3;
+    const int q1 = (rr + 2) % 3, q2 = (rr + 1) % 3;
+    const float sl1 = diag ? Mo[4 * q1 + 3] : Mo[12 + q1], sl2 = diag ? Mo[4 * q2 + 3] : Mo[12 + q2];
+    pt = (rr == j) ? 0.f : ((j == (rr + 1) % 3) ? sl1 : -sl2);
+  } else {
+    pt = (i == j) ? Mo[15] : 0.f;
+  }
+  return w_data * d + G[6 * i + j] + w_pt * pt;
+}
+
 // Row r of the block B(j,l) of upper slot u (tr: row r of B^T), same formula as
 // upper_block; one thread per (entry, row) keeps the loads parallel.
 __device__ __forceinline__ void block_row(const AccView& acc, float w_data, float w_pt, int64_t u, bool diag, bool tr,

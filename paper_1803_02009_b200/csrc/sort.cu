@@ -239,7 +239,7 @@ __device__ __forceinline__ int64_t find_key(const uint64_t* u, int64_t nnz, uint
 }
 
 __global__ void k_rows(int64_t cap, const int64_t* nnz_dev, const uint64_t* u, int m, int32_t* row_ptr, int32_t* col,
-                       int32_t* upper_of, int32_t* diag_pos, int sb) {
+                       int32_t* upper_of, int32_t* lower_of, int32_t* diag_pos, int sb) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nnz = *nnz_dev;
   if (e >= nnz || e >= cap) return;
@@ -251,6 +251,8 @@ __global__ void k_rows(int64_t cap, const int64_t* nnz_dev, const uint64_t* u, i
     for (int q = r + 1; q <= m; ++q) row_ptr[q] = (int32_t)nnz;
   if (r == cc) diag_pos[r] = (int32_t)e;
   upper_of[e] = (r <= cc) ? (int32_t)e : (int32_t)find_key(u, nnz, pkey(cc, r, sb));
+  if (r == cc) lower_of[e] = -1;                       // diagonal: no mirror
+  else if (r > cc) lower_of[upper_of[e]] = (int32_t)e;   // the upper partner's mirror
 }
 
 __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr, int nf,
@@ -379,13 +381,14 @@ cudaError_t build_pattern(Ctx* c) {
   }
   const int64_t cap = nnz;   // upper bound of the unique count
   CK(ensure(c, c->row_ptr, (c->m + 1) * 4));
-  CK(ensure(c, c->col, cap * 4)); CK(ensure(c, c->upper_of, cap * 4));
+  CK(ensure(c, c->col, cap * 4)); CK(ensure(c, c->upper_of, cap * 4)); CK(ensure(c, c->lower_of, cap * 4));
   CK(ensure(c, c->diag_pos, c->m * 4));
   CK(ensure(c, c->part, 32 * 4));
   PlanOut* plan = reinterpret_cast<PlanOut*>(c->nnz_dev.as<int64_t>() + 2);
   const int bn = (int)((cap + 255) / 256);
   k_rows<<<bn, 256, 0, c->st>>>(cap, c->nnz_dev.as<int64_t>(), c->ukeys.as<uint64_t>(), c->m, c->row_ptr.as<int32_t>(),
-                                c->col.as<int32_t>(), c->upper_of.as<int32_t>(), c->diag_pos.as<int32_t>(), sb);
+                                c->col.as<int32_t>(), c->upper_of.as<int32_t>(), c->lower_of.as<int32_t>(),
+                                c->diag_pos.as<int32_t>(), sb);
   launch_plan_cluster(c->row_ptr.as<int32_t>(), c->m, 16, plan, c->part.as<int32_t>(), c->st);
   CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
   CK(ensure(c, c->edge_slot, ((int64_t)c->m * c->prm.n_nbr + 1) * 4));
