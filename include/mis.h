@@ -63,6 +63,8 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
 #define MIS_F_NO_GRAPH     2u   /* do not capture the GN loop in a CUDA graph                    */
 #define MIS_F_GRID_SOLVER  4u   /* force the grid-wide PCG kernel (else the cluster-resident one
                                    whenever the system fits in one cluster's shared memory)       */
+#define MIS_F_STANDARD_PCG 8u   /* cluster kernel: textbook PCG recurrences (2 barriers/iteration)
+                                   instead of the pipelined variant (1 barrier/iteration)         */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {

@@ -680,6 +680,7 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.max_nnz = c->cl_max_nnz;
   s.smem_bytes = c->cl_smem;
   s.write_global = update ? 0 : 1;
+  s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) ? 0 : 1;
   s.tstamp = c->tstamp.as<unsigned long long>();
   return s;
 }

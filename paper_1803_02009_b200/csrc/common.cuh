@@ -148,7 +148,8 @@ struct SolveArgs {
   const int32_t* part;        // cluster_size+1 row boundaries (balanced by nnz)
   int max_rows, max_nnz;      // per-CTA maxima (uniform smem layout)
   size_t smem_bytes;
-  int write_global;           // also write Hval / rhs to global memory (debug)
+  int write_global;           // also write x to global memory (debug)
+  int pipelined;              // cluster variant: pipelined PCG (1 barrier / iteration) instead of standard
   unsigned long long* tstamp; // 8 %globaltimer stamps of the phases (rank 0, thread 0)
 };
 

@@ -24,14 +24,16 @@ namespace mis {
 constexpr int kCT = 1024;          // threads per CTA
 constexpr int kMaxCluster = 16;
 
+constexpr int kNVec = 10;         // local vectors (pipelined PCG needs 10, standard 6)
+
 struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
   size_t dots, vec, zf, mi, col, own, h, total;
   __host__ __device__ CLay(int max_rows, int max_nnz, int m) {
-    dots = 0;                                        // double partA[16], partB[16], partF[16], red[32]
-    vec = dots + sizeof(double) * (3 * kMaxCluster + 32);
+    dots = 0;                                        // double partA..partE[16], red[32]
+    vec = dots + sizeof(double) * (5 * kMaxCluster + 64);
     const size_t nv = (size_t)max_rows * 6;
-    zf = vec + sizeof(float) * 6 * nv;               // x r z p Ap Az, then the replicated full z
-    mi = zf + sizeof(float) * 6 * (size_t)m;
+    zf = vec + sizeof(float) * kNVec * nv;           // local vectors, then two replicated full vectors
+    mi = zf + sizeof(float) * 2 * 6 * (size_t)m;
     col = mi + sizeof(float) * 36 * max_rows;
     own = col + sizeof(int) * max_nnz;
     h = (own + sizeof(int) * (max_nnz + 1) + 15) & ~(size_t)15;
@@ -39,23 +41,6 @@ struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
   }
 };
 
-__device__ __forceinline__ double cta_sum(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  double s = 0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < kCT / 32; ++i) s += red[i];
-  return s;   // thread 0
-}
-
-// thread 0 of every CTA writes its partial into slot [rank] of `slot` in all CTAs
-__device__ __forceinline__ void publish(cg::cluster_group& cl, double* slot, double v, int rank, int cs) {
-  if (threadIdx.x == 0)
-    for (int c = 0; c < cs; ++c) cl.map_shared_rank(slot, c)[rank] = v;
-}
 
 // push this CTA's z slice into every CTA's full-length copy (remote stores,
 // made visible by the following cluster barrier)
@@ -68,10 +53,155 @@ __device__ __forceinline__ void replicate(cg::cluster_group& cl, float* zf, cons
   }
 }
 
+// xor-butterfly sum: every lane ends with the bitwise-same value (IEEE + is commutative)
+__device__ __forceinline__ double warp_sum_all(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CTA sum of v, published by warp 0 (lane c writes CTA c's slot[rank]); no serial loops
+__device__ __forceinline__ void cta_publish(cg::cluster_group& cl, double v, double* red, double* slot, int rank,
+                                            int cs) {
+  v = warp_sum_all(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const double x = warp_sum_all(red[l]);   // kCT / 32 == 32 warps
+    if (l < cs) cl.map_shared_rank(slot, l)[rank] = x;
+  }
+}
+
+// sum of the cs published partials, identical in every thread of every CTA
 __device__ __forceinline__ double gather_sum(const double* slot, int cs) {
-  double s = 0;
-  for (int c = 0; c < cs; ++c) s += slot[c];
-  return s;
+  const int l = threadIdx.x & 31;
+  return warp_sum_all(l < cs ? slot[l] : 0.0);
+}
+
+
+// out = (H + lambda I) v for the CTA's rows; v read from the replicated full vector Z
+__device__ __forceinline__ void spmv_local(const int* lrp, const int* col, const float* H, const float* Z,
+                                           const float* v_local, float lambda, float* out, int nr) {
+  const int n_items = 12 * nr;
+  for (int base = 0; base < n_items; base += kCT) {
+    const int item = base + threadIdx.x;
+    const bool act = item < n_items;
+    const int i = item / 12, c = (item % 12) >> 1, hf = item & 1;
+    float v = 0.f;
+    if (act)
+      for (int k = lrp[i] + hf; k < lrp[i + 1]; k += 2) {
+        const float* zr = Z + 6 * col[k];
+        const float* h = H + 36 * (size_t)k + 6 * c;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) v = fmaf(h[b], zr[b], v);
+      }
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    if (act && hf == 0) out[6 * i + c] = fmaf(lambda, v_local[6 * i + c], v);
+  }
+}
+
+// Pipelined PCG (Ghysels & Vanroose 2014): the same Krylov iterates as PCG in
+// exact arithmetic, with the two dot products of an iteration reduced together
+// and overlapped with the preconditioner + replication of m = M w, so each
+// iteration needs ONE cluster barrier:
+//   gamma = (r, u), delta = (w, u), m = M w   [publish, replicate]   barrier
+//   beta = gamma / gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev)
+//   n = A m; z = n + beta z; q = m + beta q; s = w + beta s; p = u + beta p;
+//   x += alpha p; r -= alpha s; u -= alpha q; w -= alpha z
+// gamma == r.z and delta - beta gamma/alpha_prev == p.A p, so the oracle's
+// MIRROR early stops (r.z == 0, p.Ap <= 0) are the same tests.
+__device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_group& cl, unsigned char* sm,
+                                              const CLay& L, int rank, int cs, int r0, int nr, const int* lrp,
+                                              const int* col, const float* H, const float* Mi, double* g_last,
+                                              double* g_first) {
+  const int t = threadIdx.x, nv = a.max_rows * 6, n6 = 6 * nr;
+  double* base = reinterpret_cast<double*>(sm + L.dots);
+  double* gam[2] = {base, base + kMaxCluster};
+  double* del[2] = {base + 3 * kMaxCluster, base + 4 * kMaxCluster};   // partF (= base + 2*16) stays free
+  double* red = base + 5 * kMaxCluster;
+  float* x = reinterpret_cast<float*>(sm + L.vec);
+  float* r = x + nv;
+  float* u = r + nv;
+  float* w = u + nv;
+  float* mm = w + nv;
+  float* nn = mm + nv;
+  float* zz = nn + nv;
+  float* q = zz + nv;
+  float* s = q + nv;
+  float* p = s + nv;
+  float* Z[2] = {reinterpret_cast<float*>(sm + L.zf), reinterpret_cast<float*>(sm + L.zf) + 6 * a.m};
+  // u = M r; z = q = s = p = 0   (x = 0, r = b from phase 0)
+  for (int e = t; e < n6; e += kCT) {
+    const int i = e / 6, c = e - 6 * (e / 6);
+    float v = 0.f;
+    for (int b = 0; b < 6; ++b) v = fmaf(Mi[36 * i + 6 * c + b], r[6 * i + b], v);
+    u[e] = v;
+    zz[e] = 0.f; q[e] = 0.f; s[e] = 0.f; p[e] = 0.f;
+  }
+  __syncthreads();
+  replicate(cl, Z[0], u, r0, nr, cs);
+  cl.sync();
+  spmv_local(lrp, col, H, Z[0], u, a.lambda, w, nr);   // w = A u
+  __syncthreads();
+  double gprev = 1.0, aprev = 1.0, g0 = 0.0, g = 0.0;
+  for (int it = 0; it < a.pcg_iters; ++it) {
+    double dg = 0.0, dd = 0.0;
+    for (int e = t; e < n6; e += kCT) {
+      const int i = e / 6, c = e - 6 * (e / 6);
+      dg += (double)r[e] * (double)u[e];
+      dd += (double)w[e] * (double)u[e];
+      float v = 0.f;
+      for (int b = 0; b < 6; ++b) v = fmaf(Mi[36 * i + 6 * c + b], w[6 * i + b], v);
+      mm[e] = v;
+    }
+    __syncthreads();
+    const int nb = (it + 1) & 1;
+    replicate(cl, Z[nb], mm, r0, nr, cs);
+    {   // both dots in one CTA reduction, published by warp 0 lanes (lane c -> CTA c)
+      dg = warp_sum_all(dg);
+      dd = warp_sum_all(dd);
+      const int wi = t >> 5, l = t & 31;
+      __syncthreads();
+      if (l == 0) { red[wi] = dg; red[32 + wi] = dd; }
+      __syncthreads();
+      if (wi == 0) {
+        const double sg = warp_sum_all(red[l]), sd = warp_sum_all(red[32 + l]);
+        if (l < cs) {
+          cl.map_shared_rank(gam[it & 1], l)[rank] = sg;
+          cl.map_shared_rank(del[it & 1], l)[rank] = sd;
+        }
+      }
+    }
+    cl.sync();
+    g = gather_sum(gam[it & 1], cs);
+    const double d = gather_sum(del[it & 1], cs);
+    if (it == 0) g0 = g;
+    if (g == 0.0) break;
+    const double beta = it == 0 ? 0.0 : g / gprev;
+    const double den = it == 0 ? d : d - beta * g / aprev;
+    if (!(den > 0.0)) break;
+    const double alpha = g / den;
+    spmv_local(lrp, col, H, Z[nb], mm, a.lambda, nn, nr);   // n = A m
+    __syncthreads();
+    const float fb = (float)beta, fa = (float)alpha;
+    for (int e = t; e < n6; e += kCT) {
+      zz[e] = fmaf(fb, zz[e], nn[e]);
+      q[e] = fmaf(fb, q[e], mm[e]);
+      s[e] = fmaf(fb, s[e], w[e]);
+      p[e] = fmaf(fb, p[e], u[e]);
+      x[e] = fmaf(fa, p[e], x[e]);
+      r[e] = fmaf(-fa, s[e], r[e]);
+      u[e] = fmaf(-fa, q[e], u[e]);
+      w[e] = fmaf(-fa, zz[e], w[e]);
+    }
+    __syncthreads();
+    gprev = g;
+    aprev = alpha;
+  }
+  *g_last = g;
+  *g_first = g0;
 }
 
 __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
@@ -81,7 +211,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   double* partA = reinterpret_cast<double*>(sm + L.dots);
   double* partB = partA + kMaxCluster;
   double* partF = partB + kMaxCluster;
-  double* red = partF + kMaxCluster;
+  double* red = partF + 3 * kMaxCluster;   // partC, partD (pipelined PCG) sit between
   const int nv = a.max_rows * 6;
   float* x = reinterpret_cast<float*>(sm + L.vec);
   float* r = x + nv;
@@ -164,6 +294,11 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   }
   __syncthreads();
   if (stamp) ts[2] = gtimer();
+  double rz = 0.0, rz0 = 0.0;
+  if (a.pipelined) {
+    pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0);
+    if (stamp) ts[3] = ts[2];
+  } else {
   double my = 0.0;
   for (int q = t; q < 6 * nr; q += kCT) {
     const int i = q / 6, c = q % 6;
@@ -175,12 +310,12 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   __syncthreads();
   replicate(cl, zf, z, r0, nr, cs);
   if (stamp) ts[6] = gtimer();
-  double s = cta_sum(my, red);
-  publish(cl, partA, s, rank, cs);
+  cta_publish(cl, my, red, partA, rank, cs);
   if (stamp) ts[7] = gtimer();
   cl.sync();
-  double rz = gather_sum(partA, cs), rz_prev = 1.0;
-  const double rz0 = rz;
+  rz = gather_sum(partA, cs);
+  double rz_prev = 1.0;
+  rz0 = rz;
   if (stamp) ts[3] = gtimer();
   int done = 0;
   const int n_items = 12 * nr, passes = (n_items + kCT - 1) / kCT;
@@ -217,8 +352,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
       Ap[q] = apn;
       my += (double)pn * (double)apn;
     }
-    s = cta_sum(my, red);
-    publish(cl, partB, s, rank, cs);
+    cta_publish(cl, my, red, partB, rank, cs);
     if (st1) ts[10] = gtimer();
     cl.sync();   // (B) p.Ap known everywhere; every CTA is done reading z
     if (st1) ts[11] = gtimer();
@@ -241,14 +375,14 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     __syncthreads();
     if (st1) ts[12] = gtimer();
     replicate(cl, zf, z, r0, nr, cs);
-    s = cta_sum(my, red);
-    publish(cl, partA, s, rank, cs);
+    cta_publish(cl, my, red, partA, rank, cs);
     if (st1) ts[13] = gtimer();
     cl.sync();   // (A) r.z known everywhere; z complete and replicated
     if (st1) ts[14] = gtimer();
     rz_prev = rz;
     rz = gather_sum(partA, cs);
   }
+  }   // standard PCG
   if (stamp) ts[4] = gtimer();
   if (rank == 0 && t == 0) a.rep_res[a.gn_it] = (float)(rz0 > 0 ? sqrt(fabs(rz / rz0)) : 0.0);
   if (a.write_global)
@@ -258,11 +392,10 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     return;
   }
   // ---- node update; a non-finite step anywhere rolls the whole update back
-  my = 0.0;
+  double bad = 0.0;
   for (int q = t; q < 6 * nr; q += kCT)
-    if (!isfinite(x[q])) my = 1.0;
-  s = cta_sum(my, red);
-  publish(cl, partF, s, rank, cs);
+    if (!isfinite(x[q])) bad = 1.0;
+  cta_publish(cl, bad, red, partF, rank, cs);
   cl.sync();
   if (gather_sum(partF, cs) != 0.0) {
     if (rank == 0 && t == 0) atomicOr(a.numeric_flag, 1);

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("MIS_LIB_PATH", os.path.join(_HERE, "libmis.so"))   # 
 
 MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
-MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH, MIS_F_GRID_SOLVER = 1, 2, 4
+MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 2, 4, 8
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
 
