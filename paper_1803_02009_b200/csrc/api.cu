@@ -99,7 +99,7 @@ struct NcclApi {
 };
 // ncclDataType_t / ncclRedOp_t values (nccl.h, NCCL 2.x)
 enum { kNcclInt64 = 4, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8 };
-enum { kNcclSum = 0, kNcclMax = 2 };
+enum { kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 
 static NcclApi& nccl() {
   static NcclApi api;
@@ -897,6 +897,7 @@ static FuseArgs fuse_args(Ctx* c, const float* rgb, int32_t frame) {
   a.pixkey = c->pixkey.as<unsigned long long>();
   a.pix = c->pix.as<int32_t>();
   a.why = c->why.as<uint8_t>();
+  a.rank_tag = c->world > 1 ? ((uint32_t)c->rank << 27) : 0u;
   return a;
 }
 
@@ -909,6 +910,12 @@ static mis_status fuse_register(Ctx* c, const float* rgb, int32_t frame) {
   ProfScope ps(c, P_FREG, c->n > 0 ? 1 : 0);
   launch_fuse_register(fuse_args(c, rgb, frame), c->st);
   TRY(c, cudaGetLastError());
+  if (c->world > 1) {   // the exclusive winner per pixel over all ranks' shards (keys carry the rank)
+    if (c->n >= (1 << 27) || c->world > 32) return fail(c, MIS_E_ARG, "sharded fusion: > 2^27 points or > 32 ranks");
+    if (nccl_ret(c, nccl().AllReduce(c->pixkey.p, c->pixkey.p, px, kNcclUint64, kNcclMin, c->nccl_comm, c->st)) !=
+        cudaSuccess)
+      return MIS_E_NCCL;
+  }
   return MIS_OK;
 }
 
@@ -962,13 +969,14 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   TRY(c, cudaMemcpyAsync(&n_lift, counts + 2 * nbk + 1, 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(&n_reg, cnt, 8, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
+  if (c->world > 1 && c->rank != 0) n_lift = 0;   // sharded model: rank 0 owns the lifted points
   if (c->n + n_lift > c->cap) {
     *n_out = c->n;
     return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
   }
   const int64_t base = c->n;
-  ProfScope ps(c, P_LIFT, 1 + (n_lift > 0));
-  launch_lift_write(a, counts + nbk + 1, nbk, base, c->ids_dev.as<long long>(), c->st);
+  ProfScope ps(c, P_LIFT, n_lift > 0 ? 2 : 0);
+  if (n_lift > 0) launch_lift_write(a, counts + nbk + 1, nbk, base, c->ids_dev.as<long long>(), c->st);
   ModelView md = model_view(c);
   if (n_lift > 0) {
     launch_skin(n_lift, md.px + base, md.py + base, md.pz + base, 1, c->g.as<float>(), c->m, c->K, md.kidx + base,

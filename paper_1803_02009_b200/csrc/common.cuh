@@ -179,6 +179,7 @@ struct FuseArgs {
   unsigned long long* pixkey; // H*W
   int32_t* pix;               // n
   uint8_t* why;               // n (nullable)
+  uint32_t rank_tag;          // rank << 27 in the key's index bits (0 on one GPU): keys unique across ranks
 };
 void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);

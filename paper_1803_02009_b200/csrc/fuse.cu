@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
               why |= 32;
               pix = py * f.W + px;
               const unsigned long long key =
-                  ((unsigned long long)(dz * 1e8) << 32) | (unsigned long long)(uint32_t)i;
+                  ((unsigned long long)(dz * 1e8) << 32) | (unsigned long long)(a.rank_tag | (uint32_t)i);
               atomicMin(a.pixkey + pix, key);
             }
           }
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
   if (i >= a.md.n) return;
   const int32_t pix = a.pix[i];
   if (pix < 0) return;
-  if ((uint32_t)(a.pixkey[pix] & 0xffffffffull) != (uint32_t)i) return;
+  if ((uint32_t)(a.pixkey[pix] & 0xffffffffull) != (a.rank_tag | (uint32_t)i)) return;
   const FrameView& f = a.fr;
   const int px = pix % f.W, py = pix / f.W;
   double N[3], q[3];
