@@ -20,6 +20,10 @@
 
 namespace mis {
 
+#ifndef MIS_K3_SPLIT
+#define MIS_K3_SPLIT 2   // 2: split each tile's batch into halves across lanes (measured best at K=4)
+#endif
+
 template <int K>
 struct Lay {
   static constexpr int CD = 6 * K + 1;
@@ -34,15 +38,26 @@ struct Lay {
   static constexpr int NT = TD + TE;
   static constexpr int R = (NT + 31) / 32;           // tiles per lane
   static constexpr int P = K * (K + 1) / 2;
+  // work items = (tile, batch half): 2 NT items over 32 lanes balance better than NT
+  // (K=4: 86 items = 3 rounds of 16 points instead of 2 rounds of 32); needs 2 NT tile
+  // dumps to fit the warp's row buffer at commit
+  static constexpr int SPLIT = (MIS_K3_SPLIT == 2 && 2 * NT * 16 <= 32 * FSP) ? 2 : 1;
+  static constexpr int NI = NT * SPLIT;
+  static constexpr int RI = (NI + 31) / 32;          // items per lane
+  static constexpr int PS = 32 / SPLIT;              // points per item per batch
 };
 
 constexpr int kWarps = 8;
+#ifndef MIS_K3_MINB
+#define MIS_K3_MINB 2   // resident blocks per SM the register budget is sized for
+#endif
 #ifndef MIS_GUARD_SCALE
 #define MIS_GUARD_SCALE 1.0f
 #endif
-// Guard bands around every fp32 decision, each ~3-10x the fp32
-// error bound: u, v <= ~3.5e-4 px at 640 px; |v~ - q| <= ~3e-5 mm; n~.N <= ~1e-6.
-constexpr float kGuardPx = 1e-3f * MIS_GUARD_SCALE;     // rounding of u, v (pixels)
+// Guard bands around every fp32 decision, each >=3x the fp32
+// error bound: u, v <= ~1.5e-4 px (x_hat = v + small correction, then R x_hat + T
+// and one division); |v~ - q| <= ~3e-5 mm; n~.N <= ~1e-6.
+constexpr float kGuardPx = 5e-4f * MIS_GUARD_SCALE;     // rounding of u, v (pixels)
 constexpr float kGuardRel = 2e-5f * MIS_GUARD_SCALE;    // distance gate (relative to eps_d)
 constexpr float kGuardCos = 1e-5f * MIS_GUARD_SCALE;    // angle gate (cosine)
 
@@ -141,10 +156,27 @@ __device__ __noinline__ void assoc_fp64(const Fp64Args* __restrict__ pa, int64_t
   *pix_out = py * W_ + px;
 }
 
+// A point's inputs, loaded one batch ahead (software prefetch: the global loads
+// of batch b+1 are in flight while batch b is warped and accumulated).
+template <int K>
+struct PointIn {
+  float v[3], n[3], w[K];
+};
+
+template <int K>
+__device__ __forceinline__ void load_point(const ModelView& md, int64_t i, bool act, PointIn<K>& p) {
+  if (!act) return;
+  p.v[0] = md.px[i]; p.v[1] = md.py[i]; p.v[2] = md.pz[i];
+  p.n[0] = md.nx[i]; p.n[1] = md.ny[i]; p.n[2] = md.nz[i];
+#pragma unroll
+  for (int s = 0; s < K; ++s) p.w[s] = md.kw[s * md.cap + i];
+}
+
 // One lane, one point: warp, associate, write the factor row (zeros if not associated).
 template <int K, bool DBG>
-__device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, bool act, const float* __restrict__ ND,
-                                          const int32_t* nodes, float* __restrict__ row) {
+__device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, bool act, const PointIn<K>& pin,
+                                          const float* __restrict__ ND, const int32_t* nodes,
+                                          float* __restrict__ row) {
   using L = Lay<K>;
   bool assoc = false;
   int pix = -1;
@@ -152,12 +184,12 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
   if (act) {
     const ModelView& md = a.md;
     const FrameView& fr = a.fr;
-    const float v0 = md.px[i], v1 = md.py[i], v2 = md.pz[i];
-    const float n0 = md.nx[i], n1 = md.ny[i], n2 = md.nz[i];
+    const float v0 = pin.v[0], v1 = pin.v[1], v2 = pin.v[2];
+    const float n0 = pin.n[0], n1 = pin.n[1], n2 = pin.n[2];
     float wn[K], ax[K], ay[K], az[K];
     float W = 0.f;
 #pragma unroll
-    for (int s = 0; s < K; ++s) { wn[s] = md.kw[s * md.cap + i]; W += wn[s]; }
+    for (int s = 0; s < K; ++s) { wn[s] = pin.w[s]; W += wn[s]; }
     if (W > 0.f) {
       const float iW = 1.0f / W;
       float x0 = 0, x1 = 0, x2 = 0, m0 = 0, m1 = 0, m2 = 0;
@@ -169,13 +201,18 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
         ax[s] = nd[0] * d0 + nd[1] * d1 + nd[2] * d2;
         ay[s] = nd[3] * d0 + nd[4] * d1 + nd[5] * d2;
         az[s] = nd[6] * d0 + nd[7] * d1 + nd[8] * d2;
-        x0 += wn[s] * (ax[s] + nd[12] + nd[9]);
-        x1 += wn[s] * (ay[s] + nd[13] + nd[10]);
-        x2 += wn[s] * (az[s] + nd[14] + nd[11]);
+        // x_hat = sum w (a + g + t) = v + sum w ((R - I) d + t)  (sum w = 1): the correction is
+        // small, so its fp32 rounding is ~100x below that of summing ~60 mm terms
+        x0 += wn[s] * ((ax[s] - d0) + nd[9]);
+        x1 += wn[s] * ((ay[s] - d1) + nd[10]);
+        x2 += wn[s] * ((az[s] - d2) + nd[11]);
         m0 += wn[s] * (nd[0] * n0 + nd[1] * n1 + nd[2] * n2);
         m1 += wn[s] * (nd[3] * n0 + nd[4] * n1 + nd[5] * n2);
         m2 += wn[s] * (nd[6] * n0 + nd[7] * n1 + nd[8] * n2);
       }
+      x0 += v0;
+      x1 += v1;
+      x2 += v2;
       const float* R = fr.R;
       float vt[3] = {R[0] * x0 + R[1] * x1 + R[2] * x2 + fr.T[0], R[3] * x0 + R[4] * x1 + R[5] * x2 + fr.T[1],
                      R[6] * x0 + R[7] * x1 + R[8] * x2 + fr.T[2]};
@@ -277,7 +314,7 @@ __device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, boo
 }
 
 template <int K, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_points(AsmPointsArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(AsmPointsArgs a) {
   using L = Lay<K>;
   constexpr int P = L::P;
   constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
@@ -316,16 +353,18 @@ __global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_poin
     if (d >= 0) perm[d] = (int16_t)q;
   }
   __syncthreads();
-  // static ownership: lane owns tiles lane, lane + 32, ...
-  int offA[L::R], offB[L::R];
-  bool tV[L::R];
+  // static ownership: lane owns items lane, lane + 32, ...; item = tile + NT * half
+  int offA[L::RI], offB[L::RI], p0[L::RI];
+  bool tV[L::RI];
 #pragma unroll
-  for (int r = 0; r < L::R; ++r) {
-    const int t = lane + 32 * r;
-    tV[r] = t < L::NT;
+  for (int r = 0; r < L::RI; ++r) {
+    const int it = lane + 32 * r;
+    tV[r] = it < L::NI;
+    const int t = it % L::NT;
     const int base = (t >= L::TD) ? L::CDP : 0;
     offA[r] = tV[r] ? base + 4 * tabI[t] : 0;
     offB[r] = tV[r] ? base + 4 * tabJ[t] : 0;
+    p0[r] = (it / L::NT) * L::PS;
   }
 
   // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
@@ -339,25 +378,28 @@ __global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_poin
     __syncwarp();
     for (int t = lane; t < 16 * K; t += 32) ND[t] = a.nd.node32[16 * nodes[t >> 4] + (t & 15)];
     __syncwarp();
-    float acc[L::R][16];
+    float acc[L::RI][16];
 #pragma unroll
-    for (int r = 0; r < L::R; ++r)
+    for (int r = 0; r < L::RI; ++r)
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[r][e] = 0.f;
     unsigned n_assoc = 0;
     for (int base = ch.y; base < ch.z; base += 32) {
       const int64_t i = base + lane;
-      const bool as = point_row<K, DBG>(a, i, i < ch.z, ND, nodes, F + lane * L::FSP);
+      PointIn<K> cur;
+      load_point<K>(a.md, i, i < ch.z, cur);
+      const bool as = point_row<K, DBG>(a, i, i < ch.z, cur, ND, nodes, F + lane * L::FSP);
       n_assoc += __popc(__ballot_sync(0xffffffffu, as));
       __syncwarp();
       const int np = min(32, ch.z - base);
 #pragma unroll
-      for (int r = 0; r < L::R; ++r) {
+      for (int r = 0; r < L::RI; ++r) {
         if (!tV[r]) continue;
         const float* pa = F + offA[r];
         const float* pb = F + offB[r];
+        const int pe = min(np, p0[r] + L::PS);
 #pragma unroll 4
-        for (int p = 0; p < np; ++p) {
+        for (int p = p0[r]; p < pe; ++p) {
           const float4 A = *reinterpret_cast<const float4*>(pa + p * L::FSP);
           const float4 B = *reinterpret_cast<const float4*>(pb + p * L::FSP);
           const float Av[4] = {A.x, A.y, A.z, A.w}, Bv[4] = {B.x, B.y, B.z, B.w};
@@ -371,7 +413,7 @@ __global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_poin
     }
     // ---- commit: tiles -> shared memory -> the chunk's record (coalesced, no atomics)
 #pragma unroll
-    for (int r = 0; r < L::R; ++r) {
+    for (int r = 0; r < L::RI; ++r) {
       if (!tV[r]) continue;
       float4* d4 = reinterpret_cast<float4*>(F + 16 * (lane + 32 * r));
 #pragma unroll
@@ -379,14 +421,19 @@ __global__ void __launch_bounds__(kWarps * 32, (K <= 5 ? 3 : 2)) k_assemble_poin
     }
     __syncwarp();
     float* rec = a.records + c * (int64_t)RS;
-    int64_t nxt = 0;
-    if (lane == 0) nxt = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
+    int64_t next_chunk = 0;
+    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
     for (int d = lane; d < RS; d += 32) {
       const int q = perm[d];
-      rec[d] = q >= 0 ? F[q] : 0.f;
+      float v = 0.f;
+      if (q >= 0) {
+        v = F[q];
+        if (L::SPLIT == 2) v += F[q + 16 * L::NT];   // the second half's partial tile
+      }
+      rec[d] = v;
     }
     if (lane == 0) rec[52 * P + 18 * K + 4] = (float)n_assoc;
-    c = __shfl_sync(0xffffffffu, nxt, 0);
+    c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
 }
 
