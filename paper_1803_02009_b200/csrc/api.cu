@@ -139,24 +139,38 @@ cudaError_t nccl_allgather_u64(Ctx* c, const uint64_t* send, uint64_t* recv, siz
 }
 
 // ------------------------------------------------------------ small kernels
-__global__ void k_deinterleave3(int64_t n, const float* aos, float* x, float* y, float* z, float dflt) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (aos) { x[i] = aos[3 * i]; y[i] = aos[3 * i + 1]; z[i] = aos[3 * i + 2]; }
-  else { x[i] = dflt; y[i] = dflt; z[i] = dflt; }
-}
 __global__ void k_interleave3(int64_t n, const float* x, const float* y, const float* z, float* aos) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   aos[3 * i] = x[i]; aos[3 * i + 1] = y[i]; aos[3 * i + 2] = z[i];
 }
-__global__ void k_fill_defaults(int64_t n, int64_t id0, float* w, int32_t* stamp, int64_t* ids, bool fw, bool fs,
-                                bool fi) {
+// mis_set_model in one pass: AoS xyz / nrm / rgb -> SoA, weight / stamp / ids
+// copied or defaulted, next fresh id = max(ids) + 1 (ids_dev zeroed before).
+struct LoadSrc {
+  const float *xyz, *nrm, *rgb, *w;
+  const int32_t* stamp;
+  const int64_t* ids;
+};
+__global__ void k_load_model(int64_t n, LoadSrc src, ModelView md, long long* ids_dev) {
+  __shared__ long long bm;
+  if (threadIdx.x == 0) bm = -1;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !src.ids) ids_dev[0] = n;
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (fw) w[i] = 1.0f;
-  if (fs) stamp[i] = 0;
-  if (fi) ids[i] = id0 + i;
+  if (i < n) {
+    md.px[i] = src.xyz[3 * i]; md.py[i] = src.xyz[3 * i + 1]; md.pz[i] = src.xyz[3 * i + 2];
+    md.nx[i] = src.nrm[3 * i]; md.ny[i] = src.nrm[3 * i + 1]; md.nz[i] = src.nrm[3 * i + 2];
+    if (src.rgb) { md.cr[i] = src.rgb[3 * i]; md.cg[i] = src.rgb[3 * i + 1]; md.cb[i] = src.rgb[3 * i + 2]; }
+    else { md.cr[i] = 0.f; md.cg[i] = 0.f; md.cb[i] = 0.f; }
+    md.w[i] = src.w ? src.w[i] : 1.0f;
+    md.stamp[i] = src.stamp ? src.stamp[i] : 0;
+    const int64_t id = src.ids ? src.ids[i] : i;
+    md.ids[i] = id;
+    if (src.ids) atomicMax(&bm, (long long)id);
+  }
+  if (!src.ids) return;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(ids_dev, bm + 1);
 }
 // point-major (n x K) caller skinning -> slot-major, ids ascending; validation flags
 __global__ void k_canon_knn(int64_t n, int K, int m, const int32_t* idx_pm, const float* w_pm, int64_t cap,
@@ -230,11 +244,6 @@ __global__ void k_next_id(int64_t n, const int64_t* ids, long long* ids_dev) {
   if (threadIdx.x == 0) atomicMax(ids_dev, bm + 1);
 }
 
-__global__ void k_count_winners(int n, const unsigned long long* key, unsigned long long* cnt) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = __syncthreads_count(p < n && key[p] != ~0ull);
-  if (threadIdx.x == 0 && c) atomicAdd(cnt, (unsigned long long)c);
-}
 
 static inline int nb(int64_t n, int t = 256) { return (int)((n + t - 1) / t); }
 
@@ -428,28 +437,33 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
   c->cap = capacity;
   c->n = n;
   ModelView md = model_view(c);
-  if (n > 0) {
-    TRY(c, ensure(c, c->stage, n * 12));
-    ProfScope ps(c, P_IO, 4);
-    float* st = c->stage.as<float>();
-    TRY(c, cudaMemcpyAsync(st, xyz, n * 12, kind_in(mem), c->st));
-    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, st, md.px, md.py, md.pz, 0.f);
-    TRY(c, cudaMemcpyAsync(st, nrm, n * 12, kind_in(mem), c->st));
-    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, st, md.nx, md.ny, md.nz, 0.f);
-    if (rgb) TRY(c, cudaMemcpyAsync(st, rgb, n * 12, kind_in(mem), c->st));
-    k_deinterleave3<<<nb(n), 256, 0, c->st>>>(n, rgb ? st : nullptr, md.cr, md.cg, md.cb, 0.f);
-    if (weight) TRY(c, cudaMemcpyAsync(md.w, weight, n * 4, kind_in(mem), c->st));
-    if (stamp) TRY(c, cudaMemcpyAsync(md.stamp, stamp, n * 4, kind_in(mem), c->st));
-    if (ids) TRY(c, cudaMemcpyAsync(md.ids, ids, n * 8, kind_in(mem), c->st));
-    k_fill_defaults<<<nb(n), 256, 0, c->st>>>(n, 0, md.w, md.stamp, md.ids, !weight, !stamp, !ids);
-    TRY(c, cudaGetLastError());
-  }
-  // next fresh id = max(ids) + 1, kept on the device (no host synchronisation)
   TRY(c, ensure(c, c->ids_dev, 16));
   TRY(c, cudaMemsetAsync(c->ids_dev.p, 0, 16, c->st));
-  {
+  if (n > 0) {
+    LoadSrc src{xyz, nrm, rgb, weight, stamp, ids};
+    if (mem == MIS_MEM_HOST) {   // stage the host arrays once, then the same single pass
+      TRY(c, ensure(c, c->stage, n * 56));
+      char* st = c->stage.as<char>();
+      cudaError_t err = cudaSuccess;
+      auto put = [&](const void* h, size_t bytes, size_t off) -> const void* {
+        if (!h) return nullptr;
+        const cudaError_t e = cudaMemcpyAsync(st + off, h, bytes, cudaMemcpyHostToDevice, c->st);
+        if (e != cudaSuccess) err = e;
+        return st + off;
+      };
+      src.xyz = (const float*)put(xyz, n * 12, 0);
+      src.nrm = (const float*)put(nrm, n * 12, n * 12);
+      src.rgb = (const float*)put(rgb, n * 12, n * 24);
+      src.w = (const float*)put(weight, n * 4, n * 36);
+      src.stamp = (const int32_t*)put(stamp, n * 4, n * 40);
+      src.ids = (const int64_t*)put(ids, n * 8, n * 48);
+      TRY(c, err);
+    }
     ProfScope ps(c, P_IO, 1);
-    k_next_id<<<n > 0 ? nb(n) : 1, 256, 0, c->st>>>(n, ids ? md.ids : nullptr, c->ids_dev.as<long long>());
+    k_load_model<<<nb(n), 256, 0, c->st>>>(n, src, md, c->ids_dev.as<long long>());
+  } else {
+    ProfScope ps(c, P_IO, 1);
+    k_next_id<<<1, 256, 0, c->st>>>(0, nullptr, c->ids_dev.as<long long>());
   }
   TRY(c, cudaGetLastError());
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
@@ -487,11 +501,17 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   if (n > 0) {
     ProfScope ps(c, knn_idx ? P_IO : P_SKIN, 1);
     if (knn_idx) {
-      TRY(c, ensure(c, c->stage, n * K * 8));
-      int32_t* si = c->stage.as<int32_t>();
-      float* sw = reinterpret_cast<float*>(si + n * K);
-      TRY(c, cudaMemcpyAsync(si, knn_idx, n * K * 4, kind_in(mem), c->st));
-      TRY(c, cudaMemcpyAsync(sw, knn_w, n * K * 4, kind_in(mem), c->st));
+      const int32_t* si = knn_idx;
+      const float* sw = knn_w;
+      if (mem == MIS_MEM_HOST) {   // device pointers are read in place
+        TRY(c, ensure(c, c->stage, n * K * 8));
+        int32_t* di = c->stage.as<int32_t>();
+        float* dw = reinterpret_cast<float*>(di + n * K);
+        TRY(c, cudaMemcpyAsync(di, knn_idx, n * K * 4, cudaMemcpyHostToDevice, c->st));
+        TRY(c, cudaMemcpyAsync(dw, knn_w, n * K * 4, cudaMemcpyHostToDevice, c->st));
+        si = di;
+        sw = dw;
+      }
       k_canon_knn<<<nb(n), 256, 0, c->st>>>(n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
     } else {
       launch_skin(n, md.px, md.py, md.pz, 1, c->g.as<float>(), m, K, md.kidx, md.kw, c->cap, c->st);
@@ -636,6 +656,9 @@ static mis_status assemble(Ctx* c, bool dbg) {
     r.acc = acc;
     r.Hval = c->Hval.as<float>();
     r.rhs = c->rhs.as<float>();
+    r.Minv = c->world == 1 ? c->Minv.as<float>() : nullptr;   // several ranks: H is final only after the all-reduce
+    r.diag_pos = c->diag_pos.as<int32_t>();
+    r.lambda = c->prm.lambda;
     launch_reduce_records(r, c->st);
   }
   TRY(c, cudaGetLastError());
@@ -681,6 +704,7 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.smem_bytes = c->cl_smem;
   s.write_global = update ? 0 : 1;
   s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) ? 0 : 1;
+  s.minv_ready = c->world == 1 ? 1 : 0;
   s.tstamp = c->tstamp.as<unsigned long long>();
   return s;
 }
@@ -960,9 +984,8 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   unsigned long long* cnt = c->counter.as<unsigned long long>();
   TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
   {
-    ProfScope ps(c, P_LIFT, 3);
-    launch_lift_count(a, counts, nbk, c->ids_dev.as<long long>(), c->st);
-    k_count_winners<<<nb((int64_t)px), 256, 0, c->st>>>((int)px, c->pixkey.as<unsigned long long>(), cnt);
+    ProfScope ps(c, P_LIFT, 2);
+    launch_lift_count(a, counts, nbk, c->ids_dev.as<long long>(), cnt, c->st);
   }
   int32_t n_lift = 0;
   unsigned long long n_reg = 0;

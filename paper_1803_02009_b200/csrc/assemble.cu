@@ -444,15 +444,22 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
 //   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j));
 // one warp per node writes b_j; then the energies.
 __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
-  __shared__ float stage[8][88];
+  __shared__ float stage[8][124];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int P = r.K * (r.K + 1) / 2;
   const int RS = r.rec_stride;
   float* st = stage[wib];
-  if (gw < r.nnzb) {
-    const int64_t e = gw;
-    if (r.upper_of[e] != e) return;   // lower-triangle entries are written as mirrors
+  // warps [0, m): diagonal blocks (first, so their preconditioner inverses overlap
+  // the rest); [m, m + nnzb): off-diagonal upper entries; then nodes; then energies
+  int64_t e = -1;
+  if (gw < r.m) {
+    e = r.diag_pos[gw];
+  } else if (gw < r.m + r.nnzb) {
+    e = gw - r.m;
+    if (r.upper_of[e] != e || r.lower_of[e] < 0) return;   // mirrors and diagonals are written elsewhere
+  }
+  if (e >= 0) {
     float v0 = 0.f, v1 = 0.f;         // lane owns record floats lane and lane + 32 (< 52)
     for (int k = r.slot_ptr[e]; k < r.slot_ptr[e + 1]; ++k) {
       const int src = r.slot_src[k];
@@ -472,10 +479,41 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
       const float h = block_entry(st, st + 36, st + 52, diag, i, j, r.w_data, r.w_pt);
       r.Hval[36 * e + l] = h;
       if (!diag) r.Hval[36 * (int64_t)lo + 6 * j + i] = h;
+      st[88 + l] = h;
+    }
+    if (diag && r.Minv) {   // block-Jacobi inverse of this node (K7), off the solver's critical path:
+      __syncwarp();         // fp64 Gauss-Jordan, lane rr < 6 holds row rr of [H + (lambda + mu) I | I]
+      const int64_t row_j = gw;
+      const int rr = lane < 6 ? lane : 0;
+      double trc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) trc += (double)st[88 + 7 * q];
+      const double mu = 1e-9 * trc / 6.0;
+      double row[12];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        row[q] = (double)st[88 + 6 * rr + q] + (q == rr ? (double)r.lambda + mu : 0.0);
+        row[6 + q] = q == rr ? 1.0 : 0.0;
+      }
+      bool pd = true;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const double pv = __shfl_sync(0xffffffffu, row[p], p);
+        if (!(pv > 0.0)) pd = false;
+        const double ipv = 1.0 / pv, f = row[p] * ipv;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+          const double pq = __shfl_sync(0xffffffffu, row[q], p);
+          row[q] = rr == p ? pq * ipv : row[q] - f * pq;
+        }
+      }
+      if (lane < 6)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) r.Minv[36 * (int64_t)row_j + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
     }
     return;
   }
-  const int64_t gn = gw - r.nnzb;
+  const int64_t gn = gw - r.m - r.nnzb;
   if (gn < r.m) {
     const int n = (int)gn;
     float v = 0.f;   // lanes 0..17: 6 rhs_data + 12 node moments
@@ -522,7 +560,7 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
 }
 
 void launch_reduce_records(const ReduceArgs& r, cudaStream_t s) {
-  const int64_t warps = r.nnzb + r.m + (r.nchunk + 31) / 32;
+  const int64_t warps = r.m + r.nnzb + r.m + (r.nchunk + 31) / 32;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 0) k_reduce_records<<<(unsigned)blocks, 256, 0, s>>>(r);
 }

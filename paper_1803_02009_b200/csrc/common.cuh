@@ -101,6 +101,9 @@ struct ReduceArgs {
   AccView acc;                // graph / rhs_graph (K4/K5) in, energies out
   float* Hval;                // nnzb*36 final blocks (both triangles)
   float* rhs;                 // 6m final right-hand side
+  float* Minv;                // nullable: m*36 block-Jacobi inverses (one GPU: H is final here)
+  const int32_t* diag_pos;    // m: BSR entry of each diagonal block
+  float lambda;
 };
 void launch_reduce_records(const ReduceArgs& r, cudaStream_t s);
 
@@ -150,6 +153,7 @@ struct SolveArgs {
   size_t smem_bytes;
   int write_global;           // also write x to global memory (debug)
   int pipelined;              // cluster variant: pipelined PCG (1 barrier / iteration) instead of standard
+  int minv_ready;             // Minv already built by the record reduction (single GPU)
   unsigned long long* tstamp; // 8 %globaltimer stamps of the phases (rank 0, thread 0)
 };
 
@@ -184,7 +188,8 @@ struct FuseArgs {
 void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);
 // lift: count pass (per-block counts) then write pass; returns via device counters
-void launch_lift_count(const FuseArgs& a, int32_t* block_counts, int nblocks, long long* ids_dev, cudaStream_t s);
+void launch_lift_count(const FuseArgs& a, int32_t* block_counts, int nblocks, long long* ids_dev,
+                       unsigned long long* n_registered, cudaStream_t s);
 void launch_lift_write(const FuseArgs& a, const int32_t* block_offsets, int nblocks, int64_t base,
                        const long long* ids_dev, cudaStream_t s);
 int lift_blocks(int W, int H);

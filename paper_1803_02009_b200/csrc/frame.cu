@@ -57,12 +57,20 @@ void launch_frame_prep(const FrameView& f, float4* nmap, cudaStream_t s) {
 // (k+1)-th, normalised (d_max = 0 -> 1/k).  Output ids
 // ascending (the canonical tuple order used by the K13 sort).  Brute force
 // over all nodes staged through shared memory.
-template <int K>
+//
+// A team of S lanes (S | 32) serves one query: lane l scans nodes l, l+S, ...
+// (ascending, so its strict-< insertion keeps the lower id on equal distance),
+// then the team merges its S sorted lists in k+1 rounds of a butterfly
+// (d, id)-lexicographic min -- the same k+1 nodes the sequential scan picks.
+// S is chosen so that nq * S fills the GPU: feature points (nq ~ 500) and lifted
+// points (nq ~ 10^4) get 32 / 16 lanes, the full model (nq ~ 10^5+) one.
+template <int K, int S>
 __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restrict__ px, const float* __restrict__ py,
                                               const float* __restrict__ pz, int64_t sxyz, const float* __restrict__ g,
                                               int m, int32_t* __restrict__ idx, float* __restrict__ w, int64_t os) {
   __shared__ float4 sg[1024];
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int tl = threadIdx.x % S;   // lane within the team
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S;
   const bool act = i < nq;
   float vx = 0, vy = 0, vz = 0;
   if (act) { vx = px[i * sxyz]; vy = py[i * sxyz]; vz = pz[i * sxyz]; }
@@ -78,7 +86,7 @@ __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restric
     __syncthreads();
     if (act) {
 #pragma unroll 8
-      for (int t = 0; t < cnt; ++t) {
+      for (int t = tl; t < cnt; t += S) {
         const float4 q = sg[t];
         const float dx = vx - q.x, dy = vy - q.y, dz = vz - q.z;
         const float d2 = dx * dx + dy * dy + dz * dz;
@@ -94,7 +102,30 @@ __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restric
       }
     }
   }
-  if (!act) return;
+  if (S > 1) {   // merge the team's sorted lists: k+1 rounds of (d, id) min + pop
+    float od[K + 1];
+    int oi[K + 1];
+#pragma unroll
+    for (int r = 0; r <= K; ++r) {
+      float d = bd[0];
+      int id = bi[0];
+#pragma unroll
+      for (int o = S / 2; o > 0; o >>= 1) {
+        const float d2 = __shfl_xor_sync(0xffffffffu, d, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, id, o);
+        if (d2 < d || (d2 == d && i2 < id)) { d = d2; id = i2; }
+      }
+      od[r] = d;
+      oi[r] = id;
+      const bool pop = bi[0] == id && bd[0] == d;
+#pragma unroll
+      for (int s = 0; s < K; ++s) { bd[s] = pop ? bd[s + 1] : bd[s]; bi[s] = pop ? bi[s + 1] : bi[s]; }
+      if (pop) { bd[K] = INFINITY; bi[K] = 0x7fffffff; }
+    }
+#pragma unroll
+    for (int s = 0; s <= K; ++s) { bd[s] = od[s]; bi[s] = oi[s]; }
+  }
+  if (!act || tl != 0) return;
   const float dmax = sqrtf(bd[K]);
   float ww[K];
   float sum = 0.f;
@@ -118,12 +149,32 @@ __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restric
   for (int s = 0; s < K; ++s) { idx[s * os + i] = bi[s]; w[s * os + i] = ww[s]; }
 }
 
+template <int K>
+static void skin_k(int64_t nq, const float* px, const float* py, const float* pz, int64_t sxyz, const float* g, int m,
+                   int32_t* idx, float* w, int64_t os, cudaStream_t s) {
+  static int fill = 0;   // threads that fill the device (SMs x 2048)
+  if (!fill) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    fill = sms * 2048;
+  }
+  int S = 1;
+  while (S < 32 && nq * S < fill && S * 8 <= m) S *= 2;
+  const int blocks = (int)((nq * S + 255) / 256);
+  switch (S) {
+#define SK(SS) case SS: k_skin<K, SS><<<blocks, 256, 0, s>>>(nq, px, py, pz, sxyz, g, m, idx, w, os); break;
+    SK(1) SK(2) SK(4) SK(8) SK(16) SK(32)
+#undef SK
+    default: break;
+  }
+}
+
 void launch_skin(int64_t nq, const float* px, const float* py, const float* pz, int64_t sxyz, const float* g, int m,
                  int K, int32_t* idx, float* w, int64_t os, cudaStream_t s) {
   if (nq <= 0) return;
-  const int blocks = (int)((nq + 255) / 256);
   switch (K) {
-#define SK(KK) case KK: k_skin<KK><<<blocks, 256, 0, s>>>(nq, px, py, pz, sxyz, g, m, idx, w, os); break;
+#define SK(KK) case KK: skin_k<KK>(nq, px, py, pz, sxyz, g, m, idx, w, os, s); break;
     SK(1) SK(2) SK(3) SK(4) SK(5) SK(6) SK(7) SK(8)
 #undef SK
     default: break;

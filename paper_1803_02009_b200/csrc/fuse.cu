@@ -208,31 +208,50 @@ __device__ __forceinline__ bool lift_pixel(const FuseArgs& a, int p) {
   return nm.w > 0.f && (nm.x != 0.f || nm.y != 0.f || nm.z != 0.f) && a.pixkey[p] == ~0ull;
 }
 
-__global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts) {
+// per block: lifted pixels (scanned next) and registered pixels (the fusion count)
+__global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts, unsigned long long* n_reg) {
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const int c = __syncthreads_count(lift_pixel(a, p));
-  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+  const int r = __syncthreads_count(p < a.fr.W * a.fr.H && a.pixkey[p] != ~0ull);
+  if (threadIdx.x == 0) {
+    counts[blockIdx.x] = c;
+    if (r) atomicAdd(n_reg, (unsigned long long)r);
+  }
 }
 
 // exclusive scan of the per-block counts (single block; counts[nb] = total)
 __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb,
                                                       long long* ids_dev) {
-  __shared__ int32_t part[1024];
+  __shared__ int32_t wtot[32];
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int32_t s = 0;
   for (int b = b0; b < min(nb, b0 + per); ++b) s += counts[b];
-  part[threadIdx.x] = s;
+  int32_t inc = s;   // warp inclusive scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wtot[wid] = inc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int t = 0; t < 1024; ++t) { int32_t v = part[t]; part[t] = run; run += v; }
-    offs[nb] = run;
-    ids_dev[1] = ids_dev[0];   // ids of the lifted points: ids_dev[1] + rank
-    ids_dev[0] += run;
+  if (wid == 0) {
+    int32_t t = wtot[lane], ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += v;
+    }
+    wtot[lane] = ti - t;   // exclusive warp offsets
+    if (lane == 31) {
+      offs[nb] = ti;
+      ids_dev[1] = ids_dev[0];   // ids of the lifted points: ids_dev[1] + rank
+      ids_dev[0] += ti;
+    }
   }
   __syncthreads();
-  int32_t run = part[threadIdx.x];
+  int32_t run = wtot[wid] + inc - s;
   for (int b = b0; b < min(nb, b0 + per); ++b) { offs[b] = run; run += counts[b]; }
 }
 
@@ -272,8 +291,9 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   md.ids[o] = ids_dev[1] + (o - base);
 }
 
-void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long long* ids_dev, cudaStream_t s) {
-  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts);
+void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long long* ids_dev, unsigned long long* n_reg,
+                       cudaStream_t s) {
+  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts, n_reg);
   k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks, ids_dev);
 }
 

@@ -21,36 +21,107 @@ namespace cg = cooperative_groups;
 
 namespace mis {
 
-constexpr int kCT = 1024;          // threads per CTA
+#ifndef MIS_PCG_THREADS
+#define MIS_PCG_THREADS 512
+#endif
+constexpr int kCT = MIS_PCG_THREADS;   // threads per CTA
+constexpr int kWarps = kCT / 32;
 constexpr int kMaxCluster = 16;
 
 constexpr int kNVec = 10;         // local vectors (pipelined PCG needs 10, standard 6)
 
+constexpr int kPiece = 4;         // SpMV work unit: <= kPiece consecutive blocks of one row
+
+__host__ __device__ inline int max_pieces(int max_rows, int max_nnz) { return max_nnz / kPiece + max_rows + 1; }
+
 struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
-  size_t dots, vec, zf, mi, col, own, h, total;
+  size_t dots, vec, zf, mi, col, own, pptr, pc, part, mask, push, h, total;
   __host__ __device__ CLay(int max_rows, int max_nnz, int m) {
-    dots = 0;                                        // double partA..partE[16], red[32]
+    dots = 0;                                        // double partA..partE[16], red[64]
     vec = dots + sizeof(double) * (5 * kMaxCluster + 64);
     const size_t nv = (size_t)max_rows * 6;
     zf = vec + sizeof(float) * kNVec * nv;           // local vectors, then two replicated full vectors
     mi = zf + sizeof(float) * 2 * 6 * (size_t)m;
     col = mi + sizeof(float) * 36 * max_rows;
-    own = col + sizeof(int) * max_nnz;
-    h = (own + sizeof(int) * (max_nnz + 1) + 15) & ~(size_t)15;
+    own = col + sizeof(int) * max_nnz;               // local row pointers (nr + 1)
+    pptr = own + sizeof(int) * (max_rows + 1);       // first SpMV piece of each local row (nr + 1)
+    pc = pptr + sizeof(int) * (max_rows + 1);        // pieces: first block | count << 24
+    part = pc + sizeof(int) * max_pieces(max_rows, max_nnz);   // 6 partial sums per piece
+    mask = part + sizeof(float) * 6 * max_pieces(max_rows, max_nnz);   // per own row: CTAs that read it
+    push = mask + sizeof(unsigned) * max_rows;       // (destination CTA << 16 | local row), by destination
+    h = (push + sizeof(int) * (size_t)max_rows * kMaxCluster + 15) & ~(size_t)15;
     total = h + sizeof(float) * 36 * (size_t)max_nnz;
   }
 };
 
-
-// push this CTA's z slice into every CTA's full-length copy (remote stores,
-// made visible by the following cluster barrier)
-__device__ __forceinline__ void replicate(cg::cluster_group& cl, float* zf, const float* z, int r0, int nr, int cs) {
-  const int n = 3 * nr;   // float2 units (6 r0 floats = 24 r0 bytes: 8-byte aligned)
-  const float2* z2 = reinterpret_cast<const float2*>(z);
-  for (int w = threadIdx.x; w < n * cs; w += kCT) {
-    const int d = w / n, q = w - d * n;
-    reinterpret_cast<float2*>(cl.map_shared_rank(zf, d) + 6 * r0)[q] = z2[q];
+// Split the local rows into pieces of <= kPiece blocks (row order, then block
+// order) so the SpMV's work units are balanced whatever the row lengths.
+__device__ __forceinline__ void build_pieces(const int* lrp, int nr, int* pptr, int* pc) {
+  if (threadIdx.x < 32) {   // one warp: lane-chunked exclusive scan of the per-row piece counts
+    const int l = threadIdx.x, per = (nr + 31) / 32, i0 = l * per, i1 = min(nr, i0 + per);
+    int s = 0;
+    for (int i = i0; i < i1; ++i) s += (lrp[i + 1] - lrp[i] + kPiece - 1) / kPiece;
+    int inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (l >= o) inc += v;
+    }
+    int run = inc - s;
+    for (int i = i0; i < i1; ++i) {
+      pptr[i] = run;
+      for (int k = lrp[i]; k < lrp[i + 1]; k += kPiece) pc[run++] = k | (min(kPiece, lrp[i + 1] - k) << 24);
+    }
+    if (l == 31) pptr[nr] = inc;
   }
+}
+
+// push the CTA's slice of a vector into the full-length copies of the CTAs
+// whose rows read it (the halo lists of build_push; itself included), as
+// 8-byte remote stores made visible by the following cluster barrier.  The
+// node graph is spatially local, so this moves ~1/7 of a full replication
+// (c3: 2.2k of 15k rows) -- DSMEM bandwidth (~20 B/clk/SM) is what it costs.
+__device__ __forceinline__ void replicate(cg::cluster_group& cl, float* zf, const float* z, int r0, const int* push,
+                                          int npush) {
+  for (int w = threadIdx.x; w < 3 * npush; w += kCT) {
+    const int e = push[w / 3], q = w - 3 * (w / 3), d = e >> 16, i = e & 0xffff;
+    const float2 v = reinterpret_cast<const float2*>(z + 6 * i)[q];
+    reinterpret_cast<float2*>(cl.map_shared_rank(zf, d) + 6 * (r0 + i))[q] = v;
+  }
+}
+
+// Halo lists (once per solve): every CTA marks, in the owner's mask, the rows
+// its blocks read (DSMEM atomicOr), then lists (destination, row) pairs grouped
+// by destination.  Returns the list length (all threads).
+__device__ __forceinline__ int build_push(cg::cluster_group& cl, unsigned* mask, int* push, const int* col, int ne,
+                                          const int32_t* part, int rank, int cs, int r0, int nr) {
+  __shared__ int s_part[kMaxCluster + 1], s_npush;
+  if (threadIdx.x <= cs) s_part[threadIdx.x] = part[threadIdx.x];
+  for (int i = threadIdx.x; i < nr; i += kCT) mask[i] = 1u << rank;
+  cl.sync();   // masks initialised in every CTA
+  for (int k = threadIdx.x; k < ne; k += kCT) {
+    const int j = col[k];
+    if (j >= r0 && j < r0 + nr) continue;
+    int o = 0;
+    while (s_part[o + 1] <= j) ++o;
+    atomicOr(cl.map_shared_rank(mask, o) + (j - s_part[o]), 1u << rank);
+  }
+  cl.sync();   // all marks landed
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    int n = 0;
+    for (int d = 0; d < cs; ++d)
+      for (int b = 0; b < nr; b += 32) {
+        const int i = b + l;
+        const bool on = i < nr && ((mask[i] >> d) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (on) push[n + __popc(bal & ((1u << l) - 1u))] = (d << 16) | i;
+        n += __popc(bal);
+      }
+    if (l == 0) s_npush = n;
+  }
+  __syncthreads();
+  return s_npush;
 }
 
 // xor-butterfly sum: every lane ends with the bitwise-same value (IEEE + is commutative)
@@ -69,7 +140,7 @@ __device__ __forceinline__ void cta_publish(cg::cluster_group& cl, double v, dou
   if (l == 0) red[w] = v;
   __syncthreads();
   if (w == 0) {
-    const double x = warp_sum_all(red[l]);   // kCT / 32 == 32 warps
+    const double x = warp_sum_all(l < kWarps ? red[l] : 0.0);
     if (l < cs) cl.map_shared_rank(slot, l)[rank] = x;
   }
 }
@@ -81,24 +152,93 @@ __device__ __forceinline__ double gather_sum(const double* slot, int cs) {
 }
 
 
-// out = (H + lambda I) v for the CTA's rows; v read from the replicated full vector Z
-__device__ __forceinline__ void spmv_local(const int* lrp, const int* col, const float* H, const float* Z,
-                                           const float* v_local, float lambda, float* out, int nr) {
-  const int n_items = 12 * nr;
-  for (int base = 0; base < n_items; base += kCT) {
-    const int item = base + threadIdx.x;
-    const bool act = item < n_items;
-    const int i = item / 12, c = (item % 12) >> 1, hf = item & 1;
-    float v = 0.f;
-    if (act)
-      for (int k = lrp[i] + hf; k < lrp[i + 1]; k += 2) {
-        const float* zr = Z + 6 * col[k];
-        const float* h = H + 36 * (size_t)k + 6 * c;
+// The SpMV's H operand lives in registers: thread t owns work units t, t + kCT,
+// ..., t + (kU-1) kCT, each <= kPiece blocks x 6 entries of one block row,
+// loaded once per solve.  Streaming H from shared memory every iteration was
+// bound by the shared-memory port (c3: 127 KB per CTA per SpMV at 128 B/clk);
+// registers leave only the (broadcast) z loads.  Units beyond kU kCT (larger
+// systems) read H from shared memory.
+#ifndef MIS_PCG_REG_UNITS
+#define MIS_PCG_REG_UNITS 3
+#endif
+constexpr int kU = MIS_PCG_REG_UNITS;
+struct HReg {
+  float h[kU][kPiece][6];
+};
+
+__device__ __forceinline__ void load_hreg(HReg& R, const int* pptr, const int* pc, const float* H, int nr) {
+  const int units = 6 * pptr[nr];
 #pragma unroll
-        for (int b = 0; b < 6; ++b) v = fmaf(h[b], zr[b], v);
+  for (int j = 0; j < kU; ++j) {
+    const int u = threadIdx.x + j * kCT;
+    int k0 = 0, cnt = 0, c = 0;
+    if (u < units) {
+      const int p = u / 6, w = pc[p];
+      c = u - 6 * p;
+      k0 = w & 0xffffff;
+      cnt = w >> 24;
+    }
+#pragma unroll
+    for (int b = 0; b < kPiece; ++b)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) R.h[j][b][q] = b < cnt ? H[36 * (size_t)(k0 + b) + 6 * c + q] : 0.f;
+  }
+}
+
+// out = (H + lambda I) v for the CTA's rows; v read from the replicated full vector Z.
+// Pass 1: one thread per (piece, component) -- <= kPiece blocks, loads issued
+// together (unrolled, predicated); pass 2: per (row, component) the row's piece
+// partials summed in piece order (deterministic).
+__device__ __forceinline__ void spmv_local(const HReg& R, const int* pptr, const int* pc, float* part, const int* col,
+                                           const float* H, const float* Z, const float* v_local, float lambda,
+                                           float* out, int nr) {
+  const int units = 6 * pptr[nr];
+#pragma unroll
+  for (int j = 0; j < kU; ++j) {
+    const int u = threadIdx.x + j * kCT;
+    if (u < units) {
+      const int p = u / 6, w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
+      float v = 0.f;
+#pragma unroll
+      for (int b = 0; b < kPiece; ++b) {
+        if (b < cnt) {
+          const float2* zr = reinterpret_cast<const float2*>(Z + 6 * col[k0 + b]);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float2 zv = zr[q];
+            v = fmaf(R.h[j][b][2 * q], zv.x, v);
+            v = fmaf(R.h[j][b][2 * q + 1], zv.y, v);
+          }
+        }
       }
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    if (act && hf == 0) out[6 * i + c] = fmaf(lambda, v_local[6 * i + c], v);
+      part[u] = v;
+    }
+  }
+  for (int u = threadIdx.x + kU * kCT; u < units; u += kCT) {
+    const int p = u / 6, c = u - 6 * (u / 6);
+    const int w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
+    float v = 0.f;
+#pragma unroll
+    for (int j = 0; j < kPiece; ++j) {
+      if (j < cnt) {
+        const float2* zr = reinterpret_cast<const float2*>(Z + 6 * col[k0 + j]);
+        const float2* h = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + j) + 6 * c);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const float2 hv = h[b], zv = zr[b];
+          v = fmaf(hv.x, zv.x, v);
+          v = fmaf(hv.y, zv.y, v);
+        }
+      }
+    }
+    part[u] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 6 * nr; e += kCT) {
+    const int i = e / 6, c = e - 6 * (e / 6);
+    float v = 0.f;
+    for (int p = pptr[i]; p < pptr[i + 1]; ++p) v += part[6 * p + c];
+    out[e] = fmaf(lambda, v_local[e], v);
   }
 }
 
@@ -115,11 +255,13 @@ __device__ __forceinline__ void spmv_local(const int* lrp, const int* col, const
 __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_group& cl, unsigned char* sm,
                                               const CLay& L, int rank, int cs, int r0, int nr, const int* lrp,
                                               const int* col, const float* H, const float* Mi, double* g_last,
-                                              double* g_first) {
+                                              double* g_first, unsigned long long* ts, const int* pptr,
+                                              const int* pc, float* part, const int* push, int npush,
+                                              const HReg& R) {
   const int t = threadIdx.x, nv = a.max_rows * 6, n6 = 6 * nr;
   double* base = reinterpret_cast<double*>(sm + L.dots);
-  double* gam[2] = {base, base + kMaxCluster};
-  double* del[2] = {base + 3 * kMaxCluster, base + 4 * kMaxCluster};   // partF (= base + 2*16) stays free
+  // double-buffered dot slots: gamma at base + (it & 1) * 16, delta at base + 48 + (it & 1) * 16
+  // (partF = base + 32 stays free); selected arithmetically so they stay in shared space
   double* red = base + 5 * kMaxCluster;
   float* x = reinterpret_cast<float*>(sm + L.vec);
   float* r = x + nv;
@@ -131,7 +273,7 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
   float* q = zz + nv;
   float* s = q + nv;
   float* p = s + nv;
-  float* Z[2] = {reinterpret_cast<float*>(sm + L.zf), reinterpret_cast<float*>(sm + L.zf) + 6 * a.m};
+  float* const Z0 = reinterpret_cast<float*>(sm + L.zf);   // two full-length buffers: Z0, Z0 + 6 m
   // u = M r; z = q = s = p = 0   (x = 0, r = b from phase 0)
   for (int e = t; e < n6; e += kCT) {
     const int i = e / 6, c = e - 6 * (e / 6);
@@ -141,12 +283,14 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
     zz[e] = 0.f; q[e] = 0.f; s[e] = 0.f; p[e] = 0.f;
   }
   __syncthreads();
-  replicate(cl, Z[0], u, r0, nr, cs);
+  replicate(cl, Z0, u, r0, push, npush);
   cl.sync();
-  spmv_local(lrp, col, H, Z[0], u, a.lambda, w, nr);   // w = A u
+  spmv_local(R, pptr, pc, part, col, H, Z0, u, a.lambda, w, nr);   // w = A u
   __syncthreads();
   double gprev = 1.0, aprev = 1.0, g0 = 0.0, g = 0.0;
   for (int it = 0; it < a.pcg_iters; ++it) {
+    const bool st1 = ts && it == 1;   // sub-phase stamps of iteration 1 (slots 8-14, 15 = marker)
+    if (st1) ts[8] = gtimer();
     double dg = 0.0, dd = 0.0;
     for (int e = t; e < n6; e += kCT) {
       const int i = e / 6, c = e - 6 * (e / 6);
@@ -157,8 +301,12 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
       mm[e] = v;
     }
     __syncthreads();
-    const int nb = (it + 1) & 1;
-    replicate(cl, Z[nb], mm, r0, nr, cs);
+    if (st1) ts[9] = gtimer();
+    float* const Zb = Z0 + ((it + 1) & 1) * 6 * a.m;
+    double* const gam = base + (it & 1) * kMaxCluster;
+    double* const del = base + 3 * kMaxCluster + (it & 1) * kMaxCluster;
+    replicate(cl, Zb, mm, r0, push, npush);
+    if (st1) ts[10] = gtimer();
     {   // both dots in one CTA reduction, published by warp 0 lanes (lane c -> CTA c)
       dg = warp_sum_all(dg);
       dd = warp_sum_all(dd);
@@ -167,24 +315,28 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
       if (l == 0) { red[wi] = dg; red[32 + wi] = dd; }
       __syncthreads();
       if (wi == 0) {
-        const double sg = warp_sum_all(red[l]), sd = warp_sum_all(red[32 + l]);
+        const double sg = warp_sum_all(l < kWarps ? red[l] : 0.0), sd = warp_sum_all(l < kWarps ? red[32 + l] : 0.0);
         if (l < cs) {
-          cl.map_shared_rank(gam[it & 1], l)[rank] = sg;
-          cl.map_shared_rank(del[it & 1], l)[rank] = sd;
+          cl.map_shared_rank(gam, l)[rank] = sg;
+          cl.map_shared_rank(del, l)[rank] = sd;
         }
       }
     }
+    if (st1) ts[11] = gtimer();
     cl.sync();
-    g = gather_sum(gam[it & 1], cs);
-    const double d = gather_sum(del[it & 1], cs);
+    if (st1) ts[12] = gtimer();
+    g = gather_sum(gam, cs);
+    const double d = gather_sum(del, cs);
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g / gprev;
     const double den = it == 0 ? d : d - beta * g / aprev;
     if (!(den > 0.0)) break;
     const double alpha = g / den;
-    spmv_local(lrp, col, H, Z[nb], mm, a.lambda, nn, nr);   // n = A m
+    if (st1) ts[6] = gtimer();
+    spmv_local(R, pptr, pc, part, col, H, Zb, mm, a.lambda, nn, nr);   // n = A m
     __syncthreads();
+    if (st1) ts[13] = gtimer();
     const float fb = (float)beta, fa = (float)alpha;
     for (int e = t; e < n6; e += kCT) {
       zz[e] = fmaf(fb, zz[e], nn[e]);
@@ -197,6 +349,7 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
       w[e] = fmaf(-fa, zz[e], w[e]);
     }
     __syncthreads();
+    if (st1) { ts[14] = gtimer(); ts[15] = 1; }
     gprev = g;
     aprev = alpha;
   }
@@ -223,6 +376,11 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   float* Mi = reinterpret_cast<float*>(sm + L.mi);
   int* col = reinterpret_cast<int*>(sm + L.col);
   int* lrp = reinterpret_cast<int*>(sm + L.own);   // local row pointers (nr + 1)
+  int* pptr = reinterpret_cast<int*>(sm + L.pptr);
+  int* pc = reinterpret_cast<int*>(sm + L.pc);
+  float* part = reinterpret_cast<float*>(sm + L.part);
+  unsigned* hmask = reinterpret_cast<unsigned*>(sm + L.mask);
+  int* push = reinterpret_cast<int*>(sm + L.push);
   float* H = reinterpret_cast<float*>(sm + L.h);
 
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
@@ -234,10 +392,9 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[0] = gtimer();
 
   // ---- phase 0: local rows of H (from the accumulators), b, column owners
-  __shared__ int spart[kMaxCluster + 1];
-  if (t <= cs) spart[t] = a.part[t];
   for (int i = t; i <= nr; i += kCT) lrp[i] = a.row_ptr[r0 + i] - e0;
   __syncthreads();
+  build_pieces(lrp, nr, pptr, pc);   // warp 0, while the others stream H (covered by the next barrier)
   {   // stream this CTA's rows of the final H (built by the record reduction) into shared memory
     const float4* src = reinterpret_cast<const float4*>(a.Hval + 36 * (int64_t)e0);
     float4* dst = reinterpret_cast<float4*>(H);
@@ -253,11 +410,19 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   __syncthreads();
   if (stamp) ts[1] = gtimer();
   if (a.pcg_iters <= 0 && !a.do_update) return;
+  const int npush = build_push(cl, hmask, push, col, ne, a.part, rank, cs, r0, nr);
+  HReg R;
+  load_hreg(R, pptr, pc, H, nr);
 
   // ---- phase 1: block-Jacobi preconditioner, z = M r, r.z
-  // M_j = (H_jj + (lambda + mu_j) I)^-1 in fp64 by Gauss-Jordan, 6 lanes per node
+  // M_j = (H_jj + (lambda + mu_j) I)^-1: built by the record reduction on one GPU
+  // (minv_ready); otherwise here in fp64 by Gauss-Jordan, 6 lanes per node
   // (one row each, pivot rows broadcast by shuffles), 5 nodes per warp.
-  {
+  if (a.minv_ready) {
+    const float4* src = reinterpret_cast<const float4*>(a.Minv + 36 * (int64_t)r0);
+    float4* dst = reinterpret_cast<float4*>(Mi);
+    for (int q = t; q < 9 * nr; q += kCT) dst[q] = src[q];
+  } else {
     const int wid = t >> 5, ln = t & 31, slot = ln / 6, rr = ln - 6 * slot;
     for (int base = 0; base < nr; base += 5 * (kCT / 32)) {
       const int i = base + 5 * wid + slot;
@@ -296,7 +461,8 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
   if (a.pipelined) {
-    pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0);
+    pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
+                  npush, R);
     if (stamp) ts[3] = ts[2];
   } else {
   double my = 0.0;
@@ -308,7 +474,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     my += (double)r[q] * (double)zz;
   }
   __syncthreads();
-  replicate(cl, zf, z, r0, nr, cs);
+  replicate(cl, zf, z, r0, push, npush);
   if (stamp) ts[6] = gtimer();
   cta_publish(cl, my, red, partA, rank, cs);
   if (stamp) ts[7] = gtimer();
@@ -318,30 +484,12 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   rz0 = rz;
   if (stamp) ts[3] = gtimer();
   int done = 0;
-  const int n_items = 12 * nr, passes = (n_items + kCT - 1) / kCT;
   for (int it = 0; it < a.pcg_iters && !done; ++it) {
     if (rz == 0.0) break;
     const bool st1 = stamp && it == 1;
     if (st1) ts[8] = gtimer();
     const float beta = it == 0 ? 0.f : (float)(rz / rz_prev);
-    // Az = (H + lambda I) z: two threads per (row, component) split the row's blocks,
-    // reading the replicated z from local shared memory, pair-reduced by shuffle
-    for (int ps = 0; ps < passes; ++ps) {
-      const int item = t + ps * kCT;
-      const bool act = item < n_items;
-      const int i = item / 12, c = (item % 12) >> 1, hf = item & 1;
-      float v = 0.f;
-      if (act) {
-        for (int k = lrp[i] + hf; k < lrp[i + 1]; k += 2) {
-          const float* zr = zf + 6 * col[k];
-          const float* h = H + 36 * (size_t)k + 6 * c;
-#pragma unroll
-          for (int b = 0; b < 6; ++b) v = fmaf(h[b], zr[b], v);
-        }
-      }
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if (act && hf == 0) Az[6 * i + c] = fmaf(a.lambda, z[6 * i + c], v);
-    }
+    spmv_local(R, pptr, pc, part, col, H, zf, z, a.lambda, Az, nr);   // Az = (H + lambda I) z
     __syncthreads();
     if (st1) ts[9] = gtimer();
     my = 0.0;
@@ -374,7 +522,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     }
     __syncthreads();
     if (st1) ts[12] = gtimer();
-    replicate(cl, zf, z, r0, nr, cs);
+    replicate(cl, zf, z, r0, push, npush);
     cta_publish(cl, my, red, partA, rank, cs);
     if (st1) ts[13] = gtimer();
     cl.sync();   // (A) r.z known everywhere; z complete and replicated

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   double my = 0.0;
   for (int64_t j = tid; j < m; j += nth) {
     float* Mi = a.Minv + 36 * j;
-    precond_block(a.Hval + 36 * (int64_t)a.diag_pos[j], a.lambda, Mi);
+    if (!a.minv_ready) precond_block(a.Hval + 36 * (int64_t)a.diag_pos[j], a.lambda, Mi);
     for (int r = 0; r < 6; ++r) {
       float z = 0.f;
       for (int c = 0; c < 6; ++c) z = fmaf(Mi[6 * r + c], a.rhs[6 * j + c], z);

@@ -164,7 +164,7 @@ __device__ inline void precond_block(const float* Hjj, float lambda, float* Mi) 
   for (int i = 0; i < 36; ++i) Mi[i] = (float)Ai[i];
 }
 
-// R_j <- Exp(dtheta) R_j (Rodrigues, theta < 1e-12 first order), t_j += dt (reading A18)
+// R_j <- Exp(dtheta) R_j (Rodrigues; series coefficients for small theta), t_j += dt (reading A18)
 __device__ inline void node_update(const float* dx, double* Rt, float* n32) {
   const double w0 = dx[0], w1 = dx[1], w2 = dx[2];
   const double th = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
@@ -173,8 +173,14 @@ __device__ inline void node_update(const float* dx, double* Rt, float* n32) {
   for (int i = 0; i < 3; ++i)
     for (int jj = 0; jj < 3; ++jj) K2[3 * i + jj] = K[3 * i] * K[jj] + K[3 * i + 1] * K[3 + jj] + K[3 * i + 2] * K[6 + jj];
   double A, Bc;
-  if (th < 1e-12) { A = 1.0; Bc = 0.0; }
-  else { A = sin(th) / th; Bc = (1.0 - cos(th)) / (th * th); }
+  if (th < 0.05) {   // Taylor series of sin(th)/th and (1 - cos th)/th^2: truncation < 1e-20 here
+    const double t2 = th * th;
+    A = 1.0 + t2 * (-1.0 / 6 + t2 * (1.0 / 120 + t2 * (-1.0 / 5040 + t2 * (1.0 / 362880))));
+    Bc = 0.5 + t2 * (-1.0 / 24 + t2 * (1.0 / 720 + t2 * (-1.0 / 40320 + t2 * (1.0 / 3628800))));
+  } else {
+    A = sin(th) / th;
+    Bc = (1.0 - cos(th)) / (th * th);
+  }
   double E[9];
   for (int i = 0; i < 9; ++i) E[i] = ((i % 4) == 0 ? 1.0 : 0.0) + A * K[i] + Bc * K2[i];
   double Rn[9];

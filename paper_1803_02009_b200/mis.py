@@ -345,8 +345,13 @@ def mis_dbg_solver_phases(ctx):
     it1 = None
     if len(t) and (t[:, 14] > 0).all():
         it1 = {}
-        for n, a_, b_ in [("spmv", 8, 9), ("pAp_sum", 9, 10), ("syncB", 10, 11), ("xr_z", 11, 12),
-                          ("replicate_sum", 12, 13), ("syncA", 13, 14)]:
+        if (t[:, 15] == 1).all():   # pipelined PCG
+            parts = [("dots_Mw", 8, 9), ("replicate", 9, 10), ("publish", 10, 11), ("cluster_sync", 11, 12),
+                     ("scalars", 12, 6), ("spmv", 6, 13), ("update", 13, 14)]
+        else:
+            parts = [("spmv", 8, 9), ("pAp_sum", 9, 10), ("syncB", 10, 11), ("xr_z", 11, 12),
+                     ("replicate_sum", 12, 13), ("syncA", 13, 14)]
+        for n, a_, b_ in parts:
             d = (t[:, b_] - t[:, a_]) / 1e3
             it1[n] = (round(float(d.min()), 2), round(float(d.max()), 2))
     if len(t) == 0:
