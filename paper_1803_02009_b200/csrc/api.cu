@@ -74,12 +74,12 @@ AccView acc_view(Ctx* c) {
   AccView a;
   float* base = c->acc.as<float>();
   const size_t nz = (size_t)c->nnzb, m = (size_t)c->m;
-  // written whole by the record reduction: data | mom | rhs_data | node_mom
-  // accumulated by K4/K5 atomics (zeroed each iteration): graph | rhs_graph
+  // all accumulated atomically (K3 float4 / float2 adds, K4 / K5), zeroed every iteration:
+  // data | mom | rhs_data (padded to 4 floats: 16-byte aligned node moments) | node_mom | graph | rhs_graph
   a.data = base;
   a.mom = a.data + nz * 36;
   a.rhs_data = a.mom + nz * 16;
-  a.node_mom = a.rhs_data + 6 * m;
+  a.node_mom = a.rhs_data + ((6 * m + 3) & ~(size_t)3);
   a.graph = a.node_mom + 12 * m;
   a.rhs_graph = a.graph + nz * 36;
   a.energy = c->energy.as<double>();
@@ -259,8 +259,8 @@ static cudaEvent_t pool_get(Ctx* c) {
 }
 
 ProfScope::ProfScope(Ctx* c_, int cat_, int nk) : c(c_), cat(cat_) {
+  l0 = g_launches;
   g_launches += nk;
-  c->prof_n[cat] += nk;
   if (c->prof) {
     cudaEvent_t a = pool_get(c);
     b = pool_get(c);
@@ -269,6 +269,7 @@ ProfScope::ProfScope(Ctx* c_, int cat_, int nk) : c(c_), cat(cat_) {
   }
 }
 ProfScope::~ProfScope() {
+  c->prof_n[cat] += g_launches - l0;   // includes count_launches() calls made inside the scope
   if (b) cudaEventRecord(b, c->st);
 }
 
@@ -303,7 +304,7 @@ static mis_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
   } while (0)
 
 static cudaError_t run_build_order(Ctx* c) {
-  ProfScope ps(c, P_ORDER, c->n > 0 ? 6 : 0);
+  ProfScope ps(c, P_ORDER, 0);   // build_order counts its own launches
   return build_order(c);
 }
 
@@ -387,12 +388,13 @@ mis_status mis_destroy(mis_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   DBuf* all[] = {&c->g, &c->nbr, &c->node32, &c->Rt64, &c->keys, &c->keys2, &c->vals, &c->vals2, &c->flags,
-                 &c->scan, &c->seg_start, &c->seg_nodes, &c->chunks, &c->chunk_off, &c->ckeys, &c->ckeys2,
-                 &c->uflag, &c->upos, &c->ukeys, &c->row_ptr, &c->col, &c->diag_pos, &c->upper_of, &c->seg_slot,
-                 &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->acc, &c->energy, &c->Hval, &c->rhs, &c->Minv,
-                 &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots, &c->numeric_flag, &c->depth, &c->nmap,
-                 &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey, &c->pix, &c->why,
-                 &c->lift_counts, &c->counter, &c->rep_energy, &c->rep_nassoc, &c->rep_res, &c->cub_tmp};
+                 &c->scan, &c->seg_start, &c->seg_nodes, &c->chunks, &c->chunk_off, &c->bitmap, &c->bitmap_all,
+                 &c->row_cnt, &c->row_ptr, &c->col, &c->row_of, &c->diag_pos, &c->upper_of, &c->lower_of,
+                 &c->seg_slot, &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->part, &c->tstamp, &c->acc, &c->energy,
+                 &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots, &c->numeric_flag,
+                 &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
+                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep_energy, &c->rep_nassoc,
+                 &c->rep_res, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -586,10 +588,7 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
 // zero the accumulators, run K3 (+ K4/K5 on rank 0), all-reduce across ranks
 static mis_status assemble(Ctx* c, bool dbg) {
   AccView acc = acc_view(c);
-  {   // only the atomically accumulated graph part needs zeroing; the record reduction writes the rest
-    const size_t head = (size_t)c->nnzb * 52 + 18 * (size_t)c->m;
-    TRY(c, cudaMemsetAsync(c->acc.as<float>() + head, 0, (c->acc_floats - head) * 4, c->st));
-  }
+  TRY(c, cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));   // K3 / K4 / K5 add atomically
   TRY(c, cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
   const double d2r = M_PI / 180.0;
   AsmPointsArgs a;
@@ -604,7 +603,7 @@ static mis_status assemble(Ctx* c, bool dbg) {
   a.eps_dd = c->prm.eps_d_mm;
   a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
   a.cos_eps_n = (float)a.cos_eps_nd;
-  a.records = c->records.as<float>();
+  a.acc = acc;
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
   a.guard_counter = c->energy.as<double>() + 5;
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
@@ -636,37 +635,28 @@ static mis_status assemble(Ctx* c, bool dbg) {
     launch_assemble_graph(gA, c->st);
     TRY(c, cudaGetLastError());
   }
-  {   // records (+ graph part) -> final H, b and energies
+  if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
+    if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
+    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 6) != cudaSuccess) return MIS_E_NCCL;
+  }
+  {   // accumulators -> final H (both triangles), b, block-Jacobi inverses
     ProfScope ps(c, P_REDUCE, 1);
-    ReduceArgs r;
-    r.records = c->records.as<float>();
-    r.rec_stride = rec_stride(c->K);
-    r.K = c->K;
-    r.nchunk = c->nchunk;
+    FinalArgs r;
     r.nnzb = c->nnzb;
     r.m = c->m;
     r.upper_of = c->upper_of.as<int32_t>();
-    r.slot_ptr = c->slot_ptr.as<int32_t>();
-    r.slot_src = c->slot_src.as<int32_t>();
-    r.node_ptr = c->node_ptr.as<int32_t>();
-    r.node_src = c->node_src.as<int32_t>();
     r.lower_of = c->lower_of.as<int32_t>();
+    r.diag_pos = c->diag_pos.as<int32_t>();
     r.w_data = c->prm.w_data;
     r.w_pt = c->prm.w_point;
     r.acc = acc;
     r.Hval = c->Hval.as<float>();
     r.rhs = c->rhs.as<float>();
-    r.Minv = c->world == 1 ? c->Minv.as<float>() : nullptr;   // several ranks: H is final only after the all-reduce
-    r.diag_pos = c->diag_pos.as<int32_t>();
+    r.Minv = c->Minv.as<float>();
     r.lambda = c->prm.lambda;
-    launch_reduce_records(r, c->st);
+    launch_finalize(r, c->st);
   }
   TRY(c, cudaGetLastError());
-  if (c->world > 1) {   // H, b and the energies are linear in the per-rank sums: all-reduce them
-    if (nccl_allreduce_sum_f32(c, c->Hval.as<float>(), (size_t)c->nnzb * 36) != cudaSuccess) return MIS_E_NCCL;
-    if (nccl_allreduce_sum_f32(c, c->rhs.as<float>(), (size_t)c->m * 6) != cudaSuccess) return MIS_E_NCCL;
-    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 6) != cudaSuccess) return MIS_E_NCCL;
-  }
   return MIS_OK;
 }
 
@@ -704,7 +694,7 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.smem_bytes = c->cl_smem;
   s.write_global = update ? 0 : 1;
   s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) ? 0 : 1;
-  s.minv_ready = c->world == 1 ? 1 : 0;
+  s.minv_ready = 1;   // built by the finalisation (after the all-reduce when sharded)
   s.tstamp = c->tstamp.as<unsigned long long>();
   return s;
 }
@@ -731,7 +721,7 @@ static mis_status prepare(Ctx* c) {
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
   if (c->dirty) TRY(c, run_build_order(c));
   if (!c->pattern_valid) {
-    ProfScope ps(c, P_PATTERN, (c->world > 1 ? 8 : 5) + (c->nchunk > 0 ? 4 : 0));
+    ProfScope ps(c, P_PATTERN, 0);   // build_pattern counts its own launches
     TRY(c, build_pattern(c));
   }
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
@@ -873,7 +863,6 @@ mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val
   if ((s = assemble(c, false)) != MIS_OK) return s;
   launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, 0,
                        c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
-  TRY(c, run_solve(c, solve_args(c, 0, false, 0)));
   if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
   if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
@@ -1089,7 +1078,7 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
 const char* mis_prof_name(int cat) {
   static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assemble_points",
                                              "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
-                                             "lift", "io", "reduce_records"};
+                                             "lift", "io", "finalize"};
   return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
 }
 

@@ -367,6 +367,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
     p0[r] = (it / L::NT) * L::PS;
   }
 
+  double e_data = 0.0, e_pt = 0.0;   // per-lane energy partials (fp64 across chunks)
+  unsigned long long n_tot = 0;      // associations of this warp's chunks
   // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
   int64_t c = 0;
   if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
       }
       __syncwarp();
     }
-    // ---- commit: tiles -> shared memory -> the chunk's record (coalesced, no atomics)
+    // ---- commit: tiles -> shared memory -> atomic adds into the BSR accumulators
 #pragma unroll
     for (int r = 0; r < L::RI; ++r) {
       if (!tV[r]) continue;
@@ -420,38 +422,78 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
       for (int x = 0; x < 4; ++x) d4[x] = make_float4(acc[r][4 * x], acc[r][4 * x + 1], acc[r][4 * x + 2], acc[r][4 * x + 3]);
     }
     __syncwarp();
-    float* rec = a.records + c * (int64_t)RS;
     int64_t next_chunk = 0;
     if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
-    for (int d = lane; d < RS; d += 32) {
+    // vector atomic adds (sm_90+ float4 / float2 RED) into the accumulators: per pair
+    // 9 x 4 data + 4 x 4 moments of its BSR slot, per node slot 3 x 2 rhs + 3 x 4
+    // moments; all-zero vectors (no association) are skipped.  Energies stay in registers.
+    const int32_t* slots = a.seg_slot + (int64_t)seg * P;
+    auto rv = [&](int d) -> float {
       const int q = perm[d];
-      float v = 0.f;
-      if (q >= 0) {
-        v = F[q];
-        if (L::SPLIT == 2) v += F[q + 16 * L::NT];   // the second half's partial tile
+      if (q < 0) return 0.f;
+      float v = F[q];
+      if (L::SPLIT == 2) v += F[q + 16 * L::NT];   // the second half's partial tile
+      return v;
+    };
+    for (int it = lane; it < 13 * P + 6 * K; it += 32) {
+      if (it < 13 * P) {
+        const int pr = it / 13, q = it - 13 * pr;
+        const int d0 = 52 * pr + 4 * q;   // data (q < 9) then moments: contiguous in the record
+        const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+        const int64_t u = slots[pr];
+        float* dst = q < 9 ? a.acc.data + 36 * u + 4 * q : a.acc.mom + 16 * u + 4 * (q - 9);
+        atomicAdd(reinterpret_cast<float4*>(dst), v);
+      } else {
+        const int t2 = it - 13 * P, sl = t2 / 6, q = t2 - 6 * sl;
+        const int64_t nd = nodes[sl];
+        if (q < 3) {
+          const int d0 = 52 * P + 18 * sl + 2 * q;
+          const float2 v = make_float2(rv(d0), rv(d0 + 1));
+          if (v.x != 0.f || v.y != 0.f) atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * nd + 2 * q), v);
+        } else {
+          const int d0 = 52 * P + 18 * sl + 6 + 4 * (q - 3);
+          const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+            atomicAdd(reinterpret_cast<float4*>(a.acc.node_mom + 12 * nd + 4 * (q - 3)), v);
+        }
       }
-      rec[d] = v;
     }
-    if (lane == 0) rec[52 * P + 18 * K + 4] = (float)n_assoc;
+    if (lane == 0) {
+      const int de = 52 * P + 18 * K;
+      e_data += rv(de);
+      e_pt += (double)rv(de + 1) + rv(de + 2) + rv(de + 3);
+    }
+    n_tot += n_assoc;
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
+  }
+  // energies and association count: warp, then block, then one fp64 atomic per block
+  __shared__ double red_e[3][kWarps];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e_data += __shfl_xor_sync(0xffffffffu, e_data, o);
+    e_pt += __shfl_xor_sync(0xffffffffu, e_pt, o);
+  }
+  if (lane == 0) { red_e[0][warp] = e_data; red_e[1][warp] = e_pt; red_e[2][warp] = (double)n_tot; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < kWarps; ++w) t += red_e[threadIdx.x][w];
+    if (t != 0.0) atomicAdd(a.acc.energy + (threadIdx.x == 2 ? 4 : threadIdx.x), t);
   }
 }
 
-// Deterministic slot-major reduction of the chunk records, fused with the
-// finalisation of the normal equations (so the latency-bound solver only
-// streams its rows): one warp per upper BSR entry gathers its (chunk, pair)
-// contributions in sorted order, adds the K4/K5 graph block and writes
-//   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j));
-// one warp per node writes b_j; then the energies.
-__global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
+// Finalisation of the normal equations from the accumulators (so the
+// latency-bound solver only streams its rows): warps [0, m) the diagonal blocks
+// -- first, so their block-Jacobi inverses (K7) overlap the rest --, then one
+// warp per off-diagonal upper entry, then one per node:
+//   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j)),
+//   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
+__global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   __shared__ float stage[8][124];
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int P = r.K * (r.K + 1) / 2;
-  const int RS = r.rec_stride;
   float* st = stage[wib];
-  // warps [0, m): diagonal blocks (first, so their preconditioner inverses overlap
-  // the rest); [m, m + nnzb): off-diagonal upper entries; then nodes; then energies
   int64_t e = -1;
   if (gw < r.m) {
     e = r.diag_pos[gw];
@@ -460,15 +502,9 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
     if (r.upper_of[e] != e || r.lower_of[e] < 0) return;   // mirrors and diagonals are written elsewhere
   }
   if (e >= 0) {
-    float v0 = 0.f, v1 = 0.f;         // lane owns record floats lane and lane + 32 (< 52)
-    for (int k = r.slot_ptr[e]; k < r.slot_ptr[e + 1]; ++k) {
-      const int src = r.slot_src[k];
-      const float* rec = r.records + (int64_t)(src / P) * RS + 52 * (src % P);
-      v0 += rec[lane];
-      if (lane < 20) v1 += rec[32 + lane];
-    }
-    st[lane] = v0;                                    // D (36) | Mo (16) | G (36)
-    if (lane < 20) st[32 + lane] = v1;
+    st[lane] = r.acc.data[36 * e + lane];                  // D (36) | Mo (16) | G (36)
+    if (lane < 4) st[32 + lane] = r.acc.data[36 * e + 32 + lane];
+    if (lane < 16) st[36 + lane] = r.acc.mom[16 * e + lane];
     st[52 + lane] = r.acc.graph[36 * e + lane];
     if (lane < 4) st[84 + lane] = r.acc.graph[36 * e + 32 + lane];
     __syncwarp();
@@ -509,60 +545,32 @@ __global__ void __launch_bounds__(256) k_reduce_records(ReduceArgs r) {
       }
       if (lane < 6)
 #pragma unroll
-        for (int q = 0; q < 6; ++q) r.Minv[36 * (int64_t)row_j + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
+        for (int q = 0; q < 6; ++q) r.Minv[36 * row_j + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
     }
     return;
   }
-  const int64_t gn = gw - r.m - r.nnzb;
-  if (gn < r.m) {
-    const int n = (int)gn;
-    float v = 0.f;   // lanes 0..17: 6 rhs_data + 12 node moments
-    if (lane < 18)
-      for (int k = r.node_ptr[n]; k < r.node_ptr[n + 1]; ++k) {
-        const int src = r.node_src[k];
-        v += r.records[(int64_t)(src / r.K) * RS + 52 * P + 18 * (src % r.K) + lane];
-      }
-    st[lane] = v;
-    __syncwarp();
-    if (lane < 6) {   // b = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs
-      const float* Nm = st + 6;
-      float pt;
-      if (lane < 3) {
-        const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
-        pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
-      } else {
-        pt = Nm[9 + (lane - 3)];
-      }
-      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + r.acc.rhs_graph[6 * n + lane];
+  const int64_t n = gw - r.m - r.nnzb;
+  if (n >= r.m) return;
+  if (lane < 6) st[lane] = r.acc.rhs_data[6 * n + lane];   // 6 rhs_data | 12 node moments
+  else if (lane < 18) st[lane] = r.acc.node_mom[12 * n + lane - 6];
+  __syncwarp();
+  if (lane < 6) {
+    const float* Nm = st + 6;
+    float pt;
+    if (lane < 3) {
+      const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
+      pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
+    } else {
+      pt = Nm[9 + (lane - 3)];
     }
-    return;
-  }
-  const int64_t c0 = (gn - r.m) * 32;
-  if (c0 >= r.nchunk) return;
-  const int64_t c = c0 + lane;
-  double eD = 0, eP = 0, na = 0;
-  if (c < r.nchunk) {
-    const float* t = r.records + c * RS + 52 * P + 18 * r.K;
-    eD = t[0];
-    eP = (double)t[1] + t[2] + t[3];
-    na = t[4];
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    eD += __shfl_xor_sync(0xffffffffu, eD, o);
-    eP += __shfl_xor_sync(0xffffffffu, eP, o);
-    na += __shfl_xor_sync(0xffffffffu, na, o);
-  }
-  if (lane == 0) {
-    atomicAdd(r.acc.energy + 0, eD);
-    atomicAdd(r.acc.energy + 1, eP);
-    atomicAdd(r.acc.energy + 4, na);
+    r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + r.acc.rhs_graph[6 * n + lane];
   }
 }
 
-void launch_reduce_records(const ReduceArgs& r, cudaStream_t s) {
-  const int64_t warps = r.m + r.nnzb + r.m + (r.nchunk + 31) / 32;
+void launch_finalize(const FinalArgs& r, cudaStream_t s) {
+  const int64_t warps = 2 * (int64_t)r.m + r.nnzb;
   const int64_t blocks = (warps * 32 + 255) / 256;
-  if (blocks > 0) k_reduce_records<<<(unsigned)blocks, 256, 0, s>>>(r);
+  if (blocks > 0) k_finalize<<<(unsigned)blocks, 256, 0, s>>>(r);
 }
 
 template <int K>

@@ -73,7 +73,7 @@ struct AsmPointsArgs {
   FrameView fr;
   float eps_d, cos_eps_n;
   double eps_dd, cos_eps_nd;
-  float* records;             // nchunk x rec_stride per-chunk partial sums (pair-major)
+  AccView acc;                // K3 commits atomically into the BSR accumulators
   unsigned long long* work_counter;   // zeroed before the launch (dynamic chunk scheduling)
   double* guard_counter;              // fp64 guard-band re-evaluations (energy slot 5)
   int32_t* dbg_pix;           // nullable: per point association outputs
@@ -81,31 +81,26 @@ struct AsmPointsArgs {
 };
 void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
 
-// Per-chunk record layout (floats): P pairs x [36 data (6x6, upper for the
-// diagonal pair) | 16 point-to-point moments], K slots x [6 rhs_data | 12
-// node moments], tail [E_data, E_pt x, E_pt y, E_pt z, n_assoc]; padded to 4.
+// Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator
+// addresses at commit): P pairs x [36 data (6x6, upper for the diagonal pair) |
+// 16 point-to-point moments], K slots x [6 rhs_data | 12 node moments], tail
+// [E_data, E_pt x, E_pt y, E_pt z, n_assoc]; padded to 4.
 __host__ __device__ inline int rec_stride(int K) { return (52 * (K * (K + 1) / 2) + 18 * K + 5 + 3) & ~3; }
 
-struct ReduceArgs {
-  const float* records;
-  int rec_stride, K;
-  int64_t nchunk, nnzb;
+struct FinalArgs {
+  int64_t nnzb;
   int m;
   const int32_t* upper_of;
-  const int32_t* slot_ptr;    // nnzb+1: contributions to each entry (upper entries only)
-  const int32_t* slot_src;    // (chunk * P + pair)
-  const int32_t* node_ptr;    // m+1
-  const int32_t* node_src;    // (chunk * K + slot)
   const int32_t* lower_of;    // upper entry -> its mirror (-1 on the diagonal)
+  const int32_t* diag_pos;    // m: BSR entry of each diagonal block
   float w_data, w_pt;
-  AccView acc;                // graph / rhs_graph (K4/K5) in, energies out
+  AccView acc;                // K3 / K4 / K5 sums in
   float* Hval;                // nnzb*36 final blocks (both triangles)
   float* rhs;                 // 6m final right-hand side
-  float* Minv;                // nullable: m*36 block-Jacobi inverses (one GPU: H is final here)
-  const int32_t* diag_pos;    // m: BSR entry of each diagonal block
+  float* Minv;                // m*36 block-Jacobi inverses
   float lambda;
 };
-void launch_reduce_records(const ReduceArgs& r, cudaStream_t s);
+void launch_finalize(const FinalArgs& r, cudaStream_t s);
 
 struct AsmGraphArgs {
   NodeView nd;
@@ -166,7 +161,8 @@ cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
 // cluster partition (row boundaries balancing nnz) computed on the device; cl_size 0 = does not fit
 struct PlanOut { int32_t cl_size, max_rows, max_nnz, pad; int64_t smem; };
-void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, cudaStream_t s);
+void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,
+                         cudaStream_t s);
 void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr,
                           int slot, double* rep_energy, double* rep_nassoc, cudaStream_t s);
 

@@ -48,12 +48,10 @@ struct Ctx {
   DBuf keys, keys2, vals, vals2, flags, scan, seg_start, seg_nodes, chunks, chunk_off;
 
   // ---- pattern
-  int64_t nnzb = 0, ncand = 0;
+  int64_t nnzb = 0;
   bool pattern_valid = false;
-  DBuf ckeys, ckeys2, uflag, upos, ukeys, row_ptr, col, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot,
-      nnz_dev;
-  // per-chunk records and their contribution lists (deterministic reduction)
-  DBuf records, ck_key, ck_val, ck_key2, ck_val2, slot_ptr, slot_src, node_ptr, node_src;
+  DBuf bitmap, bitmap_all, row_cnt, row_ptr, col, row_of, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot;
+  DBuf nnz_dev;   // int64 info: [0] nnz, [1] nseg, [2] nchunk, [4..6] cluster plan
 
   // ---- system and solver
   int cl_size = 0, cl_max_rows = 0, cl_max_nnz = 0;   // cluster-resident PCG plan (0: grid variant)
@@ -84,8 +82,6 @@ struct Ctx {
   DBuf rep_energy, rep_nassoc, rep_res;
 
   DBuf cub_tmp;
-  // host staging for small uploads
-  DBuf pinned_small;
 
   // ---- instrumentation
   bool prof = false;
@@ -106,6 +102,7 @@ struct ProfScope {
   Ctx* c;
   int cat;
   cudaEvent_t b = nullptr;
+  int64_t l0 = 0;
   ProfScope(Ctx* c_, int cat_, int nk);
   ~ProfScope();
 };

@@ -559,12 +559,14 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
 
 // The plan on the device (one warp; lane c binary-searches boundary c), so the
 // host never reads the row structure back.  Same rule as plan_cluster.
-__global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part) {
+__global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part,
+                               int64_t* nnz_out) {
   __shared__ int32_t b[kMaxCluster + 1];
   int cs = max_cluster < m ? max_cluster : m;
   if (cs > kMaxCluster) cs = kMaxCluster;
   const int lane = threadIdx.x;
   const int64_t nnz = row_ptr[m];
+  if (lane == 0 && nnz_out) *nnz_out = nnz;
   if (lane > 0 && lane < cs) {
     const int64_t target = (nnz * lane) / cs;
     int lo = 0, hi = m;   // first row with row_ptr[row] >= target
@@ -600,8 +602,9 @@ __global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, P
   for (int c = 0; c <= cs; ++c) part[c] = b[c];
 }
 
-void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, cudaStream_t s) {
-  k_plan_cluster<<<1, 32, 0, s>>>(row_ptr, m, max_cluster, out, part);
+void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,
+                         cudaStream_t s) {
+  k_plan_cluster<<<1, 32, 0, s>>>(row_ptr, m, max_cluster, out, part, nnz_out);
 }
 
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {

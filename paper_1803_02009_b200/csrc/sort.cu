@@ -5,6 +5,8 @@
 // change every frame).  CUB radix sort / scan are library primitives here.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "ctx.cuh"
 
 namespace mis {
@@ -59,19 +61,6 @@ __global__ void k_gather_model(int64_t n, const uint32_t* perm, ModelView a, Mod
   }
 }
 
-template <class T>
-__global__ void k_gather(int64_t n, const uint32_t* perm, const T* src, T* dst) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src[perm[i]];
-}
-
-template <class T>
-static void gather(Ctx* c, const uint32_t* perm, const DBuf& src, const DBuf& dst, int64_t n, int slots) {
-  const int b = (int)((n + 255) / 256);
-  for (int s = 0; s < slots; ++s)
-    k_gather<T><<<b, 256, 0, c->st>>>(n, perm, src.as<T>() + s * c->cap, dst.as<T>() + s * c->cap);
-}
-
 __global__ void k_seg_flags(int64_t n, int64_t cap, const int32_t* kidx, int K, int32_t* flags) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -103,8 +92,9 @@ __global__ void k_chunk_count(int64_t n, const int32_t* nseg_dev, const int32_t*
 }
 
 __global__ void k_chunk_write(int64_t n, const int32_t* nseg_dev, const int32_t* seg_start, const int32_t* off,
-                              int4* chunks) {
+                              int4* chunks, int64_t* info) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) { info[1] = *nseg_dev; info[2] = off[n - 1]; }   // device-resident counts (read back with the pattern)
   if (s >= n || s >= *nseg_dev) return;
   const int32_t a = seg_start[s], b = seg_start[s + 1];
   int32_t o = off[s] - (b - a + kChunk - 1) / kChunk;   // inclusive scan -> start
@@ -137,13 +127,17 @@ cudaError_t build_order(Ctx* c) {
                                              c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, K * bits <= 64 ? K * bits : 64, c->st);
     }));
     k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
+    const int kb = K * bits <= 64 ? K * bits : 64;
+    count_launches(2 + 2 + (kb + 7) / 8);   // keys, gather + the onesweep sort (histogram, exclusive sum, passes)
     CK(cudaGetLastError());
     c->cur = 1 - c->cur;
   }
   ModelBufs& S = c->mb[c->cur];
-  // segments and chunks, sized by the upper bound n: one host readback at the end
-  c->nseg = 0;
-  c->nchunk = 0;
+  // segments and chunks, sized by the upper bound n; the counts stay on the device
+  // (info[1], info[2]) and reach the host with the single readback of build_pattern
+  CK(ensure(c, c->nnz_dev, 64));
+  c->nseg = -1;
+  c->nchunk = -1;
   if (n > 0) {
     CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
     CK(ensure(c, c->seg_start, (n + 1) * 4));
@@ -163,14 +157,11 @@ cudaError_t build_order(Ctx* c) {
       return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->chunk_off.as<int32_t>(), (int)n, c->st);
     }));
     k_chunk_write<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
-                                        c->chunks.as<int4>());
-    int32_t cnt[2] = {0, 0};
-    CK(cudaMemcpyAsync(&cnt[0], nseg_dev, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&cnt[1], c->chunk_off.as<int32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    c->nseg = cnt[0];
-    c->nchunk = cnt[1];
+                                        c->chunks.as<int4>(), c->nnz_dev.as<int64_t>());
+    count_launches(8);   // flags, 2 x (scan init + scan), segment write, chunk count, chunk write
     CK(cudaGetLastError());
+  } else {
+    CK(cudaMemsetAsync(c->nnz_dev.as<int64_t>() + 1, 0, 16, c->st));
   }
   c->dirty = false;
   c->pattern_valid = false;
@@ -178,247 +169,233 @@ cudaError_t build_order(Ctx* c) {
 }
 
 // ---------------------------------------------------------------- pattern
-// (row, col) key with sb = bits_for(m) bits per index: radix sorts need only 2 sb + 1 bits
-__device__ __forceinline__ uint64_t pkey(int r, int col, int sb) { return ((uint64_t)(uint32_t)r << sb) | (uint32_t)col; }
-constexpr uint64_t kNoKey = ~0ull;
+// The BSR pattern of the normal equations from a node-pair bitmap (m x m bits,
+// 64-bit words): every candidate (segment pair, graph edge, feature pair,
+// diagonal) sets its two bits; rows are then read out in column order.  No
+// sort, and every count stays on the device until the one host readback.
+// info (int64): [0] nnz, [1] nseg, [2] nchunk, [4..6] PlanOut.
 
-// candidates: [segment pairs nseg*P][edges m*n_nbr][feature pairs nf*P][diagonal m]; 2 keys each
-__global__ void k_candidates(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr,
-                             int nf, const int32_t* fidx, uint64_t* keys, int64_t total, int sb) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= total) return;
+// slot position p of a K-tuple -> (j, j + off): pairs (j <= l) in pair_index order
+__device__ __forceinline__ void pair_of(int p, int K, int& j, int& off) {
+  j = 0;
+  while (p >= K - j) { p -= K - j; ++j; }
+  off = p;
+}
+
+__device__ __forceinline__ void mark(unsigned long long* bm, int64_t W, int a, int b) {
+  unsigned long long* w = bm + (int64_t)a * W + (b >> 6);
+  const unsigned long long bit = 1ull << (b & 63);
+  if (!(*w & bit)) atomicOr(w, bit);
+}
+
+// candidates: [tuples ntup*P][edges m*n_nbr][feature pairs nf*P][diagonal m]; tuples with a
+// negative first id are padding (gathered shards)
+__global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup_host, int K, int m, int n_nbr,
+                       const int32_t* nbr, int nf, const int32_t* fidx, unsigned long long* bm, int64_t W) {
   const int P = K * (K + 1) / 2;
-  const int64_t ns = nseg * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P;
-  int a = -1, b = -1;
-  if (t < ns) {
-    const int64_t s = t / P;
-    int p = (int)(t % P), j = 0;
-    while (p >= K - j) { p -= K - j; ++j; }
-    a = seg_nodes[s * K + j];
-    b = seg_nodes[s * K + j + p];
-  } else if (t < ns + ne) {
-    const int64_t e = t - ns;
-    const int l = nbr[e];
-    if (l >= 0) { a = (int)(e / n_nbr); b = l; }
-  } else if (t < ns + ne + nfp) {
-    const int64_t e = t - ns - ne;
-    const int64_t f = e / P;
-    int p = (int)(e % P), j = 0;
-    while (p >= K - j) { p -= K - j; ++j; }
-    a = fidx[(int64_t)j * nf + f];
-    b = fidx[(int64_t)(j + p) * nf + f];
-  } else {
-    a = b = (int)(t - ns - ne - nfp);
+  const int64_t ntup = ntup_dev ? *ntup_dev : ntup_host;
+  const int64_t ns = ntup * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P, total = ns + ne + nfp + m;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int a, b;
+    if (t < ns) {
+      const int64_t sg = t / P;
+      int j, off;
+      pair_of((int)(t % P), K, j, off);
+      a = tup[sg * K + j];
+      b = tup[sg * K + j + off];
+    } else if (t < ns + ne) {
+      const int64_t e = t - ns;
+      a = (int)(e / n_nbr);
+      b = nbr[e];
+    } else if (t < ns + ne + nfp) {
+      const int64_t e = t - ns - ne, f = e / P;
+      int j, off;
+      pair_of((int)(e % P), K, j, off);
+      a = fidx[(int64_t)j * nf + f];
+      b = fidx[(int64_t)(j + off) * nf + f];
+    } else {
+      a = b = (int)(t - ns - ne - nfp);
+    }
+    if (a < 0 || b < 0) continue;
+    mark(bm, W, a, b);
+    if (a != b) mark(bm, W, b, a);
   }
-  if (a < 0) { keys[2 * t] = kNoKey; keys[2 * t + 1] = kNoKey; return; }
-  keys[2 * t] = pkey(a, b, sb);
-  keys[2 * t + 1] = (a != b) ? pkey(b, a, sb) : kNoKey;
 }
 
-__global__ void k_unique_flags(int64_t n, const uint64_t* k, int32_t* f) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  f[i] = (k[i] != kNoKey) && (i == 0 || k[i] != k[i - 1]);
+__global__ void k_bitmap_or(int64_t words, int world, const unsigned long long* all, unsigned long long* bm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long v = 0;
+    for (int r = 0; r < world; ++r) v |= all[(int64_t)r * words + i];
+    bm[i] = v;
+  }
 }
 
-__global__ void k_unique_write(int64_t n, const uint64_t* k, const int32_t* f, const int32_t* pos, uint64_t* u,
-                               int64_t* nnz) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (f[i]) u[pos[i] - 1] = k[i];
-  if (i == n - 1) *nnz = pos[i];
+// one warp per row: number of set bits (cnt[m] = 0 for the exclusive scan)
+__global__ void k_row_count(const unsigned long long* bm, int64_t W, int m, int32_t* cnt) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r > m) return;
+  int s = 0;
+  if (r < m)
+    for (int64_t w = lane; w < W; w += 32) s += __popcll(bm[r * W + w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) cnt[r] = s;
 }
 
-__device__ __forceinline__ int64_t find_key(const uint64_t* u, int64_t nnz, uint64_t key) {
-  int64_t lo = 0, hi = nnz;
+// one warp per row: columns in ascending order, row index of each entry, diagonal position
+__global__ void k_row_fill(const unsigned long long* bm, int64_t W, int m, const int32_t* row_ptr, int32_t* col,
+                           int32_t* row_of, int32_t* diag_pos) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= m) return;
+  int pos = row_ptr[r];
+  for (int64_t w0 = 0; w0 < W; w0 += 32) {
+    const int64_t w = w0 + lane;
+    unsigned long long word = w < W ? bm[r * W + w] : 0ull;
+    const int cnt = __popcll(word);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int p = pos + inc - cnt;
+    while (word) {
+      const int b = __ffsll((long long)word) - 1;
+      word &= word - 1;
+      const int cc = (int)(64 * w + b);
+      col[p] = cc;
+      row_of[p] = (int32_t)r;
+      if (cc == r) diag_pos[r] = p;
+      ++p;
+    }
+    pos += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+// entry of (a, b) in the sorted column list of row a (-1 if absent)
+__device__ __forceinline__ int find_entry(const int32_t* row_ptr, const int32_t* col, int a, int b) {
+  int lo = row_ptr[a], hi = row_ptr[a + 1];
   while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (u[mid] < key) lo = mid + 1; else hi = mid;
+    const int mid = (lo + hi) >> 1;
+    if (col[mid] < b) lo = mid + 1; else hi = mid;
   }
-  return (lo < nnz && u[lo] == key) ? lo : -1;
+  return (lo < row_ptr[a + 1] && col[lo] == b) ? lo : -1;
 }
 
-__global__ void k_rows(int64_t cap, const int64_t* nnz_dev, const uint64_t* u, int m, int32_t* row_ptr, int32_t* col,
-                       int32_t* upper_of, int32_t* lower_of, int32_t* diag_pos, int sb) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nnz = *nnz_dev;
-  if (e >= nnz || e >= cap) return;
-  const int r = (int)(u[e] >> sb), cc = (int)(u[e] & ((1ull << sb) - 1));
-  col[e] = cc;
-  const int rp = (e == 0) ? -1 : (int)(u[e - 1] >> sb);
-  for (int q = rp + 1; q <= r; ++q) row_ptr[q] = (int32_t)e;
-  if (e == nnz - 1)
-    for (int q = r + 1; q <= m; ++q) row_ptr[q] = (int32_t)nnz;
-  if (r == cc) diag_pos[r] = (int32_t)e;
-  upper_of[e] = (r <= cc) ? (int32_t)e : (int32_t)find_key(u, nnz, pkey(cc, r, sb));
-  if (r == cc) lower_of[e] = -1;                       // diagonal: no mirror
-  else if (r > cc) lower_of[upper_of[e]] = (int32_t)e;   // the upper partner's mirror
+// upper_of: the (min, max) entry of each entry; lower_of[upper] = its mirror (-1 on the diagonal)
+__global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const int32_t* row_of, int m,
+                              int32_t* upper_of, int32_t* lower_of) {
+  const int64_t nnz = row_ptr[m];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = row_of[e], cc = col[e];
+    if (r == cc) {
+      upper_of[e] = (int32_t)e;
+      lower_of[e] = -1;
+    } else if (r < cc) {
+      upper_of[e] = (int32_t)e;
+      lower_of[e] = find_entry(row_ptr, col, cc, r);
+    } else {
+      upper_of[e] = find_entry(row_ptr, col, cc, r);
+    }
+  }
 }
 
+// slot tables: (segment, pair), (node, edge), (feature, pair) -> upper BSR entry
 __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr, int nf,
-                        const int32_t* fidx, const uint64_t* u, const int64_t* nnz_dev, int32_t* seg_slot, int32_t* edge_slot,
-                        int32_t* feat_slot, int64_t total, int sb) {
+                        const int32_t* fidx, const int32_t* row_ptr, const int32_t* col, int32_t* seg_slot,
+                        int32_t* edge_slot, int32_t* feat_slot, int64_t total) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nnz = *nnz_dev;
   if (t >= total) return;
   const int P = K * (K + 1) / 2;
-  const int64_t ns = nseg * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P;
+  const int64_t ns = nseg * P, ne = (int64_t)m * n_nbr;
+  int j, off;
   if (t < ns) {
-    const int64_t s = t / P;
-    int p = (int)(t % P), j = 0;
-    while (p >= K - j) { p -= K - j; ++j; }
-    seg_slot[t] = (int32_t)find_key(u, nnz, pkey(seg_nodes[s * K + j], seg_nodes[s * K + j + p], sb));
+    const int64_t sg = t / P;
+    pair_of((int)(t % P), K, j, off);
+    seg_slot[t] = find_entry(row_ptr, col, seg_nodes[sg * K + j], seg_nodes[sg * K + j + off]);
   } else if (t < ns + ne) {
     const int64_t e = t - ns;
-    const int l = nbr[e], j = (int)(e / n_nbr);
-    edge_slot[e] = (l >= 0) ? (int32_t)find_key(u, nnz, pkey(min(j, l), max(j, l), sb)) : -1;
-  } else if (t < ns + ne + nfp) {
-    const int64_t e = t - ns - ne;
-    const int64_t f = e / P;
-    int p = (int)(e % P), j = 0;
-    while (p >= K - j) { p -= K - j; ++j; }
-    feat_slot[e] = (int32_t)find_key(u, nnz, pkey(fidx[(int64_t)j * nf + f], fidx[(int64_t)(j + p) * nf + f], sb));
+    const int l = nbr[e], a = (int)(e / n_nbr);
+    edge_slot[e] = (l >= 0) ? find_entry(row_ptr, col, min(a, l), max(a, l)) : -1;
+  } else {
+    const int64_t e = t - ns - ne, f = e / P;
+    pair_of((int)(e % P), K, j, off);
+    feat_slot[e] = find_entry(row_ptr, col, fidx[(int64_t)j * nf + f], fidx[(int64_t)(j + off) * nf + f]);
   }
-}
-
-// contributions of the chunk records: (key = BSR slot or node, value = chunk * W + position)
-__global__ void k_contrib(int64_t nchunk, const int4* chunks, const int32_t* table, int W, int32_t* key,
-                          int32_t* val) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nchunk * W) return;
-  const int64_t c = t / W;
-  const int p = (int)(t % W);
-  key[t] = table[(int64_t)chunks[c].x * W + p];
-  val[t] = (int32_t)t;
-}
-
-// CSR row pointers over nbins from sorted keys
-__global__ void k_csr_ptr(int64_t n, const int32_t* key, const int64_t* nbins_dev, int nbins_host, int32_t* ptr) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int nbins = nbins_dev ? (int)*nbins_dev : nbins_host;
-  const int k = key[i];
-  const int kp = (i == 0) ? -1 : key[i - 1];
-  for (int b = kp + 1; b <= k; ++b) ptr[b] = (int32_t)i;
-  if (i == n - 1)
-    for (int b = k + 1; b <= nbins; ++b) ptr[b] = (int32_t)n;
-}
-
-// nbins: upper bound (host); nbins_dev: exact count on the device (or null: nbins is exact)
-static cudaError_t build_contrib(Ctx* c, const int32_t* table, int W, int nbins, const int64_t* nbins_dev, DBuf& ptr,
-                                 DBuf& src) {
-  const int64_t n = c->nchunk * W;
-  CK(ensure(c, ptr, (size_t)(nbins + 1) * 4));
-  CK(ensure(c, src, (size_t)n * 4 + 16));
-  if (n == 0) return cudaMemsetAsync(ptr.p, 0, (size_t)(nbins + 1) * 4, c->st);
-  CK(ensure(c, c->ck_key, n * 4)); CK(ensure(c, c->ck_val, n * 4));
-  CK(ensure(c, c->ck_key2, n * 4));
-  const int b = (int)((n + 255) / 256);
-  k_contrib<<<b, 256, 0, c->st>>>(c->nchunk, c->chunks.as<int4>(), table, W, c->ck_key.as<int32_t>(),
-                                  c->ck_val.as<int32_t>());
-  int bits = 1;
-  while ((1ll << bits) <= (int64_t)nbins) ++bits;
-  CK(cub_call(c, [&](void* t, size_t& s) {
-    return cub::DeviceRadixSort::SortPairs(t, s, c->ck_key.as<int32_t>(), c->ck_key2.as<int32_t>(),
-                                           c->ck_val.as<int32_t>(), src.as<int32_t>(), (int)n, 0, bits, c->st);
-  }));
-  k_csr_ptr<<<b, 256, 0, c->st>>>(n, c->ck_key2.as<int32_t>(), nbins_dev, nbins, ptr.as<int32_t>());
-  return cudaGetLastError();
 }
 
 cudaError_t build_pattern(Ctx* c) {
-  const int K = c->K, P = K * (K + 1) / 2;
-  const int64_t total = c->nseg * P + (int64_t)c->m * c->prm.n_nbr + (int64_t)c->nf * P + c->m;
-  const int64_t nk = 2 * total;
-  const int sb = bits_for(c->m);
-  CK(ensure(c, c->ckeys, nk * 8)); CK(ensure(c, c->ckeys2, nk * 8));
-  CK(ensure(c, c->uflag, nk * 4)); CK(ensure(c, c->upos, nk * 4));
-  CK(ensure(c, c->nnz_dev, 64));
-  const int bt = (int)((total + 255) / 256), bk = (int)((nk + 255) / 256);
-  k_candidates<<<bt, 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, c->m, c->prm.n_nbr,
-                                      c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(), c->ckeys.as<uint64_t>(), total, sb);
-  CK(cub_call(c, [&](void* t, size_t& s) {
-    return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)nk, 0, 2 * sb + 1, c->st);
-  }));
-  k_unique_flags<<<bk, 256, 0, c->st>>>(nk, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>());
-  CK(cub_call(c, [&](void* t, size_t& s) {
-    return cub::DeviceScan::InclusiveSum(t, s, c->uflag.as<int32_t>(), c->upos.as<int32_t>(), (int)nk, c->st);
-  }));
-  CK(ensure(c, c->ukeys, nk * 8));
-  k_unique_write<<<bk, 256, 0, c->st>>>(nk, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>(), c->upos.as<int32_t>(),
-                                        c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>());
-  int64_t nnz = nk;   // upper bound until the single readback below
-  if (c->world > 1) {
-    // union of the ranks' patterns: every rank ends with the same sorted unique keys
-    CK(cudaMemcpyAsync(&nnz, c->nnz_dev.p, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    int64_t mx = nnz;
-    int64_t* dmx = c->nnz_dev.as<int64_t>() + 1;
-    CK(cudaMemcpyAsync(dmx, &mx, 8, cudaMemcpyHostToDevice, c->st));
-    CK(nccl_allreduce_max_i64(c, dmx, 1));
-    CK(cudaMemcpyAsync(&mx, dmx, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    const int64_t all = mx * c->world;
-    // send buffer: local unique keys padded to mx with kNoKey (ckeys2 is free now)
-    CK(ensure(c, c->ckeys2, mx * 8));
-    CK(cudaMemcpyAsync(c->ckeys2.p, c->ukeys.p, nnz * 8, cudaMemcpyDeviceToDevice, c->st));
-    if (mx > nnz) CK(cudaMemsetAsync(c->ckeys2.as<uint64_t>() + nnz, 0xff, (mx - nnz) * 8, c->st));
-    CK(ensure(c, c->ckeys, all * 8));
-    CK(nccl_allgather_u64(c, c->ckeys2.as<uint64_t>(), c->ckeys.as<uint64_t>(), (size_t)mx));
-    CK(ensure(c, c->ckeys2, all * 8));
-    CK(ensure(c, c->uflag, all * 4)); CK(ensure(c, c->upos, all * 4)); CK(ensure(c, c->ukeys, all * 8));
-    CK(cub_call(c, [&](void* t, size_t& s) {
-      return cub::DeviceRadixSort::SortKeys(t, s, c->ckeys.as<uint64_t>(), c->ckeys2.as<uint64_t>(), (int)all, 0, 2 * sb + 1, c->st);
-    }));
-    const int ba = (int)((all + 255) / 256);
-    k_unique_flags<<<ba, 256, 0, c->st>>>(all, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>());
-    CK(cub_call(c, [&](void* t, size_t& s) {
-      return cub::DeviceScan::InclusiveSum(t, s, c->uflag.as<int32_t>(), c->upos.as<int32_t>(), (int)all, c->st);
-    }));
-    k_unique_write<<<ba, 256, 0, c->st>>>(all, c->ckeys2.as<uint64_t>(), c->uflag.as<int32_t>(),
-                                          c->upos.as<int32_t>(), c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>());
-    nnz = all;
+  const int K = c->K, P = K * (K + 1) / 2, m = c->m;
+  const int64_t W = (m + 63) / 64, words = (int64_t)m * W;
+  int64_t* info = c->nnz_dev.as<int64_t>();
+  CK(ensure(c, c->bitmap, words * 8));
+  CK(cudaMemsetAsync(c->bitmap.p, 0, words * 8, c->st));
+  unsigned long long* bm = c->bitmap.as<unsigned long long>();
+  const int grid = c->num_sms * 8;
+  k_mark<<<grid, 256, 0, c->st>>>(c->seg_nodes.as<int32_t>(), info + 1, 0, K, m, c->prm.n_nbr, c->nbr.as<int32_t>(),
+                                  c->nf, c->fidx.as<int32_t>(), bm, W);
+  if (c->world > 1) {   // union over the ranks: all-gather the bitmaps and OR them (same pattern everywhere)
+    CK(ensure(c, c->bitmap_all, (size_t)words * 8 * c->world));
+    CK(nccl_allgather_u64(c, reinterpret_cast<const uint64_t*>(bm), c->bitmap_all.as<uint64_t>(), (size_t)words));
+    k_bitmap_or<<<grid, 256, 0, c->st>>>(words, c->world, c->bitmap_all.as<unsigned long long>(), bm);
   }
-  const int64_t cap = nnz;   // upper bound of the unique count
-  CK(ensure(c, c->row_ptr, (c->m + 1) * 4));
-  CK(ensure(c, c->col, cap * 4)); CK(ensure(c, c->upper_of, cap * 4)); CK(ensure(c, c->lower_of, cap * 4));
-  CK(ensure(c, c->diag_pos, c->m * 4));
+  count_launches(c->world > 1 ? 2 : 1);
+  CK(ensure(c, c->row_cnt, (size_t)(m + 1) * 4));
+  CK(ensure(c, c->row_ptr, (size_t)(m + 1) * 4));
+  CK(ensure(c, c->diag_pos, (size_t)m * 4));
   CK(ensure(c, c->part, 32 * 4));
-  PlanOut* plan = reinterpret_cast<PlanOut*>(c->nnz_dev.as<int64_t>() + 2);
-  const int bn = (int)((cap + 255) / 256);
-  k_rows<<<bn, 256, 0, c->st>>>(cap, c->nnz_dev.as<int64_t>(), c->ukeys.as<uint64_t>(), c->m, c->row_ptr.as<int32_t>(),
-                                c->col.as<int32_t>(), c->upper_of.as<int32_t>(), c->lower_of.as<int32_t>(),
-                                c->diag_pos.as<int32_t>(), sb);
-  launch_plan_cluster(c->row_ptr.as<int32_t>(), c->m, 16, plan, c->part.as<int32_t>(), c->st);
-  CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
-  CK(ensure(c, c->edge_slot, ((int64_t)c->m * c->prm.n_nbr + 1) * 4));
-  CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
-  k_slots<<<bt, 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, c->m, c->prm.n_nbr, c->nbr.as<int32_t>(),
-                                 c->nf, c->fidx.as<int32_t>(), c->ukeys.as<uint64_t>(), c->nnz_dev.as<int64_t>(),
-                                 c->seg_slot.as<int32_t>(), c->edge_slot.as<int32_t>(), c->feat_slot.as<int32_t>(), total,
-                                 sb);
+  const int wb = (int)(((int64_t)(m + 1) * 32 + 255) / 256);
+  k_row_count<<<wb, 256, 0, c->st>>>(bm, W, m, c->row_cnt.as<int32_t>());
+  CK(cub_call(c, [&](void* t, size_t& s) {
+    return cub::DeviceScan::ExclusiveSum(t, s, c->row_cnt.as<int32_t>(), c->row_ptr.as<int32_t>(), m + 1, c->st);
+  }));
+  launch_plan_cluster(c->row_ptr.as<int32_t>(), m, 16, reinterpret_cast<PlanOut*>(info + 4), c->part.as<int32_t>(),
+                      info, c->st);
+  count_launches(4);   // row count, scan init + scan, plan
   CK(cudaGetLastError());
-  // chunk records and their (deterministic, sorted) contribution lists
-  CK(ensure(c, c->records, (size_t)c->nchunk * rec_stride(K) * 4 + 16));
-  CK(build_contrib(c, c->seg_slot.as<int32_t>(), P, (int)cap, c->nnz_dev.as<int64_t>(), c->slot_ptr, c->slot_src));
-  CK(build_contrib(c, c->seg_nodes.as<int32_t>(), K, c->m, nullptr, c->node_ptr, c->node_src));
-  // the single host readback of the pattern build: nnz and the cluster plan
-  struct { int64_t nnz, pad; PlanOut plan; } info;
-  CK(cudaMemcpyAsync(&info, c->nnz_dev.p, sizeof(info), cudaMemcpyDeviceToHost, c->st));
+  // the single host readback of the frame: nnz, segment / chunk counts, cluster plan
+  int64_t h[8];
+  CK(cudaMemcpyAsync(h, info, sizeof(h), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  nnz = info.nnz;
+  const int64_t nnz = h[0];
   c->nnzb = nnz;
-  c->cl_size = info.plan.cl_size;
-  c->cl_max_rows = info.plan.max_rows;
-  c->cl_max_nnz = info.plan.max_nnz;
-  c->cl_smem = (size_t)info.plan.smem;
-  // accumulators and solver buffers
-  const size_t m6 = 6 * (size_t)c->m;
-  c->acc_floats = (size_t)nnz * (36 + 16 + 36) + m6 + 12 * (size_t)c->m + m6;
+  c->nseg = h[1];
+  c->nchunk = h[2];
+  const PlanOut* plan = reinterpret_cast<const PlanOut*>(h + 4);
+  c->cl_size = plan->cl_size;
+  c->cl_max_rows = plan->max_rows;
+  c->cl_max_nnz = plan->max_nnz;
+  c->cl_smem = (size_t)plan->smem;
+  CK(ensure(c, c->col, nnz * 4 + 4)); CK(ensure(c, c->row_of, nnz * 4 + 4));
+  CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
+  k_row_fill<<<wb, 256, 0, c->st>>>(bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(),
+                                    c->diag_pos.as<int32_t>());
+  count_launches(1 + (nnz > 0) + (c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P > 0));
+  if (nnz > 0)
+    k_upper_lower<<<(int)std::min<int64_t>(grid, (nnz + 255) / 256), 256, 0, c->st>>>(
+        c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(), m, c->upper_of.as<int32_t>(),
+        c->lower_of.as<int32_t>());
+  // slot tables (exact sizes now)
+  const int64_t total = c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P;
+  CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
+  CK(ensure(c, c->edge_slot, ((int64_t)m * c->prm.n_nbr + 1) * 4));
+  CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
+  if (total > 0)
+    k_slots<<<(int)((total + 255) / 256), 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, m, c->prm.n_nbr,
+                                                          c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(),
+                                                          c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
+                                                          c->seg_slot.as<int32_t>(), c->edge_slot.as<int32_t>(),
+                                                          c->feat_slot.as<int32_t>(), total);
+  CK(cudaGetLastError());
+  // accumulators (K3 commits atomically into them) and solver buffers
+  const size_t m6 = 6 * (size_t)m;
+  c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)m + m6;
   CK(ensure(c, c->acc, c->acc_floats * 4));
   CK(ensure(c, c->energy, 8 * 8));
   CK(ensure(c, c->Hval, (size_t)nnz * 36 * 4));
-  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)c->m * 36 * 4));
+  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)m * 36 * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
   CK(ensure(c, c->p, m6 * 4)); CK(ensure(c, c->Ap, m6 * 4));
   CK(ensure(c, c->dots, (2 * (size_t)c->prm.pcg_iters + 8) * 8));
