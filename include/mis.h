@@ -222,8 +222,9 @@ mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
  * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),
  * 11 io (uploads, layout conversion), 12 reduce_records (K3 chunk records -> blocks). */
 const char* mis_prof_name(int cat);
-/* on != 0: record a CUDA event pair on the context stream around every kernel
- * group launched by this context (adds no synchronisation). */
+/* on = 1: record a CUDA event pair on the context stream around every kernel
+ * group launched by this context; on = 2: only around the K3 and solver groups
+ * (less host work per step); 0: off.  Adds no synchronisation. */
 mis_status mis_prof_enable(mis_ctx* ctx, int on);
 /* Accumulated device milliseconds and launches per group since the last reset
  * (synchronises the context stream).  ms / launches: MIS_PROF_NCAT entries. */

@@ -261,7 +261,7 @@ static cudaEvent_t pool_get(Ctx* c) {
 ProfScope::ProfScope(Ctx* c_, int cat_, int nk) : c(c_), cat(cat_) {
   l0 = g_launches;
   g_launches += nk;
-  if (c->prof) {
+  if (c->prof && (!c->prof_light || cat == P_POINTS || cat == P_SOLVE)) {
     cudaEvent_t a = pool_get(c);
     b = pool_get(c);
     cudaEventRecord(a, c->st);
@@ -1085,6 +1085,7 @@ const char* mis_prof_name(int cat) {
 mis_status mis_prof_enable(mis_ctx* c, int on) {
   if (!c) return MIS_E_ARG;
   c->prof = on != 0;
+  c->prof_light = on == 2;
   return MIS_OK;
 }
 

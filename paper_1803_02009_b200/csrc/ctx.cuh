@@ -84,7 +84,7 @@ struct Ctx {
   DBuf cub_tmp;
 
   // ---- instrumentation
-  bool prof = false;
+  bool prof = false, prof_light = false;   // light: only the K3 and solver groups
   struct PEv { int cat; cudaEvent_t a, b; };
   std::vector<PEv> pev;
   std::vector<cudaEvent_t> pool;
@@ -126,5 +126,8 @@ cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
 cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count);
 cudaError_t nccl_allgather_u64(Ctx* c, const uint64_t* send, uint64_t* recv, size_t count);
 
-constexpr int kChunk = 256;   // max points per K3 chunk
+#ifndef MIS_KCHUNK
+#define MIS_KCHUNK 64
+#endif
+constexpr int kChunk = MIS_KCHUNK;   // max points per K3 chunk (a segment splits into equal chunks)
 }  // namespace mis

@@ -97,8 +97,10 @@ __global__ void k_chunk_write(int64_t n, const int32_t* nseg_dev, const int32_t*
   if (s == 0) { info[1] = *nseg_dev; info[2] = off[n - 1]; }   // device-resident counts (read back with the pattern)
   if (s >= n || s >= *nseg_dev) return;
   const int32_t a = seg_start[s], b = seg_start[s + 1];
-  int32_t o = off[s] - (b - a + kChunk - 1) / kChunk;   // inclusive scan -> start
-  for (int32_t p = a; p < b; p += kChunk) chunks[o++] = make_int4((int)s, p, min(b, p + kChunk), 0);
+  const int32_t nc = (b - a + kChunk - 1) / kChunk, len = b - a;
+  const int32_t o = off[s] - nc;   // inclusive scan -> start
+  for (int32_t q = 0; q < nc; ++q)   // equal-size chunks: the last one is not a short tail
+    chunks[o + q] = make_int4((int)s, a + (int32_t)((int64_t)len * q / nc), a + (int32_t)((int64_t)len * (q + 1) / nc), 0);
 }
 
 template <class F>
@@ -127,8 +129,7 @@ cudaError_t build_order(Ctx* c) {
                                              c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, K * bits <= 64 ? K * bits : 64, c->st);
     }));
     k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
-    const int kb = K * bits <= 64 ? K * bits : 64;
-    count_launches(2 + 2 + (kb + 7) / 8);   // keys, gather + the onesweep sort (histogram, exclusive sum, passes)
+    count_launches(2);   // keys, gather (CUB's sort kernels are library code, not counted)
     CK(cudaGetLastError());
     c->cur = 1 - c->cur;
   }
@@ -158,7 +159,7 @@ cudaError_t build_order(Ctx* c) {
     }));
     k_chunk_write<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
                                         c->chunks.as<int4>(), c->nnz_dev.as<int64_t>());
-    count_launches(8);   // flags, 2 x (scan init + scan), segment write, chunk count, chunk write
+    count_launches(4);   // flags, segment write, chunk count, chunk write (+ 2 CUB scans)
     CK(cudaGetLastError());
   } else {
     CK(cudaMemsetAsync(c->nnz_dev.as<int64_t>() + 1, 0, 16, c->st));
@@ -353,7 +354,7 @@ cudaError_t build_pattern(Ctx* c) {
   }));
   launch_plan_cluster(c->row_ptr.as<int32_t>(), m, 16, reinterpret_cast<PlanOut*>(info + 4), c->part.as<int32_t>(),
                       info, c->st);
-  count_launches(4);   // row count, scan init + scan, plan
+  count_launches(2);   // row count, plan (+ the CUB scan)
   CK(cudaGetLastError());
   // the single host readback of the frame: nnz, segment / chunk counts, cluster plan
   int64_t h[8];

@@ -321,8 +321,9 @@ def mis_prof_name(cat):
     return _lib.mis_prof_name(cat).decode()
 
 
-def mis_prof_enable(ctx, on=True):
-    _check(ctx, _lib.mis_prof_enable(ctx, 1 if on else 0))
+def mis_prof_enable(ctx, on=True, light=False):
+    """on: event pairs around every kernel group; light: only the K3 and solver groups."""
+    _check(ctx, _lib.mis_prof_enable(ctx, (2 if light else 1) if on else 0))
 
 
 def mis_prof_read(ctx, reset=False):

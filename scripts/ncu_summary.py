@@ -16,7 +16,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GROUP = {"k_assemble_points": "assemble_points", "k_pcg_cluster": "solve", "k_solve": "solve",
-         "k_reduce_records": "reduce_records", "k_assemble_graph": "assemble_graph", "k_frame_prep": "frame_prep",
+         "k_finalize": "finalize", "k_assemble_graph": "assemble_graph", "k_frame_prep": "frame_prep",
          "k_warp_model": "warp_model", "k_fuse_register": "fuse_register", "k_fuse_apply": "fuse_apply"}
 
 
