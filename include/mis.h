@@ -136,7 +136,11 @@ mis_status mis_set_model(mis_ctx* ctx, int64_t n, mis_mem mem, const float* xyz,
  * reading A6).  knn_idx == NULL: the skinning is computed on the device by
  * Eq. 2 (k+1 nearest nodes, ties to the lower id; requires m >= k+1).
  * Resets every node transform to the identity (R_j = I, t_j = 0).  Sorts the
- * points by their canonical kNN tuple (internal order). */
+ * points by their canonical kNN tuple (internal order).
+ * Validation (MIS_E_ARG): with MIS_MEM_HOST inputs before returning; with
+ * MIS_MEM_DEVICE inputs without a host synchronisation -- invalid ids are
+ * clamped / dropped on the device and the next mis_register (or mis_dbg_*)
+ * returns MIS_E_ARG and unbinds the graph. */
 mis_status mis_set_graph(mis_ctx* ctx, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
                          const int32_t* knn_idx, const float* knn_w);
 

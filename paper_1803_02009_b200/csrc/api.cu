@@ -204,11 +204,14 @@ __global__ void k_to_point_major(int64_t n, int K, int64_t cap, const int32_t* k
     if (w_pm) w_pm[i * K + s] = kw[s * cap + i];
   }
 }
-__global__ void k_check_nbr(int m, int n_nbr, const int32_t* nbr, int* flag) {
+__global__ void k_check_nbr(int m, int n_nbr, int32_t* nbr, int* flag) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * n_nbr) return;
   const int l = nbr[t];
-  if (l < -1 || l >= m || l == t / n_nbr) atomicOr(flag, 8);
+  if (l < -1 || l >= m || l == t / n_nbr) {   // flagged, and neutralised so later kernels stay in bounds
+    atomicOr(flag, 8);
+    nbr[t] = -1;
+  }
 }
 __global__ void k_init_nodes(int m, const float* g, double* Rt64, float* node32) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -439,8 +442,8 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
   c->cap = capacity;
   c->n = n;
   ModelView md = model_view(c);
-  TRY(c, ensure(c, c->ids_dev, 16));
-  TRY(c, cudaMemsetAsync(c->ids_dev.p, 0, 16, c->st));
+  TRY(c, ensure(c, c->ids_dev, 32));
+  TRY(c, cudaMemsetAsync(c->ids_dev.p, 0, 32, c->st));
   if (n > 0) {
     LoadSrc src{xyz, nrm, rgb, weight, stamp, ids};
     if (mem == MIS_MEM_HOST) {   // stage the host arrays once, then the same single pass
@@ -475,6 +478,17 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
   return MIS_OK;
 }
 
+static cudaError_t skin(Ctx* c, int64_t nq, const float* px, const float* py, const float* pz, int64_t sxyz,
+                        int32_t* idx, float* w, int64_t os) {
+  launch_skin(nq, px, py, pz, sxyz, c->g.as<float>(), c->m, c->K, idx, w, os, c->st);
+  return cudaGetLastError();
+}
+
+static std::string graph_flag_message(int f) {
+  return std::string("set_graph: invalid") + ((f & 1) ? " node id" : "") + ((f & 2) ? " duplicate id" : "") +
+         ((f & 4) ? " weight" : "") + ((f & 8) ? " neighbour list" : "");
+}
+
 mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
                          const int32_t* knn_idx, const float* knn_w) {
   if (!c) return MIS_E_ARG;
@@ -492,8 +506,9 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   TRY(c, ensure(c, c->Rt64, (size_t)m * 96));
   TRY(c, cudaMemcpyAsync(c->g.p, node_pos, (size_t)m * 12, kind_in(mem), c->st));
   if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, kind_in(mem), c->st));
-  int* flag = c->counter.as<int>();
-  TRY(c, cudaMemsetAsync(flag, 0, 4, c->st));
+  TRY(c, ensure(c, c->nnz_dev, 64));
+  int* flag = reinterpret_cast<int*>(c->nnz_dev.as<int64_t>() + 3);   // validation flags (info[3])
+  TRY(c, cudaMemsetAsync(flag, 0, 8, c->st));
   if (nn > 0) {
     ProfScope ps(c, P_IO, 1);
     k_check_nbr<<<nb((int64_t)m * nn), 256, 0, c->st>>>(m, nn, c->nbr.as<int32_t>(), flag);
@@ -516,17 +531,23 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
       }
       k_canon_knn<<<nb(n), 256, 0, c->st>>>(n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
     } else {
-      launch_skin(n, md.px, md.py, md.pz, 1, c->g.as<float>(), m, K, md.kidx, md.kw, c->cap, c->st);
+      TRY(c, skin(c, n, md.px, md.py, md.pz, 1, md.kidx, md.kw, c->cap));
     }
   }
-  int hflag = 0;
-  TRY(c, cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaStreamSynchronize(c->st));
-  if (hflag) {
-    c->have_graph = false;
-    return fail(c, MIS_E_ARG, std::string("set_graph: invalid") + ((hflag & 1) ? " node id" : "") +
-                                  ((hflag & 2) ? " duplicate id" : "") + ((hflag & 4) ? " weight" : "") +
-                                  ((hflag & 8) ? " neighbour list" : ""));
+  if (mem == MIS_MEM_HOST) {   // host inputs: validate now (the copies synchronise anyway)
+    int hflag = 0;
+    TRY(c, cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, c->st));
+    TRY(c, cudaStreamSynchronize(c->st));
+    if (hflag) {
+      c->have_graph = false;
+      return fail(c, MIS_E_ARG, graph_flag_message(hflag));
+    }
+    c->graph_check = false;
+  } else {
+    // device inputs: no host synchronisation here; invalid ids were clamped / neutralised on
+    // the device and the flags come back with the pattern readback (the next mis_register
+    // fails with MIS_E_ARG)
+    c->graph_check = true;
   }
   {
     ProfScope ps(c, P_IO, 1);
@@ -577,8 +598,7 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
     TRY(c, cudaMemcpyAsync(c->fdst.p, dst, (size_t)n_feat * 12, kind_in(mem), c->st));
     const float* s = c->fsrc.as<float>();
     ProfScope ps(c, P_SKIN, 1);
-    launch_skin(n_feat, s, s + 1, s + 2, 3, c->g.as<float>(), c->m, K, c->fidx.as<int32_t>(), c->fw.as<float>(),
-                n_feat, c->st);
+    TRY(c, skin(c, n_feat, s, s + 1, s + 2, 3, c->fidx.as<int32_t>(), c->fw.as<float>(), n_feat));
     TRY(c, cudaGetLastError());
   }
   c->pattern_valid = false;
@@ -721,8 +741,18 @@ static mis_status prepare(Ctx* c) {
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
   if (c->dirty) TRY(c, run_build_order(c));
   if (!c->pattern_valid) {
-    ProfScope ps(c, P_PATTERN, 0);   // build_pattern counts its own launches
-    TRY(c, build_pattern(c));
+    {
+      ProfScope ps(c, P_PATTERN, 0);   // build_pattern counts its own launches
+      TRY(c, build_pattern(c));
+    }
+    if (c->graph_check) {   // deferred validation of a device-memory mis_set_graph
+      c->graph_check = false;
+      if (c->graph_flags) {
+        c->have_graph = false;
+        c->pattern_valid = false;
+        return fail(c, MIS_E_ARG, graph_flag_message(c->graph_flags));
+      }
+    }
   }
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
   return MIS_OK;
@@ -972,27 +1002,29 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   int32_t* counts = c->lift_counts.as<int32_t>();
   unsigned long long* cnt = c->counter.as<unsigned long long>();
   TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
+  // lift: count + offsets, one host readback (the API returns the new model size), then
+  // the writes and K2 of the new points run behind the return (overlapping the caller)
+  const int64_t base = c->n;
+  const int do_lift = (c->world == 1 || c->rank == 0) ? 1 : 0;   // sharded model: rank 0 owns the lifted points
+  long long* ids_dev = c->ids_dev.as<long long>();
   {
     ProfScope ps(c, P_LIFT, 2);
-    launch_lift_count(a, counts, nbk, c->ids_dev.as<long long>(), cnt, c->st);
+    launch_lift_count(a, counts, nbk, ids_dev, cnt, do_lift, base, c->cap, c->st);
   }
   int32_t n_lift = 0;
   unsigned long long n_reg = 0;
   TRY(c, cudaMemcpyAsync(&n_lift, counts + 2 * nbk + 1, 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(&n_reg, cnt, 8, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
-  if (c->world > 1 && c->rank != 0) n_lift = 0;   // sharded model: rank 0 owns the lifted points
   if (c->n + n_lift > c->cap) {
     *n_out = c->n;
     return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
   }
-  const int64_t base = c->n;
-  ProfScope ps(c, P_LIFT, n_lift > 0 ? 2 : 0);
-  if (n_lift > 0) launch_lift_write(a, counts + nbk + 1, nbk, base, c->ids_dev.as<long long>(), c->st);
-  ModelView md = model_view(c);
   if (n_lift > 0) {
-    launch_skin(n_lift, md.px + base, md.py + base, md.pz + base, 1, c->g.as<float>(), c->m, c->K, md.kidx + base,
-                md.kw + base, c->cap, c->st);
+    ProfScope ps(c, P_LIFT, 2);
+    ModelView md = model_view(c);
+    launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->st);
+    TRY(c, skin(c, n_lift, md.px + base, md.py + base, md.pz + base, 1, md.kidx + base, md.kw + base, c->cap));
     c->dirty = true;
   }
   TRY(c, cudaGetLastError());
@@ -1066,7 +1098,7 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
   float* pw = reinterpret_cast<float*>(pi + nq * K);
   TRY(c, cudaMemcpyAsync(sp, pts, nq * 12, kind_in(mem), c->st));
   ProfScope ps(c, P_SKIN, 2);
-  launch_skin(nq, sp, sp + 1, sp + 2, 3, c->g.as<float>(), c->m, K, si, sw, nq, c->st);
+  TRY(c, skin(c, nq, sp, sp + 1, sp + 2, 3, si, sw, nq));
   k_to_point_major<<<nb(nq), 256, 0, c->st>>>(nq, K, nq, si, sw, pi, pw);
   TRY(c, cudaGetLastError());
   TRY(c, cudaMemcpyAsync(idx, pi, nq * K * 4, kind_out(mem), c->st));

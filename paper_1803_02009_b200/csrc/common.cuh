@@ -185,8 +185,8 @@ void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);
 // lift: count pass (per-block counts) then write pass; returns via device counters
 void launch_lift_count(const FuseArgs& a, int32_t* block_counts, int nblocks, long long* ids_dev,
-                       unsigned long long* n_registered, cudaStream_t s);
-void launch_lift_write(const FuseArgs& a, const int32_t* block_offsets, int nblocks, int64_t base,
+                       unsigned long long* n_registered, int do_lift, int64_t base, int64_t cap, cudaStream_t s);
+void launch_lift_write(const FuseArgs& a, const int32_t* block_offsets, int nblocks, int64_t base, int64_t cap,
                        const long long* ids_dev, cudaStream_t s);
 int lift_blocks(int W, int H);
 

@@ -38,6 +38,8 @@ struct Ctx {
   ModelBufs mb[2];
   int cur = 0;
   bool have_model = false, have_graph = false, dirty = false;
+  bool graph_check = false;   // device-memory set_graph: validation flags still to be read back
+  int graph_flags = 0;
 
   // ---- graph
   int m = 0;
@@ -51,7 +53,7 @@ struct Ctx {
   int64_t nnzb = 0;
   bool pattern_valid = false;
   DBuf bitmap, bitmap_all, row_cnt, row_ptr, col, row_of, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot;
-  DBuf nnz_dev;   // int64 info: [0] nnz, [1] nseg, [2] nchunk, [4..6] cluster plan
+  DBuf nnz_dev;   // int64 info: [0] nnz, [1] nseg, [2] nchunk, [3] set_graph validation flags, [4..6] plan
 
   // ---- system and solver
   int cl_size = 0, cl_max_rows = 0, cl_max_nnz = 0;   // cluster-resident PCG plan (0: grid variant)
@@ -76,7 +78,7 @@ struct Ctx {
 
   // ---- fuse
   DBuf pixkey, pix, why, lift_counts, counter;
-  DBuf ids_dev;   // int64 [0] next fresh point id, [1] id base of the last lift (device-resident: no host sync)
+  DBuf ids_dev;   // int64 [0] next fresh point id, [1] id base of the last lift, [2] lifted points written
 
   // ---- report
   DBuf rep_energy, rep_nassoc, rep_res;

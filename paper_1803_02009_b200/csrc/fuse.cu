@@ -209,9 +209,10 @@ __device__ __forceinline__ bool lift_pixel(const FuseArgs& a, int p) {
 }
 
 // per block: lifted pixels (scanned next) and registered pixels (the fusion count)
-__global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts, unsigned long long* n_reg) {
+__global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts, unsigned long long* n_reg,
+                                                           int do_lift) {
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
-  const int c = __syncthreads_count(lift_pixel(a, p));
+  const int c = __syncthreads_count(do_lift && lift_pixel(a, p));
   const int r = __syncthreads_count(p < a.fr.W * a.fr.H && a.pixkey[p] != ~0ull);
   if (threadIdx.x == 0) {
     counts[blockIdx.x] = c;
@@ -219,9 +220,10 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* 
   }
 }
 
-// exclusive scan of the per-block counts (single block; counts[nb] = total)
+// exclusive scan of the per-block counts (single block; offs[nb] = total);
+// ids_dev[2] = lifted points that fit the capacity
 __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb,
-                                                      long long* ids_dev) {
+                                                      long long* ids_dev, int64_t base, int64_t cap) {
   __shared__ int32_t wtot[32];
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
       offs[nb] = ti;
       ids_dev[1] = ids_dev[0];   // ids of the lifted points: ids_dev[1] + rank
       ids_dev[0] += ti;
+      ids_dev[2] = ti < cap - base ? ti : cap - base;
     }
   }
   __syncthreads();
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
 }
 
 __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int32_t* offs, int64_t base,
-                                                           const long long* ids_dev) {
+                                                           int64_t cap, const long long* ids_dev) {
   __shared__ int wsum[kLiftBlock / 32];
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const bool on = lift_pixel(a, p);
@@ -268,6 +271,7 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   for (int i = 0; i < w; ++i) before += wsum[i];
   if (!on) return;
   const int64_t o = base + offs[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
+  if (o >= cap) return;   // over capacity: reported by mis_fuse (MIS_E_CAPACITY)
   const FrameView& f = a.fr;
   const int px = p % f.W, py = p / f.W;
   double N[3], q[3];
@@ -292,14 +296,14 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
 }
 
 void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long long* ids_dev, unsigned long long* n_reg,
-                       cudaStream_t s) {
-  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts, n_reg);
-  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks, ids_dev);
+                       int do_lift, int64_t base, int64_t cap, cudaStream_t s) {
+  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts, n_reg, do_lift);
+  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks, ids_dev, base, cap);
 }
 
-void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, const long long* ids_dev,
-                       cudaStream_t s) {
-  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, ids_dev);
+void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, int64_t cap,
+                       const long long* ids_dev, cudaStream_t s) {
+  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, cap, ids_dev);
 }
 
 }  // namespace mis

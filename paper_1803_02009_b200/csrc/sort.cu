@@ -174,7 +174,7 @@ cudaError_t build_order(Ctx* c) {
 // 64-bit words): every candidate (segment pair, graph edge, feature pair,
 // diagonal) sets its two bits; rows are then read out in column order.  No
 // sort, and every count stays on the device until the one host readback.
-// info (int64): [0] nnz, [1] nseg, [2] nchunk, [4..6] PlanOut.
+// info (int64): [0] nnz, [1] nseg, [2] nchunk, [3] set_graph validation flags, [4..6] PlanOut.
 
 // slot position p of a K-tuple -> (j, j + off): pairs (j <= l) in pair_index order
 __device__ __forceinline__ void pair_of(int p, int K, int& j, int& off) {
@@ -217,7 +217,7 @@ __global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup
     } else {
       a = b = (int)(t - ns - ne - nfp);
     }
-    if (a < 0 || b < 0) continue;
+    if (a < 0 || b < 0 || a >= m || b >= m) continue;
     mark(bm, W, a, b);
     if (a != b) mark(bm, W, b, a);
   }
@@ -364,6 +364,7 @@ cudaError_t build_pattern(Ctx* c) {
   c->nnzb = nnz;
   c->nseg = h[1];
   c->nchunk = h[2];
+  c->graph_flags = (int)h[3];
   const PlanOut* plan = reinterpret_cast<const PlanOut*>(h + 4);
   c->cl_size = plan->cl_size;
   c->cl_max_rows = plan->max_rows;

@@ -315,3 +315,24 @@ def test_empty_model_and_errors():
         M.mis_set_graph(ctx.ptr, pb.g, bad)
     with pytest.raises(M.MisError):
         M.mis_set_frame(ctx.ptr, sc["depth"], M.intrinsics(-1, 1, 1, 1, it["W"], it["H"]), sc["pose"])
+
+
+def test_device_graph_validation_deferred():
+    """Device-memory mis_set_graph does not synchronise: bad ids surface at the next register."""
+    torch = pytest.importorskip("torch")
+    sc, pb, fr, _ = scene_problem("c1")
+    ctx = M.Context(M.mis_default_params())
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    M.mis_set_model(ctx.ptr, t(pb.xyz), t(pb.nrm), capacity=pb.xyz.shape[0] + 6000)
+    bad = pb.nbr.copy()
+    bad[3, 1] = pb.g.shape[0] + 7                     # out of range
+    M.mis_set_graph(ctx.ptr, t(pb.g), t(bad))          # returns without a host sync
+    it = sc["intr"]
+    intr = M.intrinsics(it["fx"], it["fy"], it["cx"], it["cy"], it["W"], it["H"])
+    with pytest.raises(M.MisError, match="neighbour list"):
+        M.mis_register(ctx.ptr, t(sc["depth"]), intr, sc["pose"])
+    with pytest.raises(M.MisError):                    # the graph is unbound afterwards
+        M.mis_register(ctx.ptr)
+    M.mis_set_graph(ctx.ptr, t(pb.g), t(pb.nbr))        # a valid graph binds again
+    r = M.report_dict(M.mis_register(ctx.ptr, t(sc["depth"]), intr, sc["pose"]))
+    assert r["status"] == 0
