@@ -374,9 +374,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
     memcpy(id, nccl_unique_id, 128);
     if (api.CommInitRank(&c->nccl_comm, world, id, rank) != 0) { delete c; return MIS_E_NCCL; }
   }
-  if (ensure(c, c->rep_energy, (MIS_MAX_GN + 1) * 5 * 8) != cudaSuccess ||
-      ensure(c, c->rep_nassoc, 2 * (MIS_MAX_GN + 1) * 8) != cudaSuccess ||
-      ensure(c, c->rep_res, MIS_MAX_GN * 4) != cudaSuccess || ensure(c, c->numeric_flag, 16) != cudaSuccess ||
+  if (ensure(c, c->rep, kRepBytes) != cudaSuccess ||
       ensure(c, c->tstamp, 2048) != cudaSuccess || cudaMemset(c->tstamp.p, 0, 2048) != cudaSuccess ||
       ensure(c, c->counter, 64) != cudaSuccess) {
     delete c;
@@ -394,10 +392,9 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->scan, &c->seg_start, &c->seg_nodes, &c->chunks, &c->chunk_off, &c->bitmap, &c->bitmap_all,
                  &c->row_cnt, &c->row_ptr, &c->col, &c->row_of, &c->diag_pos, &c->upper_of, &c->lower_of,
                  &c->seg_slot, &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->part, &c->tstamp, &c->acc, &c->energy,
-                 &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots, &c->numeric_flag,
+                 &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
-                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep_energy, &c->rep_nassoc,
-                 &c->rep_res, &c->cub_tmp};
+                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -605,11 +602,10 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
   return MIS_OK;
 }
 
-// zero the accumulators, run K3 (+ K4/K5 on rank 0), all-reduce across ranks
-static mis_status assemble(Ctx* c, bool dbg) {
+// K3 (+ K4/K5 on rank 0) into the zeroed accumulators, all-reduce across ranks, finalise
+// (which writes report slot `slot` if >= 0 and re-zeroes everything it read)
+static mis_status assemble(Ctx* c, bool dbg, int slot) {
   AccView acc = acc_view(c);
-  TRY(c, cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));   // K3 / K4 / K5 add atomically
-  TRY(c, cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
   const double d2r = M_PI / 180.0;
   AsmPointsArgs a;
   a.md = model_view(c);
@@ -674,6 +670,11 @@ static mis_status assemble(Ctx* c, bool dbg) {
     r.rhs = c->rhs.as<float>();
     r.Minv = c->Minv.as<float>();
     r.lambda = c->prm.lambda;
+    r.w_reg = c->prm.w_reg;
+    r.w_corr = c->prm.w_corr;
+    r.slot = slot;
+    r.rep_energy = rep_energy(c);
+    r.rep_nassoc = rep_nassoc(c);
     launch_finalize(r, c->st);
   }
   TRY(c, cudaGetLastError());
@@ -702,10 +703,8 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.nd = node_view(c);
   s.do_update = update ? 1 : 0;
   s.gn_it = it;
-  s.rep_energy = c->rep_energy.as<double>();
-  s.rep_nassoc = c->rep_nassoc.as<double>();
-  s.rep_res = c->rep_res.as<float>();
-  s.numeric_flag = c->numeric_flag.as<int>();
+  s.rep_res = rep_res(c);
+  s.numeric_flag = numeric_flag(c);
   const bool cl = c->cl_size > 0 && c->cluster_ok && !(c->prm.flags & MIS_F_GRID_SOLVER);
   s.cluster_size = cl ? c->cl_size : 0;
   s.part = c->part.as<int32_t>();
@@ -760,13 +759,14 @@ static mis_status prepare(Ctx* c) {
 
 static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
   memset(rep, 0, sizeof(*rep));
-  double e[(MIS_MAX_GN + 1) * 5], na[2 * (MIS_MAX_GN + 1)];
-  TRY(c, cudaMemcpyAsync(e, c->rep_energy.p, sizeof(e), cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaMemcpyAsync(na, c->rep_nassoc.p, sizeof(na), cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaMemcpyAsync(rep->pcg_rel_res, c->rep_res.p, sizeof(rep->pcg_rel_res), cudaMemcpyDeviceToHost, c->st));
-  int flag = 0;
-  TRY(c, cudaMemcpyAsync(&flag, c->numeric_flag.p, 4, cudaMemcpyDeviceToHost, c->st));
+  double blk[kRepBytes / 8];
+  TRY(c, cudaMemcpyAsync(blk, c->rep.p, kRepBytes, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
+  const double* e = blk;
+  const double* na = blk + kRepN;
+  memcpy(rep->pcg_rel_res, blk + kRepR, sizeof(rep->pcg_rel_res));
+  int flag = 0;
+  memcpy(&flag, blk + kRepF, 4);
   rep->iters = iters;
   rep->status = flag ? MIS_E_NUMERIC : MIS_OK;
   for (int i = 0; i <= MIS_MAX_GN; ++i) {
@@ -795,22 +795,14 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
     if ((s = mis_set_features(c, mem, n_feat, feat_src, feat_dst)) != MIS_OK) return s;
   if ((s = prepare(c)) != MIS_OK) return s;
   const int G = c->prm.gn_iters;
-  TRY(c, cudaMemsetAsync(c->numeric_flag.p, 0, 4, c->st));
-  TRY(c, cudaMemsetAsync(c->rep_energy.p, 0, (MIS_MAX_GN + 1) * 5 * 8, c->st));
-  TRY(c, cudaMemsetAsync(c->rep_nassoc.p, 0, 2 * (MIS_MAX_GN + 1) * 8, c->st));
+  TRY(c, cudaMemsetAsync(c->rep.p, 0, kRepBytes, c->st));
   for (int it = 0; it < G; ++it) {
-    if ((s = assemble(c, false)) != MIS_OK) return s;
-    ProfScope ps(c, P_SOLVE, 2);
-    launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, it,
-                         c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
+    if ((s = assemble(c, false, it)) != MIS_OK) return s;
+    ProfScope ps(c, P_SOLVE, 1);
     TRY(c, run_solve(c, solve_args(c, it, true, c->prm.pcg_iters)));
   }
-  if (c->prm.flags & MIS_F_FINAL_ENERGY) {
-    if ((s = assemble(c, false)) != MIS_OK) return s;
-    ProfScope ps(c, P_SOLVE, 1);
-    launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, G,
-                         c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
-  }
+  if (c->prm.flags & MIS_F_FINAL_ENERGY)
+    if ((s = assemble(c, false, G)) != MIS_OK) return s;
   TRY(c, cudaGetLastError());
   if (rep) return fill_report(c, rep, G);
   return MIS_OK;
@@ -875,7 +867,7 @@ mis_status mis_dbg_associate(mis_ctx* c, mis_mem mem, int32_t* pix, uint8_t* why
   if ((s = prepare(c)) != MIS_OK) return s;
   TRY(c, ensure(c, c->pix, c->cap * 4));
   TRY(c, ensure(c, c->why, c->cap));
-  if ((s = assemble(c, true)) != MIS_OK) return s;
+  if ((s = assemble(c, true, -1)) != MIS_OK) return s;
   TRY(c, cudaMemcpyAsync(pix, c->pix.p, c->n * 4, kind_out(mem), c->st));
   TRY(c, cudaMemcpyAsync(why, c->why.p, c->n, kind_out(mem), c->st));
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
@@ -890,14 +882,12 @@ mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val
   if ((s = prepare(c)) != MIS_OK) return s;
   *nnzb = c->nnzb;
   if (!val) return MIS_OK;
-  if ((s = assemble(c, false)) != MIS_OK) return s;
-  launch_energy_report(acc_view(c), c->prm.w_data, c->prm.w_point, c->prm.w_reg, c->prm.w_corr, 0,
-                       c->rep_energy.as<double>(), c->rep_nassoc.as<double>(), c->st);
+  if ((s = assemble(c, false, 0)) != MIS_OK) return s;
   if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
   if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
   if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)c->m * 24, cudaMemcpyDeviceToHost, c->st));
-  if (energy) TRY(c, cudaMemcpyAsync(energy, c->rep_energy.p, 40, cudaMemcpyDeviceToHost, c->st));
+  if (energy) TRY(c, cudaMemcpyAsync(energy, rep_energy(c), 40, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
   return MIS_OK;
 }
@@ -941,15 +931,22 @@ static FuseArgs fuse_args(Ctx* c, const float* rgb, int32_t frame) {
   a.pix = c->pix.as<int32_t>();
   a.why = c->why.as<uint8_t>();
   a.rank_tag = c->world > 1 ? ((uint32_t)c->rank << 27) : 0u;
+  const int nbk = lift_blocks(c->W, c->H);   // lift counts: [nbk counts | nbk + 1 offsets | u64 n_reg]
+  a.n_reg = c->lift_counts.bytes >= (size_t)(2 * nbk + 4) * 4
+                ? reinterpret_cast<unsigned long long*>(c->lift_counts.as<int32_t>() + 2 * nbk + 2)
+                : nullptr;
   return a;
 }
 
 static mis_status fuse_register(Ctx* c, const float* rgb, int32_t frame) {
   const size_t px = (size_t)c->W * c->H;
+  TRY(c, ensure(c, c->lift_counts, (size_t)(2 * lift_blocks(c->W, c->H) + 4) * 4));
+  if (c->pixkey.bytes < px * 8) c->pixkey_clean = false;
   TRY(c, ensure(c, c->pixkey, px * 8));
   TRY(c, ensure(c, c->pix, c->cap * 4));
   TRY(c, ensure(c, c->why, c->cap));
-  TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
+  if (!c->pixkey_clean) TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));   // else reset by K12
+  c->pixkey_clean = false;
   ProfScope ps(c, P_FREG, c->n > 0 ? 1 : 0);
   launch_fuse_register(fuse_args(c, rgb, frame), c->st);
   TRY(c, cudaGetLastError());
@@ -998,10 +995,9 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
     launch_fuse_apply(a, c->st);
   }
   const int nbk = lift_blocks(c->W, c->H);
-  TRY(c, ensure(c, c->lift_counts, (size_t)(2 * nbk + 4) * 4));
   int32_t* counts = c->lift_counts.as<int32_t>();
-  unsigned long long* cnt = c->counter.as<unsigned long long>();
-  TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(counts + 2 * nbk + 2);   // zeroed by K10
+  if (c->n == 0) TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));   // (K10 not launched)
   // lift: count + offsets, one host readback (the API returns the new model size), then
   // the writes and K2 of the new points run behind the return (overlapping the caller)
   const int64_t base = c->n;
@@ -1011,11 +1007,12 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
     ProfScope ps(c, P_LIFT, 2);
     launch_lift_count(a, counts, nbk, ids_dev, cnt, do_lift, base, c->cap, c->st);
   }
-  int32_t n_lift = 0;
-  unsigned long long n_reg = 0;
-  TRY(c, cudaMemcpyAsync(&n_lift, counts + 2 * nbk + 1, 4, cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaMemcpyAsync(&n_reg, cnt, 8, cudaMemcpyDeviceToHost, c->st));
+  int32_t hb[3];   // [lifted total, registered pixels (u64)]: one readback
+  TRY(c, cudaMemcpyAsync(hb, counts + 2 * nbk + 1, 12, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
+  const int32_t n_lift = hb[0];
+  unsigned long long n_reg = 0;
+  memcpy(&n_reg, hb + 1, 8);
   if (c->n + n_lift > c->cap) {
     *n_out = c->n;
     return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
@@ -1023,10 +1020,13 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   if (n_lift > 0) {
     ProfScope ps(c, P_LIFT, 2);
     ModelView md = model_view(c);
-    launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->st);
+    launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->st);   // also resets the pixel keys
     TRY(c, skin(c, n_lift, md.px + base, md.py + base, md.pz + base, 1, md.kidx + base, md.kw + base, c->cap));
     c->dirty = true;
+  } else {
+    TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
   }
+  c->pixkey_clean = true;
   TRY(c, cudaGetLastError());
   c->n += n_lift;
   *n_out = c->n;

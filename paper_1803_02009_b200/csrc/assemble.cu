@@ -486,7 +486,9 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
 // Finalisation of the normal equations from the accumulators (so the
 // latency-bound solver only streams its rows): warps [0, m) the diagonal blocks
 // -- first, so their block-Jacobi inverses (K7) overlap the rest --, then one
-// warp per off-diagonal upper entry, then one per node:
+// warp per off-diagonal upper entry, then one per node, then one for the
+// energies (report slot).  Every accumulator is re-zeroed after it is read, so
+// the next assembly needs no memset:
 //   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j)),
 //   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
 __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
@@ -507,6 +509,11 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     if (lane < 16) st[36 + lane] = r.acc.mom[16 * e + lane];
     st[52 + lane] = r.acc.graph[36 * e + lane];
     if (lane < 4) st[84 + lane] = r.acc.graph[36 * e + 32 + lane];
+    r.acc.data[36 * e + lane] = 0.f;                       // ready for the next assembly
+    if (lane < 4) r.acc.data[36 * e + 32 + lane] = 0.f;
+    if (lane < 16) r.acc.mom[16 * e + lane] = 0.f;
+    r.acc.graph[36 * e + lane] = 0.f;
+    if (lane < 4) r.acc.graph[36 * e + 32 + lane] = 0.f;
     __syncwarp();
     const int lo = r.lower_of[e];
     const bool diag = lo < 0;
@@ -550,9 +557,25 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     return;
   }
   const int64_t n = gw - r.m - r.nnzb;
-  if (n >= r.m) return;
+  if (n == r.m) {   // energies -> report slot; zeroed (with K3's work counter) for the next assembly
+    if (lane == 0) {
+      double* E = r.acc.energy;
+      if (r.slot >= 0) {
+        double* rep = r.rep_energy + 5 * r.slot;
+        rep[0] = E[0]; rep[1] = E[1]; rep[2] = E[2]; rep[3] = E[3];
+        rep[4] = (double)r.w_data * E[0] + (double)r.w_pt * E[1] + (double)r.w_reg * E[2] + (double)r.w_corr * E[3];
+        r.rep_nassoc[r.slot] = E[4];
+        r.rep_nassoc[MIS_MAX_GN + 1 + r.slot] = E[5];   // fp64 guard-band re-evaluations
+      }
+      for (int q = 0; q < 7; ++q) E[q] = 0.0;
+    }
+    return;
+  }
+  if (n > r.m) return;
   if (lane < 6) st[lane] = r.acc.rhs_data[6 * n + lane];   // 6 rhs_data | 12 node moments
   else if (lane < 18) st[lane] = r.acc.node_mom[12 * n + lane - 6];
+  if (lane < 6) { r.acc.rhs_data[6 * n + lane] = 0.f; }
+  else if (lane < 18) r.acc.node_mom[12 * n + lane - 6] = 0.f;
   __syncwarp();
   if (lane < 6) {
     const float* Nm = st + 6;
@@ -564,11 +587,12 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
       pt = Nm[9 + (lane - 3)];
     }
     r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + r.acc.rhs_graph[6 * n + lane];
+    r.acc.rhs_graph[6 * n + lane] = 0.f;
   }
 }
 
 void launch_finalize(const FinalArgs& r, cudaStream_t s) {
-  const int64_t warps = 2 * (int64_t)r.m + r.nnzb;
+  const int64_t warps = 2 * (int64_t)r.m + r.nnzb + 1;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 0) k_finalize<<<(unsigned)blocks, 256, 0, s>>>(r);
 }

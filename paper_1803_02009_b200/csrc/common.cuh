@@ -98,7 +98,10 @@ struct FinalArgs {
   float* Hval;                // nnzb*36 final blocks (both triangles)
   float* rhs;                 // 6m final right-hand side
   float* Minv;                // m*36 block-Jacobi inverses
-  float lambda;
+  float lambda, w_reg, w_corr;
+  int slot;                   // report slot of this assembly (-1: none)
+  double* rep_energy;         // (MIS_MAX_GN+1)*5
+  double* rep_nassoc;         // 2*(MIS_MAX_GN+1): association counts, fp64 guard counts
 };
 void launch_finalize(const FinalArgs& r, cudaStream_t s);
 
@@ -137,8 +140,6 @@ struct SolveArgs {
   NodeView nd;
   int do_update;              // 0: only build the system (debug)
   int gn_it;                  // report slot
-  double* rep_energy;         // (MIS_MAX_GN+1)*5
-  double* rep_nassoc;         // MIS_MAX_GN+1
   float* rep_res;             // MIS_MAX_GN
   int* numeric_flag;
   // cluster-resident variant (pcg_cluster.cu); cluster_size == 0 -> grid variant
@@ -163,8 +164,6 @@ cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
 struct PlanOut { int32_t cl_size, max_rows, max_nnz, pad; int64_t smem; };
 void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,
                          cudaStream_t s);
-void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr,
-                          int slot, double* rep_energy, double* rep_nassoc, cudaStream_t s);
 
 // ---- fusion (fuse.cu)
 void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const FrameView& fr, float* xyz_cam,
@@ -180,6 +179,7 @@ struct FuseArgs {
   int32_t* pix;               // n
   uint8_t* why;               // n (nullable)
   uint32_t rank_tag;          // rank << 27 in the key's index bits (0 on one GPU): keys unique across ranks
+  unsigned long long* n_reg;  // registered-pixel counter (zeroed by K10, filled by the lift count)
 };
 void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);

@@ -53,6 +53,8 @@ struct Ctx {
   int64_t nnzb = 0;
   bool pattern_valid = false;
   DBuf bitmap, bitmap_all, row_cnt, row_ptr, col, row_of, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot;
+  bool bitmap_clean = false;   // pattern bitmap all-zero (cleared by k_row_fill) -> no memset
+  int64_t bitmap_words = 0;
   DBuf nnz_dev;   // int64 info: [0] nnz, [1] nseg, [2] nchunk, [3] set_graph validation flags, [4..6] plan
 
   // ---- system and solver
@@ -63,7 +65,7 @@ struct Ctx {
   int last_solver = 0;   // cluster size of the last PCG launch (0: grid kernel)
   DBuf part, tstamp;
   size_t acc_floats = 0;
-  DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots, numeric_flag;
+  DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots;
 
   // ---- frame
   bool have_frame = false;
@@ -78,10 +80,11 @@ struct Ctx {
 
   // ---- fuse
   DBuf pixkey, pix, why, lift_counts, counter;
+  bool pixkey_clean = false;   // pixel keys all-ones (reset by the lift write) -> no memset before K10
   DBuf ids_dev;   // int64 [0] next fresh point id, [1] id base of the last lift, [2] lifted points written
 
   // ---- report
-  DBuf rep_energy, rep_nassoc, rep_res;
+  DBuf rep;   // report block (one memset / one readback per registration), layout below
 
   DBuf cub_tmp;
 
@@ -97,6 +100,15 @@ struct Ctx {
 enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO,
        P_REDUCE };
 void count_launches(int64_t k);
+
+// report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual
+// MIS_MAX_GN floats | numeric flag], doubles
+constexpr size_t kRepN = 5 * (MIS_MAX_GN + 1), kRepR = kRepN + 2 * (MIS_MAX_GN + 1), kRepF = kRepR + MIS_MAX_GN / 2,
+                 kRepBytes = (kRepF + 1) * 8;
+inline double* rep_energy(Ctx* c) { return c->rep.as<double>(); }
+inline double* rep_nassoc(Ctx* c) { return c->rep.as<double>() + kRepN; }
+inline float* rep_res(Ctx* c) { return reinterpret_cast<float*>(c->rep.as<double>() + kRepR); }
+inline int* numeric_flag(Ctx* c) { return reinterpret_cast<int*>(c->rep.as<double>() + kRepF); }
 
 // Records an event pair around a group of `nk` kernel launches on the context
 // stream when profiling is on; always adds nk to the launch counter.

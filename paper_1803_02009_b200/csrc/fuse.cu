@@ -107,6 +107,7 @@ __device__ bool normal64(const FrameView& f, int px, int py, double* N, double* 
 // of ((|dz| in 1e-8 mm units) << 32 | point index) per pixel (reading A19).
 __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && a.n_reg) *a.n_reg = 0;   // counted later by the lift count
   if (i >= a.md.n) return;
   const FrameView& f = a.fr;
   const double v[3] = {a.md.px[i], a.md.py[i], a.md.pz[i]}, n[3] = {a.md.nx[i], a.md.ny[i], a.md.nz[i]};
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   __shared__ int wsum[kLiftBlock / 32];
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const bool on = lift_pixel(a, p);
+  if (p < a.fr.W * a.fr.H) a.pixkey[p] = ~0ull;   // the next fusion finds the keys reset (no memset)
   const unsigned bal = __ballot_sync(0xffffffffu, on);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) wsum[w] = __popc(bal);

@@ -140,19 +140,4 @@ cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s) {
   return launch_solve_grid(a, num_sms, s);
 }
 
-__global__ void k_energy_report(AccView acc, float w_data, float w_pt, float w_reg, float w_corr, int slot,
-                                double* rep_energy, double* rep_nassoc) {
-  const double* E = acc.energy;
-  double* rep = rep_energy + 5 * slot;
-  rep[0] = E[0]; rep[1] = E[1]; rep[2] = E[2]; rep[3] = E[3];
-  rep[4] = (double)w_data * E[0] + (double)w_pt * E[1] + (double)w_reg * E[2] + (double)w_corr * E[3];
-  rep_nassoc[slot] = E[4];
-  rep_nassoc[MIS_MAX_GN + 1 + slot] = E[5];   // fp64 guard-band re-evaluations
-}
-
-void launch_energy_report(const AccView& acc, float w_data, float w_pt, float w_reg, float w_corr, int slot,
-                          double* rep_energy, double* rep_nassoc, cudaStream_t s) {
-  k_energy_report<<<1, 1, 0, s>>>(acc, w_data, w_pt, w_reg, w_corr, slot, rep_energy, rep_nassoc);
-}
-
 }  // namespace mis

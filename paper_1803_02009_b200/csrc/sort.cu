@@ -28,21 +28,19 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-// key: exact big-endian packing of the ascending ids when K * bits <= 64,
-// else (first id, 64-bits hash of the rest); equal tuples -> equal keys.
-__global__ void k_tuple_keys(int64_t n, int64_t cap, const int32_t* kidx, int K, int bits, uint64_t* keys,
+// key: the top kb bits of a 64-bit mix of the (ascending) id tuple.  Equal tuples get
+// equal keys, so the stable radix sort makes every tuple's points contiguous up to
+// key collisions; a collision only interleaves the points of two tuples, which
+// k_seg_flags (comparing whole tuples) then splits into more, shorter segments --
+// never a wrong one.  kb ~ log2(#tuples) + 7 keeps collisions rare with 8-bit
+// radix passes: 3 passes at c3 instead of 5 for the exact 40-bit packing.
+__global__ void k_tuple_keys(int64_t n, int64_t cap, const int32_t* kidx, int K, int kb, uint64_t* keys,
                              uint32_t* vals) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint64_t key = 0;
-  if (K * bits <= 64) {
-    for (int s = 0; s < K; ++s) key = (key << bits) | (uint64_t)kidx[s * cap + i];
-  } else {
-    uint64_t h = 0x9e3779b97f4a7c15ull;
-    for (int s = 1; s < K; ++s) h = mix64(h ^ (uint64_t)kidx[s * cap + i]);
-    key = ((uint64_t)kidx[i] << (64 - bits)) | (h >> bits);
-  }
-  keys[i] = key;
+  uint64_t h = 0x9e3779b97f4a7c15ull;
+  for (int s = 0; s < K; ++s) h = mix64(h ^ (uint64_t)(uint32_t)kidx[s * cap + i]);
+  keys[i] = kb >= 64 ? h : (h >> (64 - kb));
   vals[i] = (uint32_t)i;
 }
 
@@ -120,13 +118,16 @@ cudaError_t build_order(Ctx* c) {
   if (n > 0) {
     CK(ensure(c, c->keys, n * 8)); CK(ensure(c, c->keys2, n * 8));
     CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
-    const int bits = bits_for(c->m);
+    // tuples expected: the last pattern's segment count (the model changes little between
+    // frames), else n / 8; key bits = log2 of that + 7, rounded up to whole 8-bit passes
+    const int64_t t_est = c->nseg > 0 ? c->nseg : std::max<int64_t>(n / 8, 1);
+    const int kb = std::min(64, (bits_for((int)std::min<int64_t>(t_est, 1 << 30)) + 7 + 7) / 8 * 8);
     const int b = (int)((n + 255) / 256);
-    k_tuple_keys<<<b, 256, 0, c->st>>>(n, c->cap, A.kidx.as<int32_t>(), K, bits, c->keys.as<uint64_t>(),
+    k_tuple_keys<<<b, 256, 0, c->st>>>(n, c->cap, A.kidx.as<int32_t>(), K, kb, c->keys.as<uint64_t>(),
                                         c->vals.as<uint32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceRadixSort::SortPairs(t, s, c->keys.as<uint64_t>(), c->keys2.as<uint64_t>(),
-                                             c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, K * bits <= 64 ? K * bits : 64, c->st);
+                                             c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, kb, c->st);
     }));
     k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
     count_launches(2);   // keys, gather (CUB's sort kernels are library code, not counted)
@@ -245,7 +246,7 @@ __global__ void k_row_count(const unsigned long long* bm, int64_t W, int m, int3
 }
 
 // one warp per row: columns in ascending order, row index of each entry, diagonal position
-__global__ void k_row_fill(const unsigned long long* bm, int64_t W, int m, const int32_t* row_ptr, int32_t* col,
+__global__ void k_row_fill(unsigned long long* bm, int64_t W, int m, const int32_t* row_ptr, int32_t* col,
                            int32_t* row_of, int32_t* diag_pos) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -253,7 +254,11 @@ __global__ void k_row_fill(const unsigned long long* bm, int64_t W, int m, const
   int pos = row_ptr[r];
   for (int64_t w0 = 0; w0 < W; w0 += 32) {
     const int64_t w = w0 + lane;
-    unsigned long long word = w < W ? bm[r * W + w] : 0ull;
+    unsigned long long word = 0ull;
+    if (w < W) {
+      word = bm[r * W + w];
+      bm[r * W + w] = 0ull;   // cleared for the next pattern build (no memset)
+    }
     const int cnt = __popcll(word);
     int inc = cnt;
 #pragma unroll
@@ -331,8 +336,11 @@ cudaError_t build_pattern(Ctx* c) {
   const int K = c->K, P = K * (K + 1) / 2, m = c->m;
   const int64_t W = (m + 63) / 64, words = (int64_t)m * W;
   int64_t* info = c->nnz_dev.as<int64_t>();
+  if (c->bitmap.bytes < (size_t)words * 8 || c->bitmap_words != words) c->bitmap_clean = false;
   CK(ensure(c, c->bitmap, words * 8));
-  CK(cudaMemsetAsync(c->bitmap.p, 0, words * 8, c->st));
+  if (!c->bitmap_clean) CK(cudaMemsetAsync(c->bitmap.p, 0, words * 8, c->st));   // else cleared by k_row_fill
+  c->bitmap_clean = false;
+  c->bitmap_words = words;
   unsigned long long* bm = c->bitmap.as<unsigned long long>();
   const int grid = c->num_sms * 8;
   k_mark<<<grid, 256, 0, c->st>>>(c->seg_nodes.as<int32_t>(), info + 1, 0, K, m, c->prm.n_nbr, c->nbr.as<int32_t>(),
@@ -374,6 +382,7 @@ cudaError_t build_pattern(Ctx* c) {
   CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
   k_row_fill<<<wb, 256, 0, c->st>>>(bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(),
                                     c->diag_pos.as<int32_t>());
+  c->bitmap_clean = true;
   count_launches(1 + (nnz > 0) + (c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P > 0));
   if (nnz > 0)
     k_upper_lower<<<(int)std::min<int64_t>(grid, (nnz + 255) / 256), 256, 0, c->st>>>(
@@ -396,6 +405,9 @@ cudaError_t build_pattern(Ctx* c) {
   c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)m + m6;
   CK(ensure(c, c->acc, c->acc_floats * 4));
   CK(ensure(c, c->energy, 8 * 8));
+  // zeroed once per pattern; afterwards every finalisation re-zeroes what it read
+  CK(cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));
+  CK(cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
   CK(ensure(c, c->Hval, (size_t)nnz * 36 * 4));
   CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)m * 36 * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
