@@ -63,8 +63,10 @@ FrameView frame_view(Ctx* c) {
   f.W = c->W; f.H = c->H;
   f.fx = c->intr.fx; f.fy = c->intr.fy; f.cx = c->intr.cx; f.cy = c->intr.cy;
   f.fxd = c->intr.fx; f.fyd = c->intr.fy; f.cxd = c->intr.cx; f.cyd = c->intr.cy;
+  f.ifxd = 1.0 / f.fxd; f.ifyd = 1.0 / f.fyd;
   f.depth = c->depth.as<float>();
   f.nmap = c->nmap.as<float4>();
+  f.nmapd = c->nmapd.as<double4>();
   for (int i = 0; i < 9; ++i) { f.R[i] = c->pose[i]; f.Rd[i] = c->pose[i]; }
   for (int i = 0; i < 3; ++i) { f.T[i] = c->pose[9 + i]; f.Td[i] = c->pose[9 + i]; }
   return f;
@@ -367,6 +369,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
     if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) { delete c; return MIS_E_CUDA; }
     c->own_stream = true;
   }
+
   if (world > 1) {
     NcclApi& api = nccl();
     if (!api.ok || !nccl_unique_id) { delete c; return MIS_E_NCCL; }
@@ -394,7 +397,7 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->seg_slot, &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->part, &c->tstamp, &c->acc, &c->energy,
                  &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
-                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->cub_tmp};
+                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -403,6 +406,7 @@ mis_status mis_destroy(mis_ctx* c) {
   }
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(c->nccl_comm);
   if (c->own_stream) cudaStreamDestroy(c->st);
+
   delete c;
   return MIS_OK;
 }
@@ -570,9 +574,10 @@ mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const m
   const size_t px = (size_t)c->W * c->H;
   TRY(c, ensure(c, c->depth, px * 4));
   TRY(c, ensure(c, c->nmap, px * 16));
+  TRY(c, ensure(c, c->nmapd, px * 32));
   TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, kind_in(mem), c->st));
   ProfScope ps(c, P_FRAME, 1);
-  launch_frame_prep(frame_view(c), c->nmap.as<float4>(), c->st);
+  launch_frame_prep(frame_view(c), c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
   TRY(c, cudaGetLastError());
   c->have_frame = true;
   return MIS_OK;
@@ -606,6 +611,7 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
 // (which writes report slot `slot` if >= 0 and re-zeroes everything it read)
 static mis_status assemble(Ctx* c, bool dbg, int slot) {
   AccView acc = acc_view(c);
+  c->acc_dirty = true;   // until the finalisation below has re-zeroed them
   const double d2r = M_PI / 180.0;
   AsmPointsArgs a;
   a.md = model_view(c);
@@ -620,12 +626,15 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
   a.cos_eps_n = (float)a.cos_eps_nd;
   a.acc = acc;
+  TRY(c, ensure(c, c->pstate, (size_t)(c->K + 2) * 16 * (size_t)std::max<int64_t>(c->n, 1)));
+  a.pstate = c->pstate.as<float4>();
+  a.pstride = std::max<int64_t>(c->n, 1);
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
-  a.guard_counter = c->energy.as<double>() + 5;
+
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
-  if (a.nchunk > 0) {
-    ProfScope ps(c, P_POINTS, 1);
+  if (c->n > 0) {
+    ProfScope ps(c, P_POINTS, a.nchunk > 0 ? 2 : 1);   // K3a, K3b
     launch_assemble_points(c->K, a, c->num_sms, c->st);
   }
   TRY(c, cudaGetLastError());
@@ -653,7 +662,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   }
   if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
     if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
-    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), 6) != cudaSuccess) return MIS_E_NCCL;
+    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), kEnergyDoubles) != cudaSuccess) return MIS_E_NCCL;
   }
   {   // accumulators -> final H (both triangles), b, block-Jacobi inverses
     ProfScope ps(c, P_REDUCE, 1);
@@ -677,6 +686,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     r.rep_nassoc = rep_nassoc(c);
     launch_finalize(r, c->st);
   }
+  c->acc_dirty = false;
   TRY(c, cudaGetLastError());
   return MIS_OK;
 }

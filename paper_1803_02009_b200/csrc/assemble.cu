@@ -1,20 +1,26 @@
 // assemble.cu -- K3 (per-point warp + association + residuals + J^T J) and
 // K4/K5 (regulariser and feature terms) of one Gauss-Newton iteration.
 //
-// K3 design: points are sorted by their canonical kNN tuple
-// (K13), so a "chunk" (<= 256 consecutive points of one tuple segment) shares
-// all K nodes.  One warp owns a chunk: each lane warps one point (Eq. 1),
-// associates it (Eq. 7, with an fp64 guard band at every decision boundary)
-// and writes one row f of per-point factors to shared memory:
-//   c' = [w_1 u_1, ..., w_K u_K, r_pl]      u_j = [a_j x n', n'] (Eq. 8 Jacobian row / w_j)
-//   e' = [w_1 a_1, w_1, ..., w_K a_K, w_K, r']   (point-to-point moments, r' = R^T (v~ - q))
-// Every per-chunk sum the normal equations need is an entry of sum_i c'c'^T or
-// sum_i e'e'^T (upper triangles), i.e. two tiny SYRKs.  Lanes own 4x4 tiles of
-// those triangles and accumulate them from shared memory in registers over the
-// chunk's points (16 FFMA per 2 LDS.128), then commit each entry once per
-// chunk with a global atomic add.  K_finalize (solve.cu) turns the moments
-// into 6x6 point-to-point blocks: sum of w_j w_l [-[a_j]x[a_l]x, [a_j]x; -[a_l]x, I].
+// K3 design, two kernels per Gauss-Newton iteration:
+//  K3a, one thread per point: warp (Eq. 1), projective association (Eq. 7) and
+//   residuals in fp64 (the oracle's arithmetic: decisions agree up to rounding
+//   order), writing a compact per-point factor state;
+//  K3b, one warp per chunk (<= kChunk consecutive points of one kNN-tuple
+//   segment, so all points share the K nodes): lanes rebuild the factor rows
+//     c' = [w_1 u_1, ..., w_K u_K, r_pl]      u_j = [a_j x n', n'] (Eq. 8 Jacobian row / w_j)
+//     e' = [w_1 a_1, w_1, ..., w_K a_K, w_K, r']   (point-to-point moments, r' = R^T (v~ - q))
+//   in shared memory.  Every per-chunk sum the normal equations need is an entry
+//   of sum_i c'c'^T or sum_i e'e'^T (upper triangles), i.e. two tiny SYRKs: lanes
+//   own 4x4 tiles and accumulate them in registers (16 FFMA per 2 LDS.128), then
+//   commit each chunk's sums with float4 / float2 atomic adds.  K_finalize turns
+//   the moments into 6x6 point-to-point blocks:
+//   sum of w_j w_l [-[a_j]x[a_l]x, [a_j]x; -[a_l]x, I].
+// Splitting the latency-bound per-point pass (light threads, many warps in
+// flight) from the register-heavy SYRK pass doubled the K3 throughput over a
+// fused kernel that could keep only 16 warps per SM resident.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "solve_common.cuh"
 
@@ -51,277 +57,213 @@ constexpr int kWarps = 8;
 #ifndef MIS_K3_MINB
 #define MIS_K3_MINB 2   // resident blocks per SM the register budget is sized for
 #endif
-#ifndef MIS_GUARD_SCALE
-#define MIS_GUARD_SCALE 1.0f
+// ---------------------------------------------------------------- K3a
+// One thread per point (points in tuple order, so neighbouring threads read the
+// same node states from L1): warp (Eq. 1), projective association (Eq. 7) and
+// residuals (Eq. 8, point to point), all in fp64 from the fp64 node state --
+// the same arithmetic as the oracle, so every association decision agrees with
+// it up to fp64 rounding order (B200 runs fp64 at half the fp32 rate; this pass
+// is bound by its loads).  Writes the point's compact factor state, K + 2 float4
+// planes
+//   s < K: (w_s a_s, w_s)     K: (r', r_pl)     K + 1: (n', 0)
+// (zeros when not associated) from which K3b rebuilds the factor rows, and
+// accumulates E_data = sum r_pl^2, E_pt = sum |r'|^2 and the association count.
+#ifndef MIS_K3A_MINB
+#define MIS_K3A_MINB 2
 #endif
-// Guard bands around every fp32 decision, each >=3x the fp32
-// error bound: u, v <= ~1.5e-4 px (x_hat = v + small correction, then R x_hat + T
-// and one division); |v~ - q| <= ~3e-5 mm; n~.N <= ~1e-6.
-constexpr float kGuardPx = 5e-4f * MIS_GUARD_SCALE;     // rounding of u, v (pixels)
-constexpr float kGuardRel = 2e-5f * MIS_GUARD_SCALE;    // distance gate (relative to eps_d)
-constexpr float kGuardCos = 1e-5f * MIS_GUARD_SCALE;    // angle gate (cosine)
-
-__device__ __forceinline__ bool depth_ok_d(float d) { return isfinite(d) && d > 0.0f; }
-
-// fp64 re-evaluation of one point's warp and Eq. 7 gates (the oracle's
-// arithmetic order is irrelevant here; only decisions within ~1e-12 of a
-// threshold can differ).  Used for the rare points whose fp32 quantities lie
-// inside a guard band.
-// Arguments by value / pointer-to-global only: a reference to the kernel's
-// parameter struct would force an addressable (local-memory) copy of it.
-struct Fp64Args {
-  const float *px, *py, *pz, *nx, *ny, *nz, *kw;
-  int64_t cap;
-  const double* Rt64;
-  const float* g;
-  const float* depth;
-  int W, H;
-  double fxd, fyd, cxd, cyd;
-  double Rd[9], Td[3];
-  double eps_dd, cos_eps_nd;
+template <int K>
+struct PState {   // a point's compact factor state (zeros: not associated)
+  float4 wa[K];   // (w_s a_s, w_s)
+  float4 rr;      // (r', r_pl)
+  float4 nn;      // (n', 0)
 };
 
-template <int K>
-__device__ __noinline__ void assoc_fp64(const Fp64Args* __restrict__ pa, int64_t i, const int32_t* nodes, float* vt_out,
-                                        float* q_out, float* N_out, int* pix_out, uint8_t* why_out) {
-  const Fp64Args& a = *pa;
-  struct MV { const float *px, *py, *pz, *nx, *ny, *nz, *kw; int64_t cap; } md = {a.px, a.py, a.pz, a.nx, a.ny, a.nz,
-                                                                                 a.kw, a.cap};
-  struct FV { int W, H; double fxd, fyd, cxd, cyd; const double *Rd, *Td; const float* depth; } f = {
-      a.W, a.H, a.fxd, a.fyd, a.cxd, a.cyd, a.Rd, a.Td, a.depth};
-  struct ND { const double* Rt64; const float* g; } ndv = {a.Rt64, a.g};
-  double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
-  double W = 0, wr[K];
-  for (int s = 0; s < K; ++s) { wr[s] = md.kw[s * md.cap + i]; W += wr[s]; }
-  *pix_out = -1;
-  *why_out = 0;
-  if (!(W > 0)) return;
-  double xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
-  for (int s = 0; s < K; ++s) {
-    const double* Rt = ndv.Rt64 + 12 * nodes[s];
-    const float* g = ndv.g + 3 * nodes[s];
-    const double wn = wr[s] / W;
-    double d[3] = {v[0] - g[0], v[1] - g[1], v[2] - g[2]};
-    for (int r = 0; r < 3; ++r) {
-      double ar = Rt[3 * r] * d[0] + Rt[3 * r + 1] * d[1] + Rt[3 * r + 2] * d[2];
-      xh[r] += wn * (ar + (double)g[r] + Rt[9 + r]);
-      mh[r] += wn * (Rt[3 * r] * n[0] + Rt[3 * r + 1] * n[1] + Rt[3 * r + 2] * n[2]);
-    }
-  }
-  double vt[3], nt[3];
-  for (int r = 0; r < 3; ++r) {
-    vt[r] = f.Rd[3 * r] * xh[0] + f.Rd[3 * r + 1] * xh[1] + f.Rd[3 * r + 2] * xh[2] + f.Td[r];
-    nt[r] = f.Rd[3 * r] * mh[0] + f.Rd[3 * r + 1] * mh[1] + f.Rd[3 * r + 2] * mh[2];
-  }
-  const double ml = sqrt(mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2]);
-  if (ml < 1e-12) return;
-  for (int r = 0; r < 3; ++r) { nt[r] /= ml; vt_out[r] = (float)vt[r]; }
-  uint8_t why = 0;
-  if (!(vt[2] > 0)) { *why_out = why; return; }
-  why |= 1;
-  const double u = f.fxd * vt[0] / vt[2] + f.cxd, vv = f.fyd * vt[1] / vt[2] + f.cyd;
-  const double fu = floor(u + 0.5), fv = floor(vv + 0.5);
-  if (fu < 0 || fv < 0 || fu >= f.W || fv >= f.H) { *why_out = why; return; }
-  why |= 2;
-  const int px = (int)fu, py = (int)fv, W_ = f.W;
-  const float D = f.depth[py * W_ + px];
-  if (!depth_ok_d(D)) { *why_out = why; return; }
-  why |= 4;
-  // normal in fp64 from the five depths (reading A11)
-  if (px <= 0 || py <= 0 || px >= W_ - 1 || py >= f.H - 1) { *why_out = why; return; }
-  const float l = f.depth[py * W_ + px - 1], r = f.depth[py * W_ + px + 1];
-  const float up = f.depth[(py - 1) * W_ + px], dn = f.depth[(py + 1) * W_ + px];
-  if (!depth_ok_d(l) || !depth_ok_d(r) || !depth_ok_d(up) || !depth_ok_d(dn)) { *why_out = why; return; }
-  const double ax = ((px + 1) - f.cxd) * r / f.fxd - ((px - 1) - f.cxd) * l / f.fxd;
-  const double ay = (py - f.cyd) * (double)r / f.fyd - (py - f.cyd) * (double)l / f.fyd;
-  const double az = (double)r - (double)l;
-  const double bx = (px - f.cxd) * (double)dn / f.fxd - (px - f.cxd) * (double)up / f.fxd;
-  const double by = ((py + 1) - f.cyd) * dn / f.fyd - ((py - 1) - f.cyd) * up / f.fyd;
-  const double bz = (double)dn - (double)up;
-  double N[3] = {ay * bz - az * by, az * bx - ax * bz, ax * by - ay * bx};
-  const double len = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
-  if (len < 1e-12) { *why_out = why; return; }
-  const double q[3] = {(px - f.cxd) * D / f.fxd, (py - f.cyd) * D / f.fyd, (double)D};
-  for (int c = 0; c < 3; ++c) N[c] /= len;
-  if (N[0] * q[0] + N[1] * q[1] + N[2] * q[2] > 0) for (int c = 0; c < 3; ++c) N[c] = -N[c];
-  why |= 8;
-  const double dd = sqrt((vt[0] - q[0]) * (vt[0] - q[0]) + (vt[1] - q[1]) * (vt[1] - q[1]) + (vt[2] - q[2]) * (vt[2] - q[2]));
-  for (int c = 0; c < 3; ++c) { q_out[c] = (float)q[c]; N_out[c] = (float)N[c]; }
-  if (!(dd < a.eps_dd)) { *why_out = why; return; }
-  why |= 16;
-  const double cs = nt[0] * N[0] + nt[1] * N[1] + nt[2] * N[2];
-  if (!(cs > a.cos_eps_nd)) { *why_out = why; return; }
-  why |= 32;
-  *why_out = why;
-  *pix_out = py * W_ + px;
-}
-
-// A point's inputs, loaded one batch ahead (software prefetch: the global loads
-// of batch b+1 are in flight while batch b is warped and accumulated).
-template <int K>
-struct PointIn {
-  float v[3], n[3], w[K];
-};
-
-template <int K>
-__device__ __forceinline__ void load_point(const ModelView& md, int64_t i, bool act, PointIn<K>& p) {
-  if (!act) return;
-  p.v[0] = md.px[i]; p.v[1] = md.py[i]; p.v[2] = md.pz[i];
-  p.n[0] = md.nx[i]; p.n[1] = md.ny[i]; p.n[2] = md.nz[i];
-#pragma unroll
-  for (int s = 0; s < K; ++s) p.w[s] = md.kw[s * md.cap + i];
-}
-
-// One lane, one point: warp, associate, write the factor row (zeros if not associated).
 template <int K, bool DBG>
-__device__ __forceinline__ bool point_row(const AsmPointsArgs& a, int64_t i, bool act, const PointIn<K>& pin,
-                                          const float* __restrict__ ND, const int32_t* nodes,
-                                          float* __restrict__ row) {
-  using L = Lay<K>;
-  bool assoc = false;
+__device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, PState<K>& st, double& ed, double& ep,
+                                            int& as) {
+  const ModelView& md = a.md;
+  const FrameView& fr = a.fr;
+  const double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
+  double wn[K], W = 0.0;
+  int nid[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    wn[s] = md.kw[s * md.cap + i];
+    nid[s] = md.kidx[s * md.cap + i];
+    W += wn[s];
+  }
   int pix = -1;
   uint8_t why = 0;
-  if (act) {
-    const ModelView& md = a.md;
-    const FrameView& fr = a.fr;
-    const float v0 = pin.v[0], v1 = pin.v[1], v2 = pin.v[2];
-    const float n0 = pin.n[0], n1 = pin.n[1], n2 = pin.n[2];
-    float wn[K], ax[K], ay[K], az[K];
-    float W = 0.f;
+  double vt[3] = {0, 0, 0}, q[3] = {0, 0, 0}, N[3] = {0, 0, 0};
+  float af[K][3];
 #pragma unroll
-    for (int s = 0; s < K; ++s) { wn[s] = pin.w[s]; W += wn[s]; }
-    if (W > 0.f) {
-      const float iW = 1.0f / W;
-      float x0 = 0, x1 = 0, x2 = 0, m0 = 0, m1 = 0, m2 = 0;
+  for (int s = 0; s < K; ++s) af[s][0] = af[s][1] = af[s][2] = 0.f;
+  if (W > 0.0) {
+    // divisions and square roots (slow fp64 sequences) are replaced by one reciprocal
+    // each and squared comparisons: the results differ from the oracle's only in the
+    // last bits, so only exact ties could decide differently
+    const double iW = 1.0 / W;
+    double xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
 #pragma unroll
-      for (int s = 0; s < K; ++s) {
-        const float* nd = ND + 16 * s;   // R(9) t(3) g(3)
-        wn[s] *= iW;
-        const float d0 = v0 - nd[12], d1 = v1 - nd[13], d2 = v2 - nd[14];
-        ax[s] = nd[0] * d0 + nd[1] * d1 + nd[2] * d2;
-        ay[s] = nd[3] * d0 + nd[4] * d1 + nd[5] * d2;
-        az[s] = nd[6] * d0 + nd[7] * d1 + nd[8] * d2;
-        // x_hat = sum w (a + g + t) = v + sum w ((R - I) d + t)  (sum w = 1): the correction is
-        // small, so its fp32 rounding is ~100x below that of summing ~60 mm terms
-        x0 += wn[s] * ((ax[s] - d0) + nd[9]);
-        x1 += wn[s] * ((ay[s] - d1) + nd[10]);
-        x2 += wn[s] * ((az[s] - d2) + nd[11]);
-        m0 += wn[s] * (nd[0] * n0 + nd[1] * n1 + nd[2] * n2);
-        m1 += wn[s] * (nd[3] * n0 + nd[4] * n1 + nd[5] * n2);
-        m2 += wn[s] * (nd[6] * n0 + nd[7] * n1 + nd[8] * n2);
-      }
-      x0 += v0;
-      x1 += v1;
-      x2 += v2;
-      const float* R = fr.R;
-      float vt[3] = {R[0] * x0 + R[1] * x1 + R[2] * x2 + fr.T[0], R[3] * x0 + R[4] * x1 + R[5] * x2 + fr.T[1],
-                     R[6] * x0 + R[7] * x1 + R[8] * x2 + fr.T[2]};
-      const float ml = sqrtf(m0 * m0 + m1 * m1 + m2 * m2);
-      float q[3] = {0, 0, 0}, N[3] = {0, 0, 0};
-      bool guard = !(ml > 1e-6f) || fabsf(vt[2]) < 1e-3f;
-      if (!guard && vt[2] > 0.f) {
-        why = 1;
-        const float iz = 1.0f / vt[2];
-        const float uu = fr.fx * vt[0] * iz + fr.cx + 0.5f, vv = fr.fy * vt[1] * iz + fr.cy + 0.5f;
-        const float fu = floorf(uu), fv = floorf(vv);
-        if (fminf(uu - fu, fu + 1.f - uu) < kGuardPx || fminf(vv - fv, fv + 1.f - vv) < kGuardPx) {
-          guard = true;
-        } else if (fu >= 0.f && fv >= 0.f && fu < (float)fr.W && fv < (float)fr.H) {
-          why |= 2;
-          const int px = (int)fu, py = (int)fv;
-          const float4 nm = fr.nmap[py * fr.W + px];
-          if (nm.w > 0.f) {
-            why |= 4;
-            if (nm.x != 0.f || nm.y != 0.f || nm.z != 0.f) {
-              why |= 8;
-              N[0] = nm.x; N[1] = nm.y; N[2] = nm.z;
-              q[0] = (px - fr.cx) * nm.w / fr.fx;
-              q[1] = (py - fr.cy) * nm.w / fr.fy;
-              q[2] = nm.w;
-              const float e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
-              const float dd = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
-              if (fabsf(dd - a.eps_d) < kGuardRel * a.eps_d) {
-                guard = true;
-              } else if (dd < a.eps_d) {
-                why |= 16;
-                const float im = 1.0f / ml;
-                const float nt0 = (R[0] * m0 + R[1] * m1 + R[2] * m2) * im;
-                const float nt1 = (R[3] * m0 + R[4] * m1 + R[5] * m2) * im;
-                const float nt2 = (R[6] * m0 + R[7] * m1 + R[8] * m2) * im;
-                const float cs = nt0 * N[0] + nt1 * N[1] + nt2 * N[2];
-                if (fabsf(cs - a.cos_eps_n) < kGuardCos) guard = true;
-                else if (cs > a.cos_eps_n) { why |= 32; pix = py * fr.W + px; }
-              }
+    for (int s = 0; s < K; ++s) {
+      const double2* rt = reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nid[s]);   // R (9), t (3)
+      const double2 R01 = __ldg(rt), R23 = __ldg(rt + 1), R45 = __ldg(rt + 2), R67 = __ldg(rt + 3),
+                    R8t0 = __ldg(rt + 4), t12 = __ldg(rt + 5);
+      const float* g = a.nd.g + 3 * (int64_t)nid[s];
+      wn[s] *= iW;
+      const double d0 = v[0] - g[0], d1 = v[1] - g[1], d2 = v[2] - g[2];
+      const double a0 = R01.x * d0 + R01.y * d1 + R23.x * d2;
+      const double a1 = R23.y * d0 + R45.x * d1 + R45.y * d2;
+      const double a2 = R67.x * d0 + R67.y * d1 + R8t0.x * d2;
+      af[s][0] = (float)a0; af[s][1] = (float)a1; af[s][2] = (float)a2;
+      xh[0] += wn[s] * (a0 + (double)g[0] + R8t0.y);
+      xh[1] += wn[s] * (a1 + (double)g[1] + t12.x);
+      xh[2] += wn[s] * (a2 + (double)g[2] + t12.y);
+      mh[0] += wn[s] * (R01.x * n[0] + R01.y * n[1] + R23.x * n[2]);
+      mh[1] += wn[s] * (R23.y * n[0] + R45.x * n[1] + R45.y * n[2]);
+      mh[2] += wn[s] * (R67.x * n[0] + R67.y * n[1] + R8t0.x * n[2]);
+    }
+    const double* Rd = fr.Rd;
+    double nt[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      vt[r] = Rd[3 * r] * xh[0] + Rd[3 * r + 1] * xh[1] + Rd[3 * r + 2] * xh[2] + fr.Td[r];
+      nt[r] = Rd[3 * r] * mh[0] + Rd[3 * r + 1] * mh[1] + Rd[3 * r + 2] * mh[2];
+    }
+    const double ml2 = mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2];
+    if (ml2 >= 1e-24 && vt[2] > 0) {
+      why = 1;
+      const double iz = 1.0 / vt[2];
+      const double fu = floor(fr.fxd * vt[0] * iz + fr.cxd + 0.5), fv = floor(fr.fyd * vt[1] * iz + fr.cyd + 0.5);
+      if (fu >= 0 && fv >= 0 && fu < fr.W && fv < fr.H) {
+        why |= 2;
+        const int px = (int)fu, py = (int)fv;
+        const double4 nm = fr.nmapd[py * fr.W + px];   // (N, D) in fp64 (K1)
+        if (nm.w > 0) {
+          why |= 4;
+          if (nm.x != 0 || nm.y != 0 || nm.z != 0) {
+            why |= 8;
+            N[0] = nm.x; N[1] = nm.y; N[2] = nm.z;
+            q[0] = (px - fr.cxd) * nm.w * fr.ifxd;
+            q[1] = (py - fr.cyd) * nm.w * fr.ifyd;
+            q[2] = nm.w;
+            const double e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
+            if (e0 * e0 + e1 * e1 + e2 * e2 < a.eps_dd * a.eps_dd) {   // |v~ - q| < eps_d
+              why |= 16;
+              const double dot = nt[0] * N[0] + nt[1] * N[1] + nt[2] * N[2];   // n~.N = dot / |m|
+              const double ce = a.cos_eps_nd;
+              const bool pass = ce >= 0 ? (dot > 0 && dot * dot > ce * ce * ml2) : (dot > 0 || dot * dot < ce * ce * ml2);
+              if (pass) { why |= 32; pix = py * fr.W + px; }
             }
           }
         }
       }
-      if (guard) {
-        atomicAdd(a.guard_counter, 1.0);
-        Fp64Args fa;
-        fa.px = md.px; fa.py = md.py; fa.pz = md.pz; fa.nx = md.nx; fa.ny = md.ny; fa.nz = md.nz; fa.kw = md.kw;
-        fa.cap = md.cap;
-        fa.Rt64 = a.nd.Rt64;
-        fa.g = a.nd.g;
-        fa.depth = fr.depth;
-        fa.W = fr.W; fa.H = fr.H;
-        fa.fxd = fr.fxd; fa.fyd = fr.fyd; fa.cxd = fr.cxd; fa.cyd = fr.cyd;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) fa.Rd[k] = fr.Rd[k];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) fa.Td[k] = fr.Td[k];
-        fa.eps_dd = a.eps_dd;
-        fa.cos_eps_nd = a.cos_eps_nd;
-        assoc_fp64<K>(&fa, i, nodes, vt, q, N, &pix, &why);
-      }
-      assoc = (pix >= 0);
-      if (assoc) {
-        const float e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
-        const float rpl = N[0] * e0 + N[1] * e1 + N[2] * e2;                 // Eq. 8
-        const float np0 = R[0] * N[0] + R[3] * N[1] + R[6] * N[2];         // n' = R^T N
-        const float np1 = R[1] * N[0] + R[4] * N[1] + R[7] * N[2];
-        const float np2 = R[2] * N[0] + R[5] * N[1] + R[8] * N[2];
-        const float rp0 = R[0] * e0 + R[3] * e1 + R[6] * e2;               // r' = R^T (v~ - q)
-        const float rp1 = R[1] * e0 + R[4] * e1 + R[7] * e2;
-        const float rp2 = R[2] * e0 + R[5] * e1 + R[8] * e2;
-        // the factor row, straight to shared memory (8-byte / 16-byte stores)
-#pragma unroll
-        for (int s = 0; s < K; ++s) {
-          float2* c2 = reinterpret_cast<float2*>(row + 6 * s);
-          c2[0] = make_float2(wn[s] * (ay[s] * np2 - az[s] * np1), wn[s] * (az[s] * np0 - ax[s] * np2));  // w_j (a_j x n')
-          c2[1] = make_float2(wn[s] * (ax[s] * np1 - ay[s] * np0), wn[s] * np0);
-          c2[2] = make_float2(wn[s] * np1, wn[s] * np2);
-          *reinterpret_cast<float4*>(row + L::CDP + 4 * s) = make_float4(wn[s] * ax[s], wn[s] * ay[s], wn[s] * az[s], wn[s]);
-        }
-        row[6 * K] = rpl;
-#pragma unroll
-        for (int c = 6 * K + 1; c < L::CDP; ++c) row[c] = 0.f;
-        row[L::CDP + 4 * K + 0] = rp0;
-        row[L::CDP + 4 * K + 1] = rp1;
-        row[L::CDP + 4 * K + 2] = rp2;
-#pragma unroll
-        for (int c = L::CDP + 4 * K + 3; c < L::FS; ++c) row[c] = 0.f;
-      }
     }
-    if (DBG) { a.dbg_pix[i] = pix; a.dbg_why[i] = why; }
   }
-  if (!assoc) {
-    float4* r4 = reinterpret_cast<float4*>(row);
+  if (DBG) { a.dbg_pix[i] = pix; a.dbg_why[i] = why; }
+  if (pix >= 0) {
+    as = 1;
+    const double* Rd = fr.Rd;
+    const double e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
+    const double rpl = N[0] * e0 + N[1] * e1 + N[2] * e2;                        // Eq. 8
+    const float np0 = (float)(Rd[0] * N[0] + Rd[3] * N[1] + Rd[6] * N[2]);      // n' = R^T N
+    const float np1 = (float)(Rd[1] * N[0] + Rd[4] * N[1] + Rd[7] * N[2]);
+    const float np2 = (float)(Rd[2] * N[0] + Rd[5] * N[1] + Rd[8] * N[2]);
+    const double rp0 = Rd[0] * e0 + Rd[3] * e1 + Rd[6] * e2;                     // r' = R^T (v~ - q)
+    const double rp1 = Rd[1] * e0 + Rd[4] * e1 + Rd[7] * e2;
+    const double rp2 = Rd[2] * e0 + Rd[5] * e1 + Rd[8] * e2;
 #pragma unroll
-    for (int c = 0; c < L::FS / 4; ++c) r4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < K; ++s) {
+      const float w = (float)wn[s];
+      st.wa[s] = make_float4(w * af[s][0], w * af[s][1], w * af[s][2], w);
+    }
+    st.rr = make_float4((float)rp0, (float)rp1, (float)rp2, (float)rpl);
+    st.nn = make_float4(np0, np1, np2, 0.f);
+    ed += rpl * rpl;
+    ep += rp0 * rp0 + rp1 * rp1 + rp2 * rp2;
+  } else {
+#pragma unroll
+    for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+    st.rr = st.nn = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  return assoc;
+}
+
+// energies and association count: warp sums, one striped fp64 atomic each per warp
+__device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, double ed, double ep, int as) {
+  double ca = as;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ed += __shfl_xor_sync(0xffffffffu, ed, o);
+    ep += __shfl_xor_sync(0xffffffffu, ep, o);
+    ca += __shfl_xor_sync(0xffffffffu, ca, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    energy_add(a.acc.energy, 0, ed);
+    energy_add(a.acc.energy, 1, ep);
+    energy_add(a.acc.energy, 4, ca);
+  }
 }
 
 template <int K, bool DBG>
-__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(AsmPointsArgs a) {
+__global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double ed = 0.0, ep = 0.0;
+  int as = 0;
+  if (i < a.md.n) {
+    PState<K> st;
+    assoc_point<K, DBG>(a, i, st, ed, ep, as);
+    float4* ps = a.pstate;
+    const int64_t S = a.pstride;
+#pragma unroll
+    for (int s = 0; s < K; ++s) ps[s * S + i] = st.wa[s];
+    ps[K * S + i] = st.rr;
+    ps[(K + 1) * S + i] = st.nn;
+  }
+  commit_point_energies(a, ed, ep, as);
+}
+
+// factor row of one point from its compact state (K3b: shared memory, FSP floats)
+template <int K>
+__device__ __forceinline__ void build_row(const PState<K>& st, float* row) {
+  using L = Lay<K>;
+  const float4 nn = st.nn;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const float4 wa = st.wa[s];   // (w a, w)
+    float2* c2 = reinterpret_cast<float2*>(row + 6 * s);
+    c2[0] = make_float2(wa.y * nn.z - wa.z * nn.y, wa.z * nn.x - wa.x * nn.z);   // w_j (a_j x n')
+    c2[1] = make_float2(wa.x * nn.y - wa.y * nn.x, wa.w * nn.x);                 // w_j n'
+    c2[2] = make_float2(wa.w * nn.y, wa.w * nn.z);
+    *reinterpret_cast<float4*>(row + L::CDP + 4 * s) = wa;
+  }
+  row[6 * K] = st.rr.w;
+#pragma unroll
+  for (int q = 6 * K + 1; q < L::CDP; ++q) row[q] = 0.f;
+  row[L::CDP + 4 * K + 0] = st.rr.x;
+  row[L::CDP + 4 * K + 1] = st.rr.y;
+  row[L::CDP + 4 * K + 2] = st.rr.z;
+#pragma unroll
+  for (int q = L::CDP + 4 * K + 3; q < L::FS; ++q) row[q] = 0.f;
+}
+
+// ---------------------------------------------------------------- K3b
+// One warp per chunk (<= kChunk consecutive points of one tuple segment, dynamic
+// scheduling): each lane rebuilds its point's factor row from the K3a state
+//   c' = [w_1 u_1, ..., w_K u_K, r_pl]      u_j = [a_j x n', n'] (Eq. 8 Jacobian row / w_j)
+//   e' = [w_1 a_1, w_1, ..., w_K a_K, w_K, r']   (point-to-point moments)
+// in shared memory; lanes own 4x4 tiles of the upper triangles of sum c'c'^T and
+// sum e'e'^T and accumulate them in registers (16 FFMA per 2 LDS.128); the
+// chunk's sums are committed with float4 / float2 atomic adds into its BSR slots.
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPointsArgs a) {
   using L = Lay<K>;
   constexpr int P = L::P;
   constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
   extern __shared__ float4 smem4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* F = reinterpret_cast<float*>(smem4) + warp * (32 * L::FSP + 16 * K);
-  float* ND = F + 32 * L::FSP;
+  float* F = reinterpret_cast<float*>(smem4) + warp * (32 * L::FSP);
+  __shared__ int32_t slot_sm[kWarps][P];   // the chunk's BSR slots (loaded with the header)
+  int32_t* slots = slot_sm[warp];
 
   // tile table of the two upper triangles: (I, J) in units of 4 entries
   __shared__ uint8_t tabI[L::NT], tabJ[L::NT];
@@ -344,11 +286,9 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
     if (t < L::TD) {             // c' = [w_j u_j ..., r_pl]
       if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
       else if (B == 6 * K && A < 6 * K) d = 52 * P + 18 * (A / 6) + (A % 6);
-      else if (B == 6 * K && A == 6 * K) d = 52 * P + 18 * K;
     } else {                     // e' = [w_j a_j, w_j ..., r']
       if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
       else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 18 * (A / 4) + 6 + 3 * (A % 4) + (B - 4 * K);
-      else if (B < 4 * K + 3 && A == B) d = 52 * P + 18 * K + 1 + (A - 4 * K);
     }
     if (d >= 0) perm[d] = (int16_t)q;
   }
@@ -367,31 +307,34 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
     p0[r] = (it / L::NT) * L::PS;
   }
 
-  double e_data = 0.0, e_pt = 0.0;   // per-lane energy partials (fp64 across chunks)
-  unsigned long long n_tot = 0;      // associations of this warp's chunks
   // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
   int64_t c = 0;
   if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
   c = __shfl_sync(0xffffffffu, c, 0);
+  const float4* ps = a.pstate;
+  const int64_t S = a.pstride;
   for (; c < a.nchunk;) {
     const int4 ch = a.chunks[c];
     const int seg = ch.x;
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
     __syncwarp();
-    for (int t = lane; t < 16 * K; t += 32) ND[t] = a.nd.node32[16 * nodes[t >> 4] + (t & 15)];
-    __syncwarp();
+    for (int q = lane; q < P; q += 32) slots[q] = a.seg_slot[(int64_t)seg * P + q];
     float acc[L::RI][16];
 #pragma unroll
     for (int r = 0; r < L::RI; ++r)
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[r][e] = 0.f;
-    unsigned n_assoc = 0;
     for (int base = ch.y; base < ch.z; base += 32) {
       const int64_t i = base + lane;
-      PointIn<K> cur;
-      load_point<K>(a.md, i, i < ch.z, cur);
-      const bool as = point_row<K, DBG>(a, i, i < ch.z, cur, ND, nodes, F + lane * L::FSP);
-      n_assoc += __popc(__ballot_sync(0xffffffffu, as));
+      float* row = F + lane * L::FSP;
+      if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point)
+        PState<K> st;
+#pragma unroll
+        for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+        st.rr = ps[K * S + i];
+        st.nn = ps[(K + 1) * S + i];
+        build_row<K>(st, row);
+      }
       __syncwarp();
       const int np = min(32, ch.z - base);
 #pragma unroll
@@ -424,10 +367,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
     __syncwarp();
     int64_t next_chunk = 0;
     if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
-    // vector atomic adds (sm_90+ float4 / float2 RED) into the accumulators: per pair
-    // 9 x 4 data + 4 x 4 moments of its BSR slot, per node slot 3 x 2 rhs + 3 x 4
-    // moments; all-zero vectors (no association) are skipped.  Energies stay in registers.
-    const int32_t* slots = a.seg_slot + (int64_t)seg * P;
+    // vector atomic adds (sm_90+ float4 / float2 RED): per pair 9 x 4 data + 4 x 4 moments of
+    // its BSR slot, per node slot 3 x 2 rhs + 3 x 4 moments; all-zero vectors are skipped
     auto rv = [&](int d) -> float {
       const int q = perm[d];
       if (q < 0) return 0.f;
@@ -459,27 +400,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_assemble_points(As
         }
       }
     }
-    if (lane == 0) {
-      const int de = 52 * P + 18 * K;
-      e_data += rv(de);
-      e_pt += (double)rv(de + 1) + rv(de + 2) + rv(de + 3);
-    }
-    n_tot += n_assoc;
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
-  }
-  // energies and association count: warp, then block, then one fp64 atomic per block
-  __shared__ double red_e[3][kWarps];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    e_data += __shfl_xor_sync(0xffffffffu, e_data, o);
-    e_pt += __shfl_xor_sync(0xffffffffu, e_pt, o);
-  }
-  if (lane == 0) { red_e[0][warp] = e_data; red_e[1][warp] = e_pt; red_e[2][warp] = (double)n_tot; }
-  __syncthreads();
-  if (threadIdx.x < 3) {
-    double t = 0.0;
-    for (int w = 0; w < kWarps; ++w) t += red_e[threadIdx.x][w];
-    if (t != 0.0) atomicAdd(a.acc.energy + (threadIdx.x == 2 ? 4 : threadIdx.x), t);
   }
 }
 
@@ -558,16 +479,28 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   }
   const int64_t n = gw - r.m - r.nnzb;
   if (n == r.m) {   // energies -> report slot; zeroed (with K3's work counter) for the next assembly
+    double* E = r.acc.energy;
+    double tot[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {   // striped partials: lane l sums stripes l, l + 32
+      double* st_q = E + 8 + kEnergyStripes * q;
+      double v = st_q[lane] + st_q[lane + 32];
+      st_q[lane] = 0.0;
+      st_q[lane + 32] = 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      tot[q] = E[q] + v;
+    }
     if (lane == 0) {
-      double* E = r.acc.energy;
       if (r.slot >= 0) {
         double* rep = r.rep_energy + 5 * r.slot;
-        rep[0] = E[0]; rep[1] = E[1]; rep[2] = E[2]; rep[3] = E[3];
-        rep[4] = (double)r.w_data * E[0] + (double)r.w_pt * E[1] + (double)r.w_reg * E[2] + (double)r.w_corr * E[3];
-        r.rep_nassoc[r.slot] = E[4];
-        r.rep_nassoc[MIS_MAX_GN + 1 + r.slot] = E[5];   // fp64 guard-band re-evaluations
+        rep[0] = tot[0]; rep[1] = tot[1]; rep[2] = tot[2]; rep[3] = tot[3];
+        rep[4] = (double)r.w_data * tot[0] + (double)r.w_pt * tot[1] + (double)r.w_reg * tot[2] +
+                 (double)r.w_corr * tot[3];
+        r.rep_nassoc[r.slot] = tot[4];
+        r.rep_nassoc[MIS_MAX_GN + 1 + r.slot] = 0.0;   // (no fp32 guard band: the association runs in fp64)
       }
-      for (int q = 0; q < 7; ++q) E[q] = 0.0;
+      for (int q = 0; q < 8; ++q) E[q] = 0.0;
     }
     return;
   }
@@ -600,13 +533,20 @@ void launch_finalize(const FinalArgs& r, cudaStream_t s) {
 template <int K>
 static void launch_points_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
   using L = Lay<K>;
-  const size_t smem = sizeof(float) * kWarps * (32 * L::FSP + 16 * K);
   const bool dbg = a.dbg_pix != nullptr;
-  auto kern = dbg ? k_assemble_points<K, true> : k_assemble_points<K, false>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[dbg]) {
+  const int64_t n = a.md.n;
+  if (n > 0) {
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dbg) k_assoc_points<K, true><<<g, 256, 0, s>>>(a);
+    else k_assoc_points<K, false><<<g, 256, 0, s>>>(a);
+  }
+  if (a.nchunk <= 0) return;
+  const size_t smem = sizeof(float) * kWarps * 32 * L::FSP;
+  auto kern = k_accum_points<K>;
+  static bool attr_set = false;
+  if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set[dbg] = true;
+    attr_set = true;
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
@@ -619,16 +559,10 @@ static void launch_points_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s)
 }
 
 void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
-  if (a.nchunk <= 0) return;
   switch (K) {
-    case 1: launch_points_k<1>(a, num_sms, s); break;
-    case 2: launch_points_k<2>(a, num_sms, s); break;
-    case 3: launch_points_k<3>(a, num_sms, s); break;
-    case 4: launch_points_k<4>(a, num_sms, s); break;
-    case 5: launch_points_k<5>(a, num_sms, s); break;
-    case 6: launch_points_k<6>(a, num_sms, s); break;
-    case 7: launch_points_k<7>(a, num_sms, s); break;
-    case 8: launch_points_k<8>(a, num_sms, s); break;
+#define LP(KK) case KK: launch_points_k<KK>(a, num_sms, s); break;
+    LP(1) LP(2) LP(3) LP(4) LP(5) LP(6) LP(7) LP(8)
+#undef LP
     default: break;
   }
 }
@@ -761,8 +695,8 @@ __global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
     eC += __shfl_xor_sync(0xffffffffu, eC, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    if (eR != 0.f) atomicAdd(a.acc.energy + 2, (double)eR);
-    if (eC != 0.f) atomicAdd(a.acc.energy + 3, (double)eC);
+    energy_add(a.acc.energy, 2, (double)eR);
+    energy_add(a.acc.energy, 3, (double)eC);
   }
 }
 

@@ -15,10 +15,12 @@ struct FrameView {
   int W, H;
   float fx, fy, cx, cy;
   double fxd, fyd, cxd, cyd;
+  double ifxd, ifyd;     // 1 / fx, 1 / fy
   const float* depth;    // H*W
   const float4* nmap;    // H*W: (nx, ny, nz, D); n = 0 invalid normal, D = 0 invalid depth
+  const double4* nmapd;  // H*W: the same in fp64 (the association's precision)
   float R[9], T[3];      // world -> camera (fp32 copy)
-  double Rd[9], Td[3];   // fp64 copy (guard-band recompute)
+  double Rd[9], Td[3];   // fp64 copy (the association and fusion decisions)
 };
 
 struct ModelView {
@@ -53,13 +55,22 @@ struct AccView {
   float* rhs_data;
   float* node_mom;
   float* rhs_graph;
-  double* energy;              // [0..3] energies, [4] n_assoc (as double)
+  double* energy;              // [0..3] energies, [4] n_assoc, [6] K3b work counter (u64);
+                               // [8 + 64 q + s]: striped partials of quantity q (0 E_data, 1 E_pt, 2 E_reg,
+                               // 3 E_corr, 4 n_assoc), summed by the finalisation
 };
+constexpr int kEnergyStripes = 64;
+constexpr int kEnergyDoubles = 8 + 5 * kEnergyStripes;
+// one fp64 atomic per warp into a stripe picked by the warp index: no same-address serialisation
+__device__ __forceinline__ void energy_add(double* energy, int q, double v) {
+  const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (v != 0.0) atomicAdd(energy + 8 + kEnergyStripes * q + (w % kEnergyStripes), v);
+}
 
 // ------------------------------------------------------------- host-side launchers
 struct Ctx;   // defined in api.cu
 
-void launch_frame_prep(const FrameView& f, float4* nmap, cudaStream_t s);
+void launch_frame_prep(const FrameView& f, float4* nmap, double4* nmapd, cudaStream_t s);
 void launch_skin(int64_t nq, const float* px, const float* py, const float* pz, int64_t stride_xyz,
                  const float* g, int m, int K, int32_t* idx, float* w, int64_t out_stride, cudaStream_t s);
 
@@ -74,11 +85,13 @@ struct AsmPointsArgs {
   float eps_d, cos_eps_n;
   double eps_dd, cos_eps_nd;
   AccView acc;                // K3 commits atomically into the BSR accumulators
+  float4* pstate;             // K3a -> K3b per-point factor state: (K + 2) planes of pstride float4
+  int64_t pstride;
   unsigned long long* work_counter;   // zeroed before the launch (dynamic chunk scheduling)
-  double* guard_counter;              // fp64 guard-band re-evaluations (energy slot 5)
   int32_t* dbg_pix;           // nullable: per point association outputs
   uint8_t* dbg_why;
 };
+// K3a (per point) then K3b (per chunk) on s
 void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
 
 // Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator

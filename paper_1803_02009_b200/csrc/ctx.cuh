@@ -65,6 +65,8 @@ struct Ctx {
   int last_solver = 0;   // cluster size of the last PCG launch (0: grid kernel)
   DBuf part, tstamp;
   size_t acc_floats = 0;
+  DBuf pstate;   // K3a -> K3b per-point factor state
+  bool acc_dirty = true;   // accumulators may be nonzero (set while an assembly is in flight)
   DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots;
 
   // ---- frame
@@ -72,7 +74,7 @@ struct Ctx {
   int W = 0, H = 0;
   mis_intrinsics intr{};
   float pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
-  DBuf depth, nmap, rgb_obs, stage;
+  DBuf depth, nmap, nmapd, rgb_obs, stage;
 
   // ---- features
   int nf = 0;

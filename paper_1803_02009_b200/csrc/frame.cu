@@ -5,51 +5,53 @@ namespace mis {
 
 __device__ __forceinline__ bool depth_ok(float d) { return isfinite(d) && d > 0.0f; }
 
-// K1: per pixel (nx, ny, nz, D).  Back-projection Pi and the
-// central-difference normal (reading A11):
+// K1: per pixel the back-projection Pi and the central-difference
+// normal (reading A11), in fp64 -- the precision the association decisions are
+// taken in (K3a) --:
 //   N = normalize((q(x+1,y) - q(x-1,y)) x (q(x,y+1) - q(x,y-1))), flipped so N.q < 0;
-// invalid on the border or next to an invalid depth.  HBM-bound: 4 B read
-// (+ neighbours from L1/L2), 16 B written per pixel.
-__global__ void __launch_bounds__(256) k_frame_prep(FrameView f, float4* __restrict__ nmap) {
+// invalid (N = 0) on the border or next to an invalid depth.  Writes nmapd
+// (N in fp64, D) and nmap (N rounded to fp32, D; D = 0 for an invalid depth).
+// HBM-bound: 4 B read (+ neighbours from L1/L2), 48 B written per pixel.
+__global__ void __launch_bounds__(256) k_frame_prep(FrameView f, float4* __restrict__ nmap, double4* __restrict__ nmapd) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= f.W || y >= f.H) return;
   const int W = f.W;
   const float* D = f.depth;
   const float c = __ldg(D + y * W + x);
-  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (depth_ok(c)) {
-    out.w = c;
-    if (x > 0 && y > 0 && x < W - 1 && y < f.H - 1) {
-      const float l = __ldg(D + y * W + x - 1), r = __ldg(D + y * W + x + 1);
-      const float u = __ldg(D + (y - 1) * W + x), d = __ldg(D + (y + 1) * W + x);
-      if (depth_ok(l) && depth_ok(r) && depth_ok(u) && depth_ok(d)) {
-        const float ifx = 1.0f / f.fx, ify = 1.0f / f.fy;
-        // q(x+1,y) - q(x-1,y), q(x,y+1) - q(x,y-1)
-        const float ax = ((x + 1) - f.cx) * r * ifx - ((x - 1) - f.cx) * l * ifx;
-        const float ay = (y - f.cy) * (r - l) * ify;
-        const float az = r - l;
-        const float bx = (x - f.cx) * (d - u) * ifx;
-        const float by = ((y + 1) - f.cy) * d * ify - ((y - 1) - f.cy) * u * ify;
-        const float bz = d - u;
-        float nx = ay * bz - az * by, ny = az * bx - ax * bz, nz = ax * by - ay * bx;
-        const float len = sqrtf(nx * nx + ny * ny + nz * nz);
-        if (len > 1e-12f) {
-          const float s = 1.0f / len;
-          nx *= s; ny *= s; nz *= s;
-          const float qx = (x - f.cx) * c * ifx, qy = (y - f.cy) * c * ify;
-          if (nx * qx + ny * qy + nz * c > 0.f) { nx = -nx; ny = -ny; nz = -nz; }
-          out.x = nx; out.y = ny; out.z = nz;
-        }
+  double N[3] = {0.0, 0.0, 0.0};
+  bool dv = depth_ok(c), nv = false;
+  if (dv && x > 0 && y > 0 && x < W - 1 && y < f.H - 1) {
+    const float l = __ldg(D + y * W + x - 1), r = __ldg(D + y * W + x + 1);
+    const float u = __ldg(D + (y - 1) * W + x), d = __ldg(D + (y + 1) * W + x);
+    if (depth_ok(l) && depth_ok(r) && depth_ok(u) && depth_ok(d)) {
+      const double ax = ((x + 1) - f.cxd) * r / f.fxd - ((x - 1) - f.cxd) * l / f.fxd;
+      const double ay = (y - f.cyd) * (double)r / f.fyd - (y - f.cyd) * (double)l / f.fyd;
+      const double az = (double)r - (double)l;
+      const double bx = (x - f.cxd) * (double)d / f.fxd - (x - f.cxd) * (double)u / f.fxd;
+      const double by = ((y + 1) - f.cyd) * d / f.fyd - ((y - 1) - f.cyd) * u / f.fyd;
+      const double bz = (double)d - (double)u;
+      N[0] = ay * bz - az * by; N[1] = az * bx - ax * bz; N[2] = ax * by - ay * bx;
+      const double len = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
+      if (len >= 1e-12) {
+        nv = true;
+        for (int k = 0; k < 3; ++k) N[k] /= len;
+        const double q[3] = {(x - f.cxd) * c / f.fxd, (y - f.cyd) * c / f.fyd, (double)c};
+        if (N[0] * q[0] + N[1] * q[1] + N[2] * q[2] > 0) for (int k = 0; k < 3; ++k) N[k] = -N[k];
+      } else {
+        N[0] = N[1] = N[2] = 0.0;
       }
     }
   }
-  nmap[y * W + x] = out;
+  const int p = y * W + x;
+  nmap[p] = make_float4((float)N[0], (float)N[1], (float)N[2], dv ? c : 0.f);
+  nmapd[p] = make_double4(N[0], N[1], N[2], dv ? (double)c : 0.0);
+  (void)nv;
 }
 
-void launch_frame_prep(const FrameView& f, float4* nmap, cudaStream_t s) {
+void launch_frame_prep(const FrameView& f, float4* nmap, double4* nmapd, cudaStream_t s) {
   dim3 blk(32, 8), grd((f.W + 31) / 32, (f.H + 7) / 8);
-  k_frame_prep<<<grd, blk, 0, s>>>(f, nmap);
+  k_frame_prep<<<grd, blk, 0, s>>>(f, nmap, nmapd);
 }
 
 // K2: Eq. 2 -- the k+1 nearest nodes of each query (ties to the

@@ -403,11 +403,16 @@ cudaError_t build_pattern(Ctx* c) {
   // accumulators (K3 commits atomically into them) and solver buffers
   const size_t m6 = 6 * (size_t)m;
   c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)m + m6;
+  // accumulators: every finalisation re-zeroes what it read, so they need a memset only when
+  // (re)allocated or after an assembly that did not reach its finalisation
+  if (c->acc.bytes < c->acc_floats * 4 || c->energy.bytes < (size_t)kEnergyDoubles * 8) c->acc_dirty = true;
   CK(ensure(c, c->acc, c->acc_floats * 4));
-  CK(ensure(c, c->energy, 8 * 8));
-  // zeroed once per pattern; afterwards every finalisation re-zeroes what it read
-  CK(cudaMemsetAsync(c->acc.p, 0, c->acc_floats * 4, c->st));
-  CK(cudaMemsetAsync(c->energy.p, 0, 8 * 8, c->st));
+  CK(ensure(c, c->energy, kEnergyDoubles * 8));
+  if (c->acc_dirty) {
+    CK(cudaMemsetAsync(c->acc.p, 0, c->acc.bytes, c->st));
+    CK(cudaMemsetAsync(c->energy.p, 0, kEnergyDoubles * 8, c->st));
+    c->acc_dirty = false;
+  }
   CK(ensure(c, c->Hval, (size_t)nnz * 36 * 4));
   CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)m * 36 * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
