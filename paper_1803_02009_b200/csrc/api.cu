@@ -397,7 +397,8 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->seg_slot, &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->part, &c->tstamp, &c->acc, &c->energy,
                  &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
-                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->cub_tmp};
+                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->pcg_pptr, &c->pcg_pc, &c->pcg_push,
+                 &c->pcg_npush, &c->pcg_mask, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -725,6 +726,10 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) ? 0 : 1;
   s.minv_ready = 1;   // built by the finalisation (after the all-reduce when sharded)
   s.tstamp = c->tstamp.as<unsigned long long>();
+  s.pptr = c->pcg_pptr.as<int32_t>();
+  s.pc = c->pcg_pc.as<int32_t>();
+  s.push = c->pcg_push.as<int32_t>();
+  s.npush = c->pcg_npush.as<int32_t>();
   return s;
 }
 

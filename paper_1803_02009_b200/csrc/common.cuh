@@ -164,6 +164,7 @@ struct SolveArgs {
   int pipelined;              // cluster variant: pipelined PCG (1 barrier / iteration) instead of standard
   int minv_ready;             // Minv already built by the record reduction (single GPU)
   unsigned long long* tstamp; // 8 %globaltimer stamps of the phases (rank 0, thread 0)
+  const int32_t *pptr, *pc, *push, *npush;   // cluster variant: per-rank SpMV pieces and halo lists (per frame)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -173,6 +174,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
+// per frame, after the pattern: the cluster ranks' SpMV pieces and halo push lists
+void launch_pcg_prep(const int32_t* row_ptr, const int32_t* col, const int32_t* part, int cs, int max_rows, int max_nnz,
+                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s);
+int pcg_max_pieces(int max_rows, int max_nnz);
 // cluster partition (row boundaries balancing nnz) computed on the device; cl_size 0 = does not fit
 struct PlanOut { int32_t cl_size, max_rows, max_nnz, pad; int64_t smem; };
 void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,

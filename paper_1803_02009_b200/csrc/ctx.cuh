@@ -64,6 +64,7 @@ struct Ctx {
   std::string solver_note;
   int last_solver = 0;   // cluster size of the last PCG launch (0: grid kernel)
   DBuf part, tstamp;
+  DBuf pcg_pptr, pcg_pc, pcg_push, pcg_npush, pcg_mask;   // cluster PCG lists (per frame)
   size_t acc_floats = 0;
   DBuf pstate;   // K3a -> K3b per-point factor state
   bool acc_dirty = true;   // accumulators may be nonzero (set while an assembly is in flight)

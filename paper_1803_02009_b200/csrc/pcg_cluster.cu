@@ -35,7 +35,7 @@ constexpr int kPiece = 4;         // SpMV work unit: <= kPiece consecutive block
 __host__ __device__ inline int max_pieces(int max_rows, int max_nnz) { return max_nnz / kPiece + max_rows + 1; }
 
 struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
-  size_t dots, vec, zf, mi, col, own, pptr, pc, part, mask, push, h, total;
+  size_t dots, vec, zf, mi, col, own, pptr, pc, part, push, h, total;
   __host__ __device__ CLay(int max_rows, int max_nnz, int m) {
     dots = 0;                                        // double partA..partE[16], red[64]
     vec = dots + sizeof(double) * (5 * kMaxCluster + 64);
@@ -47,20 +47,44 @@ struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
     pptr = own + sizeof(int) * (max_rows + 1);       // first SpMV piece of each local row (nr + 1)
     pc = pptr + sizeof(int) * (max_rows + 1);        // pieces: first block | count << 24
     part = pc + sizeof(int) * max_pieces(max_rows, max_nnz);   // 6 partial sums per piece
-    mask = part + sizeof(float) * 6 * max_pieces(max_rows, max_nnz);   // per own row: CTAs that read it
-    push = mask + sizeof(unsigned) * max_rows;       // (destination CTA << 16 | local row), by destination
+    push = part + sizeof(float) * 6 * max_pieces(max_rows, max_nnz);   // (destination CTA << 16 | local row)
     h = (push + sizeof(int) * (size_t)max_rows * kMaxCluster + 15) & ~(size_t)15;
     total = h + sizeof(float) * 36 * (size_t)max_nnz;
   }
 };
 
-// Split the local rows into pieces of <= kPiece blocks (row order, then block
-// order) so the SpMV's work units are balanced whatever the row lengths.
-__device__ __forceinline__ void build_pieces(const int* lrp, int nr, int* pptr, int* pc) {
-  if (threadIdx.x < 32) {   // one warp: lane-chunked exclusive scan of the per-row piece counts
-    const int l = threadIdx.x, per = (nr + 31) / 32, i0 = l * per, i1 = min(nr, i0 + per);
+// ---- per-frame preparation (the pattern and the partition are fixed for the
+// frame's G Gauss-Newton iterations): SpMV pieces and halo push lists of every
+// cluster rank, in global memory; each PCG launch only copies its rank's lists.
+// Global layout (rank r): pptr [r * (max_rows + 1)], pieces [r * max_pieces],
+// push [r * max_rows * 16], npush [r].
+struct PcgLists {
+  int32_t *pptr, *pc, *push, *npush;
+  uint32_t* mask;   // m: ranks that read each row (zero outside the prep kernels)
+};
+
+// every rank marks the rows its blocks read in other ranks' ranges
+__global__ void k_pcg_mark(const int32_t* row_ptr, const int32_t* col, const int32_t* part, PcgLists L) {
+  const int rank = blockIdx.x, r0 = part[rank], r1 = part[rank + 1];
+  for (int k = row_ptr[r0] + threadIdx.x; k < row_ptr[r1]; k += blockDim.x) {
+    const int j = col[k];
+    if (j < r0 || j >= r1) atomicOr(L.mask + j, 1u << rank);
+  }
+}
+
+// per rank: the pieces (<= kPiece blocks of one row, row order then block order) so the
+// SpMV's work units are balanced whatever the row lengths; the push list ((destination,
+// row) pairs grouped by destination, itself included); the rows' marks are cleared
+__global__ void k_pcg_lists(const int32_t* row_ptr, const int32_t* part, int cs, int max_rows, int max_pc, PcgLists L) {
+  const int rank = blockIdx.x, r0 = part[rank], nr = part[rank + 1] - r0, l = threadIdx.x;
+  const int e0 = row_ptr[r0];
+  int32_t* pptr = L.pptr + (int64_t)rank * (max_rows + 1);
+  int32_t* pc = L.pc + (int64_t)rank * max_pc;
+  int32_t* push = L.push + (int64_t)rank * max_rows * kMaxCluster;
+  {   // one warp: lane-chunked exclusive scan of the per-row piece counts
+    const int per = (nr + 31) / 32, i0 = l * per, i1 = min(nr, i0 + per);
     int s = 0;
-    for (int i = i0; i < i1; ++i) s += (lrp[i + 1] - lrp[i] + kPiece - 1) / kPiece;
+    for (int i = i0; i < i1; ++i) s += (row_ptr[r0 + i + 1] - row_ptr[r0 + i] + kPiece - 1) / kPiece;
     int inc = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -70,10 +94,23 @@ __device__ __forceinline__ void build_pieces(const int* lrp, int nr, int* pptr, 
     int run = inc - s;
     for (int i = i0; i < i1; ++i) {
       pptr[i] = run;
-      for (int k = lrp[i]; k < lrp[i + 1]; k += kPiece) pc[run++] = k | (min(kPiece, lrp[i + 1] - k) << 24);
+      const int a = row_ptr[r0 + i] - e0, b = row_ptr[r0 + i + 1] - e0;
+      for (int k = a; k < b; k += kPiece) pc[run++] = k | (min(kPiece, b - k) << 24);
     }
     if (l == 31) pptr[nr] = inc;
   }
+  int n = 0;
+  for (int d = 0; d < cs; ++d)
+    for (int b = 0; b < nr; b += 32) {
+      const int i = b + l;
+      const bool on = i < nr && (d == rank || ((L.mask[r0 + i] >> d) & 1u));
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (on) push[n + __popc(bal & ((1u << l) - 1u))] = (d << 16) | i;
+      n += __popc(bal);
+    }
+  __syncwarp();
+  for (int i = l; i < nr; i += 32) L.mask[r0 + i] = 0u;
+  if (l == 0) L.npush[rank] = n;
 }
 
 // push the CTA's slice of a vector into the full-length copies of the CTAs
@@ -179,9 +216,13 @@ __device__ __forceinline__ void load_hreg(HReg& R, const int* pptr, const int* p
       cnt = w >> 24;
     }
 #pragma unroll
-    for (int b = 0; b < kPiece; ++b)
-#pragma unroll
-      for (int q = 0; q < 6; ++q) R.h[j][b][q] = b < cnt ? H[36 * (size_t)(k0 + b) + 6 * c + q] : 0.f;
+    for (int b = 0; b < kPiece; ++b) {   // 8-byte loads: a block row is 6 contiguous floats at 24-byte offsets
+      const float2* h2 = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + b) + 6 * c);
+      float2 v0 = make_float2(0.f, 0.f), v1 = v0, v2 = v0;
+      if (b < cnt) { v0 = h2[0]; v1 = h2[1]; v2 = h2[2]; }
+      R.h[j][b][0] = v0.x; R.h[j][b][1] = v0.y; R.h[j][b][2] = v1.x;
+      R.h[j][b][3] = v1.y; R.h[j][b][4] = v2.x; R.h[j][b][5] = v2.y;
+    }
   }
 }
 
@@ -379,7 +420,6 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   int* pptr = reinterpret_cast<int*>(sm + L.pptr);
   int* pc = reinterpret_cast<int*>(sm + L.pc);
   float* part = reinterpret_cast<float*>(sm + L.part);
-  unsigned* hmask = reinterpret_cast<unsigned*>(sm + L.mask);
   int* push = reinterpret_cast<int*>(sm + L.push);
   float* H = reinterpret_cast<float*>(sm + L.h);
 
@@ -392,72 +432,41 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[0] = gtimer();
 
   // ---- phase 0: local rows of H (from the accumulators), b, column owners
-  for (int i = t; i <= nr; i += kCT) lrp[i] = a.row_ptr[r0 + i] - e0;
-  __syncthreads();
-  build_pieces(lrp, nr, pptr, pc);   // warp 0, while the others stream H (covered by the next barrier)
-  {   // stream this CTA's rows of the final H (built by the record reduction) into shared memory
-    const float4* src = reinterpret_cast<const float4*>(a.Hval + 36 * (int64_t)e0);
-    float4* dst = reinterpret_cast<float4*>(H);
-    for (int q = t; q < 9 * ne; q += kCT) dst[q] = src[q];
-    for (int k = t; k < ne; k += kCT) col[k] = a.col[e0 + k];
-  }
+  // lists of this rank (built once per frame), columns, b, block inverses
+  const int max_pc = max_pieces(a.max_rows, a.max_nnz);
+  const int32_t* g_pptr = a.pptr + (int64_t)rank * (a.max_rows + 1);
+  for (int i = t; i <= nr; i += kCT) pptr[i] = g_pptr[i];
+  const int npush = a.npush[rank];
+  const int32_t* g_push = a.push + (int64_t)rank * a.max_rows * kMaxCluster;
+  for (int i = t; i < npush; i += kCT) push[i] = g_push[i];
+  for (int k = t; k < ne; k += kCT) col[k] = a.col[e0 + k];
   for (int i = t; i < 6 * nr; i += kCT) {
     r[i] = a.rhs[6 * (int64_t)r0 + i];
     x[i] = 0.f;
     p[i] = 0.f;
     Ap[i] = 0.f;
   }
-  __syncthreads();
-  if (stamp) ts[1] = gtimer();
-  if (a.pcg_iters <= 0 && !a.do_update) return;
-  const int npush = build_push(cl, hmask, push, col, ne, a.part, rank, cs, r0, nr);
-  HReg R;
-  load_hreg(R, pptr, pc, H, nr);
-
-  // ---- phase 1: block-Jacobi preconditioner, z = M r, r.z
-  // M_j = (H_jj + (lambda + mu_j) I)^-1: built by the record reduction on one GPU
-  // (minv_ready); otherwise here in fp64 by Gauss-Jordan, 6 lanes per node
-  // (one row each, pivot rows broadcast by shuffles), 5 nodes per warp.
-  if (a.minv_ready) {
+  {
     const float4* src = reinterpret_cast<const float4*>(a.Minv + 36 * (int64_t)r0);
     float4* dst = reinterpret_cast<float4*>(Mi);
     for (int q = t; q < 9 * nr; q += kCT) dst[q] = src[q];
-  } else {
-    const int wid = t >> 5, ln = t & 31, slot = ln / 6, rr = ln - 6 * slot;
-    for (int base = 0; base < nr; base += 5 * (kCT / 32)) {
-      const int i = base + 5 * wid + slot;
-      const bool act = slot < 5 && i < nr;
-      const float* Hd = H + 36 * (size_t)(act ? a.diag_pos[r0 + i] - e0 : 0);
-      double row[12];
-      double trc = 0.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) trc += act ? (double)Hd[7 * q] : 0.0;
-      const double mu = 1e-9 * trc / 6.0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        row[q] = act ? (double)Hd[6 * rr + q] + (q == rr ? (double)a.lambda + mu : 0.0) : (q == rr ? 1.0 : 0.0);
-        row[6 + q] = (q == rr) ? 1.0 : 0.0;
-      }
-      bool pd = true;
-      const int src0 = slot < 5 ? 6 * slot : 0;
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        const double pv = __shfl_sync(0xffffffffu, row[p], src0 + p);
-        if (!(pv > 0.0)) pd = false;
-        const double ipv = 1.0 / pv;
-        const double f = row[p] * ipv;
-#pragma unroll
-        for (int q = 0; q < 12; ++q) {
-          const double pq = __shfl_sync(0xffffffffu, row[q], src0 + p);
-          row[q] = (rr == p) ? pq * ipv : row[q] - f * pq;
-        }
-      }
-      if (act)
-#pragma unroll
-        for (int q = 0; q < 6; ++q) Mi[36 * i + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
-    }
   }
   __syncthreads();
+  const int npc = pptr[nr];
+  const int32_t* g_pc = a.pc + (int64_t)rank * max_pc;
+  for (int i = t; i < npc; i += kCT) pc[i] = g_pc[i];
+  const float* Hg = a.Hval + 36 * (int64_t)e0;
+  const bool h_in_smem = 6 * npc > kU * kCT;   // units beyond the registers read H from shared memory
+  if (h_in_smem) {
+    const float4* src = reinterpret_cast<const float4*>(Hg);
+    float4* dst = reinterpret_cast<float4*>(H);
+    for (int q = t; q < 9 * ne; q += kCT) dst[q] = src[q];
+  }
+  __syncthreads();
+  if (stamp) ts[1] = gtimer();
+  if (a.pcg_iters <= 0 && !a.do_update) return;
+  HReg R;
+  load_hreg(R, pptr, pc, Hg, nr);   // straight from global memory into registers
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
   if (a.pipelined) {
@@ -601,6 +610,14 @@ __global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, P
   out->smem = (int64_t)L.total;
   for (int c = 0; c <= cs; ++c) part[c] = b[c];
 }
+
+void launch_pcg_prep(const int32_t* row_ptr, const int32_t* col, const int32_t* part, int cs, int max_rows, int max_nnz,
+                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s) {
+  PcgLists L{pptr, pc, push, npush, mask};
+  k_pcg_mark<<<cs, 256, 0, s>>>(row_ptr, col, part, L);
+  k_pcg_lists<<<cs, 32, 0, s>>>(row_ptr, part, cs, max_rows, max_pieces(max_rows, max_nnz), L);
+}
+int pcg_max_pieces(int max_rows, int max_nnz) { return max_pieces(max_rows, max_nnz); }
 
 void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,
                          cudaStream_t s) {

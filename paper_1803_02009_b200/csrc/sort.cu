@@ -388,6 +388,21 @@ cudaError_t build_pattern(Ctx* c) {
     k_upper_lower<<<(int)std::min<int64_t>(grid, (nnz + 255) / 256), 256, 0, c->st>>>(
         c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(), m, c->upper_of.as<int32_t>(),
         c->lower_of.as<int32_t>());
+  if (c->cl_size > 0 && nnz > 0) {   // cluster PCG: per-rank SpMV pieces and halo lists for the frame
+    const int cs = c->cl_size, mr = c->cl_max_rows, mp = pcg_max_pieces(c->cl_max_rows, c->cl_max_nnz);
+    CK(ensure(c, c->pcg_pptr, (size_t)cs * (mr + 1) * 4));
+    CK(ensure(c, c->pcg_pc, (size_t)cs * mp * 4));
+    CK(ensure(c, c->pcg_push, (size_t)cs * mr * 16 * 4));
+    CK(ensure(c, c->pcg_npush, 16 * 4));
+    if (c->pcg_mask.bytes < (size_t)m * 4) {
+      CK(ensure(c, c->pcg_mask, (size_t)m * 4));
+      CK(cudaMemsetAsync(c->pcg_mask.p, 0, (size_t)m * 4, c->st));   // kept zero by k_pcg_lists
+    }
+    launch_pcg_prep(c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->part.as<int32_t>(), cs, mr, c->cl_max_nnz,
+                    c->pcg_pptr.as<int32_t>(), c->pcg_pc.as<int32_t>(), c->pcg_push.as<int32_t>(),
+                    c->pcg_npush.as<int32_t>(), c->pcg_mask.as<uint32_t>(), c->st);
+    count_launches(2);
+  }
   // slot tables (exact sizes now)
   const int64_t total = c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P;
   CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
