@@ -321,7 +321,6 @@ def run_mis(args, rank, world, local_rank):
         "registration": {"E_first": rep["energy"][0, 4], "E_last_iter": rep["energy"][G - 1, 4],
                          "n_assoc": int(rep["n_assoc"][0]), "nnzb": int(nnzb), "segments": int(rep["n_segments"]),
                          "pcg_cluster_ctas": int(rep["solver_cluster"]),
-                         "fp64_guard_points_iter0": int(rep["n_guard"][0]),
                          "fuse_stats": [int(x) for x in stats_last[1]]},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

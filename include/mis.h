@@ -99,7 +99,7 @@ typedef struct {
   int64_t n_segments;                  /* distinct kNN tuples in the model                  */
   int32_t solver_cluster;              /* CTAs of the cluster-resident PCG (0: grid kernel)  */
   int32_t reserved;
-  int64_t n_guard[MIS_MAX_GN + 1];     /* points re-evaluated in fp64 (guard band) per iteration */
+  int64_t n_guard[MIS_MAX_GN + 1];     /* reserved (0: the association runs in fp64, no guard band) */
 } mis_report;
 
 int32_t mis_abi_version(void);
