@@ -398,7 +398,7 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
                  &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->pcg_pptr, &c->pcg_pc, &c->pcg_push,
-                 &c->pcg_npush, &c->pcg_mask, &c->cub_tmp};
+                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -1035,8 +1035,9 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   if (n_lift > 0) {
     ProfScope ps(c, P_LIFT, 2);
     ModelView md = model_view(c);
-    launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->st);   // also resets the pixel keys
-    TRY(c, skin(c, n_lift, md.px + base, md.py + base, md.pz + base, 1, md.kidx + base, md.kw + base, c->cap));
+    TRY(c, ensure(c, c->lift_pos, px * 4));
+    launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->lift_pos.as<int32_t>(), c->st);   // + key reset
+    launch_skin_lifted(c->K, c->W, c->H, c->lift_pos.as<int32_t>(), md, c->g.as<float>(), c->m, c->st);
     c->dirty = true;
   } else {
     TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));

@@ -205,7 +205,10 @@ void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);
 void launch_lift_count(const FuseArgs& a, int32_t* block_counts, int nblocks, long long* ids_dev,
                        unsigned long long* n_registered, int do_lift, int64_t base, int64_t cap, cudaStream_t s);
 void launch_lift_write(const FuseArgs& a, const int32_t* block_offsets, int nblocks, int64_t base, int64_t cap,
-                       const long long* ids_dev, cudaStream_t s);
+                       const long long* ids_dev, int32_t* lift_pos, cudaStream_t s);
+// K2 (Eq. 2) of the lifted points, per pixel tile with a candidate-node bound (exact)
+void launch_skin_lifted(int K, int W, int H, const int32_t* lift_pos, const ModelView& md, const float* g, int m,
+                        cudaStream_t s);
 int lift_blocks(int W, int H);
 
 // ---- model order / pattern (sort.cu)

@@ -83,6 +83,7 @@ struct Ctx {
 
   // ---- fuse
   DBuf pixkey, pix, why, lift_counts, counter;
+  DBuf lift_pos;   // per pixel: the lifted point's model index (-1: none)
   bool pixkey_clean = false;   // pixel keys all-ones (reset by the lift write) -> no memset before K10
   DBuf ids_dev;   // int64 [0] next fresh point id, [1] id base of the last lift, [2] lifted points written
 

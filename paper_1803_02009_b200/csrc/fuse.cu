@@ -80,28 +80,16 @@ void launch_advance_nodes(const NodeView& nd, float* g, cudaStream_t s) {
 }
 
 // fp64 normal at a pixel from the five depths (reading A11); false if invalid
-__device__ bool normal64(const FrameView& f, int px, int py, double* N, double* q) {
-  const int W = f.W;
-  const float D = f.depth[py * W + px];
-  if (!dok(D)) return false;
-  q[0] = (px - f.cxd) * D / f.fxd; q[1] = (py - f.cyd) * D / f.fyd; q[2] = D;
-  if (px <= 0 || py <= 0 || px >= W - 1 || py >= f.H - 1) return false;
-  const float l = f.depth[py * W + px - 1], r = f.depth[py * W + px + 1];
-  const float u = f.depth[(py - 1) * W + px], d = f.depth[(py + 1) * W + px];
-  if (!dok(l) || !dok(r) || !dok(u) || !dok(d)) return false;
-  const double ax = ((px + 1) - f.cxd) * r / f.fxd - ((px - 1) - f.cxd) * l / f.fxd;
-  const double ay = (py - f.cyd) * (double)r / f.fyd - (py - f.cyd) * (double)l / f.fyd;
-  const double az = (double)r - (double)l;
-  const double bx = (px - f.cxd) * (double)d / f.fxd - (px - f.cxd) * (double)u / f.fxd;
-  const double by = ((py + 1) - f.cyd) * d / f.fyd - ((py - 1) - f.cyd) * u / f.fyd;
-  const double bz = (double)d - (double)u;
-  N[0] = ay * bz - az * by; N[1] = az * bx - ax * bz; N[2] = ax * by - ay * bx;
-  const double len = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
-  if (len < 1e-12) return false;
-  for (int c = 0; c < 3; ++c) N[c] /= len;
-  if (N[0] * q[0] + N[1] * q[1] + N[2] * q[2] > 0) for (int c = 0; c < 3; ++c) N[c] = -N[c];
+// (N, q) at pixel (px, py) from the fp64 normal map of K1 (central differences, reading A11)
+__device__ __forceinline__ bool normal_map64(const FrameView& f, int px, int py, double* N, double* q) {
+  const double4 nm = f.nmapd[py * f.W + px];
+  if (!(nm.w > 0)) return false;
+  q[0] = (px - f.cxd) * nm.w / f.fxd; q[1] = (py - f.cyd) * nm.w / f.fyd; q[2] = nm.w;
+  if (nm.x == 0 && nm.y == 0 && nm.z == 0) return false;
+  N[0] = nm.x; N[1] = nm.y; N[2] = nm.z;
   return true;
 }
+
 
 // K10: Alg. 1 gates + exclusive registration by 64-bit atomicMin
 // of ((|dz| in 1e-8 mm units) << 32 | point index) per pixel (reading A19).
@@ -128,7 +116,7 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
       double N[3], q[3];
       if (dok(D)) {
         why |= 4;
-        if (normal64(f, px, py, N, q)) {
+        if (normal_map64(f, px, py, N, q)) {
           why |= 8;
           const double dz = fabs(vt[2] - (double)D);
           if (dz < a.tz) {
@@ -164,7 +152,7 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
   const FrameView& f = a.fr;
   const int px = pix % f.W, py = pix / f.W;
   double N[3], q[3];
-  normal64(f, px, py, N, q);
+  normal_map64(f, px, py, N, q);
   const double v[3] = {a.md.px[i], a.md.py[i], a.md.pz[i]}, n[3] = {a.md.nx[i], a.md.ny[i], a.md.nz[i]};
   const double om = a.md.w[i];
   double pf[3], nf[3];
@@ -260,11 +248,14 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
 }
 
 __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int32_t* offs, int64_t base,
-                                                           int64_t cap, const long long* ids_dev) {
+                                                           int64_t cap, const long long* ids_dev, int32_t* lift_pos) {
   __shared__ int wsum[kLiftBlock / 32];
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const bool on = lift_pixel(a, p);
-  if (p < a.fr.W * a.fr.H) a.pixkey[p] = ~0ull;   // the next fusion finds the keys reset (no memset)
+  if (p < a.fr.W * a.fr.H) {
+    a.pixkey[p] = ~0ull;   // the next fusion finds the keys reset (no memset)
+    lift_pos[p] = -1;
+  }
   const unsigned bal = __ballot_sync(0xffffffffu, on);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) wsum[w] = __popc(bal);
@@ -274,10 +265,11 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   if (!on) return;
   const int64_t o = base + offs[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
   if (o >= cap) return;   // over capacity: reported by mis_fuse (MIS_E_CAPACITY)
+  lift_pos[p] = (int32_t)o;
   const FrameView& f = a.fr;
   const int px = p % f.W, py = p / f.W;
   double N[3], q[3];
-  normal64(f, px, py, N, q);
+  normal_map64(f, px, py, N, q);
   for (int c = 0; c < 3; ++c) q[c] -= f.Td[c];
   float vo[3], no[3];
   for (int c = 0; c < 3; ++c) {
@@ -304,8 +296,182 @@ void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long lon
 }
 
 void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, int64_t cap,
-                       const long long* ids_dev, cudaStream_t s) {
-  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, cap, ids_dev);
+                       const long long* ids_dev, int32_t* lift_pos, cudaStream_t s) {
+  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, cap, ids_dev, lift_pos);
+}
+
+// K2 for the lifted points, per 16 x 16 pixel tile (the lifted points of a tile are close in 3-D):
+// the tile's candidate nodes are those whose distance to the points' bounding box can be <= U, U
+// the (k+1)-th smallest farthest-corner distance -- every point of the box has k+1 nodes within U,
+// so every node of its k+1 nearest is a candidate; the points then scan only the candidates, keeping
+// (d^2, id) in lexicographic order (ties to the lower id).  Exact Eq. 2, ~20x fewer distances than
+// scanning all m nodes per point.
+constexpr int kTile = 16, kMaxCand = 2048;
+
+template <int K>
+__device__ __forceinline__ void knn_insert(float (&bd)[K + 1], int (&bi)[K + 1], float d2, int id) {
+  if (d2 > bd[K] || (d2 == bd[K] && id >= bi[K])) return;
+  float cd = d2;
+  int ci = id;
+#pragma unroll
+  for (int s = 0; s <= K; ++s) {
+    if (cd < bd[s] || (cd == bd[s] && ci < bi[s])) {
+      const float td = bd[s];
+      const int ti = bi[s];
+      bd[s] = cd; bi[s] = ci; cd = td; ci = ti;
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kTile * kTile) k_skin_tiles(int W, int H, const int32_t* __restrict__ lift_pos,
+                                                              ModelView md, const float* __restrict__ g, int m) {
+  __shared__ float4 cand[kMaxCand];
+  __shared__ float red[6][8];
+  __shared__ float sel[kTile * kTile / 32][K + 1];
+  __shared__ int ncand, any;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int x = blockIdx.x * kTile + (t % kTile), y = blockIdx.y * kTile + (t / kTile);
+  const int o = (x < W && y < H) ? lift_pos[y * W + x] : -1;
+  float v[3] = {0.f, 0.f, 0.f};
+  if (o >= 0) { v[0] = md.px[o]; v[1] = md.py[o]; v[2] = md.pz[o]; }
+  // bounding box of the tile's lifted points
+  float lo[3], hi[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { lo[c] = o >= 0 ? v[c] : INFINITY; hi[c] = o >= 0 ? v[c] : -INFINITY; }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int s = 16; s > 0; s >>= 1) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], s));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], s));
+    }
+  if (t == 0) { ncand = 0; any = 0; }
+  if (lane == 0) for (int c = 0; c < 3; ++c) { red[c][wid] = lo[c]; red[3 + c][wid] = hi[c]; }
+  __syncthreads();
+  if (o >= 0) any = 1;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = red[c][0]; hi[c] = red[3 + c][0];
+    for (int w = 1; w < 8; ++w) { lo[c] = fminf(lo[c], red[c][w]); hi[c] = fmaxf(hi[c], red[3 + c][w]); }
+  }
+  __syncthreads();
+  if (!any) return;
+  // U^2: the (k+1)-th smallest farthest-corner squared distance (per thread, per warp, per block)
+  float ub[K + 1];
+#pragma unroll
+  for (int s = 0; s <= K; ++s) ub[s] = INFINITY;
+  for (int j = t; j < m; j += blockDim.x) {
+    float u2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float gc = g[3 * j + c], e = fmaxf(fabsf(gc - lo[c]), fabsf(gc - hi[c]));
+      u2 += e * e;
+    }
+    if (u2 < ub[K]) {
+      float cu = u2;
+#pragma unroll
+      for (int s = 0; s <= K; ++s) if (cu < ub[s]) { const float tt = ub[s]; ub[s] = cu; cu = tt; }
+    }
+  }
+  // warp merge: k+1 rounds of (min, pop) over the lanes' sorted lists
+  float wsel[K + 1];
+#pragma unroll
+  for (int r = 0; r <= K; ++r) {
+    float mn = ub[0];
+    for (int s = 16; s > 0; s >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, s));
+    wsel[r] = mn;
+    const unsigned who = __ballot_sync(0xffffffffu, ub[0] == mn);
+    if (lane == __ffs(who) - 1) {
+#pragma unroll
+      for (int s = 0; s < K; ++s) ub[s] = ub[s + 1];
+      ub[K] = INFINITY;
+    }
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r <= K; ++r) sel[wid][r] = wsel[r];
+  __syncthreads();
+  float U2 = INFINITY;
+  {   // block: the (k+1)-th smallest of the 8 warps' sorted lists (every thread, same order: identical)
+    float best[K + 1];
+#pragma unroll
+    for (int s = 0; s <= K; ++s) best[s] = INFINITY;
+    for (int w = 0; w < kTile * kTile / 32; ++w)
+#pragma unroll
+      for (int r = 0; r <= K; ++r) {
+        float cu = sel[w][r];
+        if (cu < best[K])
+#pragma unroll
+          for (int s = 0; s <= K; ++s) if (cu < best[s]) { const float tt = best[s]; best[s] = cu; cu = tt; }
+      }
+    U2 = best[K] * (1.0f + 1e-5f) + 1e-6f;   // conservative against rounding
+  }
+  // candidates: nodes whose squared distance to the box can be <= U^2
+  for (int j = t; j < m; j += blockDim.x) {
+    float l2 = 0.f;
+    float gj[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      gj[c] = g[3 * j + c];
+      const float e = fmaxf(0.f, fmaxf(lo[c] - gj[c], gj[c] - hi[c]));
+      l2 += e * e;
+    }
+    if (l2 <= U2) {
+      const int q = atomicAdd(&ncand, 1);
+      if (q < kMaxCand) cand[q] = make_float4(gj[0], gj[1], gj[2], __int_as_float(j));
+    }
+  }
+  __syncthreads();
+  if (o < 0) return;
+  const int nc = ncand;
+  float bd[K + 1];
+  int bi[K + 1];
+#pragma unroll
+  for (int s = 0; s <= K; ++s) { bd[s] = INFINITY; bi[s] = 0x7fffffff; }
+  if (nc <= kMaxCand) {
+    for (int q = 0; q < nc; ++q) {
+      const float4 c4 = cand[q];
+      const float dx = v[0] - c4.x, dy = v[1] - c4.y, dz = v[2] - c4.z;
+      knn_insert<K>(bd, bi, dx * dx + dy * dy + dz * dz, __float_as_int(c4.w));
+    }
+  } else {   // candidate overflow (a very spread-out tile): all nodes
+    for (int j = 0; j < m; ++j) {
+      const float dx = v[0] - g[3 * j], dy = v[1] - g[3 * j + 1], dz = v[2] - g[3 * j + 2];
+      knn_insert<K>(bd, bi, dx * dx + dy * dy + dz * dz, j);
+    }
+  }
+  // Eq. 2 weights (as K2), ids ascending
+  const float dmax = sqrtf(bd[K]);
+  float ww[K];
+  float sum = 0.f;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    ww[s] = dmax > 0.f ? 1.0f - sqrtf(bd[s]) / dmax : 1.0f / K;
+    sum += ww[s];
+  }
+#pragma unroll
+  for (int s = 0; s < K; ++s) ww[s] = sum > 0.f ? ww[s] / sum : 1.0f / K;
+#pragma unroll
+  for (int a = 1; a < K; ++a)
+#pragma unroll
+    for (int b = a; b > 0; --b)
+      if (bi[b] < bi[b - 1]) {
+        int ti = bi[b]; bi[b] = bi[b - 1]; bi[b - 1] = ti;
+        float tw = ww[b]; ww[b] = ww[b - 1]; ww[b - 1] = tw;
+      }
+#pragma unroll
+  for (int s = 0; s < K; ++s) { md.kidx[s * md.cap + o] = bi[s]; md.kw[s * md.cap + o] = ww[s]; }
+}
+
+void launch_skin_lifted(int K, int W, int H, const int32_t* lift_pos, const ModelView& md, const float* g, int m,
+                        cudaStream_t s) {
+  dim3 grd((W + kTile - 1) / kTile, (H + kTile - 1) / kTile);
+  switch (K) {
+#define SK(KK) case KK: k_skin_tiles<KK><<<grd, kTile * kTile, 0, s>>>(W, H, lift_pos, md, g, m); break;
+    SK(1) SK(2) SK(3) SK(4) SK(5) SK(6) SK(7) SK(8)
+#undef SK
+    default: break;
+  }
 }
 
 }  // namespace mis
