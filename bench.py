@@ -240,58 +240,54 @@ def run_mis(args, rank, world, local_rank):
     M.mis_prof_enable(ctx.ptr, False)
     breakdown = M.mis_prof_read(ctx.ptr, reset=True)
 
-    # ---------------- roofline of the dominant kernel group
+    # ---------------- roofline of the dominant kernel (timed region: events around K3a, K3b, solver)
     hbm, _, peak_kind = peaks()
     groups = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(groups, key=lambda k: groups[k][0])
     nnzb, m = rep["nnzb"], sc["g"].shape[0]
     P, G = cfg.pcg_iters, cfg.gn_iters
+    kk = cfg.k
     n_assoc = float(np.mean(rep["n_assoc"][:G]))
+    nseg = int(rep["n_segments"])
     # algorithmic bytes per launch
     cluster = rep["solver_cluster"] > 0
     algo = {
-        "assemble_points": n * (24 + 4 * cfg.k) + 16 * n_assoc,
+        # K3a: point (24 B), skinning (8k B), one normal-map gather (32 B), compact state written (16(k+2) B)
+        "assoc_points": n * (24 + 8 * kk + 32 + 16 * (kk + 2)),
+        # K3b: compact state read once, one vector atomic per 4 accumulated floats per chunk (>= segments)
+        "accum_points": n * 16 * (kk + 2) + nseg * (13 * kk * (kk + 1) // 2 + 6 * kk) * 16,
         # cluster PCG: H (nnzb 6x6 blocks) and b read once, node state read/written once;
         # grid PCG: H streamed every iteration
         "solve": (nnzb * 144 + m * (24 + 96 + 64)) if cluster else (P * (nnzb * 144 + 6 * m * 4 * 11) + m * 160),
         # accumulators read once, H (both triangles), b and the block inverses written
         "finalize": nnzb * 88 * 4 + m * 24 * 4 + nnzb * 144 + m * (24 + 144),
-        "frame_prep": cfg.H * cfg.W * 20,
-        "warp_model": n * (24 + 8 * cfg.k) * 2 // 2 + n * 24,
-        "fuse_register": n * 24 + cfg.H * cfg.W * 8,
-        "fuse_apply": n * 64,
-        "lift": cfg.H * cfg.W * 28,
     }
-    ms_dom, n_dom = groups[dom]
-    per_launch_ms = ms_dom / max(1, n_dom if dom not in ("solve",) else n_dom / 2)
-    traffic = None
+    # K3b flops: the two upper-triangle SYRKs per associated point
+    flops_pt = 2 * ((6 * kk + 1) * (6 * kk + 2) // 2 + (4 * kk + 3) * (4 * kk + 4) // 2)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = sm_count * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s at the max SM clock (guide: 148 SMs)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dom)
-    bytes_dom = algo.get(dom)
-    roof = None
-    if bytes_dom is not None:
-        ach = bytes_dom / (per_launch_ms * 1e-3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": traffic, "peak_source": peak_kind,
-                "algorithmic_bytes_per_launch": int(bytes_dom), "launch_ms": round(per_launch_ms, 5),
-                "share_of_step": round(ms_dom / max(dev_ms, 1e-9), 3)}
+    traffic_all = json.load(open(tp)) if os.path.exists(tp) else {}
 
-    # the per-point hot kernel (north_star target), both views: HBM bytes and FP32 flops
-    roof_k3 = None
-    if "assemble_points" in groups:
-        ms3, n3 = groups["assemble_points"]
-        t3 = ms3 / max(1, n3) * 1e-3
-        kk = cfg.k
-        flops_pt = 2 * ((6 * kk + 1) * (6 * kk + 2) // 2 + (4 * kk + 3) * (4 * kk + 4) // 2) + 60 * kk + 80
-        flops = n_assoc * flops_pt + (n - n_assoc) * (60 * kk + 80)
-        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-        fp32_peak = sm_count * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s at the max SM clock (guide: 148 SMs)
-        roof_k3 = {"kernel": "assemble_points", "launch_ms": round(t3 * 1e3, 5),
-                   "hbm": {"achieved": round(algo["assemble_points"] / t3 / 1e9, 2), "peak": hbm, "unit": "GB/s",
-                           "frac": round(algo["assemble_points"] / t3 / 1e9 / hbm, 4)},
-                   "alu": {"achieved": round(flops / t3 / 1e12, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
-                           "frac": round(flops / t3 / 1e12 / fp32_peak, 4), "flops_per_associated_point": flops_pt}}
+    def roofline_of(name):
+        ms_k, n_k = groups[name]
+        t = ms_k / max(1, n_k) * 1e-3
+        base = {"kernel": name, "launch_ms": round(t * 1e3, 5), "share_of_step": round(ms_k / max(dev_ms, 1e-9), 3)}
+        if name == "accum_points":
+            ach = n_assoc * flops_pt / t / 1e12
+            base.update({"bound": "alu", "achieved": round(ach, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
+                         "frac": round(ach / fp32_peak, 4), "flops_per_associated_point": flops_pt,
+                         "peak_source": "FP32 FMA: SMs x 128 lanes x 2 x max SM clock"})
+        else:
+            ach = algo[name] / t / 1e9
+            base.update({"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": int(algo[name])})
+        base["traffic"] = traffic_all.get(name)
+        return base
+
+    roof = roofline_of(dom)
+    roof_k3 = {k: roofline_of(k) for k in ("assoc_points", "accum_points") if k in groups}
 
     jobs = 1 if sharded else world   # registrations per step over the whole job
     value = jobs * K / (dev_ms_max / 1e3)
@@ -310,7 +306,7 @@ def run_mis(args, rank, world, local_rank):
         "e2e": {"value": round(jobs * Ke / (e2e_ms_max / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": rep_bytes + 8, "steps": Ke},
         "roofline": roof,
-        "roofline_points_kernel": roof_k3,
+        "roofline_k3": roof_k3,
         "kernels_ms_per_step": {k: round(v[0] / K, 5) for k, v in breakdown.items() if v[1] > 0 or v[0] > 0},
         "kernels_note": "kernels_ms_per_step: separate pass of the same K steps with events around every group "
                         "(the timed region records events only around K3 and the solver)",

@@ -220,7 +220,7 @@ mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* v
 mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
 
 /* ---- instrumentation (bench / profiling) ---- */
-#define MIS_PROF_NCAT 13
+#define MIS_PROF_NCAT 14
 /* Kernel groups: 0 frame_prep (K1), 1 skin (K2), 2 sort_order (K13), 3 pattern,
  * 4 assemble_points (K3), 5 assemble_graph (K4/K5), 6 solve (K6-K8),
  * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),

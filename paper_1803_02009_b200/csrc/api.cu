@@ -266,7 +266,7 @@ static cudaEvent_t pool_get(Ctx* c) {
 ProfScope::ProfScope(Ctx* c_, int cat_, int nk) : c(c_), cat(cat_) {
   l0 = g_launches;
   g_launches += nk;
-  if (c->prof && (!c->prof_light || cat == P_POINTS || cat == P_SOLVE)) {
+  if (c->prof && (!c->prof_light || cat == P_POINTS || cat == P_ACCUM || cat == P_SOLVE)) {
     cudaEvent_t a = pool_get(c);
     b = pool_get(c);
     cudaEventRecord(a, c->st);
@@ -635,8 +635,12 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
   if (c->n > 0) {
-    ProfScope ps(c, P_POINTS, a.nchunk > 0 ? 2 : 1);   // K3a, K3b
-    launch_assemble_points(c->K, a, c->num_sms, c->st);
+    ProfScope ps(c, P_POINTS, 1);
+    launch_assoc_points(c->K, a, c->st);
+  }
+  if (a.nchunk > 0) {
+    ProfScope ps(c, P_ACCUM, 1);
+    launch_accum_points(c->K, a, c->num_sms, c->st);
   }
   TRY(c, cudaGetLastError());
   if (c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0) {
@@ -1124,9 +1128,9 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
 }
 
 const char* mis_prof_name(int cat) {
-  static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assemble_points",
+  static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assoc_points",
                                              "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
-                                             "lift", "io", "finalize"};
+                                             "lift", "io", "finalize", "accum_points"};
   return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
 }
 

@@ -531,15 +531,17 @@ void launch_finalize(const FinalArgs& r, cudaStream_t s) {
 }
 
 template <int K>
-static void launch_points_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
-  using L = Lay<K>;
-  const bool dbg = a.dbg_pix != nullptr;
+static void launch_assoc_k(const AsmPointsArgs& a, cudaStream_t s) {
   const int64_t n = a.md.n;
-  if (n > 0) {
-    const unsigned g = (unsigned)((n + 255) / 256);
-    if (dbg) k_assoc_points<K, true><<<g, 256, 0, s>>>(a);
-    else k_assoc_points<K, false><<<g, 256, 0, s>>>(a);
-  }
+  if (n <= 0) return;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (a.dbg_pix != nullptr) k_assoc_points<K, true><<<g, 256, 0, s>>>(a);
+  else k_assoc_points<K, false><<<g, 256, 0, s>>>(a);
+}
+
+template <int K>
+static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+  using L = Lay<K>;
   if (a.nchunk <= 0) return;
   const size_t smem = sizeof(float) * kWarps * 32 * L::FSP;
   auto kern = k_accum_points<K>;
@@ -558,9 +560,18 @@ static void launch_points_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s)
   kern<<<(int)grid, kWarps * 32, smem, s>>>(a);
 }
 
-void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+void launch_assoc_points(int K, const AsmPointsArgs& a, cudaStream_t s) {
   switch (K) {
-#define LP(KK) case KK: launch_points_k<KK>(a, num_sms, s); break;
+#define LP(KK) case KK: launch_assoc_k<KK>(a, s); break;
+    LP(1) LP(2) LP(3) LP(4) LP(5) LP(6) LP(7) LP(8)
+#undef LP
+    default: break;
+  }
+}
+
+void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+  switch (K) {
+#define LP(KK) case KK: launch_accum_k<KK>(a, num_sms, s); break;
     LP(1) LP(2) LP(3) LP(4) LP(5) LP(6) LP(7) LP(8)
 #undef LP
     default: break;

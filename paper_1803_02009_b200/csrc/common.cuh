@@ -91,8 +91,9 @@ struct AsmPointsArgs {
   int32_t* dbg_pix;           // nullable: per point association outputs
   uint8_t* dbg_why;
 };
-// K3a (per point) then K3b (per chunk) on s
-void launch_assemble_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
+// K3a (per point), then K3b (per chunk)
+void launch_assoc_points(int K, const AsmPointsArgs& a, cudaStream_t s);
+void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
 
 // Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator
 // addresses at commit): P pairs x [36 data (6x6, upper for the diagonal pair) |

@@ -102,7 +102,7 @@ struct Ctx {
 };
 
 enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO,
-       P_REDUCE };
+       P_REDUCE, P_ACCUM };
 void count_launches(int64_t k);
 
 // report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual

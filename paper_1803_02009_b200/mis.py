@@ -87,7 +87,7 @@ _sig = {
     "mis_launch_count": ([], C.c_int64),
     "mis_dbg_solver_phases": ([_V, _V], C.c_int),
 }
-MIS_PROF_NCAT = 13
+MIS_PROF_NCAT = 14
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
