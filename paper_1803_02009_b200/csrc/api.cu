@@ -631,21 +631,11 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.pstate = c->pstate.as<float4>();
   a.pstride = std::max<int64_t>(c->n, 1);
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
-
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
-  if (c->n > 0) {
-    ProfScope ps(c, P_POINTS, 1);
-    launch_assoc_points(c->K, a, c->st);
-  }
-  if (a.nchunk > 0) {
-    ProfScope ps(c, P_ACCUM, 1);
-    launch_accum_points(c->K, a, c->num_sms, c->st);
-  }
-  TRY(c, cudaGetLastError());
-  if (c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0) {
-    ProfScope ps(c, P_GRAPH, 1);
-    AsmGraphArgs gA;
+  const bool graph_terms = c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0;   // K4/K5 on rank 0
+  AsmGraphArgs gA;
+  if (graph_terms) {
     gA.nd = node_view(c);
     gA.n_nbr = c->prm.n_nbr;
     gA.nbr = c->nbr.as<int32_t>();
@@ -662,9 +652,16 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     gA.w_corr = c->prm.w_corr;
     gA.acc = acc;
     gA.K = c->K;
-    launch_assemble_graph(gA, c->st);
-    TRY(c, cudaGetLastError());
   }
+  if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch
+    ProfScope ps(c, P_POINTS, 1);
+    launch_assoc_points(c->K, a, graph_terms ? &gA : nullptr, c->st);
+  }
+  if (a.nchunk > 0) {
+    ProfScope ps(c, P_ACCUM, 1);
+    launch_accum_points(c->K, a, c->num_sms, c->st);
+  }
+  TRY(c, cudaGetLastError());
   if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
     if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
     if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), kEnergyDoubles) != cudaSuccess) return MIS_E_NCCL;

@@ -27,7 +27,7 @@
 namespace mis {
 
 #ifndef MIS_K3_SPLIT
-#define MIS_K3_SPLIT 2   // 2: split each tile's batch into halves across lanes (measured best at K=4)
+#define MIS_K3_SPLIT 1   // 2: split each tile batch into halves across lanes (K3b measured best with 1)
 #endif
 
 template <int K>
@@ -204,8 +204,16 @@ __device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, do
   }
 }
 
+__device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid);
+
+// K3a; the blocks after the points' run the K4/K5 items (independent of K3a, same launch)
 template <int K, bool DBG>
-__global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a) {
+__global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
+                                                                   unsigned point_blocks) {
+  if (blockIdx.x >= point_blocks) {
+    graph_item(ga, (int64_t)(blockIdx.x - point_blocks) * blockDim.x + threadIdx.x);
+    return;
+  }
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double ed = 0.0, ep = 0.0;
   int as = 0;
@@ -531,12 +539,20 @@ void launch_finalize(const FinalArgs& r, cudaStream_t s) {
 }
 
 template <int K>
-static void launch_assoc_k(const AsmPointsArgs& a, cudaStream_t s) {
+static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s) {
   const int64_t n = a.md.n;
-  if (n <= 0) return;
   const unsigned g = (unsigned)((n + 255) / 256);
-  if (a.dbg_pix != nullptr) k_assoc_points<K, true><<<g, 256, 0, s>>>(a);
-  else k_assoc_points<K, false><<<g, 256, 0, s>>>(a);
+  AsmGraphArgs gz{};
+  int64_t ng = 0;
+  if (ga) {
+    gz = *ga;
+    const int P = K * (K + 1) / 2;
+    ng = (int64_t)gz.nd.m * gz.n_nbr * 6 + (int64_t)gz.nf * P * 6 + (int64_t)gz.nf * K;
+  }
+  const unsigned gg = (unsigned)((ng + 255) / 256);
+  if (g + gg == 0) return;
+  if (a.dbg_pix != nullptr) k_assoc_points<K, true><<<g + gg, 256, 0, s>>>(a, gz, g);
+  else k_assoc_points<K, false><<<g + gg, 256, 0, s>>>(a, gz, g);
 }
 
 template <int K>
@@ -560,9 +576,9 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) 
   kern<<<(int)grid, kWarps * 32, smem, s>>>(a);
 }
 
-void launch_assoc_points(int K, const AsmPointsArgs& a, cudaStream_t s) {
+void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s) {
   switch (K) {
-#define LP(KK) case KK: launch_assoc_k<KK>(a, s); break;
+#define LP(KK) case KK: launch_assoc_k<KK>(a, ga, s); break;
     LP(1) LP(2) LP(3) LP(4) LP(5) LP(6) LP(7) LP(8)
 #undef LP
     default: break;
@@ -630,8 +646,13 @@ __device__ __forceinline__ void add_row(float* B, int r, const float* row, float
     if (row[c] != 0.f) atomicAdd(B + 6 * r + c, w * row[c]);
 }
 
-__global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ int64_t graph_items(const AsmGraphArgs& a) {
+  const int P = a.K * (a.K + 1) / 2;
+  return (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.K;
+}
+
+// one K4/K5 item per thread (whole warps call this; tid >= graph_items: no work)
+__device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
   const int K = a.K, P = K * (K + 1) / 2;
   const int64_t n_edge = (int64_t)a.nd.m * a.n_nbr * 6, n_fp = (int64_t)a.nf * P * 6, n_fr = (int64_t)a.nf * K;
   float eR = 0.f, eC = 0.f;
@@ -709,6 +730,10 @@ __global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
     energy_add(a.acc.energy, 2, (double)eR);
     energy_add(a.acc.energy, 3, (double)eC);
   }
+}
+
+__global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
+  graph_item(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s) {

@@ -92,7 +92,9 @@ struct AsmPointsArgs {
   uint8_t* dbg_why;
 };
 // K3a (per point), then K3b (per chunk)
-void launch_assoc_points(int K, const AsmPointsArgs& a, cudaStream_t s);
+struct AsmGraphArgs;
+// K3a (per point; with K4/K5 items in the same launch when ga != null), then K3b (per chunk)
+void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s);
 void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
 
 // Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator
