@@ -210,8 +210,10 @@ __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid);
 template <int K, bool DBG>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_blocks) {
+  pdl_wait();   // node states from the previous solve
   if (blockIdx.x >= point_blocks) {
     graph_item(ga, (int64_t)(blockIdx.x - point_blocks) * blockDim.x + threadIdx.x);
+    pdl_trigger();
     return;
   }
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArg
     ps[(K + 1) * S + i] = st.nn;
   }
   commit_point_energies(a, ed, ep, as);
+  pdl_trigger();
 }
 
 // factor row of one point from its compact state (K3b: shared memory, FSP floats)
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     p0[r] = (it / L::NT) * L::PS;
   }
 
+  pdl_wait();   // K3a's factor state (the tables above are independent of it)
   // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
   int64_t c = 0;
   if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     }
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
+  pdl_trigger();
 }
 
 // Finalisation of the normal equations from the accumulators (so the
@@ -422,6 +427,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
 //   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
 __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   __shared__ float stage[8][124];
+  pdl_wait();   // K3a/K3b/K4 accumulators
+  pdl_trigger();   // the solver may launch (it waits for this grid's completion before reading)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* st = stage[wib];
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
 void launch_finalize(const FinalArgs& r, cudaStream_t s) {
   const int64_t warps = 2 * (int64_t)r.m + r.nnzb + 1;
   const int64_t blocks = (warps * 32 + 255) / 256;
-  if (blocks > 0) k_finalize<<<(unsigned)blocks, 256, 0, s>>>(r);
+  if (blocks > 0) launch_pdl(k_finalize, dim3((unsigned)blocks), dim3(256), 0, s, r);
 }
 
 template <int K>
@@ -551,8 +558,8 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
   }
   const unsigned gg = (unsigned)((ng + 255) / 256);
   if (g + gg == 0) return;
-  if (a.dbg_pix != nullptr) k_assoc_points<K, true><<<g + gg, 256, 0, s>>>(a, gz, g);
-  else k_assoc_points<K, false><<<g + gg, 256, 0, s>>>(a, gz, g);
+  if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+  else launch_pdl(k_assoc_points<K, false>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
 }
 
 template <int K>
@@ -573,7 +580,7 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) 
   int64_t grid = (int64_t)num_sms * per_sm;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
-  kern<<<(int)grid, kWarps * 32, smem, s>>>(a);
+  launch_pdl(kern, dim3((unsigned)grid), dim3(kWarps * 32), smem, s, a);
 }
 
 void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s) {

@@ -10,6 +10,30 @@
 
 namespace mis {
 
+// Programmatic dependent launch (sm_90+): kernels of the Gauss-Newton chain are launched with
+// programmatic stream serialisation, so a kernel's launch and block scheduling overlap the tail
+// of its predecessor; pdl_wait() (before reading anything the predecessor wrote) blocks until the
+// predecessor grid has completed and its writes are visible; pdl_trigger() lets the successor
+// launch.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // ------------------------------------------------------------- device views
 struct FrameView {
   int W, H;

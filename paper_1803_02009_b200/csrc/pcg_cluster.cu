@@ -423,6 +423,8 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   int* push = reinterpret_cast<int*>(sm + L.push);
   float* H = reinterpret_cast<float*>(sm + L.h);
 
+  pdl_wait();      // H, b, M^-1 from the finalisation
+  pdl_trigger();   // the next K3a may launch on the SMs this cluster leaves free (it waits for completion)
   const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   const int r0 = a.part[rank], r1 = a.part[rank + 1], nr = r1 - r0;
   const int e0 = a.row_ptr[r0], e1 = a.row_ptr[r1], ne = e1 - e0;
@@ -644,13 +646,15 @@ cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {
   cfg.blockDim = dim3(kCT);
   cfg.dynamicSmemBytes = a.smem_bytes;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)a.cluster_size;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlaps the finalisation's tail
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_pcg_cluster, a);
 }
 
