@@ -154,6 +154,8 @@ struct LoadSrc {
   const int64_t* ids;
 };
 __global__ void k_load_model(int64_t n, LoadSrc src, ModelView md, long long* ids_dev) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ long long bm;
   if (threadIdx.x == 0) bm = -1;
   if (blockIdx.x == 0 && threadIdx.x == 0 && !src.ids) ids_dev[0] = n;
@@ -177,6 +179,8 @@ __global__ void k_load_model(int64_t n, LoadSrc src, ModelView md, long long* id
 // point-major (n x K) caller skinning -> slot-major, ids ascending; validation flags
 __global__ void k_canon_knn(int64_t n, int K, int m, const int32_t* idx_pm, const float* w_pm, int64_t cap,
                             int32_t* kidx, float* kw, int* flag) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int id[MIS_MAX_K];
@@ -207,6 +211,8 @@ __global__ void k_to_point_major(int64_t n, int K, int64_t cap, const int32_t* k
   }
 }
 __global__ void k_check_nbr(int m, int n_nbr, int32_t* nbr, int* flag) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * n_nbr) return;
   const int l = nbr[t];
@@ -216,6 +222,8 @@ __global__ void k_check_nbr(int m, int n_nbr, int32_t* nbr, int* flag) {
   }
 }
 __global__ void k_init_nodes(int m, const float* g, double* Rt64, float* node32) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   for (int i = 0; i < 12; ++i) Rt64[12 * j + i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
@@ -467,7 +475,7 @@ mis_status mis_set_model(mis_ctx* c, int64_t n, mis_mem mem, const float* xyz, c
       TRY(c, err);
     }
     ProfScope ps(c, P_IO, 1);
-    k_load_model<<<nb(n), 256, 0, c->st>>>(n, src, md, c->ids_dev.as<long long>());
+    launch_pdl(k_load_model, dim3(nb(n)), dim3(256), 0, c->st, n, src, md, c->ids_dev.as<long long>());
   } else {
     ProfScope ps(c, P_IO, 1);
     k_next_id<<<1, 256, 0, c->st>>>(0, nullptr, c->ids_dev.as<long long>());
@@ -513,7 +521,7 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   TRY(c, cudaMemsetAsync(flag, 0, 8, c->st));
   if (nn > 0) {
     ProfScope ps(c, P_IO, 1);
-    k_check_nbr<<<nb((int64_t)m * nn), 256, 0, c->st>>>(m, nn, c->nbr.as<int32_t>(), flag);
+    launch_pdl(k_check_nbr, dim3(nb((int64_t)m * nn)), dim3(256), 0, c->st, m, nn, c->nbr.as<int32_t>(), flag);
   }
   ModelView md = model_view(c);
   const int64_t n = c->n;
@@ -531,7 +539,7 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
         si = di;
         sw = dw;
       }
-      k_canon_knn<<<nb(n), 256, 0, c->st>>>(n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
+      launch_pdl(k_canon_knn, dim3(nb(n)), dim3(256), 0, c->st, n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
     } else {
       TRY(c, skin(c, n, md.px, md.py, md.pz, 1, md.kidx, md.kw, c->cap));
     }
@@ -553,7 +561,7 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   }
   {
     ProfScope ps(c, P_IO, 1);
-    k_init_nodes<<<nb(m), 256, 0, c->st>>>(m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
+    launch_pdl(k_init_nodes, dim3(nb(m)), dim3(256), 0, c->st, m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
   }
   TRY(c, cudaGetLastError());
   TRY(c, run_build_order(c));

@@ -13,6 +13,8 @@ __device__ __forceinline__ bool depth_ok(float d) { return isfinite(d) && d > 0.
 // (N in fp64, D) and nmap (N rounded to fp32, D; D = 0 for an invalid depth).
 // HBM-bound: 4 B read (+ neighbours from L1/L2), 48 B written per pixel.
 __global__ void __launch_bounds__(256) k_frame_prep(FrameView f, float4* __restrict__ nmap, double4* __restrict__ nmapd) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= f.W || y >= f.H) return;
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(256) k_frame_prep(FrameView f, float4* __restr
 
 void launch_frame_prep(const FrameView& f, float4* nmap, double4* nmapd, cudaStream_t s) {
   dim3 blk(32, 8), grd((f.W + 31) / 32, (f.H + 7) / 8);
-  k_frame_prep<<<grd, blk, 0, s>>>(f, nmap, nmapd);
+  launch_pdl(k_frame_prep, dim3(grd), dim3(blk), 0, s, f, nmap, nmapd);
 }
 
 // K2: Eq. 2 -- the k+1 nearest nodes of each query (ties to the
@@ -70,6 +72,8 @@ template <int K, int S>
 __global__ void __launch_bounds__(256) k_skin(int64_t nq, const float* __restrict__ px, const float* __restrict__ py,
                                               const float* __restrict__ pz, int64_t sxyz, const float* __restrict__ g,
                                               int m, int32_t* __restrict__ idx, float* __restrict__ w, int64_t os) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ float4 sg[1024];
   const int tl = threadIdx.x % S;   // lane within the team
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S;
@@ -165,7 +169,7 @@ static void skin_k(int64_t nq, const float* px, const float* py, const float* pz
   while (S < 32 && nq * S < fill && S * 8 <= m) S *= 2;
   const int blocks = (int)((nq * S + 255) / 256);
   switch (S) {
-#define SK(SS) case SS: k_skin<K, SS><<<blocks, 256, 0, s>>>(nq, px, py, pz, sxyz, g, m, idx, w, os); break;
+#define SK(SS) case SS: launch_pdl(k_skin<K, SS>, dim3(blocks), dim3(256), 0, s, nq, px, py, pz, sxyz, g, m, idx, w, os); break;
     SK(1) SK(2) SK(4) SK(8) SK(16) SK(32)
 #undef SK
     default: break;

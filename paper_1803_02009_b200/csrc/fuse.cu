@@ -12,6 +12,8 @@ __device__ __forceinline__ bool dok(float d) { return isfinite(d) && d > 0.0f; }
 template <int K>
 __global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, FrameView fr, float* xyz_cam,
                                                    float* nrm_cam) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= md.n) return;
   float v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
@@ -52,7 +54,7 @@ void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const Fra
   if (md.n <= 0) return;
   const int b = (int)((md.n + 255) / 256);
   switch (K) {
-#define WK(KK) case KK: k_warp_model<KK><<<b, 256, 0, s>>>(md, nd, fr, xyz_cam, nrm_cam); break;
+#define WK(KK) case KK: launch_pdl(k_warp_model<KK>, dim3(b), dim3(256), 0, s, md, nd, fr, xyz_cam, nrm_cam); break;
     WK(1) WK(2) WK(3) WK(4) WK(5) WK(6) WK(7) WK(8)
 #undef WK
     default: break;
@@ -61,6 +63,8 @@ void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const Fra
 
 // Reading A26: g_j += t_j, then R_j = I, t_j = 0.
 __global__ void k_advance_nodes(NodeView nd, float* g) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nd.m) return;
   double* Rt = nd.Rt64 + 12 * j;
@@ -76,7 +80,7 @@ __global__ void k_advance_nodes(NodeView nd, float* g) {
 
 void launch_advance_nodes(const NodeView& nd, float* g, cudaStream_t s) {
   if (nd.m <= 0) return;
-  k_advance_nodes<<<(nd.m + 255) / 256, 256, 0, s>>>(nd, g);
+  launch_pdl(k_advance_nodes, dim3((nd.m + 255) / 256), dim3(256), 0, s, nd, g);
 }
 
 // fp64 normal at a pixel from the five depths (reading A11); false if invalid
@@ -94,6 +98,8 @@ __device__ __forceinline__ bool normal_map64(const FrameView& f, int px, int py,
 // K10: Alg. 1 gates + exclusive registration by 64-bit atomicMin
 // of ((|dz| in 1e-8 mm units) << 32 | point index) per pixel (reading A19).
 __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 && a.n_reg) *a.n_reg = 0;   // counted later by the lift count
   if (i >= a.md.n) return;
@@ -139,11 +145,13 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
 
 void launch_fuse_register(const FuseArgs& a, cudaStream_t s) {
   if (a.md.n <= 0) return;
-  k_fuse_register<<<(int)((a.md.n + 255) / 256), 256, 0, s>>>(a);
+  launch_pdl(k_fuse_register, dim3((int)((a.md.n + 255) / 256)), dim3(256), 0, s, a);
 }
 
 // K11: Eq. 12-15 on each pixel's winner; 3-D weighted average (reading A21)
 __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.md.n) return;
   const int32_t pix = a.pix[i];
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
 
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s) {
   if (a.md.n <= 0) return;
-  k_fuse_apply<<<(int)((a.md.n + 255) / 256), 256, 0, s>>>(a);
+  launch_pdl(k_fuse_apply, dim3((int)((a.md.n + 255) / 256)), dim3(256), 0, s, a);
 }
 
 // K12: valid (depth and normal), unregistered pixels -> new points, row-major.
@@ -200,6 +208,8 @@ __device__ __forceinline__ bool lift_pixel(const FuseArgs& a, int p) {
 // per block: lifted pixels (scanned next) and registered pixels (the fusion count)
 __global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* counts, unsigned long long* n_reg,
                                                            int do_lift) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const int c = __syncthreads_count(do_lift && lift_pixel(a, p));
   const int r = __syncthreads_count(p < a.fr.W * a.fr.H && a.pixkey[p] != ~0ull);
@@ -213,6 +223,8 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_count(FuseArgs a, int32_t* 
 // ids_dev[2] = lifted points that fit the capacity
 __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int32_t* offs, int nb,
                                                       long long* ids_dev, int64_t base, int64_t cap) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ int32_t wtot[32];
   const int per = (nb + 1023) / 1024;
   const int b0 = threadIdx.x * per;
@@ -249,6 +261,8 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
 
 __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int32_t* offs, int64_t base,
                                                            int64_t cap, const long long* ids_dev, int32_t* lift_pos) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ int wsum[kLiftBlock / 32];
   const int p = blockIdx.x * kLiftBlock + threadIdx.x;
   const bool on = lift_pixel(a, p);
@@ -291,13 +305,13 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
 
 void launch_lift_count(const FuseArgs& a, int32_t* counts, int nblocks, long long* ids_dev, unsigned long long* n_reg,
                        int do_lift, int64_t base, int64_t cap, cudaStream_t s) {
-  k_lift_count<<<nblocks, kLiftBlock, 0, s>>>(a, counts, n_reg, do_lift);
-  k_scan_counts<<<1, 1024, 0, s>>>(counts, counts + nblocks + 1, nblocks, ids_dev, base, cap);
+  launch_pdl(k_lift_count, dim3(nblocks), dim3(kLiftBlock), 0, s, a, counts, n_reg, do_lift);
+  launch_pdl(k_scan_counts, dim3(1), dim3(1024), 0, s, counts, counts + nblocks + 1, nblocks, ids_dev, base, cap);
 }
 
 void launch_lift_write(const FuseArgs& a, const int32_t* offs, int nblocks, int64_t base, int64_t cap,
                        const long long* ids_dev, int32_t* lift_pos, cudaStream_t s) {
-  k_lift_write<<<nblocks, kLiftBlock, 0, s>>>(a, offs, base, cap, ids_dev, lift_pos);
+  launch_pdl(k_lift_write, dim3(nblocks), dim3(kLiftBlock), 0, s, a, offs, base, cap, ids_dev, lift_pos);
 }
 
 // K2 for the lifted points, per 16 x 16 pixel tile (the lifted points of a tile are close in 3-D):
@@ -326,6 +340,8 @@ __device__ __forceinline__ void knn_insert(float (&bd)[K + 1], int (&bi)[K + 1],
 template <int K>
 __global__ void __launch_bounds__(kTile * kTile) k_skin_tiles(int W, int H, const int32_t* __restrict__ lift_pos,
                                                               ModelView md, const float* __restrict__ g, int m) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ float4 cand[kMaxCand];
   __shared__ float red[6][8];
   __shared__ float sel[kTile * kTile / 32][K + 1];
@@ -467,7 +483,7 @@ void launch_skin_lifted(int K, int W, int H, const int32_t* lift_pos, const Mode
                         cudaStream_t s) {
   dim3 grd((W + kTile - 1) / kTile, (H + kTile - 1) / kTile);
   switch (K) {
-#define SK(KK) case KK: k_skin_tiles<KK><<<grd, kTile * kTile, 0, s>>>(W, H, lift_pos, md, g, m); break;
+#define SK(KK) case KK: launch_pdl(k_skin_tiles<KK>, dim3(grd), dim3(kTile * kTile), 0, s, W, H, lift_pos, md, g, m); break;
     SK(1) SK(2) SK(3) SK(4) SK(5) SK(6) SK(7) SK(8)
 #undef SK
     default: break;

@@ -65,6 +65,8 @@ struct PcgLists {
 
 // every rank marks the rows its blocks read in other ranks' ranges
 __global__ void k_pcg_mark(const int32_t* row_ptr, const int32_t* col, const int32_t* part, PcgLists L) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int rank = blockIdx.x, r0 = part[rank], r1 = part[rank + 1];
   for (int k = row_ptr[r0] + threadIdx.x; k < row_ptr[r1]; k += blockDim.x) {
     const int j = col[k];
@@ -76,6 +78,8 @@ __global__ void k_pcg_mark(const int32_t* row_ptr, const int32_t* col, const int
 // SpMV's work units are balanced whatever the row lengths; the push list ((destination,
 // row) pairs grouped by destination, itself included); the rows' marks are cleared
 __global__ void k_pcg_lists(const int32_t* row_ptr, const int32_t* part, int cs, int max_rows, int max_pc, PcgLists L) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int rank = blockIdx.x, r0 = part[rank], nr = part[rank + 1] - r0, l = threadIdx.x;
   const int e0 = row_ptr[r0];
   int32_t* pptr = L.pptr + (int64_t)rank * (max_rows + 1);
@@ -572,6 +576,8 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
 // host never reads the row structure back.  Same rule as plan_cluster.
 __global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part,
                                int64_t* nnz_out) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   __shared__ int32_t b[kMaxCluster + 1];
   int cs = max_cluster < m ? max_cluster : m;
   if (cs > kMaxCluster) cs = kMaxCluster;
@@ -616,14 +622,14 @@ __global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, P
 void launch_pcg_prep(const int32_t* row_ptr, const int32_t* col, const int32_t* part, int cs, int max_rows, int max_nnz,
                      int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s) {
   PcgLists L{pptr, pc, push, npush, mask};
-  k_pcg_mark<<<cs, 256, 0, s>>>(row_ptr, col, part, L);
-  k_pcg_lists<<<cs, 32, 0, s>>>(row_ptr, part, cs, max_rows, max_pieces(max_rows, max_nnz), L);
+  launch_pdl(k_pcg_mark, dim3(cs), dim3(256), 0, s, row_ptr, col, part, L);
+  launch_pdl(k_pcg_lists, dim3(cs), dim3(32), 0, s, row_ptr, part, cs, max_rows, max_pieces(max_rows, max_nnz), L);
 }
 int pcg_max_pieces(int max_rows, int max_nnz) { return max_pieces(max_rows, max_nnz); }
 
 void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut* out, int32_t* part, int64_t* nnz_out,
                          cudaStream_t s) {
-  k_plan_cluster<<<1, 32, 0, s>>>(row_ptr, m, max_cluster, out, part, nnz_out);
+  launch_pdl(k_plan_cluster, dim3(1), dim3(32), 0, s, row_ptr, m, max_cluster, out, part, nnz_out);
 }
 
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {

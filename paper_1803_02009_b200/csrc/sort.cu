@@ -36,6 +36,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 // radix passes: 3 passes at c3 instead of 5 for the exact 40-bit packing.
 __global__ void k_tuple_keys(int64_t n, int64_t cap, const int32_t* kidx, int K, int kb, uint64_t* keys,
                              uint32_t* vals) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t h = 0x9e3779b97f4a7c15ull;
@@ -46,6 +48,8 @@ __global__ void k_tuple_keys(int64_t n, int64_t cap, const int32_t* kidx, int K,
 
 // all model arrays in one launch: dst[i] = src[perm[i]]
 __global__ void k_gather_model(int64_t n, const uint32_t* perm, ModelView a, ModelView b, int K) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t j = perm[i];
@@ -60,6 +64,8 @@ __global__ void k_gather_model(int64_t n, const uint32_t* perm, ModelView a, Mod
 }
 
 __global__ void k_seg_flags(int64_t n, int64_t cap, const int32_t* kidx, int K, int32_t* flags) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int f = (i == 0);
@@ -72,6 +78,8 @@ __global__ void k_seg_flags(int64_t n, int64_t cap, const int32_t* kidx, int K, 
 // scan = inclusive sum of flags; seg id = scan - 1
 __global__ void k_seg_write(int64_t n, int64_t cap, const int32_t* kidx, int K, const int32_t* flags,
                             const int32_t* scan, int32_t* seg_start, int32_t* seg_nodes) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (!flags[i]) return;
@@ -82,6 +90,8 @@ __global__ void k_seg_write(int64_t n, int64_t cap, const int32_t* kidx, int K, 
 }
 
 __global__ void k_chunk_count(int64_t n, const int32_t* nseg_dev, const int32_t* seg_start, int32_t* cnt) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   if (s >= *nseg_dev) { cnt[s] = 0; return; }
@@ -91,6 +101,8 @@ __global__ void k_chunk_count(int64_t n, const int32_t* nseg_dev, const int32_t*
 
 __global__ void k_chunk_write(int64_t n, const int32_t* nseg_dev, const int32_t* seg_start, const int32_t* off,
                               int4* chunks, int64_t* info) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s == 0) { info[1] = *nseg_dev; info[2] = off[n - 1]; }   // device-resident counts (read back with the pattern)
   if (s >= n || s >= *nseg_dev) return;
@@ -123,13 +135,13 @@ cudaError_t build_order(Ctx* c) {
     const int64_t t_est = c->nseg > 0 ? c->nseg : std::max<int64_t>(n / 8, 1);
     const int kb = std::min(64, (bits_for((int)std::min<int64_t>(t_est, 1 << 30)) + 7 + 7) / 8 * 8);
     const int b = (int)((n + 255) / 256);
-    k_tuple_keys<<<b, 256, 0, c->st>>>(n, c->cap, A.kidx.as<int32_t>(), K, kb, c->keys.as<uint64_t>(),
+    launch_pdl(k_tuple_keys, dim3(b), dim3(256), 0, c->st, n, c->cap, A.kidx.as<int32_t>(), K, kb, c->keys.as<uint64_t>(),
                                         c->vals.as<uint32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceRadixSort::SortPairs(t, s, c->keys.as<uint64_t>(), c->keys2.as<uint64_t>(),
                                              c->vals.as<uint32_t>(), c->vals2.as<uint32_t>(), (int)n, 0, kb, c->st);
     }));
-    k_gather_model<<<b, 256, 0, c->st>>>(n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
+    launch_pdl(k_gather_model, dim3(b), dim3(256), 0, c->st, n, c->vals2.as<uint32_t>(), model_view(c), model_view_of(c, B), K);
     count_launches(2);   // keys, gather (CUB's sort kernels are library code, not counted)
     CK(cudaGetLastError());
     c->cur = 1 - c->cur;
@@ -147,18 +159,18 @@ cudaError_t build_order(Ctx* c) {
     CK(ensure(c, c->chunk_off, (n + 1) * 4));
     CK(ensure(c, c->chunks, (size_t)n * 16));
     const int b = (int)((n + 255) / 256);
-    k_seg_flags<<<b, 256, 0, c->st>>>(n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>());
+    launch_pdl(k_seg_flags, dim3(b), dim3(256), 0, c->st, n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->scan.as<int32_t>(), (int)n, c->st);
     }));
     const int32_t* nseg_dev = c->scan.as<int32_t>() + n - 1;
-    k_seg_write<<<b, 256, 0, c->st>>>(n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>(),
+    launch_pdl(k_seg_write, dim3(b), dim3(256), 0, c->st, n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>(),
                                       c->scan.as<int32_t>(), c->seg_start.as<int32_t>(), c->seg_nodes.as<int32_t>());
-    k_chunk_count<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->flags.as<int32_t>());
+    launch_pdl(k_chunk_count, dim3(b), dim3(256), 0, c->st, n, nseg_dev, c->seg_start.as<int32_t>(), c->flags.as<int32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
       return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->chunk_off.as<int32_t>(), (int)n, c->st);
     }));
-    k_chunk_write<<<b, 256, 0, c->st>>>(n, nseg_dev, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
+    launch_pdl(k_chunk_write, dim3(b), dim3(256), 0, c->st, n, nseg_dev, c->seg_start.as<int32_t>(), c->chunk_off.as<int32_t>(),
                                         c->chunks.as<int4>(), c->nnz_dev.as<int64_t>());
     count_launches(4);   // flags, segment write, chunk count, chunk write (+ 2 CUB scans)
     CK(cudaGetLastError());
@@ -194,6 +206,8 @@ __device__ __forceinline__ void mark(unsigned long long* bm, int64_t W, int a, i
 // negative first id are padding (gathered shards)
 __global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup_host, int K, int m, int n_nbr,
                        const int32_t* nbr, int nf, const int32_t* fidx, unsigned long long* bm, int64_t W) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int P = K * (K + 1) / 2;
   const int64_t ntup = ntup_dev ? *ntup_dev : ntup_host;
   const int64_t ns = ntup * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P, total = ns + ne + nfp + m;
@@ -225,6 +239,8 @@ __global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup
 }
 
 __global__ void k_bitmap_or(int64_t words, int world, const unsigned long long* all, unsigned long long* bm) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long v = 0;
     for (int r = 0; r < world; ++r) v |= all[(int64_t)r * words + i];
@@ -234,6 +250,8 @@ __global__ void k_bitmap_or(int64_t words, int world, const unsigned long long* 
 
 // one warp per row: number of set bits (cnt[m] = 0 for the exclusive scan)
 __global__ void k_row_count(const unsigned long long* bm, int64_t W, int m, int32_t* cnt) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r > m) return;
@@ -248,6 +266,8 @@ __global__ void k_row_count(const unsigned long long* bm, int64_t W, int m, int3
 // one warp per row: columns in ascending order, row index of each entry, diagonal position
 __global__ void k_row_fill(unsigned long long* bm, int64_t W, int m, const int32_t* row_ptr, int32_t* col,
                            int32_t* row_of, int32_t* diag_pos) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= m) return;
@@ -293,6 +313,8 @@ __device__ __forceinline__ int find_entry(const int32_t* row_ptr, const int32_t*
 // upper_of: the (min, max) entry of each entry; lower_of[upper] = its mirror (-1 on the diagonal)
 __global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const int32_t* row_of, int m,
                               int32_t* upper_of, int32_t* lower_of) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t nnz = row_ptr[m];
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = row_of[e], cc = col[e];
@@ -312,6 +334,8 @@ __global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const 
 __global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr, int nf,
                         const int32_t* fidx, const int32_t* row_ptr, const int32_t* col, int32_t* seg_slot,
                         int32_t* edge_slot, int32_t* feat_slot, int64_t total) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   const int P = K * (K + 1) / 2;
@@ -343,12 +367,12 @@ cudaError_t build_pattern(Ctx* c) {
   c->bitmap_words = words;
   unsigned long long* bm = c->bitmap.as<unsigned long long>();
   const int grid = c->num_sms * 8;
-  k_mark<<<grid, 256, 0, c->st>>>(c->seg_nodes.as<int32_t>(), info + 1, 0, K, m, c->prm.n_nbr, c->nbr.as<int32_t>(),
+  launch_pdl(k_mark, dim3(grid), dim3(256), 0, c->st, c->seg_nodes.as<int32_t>(), info + 1, 0, K, m, c->prm.n_nbr, c->nbr.as<int32_t>(),
                                   c->nf, c->fidx.as<int32_t>(), bm, W);
   if (c->world > 1) {   // union over the ranks: all-gather the bitmaps and OR them (same pattern everywhere)
     CK(ensure(c, c->bitmap_all, (size_t)words * 8 * c->world));
     CK(nccl_allgather_u64(c, reinterpret_cast<const uint64_t*>(bm), c->bitmap_all.as<uint64_t>(), (size_t)words));
-    k_bitmap_or<<<grid, 256, 0, c->st>>>(words, c->world, c->bitmap_all.as<unsigned long long>(), bm);
+    launch_pdl(k_bitmap_or, dim3(grid), dim3(256), 0, c->st, words, c->world, c->bitmap_all.as<unsigned long long>(), bm);
   }
   count_launches(c->world > 1 ? 2 : 1);
   CK(ensure(c, c->row_cnt, (size_t)(m + 1) * 4));
@@ -356,7 +380,7 @@ cudaError_t build_pattern(Ctx* c) {
   CK(ensure(c, c->diag_pos, (size_t)m * 4));
   CK(ensure(c, c->part, 32 * 4));
   const int wb = (int)(((int64_t)(m + 1) * 32 + 255) / 256);
-  k_row_count<<<wb, 256, 0, c->st>>>(bm, W, m, c->row_cnt.as<int32_t>());
+  launch_pdl(k_row_count, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_cnt.as<int32_t>());
   CK(cub_call(c, [&](void* t, size_t& s) {
     return cub::DeviceScan::ExclusiveSum(t, s, c->row_cnt.as<int32_t>(), c->row_ptr.as<int32_t>(), m + 1, c->st);
   }));
@@ -380,12 +404,12 @@ cudaError_t build_pattern(Ctx* c) {
   c->cl_smem = (size_t)plan->smem;
   CK(ensure(c, c->col, nnz * 4 + 4)); CK(ensure(c, c->row_of, nnz * 4 + 4));
   CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
-  k_row_fill<<<wb, 256, 0, c->st>>>(bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(),
+  launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(),
                                     c->diag_pos.as<int32_t>());
   c->bitmap_clean = true;
   count_launches(1 + (nnz > 0) + (c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P > 0));
   if (nnz > 0)
-    k_upper_lower<<<(int)std::min<int64_t>(grid, (nnz + 255) / 256), 256, 0, c->st>>>(
+    launch_pdl(k_upper_lower, dim3((unsigned)std::min<int64_t>(grid, (nnz + 255) / 256)), dim3(256), 0, c->st,
         c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(), m, c->upper_of.as<int32_t>(),
         c->lower_of.as<int32_t>());
   if (c->cl_size > 0 && nnz > 0) {   // cluster PCG: per-rank SpMV pieces and halo lists for the frame
@@ -409,7 +433,7 @@ cudaError_t build_pattern(Ctx* c) {
   CK(ensure(c, c->edge_slot, ((int64_t)m * c->prm.n_nbr + 1) * 4));
   CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
   if (total > 0)
-    k_slots<<<(int)((total + 255) / 256), 256, 0, c->st>>>(c->nseg, c->seg_nodes.as<int32_t>(), K, m, c->prm.n_nbr,
+    launch_pdl(k_slots, dim3((int)((total + 255) / 256)), dim3(256), 0, c->st, c->nseg, c->seg_nodes.as<int32_t>(), K, m, c->prm.n_nbr,
                                                           c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(),
                                                           c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
                                                           c->seg_slot.as<int32_t>(), c->edge_slot.as<int32_t>(),
