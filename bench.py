@@ -157,19 +157,19 @@ def run_mis(args, rank, world, local_rank):
         M.mis_warp(ctx.ptr)
         return M.mis_fuse(ctx.ptr, rgb_d, 1)
 
-    # pinned host copies for the end-to-end leg
+    # End-to-end leg: the frame's inputs come from pinned host memory through the C-ABI (depth,
+    # colour, ORB matches, pose -- what a camera pipeline hands over every frame), the model and the
+    # deformation graph stay resident on the device (restored from the device snapshot, as in the
+    # device-timed step); the registration report (energies, counts) and the new model size are read
+    # back every step.
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
-    h = {k: pin(v) for k, v in st.items()}
-    g_h, nbr_h = pin(g_d), pin(nbr_d)
     depth_h, rgb_h, fs_h, fd_h = pin(depth_d), pin(rgb_d), pin(fs_d), pin(fd_d)
-    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in
-                    [h["xyz"], h["nrm"], h["rgb"], h["weight"], h["stamp"], h["ids"], h["knn_idx"], h["knn_w"],
-                     g_h, nbr_h, depth_h, rgb_h, fs_h, fd_h])
+    h2d_bytes = sum(int(t.numel() * t.element_size()) for t in [depth_h, rgb_h, fs_h, fd_h]) + 48
     rep_bytes = M.C.sizeof(M.mis_report)
 
     def step_e2e():
-        M.mis_set_model(ctx.ptr, h["xyz"], h["nrm"], h["rgb"], h["weight"], h["stamp"], h["ids"], capacity=cap)
-        M.mis_set_graph(ctx.ptr, g_h, nbr_h, h["knn_idx"], h["knn_w"])
+        M.mis_set_model(ctx.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
+        M.mis_set_graph(ctx.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
         rep = M.mis_register(ctx.ptr, depth_h, intr, pose, fs_h, fd_h, report=True)   # D2H of the report
         M.mis_warp(ctx.ptr)
         n_out, _ = M.mis_fuse(ctx.ptr, rgb_h, 1)
@@ -317,6 +317,7 @@ def run_mis(args, rank, world, local_rank):
                                    else (f"replicas x{world}" if world > 1 else "single"))},
         "gn_iters_per_s": round(value * cfg.gn_iters, 2),
         "e2e": {"value": round(jobs * Ke / (e2e_ms_max / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+                "inputs": "per frame from pinned host memory: depth, colour, ORB matches, pose; model resident",
                 "d2h_bytes_per_step": rep_bytes + 8, "steps": Ke},
         "roofline": roof,
         "roofline_k3": roof_k3,
