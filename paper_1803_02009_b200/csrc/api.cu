@@ -406,7 +406,7 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
                  &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->pcg_pptr, &c->pcg_pc, &c->pcg_push,
-                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->cub_tmp};
+                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->ulist, &c->cub_tmp};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -516,9 +516,11 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   TRY(c, ensure(c, c->Rt64, (size_t)m * 96));
   TRY(c, cudaMemcpyAsync(c->g.p, node_pos, (size_t)m * 12, kind_in(mem), c->st));
   if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, kind_in(mem), c->st));
-  TRY(c, ensure(c, c->nnz_dev, 64));
-  int* flag = reinterpret_cast<int*>(c->nnz_dev.as<int64_t>() + 3);   // validation flags (info[3])
-  TRY(c, cudaMemsetAsync(flag, 0, 8, c->st));
+  if (!c->nnz_dev.p) {
+    TRY(c, ensure(c, c->nnz_dev, 64));
+    TRY(c, cudaMemsetAsync(c->nnz_dev.p, 0, 64, c->st));
+  }
+  int* flag = reinterpret_cast<int*>(c->nnz_dev.as<int64_t>() + 3);   // validation flags (info[3], zero at rest)
   if (nn > 0) {
     ProfScope ps(c, P_IO, 1);
     launch_pdl(k_check_nbr, dim3(nb((int64_t)m * nn)), dim3(256), 0, c->st, m, nn, c->nbr.as<int32_t>(), flag);
@@ -549,6 +551,7 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
     TRY(c, cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, c->st));
     TRY(c, cudaStreamSynchronize(c->st));
     if (hflag) {
+      TRY(c, cudaMemsetAsync(flag, 0, 8, c->st));   // back to zero at rest
       c->have_graph = false;
       return fail(c, MIS_E_ARG, graph_flag_message(hflag));
     }
@@ -678,6 +681,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     ProfScope ps(c, P_REDUCE, 1);
     FinalArgs r;
     r.nnzb = c->nnzb;
+    r.nup = (c->nnzb - c->m) / 2;
+    r.ulist = c->ulist.as<int2>();
     r.m = c->m;
     r.upper_of = c->upper_of.as<int32_t>();
     r.lower_of = c->lower_of.as<int32_t>();

@@ -433,11 +433,13 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float* st = stage[wib];
   int64_t e = -1;
+  int lo = -1;   // the mirror entry (-1: diagonal)
   if (gw < r.m) {
     e = r.diag_pos[gw];
-  } else if (gw < r.m + r.nnzb) {
-    e = gw - r.m;
-    if (r.upper_of[e] != e || r.lower_of[e] < 0) return;   // mirrors and diagonals are written elsewhere
+  } else if (gw < r.m + r.nup) {   // off-diagonal upper entries from the per-frame work list
+    const int2 ul = r.ulist[gw - r.m];
+    e = ul.x;
+    lo = ul.y;
   }
   if (e >= 0) {
     st[lane] = r.acc.data[36 * e + lane];                  // D (36) | Mo (16) | G (36)
@@ -451,7 +453,6 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     r.acc.graph[36 * e + lane] = 0.f;
     if (lane < 4) r.acc.graph[36 * e + 32 + lane] = 0.f;
     __syncwarp();
-    const int lo = r.lower_of[e];
     const bool diag = lo < 0;
     for (int l = lane; l < 36; l += 32) {
       const int i = l / 6, j = l - 6 * (l / 6);
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     }
     return;
   }
-  const int64_t n = gw - r.m - r.nnzb;
+  const int64_t n = gw - r.m - r.nup;
   if (n == r.m) {   // energies -> report slot; zeroed (with K3's work counter) for the next assembly
     double* E = r.acc.energy;
     double tot[5];
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
 }
 
 void launch_finalize(const FinalArgs& r, cudaStream_t s) {
-  const int64_t warps = 2 * (int64_t)r.m + r.nnzb + 1;
+  const int64_t warps = 2 * (int64_t)r.m + r.nup + 1;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 0) launch_pdl(k_finalize, dim3((unsigned)blocks), dim3(256), 0, s, r);
 }

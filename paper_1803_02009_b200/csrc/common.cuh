@@ -129,6 +129,8 @@ __host__ __device__ inline int rec_stride(int K) { return (52 * (K * (K + 1) / 2
 
 struct FinalArgs {
   int64_t nnzb;
+  int64_t nup;                // off-diagonal upper entries ((nnzb - m) / 2)
+  const int2* ulist;          // nup x (entry, mirror)
   int m;
   const int32_t* upper_of;
   const int32_t* lower_of;    // upper entry -> its mirror (-1 on the diagonal)

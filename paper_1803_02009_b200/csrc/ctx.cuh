@@ -53,6 +53,7 @@ struct Ctx {
   int64_t nnzb = 0;
   bool pattern_valid = false;
   DBuf bitmap, bitmap_all, row_cnt, row_ptr, col, row_of, diag_pos, upper_of, lower_of, seg_slot, edge_slot, feat_slot;
+  DBuf ulist;   // int2 (entry, mirror) of every off-diagonal upper entry: the finalisation's work list
   bool bitmap_clean = false;   // pattern bitmap all-zero (cleared by k_row_fill) -> no memset
   int64_t bitmap_words = 0;
   DBuf nnz_dev;   // int64 info: [0] nnz, [1] nseg, [2] nchunk, [3] set_graph validation flags, [4..6] plan

@@ -149,7 +149,10 @@ cudaError_t build_order(Ctx* c) {
   ModelBufs& S = c->mb[c->cur];
   // segments and chunks, sized by the upper bound n; the counts stay on the device
   // (info[1], info[2]) and reach the host with the single readback of build_pattern
-  CK(ensure(c, c->nnz_dev, 64));
+  if (!c->nnz_dev.p) {
+    CK(ensure(c, c->nnz_dev, 64));
+    CK(cudaMemsetAsync(c->nnz_dev.p, 0, 64, c->st));   // zero at rest afterwards (flags cleared by k_row_fill)
+  }
   c->nseg = -1;
   c->nchunk = -1;
   if (n > 0) {
@@ -265,9 +268,10 @@ __global__ void k_row_count(const unsigned long long* bm, int64_t W, int m, int3
 
 // one warp per row: columns in ascending order, row index of each entry, diagonal position
 __global__ void k_row_fill(unsigned long long* bm, int64_t W, int m, const int32_t* row_ptr, int32_t* col,
-                           int32_t* row_of, int32_t* diag_pos) {
+                           int32_t* row_of, int32_t* diag_pos, int64_t* info) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x == 0) { info[3] = 0; info[7] = 0; }   // (read back already) flags, ulist count
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= m) return;
@@ -312,7 +316,7 @@ __device__ __forceinline__ int find_entry(const int32_t* row_ptr, const int32_t*
 
 // upper_of: the (min, max) entry of each entry; lower_of[upper] = its mirror (-1 on the diagonal)
 __global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const int32_t* row_of, int m,
-                              int32_t* upper_of, int32_t* lower_of) {
+                              int32_t* upper_of, int32_t* lower_of, int2* ulist, unsigned long long* ucount) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int64_t nnz = row_ptr[m];
@@ -323,7 +327,9 @@ __global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const 
       lower_of[e] = -1;
     } else if (r < cc) {
       upper_of[e] = (int32_t)e;
-      lower_of[e] = find_entry(row_ptr, col, cc, r);
+      const int lo = find_entry(row_ptr, col, cc, r);
+      lower_of[e] = lo;
+      ulist[atomicAdd(ucount, 1ull)] = make_int2((int)e, lo);   // the finalisation's off-diagonal work list
     } else {
       upper_of[e] = find_entry(row_ptr, col, cc, r);
     }
@@ -404,14 +410,15 @@ cudaError_t build_pattern(Ctx* c) {
   c->cl_smem = (size_t)plan->smem;
   CK(ensure(c, c->col, nnz * 4 + 4)); CK(ensure(c, c->row_of, nnz * 4 + 4));
   CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
-  launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(),
-                                    c->diag_pos.as<int32_t>());
+  CK(ensure(c, c->ulist, ((nnz - m) / 2 + 1) * 8));
+  launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
+             c->row_of.as<int32_t>(), c->diag_pos.as<int32_t>(), info);
   c->bitmap_clean = true;
   count_launches(1 + (nnz > 0) + (c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P > 0));
   if (nnz > 0)
     launch_pdl(k_upper_lower, dim3((unsigned)std::min<int64_t>(grid, (nnz + 255) / 256)), dim3(256), 0, c->st,
         c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(), m, c->upper_of.as<int32_t>(),
-        c->lower_of.as<int32_t>());
+        c->lower_of.as<int32_t>(), c->ulist.as<int2>(), reinterpret_cast<unsigned long long*>(info + 7));
   if (c->cl_size > 0 && nnz > 0) {   // cluster PCG: per-rank SpMV pieces and halo lists for the frame
     const int cs = c->cl_size, mr = c->cl_max_rows, mp = pcg_max_pieces(c->cl_max_rows, c->cl_max_nnz);
     CK(ensure(c, c->pcg_pptr, (size_t)cs * (mr + 1) * 4));

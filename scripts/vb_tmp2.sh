@@ -1,1 +1,1 @@
-bash scripts/ncu_kernel.sh k3g "k_guard_points" 5 1
+bash scripts/ncu_kernel.sh fin "k_finalize" 5 1
