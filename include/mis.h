@@ -10,12 +10,16 @@
  *  - mis_mem says where every pointer argument of the call lives:
  *    MIS_MEM_HOST (pageable or pinned host memory) or MIS_MEM_DEVICE (device
  *    memory of the context's GPU, e.g. a torch tensor's data_ptr()).  Device
- *    inputs are read in stream order on the context stream.
- *  - Ownership: the library copies every input into context-owned device
- *    memory (allocated with cudaMalloc on the context's device) and never
- *    retains a caller pointer after the call returns.  Outputs are written
- *    into caller buffers.  Calls with host outputs synchronise the context
- *    stream before returning; calls with device outputs do not.
+ *    inputs are read in stream order on the context stream: a device buffer
+ *    must stay valid until the work the call enqueued has run (as with any
+ *    asynchronous CUDA call; freeing it through the same stream is safe).
+ *  - Ownership: the library keeps its state in context-owned device memory
+ *    (allocated with cudaMalloc on the context's device) and never retains a
+ *    caller pointer after the enqueued work of the call has run (the depth
+ *    map and colours are read in place by the frame's kernels, everything
+ *    else is copied).  Outputs are written into caller buffers.  Calls with
+ *    host outputs synchronise the context stream before returning; calls with
+ *    device outputs do not.
  *  - Errors: every call returns a mis_status; no exception crosses the
  *    boundary.  mis_last_error() gives a human-readable message for the last
  *    failing call on that context.  Per-point degeneracies (z <= 0, invalid

@@ -64,7 +64,7 @@ FrameView frame_view(Ctx* c) {
   f.fx = c->intr.fx; f.fy = c->intr.fy; f.cx = c->intr.cx; f.cy = c->intr.cy;
   f.fxd = c->intr.fx; f.fyd = c->intr.fy; f.cxd = c->intr.cx; f.cyd = c->intr.cy;
   f.ifxd = 1.0 / f.fxd; f.ifyd = 1.0 / f.fyd;
-  f.depth = c->depth.as<float>();
+  f.depth = nullptr;   // only K1 reads the depth (the caller's buffer or its staged copy)
   f.nmap = c->nmap.as<float4>();
   f.nmapd = c->nmapd.as<double4>();
   for (int i = 0; i < 9; ++i) { f.R[i] = c->pose[i]; f.Rd[i] = c->pose[i]; }
@@ -210,16 +210,28 @@ __global__ void k_to_point_major(int64_t n, int K, int64_t cap, const int32_t* k
     if (w_pm) w_pm[i * K + s] = kw[s * cap + i];
   }
 }
-__global__ void k_check_nbr(int m, int n_nbr, int32_t* nbr, int* flag) {
+__global__ void k_copy2(int64_t n, const float* a, const float* b, float* a_out, float* b_out) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) { a_out[t] = a[t]; b_out[t] = b[t]; }
+}
+
+// mis_set_graph's inputs in one pass: node positions copied, neighbour lists copied and
+// validated (an invalid entry is flagged and neutralised so later kernels stay in bounds)
+__global__ void k_graph_in(int m, int n_nbr, const float* g_src, const int32_t* nbr_src, float* g, int32_t* nbr,
+                           int* flag) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < 3 * m) g[t] = g_src[t];
   if (t >= m * n_nbr) return;
-  const int l = nbr[t];
-  if (l < -1 || l >= m || l == t / n_nbr) {   // flagged, and neutralised so later kernels stay in bounds
+  int l = nbr_src[t];
+  if (l < -1 || l >= m || l == t / n_nbr) {
     atomicOr(flag, 8);
-    nbr[t] = -1;
+    l = -1;
   }
+  nbr[t] = l;
 }
 __global__ void k_init_nodes(int m, const float* g, double* Rt64, float* node32) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
@@ -514,16 +526,23 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   TRY(c, ensure(c, c->nbr, (size_t)m * (nn > 0 ? nn : 1) * 4));
   TRY(c, ensure(c, c->node32, (size_t)m * 64));
   TRY(c, ensure(c, c->Rt64, (size_t)m * 96));
-  TRY(c, cudaMemcpyAsync(c->g.p, node_pos, (size_t)m * 12, kind_in(mem), c->st));
-  if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, kind_in(mem), c->st));
+  const float* g_src = node_pos;            // device inputs are read in place by k_graph_in
+  const int32_t* nbr_src = node_nbr;
+  if (mem == MIS_MEM_HOST) {
+    TRY(c, cudaMemcpyAsync(c->g.p, node_pos, (size_t)m * 12, cudaMemcpyHostToDevice, c->st));
+    if (nn > 0) TRY(c, cudaMemcpyAsync(c->nbr.p, node_nbr, (size_t)m * nn * 4, cudaMemcpyHostToDevice, c->st));
+    g_src = c->g.as<float>();
+    nbr_src = c->nbr.as<int32_t>();
+  }
   if (!c->nnz_dev.p) {
     TRY(c, ensure(c, c->nnz_dev, 64));
     TRY(c, cudaMemsetAsync(c->nnz_dev.p, 0, 64, c->st));
   }
   int* flag = reinterpret_cast<int*>(c->nnz_dev.as<int64_t>() + 3);   // validation flags (info[3], zero at rest)
-  if (nn > 0) {
+  {
     ProfScope ps(c, P_IO, 1);
-    launch_pdl(k_check_nbr, dim3(nb((int64_t)m * nn)), dim3(256), 0, c->st, m, nn, c->nbr.as<int32_t>(), flag);
+    launch_pdl(k_graph_in, dim3(nb(std::max<int64_t>((int64_t)m * nn, 3 * (int64_t)m))), dim3(256), 0, c->st, m, nn,
+               g_src, nbr_src, c->g.as<float>(), c->nbr.as<int32_t>(), flag);
   }
   ModelView md = model_view(c);
   const int64_t n = c->n;
@@ -584,12 +603,18 @@ mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const m
   c->H = it->height;
   memcpy(c->pose, pose, 48);   // pose is host memory (12 floats) in every mode
   const size_t px = (size_t)c->W * c->H;
-  TRY(c, ensure(c, c->depth, px * 4));
+  const float* dsrc = depth_mm;   // device depth is read in place by K1 (stream order)
+  if (mem == MIS_MEM_HOST) {
+    TRY(c, ensure(c, c->depth, px * 4));
+    dsrc = c->depth.as<float>();
+  }
   TRY(c, ensure(c, c->nmap, px * 16));
   TRY(c, ensure(c, c->nmapd, px * 32));
-  TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, kind_in(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st));
   ProfScope ps(c, P_FRAME, 1);
-  launch_frame_prep(frame_view(c), c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
+  FrameView fv = frame_view(c);
+  fv.depth = dsrc;
+  launch_frame_prep(fv, c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
   TRY(c, cudaGetLastError());
   c->have_frame = true;
   return MIS_OK;
@@ -608,8 +633,14 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
   TRY(c, ensure(c, c->fidx, (size_t)n_feat * K * 4 + 16));
   TRY(c, ensure(c, c->fw, (size_t)n_feat * K * 4 + 16));
   if (n_feat > 0) {
-    TRY(c, cudaMemcpyAsync(c->fsrc.p, src, (size_t)n_feat * 12, kind_in(mem), c->st));
-    TRY(c, cudaMemcpyAsync(c->fdst.p, dst, (size_t)n_feat * 12, kind_in(mem), c->st));
+    if (mem == MIS_MEM_HOST) {
+      TRY(c, cudaMemcpyAsync(c->fsrc.p, src, (size_t)n_feat * 12, cudaMemcpyHostToDevice, c->st));
+      TRY(c, cudaMemcpyAsync(c->fdst.p, dst, (size_t)n_feat * 12, cudaMemcpyHostToDevice, c->st));
+    } else {   // both copies in one launch
+      ProfScope ps(c, P_IO, 1);
+      launch_pdl(k_copy2, dim3(nb(3 * (int64_t)n_feat)), dim3(256), 0, c->st, 3 * (int64_t)n_feat, src, dst,
+                 c->fsrc.as<float>(), c->fdst.as<float>());
+    }
     const float* s = c->fsrc.as<float>();
     ProfScope ps(c, P_SKIN, 1);
     TRY(c, skin(c, n_feat, s, s + 1, s + 2, 3, c->fidx.as<int32_t>(), c->fw.as<float>(), n_feat));
@@ -1010,10 +1041,10 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   cudaSetDevice(c->device);
   if (c->dirty) TRY(c, run_build_order(c));
   const size_t px = (size_t)c->W * c->H;
-  const float* rgb_dev = nullptr;
-  if (rgb) {
+  const float* rgb_dev = rgb;   // device colours are read in place by K11 / K12 (stream order)
+  if (rgb && mem == MIS_MEM_HOST) {
     TRY(c, ensure(c, c->rgb_obs, px * 12));
-    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, kind_in(mem), c->st));
+    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, cudaMemcpyHostToDevice, c->st));
     rgb_dev = c->rgb_obs.as<float>();
   }
   mis_status s;

@@ -118,13 +118,13 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
     if (fu >= 0 && fv >= 0 && fu < f.W && fv < f.H) {
       why |= 2;
       const int px = (int)fu, py = (int)fv;
-      const float D = f.depth[py * f.W + px];
+      const double D = f.nmapd[py * f.W + px].w;   // the depth (0: invalid), from K1
       double N[3], q[3];
-      if (dok(D)) {
+      if (D > 0) {
         why |= 4;
         if (normal_map64(f, px, py, N, q)) {
           why |= 8;
-          const double dz = fabs(vt[2] - (double)D);
+          const double dz = fabs(vt[2] - D);
           if (dz < a.tz) {
             why |= 16;
             if (nt[0] * N[0] + nt[1] * N[1] + nt[2] * N[2] > a.cos_delta) {
