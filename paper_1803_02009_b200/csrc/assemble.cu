@@ -420,28 +420,35 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
 // Finalisation of the normal equations from the accumulators (so the
 // latency-bound solver only streams its rows): warps [0, m) the diagonal blocks
 // -- first, so their block-Jacobi inverses (K7) overlap the rest --, then one
-// warp per off-diagonal upper entry, then one per node, then one for the
+// warp per kFB off-diagonal upper entries, then one per kFB nodes, then one for the
 // energies (report slot).  Every accumulator is re-zeroed after it is read, so
 // the next assembly needs no memset:
 //   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j)),
 //   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
+constexpr int kFB = 4;   // off-diagonal entries / nodes per warp (their loads overlap)
+
+// one 6x6 block from its staged D | Mo | G (88 floats): H entries (and the mirror's)
+__device__ __forceinline__ void final_block(const FinalArgs& r, const float* st, float* hst, int64_t e, int lo, int lane) {
+  const bool diag = lo < 0;
+  for (int l = lane; l < 36; l += 32) {
+    const int i = l / 6, j = l - 6 * (l / 6);
+    const float h = block_entry(st, st + 36, st + 52, diag, i, j, r.w_data, r.w_pt);
+    r.Hval[36 * e + l] = h;
+    if (!diag) r.Hval[36 * (int64_t)lo + 6 * j + i] = h;
+    if (hst) hst[l] = h;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
-  __shared__ float stage[8][124];
-  pdl_wait();   // K3a/K3b/K4 accumulators
+  __shared__ float stage[8][kFB][124];
+  pdl_wait();      // K3a/K3b/K4 accumulators
   pdl_trigger();   // the solver may launch (it waits for this grid's completion before reading)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float* st = stage[wib];
-  int64_t e = -1;
-  int lo = -1;   // the mirror entry (-1: diagonal)
-  if (gw < r.m) {
-    e = r.diag_pos[gw];
-  } else if (gw < r.m + r.nup) {   // off-diagonal upper entries from the per-frame work list
-    const int2 ul = r.ulist[gw - r.m];
-    e = ul.x;
-    lo = ul.y;
-  }
-  if (e >= 0) {
+  const int64_t n_off = (r.nup + kFB - 1) / kFB, n_nod = (r.m + kFB - 1) / kFB;
+  if (gw < r.m) {   // diagonal block of node gw, then its block-Jacobi inverse
+    float* st = stage[wib][0];
+    const int64_t e = r.diag_pos[gw];
     st[lane] = r.acc.data[36 * e + lane];                  // D (36) | Mo (16) | G (36)
     if (lane < 4) st[32 + lane] = r.acc.data[36 * e + 32 + lane];
     if (lane < 16) st[36 + lane] = r.acc.mom[16 * e + lane];
@@ -453,16 +460,9 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     r.acc.graph[36 * e + lane] = 0.f;
     if (lane < 4) r.acc.graph[36 * e + 32 + lane] = 0.f;
     __syncwarp();
-    const bool diag = lo < 0;
-    for (int l = lane; l < 36; l += 32) {
-      const int i = l / 6, j = l - 6 * (l / 6);
-      const float h = block_entry(st, st + 36, st + 52, diag, i, j, r.w_data, r.w_pt);
-      r.Hval[36 * e + l] = h;
-      if (!diag) r.Hval[36 * (int64_t)lo + 6 * j + i] = h;
-      st[88 + l] = h;
-    }
-    if (diag && r.Minv) {   // block-Jacobi inverse of this node (K7), off the solver's critical path:
-      __syncwarp();         // fp64 Gauss-Jordan, lane rr < 6 holds row rr of [H + (lambda + mu) I | I]
+    final_block(r, st, st + 88, e, -1, lane);
+    if (r.Minv) {   // block-Jacobi inverse of this node (K7), off the solver's critical path:
+      __syncwarp();   // fp64 Gauss-Jordan, lane rr < 6 holds row rr of [H + (lambda + mu) I | I]
       const int64_t row_j = gw;
       const int rr = lane < 6 ? lane : 0;
       double trc = 0.0;
@@ -493,19 +493,105 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     }
     return;
   }
-  const int64_t n = gw - r.m - r.nup;
-  if (n == r.m) {   // energies -> report slot; zeroed (with K3's work counter) for the next assembly
+  int64_t g2 = gw - r.m;
+  if (g2 < n_off) {   // kFB off-diagonal upper entries from the per-frame work list, loads first
+    int64_t e[kFB];
+    int lo[kFB];
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      const int64_t idx = g2 * kFB + q;
+      e[q] = -1;
+      lo[q] = -1;
+      if (idx < r.nup) {
+        const int2 ul = r.ulist[idx];
+        e[q] = ul.x;
+        lo[q] = ul.y;
+      }
+    }
+    float v[kFB][5];
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      if (e[q] < 0) continue;
+      const int64_t E = e[q];
+      v[q][0] = r.acc.data[36 * E + lane];
+      v[q][1] = lane < 4 ? r.acc.data[36 * E + 32 + lane] : 0.f;
+      v[q][2] = lane < 16 ? r.acc.mom[16 * E + lane] : 0.f;
+      v[q][3] = r.acc.graph[36 * E + lane];
+      v[q][4] = lane < 4 ? r.acc.graph[36 * E + 32 + lane] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      if (e[q] < 0) continue;
+      const int64_t E = e[q];
+      float* st = stage[wib][q];
+      st[lane] = v[q][0];
+      if (lane < 4) st[32 + lane] = v[q][1];
+      if (lane < 16) st[36 + lane] = v[q][2];
+      st[52 + lane] = v[q][3];
+      if (lane < 4) st[84 + lane] = v[q][4];
+      r.acc.data[36 * E + lane] = 0.f;
+      if (lane < 4) r.acc.data[36 * E + 32 + lane] = 0.f;
+      if (lane < 16) r.acc.mom[16 * E + lane] = 0.f;
+      r.acc.graph[36 * E + lane] = 0.f;
+      if (lane < 4) r.acc.graph[36 * E + 32 + lane] = 0.f;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kFB; ++q)
+      if (e[q] >= 0) final_block(r, stage[wib][q], nullptr, e[q], lo[q], lane);
+    return;
+  }
+  g2 -= n_off;
+  if (g2 < n_nod) {   // kFB nodes: b = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs
+    float v[kFB], gv[kFB];
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      const int64_t n = g2 * kFB + q;
+      v[q] = 0.f;
+      gv[q] = 0.f;
+      if (n >= r.m) continue;
+      if (lane < 6) { v[q] = r.acc.rhs_data[6 * n + lane]; gv[q] = r.acc.rhs_graph[6 * n + lane]; }
+      else if (lane < 18) v[q] = r.acc.node_mom[12 * n + lane - 6];
+    }
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      const int64_t n = g2 * kFB + q;
+      if (n >= r.m) continue;
+      float* st = stage[wib][q];
+      if (lane < 18) st[lane] = v[q];
+      if (lane < 6) { r.acc.rhs_data[6 * n + lane] = 0.f; r.acc.rhs_graph[6 * n + lane] = 0.f; }
+      else if (lane < 18) r.acc.node_mom[12 * n + lane - 6] = 0.f;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kFB; ++q) {
+      const int64_t n = g2 * kFB + q;
+      if (n >= r.m || lane >= 6) continue;
+      const float* st = stage[wib][q];
+      const float* Nm = st + 6;
+      float pt;
+      if (lane < 3) {
+        const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
+        pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
+      } else {
+        pt = Nm[9 + (lane - 3)];
+      }
+      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + gv[q];
+    }
+    return;
+  }
+  if (g2 == n_nod) {   // energies -> report slot; zeroed (with K3's work counter) for the next assembly
     double* E = r.acc.energy;
     double tot[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {   // striped partials: lane l sums stripes l, l + 32
       double* st_q = E + 8 + kEnergyStripes * q;
-      double v = st_q[lane] + st_q[lane + 32];
+      double vv = st_q[lane] + st_q[lane + 32];
       st_q[lane] = 0.0;
       st_q[lane + 32] = 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      tot[q] = E[q] + v;
+      for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
+      tot[q] = E[q] + vv;
     }
     if (lane == 0) {
       if (r.slot >= 0) {
@@ -518,30 +604,11 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
       }
       for (int q = 0; q < 8; ++q) E[q] = 0.0;
     }
-    return;
-  }
-  if (n > r.m) return;
-  if (lane < 6) st[lane] = r.acc.rhs_data[6 * n + lane];   // 6 rhs_data | 12 node moments
-  else if (lane < 18) st[lane] = r.acc.node_mom[12 * n + lane - 6];
-  if (lane < 6) { r.acc.rhs_data[6 * n + lane] = 0.f; }
-  else if (lane < 18) r.acc.node_mom[12 * n + lane - 6] = 0.f;
-  __syncwarp();
-  if (lane < 6) {
-    const float* Nm = st + 6;
-    float pt;
-    if (lane < 3) {
-      const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
-      pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
-    } else {
-      pt = Nm[9 + (lane - 3)];
-    }
-    r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + r.acc.rhs_graph[6 * n + lane];
-    r.acc.rhs_graph[6 * n + lane] = 0.f;
   }
 }
 
 void launch_finalize(const FinalArgs& r, cudaStream_t s) {
-  const int64_t warps = 2 * (int64_t)r.m + r.nup + 1;
+  const int64_t warps = (int64_t)r.m + (r.nup + kFB - 1) / kFB + (r.m + kFB - 1) / kFB + 1;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 0) launch_pdl(k_finalize, dim3((unsigned)blocks), dim3(256), 0, s, r);
 }
