@@ -35,7 +35,7 @@ constexpr int kPiece = 4;         // SpMV work unit: <= kPiece consecutive block
 __host__ __device__ inline int max_pieces(int max_rows, int max_nnz) { return max_nnz / kPiece + max_rows + 1; }
 
 struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
-  size_t dots, vec, zf, mi, col, own, pptr, pc, part, push, h, total;
+  size_t dots, vec, zf, mi, col, own, pptr, pc, part, push, rt, h, total;
   __host__ __device__ CLay(int max_rows, int max_nnz, int m) {
     dots = 0;                                        // double partA..partE[16], red[64]
     vec = dots + sizeof(double) * (5 * kMaxCluster + 64);
@@ -48,7 +48,8 @@ struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
     pc = pptr + sizeof(int) * (max_rows + 1);        // pieces: first block | count << 24
     part = pc + sizeof(int) * max_pieces(max_rows, max_nnz);   // 6 partial sums per piece
     push = part + sizeof(float) * 6 * max_pieces(max_rows, max_nnz);   // (destination CTA << 16 | local row)
-    h = (push + sizeof(int) * (size_t)max_rows * kMaxCluster + 15) & ~(size_t)15;
+    rt = (push + sizeof(int) * (size_t)max_rows * kMaxCluster + 15) & ~(size_t)15;   // own nodes' fp64 state
+    h = rt + sizeof(double) * 12 * (size_t)max_rows;
     total = h + sizeof(float) * 36 * (size_t)max_nnz;
   }
 };
@@ -438,7 +439,12 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[0] = gtimer();
 
   // ---- phase 0: local rows of H (from the accumulators), b, column owners
-  // lists of this rank (built once per frame), columns, b, block inverses
+  // lists of this rank (built once per frame), columns, b, block inverses, own node states
+  {
+    double* rt = reinterpret_cast<double*>(sm + L.rt);
+    for (int q = t; q < 12 * nr; q += kCT) rt[q] = a.nd.Rt64[12 * (int64_t)r0 + q];
+  }
+  const int sticky = *a.numeric_flag;   // set by an earlier launch of this registration
   const int max_pc = max_pieces(a.max_rows, a.max_nnz);
   const int32_t* g_pptr = a.pptr + (int64_t)rank * (a.max_rows + 1);
   for (int i = t; i <= nr; i += kCT) pptr[i] = g_pptr[i];
@@ -555,19 +561,23 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     return;
   }
   // ---- node update; a non-finite step anywhere rolls the whole update back
-  double bad = 0.0;
+  bool bad = false;
   for (int q = t; q < 6 * nr; q += kCT)
-    if (!isfinite(x[q])) bad = 1.0;
-  cta_publish(cl, bad, red, partF, rank, cs);
+    if (!isfinite(x[q])) bad = true;
+  const int bad_cta = __syncthreads_or(bad);
+  int* bflag = reinterpret_cast<int*>(partF);   // one int per CTA
+  if (t < cs) cl.map_shared_rank(bflag, t)[rank] = bad_cta;
   cl.sync();
-  if (gather_sum(partF, cs) != 0.0) {
+  const bool any_bad = __any_sync(0xffffffffu, (t & 31) < cs && bflag[t & 31] != 0);
+  if (any_bad) {
     if (rank == 0 && t == 0) atomicOr(a.numeric_flag, 1);
     return;
   }
-  if (*a.numeric_flag) return;   // sticky from an earlier iteration
-  for (int i = t; i < nr; i += kCT) {
-    const int j = r0 + i;
-    node_update(x + 6 * i, a.nd.Rt64 + 12 * (int64_t)j, a.nd.node32 + 16 * (int64_t)j);
+  if (sticky) return;   // a numeric failure earlier in this registration
+  const double* rt = reinterpret_cast<const double*>(sm + L.rt);
+  for (int q = t; q < 3 * nr; q += kCT) {   // 3 threads per node, one row of R each
+    const int i = q / 3, rw = q - 3 * i, j = r0 + i;
+    node_update_row(x + 6 * i, rt + 12 * i, rw, a.nd.Rt64 + 12 * (int64_t)j, a.nd.node32 + 16 * (int64_t)j);
   }
   if (stamp) ts[5] = gtimer();
 }

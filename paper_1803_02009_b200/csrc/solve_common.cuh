@@ -164,6 +164,35 @@ __device__ inline void precond_block(const float* Hjj, float lambda, float* Mi) 
   for (int i = 0; i < 36; ++i) Mi[i] = (float)Ai[i];
 }
 
+// Row r of R_j <- Exp(dtheta) R_j and t_j[r] += dt[r] (the update split over 3 threads per node);
+// Rt: the node's current fp64 state (R row-major, t), out to the fp64 master and the fp32 copy
+__device__ inline void node_update_row(const float* dx, const double* Rt, int r, double* Rt_out, float* n32) {
+  const double w0 = dx[0], w1 = dx[1], w2 = dx[2];
+  const double t2 = w0 * w0 + w1 * w1 + w2 * w2, th = sqrt(t2);
+  double A, Bc;
+  if (th < 0.05) {   // Taylor series of sin(th)/th and (1 - cos th)/th^2: truncation < 1e-20 here
+    A = 1.0 + t2 * (-1.0 / 6 + t2 * (1.0 / 120 + t2 * (-1.0 / 5040 + t2 * (1.0 / 362880))));
+    Bc = 0.5 + t2 * (-1.0 / 24 + t2 * (1.0 / 720 + t2 * (-1.0 / 40320 + t2 * (1.0 / 3628800))));
+  } else {
+    A = sin(th) / th;
+    Bc = (1.0 - cos(th)) / t2;
+  }
+  const double K[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+  double E[3];
+  for (int jj = 0; jj < 3; ++jj) {
+    const double k2 = K[3 * r] * K[jj] + K[3 * r + 1] * K[3 + jj] + K[3 * r + 2] * K[6 + jj];
+    E[jj] = (r == jj ? 1.0 : 0.0) + A * K[3 * r + jj] + Bc * k2;
+  }
+  for (int jj = 0; jj < 3; ++jj) {
+    const double v = E[0] * Rt[jj] + E[1] * Rt[3 + jj] + E[2] * Rt[6 + jj];
+    Rt_out[3 * r + jj] = v;
+    n32[3 * r + jj] = (float)v;
+  }
+  const double tv = Rt[9 + r] + (double)dx[3 + r];
+  Rt_out[9 + r] = tv;
+  n32[9 + r] = (float)tv;
+}
+
 // R_j <- Exp(dtheta) R_j (Rodrigues; series coefficients for small theta), t_j += dt (reading A18)
 __device__ inline void node_update(const float* dx, double* Rt, float* n32) {
   const double w0 = dx[0], w1 = dx[1], w2 = dx[2];
