@@ -417,6 +417,221 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
   pdl_trigger();
 }
 
+// ---------------------------------------------------------------- K3b on tensor cores (k <= 4)
+// The same per-chunk sums as k_accum_points, as two small GEMMs per 8-point step on the tensor
+// cores: C_c += F_c^T F_c (c' block, 32 x 32 padded) and C_e += F_e^T F_e (e' block, 32 x 24),
+// mma.sync m16n8k8 TF32 with the 3xTF32 split (a = a_hi + a_lo; a_hi b_hi + a_hi b_lo + a_lo b_hi,
+// FP32 accumulation): products to ~2^-21 relative, as accurate as the FP32 FMA path for these
+// sums, at a fraction of its issue slots.  Only the upper-triangle tiles are computed (10 of 14).
+constexpr int kTcFSP = 72;   // row stride: c' [0, 32) | e' [32, 64) | pad; 72 = 8 (mod 32): conflict-free
+
+template <int K>
+__device__ __forceinline__ void build_row_tc(const PState<K>& st, float* row) {
+  const float4 nn = st.nn;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const float4 wa = st.wa[s];   // (w a, w)
+    row[6 * s + 0] = wa.y * nn.z - wa.z * nn.y;   // w_j (a_j x n')
+    row[6 * s + 1] = wa.z * nn.x - wa.x * nn.z;
+    row[6 * s + 2] = wa.x * nn.y - wa.y * nn.x;
+    row[6 * s + 3] = wa.w * nn.x;                 // w_j n'
+    row[6 * s + 4] = wa.w * nn.y;
+    row[6 * s + 5] = wa.w * nn.z;
+    *reinterpret_cast<float4*>(row + 32 + 4 * s) = wa;
+  }
+  row[6 * K] = st.rr.w;
+#pragma unroll
+  for (int q = 6 * K + 1; q < 32; ++q) row[q] = 0.f;
+  row[32 + 4 * K + 0] = st.rr.x;
+  row[32 + 4 * K + 1] = st.rr.y;
+  row[32 + 4 * K + 2] = st.rr.z;
+#pragma unroll
+  for (int q = 32 + 4 * K + 3; q < 64; ++q) row[q] = 0.f;
+}
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};\n"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// A fragments (hi, lo) of F^T for the two 16-row tiles of one block (column base cb), k-step k0
+struct FragT {
+  uint32_t h[2][4], l[2][4];
+};
+__device__ __forceinline__ void load_frag(const float* F, int k0, int cb, int g, int tig, FragT& f) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+    const float x[4] = {F[(k0 + tig) * kTcFSP + cb + 16 * mi + g], F[(k0 + tig) * kTcFSP + cb + 16 * mi + g + 8],
+                        F[(k0 + tig + 4) * kTcFSP + cb + 16 * mi + g],
+                        F[(k0 + tig + 4) * kTcFSP + cb + 16 * mi + g + 8]};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      f.h[mi][q] = to_tf32(x[q]);
+      f.l[mi][q] = to_tf32(x[q] - __uint_as_float(f.h[mi][q]));
+    }
+  }
+}
+
+// tile (mi, ni): the B fragment of n8-tile ni is part of the A fragment of m16-tile ni / 2
+__device__ __forceinline__ void mma3(float (&d)[4], const FragT& f, int mi, int ni) {
+  const int bm = ni >> 1, bq = ni & 1;
+  const uint32_t bh0 = f.h[bm][bq], bh1 = f.h[bm][bq + 2], bl0 = f.l[bm][bq], bl1 = f.l[bm][bq + 2];
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], bh0, bh1);
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], bl0, bl1);
+  mma_tf32(d, f.l[mi][0], f.l[mi][1], f.l[mi][2], f.l[mi][3], bh0, bh1);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(AsmPointsArgs a) {
+  static_assert(6 * K + 1 <= 32 && 4 * K + 3 <= 24, "tensor-core K3b: k <= 4");
+  constexpr int P = K * (K + 1) / 2;
+  constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
+  extern __shared__ float4 smem4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  float* F = reinterpret_cast<float*>(smem4) + warp * (32 * kTcFSP);
+  __shared__ int32_t slot_sm[kWarps][P];
+  int32_t* slots = slot_sm[warp];
+  // record permutation: perm[d] = index in the dumped sums (c' 32 x 32 at 0, e' 32 x 24 at 1024), -1: zero
+  __shared__ int16_t perm[RS];
+  for (int d = threadIdx.x; d < RS; d += blockDim.x) perm[d] = -1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < 32 * 32 + 24 * 24; q += blockDim.x) {
+    const bool e = q >= 1024;
+    const int A = e ? (q - 1024) / 24 : q / 32, B = e ? (q - 1024) % 24 : q % 32;
+    if (A > B) continue;
+    int d = -1;
+    if (!e) {                    // c' = [w_j u_j ..., r_pl]
+      if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
+      else if (B == 6 * K && A < 6 * K) d = 52 * P + 18 * (A / 6) + (A % 6);
+    } else {                     // e' = [w_j a_j, w_j ..., r']
+      if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
+      else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 18 * (A / 4) + 6 + 3 * (A % 4) + (B - 4 * K);
+    }
+    if (d >= 0) perm[d] = (int16_t)(e ? 1024 + A * 24 + B : A * 32 + B);
+  }
+  __syncthreads();
+
+  pdl_wait();   // K3a's factor state (the tables above are independent of it)
+  int64_t c = 0;
+  if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  const float4* ps = a.pstate;
+  const int64_t S = a.pstride;
+  for (; c < a.nchunk;) {
+    const int4 ch = a.chunks[c];
+    const int seg = ch.x;
+    const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
+    __syncwarp();
+    for (int q = lane; q < P; q += 32) slots[q] = a.seg_slot[(int64_t)seg * P + q];
+    float dc[6][4], de[4][4];   // c' tiles (0,0..3),(1,2),(1,3); e' tiles (0,0..2),(1,2)
+#pragma unroll
+    for (int t = 0; t < 6; ++t) dc[t][0] = dc[t][1] = dc[t][2] = dc[t][3] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) de[t][0] = de[t][1] = de[t][2] = de[t][3] = 0.f;
+    for (int base = ch.y; base < ch.z; base += 32) {
+      const int64_t i = base + lane;
+      float* row = F + lane * kTcFSP;
+      PState<K> st;
+      if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point or past the chunk)
+#pragma unroll
+        for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+        st.rr = ps[K * S + i];
+        st.nn = ps[(K + 1) * S + i];
+      } else {
+#pragma unroll
+        for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        st.rr = st.nn = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      build_row_tc<K>(st, row);
+      __syncwarp();
+      const int np = min(32, ch.z - base);
+      for (int k0 = 0; k0 < np; k0 += 8) {
+        FragT f;
+        load_frag(F, k0, 0, g, tig, f);   // c'
+        mma3(dc[0], f, 0, 0);
+        mma3(dc[1], f, 0, 1);
+        mma3(dc[2], f, 0, 2);
+        mma3(dc[3], f, 0, 3);
+        mma3(dc[4], f, 1, 2);
+        mma3(dc[5], f, 1, 3);
+        load_frag(F, k0, 32, g, tig, f);   // e'
+        mma3(de[0], f, 0, 0);
+        mma3(de[1], f, 0, 1);
+        mma3(de[2], f, 0, 2);
+        mma3(de[3], f, 1, 2);
+      }
+      __syncwarp();
+    }
+    // ---- commit: fragments -> shared memory -> atomic adds into the BSR accumulators
+    {
+      const int tmi[6] = {0, 0, 0, 0, 1, 1}, tni[6] = {0, 1, 2, 3, 2, 3};
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const int r0 = 16 * tmi[t] + g, c0 = 8 * tni[t] + 2 * tig;
+        F[r0 * 32 + c0] = dc[t][0];
+        F[r0 * 32 + c0 + 1] = dc[t][1];
+        F[(r0 + 8) * 32 + c0] = dc[t][2];
+        F[(r0 + 8) * 32 + c0 + 1] = dc[t][3];
+      }
+      const int emi[4] = {0, 0, 0, 1}, eni[4] = {0, 1, 2, 2};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int r0 = 16 * emi[t] + g, c0 = 8 * eni[t] + 2 * tig;
+        if (r0 < 24) {
+          F[1024 + r0 * 24 + c0] = de[t][0];
+          F[1024 + r0 * 24 + c0 + 1] = de[t][1];
+        }
+        if (r0 + 8 < 24) {
+          F[1024 + (r0 + 8) * 24 + c0] = de[t][2];
+          F[1024 + (r0 + 8) * 24 + c0 + 1] = de[t][3];
+        }
+      }
+    }
+    __syncwarp();
+    int64_t next_chunk = 0;
+    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
+    auto rv = [&](int d) -> float {
+      const int q = perm[d];
+      return q < 0 ? 0.f : F[q];
+    };
+    for (int it = lane; it < 13 * P + 6 * K; it += 32) {
+      if (it < 13 * P) {
+        const int pr = it / 13, q = it - 13 * pr;
+        const int d0 = 52 * pr + 4 * q;   // data (q < 9) then moments: contiguous in the record
+        const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+        const int64_t u = slots[pr];
+        float* dst = q < 9 ? a.acc.data + 36 * u + 4 * q : a.acc.mom + 16 * u + 4 * (q - 9);
+        atomicAdd(reinterpret_cast<float4*>(dst), v);
+      } else {
+        const int t2 = it - 13 * P, sl = t2 / 6, q = t2 - 6 * sl;
+        const int64_t nd = nodes[sl];
+        if (q < 3) {
+          const int d0 = 52 * P + 18 * sl + 2 * q;
+          const float2 v = make_float2(rv(d0), rv(d0 + 1));
+          if (v.x != 0.f || v.y != 0.f) atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * nd + 2 * q), v);
+        } else {
+          const int d0 = 52 * P + 18 * sl + 6 + 4 * (q - 3);
+          const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+            atomicAdd(reinterpret_cast<float4*>(a.acc.node_mom + 12 * nd + 4 * (q - 3)), v);
+        }
+      }
+    }
+    c = __shfl_sync(0xffffffffu, next_chunk, 0);
+  }
+  pdl_trigger();
+}
+
 // Finalisation of the normal equations from the accumulators (so the
 // latency-bound solver only streams its rows): warps [0, m) the diagonal blocks
 // -- first, so their block-Jacobi inverses (K7) overlap the rest --, then one
@@ -630,12 +845,18 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
   else launch_pdl(k_assoc_points<K, false>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
 }
 
+#ifndef MIS_K3B_TC
+#define MIS_K3B_TC 1   // 0: the FP32 FMA path for every k
+#endif
 template <int K>
 static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
   using L = Lay<K>;
   if (a.nchunk <= 0) return;
-  const size_t smem = sizeof(float) * kWarps * 32 * L::FSP;
-  auto kern = k_accum_points<K>;
+  constexpr bool tc = MIS_K3B_TC && K <= 4;   // tensor-core SYRK for k <= 4, FP32 tiles above
+  const size_t smem = sizeof(float) * kWarps * 32 * (tc ? kTcFSP : L::FSP);
+  void (*kern)(AsmPointsArgs);
+  if constexpr (tc) kern = k_accum_points_tc<(K <= 4 ? K : 4)>;
+  else kern = k_accum_points<K>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
