@@ -449,11 +449,11 @@ __device__ __forceinline__ void build_row_tc(const PState<K>& st, float* row) {
   for (int q = 32 + 4 * K + 3; q < 64; ++q) row[q] = 0.f;
 }
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
+// 3xTF32 split by truncation: hi = x with the 13 low mantissa bits cleared (what the
+// tensor core reads of a TF32 operand), lo = x - hi exactly (the tensor core truncates
+// lo in turn).  Two integer/FP ops per element; cvt.rna.tf32.f32 costs ~6 on sm_100.
+// Dropped terms: lo lo' and the truncation of lo, both < 2^-20 relative per product.
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -463,9 +463,12 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// A fragments (hi, lo) of F^T for the two 16-row tiles of one block (column base cb), k-step k0
+// A fragments (hi, lo) of F^T for the two 16-row tiles of one block (column base cb), k-step k0,
+// and the B fragments of the four n8 tiles (pairs (a0, a2) / (a1, a3) of the A quads, kept as
+// their own registers so each mma reads aligned pairs without per-tile moves)
 struct FragT {
   uint32_t h[2][4], l[2][4];
+  uint32_t bh[4][2], bl[4][2];
 };
 __device__ __forceinline__ void load_frag(const float* F, int k0, int cb, int g, int tig, FragT& f) {
 #pragma unroll
@@ -475,19 +478,24 @@ __device__ __forceinline__ void load_frag(const float* F, int k0, int cb, int g,
                         F[(k0 + tig + 4) * kTcFSP + cb + 16 * mi + g + 8]};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      f.h[mi][q] = to_tf32(x[q]);
-      f.l[mi][q] = to_tf32(x[q] - __uint_as_float(f.h[mi][q]));
+      f.h[mi][q] = tf32_hi(x[q]);
+      f.l[mi][q] = __float_as_uint(x[q] - __uint_as_float(f.h[mi][q]));
+    }
+#pragma unroll
+    for (int bq = 0; bq < 2; ++bq) {
+      f.bh[2 * mi + bq][0] = f.h[mi][bq];
+      f.bh[2 * mi + bq][1] = f.h[mi][bq + 2];
+      f.bl[2 * mi + bq][0] = f.l[mi][bq];
+      f.bl[2 * mi + bq][1] = f.l[mi][bq + 2];
     }
   }
 }
 
 // tile (mi, ni): the B fragment of n8-tile ni is part of the A fragment of m16-tile ni / 2
 __device__ __forceinline__ void mma3(float (&d)[4], const FragT& f, int mi, int ni) {
-  const int bm = ni >> 1, bq = ni & 1;
-  const uint32_t bh0 = f.h[bm][bq], bh1 = f.h[bm][bq + 2], bl0 = f.l[bm][bq], bl1 = f.l[bm][bq + 2];
-  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], bh0, bh1);
-  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], bl0, bl1);
-  mma_tf32(d, f.l[mi][0], f.l[mi][1], f.l[mi][2], f.l[mi][3], bh0, bh1);
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], f.bh[ni][0], f.bh[ni][1]);
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], f.bl[ni][0], f.bl[ni][1]);
+  mma_tf32(d, f.l[mi][0], f.l[mi][1], f.l[mi][2], f.l[mi][3], f.bh[ni][0], f.bh[ni][1]);
 }
 
 template <int K>

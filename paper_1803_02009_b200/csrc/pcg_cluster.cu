@@ -195,89 +195,107 @@ __device__ __forceinline__ double gather_sum(const double* slot, int cs) {
 
 
 // The SpMV's H operand lives in registers: thread t owns work units t, t + kCT,
-// ..., t + (kU-1) kCT, each <= kPiece blocks x 6 entries of one block row,
+// ..., t + (kU-1) kCT, each <= kPiece blocks x kCU block rows (half of each 6x6 block),
 // loaded once per solve.  Streaming H from shared memory every iteration was
 // bound by the shared-memory port (c3: 127 KB per CTA per SpMV at 128 B/clk);
-// registers leave only the (broadcast) z loads.  Units beyond kU kCT (larger
-// systems) read H from shared memory.
+// registers leave only the (broadcast) z loads, each shared by the unit's kCU rows.
+// Units beyond kU kCT (larger systems) read H from shared memory.
 #ifndef MIS_PCG_REG_UNITS
-#define MIS_PCG_REG_UNITS 3
+#define MIS_PCG_REG_UNITS 1
 #endif
 constexpr int kU = MIS_PCG_REG_UNITS;
+constexpr int kCU = 3;   // block rows per unit: unit u = (piece u / 2, rows 3 (u % 2) .. + 2)
 struct HReg {
-  float h[kU][kPiece][6];
+  float h[kU][kPiece][kCU][6];
 };
 
 __device__ __forceinline__ void load_hreg(HReg& R, const int* pptr, const int* pc, const float* H, int nr) {
-  const int units = 6 * pptr[nr];
+  const int units = 2 * pptr[nr];
 #pragma unroll
   for (int j = 0; j < kU; ++j) {
     const int u = threadIdx.x + j * kCT;
-    int k0 = 0, cnt = 0, c = 0;
+    int k0 = 0, cnt = 0, c0 = 0;
     if (u < units) {
-      const int p = u / 6, w = pc[p];
-      c = u - 6 * p;
+      const int w = pc[u >> 1];
+      c0 = kCU * (u & 1);
       k0 = w & 0xffffff;
       cnt = w >> 24;
     }
 #pragma unroll
     for (int b = 0; b < kPiece; ++b) {   // 8-byte loads: a block row is 6 contiguous floats at 24-byte offsets
-      const float2* h2 = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + b) + 6 * c);
-      float2 v0 = make_float2(0.f, 0.f), v1 = v0, v2 = v0;
-      if (b < cnt) { v0 = h2[0]; v1 = h2[1]; v2 = h2[2]; }
-      R.h[j][b][0] = v0.x; R.h[j][b][1] = v0.y; R.h[j][b][2] = v1.x;
-      R.h[j][b][3] = v1.y; R.h[j][b][4] = v2.x; R.h[j][b][5] = v2.y;
+#pragma unroll
+      for (int r = 0; r < kCU; ++r) {
+        const float2* h2 = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + b) + 6 * (c0 + r));
+        float2 v0 = make_float2(0.f, 0.f), v1 = v0, v2 = v0;
+        if (b < cnt) { v0 = h2[0]; v1 = h2[1]; v2 = h2[2]; }
+        R.h[j][b][r][0] = v0.x; R.h[j][b][r][1] = v0.y; R.h[j][b][r][2] = v1.x;
+        R.h[j][b][r][3] = v1.y; R.h[j][b][r][4] = v2.x; R.h[j][b][r][5] = v2.y;
+      }
     }
   }
 }
 
 // out = (H + lambda I) v for the CTA's rows; v read from the replicated full vector Z.
-// Pass 1: one thread per (piece, component) -- <= kPiece blocks, loads issued
-// together (unrolled, predicated); pass 2: per (row, component) the row's piece
-// partials summed in piece order (deterministic).
+// Pass 1: one thread per (piece, half block row range) -- <= kPiece blocks, loads issued
+// together (unrolled, predicated), each z row used by kCU rows; pass 2: per (row,
+// component) the row's piece partials summed in piece order (deterministic).
 __device__ __forceinline__ void spmv_local(const HReg& R, const int* pptr, const int* pc, float* part, const int* col,
                                            const float* H, const float* Z, const float* v_local, float lambda,
                                            float* out, int nr) {
-  const int units = 6 * pptr[nr];
+  const int units = 2 * pptr[nr];
 #pragma unroll
   for (int j = 0; j < kU; ++j) {
     const int u = threadIdx.x + j * kCT;
     if (u < units) {
-      const int p = u / 6, w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
-      float v = 0.f;
+      const int p = u >> 1, c0 = kCU * (u & 1), w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
+      float v[kCU];
+#pragma unroll
+      for (int r = 0; r < kCU; ++r) v[r] = 0.f;
 #pragma unroll
       for (int b = 0; b < kPiece; ++b) {
         if (b < cnt) {
           const float2* zr = reinterpret_cast<const float2*>(Z + 6 * col[k0 + b]);
+          const float2 z0 = zr[0], z1 = zr[1], z2 = zr[2];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            const float2 zv = zr[q];
-            v = fmaf(R.h[j][b][2 * q], zv.x, v);
-            v = fmaf(R.h[j][b][2 * q + 1], zv.y, v);
+          for (int r = 0; r < kCU; ++r) {
+            v[r] = fmaf(R.h[j][b][r][0], z0.x, v[r]);
+            v[r] = fmaf(R.h[j][b][r][1], z0.y, v[r]);
+            v[r] = fmaf(R.h[j][b][r][2], z1.x, v[r]);
+            v[r] = fmaf(R.h[j][b][r][3], z1.y, v[r]);
+            v[r] = fmaf(R.h[j][b][r][4], z2.x, v[r]);
+            v[r] = fmaf(R.h[j][b][r][5], z2.y, v[r]);
           }
         }
       }
-      part[u] = v;
+#pragma unroll
+      for (int r = 0; r < kCU; ++r) part[6 * p + c0 + r] = v[r];
     }
   }
   for (int u = threadIdx.x + kU * kCT; u < units; u += kCT) {
-    const int p = u / 6, c = u - 6 * (u / 6);
-    const int w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
-    float v = 0.f;
+    const int p = u >> 1, c0 = kCU * (u & 1), w = pc[p], k0 = w & 0xffffff, cnt = w >> 24;
+    float v[kCU];
 #pragma unroll
-    for (int j = 0; j < kPiece; ++j) {
-      if (j < cnt) {
-        const float2* zr = reinterpret_cast<const float2*>(Z + 6 * col[k0 + j]);
-        const float2* h = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + j) + 6 * c);
+    for (int r = 0; r < kCU; ++r) v[r] = 0.f;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const float2 hv = h[b], zv = zr[b];
-          v = fmaf(hv.x, zv.x, v);
-          v = fmaf(hv.y, zv.y, v);
+    for (int b = 0; b < kPiece; ++b) {
+      if (b < cnt) {
+        const float2* zr = reinterpret_cast<const float2*>(Z + 6 * col[k0 + b]);
+        const float2 z0 = zr[0], z1 = zr[1], z2 = zr[2];
+#pragma unroll
+        for (int r = 0; r < kCU; ++r) {
+          const float2* h = reinterpret_cast<const float2*>(H + 36 * (size_t)(k0 + b) + 6 * (c0 + r));
+          const float2 h0 = h[0], h1 = h[1], h2 = h[2];
+          v[r] = fmaf(h0.x, z0.x, v[r]);
+          v[r] = fmaf(h0.y, z0.y, v[r]);
+          v[r] = fmaf(h1.x, z1.x, v[r]);
+          v[r] = fmaf(h1.y, z1.y, v[r]);
+          v[r] = fmaf(h2.x, z2.x, v[r]);
+          v[r] = fmaf(h2.y, z2.y, v[r]);
         }
       }
     }
-    part[u] = v;
+#pragma unroll
+    for (int r = 0; r < kCU; ++r) part[6 * p + c0 + r] = v[r];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 6 * nr; e += kCT) {
@@ -369,14 +387,17 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
       }
     }
     if (st1) ts[11] = gtimer();
-    cl.sync();
+    // split cluster barrier: the previous scalars' reciprocals are computed while it completes
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    const double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     if (st1) ts[12] = gtimer();
     g = gather_sum(gam, cs);
     const double d = gather_sum(del, cs);
     if (it == 0) g0 = g;
     if (g == 0.0) break;
-    const double beta = it == 0 ? 0.0 : g / gprev;
-    const double den = it == 0 ? d : d - beta * g / aprev;
+    const double beta = it == 0 ? 0.0 : g * inv_gprev;
+    const double den = it == 0 ? d : d - beta * g * inv_aprev;
     if (!(den > 0.0)) break;
     const double alpha = g / den;
     if (st1) ts[6] = gtimer();
@@ -468,17 +489,19 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   const int32_t* g_pc = a.pc + (int64_t)rank * max_pc;
   for (int i = t; i < npc; i += kCT) pc[i] = g_pc[i];
   const float* Hg = a.Hval + 36 * (int64_t)e0;
-  const bool h_in_smem = 6 * npc > kU * kCT;   // units beyond the registers read H from shared memory
-  if (h_in_smem) {
+  {   // H staged through shared memory with coalesced 16-byte loads: the register units read
+      // 72-byte row groups that would scatter global requests; units beyond the registers
+      // (larger systems) keep reading it there
     const float4* src = reinterpret_cast<const float4*>(Hg);
     float4* dst = reinterpret_cast<float4*>(H);
+#pragma unroll 8
     for (int q = t; q < 9 * ne; q += kCT) dst[q] = src[q];
   }
   __syncthreads();
   if (stamp) ts[1] = gtimer();
   if (a.pcg_iters <= 0 && !a.do_update) return;
   HReg R;
-  load_hreg(R, pptr, pc, Hg, nr);   // straight from global memory into registers
+  load_hreg(R, pptr, pc, H, nr);
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
   if (a.pipelined) {
