@@ -187,6 +187,19 @@ __device__ __forceinline__ void cta_publish(cg::cluster_group& cl, double v, dou
   }
 }
 
+// sum of the 16 published partial slots (zero beyond the cluster size) in a fixed tree:
+// identical in every thread of every CTA, no shuffles
+__device__ __forceinline__ double gather_sum16(const double* slot) {
+  const double2* s2 = reinterpret_cast<const double2*>(slot);
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = s2[k];
+    a[k] = v.x + v.y;
+  }
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // sum of the cs published partials, identical in every thread of every CTA
 __device__ __forceinline__ double gather_sum(const double* slot, int cs) {
   const int l = threadIdx.x & 31;
@@ -338,6 +351,7 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
   float* s = q + nv;
   float* p = s + nv;
   float* const Z0 = reinterpret_cast<float*>(sm + L.zf);   // two full-length buffers: Z0, Z0 + 6 m
+  if (t < 5 * kMaxCluster) base[t] = 0.0;   // unused slots (>= cluster size) stay zero for gather_sum16
   // u = M r; z = q = s = p = 0   (x = 0, r = b from phase 0)
   for (int e = t; e < n6; e += kCT) {
     const int i = e / 6, c = e - 6 * (e / 6);
@@ -392,8 +406,8 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
     const double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     if (st1) ts[12] = gtimer();
-    g = gather_sum(gam, cs);
-    const double d = gather_sum(del, cs);
+    g = gather_sum16(gam);
+    const double d = gather_sum16(del);
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
@@ -420,6 +434,118 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
     gprev = g;
     aprev = alpha;
   }
+  *g_last = g;
+  *g_first = g0;
+}
+
+// The same pipelined PCG with the CTA's vector slices in registers: thread t owns element t
+// of its 6 nr rows (requires 6 max_rows <= kCT).  Only w (read by the 6x6 preconditioner
+// products of its node), m (replicated / SpMV input) and n (SpMV output) pass through
+// shared memory.
+__device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluster_group& cl, unsigned char* sm,
+                                                  const CLay& L, int rank, int cs, int r0, int nr, const int* col,
+                                                  const float* H, const float* Mi, double* g_last, double* g_first,
+                                                  unsigned long long* ts, const int* pptr, const int* pc, float* part,
+                                                  const int* push, int npush, const HReg& R) {
+  const int t = threadIdx.x, nv = a.max_rows * 6, n6 = 6 * nr;
+  const bool own = t < n6;
+  const int ti = t / 6, tc = t - 6 * (t / 6);
+  double* base = reinterpret_cast<double*>(sm + L.dots);
+  double* red = base + 5 * kMaxCluster;
+  float* xs = reinterpret_cast<float*>(sm + L.vec);   // x (written back at the end), r (from phase 0)
+  float* rs = xs + nv;
+  float* us = rs + nv;
+  float* ws = us + nv;
+  float* ms = ws + nv;
+  float* ns = ms + nv;
+  float* const Z0 = reinterpret_cast<float*>(sm + L.zf);
+  if (t < 5 * kMaxCluster) base[t] = 0.0;
+  const float* Mrow = Mi + 36 * ti + 6 * tc;
+  float x = 0.f, r = 0.f, u = 0.f, w = 0.f, zz = 0.f, q = 0.f, s = 0.f, p = 0.f;
+  if (own) {   // u = M r
+    r = rs[t];
+    float v = 0.f;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) v = fmaf(Mrow[b], rs[6 * ti + b], v);
+    u = v;
+    us[t] = v;
+  }
+  __syncthreads();
+  replicate(cl, Z0, us, r0, push, npush);
+  cl.sync();
+  spmv_local(R, pptr, pc, part, col, H, Z0, us, a.lambda, ws, nr);   // w = A u (own element: this thread's write)
+  if (own) w = ws[t];
+  __syncthreads();
+  double gprev = 1.0, aprev = 1.0, g0 = 0.0, g = 0.0;
+  for (int it = 0; it < a.pcg_iters; ++it) {
+    const bool st1 = ts && it == 1;
+    if (st1) ts[8] = gtimer();
+    double dg = 0.0, dd = 0.0;
+    if (own) {
+      dg = (double)r * (double)u;
+      dd = (double)w * (double)u;
+      float v = 0.f;
+#pragma unroll
+      for (int b = 0; b < 6; ++b) v = fmaf(Mrow[b], ws[6 * ti + b], v);
+      ms[t] = v;
+    }
+    __syncthreads();
+    if (st1) ts[9] = gtimer();
+    float* const Zb = Z0 + ((it + 1) & 1) * 6 * a.m;
+    double* const gam = base + (it & 1) * kMaxCluster;
+    double* const del = base + 3 * kMaxCluster + (it & 1) * kMaxCluster;
+    replicate(cl, Zb, ms, r0, push, npush);
+    if (st1) ts[10] = gtimer();
+    {
+      dg = warp_sum_all(dg);
+      dd = warp_sum_all(dd);
+      const int wi = t >> 5, l = t & 31;
+      if (l == 0) { red[wi] = dg; red[32 + wi] = dd; }
+      __syncthreads();
+      if (wi == 0) {
+        const double sg = warp_sum_all(l < kWarps ? red[l] : 0.0), sd = warp_sum_all(l < kWarps ? red[32 + l] : 0.0);
+        if (l < cs) {
+          cl.map_shared_rank(gam, l)[rank] = sg;
+          cl.map_shared_rank(del, l)[rank] = sd;
+        }
+      }
+    }
+    if (st1) ts[11] = gtimer();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    const double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (st1) ts[12] = gtimer();
+    g = gather_sum16(gam);
+    const double d = gather_sum16(del);
+    if (it == 0) g0 = g;
+    if (g == 0.0) break;
+    const double beta = it == 0 ? 0.0 : g * inv_gprev;
+    const double den = it == 0 ? d : d - beta * g * inv_aprev;
+    if (!(den > 0.0)) break;
+    const double alpha = g / den;
+    if (st1) ts[6] = gtimer();
+    spmv_local(R, pptr, pc, part, col, H, Zb, ms, a.lambda, ns, nr);   // n = A m (own element: this thread's write)
+    if (st1) ts[13] = gtimer();
+    const float fb = (float)beta, fa = (float)alpha;
+    if (own) {
+      const float n = ns[t], m = ms[t];
+      zz = fmaf(fb, zz, n);
+      q = fmaf(fb, q, m);
+      s = fmaf(fb, s, w);
+      p = fmaf(fb, p, u);
+      x = fmaf(fa, p, x);
+      r = fmaf(-fa, s, r);
+      u = fmaf(-fa, q, u);
+      w = fmaf(-fa, zz, w);
+      ws[t] = w;
+    }
+    __syncthreads();
+    if (st1) { ts[14] = gtimer(); ts[15] = 1; }
+    gprev = g;
+    aprev = alpha;
+  }
+  if (own) xs[t] = x;
+  __syncthreads();
   *g_last = g;
   *g_first = g0;
 }
@@ -504,7 +630,11 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   load_hreg(R, pptr, pc, H, nr);
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
-  if (a.pipelined) {
+  if (a.pipelined && 6 * a.max_rows <= kCT) {
+    pcg_pipelined_reg(a, cl, sm, L, rank, cs, r0, nr, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
+                      npush, R);
+    if (stamp) ts[3] = ts[2];
+  } else if (a.pipelined) {
     pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
                   npush, R);
     if (stamp) ts[3] = ts[2];
