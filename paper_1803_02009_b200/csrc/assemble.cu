@@ -424,6 +424,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
 // FP32 accumulation): products to ~2^-21 relative, as accurate as the FP32 FMA path for these
 // sums, at a fraction of its issue slots.  Only the upper-triangle tiles are computed (10 of 14).
 constexpr int kTcFSP = 72;   // row stride: c' [0, 32) | e' [32, 64) | pad; 72 = 8 (mod 32): conflict-free
+// per-warp commit record of the tensor-core K3b: P pair records of 52 (36 data | 16 moments),
+// then K node records of 20 (6 rhs | 2 pad | 12 node moments), so every commit item is one
+// aligned float2 / float4 shared load
+__host__ __device__ constexpr int tc_rec_floats(int K) { return 52 * (K * (K + 1) / 2) + 20 * K; }
 
 template <int K>
 __device__ __forceinline__ void build_row_tc(const PState<K>& st, float* row) {
@@ -502,31 +506,52 @@ template <int K>
 __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(AsmPointsArgs a) {
   static_assert(6 * K + 1 <= 32 && 4 * K + 3 <= 24, "tensor-core K3b: k <= 4");
   constexpr int P = K * (K + 1) / 2;
-  constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
+  constexpr int RT = tc_rec_floats(K);
   extern __shared__ float4 smem4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
   float* F = reinterpret_cast<float*>(smem4) + warp * (32 * kTcFSP);
+  float* Rec = reinterpret_cast<float*>(smem4) + kWarps * 32 * kTcFSP + warp * RT;
   __shared__ int32_t slot_sm[kWarps][P];
   int32_t* slots = slot_sm[warp];
-  // record permutation: perm[d] = index in the dumped sums (c' 32 x 32 at 0, e' 32 x 24 at 1024), -1: zero
-  __shared__ int16_t perm[RS];
-  for (int d = threadIdx.x; d < RS; d += blockDim.x) perm[d] = -1;
-  __syncthreads();
+  // where each summed entry goes: inv[q] = record index of position q of the dumped sums
+  // (c' 32 x 32 at 0, e' 24 x 24 at 1024; upper triangles), -1: not part of the system
+  __shared__ int16_t inv[32 * 32 + 24 * 24];
   for (int q = threadIdx.x; q < 32 * 32 + 24 * 24; q += blockDim.x) {
     const bool e = q >= 1024;
     const int A = e ? (q - 1024) / 24 : q / 32, B = e ? (q - 1024) % 24 : q % 32;
-    if (A > B) continue;
     int d = -1;
-    if (!e) {                    // c' = [w_j u_j ..., r_pl]
-      if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
-      else if (B == 6 * K && A < 6 * K) d = 52 * P + 18 * (A / 6) + (A % 6);
-    } else {                     // e' = [w_j a_j, w_j ..., r']
-      if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
-      else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 18 * (A / 4) + 6 + 3 * (A % 4) + (B - 4 * K);
+    if (A <= B) {
+      if (!e) {                    // c' = [w_j u_j ..., r_pl]
+        if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
+        else if (B == 6 * K && A < 6 * K) d = 52 * P + 20 * (A / 6) + (A % 6);
+      } else {                     // e' = [w_j a_j, w_j ..., r']
+        if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
+        else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 20 * (A / 4) + 8 + 3 * (A % 4) + (B - 4 * K);
+      }
     }
-    if (d >= 0) perm[d] = (int16_t)(e ? 1024 + A * 24 + B : A * 32 + B);
+    inv[q] = (int16_t)d;
   }
+  for (int q = lane; q < RT; q += 32) Rec[q] = 0.f;   // entries no fragment maps to stay zero
   __syncthreads();
+  // this lane's 40 fragment positions -> record indices, packed in pairs (0xffff: dropped)
+  uint32_t dmap[20];
+  {
+    const int tmi[6] = {0, 0, 0, 0, 1, 1}, tni[6] = {0, 1, 2, 3, 2, 3};
+    const int emi[4] = {0, 0, 0, 1}, eni[4] = {0, 1, 2, 2};
+#pragma unroll
+    for (int t = 0; t < 10; ++t) {
+      const bool e = t >= 6;
+      const int r0 = 16 * (e ? emi[t - 6] : tmi[t]) + g, c0 = 8 * (e ? eni[t - 6] : tni[t]) + 2 * tig;
+      int d4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int rr = r0 + 8 * (h >> 1), cc = c0 + (h & 1);
+        d4[h] = e ? (rr < 24 ? inv[1024 + rr * 24 + cc] : -1) : inv[rr * 32 + cc];
+      }
+      dmap[2 * t] = (uint32_t)(d4[0] & 0xffff) | ((uint32_t)(d4[1] & 0xffff) << 16);
+      dmap[2 * t + 1] = (uint32_t)(d4[2] & 0xffff) | ((uint32_t)(d4[3] & 0xffff) << 16);
+    }
+  }
 
   pdl_wait();   // K3a's factor state (the tables above are independent of it)
   int64_t c = 0;
@@ -579,43 +604,31 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
       }
       __syncwarp();
     }
-    // ---- commit: fragments -> shared memory -> atomic adds into the BSR accumulators
+    // ---- commit: fragments -> the warp's record (scattered by the per-lane map) -> atomic adds
     {
-      const int tmi[6] = {0, 0, 0, 0, 1, 1}, tni[6] = {0, 1, 2, 3, 2, 3};
+      auto put = [&](uint32_t pk, float v0, float v1) {
+        const uint32_t d0 = pk & 0xffffu, d1 = pk >> 16;
+        if (d0 != 0xffffu) Rec[d0] = v0;
+        if (d1 != 0xffffu) Rec[d1] = v1;
+      };
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        const int r0 = 16 * tmi[t] + g, c0 = 8 * tni[t] + 2 * tig;
-        F[r0 * 32 + c0] = dc[t][0];
-        F[r0 * 32 + c0 + 1] = dc[t][1];
-        F[(r0 + 8) * 32 + c0] = dc[t][2];
-        F[(r0 + 8) * 32 + c0 + 1] = dc[t][3];
+        put(dmap[2 * t], dc[t][0], dc[t][1]);
+        put(dmap[2 * t + 1], dc[t][2], dc[t][3]);
       }
-      const int emi[4] = {0, 0, 0, 1}, eni[4] = {0, 1, 2, 2};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const int r0 = 16 * emi[t] + g, c0 = 8 * eni[t] + 2 * tig;
-        if (r0 < 24) {
-          F[1024 + r0 * 24 + c0] = de[t][0];
-          F[1024 + r0 * 24 + c0 + 1] = de[t][1];
-        }
-        if (r0 + 8 < 24) {
-          F[1024 + (r0 + 8) * 24 + c0] = de[t][2];
-          F[1024 + (r0 + 8) * 24 + c0 + 1] = de[t][3];
-        }
+        put(dmap[12 + 2 * t], de[t][0], de[t][1]);
+        put(dmap[12 + 2 * t + 1], de[t][2], de[t][3]);
       }
     }
     __syncwarp();
     int64_t next_chunk = 0;
     if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
-    auto rv = [&](int d) -> float {
-      const int q = perm[d];
-      return q < 0 ? 0.f : F[q];
-    };
     for (int it = lane; it < 13 * P + 6 * K; it += 32) {
       if (it < 13 * P) {
-        const int pr = it / 13, q = it - 13 * pr;
-        const int d0 = 52 * pr + 4 * q;   // data (q < 9) then moments: contiguous in the record
-        const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+        const int pr = it / 13, q = it - 13 * pr;   // data (q < 9) then moments: contiguous in the record
+        const float4 v = reinterpret_cast<const float4*>(Rec)[it];
         if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
         const int64_t u = slots[pr];
         float* dst = q < 9 ? a.acc.data + 36 * u + 4 * q : a.acc.mom + 16 * u + 4 * (q - 9);
@@ -623,18 +636,18 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
       } else {
         const int t2 = it - 13 * P, sl = t2 / 6, q = t2 - 6 * sl;
         const int64_t nd = nodes[sl];
+        const float* rn = Rec + 52 * P + 20 * sl;
         if (q < 3) {
-          const int d0 = 52 * P + 18 * sl + 2 * q;
-          const float2 v = make_float2(rv(d0), rv(d0 + 1));
+          const float2 v = reinterpret_cast<const float2*>(rn)[q];
           if (v.x != 0.f || v.y != 0.f) atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * nd + 2 * q), v);
         } else {
-          const int d0 = 52 * P + 18 * sl + 6 + 4 * (q - 3);
-          const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
+          const float4 v = reinterpret_cast<const float4*>(rn + 8)[q - 3];
           if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
             atomicAdd(reinterpret_cast<float4*>(a.acc.node_mom + 12 * nd + 4 * (q - 3)), v);
         }
       }
     }
+    __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
   pdl_trigger();
@@ -861,7 +874,8 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) 
   using L = Lay<K>;
   if (a.nchunk <= 0) return;
   constexpr bool tc = MIS_K3B_TC && K <= 4;   // tensor-core SYRK for k <= 4, FP32 tiles above
-  const size_t smem = sizeof(float) * kWarps * 32 * (tc ? kTcFSP : L::FSP);
+  const size_t smem = tc ? sizeof(float) * kWarps * (32 * kTcFSP + tc_rec_floats(K <= 4 ? K : 4))
+                          : sizeof(float) * kWarps * 32 * L::FSP;
   void (*kern)(AsmPointsArgs);
   if constexpr (tc) kern = k_accum_points_tc<(K <= 4 ? K : 4)>;
   else kern = k_accum_points<K>;
