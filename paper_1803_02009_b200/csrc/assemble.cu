@@ -663,20 +663,74 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
 //   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
 constexpr int kFB = 4;   // off-diagonal entries / nodes per warp (their loads overlap)
 
-// one 6x6 block from its staged D | Mo | G (88 floats): H entries (and the mirror's)
-__device__ __forceinline__ void final_block(const FinalArgs& r, const float* st, float* hst, int64_t e, int lo, int lane) {
+// Entry l = 6 i + j of a block as a branch-free recipe over the staged D | Mo | G:
+//   h = w_data D[d] + G[l] + w_pt sum_k coef_k Mo[idx_k]
+// (the same terms as block_entry: tr(S) I - S^T, [s_j]x, -[s_l]x, s0 I), built once per lane.
+struct Recipe {
+  int d, tr;          // D index (upper triangle on the diagonal), mirror position 6 j + i
+  uint32_t idx;       // four Mo indices, one per byte
+  float4 coef;        // their coefficients (0, +-1)
+};
+__device__ inline Recipe make_recipe(int l, bool diag) {
+  const int i = l / 6, j = l - 6 * (l / 6);
+  Recipe rc;
+  rc.d = diag ? 6 * min(i, j) + max(i, j) : l;
+  rc.tr = 6 * j + i;
+  int id[4] = {0, 0, 0, 0};
+  float cf[4] = {0.f, 0.f, 0.f, 0.f};
+  if (i < 3 && j < 3) {   // tr(S) I - S^T
+    if (i == j) { id[0] = 0; id[1] = 5; id[2] = 10; cf[0] = cf[1] = cf[2] = 1.f; }
+    id[3] = diag ? 4 * min(i, j) + max(i, j) : 4 * j + i;
+    cf[3] = -1.f;
+  } else if (i < 3) {     // [s_j]x (i, j-3), s_j = Mo[p][3]
+    const int c = j - 3;
+    if (i != c) {
+      if (c == (i + 1) % 3) { id[0] = 4 * ((i + 2) % 3) + 3; cf[0] = -1.f; }
+      else { id[0] = 4 * ((i + 1) % 3) + 3; cf[0] = 1.f; }
+    }
+  } else if (j < 3) {     // -[s_l]x (i-3, j), s_l = Mo[3][q] (= Mo[q][3] on the diagonal)
+    const int rr = i - 3, q1 = (rr + 2) % 3, q2 = (rr + 1) % 3;
+    if (rr != j) {
+      if (j == (rr + 1) % 3) { id[0] = diag ? 4 * q1 + 3 : 12 + q1; cf[0] = 1.f; }
+      else { id[0] = diag ? 4 * q2 + 3 : 12 + q2; cf[0] = -1.f; }
+    }
+  } else if (i == j) {
+    id[0] = 15;
+    cf[0] = 1.f;
+  }
+  rc.idx = (uint32_t)id[0] | ((uint32_t)id[1] << 8) | ((uint32_t)id[2] << 16) | ((uint32_t)id[3] << 24);
+  rc.coef = make_float4(cf[0], cf[1], cf[2], cf[3]);
+  return rc;
+}
+__device__ __forceinline__ float apply_recipe(const Recipe& rc, const float* st, int l, float w_data, float w_pt) {
+  const float* Mo = st + 36;
+  const float pt = rc.coef.x * Mo[rc.idx & 0xff] + rc.coef.y * Mo[(rc.idx >> 8) & 0xff] +
+                   rc.coef.z * Mo[(rc.idx >> 16) & 0xff] + rc.coef.w * Mo[rc.idx >> 24];
+  return fmaf(w_data, st[rc.d], st[52 + l]) + w_pt * pt;
+}
+
+// one 6x6 block from its staged D | Mo | G (88 floats): H entries (and the mirror's);
+// lane owns entries lane and lane + 32 (< 36) with their recipes rc[0], rc[1]
+__device__ __forceinline__ void final_block(const FinalArgs& r, const float* st, float* hst, int64_t e, int lo, int lane,
+                                            const Recipe (&rc)[2]) {
   const bool diag = lo < 0;
-  for (int l = lane; l < 36; l += 32) {
-    const int i = l / 6, j = l - 6 * (l / 6);
-    const float h = block_entry(st, st + 36, st + 52, diag, i, j, r.w_data, r.w_pt);
-    r.Hval[36 * e + l] = h;
-    if (!diag) r.Hval[36 * (int64_t)lo + 6 * j + i] = h;
-    if (hst) hst[l] = h;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int l = lane + 32 * k;
+    if (l < 36) {
+      const float h = apply_recipe(rc[k], st, l, r.w_data, r.w_pt);
+      r.Hval[36 * e + l] = h;
+      if (!diag) r.Hval[36 * (int64_t)lo + rc[k].tr] = h;
+      if (hst) hst[l] = h;
+    }
   }
 }
 
 __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   __shared__ float stage[8][kFB][124];
+  __shared__ Recipe rtab[2][36];   // [diagonal?][entry], built before the dependency wait
+  if (threadIdx.x < 72) rtab[threadIdx.x / 36][threadIdx.x % 36] = make_recipe(threadIdx.x % 36, threadIdx.x < 36);
+  __syncthreads();
   pdl_wait();      // K3a/K3b/K4 accumulators
   pdl_trigger();   // the solver may launch (it waits for this grid's completion before reading)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -696,7 +750,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     r.acc.graph[36 * e + lane] = 0.f;
     if (lane < 4) r.acc.graph[36 * e + 32 + lane] = 0.f;
     __syncwarp();
-    final_block(r, st, st + 88, e, -1, lane);
+    const Recipe rc[2] = {rtab[0][lane], rtab[0][lane < 4 ? lane + 32 : 0]};
+    final_block(r, st, st + 88, e, -1, lane, rc);
     if (r.Minv) {   // block-Jacobi inverse of this node (K7), off the solver's critical path:
       __syncwarp();   // fp64 Gauss-Jordan, lane rr < 6 holds row rr of [H + (lambda + mu) I | I]
       const int64_t row_j = gw;
@@ -772,9 +827,10 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
       if (lane < 4) r.acc.graph[36 * E + 32 + lane] = 0.f;
     }
     __syncwarp();
+    const Recipe rc[2] = {rtab[1][lane], rtab[1][lane < 4 ? lane + 32 : 0]};
 #pragma unroll
     for (int q = 0; q < kFB; ++q)
-      if (e[q] >= 0) final_block(r, stage[wib][q], nullptr, e[q], lo[q], lane);
+      if (e[q] >= 0) final_block(r, stage[wib][q], nullptr, e[q], lo[q], lane, rc);
     return;
   }
   g2 -= n_off;
