@@ -166,6 +166,34 @@ __device__ __forceinline__ int build_push(cg::cluster_group& cl, unsigned* mask,
   return s_npush;
 }
 
+// ---- bulk (TMA) copies global -> shared memory completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// bytes: multiple of 16, both addresses 16-byte aligned; split in <= 32 KB copies
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  for (uint32_t o = 0; o < bytes; o += 32768u) {
+    const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(static_cast<char*>(dst) + o)),
+        "l"(static_cast<const char*>(src) + o), "r"(n), "r"(smem_u32(bar))
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // xor-butterfly sum: every lane ends with the bitwise-same value (IEEE + is commutative)
 __device__ __forceinline__ double warp_sum_all(double v) {
 #pragma unroll
@@ -574,6 +602,8 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   float* part = reinterpret_cast<float*>(sm + L.part);
   int* push = reinterpret_cast<int*>(sm + L.push);
   float* H = reinterpret_cast<float*>(sm + L.h);
+  __shared__ uint64_t tma_bar;
+  if (threadIdx.x == 0) mbar_init(&tma_bar, 1);
 
   pdl_wait();      // H, b, M^-1 from the finalisation
   pdl_trigger();   // the next K3a may launch on the SMs this cluster leaves free (it waits for completion)
@@ -585,11 +615,15 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   unsigned long long* ts = a.tstamp + 16 * rank;
   if (stamp) ts[0] = gtimer();
 
-  // ---- phase 0: local rows of H (from the accumulators), b, column owners
-  // lists of this rank (built once per frame), columns, b, block inverses, own node states
-  {
-    double* rt = reinterpret_cast<double*>(sm + L.rt);
-    for (int q = t; q < 12 * nr; q += kCT) rt[q] = a.nd.Rt64[12 * (int64_t)r0 + q];
+  // ---- phase 0: the rank's rows of H, its block inverses and its nodes' fp64 states by bulk
+  // copies (one thread issues them, completion on an mbarrier) while the other threads load
+  // the lists of this rank (built once per frame), columns and b
+  const float* Hg = a.Hval + 36 * (int64_t)e0;
+  if (t == 0) {
+    mbar_expect_tx(&tma_bar, (uint32_t)(144 * ne + 144 * nr + 96 * nr));
+    bulk_g2s(H, Hg, (uint32_t)(144 * ne), &tma_bar);
+    bulk_g2s(Mi, a.Minv + 36 * (int64_t)r0, (uint32_t)(144 * nr), &tma_bar);
+    bulk_g2s(sm + L.rt, a.nd.Rt64 + 12 * (int64_t)r0, (uint32_t)(96 * nr), &tma_bar);
   }
   const int sticky = *a.numeric_flag;   // set by an earlier launch of this registration
   const int max_pc = max_pieces(a.max_rows, a.max_nnz);
@@ -605,25 +639,14 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     p[i] = 0.f;
     Ap[i] = 0.f;
   }
-  {
-    const float4* src = reinterpret_cast<const float4*>(a.Minv + 36 * (int64_t)r0);
-    float4* dst = reinterpret_cast<float4*>(Mi);
-    for (int q = t; q < 9 * nr; q += kCT) dst[q] = src[q];
-  }
   __syncthreads();
   const int npc = pptr[nr];
   const int32_t* g_pc = a.pc + (int64_t)rank * max_pc;
   for (int i = t; i < npc; i += kCT) pc[i] = g_pc[i];
-  const float* Hg = a.Hval + 36 * (int64_t)e0;
-  {   // H staged through shared memory with coalesced 16-byte loads: the register units read
-      // 72-byte row groups that would scatter global requests; units beyond the registers
-      // (larger systems) keep reading it there
-    const float4* src = reinterpret_cast<const float4*>(Hg);
-    float4* dst = reinterpret_cast<float4*>(H);
-#pragma unroll 8
-    for (int q = t; q < 9 * ne; q += kCT) dst[q] = src[q];
-  }
   __syncthreads();
+  // H is staged in shared memory (the register units read 72-byte row groups that would
+  // scatter global requests; units beyond the registers, for larger systems, read it there)
+  mbar_wait(&tma_bar, 0);
   if (stamp) ts[1] = gtimer();
   if (a.pcg_iters <= 0 && !a.do_update) return;
   HReg R;
