@@ -431,11 +431,13 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
     if (st1) ts[11] = gtimer();
     // split cluster barrier: the previous scalars' reciprocals are computed while it completes
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    const double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));   // computed here, not after the wait
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     if (st1) ts[12] = gtimer();
     g = gather_sum16(gam);
-    const double d = gather_sum16(del);
+    double d = gather_sum16(del);
+    asm volatile("" : "+d"(g), "+d"(d));   // both sums before the early-exit test
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
@@ -540,11 +542,13 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     }
     if (st1) ts[11] = gtimer();
     asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    const double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
+    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));   // computed here, not after the wait
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     if (st1) ts[12] = gtimer();
     g = gather_sum16(gam);
-    const double d = gather_sum16(del);
+    double d = gather_sum16(del);
+    asm volatile("" : "+d"(g), "+d"(d));   // both sums before the early-exit test
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
