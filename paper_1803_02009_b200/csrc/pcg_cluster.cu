@@ -60,7 +60,7 @@ struct CLay {   // uniform shared-memory layout (identical offsets in every CTA)
 // Global layout (rank r): pptr [r * (max_rows + 1)], pieces [r * max_pieces],
 // push [r * max_rows * 16], npush [r].
 struct PcgLists {
-  int32_t *pptr, *pc, *push, *npush;
+  int32_t *pptr, *pc, *push, *npush;   // npush[16] | nin[16]: halo rows each rank receives from the others
   uint32_t* mask;   // m: ranks that read each row (zero outside the prep kernels)
 };
 
@@ -69,6 +69,7 @@ __global__ void k_pcg_mark(const int32_t* row_ptr, const int32_t* col, const int
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int rank = blockIdx.x, r0 = part[rank], r1 = part[rank + 1];
+  if (rank == 0 && threadIdx.x < kMaxCluster) L.npush[kMaxCluster + threadIdx.x] = 0;   // nin, summed by k_pcg_lists
   for (int k = row_ptr[r0] + threadIdx.x; k < row_ptr[r1]; k += blockDim.x) {
     const int j = col[k];
     if (j < r0 || j >= r1) atomicOr(L.mask + j, 1u << rank);
@@ -112,6 +113,7 @@ __global__ void k_pcg_lists(const int32_t* row_ptr, const int32_t* part, int cs,
       const unsigned bal = __ballot_sync(0xffffffffu, on);
       if (on) push[n + __popc(bal & ((1u << l) - 1u))] = (d << 16) | i;
       n += __popc(bal);
+      if (l == 0 && d != rank && bal) atomicAdd(L.npush + kMaxCluster + d, __popc(bal));
     }
   __syncwarp();
   for (int i = l; i < nr; i += 32) L.mask[r0 + i] = 0u;
@@ -192,6 +194,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
           smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// remote (distributed shared memory) stores that complete_tx on the destination CTA's mbarrier
+__device__ __forceinline__ uint32_t map_rank_u32(uint32_t local_smem, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_smem), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f2(uint32_t raddr, float2 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+               "f"(v.x), "f"(v.y), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+// bounded wait: a lost transfer traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (long long spin = 0; !ok; ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (spin > (1ll << 26)) __trap();
+  }
 }
 
 // xor-butterfly sum: every lane ends with the bitwise-same value (IEEE + is commutative)
@@ -476,7 +507,8 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
                                                   const CLay& L, int rank, int cs, int r0, int nr, const int* col,
                                                   const float* H, const float* Mi, double* g_last, double* g_first,
                                                   unsigned long long* ts, const int* pptr, const int* pc, float* part,
-                                                  const int* push, int npush, const HReg& R) {
+                                                  const int* push, int npush, const HReg& R, uint64_t* bars,
+                                                  uint32_t in_bytes) {
   const int t = threadIdx.x, nv = a.max_rows * 6, n6 = 6 * nr;
   const bool own = t < n6;
   const int ti = t / 6, tc = t - 6 * (t / 6);
@@ -524,7 +556,23 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     float* const Zb = Z0 + ((it + 1) & 1) * 6 * a.m;
     double* const gam = base + (it & 1) * kMaxCluster;
     double* const del = base + 3 * kMaxCluster + (it & 1) * kMaxCluster;
-    replicate(cl, Zb, ms, r0, push, npush);
+    // No cluster barrier in the loop: the halo rows of m and the dot partials travel as
+    // st.async stores that complete_tx on the receiver's mbarrier of this iteration's parity,
+    // whose expected byte count (incoming halo rows x 24 + 16 per other CTA) is armed by
+    // the receiver itself.  Reuse of a buffer two iterations later is safe because every
+    // CTA's next partials are sent only after it has finished reading that buffer.
+    uint64_t* const bar = bars + (it & 1);
+    const uint32_t bar_u = smem_u32(bar);
+    if (t == 0) mbar_expect_tx(bar, in_bytes);
+    {
+      const uint32_t zb_u = smem_u32(Zb);
+      for (int k = t; k < 3 * npush; k += kCT) {
+        const int e = push[k / 3], qq = k - 3 * (k / 3), dst = e >> 16, i = e & 0xffff;
+        const float2 v = reinterpret_cast<const float2*>(ms + 6 * i)[qq];
+        if (dst == rank) reinterpret_cast<float2*>(Zb + 6 * (r0 + i))[qq] = v;
+        else st_async_f2(map_rank_u32(zb_u + 4u * (uint32_t)(6 * (r0 + i) + 2 * qq), dst), v, map_rank_u32(bar_u, dst));
+      }
+    }
     if (st1) ts[10] = gtimer();
     {
       dg = warp_sum_all(dg);
@@ -534,17 +582,21 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
       __syncthreads();
       if (wi == 0) {
         const double sg = warp_sum_all(l < kWarps ? red[l] : 0.0), sd = warp_sum_all(l < kWarps ? red[32 + l] : 0.0);
-        if (l < cs) {
-          cl.map_shared_rank(gam, l)[rank] = sg;
-          cl.map_shared_rank(del, l)[rank] = sd;
+        if (l == rank) {
+          gam[rank] = sg;
+          del[rank] = sd;
+        } else if (l < cs) {
+          const uint32_t rb = map_rank_u32(bar_u, l);
+          st_async_f64(map_rank_u32(smem_u32(gam + rank), l), sg, rb);
+          st_async_f64(map_rank_u32(smem_u32(del + rank), l), sd, rb);
         }
       }
     }
     if (st1) ts[11] = gtimer();
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
     double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
-    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));   // computed here, not after the wait
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));   // computed before the wait
+    mbar_wait_bounded(bar, (uint32_t)(it >> 1) & 1u);
+    __syncthreads();   // this CTA's own rows / dot slots, written by other threads, visible
     if (st1) ts[12] = gtimer();
     g = gather_sum16(gam);
     double d = gather_sum16(del);
@@ -606,8 +658,12 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   float* part = reinterpret_cast<float*>(sm + L.part);
   int* push = reinterpret_cast<int*>(sm + L.push);
   float* H = reinterpret_cast<float*>(sm + L.h);
-  __shared__ uint64_t tma_bar;
-  if (threadIdx.x == 0) mbar_init(&tma_bar, 1);
+  __shared__ uint64_t tma_bar, pcg_bar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&tma_bar, 1);
+    mbar_init(pcg_bar, 1);       // the pipelined PCG's per-iteration exchanges (initialised before the
+    mbar_init(pcg_bar + 1, 1);   // cluster barrier that precedes any remote arrival)
+  }
 
   pdl_wait();      // H, b, M^-1 from the finalisation
   pdl_trigger();   // the next K3a may launch on the SMs this cluster leaves free (it waits for completion)
@@ -658,8 +714,9 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
   if (a.pipelined && 6 * a.max_rows <= kCT) {
+    const uint32_t in_bytes = (uint32_t)(24 * a.npush[kMaxCluster + rank] + 16 * (cs - 1));
     pcg_pipelined_reg(a, cl, sm, L, rank, cs, r0, nr, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
-                      npush, R);
+                      npush, R, pcg_bar, in_bytes);
     if (stamp) ts[3] = ts[2];
   } else if (a.pipelined) {
     pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,

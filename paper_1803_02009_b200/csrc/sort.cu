@@ -424,7 +424,7 @@ cudaError_t build_pattern(Ctx* c) {
     CK(ensure(c, c->pcg_pptr, (size_t)cs * (mr + 1) * 4));
     CK(ensure(c, c->pcg_pc, (size_t)cs * mp * 4));
     CK(ensure(c, c->pcg_push, (size_t)cs * mr * 16 * 4));
-    CK(ensure(c, c->pcg_npush, 16 * 4));
+    CK(ensure(c, c->pcg_npush, 32 * 4));   // npush[16] | incoming halo rows nin[16]
     if (c->pcg_mask.bytes < (size_t)m * 4) {
       CK(ensure(c, c->pcg_mask, (size_t)m * 4));
       CK(cudaMemsetAsync(c->pcg_mask.p, 0, (size_t)m * 4, c->st));   // kept zero by k_pcg_lists
