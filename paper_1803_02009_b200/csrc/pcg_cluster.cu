@@ -538,7 +538,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
   spmv_local(R, pptr, pc, part, col, H, Z0, us, a.lambda, ws, nr);   // w = A u (own element: this thread's write)
   if (own) w = ws[t];
   __syncthreads();
-  double gprev = 1.0, aprev = 1.0, g0 = 0.0, g = 0.0;
+  double gprev = 1.0, aprev_den = 1.0, g0 = 0.0, g = 0.0;
   for (int it = 0; it < a.pcg_iters; ++it) {
     const bool st1 = ts && it == 1;
     if (st1) ts[8] = gtimer();
@@ -593,8 +593,9 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
       }
     }
     if (st1) ts[11] = gtimer();
-    double inv_gprev = 1.0 / gprev, inv_aprev = 1.0 / aprev;
-    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));   // computed before the wait
+    // reciprocals of the previous scalars (1 / alpha_prev = den_prev / g_prev) before the wait
+    double inv_gprev = 1.0 / gprev, inv_aprev = aprev_den / gprev;
+    asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));
     mbar_wait_bounded(bar, (uint32_t)(it >> 1) & 1u);
     __syncthreads();   // this CTA's own rows / dot slots, written by other threads, visible
     if (st1) ts[12] = gtimer();
@@ -606,11 +607,12 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
     const double den = it == 0 ? d : d - beta * g * inv_aprev;
     if (!(den > 0.0)) break;
-    const double alpha = g / den;
+    // alpha only enters the fp32 vector updates: one fp32 division instead of an fp64 one
+    const float fa = (float)g / (float)den;
     if (st1) ts[6] = gtimer();
     spmv_local(R, pptr, pc, part, col, H, Zb, ms, a.lambda, ns, nr);   // n = A m (own element: this thread's write)
     if (st1) ts[13] = gtimer();
-    const float fb = (float)beta, fa = (float)alpha;
+    const float fb = (float)beta;
     if (own) {
       const float n = ns[t], m = ms[t];
       zz = fmaf(fb, zz, n);
@@ -626,7 +628,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     __syncthreads();
     if (st1) { ts[14] = gtimer(); ts[15] = 1; }
     gprev = g;
-    aprev = alpha;
+    aprev_den = den;
   }
   if (own) xs[t] = x;
   __syncthreads();
