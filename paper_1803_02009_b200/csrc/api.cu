@@ -309,6 +309,17 @@ static void prof_collect(Ctx* c) {
   c->pev.clear();
 }
 
+// K1 of a frame whose launch mis_register deferred (see set_frame_impl)
+cudaError_t flush_frame(Ctx* c) {
+  if (!c->frame_pending) return cudaSuccess;
+  c->frame_pending = false;
+  ProfScope ps(c, P_FRAME, 1);
+  FrameView fv = frame_view(c);
+  fv.depth = c->frame_src;
+  launch_frame_prep(fv, c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
+  return cudaGetLastError();
+}
+
 }  // namespace mis
 
 using namespace mis;
@@ -399,7 +410,9 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
   }
   if (ensure(c, c->rep, kRepBytes) != cudaSuccess ||
       ensure(c, c->tstamp, 2048) != cudaSuccess || cudaMemset(c->tstamp.p, 0, 2048) != cudaSuccess ||
-      ensure(c, c->counter, 64) != cudaSuccess) {
+      ensure(c, c->counter, 64) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->hpin), 16 * sizeof(int64_t)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->rb_ev, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return MIS_E_NOMEM;
   }
@@ -426,6 +439,8 @@ mis_status mis_destroy(mis_ctx* c) {
     for (DBuf* b : mbv) free_buf(*b);
   }
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(c->nccl_comm);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->rb_ev) cudaEventDestroy(c->rb_ev);
   if (c->own_stream) cudaStreamDestroy(c->st);
 
   delete c;
@@ -591,7 +606,16 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
   return MIS_OK;
 }
 
+
+// defer: mis_register only -- K1 is queued behind the frame's pattern readback so it runs
+// while the host waits for it (the depth is still read within the same API call)
+static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it,
+                                 const float pose[12], bool defer);
 mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it, const float pose[12]) {
+  return set_frame_impl(c, mem, depth_mm, it, pose, false);
+}
+static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it,
+                                 const float pose[12], bool defer) {
   if (!c) return MIS_E_ARG;
   if (!depth_mm || !it || !pose) return fail(c, MIS_E_ARG, "set_frame: null argument");
   if (!(it->fx > 0) || !(it->fy > 0) || it->width < 3 || it->height < 3 || !(it->cx >= 0) || !(it->cx < it->width) ||
@@ -611,11 +635,9 @@ mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const m
   TRY(c, ensure(c, c->nmap, px * 16));
   TRY(c, ensure(c, c->nmapd, px * 32));
   if (mem == MIS_MEM_HOST) TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st));
-  ProfScope ps(c, P_FRAME, 1);
-  FrameView fv = frame_view(c);
-  fv.depth = dsrc;
-  launch_frame_prep(fv, c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
-  TRY(c, cudaGetLastError());
+  c->frame_src = dsrc;
+  c->frame_pending = true;
+  if (!defer || c->prof) TRY(c, flush_frame(c));   // (profiling: K1 in its own group)
   c->have_frame = true;
   return MIS_OK;
 }
@@ -813,6 +835,7 @@ static mis_status prepare(Ctx* c) {
       }
     }
   }
+  TRY(c, flush_frame(c));   // if the pattern was still valid (no readback to hide it behind)
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
   return MIS_OK;
 }
@@ -847,7 +870,7 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
   cudaSetDevice(c->device);
   mis_status s;
   if (depth_mm) {
-    if ((s = mis_set_frame(c, mem, depth_mm, intr, pose)) != MIS_OK) return s;
+    if ((s = set_frame_impl(c, mem, depth_mm, intr, pose, true)) != MIS_OK) return s;
   } else if (pose) {
     memcpy(c->pose, pose, 48);
   }
@@ -914,6 +937,7 @@ mis_status mis_dbg_set_nodes(mis_ctx* c, mis_mem mem, const float* Rt) {
 mis_status mis_dbg_frame(mis_ctx* c, mis_mem mem, float* nmap) {
   if (!c || !nmap) return MIS_E_ARG;
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame");
+  TRY(c, flush_frame(c));
   cudaSetDevice(c->device);
   TRY(c, cudaMemcpyAsync(nmap, c->nmap.p, (size_t)c->W * c->H * 16, kind_out(mem), c->st));
   if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
@@ -1022,6 +1046,7 @@ static mis_status fuse_register(Ctx* c, const float* rgb, int32_t frame) {
 mis_status mis_dbg_fuse_register(mis_ctx* c, int64_t* owner, uint8_t* why) {
   if (!c || !owner) return MIS_E_ARG;
   if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
+  TRY(c, flush_frame(c));
   cudaSetDevice(c->device);
   if (c->dirty) TRY(c, run_build_order(c));
   mis_status s;
@@ -1038,6 +1063,7 @@ mis_status mis_dbg_fuse_register(mis_ctx* c, int64_t* owner, uint8_t* why) {
 mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out, int64_t stats[4]) {
   if (!c || !n_out) return MIS_E_ARG;
   if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
+  TRY(c, flush_frame(c));
   cudaSetDevice(c->device);
   if (c->dirty) TRY(c, run_build_order(c));
   const size_t px = (size_t)c->W * c->H;

@@ -73,6 +73,10 @@ struct Ctx {
 
   // ---- frame
   bool have_frame = false;
+  bool frame_pending = false;        // mis_register's frame prep, launched behind the pattern readback
+  const float* frame_src = nullptr;  // its depth source
+  int64_t* hpin = nullptr;           // pinned readback buffer (16 x int64)
+  cudaEvent_t rb_ev = nullptr;       // completion of a readback copy
   int W = 0, H = 0;
   mis_intrinsics intr{};
   float pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
@@ -139,6 +143,7 @@ AccView acc_view(Ctx* c);
 
 // sort.cu
 cudaError_t build_order(Ctx* c);      // K13: tuple sort, gather, segments, chunks
+cudaError_t flush_frame(Ctx* c);      // a deferred frame prep (api.cu)
 cudaError_t build_pattern(Ctx* c);    // BSR pattern + slot tables (incl. features)
 cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
 cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);

@@ -395,9 +395,14 @@ cudaError_t build_pattern(Ctx* c) {
   count_launches(2);   // row count, plan (+ the CUB scan)
   CK(cudaGetLastError());
   // the single host readback of the frame: nnz, segment / chunk counts, cluster plan
+  // (pinned, so the copy is asynchronous: a deferred frame prep is queued behind it and runs
+  // while the host waits on the copy's event)
   int64_t h[8];
-  CK(cudaMemcpyAsync(h, info, sizeof(h), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpyAsync(c->hpin, info, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->rb_ev, c->st));
+  CK(flush_frame(c));
+  CK(cudaEventSynchronize(c->rb_ev));
+  memcpy(h, c->hpin, sizeof(h));
   const int64_t nnz = h[0];
   c->nnzb = nnz;
   c->nseg = h[1];
