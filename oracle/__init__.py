@@ -39,7 +39,7 @@ class or_params(C.Structure):
                 ("eps_d", C.c_double), ("eps_n_deg", C.c_double),
                 ("tau_z", C.c_double), ("delta_deg", C.c_double), ("trunc", C.c_double), ("omega_max", C.c_double),
                 ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_double),
-                ("solve_mode", C.c_int32)]
+                ("solve_mode", C.c_int32), ("lm", C.c_int32), ("lm_mu0", C.c_double)]
 
 
 class or_frame(C.Structure):
@@ -85,7 +85,7 @@ def lib():
             L.or_solve.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_double, C.c_int32, C.c_int32, C.c_void_p]
             L.or_solve.restype = C.c_int32
-            L.or_register.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_register.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_warp_model.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_fuse.argtypes = [P(or_params), P(or_model), P(or_frame), C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -111,7 +111,7 @@ def _i32(a):
 
 PAPER_DEFAULTS = dict(k=4, n_nbr=4, w_data=1.0, w_pt=1.0, w_reg=1e4, w_corr=10.0,
                       eps_d=15.0, eps_n_deg=10.0, tau_z=10.0, delta_deg=10.0, trunc=40.0, omega_max=10.0,
-                      gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1)
+                      gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1, lm=0, lm_mu0=1e-3)
 
 
 def params(**kw) -> or_params:
@@ -244,12 +244,15 @@ def solve(sysd, m, lam, mode, pcg_iters):
     return x, it
 
 
-def register(prm: or_params, pb: Problem, fr: Frame, Rt0=None):
+def register(prm: or_params, pb: Problem, fr: Frame, Rt0=None, with_accepted=False):
     m = pb.g.shape[0]
     Rt = identity_state(m) if Rt0 is None else np.array(Rt0, np.float64, copy=True)
     G = prm.gn_iters
     E = np.zeros((G + 1, 5)); na = np.zeros(G + 1, np.int64)
-    lib().or_register(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(E), _p(na))
+    acc = np.zeros(G + 1, np.int32)
+    lib().or_register(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(E), _p(na), _p(acc))
+    if with_accepted:
+        return Rt, E, na, acc
     return Rt, E, na
 
 

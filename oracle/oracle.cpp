@@ -704,20 +704,58 @@ int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bc
 }
 
 void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
-                 double* energy, int64_t* n_assoc) {
+                 double* energy, int64_t* n_assoc, int32_t* accepted) {
   std::vector<int32_t> fidx;
   std::vector<double> fw;
   feature_skin(p, prm->k, fidx, fw);   // O1 on the (fixed) node positions
+  if (!prm->lm) {
+    for (int it = 0; it <= prm->gn_iters; ++it) {
+      System S(p->m);
+      assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);
+      for (int a = 0; a < 4; ++a) energy[5 * it + a] = S.E[a];
+      energy[5 * it + 4] = total_energy(prm, S.E);
+      n_assoc[it] = S.n_assoc;
+      if (accepted) accepted[it] = 1;
+      if (it == prm->gn_iters) break;   // final energy only
+      std::vector<double> x;
+      solve_system(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+      update_nodes(p->m, x, Rt);
+    }
+    return;
+  }
+  // Levenberg-Marquardt, Marquardt damping H + mu diag(H) (R-A29)
+  const size_t ns = 12 * (size_t)p->m;
+  std::vector<double> base(Rt, Rt + ns);   // last accepted state
+  System acc(p->m);                        // its normal equations
+  double E_acc = 0.0, mu = prm->lm_mu0;
   for (int it = 0; it <= prm->gn_iters; ++it) {
     System S(p->m);
-    assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);
+    assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);   // at the trial state
     for (int a = 0; a < 4; ++a) energy[5 * it + a] = S.E[a];
-    energy[5 * it + 4] = total_energy(prm, S.E);
+    const double E = total_energy(prm, S.E);
+    energy[5 * it + 4] = E;
     n_assoc[it] = S.n_assoc;
-    if (it == prm->gn_iters) break;   // final energy only
+    const bool ok = it == 0 || E < E_acc;
+    if (accepted) accepted[it] = ok ? 1 : 0;
+    if (ok) {
+      std::copy(Rt, Rt + ns, base.begin());
+      acc = S;
+      E_acc = E;
+      if (it > 0) mu *= 0.5;
+    } else {
+      std::copy(base.begin(), base.end(), Rt);
+      mu *= 10.0;
+    }
+    if (it == prm->gn_iters) break;   // the final trial is only evaluated
+    System D = acc;                   // damped copy: diagonal entries of H times (1 + mu)
+    for (int j = 0; j < p->m; ++j) {
+      std::map<std::pair<int, int>, B6>::iterator d = D.blk.find(std::make_pair(j, j));
+      if (d != D.blk.end())
+        for (int a = 0; a < 6; ++a) d->second[7 * a] *= 1.0 + mu;
+    }
     std::vector<double> x;
-    solve_system(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
-    update_nodes(p->m, x, Rt);
+    solve_system(D, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+    update_nodes(p->m, x, Rt);   // Rt == base here: the step starts from the accepted state
   }
 }
 

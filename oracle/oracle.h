@@ -26,6 +26,8 @@ typedef struct {
   int32_t gn_iters, pcg_iters;
   double lambda;                        /* GN damping, R-A16                         */
   int32_t solve_mode;                   /* 0 = EXACT, 1 = MIRROR (same P as GPU)     */
+  int32_t lm;                           /* 1: Levenberg-Marquardt, R-A29 */
+  double lm_mu0;                        /* initial Marquardt damping (1e-3)    */
 } or_params;
 
 typedef struct {
@@ -88,9 +90,17 @@ int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bc
                  const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x);
 /* O3: fixed-iteration Gauss-Newton registration.  Rt (m*12, R row-major + t)
  * is the initial state on entry and the result on exit.  energy: (G+1)*5 (start
- * of each iteration, then final), n_assoc: G+1. */
+ * of each iteration, then final), n_assoc: G+1.
+ * prm->lm = 1: Levenberg-Marquardt instead ("Levenberg-Marquardt"; damping
+ * and schedule S:290; R-A29): iteration it evaluates the energy of the trial
+ * state (energy[it], it = 0 is the start), accepts it if it = 0 or the total is
+ * strictly lower than the last accepted one (accepted[it] = 1; mu *= 0.5 for it > 0),
+ * else restores the last accepted state and keeps its system (mu *= 10); then solves
+ * (H' + lambda I) x = b with H' = H whose diagonal entries are scaled by (1 + mu) and
+ * steps from the accepted state.  Entry G is the final trial, kept if it is accepted.
+ * accepted (G+1) may be NULL. */
 void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
-                 double* energy, int64_t* n_assoc);
+                 double* energy, int64_t* n_assoc, int32_t* accepted);
 /* O4: apply the field: live world state x_hat, unit normals; advanced nodes g+t. */
 void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
                    double* g_out);

@@ -647,3 +647,76 @@ def test_fusion_colour_normal_golden():
     p = 1 + 0   # first lifted point = pixel (1, 1) in row-major order
     assert np.allclose(out["xyz"][p], [(1 - it["cx"]) * 12 / 40, (1 - it["cy"]) * 12 / 40, 12], atol=1e-12)
     assert out["weight"][p] == 1.0 and out["stamp"][p] == 4 and np.allclose(out["rgb"][p], 1.0)
+
+
+# ------------------------------------------------------------------ NEXT-3: Levenberg-Marquardt (R-A29)
+def _lm_dense(prm, pb, fr, G, mu0):
+    """Levenberg-Marquardt written out with dense numpy algebra on the oracle's assembly
+    (an independent implementation of the schedule: P:166 LM, S:303 Marquardt damping
+    lambda diag(J^T J), x10 on rejection, x0.5 on acceptance; the base lambda I of R-A16)."""
+    m = pb.g.shape[0]
+    Rt = O.identity_state(m)
+    base, acc_sys, E_acc, mu = Rt.copy(), None, 0.0, mu0
+    Es, accs = [], []
+    for it in range(G + 1):
+        s = O.system(prm, pb, fr, Rt)
+        E = s["energy"][4]
+        ok = it == 0 or E < E_acc
+        Es.append(E)
+        accs.append(int(ok))
+        if ok:
+            base, acc_sys, E_acc = Rt.copy(), s, E
+            if it > 0:
+                mu *= 0.5
+        else:
+            Rt = base.copy()
+            mu *= 10.0
+        if it == G:
+            break
+        H = O.dense_H(acc_sys, m)
+        A = H + np.diag(mu * np.diag(H)) + prm.lambda_ * np.eye(6 * m)
+        x = np.linalg.solve(A, acc_sys["rhs"])
+        Rn = base.copy()
+        for j in range(m):
+            Rn[j, :9] = (O.exp_so3(x[6 * j:6 * j + 3]) @ base[j, :9].reshape(3, 3)).ravel()
+            Rn[j, 9:] = base[j, 9:] + x[6 * j + 3:6 * j + 6]
+        Rt = Rn
+    return Rt, np.array(Es), np.array(accs)
+
+
+def test_lm_matches_dense_reimplementation():
+    """The oracle's LM loop (EXACT solves) against the dense numpy rewrite: same trial
+    energies, same accept / reject decisions (including rejections), same final state."""
+    sc, pb, fr, _ = scene_problem("c1")
+    G = 8
+    prm = O.params(gn_iters=G, solve_mode=0, lm=1, lm_mu0=1e-3)
+    Rt, E, na, acc = O.register(prm, pb, fr, with_accepted=True)
+    Rd, Ed, accd = _lm_dense(prm, pb, fr, G, 1e-3)
+    assert (acc == accd).all(), (acc, accd)
+    assert (acc == 0).any() and (acc[1:] == 1).any()   # both branches exercised
+    assert np.abs(E[:, 4] - Ed).max() < 1e-9 * Ed[0]
+    assert np.abs(Rt - Rd).max() < 1e-9
+
+
+def test_lm_zero_damping_all_accepted_is_gauss_newton():
+    """mu0 = 0 and every trial accepted (GN decreasing here for 2 iterations): LM is GN."""
+    sc, pb, fr, _ = scene_problem("c1")
+    gn = O.params(gn_iters=2, solve_mode=1)
+    lm = O.params(gn_iters=2, solve_mode=1, lm=1, lm_mu0=0.0)
+    Rg, Eg, _ = O.register(gn, pb, fr)
+    Rl, El, _, acc = O.register(lm, pb, fr, with_accepted=True)
+    assert (acc == 1).all()
+    assert np.array_equal(Rg, Rl) and np.array_equal(Eg, El)
+
+
+def test_lm_accepted_energy_strictly_decreasing_and_final_is_best():
+    """the accepted energy sequence decreases; the returned state is the last
+    accepted one (its energy, re-evaluated, is the minimum of the accepted energies)."""
+    sc, pb, fr, _ = scene_problem("c1")
+    prm = O.params(gn_iters=10, solve_mode=1, lm=1, lm_mu0=1e-3)
+    Rt, E, na, acc = O.register(prm, pb, fr, with_accepted=True)
+    ea = E[acc == 1, 4]
+    assert (np.diff(ea) < 0).all(), ea
+    Ef = O.system(prm, pb, fr, Rt)["energy"][4]
+    assert abs(Ef - ea[-1]) < 1e-9 * ea[0]
+    assert (E[acc == 0, 4] >= ea.min()).all()
