@@ -252,6 +252,43 @@ def run_mis(args, rank, world, local_rank):
     M.mis_prof_enable(ctx.ptr, False)
     breakdown = M.mis_prof_read(ctx.ptr, reset=True)
 
+    # ---------------- NEXT-3: the same step with Levenberg-Marquardt registration (MIS_F_LM),
+    # device-timed the same way (events at step boundaries, L2 flushed), single GPU only
+    lm_out = None
+    if world == 1 and not args.no_lm:
+        plm = params_for(cfg, M)
+        plm.flags |= M.MIS_F_LM
+        ctx_lm = M.Context(plm, device=local_rank, stream=stream.cuda_stream)
+
+        def step_lm():
+            M.mis_set_model(ctx_lm.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"],
+                            capacity=cap)
+            M.mis_set_graph(ctx_lm.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+            M.mis_register(ctx_lm.ptr, depth_d, intr, pose, fs_d, fd_d, report=False)
+            M.mis_warp(ctx_lm.ptr)
+            return M.mis_fuse(ctx_lm.ptr, rgb_d, 1)
+
+        for _ in range(args.warmup):
+            step_lm()
+        torch.cuda.synchronize()
+        evl = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            flush.zero_()
+            evl[k][0].record(stream)
+            step_lm()
+            evl[k][1].record(stream)
+        torch.cuda.synchronize()
+        lm_ms = sum(a.elapsed_time(b) for a, b in evl) / K
+        M.mis_set_model(ctx_lm.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
+        M.mis_set_graph(ctx_lm.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+        rl = M.report_dict(M.mis_register(ctx_lm.ptr, depth_d, intr, pose, fs_d, fd_d, report=True))
+        lm_out = {"ms_per_step": round(lm_ms, 4), "value": round(1e3 / lm_ms, 3), "unit": UNIT,
+                  "what": "same step with Levenberg-Marquardt registration (MIS_F_LM: G trials + final evaluation, "
+                          "accept / reject and Marquardt damping on the device)",
+                  "accepted": [int(v) for v in rl["accepted"]],
+                  "E_first": float(rl["energy"][0, 4]), "E_final_trial": float(rl["energy"][cfg.gn_iters, 4])}
+        ctx_lm.close()
+
     # ---------------- roofline of the dominant kernel (timed region: events around K3a, K3b, solver)
     hbm, _, peak_kind = peaks()
     groups = {k: v for k, v in prof.items() if v[1] > 0 and v[0] > 0}
@@ -327,6 +364,7 @@ def run_mis(args, rank, world, local_rank):
                         "programmatic-dependent-launch chain)",
         "ms_per_step_with_kernel_events": round(kev["dev_ms_max"] / K, 4),
         "pcg_phases_us_last_launch": pcg_phases,
+        "lm": lm_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
@@ -419,6 +457,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="mis", choices=["mis", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-lm", action="store_true", help="skip the Levenberg-Marquardt (MIS_F_LM) timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one model over the ranks (else replicas)")
     args = ap.parse_args()

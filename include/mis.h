@@ -69,6 +69,17 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    whenever the system fits in one cluster's shared memory)       */
 #define MIS_F_STANDARD_PCG 8u   /* cluster kernel: textbook PCG recurrences (2 barriers/iteration)
                                    instead of the pipelined variant (1 barrier/iteration)         */
+#define MIS_F_LM          16u   /* Levenberg-Marquardt instead of Gauss-Newton (SURVEY
+                                   NEXT-3; reading A29): iteration it evaluates the trial state,
+                                   accepts it if it = 0 or its weighted total energy is strictly
+                                   lower than the last accepted one (damping mu x 0.5, mu_0 =
+                                   1e-3) else restores the last accepted state and its
+                                   system (mu x 10), then solves (H' + lambda I) x = b, H' = H
+                                   with its diagonal entries times (1 + mu), from that state.
+                                   The last trial is evaluated too (energy row [iters]) and kept
+                                   only if accepted.  Per-iteration decisions in report n_guard.
+                                   Needs the register-resident cluster PCG (systems of C1-C3
+                                   size, pipelined recurrence): else MIS_E_ARG                      */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {
@@ -103,7 +114,8 @@ typedef struct {
   int64_t n_segments;                  /* distinct kNN tuples in the model                  */
   int32_t solver_cluster;              /* CTAs of the cluster-resident PCG (0: grid kernel)  */
   int32_t reserved;
-  int64_t n_guard[MIS_MAX_GN + 1];     /* reserved (0: the association runs in fp64, no guard band) */
+  int64_t n_guard[MIS_MAX_GN + 1];     /* MIS_F_LM: 1 if the trial of iteration i (row [iters]: the
+                                          final one) was accepted, else 0; Gauss-Newton: 0        */
 } mis_report;
 
 int32_t mis_abi_version(void);

@@ -431,7 +431,8 @@ mis_status mis_destroy(mis_ctx* c) {
                  &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
                  &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
                  &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->pcg_pptr, &c->pcg_pc, &c->pcg_push,
-                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->ulist, &c->cub_tmp};
+                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->ulist, &c->cub_tmp, &c->lm, &c->Hval2, &c->rhs2,
+                 &c->Rt_acc};
   for (DBuf* b : all) free_buf(*b);
   for (int s = 0; s < 2; ++s) {
     ModelBufs& B = c->mb[s];
@@ -752,6 +753,11 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     r.slot = slot;
     r.rep_energy = rep_energy(c);
     r.rep_nassoc = rep_nassoc(c);
+    const bool lm = (c->prm.flags & MIS_F_LM) && !dbg;
+    r.lm = lm ? reinterpret_cast<const LmDev*>(c->lm.p) : nullptr;
+    r.Hval_alt = lm ? c->Hval2.as<float>() : nullptr;
+    r.rhs_alt = lm ? c->rhs2.as<float>() : nullptr;
+    if (lm) r.Minv = nullptr;   // the damped inverses are built by the solver once it has decided
     launch_finalize(r, c->st);
   }
   c->acc_dirty = false;
@@ -797,6 +803,14 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.pc = c->pcg_pc.as<int32_t>();
   s.push = c->pcg_push.as<int32_t>();
   s.npush = c->pcg_npush.as<int32_t>();
+  const bool lm = (c->prm.flags & MIS_F_LM) && update;
+  s.lm = lm ? reinterpret_cast<LmDev*>(c->lm.p) : nullptr;
+  s.lm_mu0 = 1e-3f;
+  s.Hval_alt = lm ? c->Hval2.as<float>() : nullptr;
+  s.rhs_alt = lm ? c->rhs2.as<float>() : nullptr;
+  s.Rt_acc = lm ? c->Rt_acc.as<double>() : nullptr;
+  s.rep_energy = rep_energy(c);
+  s.rep_flags = rep_nassoc(c) + MIS_MAX_GN + 1;   // the report's n_guard row
   return s;
 }
 
@@ -878,14 +892,37 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
     if ((s = mis_set_features(c, mem, n_feat, feat_src, feat_dst)) != MIS_OK) return s;
   if ((s = prepare(c)) != MIS_OK) return s;
   const int G = c->prm.gn_iters;
+  const bool lm = c->prm.flags & MIS_F_LM;
+  if (lm) {   // the register-resident pipelined cluster PCG carries the LM decisions
+    const bool ok = c->cl_size > 0 && c->cluster_ok && 6 * c->cl_max_rows <= 512 &&
+                    !(c->prm.flags & (MIS_F_GRID_SOLVER | MIS_F_STANDARD_PCG)) && c->world == 1;
+    if (!ok) return fail(c, MIS_E_ARG, "MIS_F_LM needs the register-resident cluster PCG (single GPU)");
+    const bool fresh = !c->lm.p;
+    TRY(c, ensure(c, c->lm, 64));
+    if (fresh) TRY(c, cudaMemsetAsync(c->lm.p, 0, 64, c->st));
+    TRY(c, ensure(c, c->Hval2, (size_t)c->nnzb * 36 * 4));
+    TRY(c, ensure(c, c->rhs2, (size_t)c->m * 6 * 4));
+    TRY(c, ensure(c, c->Rt_acc, (size_t)c->m * 96));
+  }
   TRY(c, cudaMemsetAsync(c->rep.p, 0, kRepBytes, c->st));
   for (int it = 0; it < G; ++it) {
     if ((s = assemble(c, false, it)) != MIS_OK) return s;
     ProfScope ps(c, P_SOLVE, 1);
-    TRY(c, run_solve(c, solve_args(c, it, true, c->prm.pcg_iters)));
+    const SolveArgs sa = solve_args(c, it, true, c->prm.pcg_iters);
+    if (lm) {   // no grid fallback: it has no LM logic
+      TRY(c, launch_solve(sa, c->num_sms, c->st));
+      c->last_solver = sa.cluster_size;
+    } else {
+      TRY(c, run_solve(c, sa));
+    }
   }
-  if (c->prm.flags & MIS_F_FINAL_ENERGY)
+  if ((c->prm.flags & MIS_F_FINAL_ENERGY) || lm)
     if ((s = assemble(c, false, G)) != MIS_OK) return s;
+  if (lm) {   // the last trial is kept only if accepted
+    ProfScope ps(c, P_SOLVE, 1);
+    launch_lm_finish(c->m, G, reinterpret_cast<const LmDev*>(c->lm.p), rep_energy(c), rep_nassoc(c) + MIS_MAX_GN + 1,
+                     c->Rt64.as<double>(), c->Rt_acc.as<double>(), c->node32.as<float>(), c->st);
+  }
   TRY(c, cudaGetLastError());
   if (rep) return fill_report(c, rep, G);
   return MIS_OK;

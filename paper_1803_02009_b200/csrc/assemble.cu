@@ -732,6 +732,10 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
   if (threadIdx.x < 72) rtab[threadIdx.x / 36][threadIdx.x % 36] = make_recipe(threadIdx.x % 36, threadIdx.x < 36);
   __syncthreads();
   pdl_wait();      // K3a/K3b/K4 accumulators
+  if (r.lm && r.lm->acc_buf == 0) {   // LM: keep the accepted system, write the trial's into the other buffer
+    r.Hval = r.Hval_alt;
+    r.rhs = r.rhs_alt;
+  }
   pdl_trigger();   // the solver may launch (it waits for this grid's completion before reading)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

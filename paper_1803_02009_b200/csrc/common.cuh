@@ -127,6 +127,14 @@ void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_
 // [E_data, E_pt x, E_pt y, E_pt z, n_assoc]; padded to 4.
 __host__ __device__ inline int rec_stride(int K) { return (52 * (K * (K + 1) / 2) + 18 * K + 5 + 3) & ~3; }
 
+// Levenberg-Marquardt state on the device (MIS_F_LM, reading A29): the
+// Marquardt damping, the last accepted energy and which of the two system buffers
+// (0: Hval / rhs, 1: the alternates) holds the last accepted normal equations.
+struct LmDev {
+  double mu, E_acc;
+  int32_t acc_buf, pad;
+};
+
 struct FinalArgs {
   int64_t nnzb;
   int64_t nup;                // off-diagonal upper entries ((nnzb - m) / 2)
@@ -144,6 +152,8 @@ struct FinalArgs {
   int slot;                   // report slot of this assembly (-1: none)
   double* rep_energy;         // (MIS_MAX_GN+1)*5
   double* rep_nassoc;         // 2*(MIS_MAX_GN+1): association counts, fp64 guard counts
+  const LmDev* lm;            // LM: write the system into the buffer not holding the accepted one
+  float *Hval_alt, *rhs_alt;
 };
 void launch_finalize(const FinalArgs& r, cudaStream_t s);
 
@@ -194,7 +204,17 @@ struct SolveArgs {
   int minv_ready;             // Minv already built by the record reduction (single GPU)
   unsigned long long* tstamp; // 8 %globaltimer stamps of the phases (rank 0, thread 0)
   const int32_t *pptr, *pc, *push, *npush;   // cluster variant: per-rank SpMV pieces and halo lists (per frame)
+  // Levenberg-Marquardt (cluster kernel, register-resident variant only): accept / reject the
+  // trial whose energy the finalisation just wrote, pick the system, damp, keep the base state
+  LmDev* lm;                  // nullptr: Gauss-Newton
+  float lm_mu0;
+  const float *Hval_alt, *rhs_alt;
+  double* Rt_acc;             // m x 12: last accepted state
+  const double* rep_energy;   // (MIS_MAX_GN+1) x 5, the trial energies
+  double* rep_flags;          // MIS_MAX_GN+1: 1 = trial accepted
 };
+void launch_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags, double* Rt64,
+                      const double* Rt_acc, float* node32, cudaStream_t s);
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;

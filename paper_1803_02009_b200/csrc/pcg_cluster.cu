@@ -508,7 +508,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
                                                   const float* H, const float* Mi, double* g_last, double* g_first,
                                                   unsigned long long* ts, const int* pptr, const int* pc, float* part,
                                                   const int* push, int npush, const HReg& R, uint64_t* bars,
-                                                  uint32_t in_bytes) {
+                                                  uint32_t in_bytes, float lam_t) {
   const int t = threadIdx.x, nv = a.max_rows * 6, n6 = 6 * nr;
   const bool own = t < n6;
   const int ti = t / 6, tc = t - 6 * (t / 6);
@@ -535,7 +535,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
   __syncthreads();
   replicate(cl, Z0, us, r0, push, npush);
   cl.sync();
-  spmv_local(R, pptr, pc, part, col, H, Z0, us, a.lambda, ws, nr);   // w = A u (own element: this thread's write)
+  spmv_local(R, pptr, pc, part, col, H, Z0, us, lam_t, ws, nr);   // w = A u (own element: this thread's write)
   if (own) w = ws[t];
   __syncthreads();
   double gprev = 1.0, aprev_den = 1.0, g0 = 0.0, g = 0.0;
@@ -610,7 +610,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     // alpha only enters the fp32 vector updates: one fp32 division instead of an fp64 one
     const float fa = (float)g / (float)den;
     if (st1) ts[6] = gtimer();
-    spmv_local(R, pptr, pc, part, col, H, Zb, ms, a.lambda, ns, nr);   // n = A m (own element: this thread's write)
+    spmv_local(R, pptr, pc, part, col, H, Zb, ms, lam_t, ns, nr);   // n = A m (own element: this thread's write)
     if (st1) ts[13] = gtimer();
     const float fb = (float)beta;
     if (own) {
@@ -677,14 +677,34 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   unsigned long long* ts = a.tstamp + 16 * rank;
   if (stamp) ts[0] = gtimer();
 
+  // ---- Levenberg-Marquardt (MIS_F_LM): every CTA takes the same decision on the trial whose
+  // energy the finalisation just reported (accept if first or strictly lower than the last
+  // accepted, reading A29) before rank 0 updates the state (after the PCG's first cluster
+  // barrier): the system to solve is the trial's (accept) or the kept one (reject)
+  const bool lm = a.lm != nullptr;
+  bool lm_accept = true;
+  double lm_mu = 0.0, lm_E = 0.0;
+  int lm_src = 0;
+  if (lm) {
+    const double Et = a.rep_energy[5 * a.gn_it + 4];
+    const LmDev st = *a.lm;
+    lm_accept = a.gn_it == 0 || Et < st.E_acc;
+    lm_mu = a.gn_it == 0 ? (double)a.lm_mu0 : (lm_accept ? 0.5 * st.mu : 10.0 * st.mu);
+    lm_E = lm_accept ? Et : st.E_acc;
+    lm_src = lm_accept ? 1 - st.acc_buf : st.acc_buf;
+  }
+  const float* Hsys = lm && lm_src == 1 ? a.Hval_alt : a.Hval;
+  const float* bsys = lm && lm_src == 1 ? a.rhs_alt : a.rhs;
+
   // ---- phase 0: the rank's rows of H, its block inverses and its nodes' fp64 states by bulk
   // copies (one thread issues them, completion on an mbarrier) while the other threads load
-  // the lists of this rank (built once per frame), columns and b
-  const float* Hg = a.Hval + 36 * (int64_t)e0;
+  // the lists of this rank (built once per frame), columns and b.  (LM: the inverses depend
+  // on the damping decided here, so they are built below from the diagonal blocks.)
+  const float* Hg = Hsys + 36 * (int64_t)e0;
   if (t == 0) {
-    mbar_expect_tx(&tma_bar, (uint32_t)(144 * ne + 144 * nr + 96 * nr));
+    mbar_expect_tx(&tma_bar, (uint32_t)(144 * ne + (lm ? 0 : 144 * nr) + 96 * nr));
     bulk_g2s(H, Hg, (uint32_t)(144 * ne), &tma_bar);
-    bulk_g2s(Mi, a.Minv + 36 * (int64_t)r0, (uint32_t)(144 * nr), &tma_bar);
+    if (!lm) bulk_g2s(Mi, a.Minv + 36 * (int64_t)r0, (uint32_t)(144 * nr), &tma_bar);
     bulk_g2s(sm + L.rt, a.nd.Rt64 + 12 * (int64_t)r0, (uint32_t)(96 * nr), &tma_bar);
   }
   const int sticky = *a.numeric_flag;   // set by an earlier launch of this registration
@@ -696,7 +716,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   for (int i = t; i < npush; i += kCT) push[i] = g_push[i];
   for (int k = t; k < ne; k += kCT) col[k] = a.col[e0 + k];
   for (int i = t; i < 6 * nr; i += kCT) {
-    r[i] = a.rhs[6 * (int64_t)r0 + i];
+    r[i] = bsys[6 * (int64_t)r0 + i];
     x[i] = 0.f;
     p[i] = 0.f;
     Ap[i] = 0.f;
@@ -709,6 +729,59 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   // H is staged in shared memory (the register units read 72-byte row groups that would
   // scatter global requests; units beyond the registers, for larger systems, read it there)
   mbar_wait(&tma_bar, 0);
+  float lam_t = a.lambda;   // this thread's diagonal shift (register-resident variant: element t)
+  if (lm) {
+    double* rt = reinterpret_cast<double*>(sm + L.rt);
+    // base state of the step: the trial (accepted: it becomes the kept state) or the kept one
+    for (int q = t; q < 12 * nr; q += kCT) {
+      if (lm_accept) a.Rt_acc[12 * (int64_t)r0 + q] = rt[q];
+      else rt[q] = a.Rt_acc[12 * (int64_t)r0 + q];
+    }
+    // damped block-Jacobi inverses: (H_jj with its diagonal times (1 + mu) + (lambda + guard) I)^-1,
+    // fp64 Gauss-Jordan, one warp per node (lane rr < 6 holds row rr)
+    const int wi = t >> 5, l = t & 31, rr = l < 6 ? l : 0;
+    for (int i = wi; i < nr; i += kWarps) {
+      const int k0 = pc[pptr[i]] & 0xffffff, k1 = i + 1 < nr ? (pc[pptr[i + 1]] & 0xffffff) : ne;
+      int kd = k0;
+      for (int k = k0; k < k1; ++k)
+        if (col[k] == r0 + i) kd = k;
+      const float* B = H + 36 * kd;
+      double row[12], trc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) trc += (double)B[7 * q] * (1.0 + lm_mu);
+      const double guard = 1e-9 * trc / 6.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const double h = (double)B[6 * rr + q];
+        row[q] = q == rr ? h * (1.0 + lm_mu) + (double)a.lambda + guard : h;
+        row[6 + q] = q == rr ? 1.0 : 0.0;
+      }
+      bool pd = true;
+#pragma unroll
+      for (int pv_i = 0; pv_i < 6; ++pv_i) {
+        const double pv = __shfl_sync(0xffffffffu, row[pv_i], pv_i);
+        if (!(pv > 0.0)) pd = false;
+        const double ipv = 1.0 / pv, f = row[pv_i] * ipv;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+          const double pq = __shfl_sync(0xffffffffu, row[q], pv_i);
+          row[q] = rr == pv_i ? pq * ipv : row[q] - f * pq;
+        }
+      }
+      if (l < 6)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) Mi[36 * i + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
+    }
+    if (t < 6 * nr) {   // the Marquardt term of element t: lambda + mu H_tt
+      const int ti = t / 6, tc = t - 6 * ti;
+      const int k0 = pc[pptr[ti]] & 0xffffff, k1 = ti + 1 < nr ? (pc[pptr[ti + 1]] & 0xffffff) : ne;
+      int kd = k0;
+      for (int k = k0; k < k1; ++k)
+        if (col[k] == r0 + ti) kd = k;
+      lam_t = (float)((double)a.lambda + lm_mu * (double)H[36 * kd + 7 * tc]);
+    }
+    __syncthreads();
+  }
   if (stamp) ts[1] = gtimer();
   if (a.pcg_iters <= 0 && !a.do_update) return;
   HReg R;
@@ -718,8 +791,14 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (a.pipelined && 6 * a.max_rows <= kCT) {
     const uint32_t in_bytes = (uint32_t)(24 * a.npush[kMaxCluster + rank] + 16 * (cs - 1));
     pcg_pipelined_reg(a, cl, sm, L, rank, cs, r0, nr, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
-                      npush, R, pcg_bar, in_bytes);
+                      npush, R, pcg_bar, in_bytes, lam_t);
     if (stamp) ts[3] = ts[2];
+    if (lm && rank == 0 && t == 0) {   // every CTA has read the LM state (first cluster barrier passed)
+      a.lm->mu = lm_mu;
+      a.lm->E_acc = lm_E;
+      a.lm->acc_buf = lm_src;
+      a.rep_flags[a.gn_it] = lm_accept ? 1.0 : 0.0;
+    }
   } else if (a.pipelined) {
     pcg_pipelined(a, cl, sm, L, rank, cs, r0, nr, lrp, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
                   npush, R);
@@ -911,6 +990,26 @@ cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_pcg_cluster, a);
+}
+
+// LM: the last trial (its energy in report slot `slot`) is kept only if accepted; otherwise
+// the kept state is restored (fp64 master and its fp32 copy)
+__global__ void k_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags,
+                            double* Rt64, const double* Rt_acc, float* node32) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
+  const bool accept = rep_energy[5 * slot + 4] < lm->E_acc;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q == 0) rep_flags[slot] = accept ? 1.0 : 0.0;
+  if (accept || q >= 12 * (int64_t)m) return;
+  const double v = Rt_acc[q];
+  Rt64[q] = v;
+  node32[16 * (q / 12) + q % 12] = (float)v;
+}
+void launch_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags, double* Rt64,
+                      const double* Rt_acc, float* node32, cudaStream_t s) {
+  launch_pdl(k_lm_finish, dim3((unsigned)((12 * (int64_t)m + 255) / 256)), dim3(256), 0, s, m, slot, lm, rep_energy,
+             rep_flags, Rt64, Rt_acc, node32);
 }
 
 }  // namespace mis

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("MIS_LIB_PATH", os.path.join(_HERE, "libmis.so"))   # 
 MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
 MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 2, 4, 8
+MIS_F_LM = 16   # Levenberg-Marquardt (include/mis.h)
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
 
@@ -214,7 +215,8 @@ def report_dict(rep: mis_report):
                 n_assoc=np.array([rep.n_assoc[i] for i in range(it + 1)]),
                 pcg_rel_res=np.array([rep.pcg_rel_res[i] for i in range(it)]),
                 nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster,
-                n_guard=np.array([rep.n_guard[i] for i in range(it + 1)]))
+                n_guard=np.array([rep.n_guard[i] for i in range(it + 1)]),
+                accepted=np.array([rep.n_guard[i] for i in range(it + 1)]))   # MIS_F_LM decisions
 
 
 def mis_get_nodes(ctx, out):
