@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
   float* F = reinterpret_cast<float*>(smem4) + warp * (32 * kTcFSP);
   float* Rec = reinterpret_cast<float*>(smem4) + kWarps * 32 * kTcFSP + warp * RT;
-  __shared__ int32_t slot_sm[kWarps][P];
+  __shared__ int32_t slot_sm[kWarps][P + K];   // the chunk's BSR slots, then its K node ids
   int32_t* slots = slot_sm[warp];
   // where each summed entry goes: inv[q] = record index of position q of the dumped sums
   // (c' 32 x 32 at 0, e' 24 x 24 at 1024; upper triangles), -1: not part of the system
@@ -532,6 +532,26 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     inv[q] = (int16_t)d;
   }
   for (int q = lane; q < RT; q += 32) Rec[q] = 0.f;   // entries no fragment maps to stay zero
+  // commit items of each lane (item it = lane + 32 k), decoded once: kind (0 data, 1 moments,
+  // 2 node rhs, 3 node moments) | record index (pair or node slot) << 2 | offset in the
+  // destination record << 10 | offset in Rec (floats) << 18; ~0u: no item
+  constexpr int NIT = (13 * P + 6 * K + 31) / 32;
+  __shared__ uint32_t cdesc[NIT][32];
+  for (int q = threadIdx.x; q < NIT * 32; q += blockDim.x) {
+    const int it = q;   // = lane + 32 k with k = q / 32
+    uint32_t d = ~0u;
+    if (it < 13 * P) {
+      const int pr = it / 13, qq = it - 13 * pr;
+      d = (qq < 9 ? 0u : 1u) | ((uint32_t)pr << 2) | ((uint32_t)(qq < 9 ? 4 * qq : 4 * (qq - 9)) << 10) |
+          ((uint32_t)(4 * it) << 18);
+    } else if (it < 13 * P + 6 * K) {
+      const int t2 = it - 13 * P, sl = t2 / 6, qq = t2 - 6 * sl;
+      d = qq < 3 ? (2u | ((uint32_t)sl << 2) | ((uint32_t)(2 * qq) << 10) | ((uint32_t)(52 * P + 20 * sl + 2 * qq) << 18))
+                 : (3u | ((uint32_t)sl << 2) | ((uint32_t)(4 * (qq - 3)) << 10) |
+                    ((uint32_t)(52 * P + 20 * sl + 8 + 4 * (qq - 3)) << 18));
+    }
+    cdesc[q / 32][q % 32] = d;
+  }
   __syncthreads();
   // this lane's 40 fragment positions -> record indices, packed in pairs (0xffff: dropped)
   uint32_t dmap[20];
@@ -564,7 +584,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     const int seg = ch.x;
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
     __syncwarp();
-    for (int q = lane; q < P; q += 32) slots[q] = a.seg_slot[(int64_t)seg * P + q];
+    if (lane < P) slots[lane] = a.seg_slot[(int64_t)seg * P + lane];
+    else if (lane < P + K) slots[lane] = nodes[lane - P];
     float dc[6][4], de[4][4];   // c' tiles (0,0..3),(1,2),(1,3); e' tiles (0,0..2),(1,2)
 #pragma unroll
     for (int t = 0; t < 6; ++t) dc[t][0] = dc[t][1] = dc[t][2] = dc[t][3] = 0.f;
@@ -625,26 +646,22 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     __syncwarp();
     int64_t next_chunk = 0;
     if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
-    for (int it = lane; it < 13 * P + 6 * K; it += 32) {
-      if (it < 13 * P) {
-        const int pr = it / 13, q = it - 13 * pr;   // data (q < 9) then moments: contiguous in the record
-        const float4 v = reinterpret_cast<const float4*>(Rec)[it];
-        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
-        const int64_t u = slots[pr];
-        float* dst = q < 9 ? a.acc.data + 36 * u + 4 * q : a.acc.mom + 16 * u + 4 * (q - 9);
-        atomicAdd(reinterpret_cast<float4*>(dst), v);
+#pragma unroll
+    for (int k = 0; k < NIT; ++k) {
+      const uint32_t d = cdesc[k][lane];
+      if (d == ~0u) continue;
+      const uint32_t kind = d & 3u, idx = (d >> 2) & 255u, off = (d >> 10) & 255u;
+      const float* src = Rec + (d >> 18);
+      if (kind == 2u) {
+        const float2 v = *reinterpret_cast<const float2*>(src);
+        if (v.x != 0.f || v.y != 0.f)
+          atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * (int64_t)slots[P + idx] + off), v);
       } else {
-        const int t2 = it - 13 * P, sl = t2 / 6, q = t2 - 6 * sl;
-        const int64_t nd = nodes[sl];
-        const float* rn = Rec + 52 * P + 20 * sl;
-        if (q < 3) {
-          const float2 v = reinterpret_cast<const float2*>(rn)[q];
-          if (v.x != 0.f || v.y != 0.f) atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * nd + 2 * q), v);
-        } else {
-          const float4 v = reinterpret_cast<const float4*>(rn + 8)[q - 3];
-          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
-            atomicAdd(reinterpret_cast<float4*>(a.acc.node_mom + 12 * nd + 4 * (q - 3)), v);
-        }
+        const float4 v = *reinterpret_cast<const float4*>(src);
+        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+        float* dst = kind == 0u ? a.acc.data + 36 * (int64_t)slots[idx]
+                   : kind == 1u ? a.acc.mom + 16 * (int64_t)slots[idx] : a.acc.node_mom + 12 * (int64_t)slots[P + idx];
+        atomicAdd(reinterpret_cast<float4*>(dst + off), v);
       }
     }
     __syncwarp();
