@@ -678,7 +678,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
 // the next assembly needs no memset:
 //   H(j,l) = w_data sum c c^T + w_pt PT(moments) + graph  (and its mirror H(l,j)),
 //   b_j = -(w_data sum c r_pl + w_pt sum w_j [a_j x r'; r']) + graph rhs.
-constexpr int kFB = 4;   // off-diagonal entries / nodes per warp (their loads overlap)
+#ifndef MIS_KFB
+#define MIS_KFB 4
+#endif
+constexpr int kFB = MIS_KFB;   // off-diagonal entries / nodes per warp (their loads overlap)
 
 // Entry l = 6 i + j of a block as a branch-free recipe over the staged D | Mo | G:
 //   h = w_data D[d] + G[l] + w_pt sum_k coef_k Mo[idx_k]
