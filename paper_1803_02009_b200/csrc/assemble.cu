@@ -553,13 +553,13 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     cdesc[q / 32][q % 32] = d;
   }
   __syncthreads();
-  // this lane's 40 fragment positions -> record indices, packed in pairs (0xffff: dropped)
-  uint32_t dmap[20];
+  // this lane's 36 fragment positions -> record indices, packed in pairs (0xffff: dropped)
+  uint32_t dmap[18];
   {
     const int tmi[6] = {0, 0, 0, 0, 1, 1}, tni[6] = {0, 1, 2, 3, 2, 3};
-    const int emi[4] = {0, 0, 0, 1}, eni[4] = {0, 1, 2, 2};
+    const int emi[3] = {0, 0, 0}, eni[3] = {0, 1, 2};
 #pragma unroll
-    for (int t = 0; t < 10; ++t) {
+    for (int t = 0; t < 9; ++t) {
       const bool e = t >= 6;
       const int r0 = 16 * (e ? emi[t - 6] : tmi[t]) + g, c0 = 8 * (e ? eni[t - 6] : tni[t]) + 2 * tig;
       int d4[4];
@@ -586,11 +586,13 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     __syncwarp();
     if (lane < P) slots[lane] = a.seg_slot[(int64_t)seg * P + lane];
     else if (lane < P + K) slots[lane] = nodes[lane - P];
-    float dc[6][4], de[4][4];   // c' tiles (0,0..3),(1,2),(1,3); e' tiles (0,0..2),(1,2)
+    // c' tiles (0,0..3),(1,2),(1,3); e' tiles (0,0..2) -- the e' rows >= 4k (r') pair only with
+    // each other there, which the system does not use
+    float dc[6][4], de[3][4];
 #pragma unroll
     for (int t = 0; t < 6; ++t) dc[t][0] = dc[t][1] = dc[t][2] = dc[t][3] = 0.f;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) de[t][0] = de[t][1] = de[t][2] = de[t][3] = 0.f;
+    for (int t = 0; t < 3; ++t) de[t][0] = de[t][1] = de[t][2] = de[t][3] = 0.f;
     for (int base = ch.y; base < ch.z; base += 32) {
       const int64_t i = base + lane;
       float* row = F + lane * kTcFSP;
@@ -621,7 +623,6 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
         mma3(de[0], f, 0, 0);
         mma3(de[1], f, 0, 1);
         mma3(de[2], f, 0, 2);
-        mma3(de[3], f, 1, 2);
       }
       __syncwarp();
     }
@@ -638,7 +639,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
         put(dmap[2 * t + 1], dc[t][2], dc[t][3]);
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < 3; ++t) {
         put(dmap[12 + 2 * t], de[t][0], de[t][1]);
         put(dmap[12 + 2 * t + 1], de[t][2], de[t][3]);
       }
