@@ -671,6 +671,238 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
   pdl_trigger();
 }
 
+// ---- tensor-core K3b for 5 <= k <= 8 (C5): the same per-chunk Gram sums as k_accum_points_tc with
+// c' padded to 64 columns and e' to 40, upper-triangle 16x8 tiles restricted to the entries the
+// system uses (c' rows < 6k, columns <= 6k; e' rows < 4k, columns < 4k + 3): 15 + 8 tiles at k = 8.
+// 92 accumulator registers, so one 8-warp CTA per SM; the fragment -> record map and the commit
+// items are tables in shared memory.
+#ifndef MIS_K3B_TCW
+#define MIS_K3B_TCW 0
+#endif
+template <int K>
+struct TcW {
+  static constexpr int CW = 64, EW = 40, S = 104;   // row: c' [0, 64) | e' [64, 104); 104 = 8 (mod 32)
+  static constexpr int CMT = (6 * K + 15) / 16, CNT = (6 * K) / 8 + 1;
+  static constexpr int EMT = (4 * K + 15) / 16, ENT = (4 * K + 2) / 8 + 1;
+  static constexpr int CQ = (CMT > (CNT + 1) / 2 ? CMT : (CNT + 1) / 2);   // A quads loaded for c'
+  static constexpr int EQ = (EMT > (ENT + 1) / 2 ? EMT : (ENT + 1) / 2);
+  static constexpr int NC = CMT * CNT - CMT * (CMT - 1), NE = EMT * ENT - EMT * (EMT - 1);
+  static constexpr int NT = NC + NE;
+  static constexpr int P = K * (K + 1) / 2;
+  static constexpr int RT = 52 * P + 20 * K;
+  static constexpr int NIT = (13 * P + 6 * K + 31) / 32;
+  __host__ __device__ static constexpr int cidx(int mi, int ni) { return mi * CNT - mi * (mi - 1) + (ni - 2 * mi); }
+  __host__ __device__ static constexpr int eidx(int mi, int ni) { return NC + mi * ENT - mi * (mi - 1) + (ni - 2 * mi); }
+};
+
+template <int QM, int NB>
+struct FragW {
+  uint32_t h[QM][4], l[QM][4];
+  uint32_t bh[NB][2], bl[NB][2];
+};
+template <int QM, int NB, int S>
+__device__ __forceinline__ void load_frag_w(const float* F, int k0, int cb, int g, int tig, FragW<QM, NB>& f) {
+#pragma unroll
+  for (int mi = 0; mi < QM; ++mi) {
+    const float x[4] = {F[(k0 + tig) * S + cb + 16 * mi + g], F[(k0 + tig) * S + cb + 16 * mi + g + 8],
+                        F[(k0 + tig + 4) * S + cb + 16 * mi + g], F[(k0 + tig + 4) * S + cb + 16 * mi + g + 8]};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      f.h[mi][q] = tf32_hi(x[q]);
+      f.l[mi][q] = __float_as_uint(x[q] - __uint_as_float(f.h[mi][q]));
+    }
+#pragma unroll
+    for (int bq = 0; bq < 2; ++bq)
+      if (2 * mi + bq < NB) {
+        f.bh[2 * mi + bq][0] = f.h[mi][bq];
+        f.bh[2 * mi + bq][1] = f.h[mi][bq + 2];
+        f.bl[2 * mi + bq][0] = f.l[mi][bq];
+        f.bl[2 * mi + bq][1] = f.l[mi][bq + 2];
+      }
+  }
+}
+template <int QM, int NB>
+__device__ __forceinline__ void mma3w(float (&d)[4], const FragW<QM, NB>& f, int mi, int ni) {
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], f.bh[ni][0], f.bh[ni][1]);
+  mma_tf32(d, f.h[mi][0], f.h[mi][1], f.h[mi][2], f.h[mi][3], f.bl[ni][0], f.bl[ni][1]);
+  mma_tf32(d, f.l[mi][0], f.l[mi][1], f.l[mi][2], f.l[mi][3], f.bh[ni][0], f.bh[ni][1]);
+}
+
+template <int K>
+__device__ __forceinline__ void build_row_w(const PState<K>& st, float* row) {
+  using T = TcW<K>;
+  const float4 nn = st.nn;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const float4 wa = st.wa[s];
+    row[6 * s + 0] = wa.y * nn.z - wa.z * nn.y;
+    row[6 * s + 1] = wa.z * nn.x - wa.x * nn.z;
+    row[6 * s + 2] = wa.x * nn.y - wa.y * nn.x;
+    row[6 * s + 3] = wa.w * nn.x;
+    row[6 * s + 4] = wa.w * nn.y;
+    row[6 * s + 5] = wa.w * nn.z;
+    *reinterpret_cast<float4*>(row + T::CW + 4 * s) = wa;
+  }
+  row[6 * K] = st.rr.w;
+#pragma unroll
+  for (int q = 6 * K + 1; q < T::CW; ++q) row[q] = 0.f;
+  row[T::CW + 4 * K + 0] = st.rr.x;
+  row[T::CW + 4 * K + 1] = st.rr.y;
+  row[T::CW + 4 * K + 2] = st.rr.z;
+#pragma unroll
+  for (int q = T::CW + 4 * K + 3; q < T::CW + T::EW; ++q) row[q] = 0.f;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_accum_points_tcw(AsmPointsArgs a) {
+  using T = TcW<K>;
+  constexpr int P = T::P, RT = T::RT, NIT = T::NIT, S = T::S;
+  extern __shared__ float4 smem4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  float* F = reinterpret_cast<float*>(smem4) + warp * (32 * S);
+  float* Rec = reinterpret_cast<float*>(smem4) + kWarps * 32 * S + warp * RT;
+  int16_t* dmap = reinterpret_cast<int16_t*>(reinterpret_cast<float*>(smem4) + kWarps * (32 * S + RT));  // [4 NT][32]
+  __shared__ int32_t slot_sm[kWarps][P + K];
+  __shared__ uint32_t cdesc[NIT][32];
+  int32_t* slots = slot_sm[warp];
+  // fragment position (row A, column B of the c' or e' Gram matrix) -> record index, -1: unused
+  auto rec_of = [&](bool e, int A, int B) -> int {
+    if (A > B) return -1;
+    if (!e) {
+      if (B < 6 * K) return 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
+      if (B == 6 * K && A < 6 * K) return 52 * P + 20 * (A / 6) + (A % 6);
+      return -1;
+    }
+    if (B < 4 * K) return 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
+    if (B < 4 * K + 3 && A < 4 * K) return 52 * P + 20 * (A / 4) + 8 + 3 * (A % 4) + (B - 4 * K);
+    return -1;
+  };
+  for (int q = threadIdx.x; q < 4 * T::NT * 32; q += blockDim.x) {   // dmap[4 t + h][lane]
+    const int ln = q & 31, th = q >> 5, t = th >> 2, h = th & 3, gg = ln >> 2, tg = ln & 3;
+    int mi = 0, ni = 0;
+    bool e = t >= T::NC;
+    {
+      int r = e ? t - T::NC : t;
+      const int MT = e ? T::EMT : T::CMT, NTL = e ? T::ENT : T::CNT;
+      for (int m = 0; m < MT; ++m) {
+        const int cnt = NTL - 2 * m;
+        if (r < cnt) { mi = m; ni = 2 * m + r; break; }
+        r -= cnt;
+      }
+    }
+    const int A = 16 * mi + gg + 8 * (h >> 1), B = 8 * ni + 2 * tg + (h & 1);
+    const int lim = e ? T::EW : T::CW;
+    dmap[q] = (int16_t)(A < lim && B < lim ? rec_of(e, A, B) : -1);
+  }
+  for (int q = threadIdx.x; q < NIT * 32; q += blockDim.x) {   // commit items, as in k_accum_points_tc
+    const int it = q;
+    uint32_t d = ~0u;
+    if (it < 13 * P) {
+      const int pr = it / 13, qq = it - 13 * pr;
+      d = (qq < 9 ? 0u : 1u) | ((uint32_t)pr << 2) | ((uint32_t)(qq < 9 ? 4 * qq : 4 * (qq - 9)) << 10) |
+          ((uint32_t)(4 * it) << 18);
+    } else if (it < 13 * P + 6 * K) {
+      const int t2 = it - 13 * P, sl = t2 / 6, qq = t2 - 6 * sl;
+      d = qq < 3 ? (2u | ((uint32_t)sl << 2) | ((uint32_t)(2 * qq) << 10) | ((uint32_t)(52 * P + 20 * sl + 2 * qq) << 18))
+                 : (3u | ((uint32_t)sl << 2) | ((uint32_t)(4 * (qq - 3)) << 10) |
+                    ((uint32_t)(52 * P + 20 * sl + 8 + 4 * (qq - 3)) << 18));
+    }
+    cdesc[q / 32][q % 32] = d;
+  }
+  for (int q = lane; q < RT; q += 32) Rec[q] = 0.f;
+  __syncthreads();
+
+  pdl_wait();   // K3a's factor state
+  int64_t c = 0;
+  if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  const float4* ps = a.pstate;
+  const int64_t SS = a.pstride;
+  for (; c < a.nchunk;) {
+    const int4 ch = a.chunks[c];
+    const int seg = ch.x;
+    const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
+    __syncwarp();
+    for (int q = lane; q < P + K; q += 32) slots[q] = q < P ? a.seg_slot[(int64_t)seg * P + q] : nodes[q - P];
+    float acc[T::NT][4];
+#pragma unroll
+    for (int t = 0; t < T::NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+    for (int base = ch.y; base < ch.z; base += 32) {
+      const int64_t i = base + lane;
+      PState<K> st;
+      if (i < ch.z) {
+#pragma unroll
+        for (int s = 0; s < K; ++s) st.wa[s] = ps[s * SS + i];
+        st.rr = ps[K * SS + i];
+        st.nn = ps[(K + 1) * SS + i];
+      } else {
+#pragma unroll
+        for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        st.rr = st.nn = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      build_row_w<K>(st, F + lane * S);
+      __syncwarp();
+      const int np = min(32, ch.z - base);
+      for (int k0 = 0; k0 < np; k0 += 8) {
+        {
+          FragW<T::CQ, T::CNT> f;
+          load_frag_w<T::CQ, T::CNT, S>(F, k0, 0, g, tig, f);   // c'
+#pragma unroll
+          for (int mi = 0; mi < T::CMT; ++mi)
+#pragma unroll
+            for (int ni = 2 * mi; ni < T::CNT; ++ni) mma3w(acc[T::cidx(mi, ni)], f, mi, ni);
+        }
+        {
+          FragW<T::EQ, T::ENT> f;
+          load_frag_w<T::EQ, T::ENT, S>(F, k0, T::CW, g, tig, f);   // e'
+#pragma unroll
+          for (int mi = 0; mi < T::EMT; ++mi)
+#pragma unroll
+            for (int ni = 2 * mi; ni < T::ENT; ++ni) mma3w(acc[T::eidx(mi, ni)], f, mi, ni);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < T::NT; ++t)
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int d = dmap[(4 * t + h) * 32 + lane];
+        if (d >= 0) Rec[d] = acc[t][h];
+      }
+    __syncwarp();
+    int64_t next_chunk = 0;
+    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);
+#pragma unroll 1
+    for (int k = 0; k < NIT; ++k) {
+      const uint32_t d = cdesc[k][lane];
+      if (d == ~0u) continue;
+      const uint32_t kind = d & 3u, idx = (d >> 2) & 255u, off = (d >> 10) & 255u;
+      const float* src = Rec + (d >> 18);
+      if (kind == 2u) {
+        const float2 v = *reinterpret_cast<const float2*>(src);
+        if (v.x != 0.f || v.y != 0.f)
+          atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * (int64_t)slots[P + idx] + off), v);
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(src);
+        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+        float* dst = kind == 0u ? a.acc.data + 36 * (int64_t)slots[idx]
+                   : kind == 1u ? a.acc.mom + 16 * (int64_t)slots[idx] : a.acc.node_mom + 12 * (int64_t)slots[P + idx];
+        atomicAdd(reinterpret_cast<float4*>(dst + off), v);
+      }
+    }
+    __syncwarp();
+    c = __shfl_sync(0xffffffffu, next_chunk, 0);
+  }
+  pdl_trigger();
+}
+__host__ inline size_t tcw_smem(int K) {
+  const int P = K * (K + 1) / 2, RT = 52 * P + 20 * K;
+  const int CMT = (6 * K + 15) / 16, CNT = (6 * K) / 8 + 1, EMT = (4 * K + 15) / 16, ENT = (4 * K + 2) / 8 + 1;
+  const int NT = CMT * CNT - CMT * (CMT - 1) + EMT * ENT - EMT * (EMT - 1);
+  return sizeof(float) * kWarps * (32 * 104 + RT) + sizeof(int16_t) * 4 * NT * 32;
+}
+
 // Finalisation of the normal equations from the accumulators (so the
 // latency-bound solver only streams its rows): warps [0, m) the diagonal blocks
 // -- first, so their block-Jacobi inverses (K7) overlap the rest --, then one
@@ -954,11 +1186,16 @@ template <int K>
 static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
   using L = Lay<K>;
   if (a.nchunk <= 0) return;
-  constexpr bool tc = MIS_K3B_TC && K <= 4;   // tensor-core SYRK for k <= 4, FP32 tiles above
-  const size_t smem = tc ? sizeof(float) * kWarps * (32 * kTcFSP + tc_rec_floats(K <= 4 ? K : 4))
-                          : sizeof(float) * kWarps * 32 * L::FSP;
+  constexpr bool tc = MIS_K3B_TC && K <= 4;   // tensor-core SYRK: k <= 4 (8 warps x 2 CTAs / SM),
+  // 5 <= k <= 8 on tensor cores (one 8-warp CTA / SM at 167 registers) measured slower than the FP32
+  // tiles at 16 warps / SM (C5: 2.9 vs 2.5 ms per launch, latency-bound), so it is opt-in
+  constexpr bool tcw = MIS_K3B_TCW && K > 4;
+  const size_t smem = tc    ? sizeof(float) * kWarps * (32 * kTcFSP + tc_rec_floats(K <= 4 ? K : 4))
+                      : tcw ? tcw_smem(K)
+                            : sizeof(float) * kWarps * 32 * L::FSP;
   void (*kern)(AsmPointsArgs);
   if constexpr (tc) kern = k_accum_points_tc<(K <= 4 ? K : 4)>;
+  else if constexpr (tcw) kern = k_accum_points_tcw<(K > 4 ? K : 5)>;
   else kern = k_accum_points<K>;
   static bool attr_set = false;
   if (!attr_set) {
