@@ -269,17 +269,21 @@ template <int K>
 __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPointsArgs a) {
   using L = Lay<K>;
   constexpr int P = L::P;
-  constexpr int RS = (52 * P + 18 * K + 5 + 3) & ~3;   // == rec_stride(K)
+  constexpr int RT = 52 * P + 20 * K;   // commit record (aliases the warp's row buffer at commit)
+  constexpr int NIT = (13 * P + 6 * K + 31) / 32;
+  static_assert(RT <= 32 * L::FSP, "record must fit the row buffer");
   extern __shared__ float4 smem4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* F = reinterpret_cast<float*>(smem4) + warp * (32 * L::FSP);
-  __shared__ int32_t slot_sm[kWarps][P];   // the chunk's BSR slots (loaded with the header)
+  float* Rec = F;
+  __shared__ int32_t slot_sm[kWarps][P + K];   // the chunk's BSR slots, then its K node ids
   int32_t* slots = slot_sm[warp];
 
   // tile table of the two upper triangles: (I, J) in units of 4 entries
   __shared__ uint8_t tabI[L::NT], tabJ[L::NT];
-  // record permutation: perm[d] = tile-dump index feeding record float d (-1: zero)
-  __shared__ int16_t perm[RS];
+  // per lane: record index of each of its items' 16 tile entries (-1: not part of the system)
+  __shared__ int16_t dm[L::RI * 16][32];
+  __shared__ uint32_t cdesc[NIT][32];   // commit items, as in k_accum_points_tc
   for (int t = threadIdx.x; t < L::NT; t += blockDim.x) {
     const bool e = t >= L::TD;
     const int nb = e ? L::NE : L::ND;
@@ -288,20 +292,38 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     tabI[t] = (uint8_t)I;
     tabJ[t] = (uint8_t)(I + u);
   }
-  for (int d = threadIdx.x; d < RS; d += blockDim.x) perm[d] = -1;
   __syncthreads();
-  for (int q = threadIdx.x; q < 16 * L::NT; q += blockDim.x) {
-    const int t = q >> 4, A = 4 * tabI[t] + ((q >> 2) & 3), B = 4 * tabJ[t] + (q & 3);
-    if (A > B) continue;
+  for (int q = threadIdx.x; q < L::RI * 16 * 32; q += blockDim.x) {
+    const int ln = q & 31, rv = q >> 5, r = rv >> 4, v = rv & 15, it = ln + 32 * r;
     int d = -1;
-    if (t < L::TD) {             // c' = [w_j u_j ..., r_pl]
-      if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
-      else if (B == 6 * K && A < 6 * K) d = 52 * P + 18 * (A / 6) + (A % 6);
-    } else {                     // e' = [w_j a_j, w_j ..., r']
-      if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
-      else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 18 * (A / 4) + 6 + 3 * (A % 4) + (B - 4 * K);
+    if (it < L::NI) {
+      const int t = it % L::NT, A = 4 * tabI[t] + (v >> 2), B = 4 * tabJ[t] + (v & 3);
+      if (A <= B) {
+        if (t < L::TD) {             // c' = [w_j u_j ..., r_pl]
+          if (B < 6 * K) d = 52 * pair_index(A / 6, B / 6, K) + 6 * (A % 6) + (B % 6);
+          else if (B == 6 * K && A < 6 * K) d = 52 * P + 20 * (A / 6) + (A % 6);
+        } else {                     // e' = [w_j a_j, w_j ..., r']
+          if (B < 4 * K) d = 52 * pair_index(A / 4, B / 4, K) + 36 + 4 * (A % 4) + (B % 4);
+          else if (B < 4 * K + 3 && A < 4 * K) d = 52 * P + 20 * (A / 4) + 8 + 3 * (A % 4) + (B - 4 * K);
+        }
+      }
     }
-    if (d >= 0) perm[d] = (int16_t)q;
+    dm[rv][ln] = (int16_t)d;
+  }
+  for (int q = threadIdx.x; q < NIT * 32; q += blockDim.x) {
+    const int it = q;
+    uint32_t d = ~0u;
+    if (it < 13 * P) {
+      const int pr = it / 13, qq = it - 13 * pr;
+      d = (qq < 9 ? 0u : 1u) | ((uint32_t)pr << 2) | ((uint32_t)(qq < 9 ? 4 * qq : 4 * (qq - 9)) << 10) |
+          ((uint32_t)(4 * it) << 18);
+    } else if (it < 13 * P + 6 * K) {
+      const int t2 = it - 13 * P, sl = t2 / 6, qq = t2 - 6 * sl;
+      d = qq < 3 ? (2u | ((uint32_t)sl << 2) | ((uint32_t)(2 * qq) << 10) | ((uint32_t)(52 * P + 20 * sl + 2 * qq) << 18))
+                 : (3u | ((uint32_t)sl << 2) | ((uint32_t)(4 * (qq - 3)) << 10) |
+                    ((uint32_t)(52 * P + 20 * sl + 8 + 4 * (qq - 3)) << 18));
+    }
+    cdesc[q / 32][q % 32] = d;
   }
   __syncthreads();
   // static ownership: lane owns items lane, lane + 32, ...; item = tile + NT * half
@@ -330,7 +352,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     const int seg = ch.x;
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
     __syncwarp();
-    for (int q = lane; q < P; q += 32) slots[q] = a.seg_slot[(int64_t)seg * P + q];
+    for (int q = lane; q < P + K; q += 32) slots[q] = q < P ? a.seg_slot[(int64_t)seg * P + q] : nodes[q - P];
     float acc[L::RI][16];
 #pragma unroll
     for (int r = 0; r < L::RI; ++r)
@@ -368,50 +390,44 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
       }
       __syncwarp();
     }
-    // ---- commit: tiles -> shared memory -> atomic adds into the BSR accumulators
-#pragma unroll
-    for (int r = 0; r < L::RI; ++r) {
-      if (!tV[r]) continue;
-      float4* d4 = reinterpret_cast<float4*>(F + 16 * (lane + 32 * r));
-#pragma unroll
-      for (int x = 0; x < 4; ++x) d4[x] = make_float4(acc[r][4 * x], acc[r][4 * x + 1], acc[r][4 * x + 2], acc[r][4 * x + 3]);
-    }
+    // ---- commit: tiles scattered into the warp's record (aliasing the row buffer; a second batch
+    // half adds to the first's entries), then one aligned shared load + vector atomic per item
+    for (int q = lane; q < RT / 4; q += 32) reinterpret_cast<float4*>(Rec)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
-    int64_t next_chunk = 0;
-    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
-    // vector atomic adds (sm_90+ float4 / float2 RED): per pair 9 x 4 data + 4 x 4 moments of
-    // its BSR slot, per node slot 3 x 2 rhs + 3 x 4 moments; all-zero vectors are skipped
-    auto rv = [&](int d) -> float {
-      const int q = perm[d];
-      if (q < 0) return 0.f;
-      float v = F[q];
-      if (L::SPLIT == 2) v += F[q + 16 * L::NT];   // the second half's partial tile
-      return v;
-    };
-    for (int it = lane; it < 13 * P + 6 * K; it += 32) {
-      if (it < 13 * P) {
-        const int pr = it / 13, q = it - 13 * pr;
-        const int d0 = 52 * pr + 4 * q;   // data (q < 9) then moments: contiguous in the record
-        const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
-        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
-        const int64_t u = slots[pr];
-        float* dst = q < 9 ? a.acc.data + 36 * u + 4 * q : a.acc.mom + 16 * u + 4 * (q - 9);
-        atomicAdd(reinterpret_cast<float4*>(dst), v);
-      } else {
-        const int t2 = it - 13 * P, sl = t2 / 6, q = t2 - 6 * sl;
-        const int64_t nd = nodes[sl];
-        if (q < 3) {
-          const int d0 = 52 * P + 18 * sl + 2 * q;
-          const float2 v = make_float2(rv(d0), rv(d0 + 1));
-          if (v.x != 0.f || v.y != 0.f) atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * nd + 2 * q), v);
-        } else {
-          const int d0 = 52 * P + 18 * sl + 6 + 4 * (q - 3);
-          const float4 v = make_float4(rv(d0), rv(d0 + 1), rv(d0 + 2), rv(d0 + 3));
-          if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
-            atomicAdd(reinterpret_cast<float4*>(a.acc.node_mom + 12 * nd + 4 * (q - 3)), v);
+#pragma unroll
+    for (int h = 0; h < L::SPLIT; ++h) {
+#pragma unroll
+      for (int r = 0; r < L::RI; ++r) {
+        if (!tV[r] || (lane + 32 * r) / L::NT != h) continue;
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const int d = dm[16 * r + v][lane];
+          if (d >= 0) Rec[d] = h == 0 ? acc[r][v] : Rec[d] + acc[r][v];
         }
       }
+      __syncwarp();
     }
+    int64_t next_chunk = 0;
+    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
+#pragma unroll 1
+    for (int k = 0; k < NIT; ++k) {
+      const uint32_t d = cdesc[k][lane];
+      if (d == ~0u) continue;
+      const uint32_t kind = d & 3u, idx = (d >> 2) & 255u, off = (d >> 10) & 255u;
+      const float* src = Rec + (d >> 18);
+      if (kind == 2u) {
+        const float2 v = *reinterpret_cast<const float2*>(src);
+        if (v.x != 0.f || v.y != 0.f)
+          atomicAdd(reinterpret_cast<float2*>(a.acc.rhs_data + 6 * (int64_t)slots[P + idx] + off), v);
+      } else {
+        const float4 v = *reinterpret_cast<const float4*>(src);
+        if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+        float* dst = kind == 0u ? a.acc.data + 36 * (int64_t)slots[idx]
+                   : kind == 1u ? a.acc.mom + 16 * (int64_t)slots[idx] : a.acc.node_mom + 12 * (int64_t)slots[P + idx];
+        atomicAdd(reinterpret_cast<float4*>(dst + off), v);
+      }
+    }
+    __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
   pdl_trigger();
