@@ -317,7 +317,10 @@ cudaError_t flush_frame(Ctx* c) {
   FrameView fv = frame_view(c);
   fv.depth = c->frame_src;
   launch_frame_prep(fv, c->nmap.as<float4>(), c->nmapd.as<double4>(), c->st);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && c->frame_src == c->depth.p)   // host-staged depth: the buffer may be overwritten
+    e = cudaEventRecord(c->ev_depth_free, c->st);     // (device inputs record nothing: no break in the PDL chain)
+  return e;
 }
 
 }  // namespace mis
@@ -442,6 +445,9 @@ mis_status mis_destroy(mis_ctx* c) {
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(c->nccl_comm);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->rb_ev) cudaEventDestroy(c->rb_ev);
+  if (c->st_copy) { cudaStreamSynchronize(c->st_copy); cudaStreamDestroy(c->st_copy); }
+  if (c->ev_depth_free) cudaEventDestroy(c->ev_depth_free);
+  if (c->ev_depth_ready) cudaEventDestroy(c->ev_depth_ready);
   if (c->own_stream) cudaStreamDestroy(c->st);
 
   delete c;
@@ -635,7 +641,20 @@ static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm,
   }
   TRY(c, ensure(c, c->nmap, px * 16));
   TRY(c, ensure(c, c->nmapd, px * 32));
-  if (mem == MIS_MEM_HOST) TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st));
+  if (mem == MIS_MEM_HOST) {
+    // on the copy stream, after the previous frame prep has read the buffer: the transfer overlaps
+    // whatever the context stream is still running (e.g. the model ordering of mis_set_graph);
+    // the context stream waits for it before K1
+    if (!c->st_copy) {   // created with the first host-memory frame
+      TRY(c, cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
+      TRY(c, cudaEventCreateWithFlags(&c->ev_depth_free, cudaEventDisableTiming));
+      TRY(c, cudaEventCreateWithFlags(&c->ev_depth_ready, cudaEventDisableTiming));
+    }
+    TRY(c, cudaStreamWaitEvent(c->st_copy, c->ev_depth_free, 0));
+    TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st_copy));
+    TRY(c, cudaEventRecord(c->ev_depth_ready, c->st_copy));
+    TRY(c, cudaStreamWaitEvent(c->st, c->ev_depth_ready, 0));
+  }
   c->frame_src = dsrc;
   c->frame_pending = true;
   if (!defer || c->prof) TRY(c, flush_frame(c));   // (profiling: K1 in its own group)
