@@ -309,6 +309,17 @@ static void prof_collect(Ctx* c) {
   c->pev.clear();
 }
 
+// copy stream for host-memory frame inputs, created with the first one
+cudaError_t copy_stream(Ctx* c) {
+  if (c->st_copy) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  cudaEvent_t* evs[] = {&c->ev_depth_free, &c->ev_depth_ready, &c->ev_rgb_free, &c->ev_rgb_ready};
+  for (cudaEvent_t* ev : evs)
+    if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
 // K1 of a frame whose launch mis_register deferred (see set_frame_impl)
 cudaError_t flush_frame(Ctx* c) {
   if (!c->frame_pending) return cudaSuccess;
@@ -446,8 +457,8 @@ mis_status mis_destroy(mis_ctx* c) {
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->rb_ev) cudaEventDestroy(c->rb_ev);
   if (c->st_copy) { cudaStreamSynchronize(c->st_copy); cudaStreamDestroy(c->st_copy); }
-  if (c->ev_depth_free) cudaEventDestroy(c->ev_depth_free);
-  if (c->ev_depth_ready) cudaEventDestroy(c->ev_depth_ready);
+  for (cudaEvent_t ev : {c->ev_depth_free, c->ev_depth_ready, c->ev_rgb_free, c->ev_rgb_ready})
+    if (ev) cudaEventDestroy(ev);
   if (c->own_stream) cudaStreamDestroy(c->st);
 
   delete c;
@@ -645,11 +656,7 @@ static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm,
     // on the copy stream, after the previous frame prep has read the buffer: the transfer overlaps
     // whatever the context stream is still running (e.g. the model ordering of mis_set_graph);
     // the context stream waits for it before K1
-    if (!c->st_copy) {   // created with the first host-memory frame
-      TRY(c, cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
-      TRY(c, cudaEventCreateWithFlags(&c->ev_depth_free, cudaEventDisableTiming));
-      TRY(c, cudaEventCreateWithFlags(&c->ev_depth_ready, cudaEventDisableTiming));
-    }
+    TRY(c, copy_stream(c));
     TRY(c, cudaStreamWaitEvent(c->st_copy, c->ev_depth_free, 0));
     TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st_copy));
     TRY(c, cudaEventRecord(c->ev_depth_ready, c->st_copy));
@@ -1125,12 +1132,19 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   const size_t px = (size_t)c->W * c->H;
   const float* rgb_dev = rgb;   // device colours are read in place by K11 / K12 (stream order)
   if (rgb && mem == MIS_MEM_HOST) {
+    // on the copy stream, after the previous fusion read the buffer: the transfer overlaps the
+    // registration of the model points (K10); the colours are first read by K11
     TRY(c, ensure(c, c->rgb_obs, px * 12));
-    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, cudaMemcpyHostToDevice, c->st));
+    TRY(c, copy_stream(c));
+    TRY(c, cudaStreamWaitEvent(c->st_copy, c->ev_rgb_free, 0));
+    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, cudaMemcpyHostToDevice, c->st_copy));
+    TRY(c, cudaEventRecord(c->ev_rgb_ready, c->st_copy));
     rgb_dev = c->rgb_obs.as<float>();
   }
   mis_status s;
   if ((s = fuse_register(c, rgb_dev, frame_index)) != MIS_OK) return s;
+  const bool rgb_staged = rgb && mem == MIS_MEM_HOST;
+  if (rgb_staged) TRY(c, cudaStreamWaitEvent(c->st, c->ev_rgb_ready, 0));
   FuseArgs a = fuse_args(c, rgb_dev, frame_index);
   {
     ProfScope ps(c, P_FAPPLY, c->n > 0 ? 1 : 0);
@@ -1170,6 +1184,7 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
     TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
   }
   c->pixkey_clean = true;
+  if (rgb_staged) TRY(c, cudaEventRecord(c->ev_rgb_free, c->st));   // K11 / K12 have read the staged colours
   TRY(c, cudaGetLastError());
   c->n += n_lift;
   *n_out = c->n;

@@ -29,7 +29,7 @@ struct Ctx {
   cudaStream_t st = nullptr;
   bool own_stream = false;
   cudaStream_t st_copy = nullptr;      // host->device copies of frame inputs (overlap the model ordering)
-  cudaEvent_t ev_depth_free = nullptr, ev_depth_ready = nullptr;
+  cudaEvent_t ev_depth_free = nullptr, ev_depth_ready = nullptr, ev_rgb_free = nullptr, ev_rgb_ready = nullptr;
   int rank = 0, world = 1;
   void* nccl_comm = nullptr;
   std::string err;
