@@ -414,6 +414,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
     if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) { delete c; return MIS_E_CUDA; }
     c->own_stream = true;
   }
+  if (const char* e = getenv("MIS_ORDER_BY_SORT")) c->order_by_sort = atoi(e) != 0;
 
   if (world > 1) {
     NcclApi& api = nccl();

@@ -50,6 +50,11 @@ struct Ctx {
   // ---- order: segments and chunks (K13)
   int64_t nseg = 0, nchunk = 0;
   DBuf keys, keys2, vals, vals2, flags, scan, seg_start, seg_nodes, chunks, chunk_off;
+  // grouping by exact tuple (k <= 4, m < 65535): hash table (keys | group ids, empty at rest),
+  // per-group key / slot / count (count zero at rest) and the group counter
+  DBuf gtab, gkeys, gslot, gcount;
+  int64_t gtab_slots = 0, gsize_cap = 0;
+  bool order_by_sort = false;   // MIS_ORDER_BY_SORT=1 in the environment: the radix-sort path
 
   // ---- pattern
   int64_t nnzb = 0;

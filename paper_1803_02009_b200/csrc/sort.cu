@@ -113,6 +113,183 @@ __global__ void k_chunk_write(int64_t n, const int32_t* nseg_dev, const int32_t*
     chunks[o + q] = make_int4((int)s, a + (int32_t)((int64_t)len * q / nc), a + (int32_t)((int64_t)len * (q + 1) / nc), 0);
 }
 
+// ---- grouping by exact tuple (k <= 4, m < 65535): the model only needs every tuple's points
+// contiguous, not an order of the tuples, so instead of sorting, each point finds its tuple in
+// a hash table (the first finder of a tuple claims a group id), takes a rank inside the group
+// with one atomic, and one CTA lays the groups out (prefix sums of sizes and chunk counts,
+// segment / chunk tables); a scatter then gives the gather permutation.  Group order and the
+// order inside a group follow the atomics (the K3 sums are atomic-order dependent anyway).
+constexpr unsigned long long kEmpty = ~0ull;
+
+__device__ __forceinline__ uint64_t tuple_key(const int32_t* kidx, int64_t cap, int64_t i, int K) {
+  uint64_t key = 0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const uint64_t id = s < K ? (uint64_t)(uint32_t)kidx[s * cap + i] : 0xffffull;
+    key |= (id & 0xffffull) << (16 * s);
+  }
+  return key;
+}
+
+__global__ void k_group_insert(int64_t n, int64_t cap, const int32_t* kidx, int K, unsigned long long* tkeys,
+                               int32_t* tgid, int64_t tmask, int32_t* gcount, uint64_t* gkeys, int32_t* gslot,
+                               int32_t* gsize, int32_t* gid_out, int32_t* rank_out) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = tuple_key(kidx, cap, i, K);
+  int64_t h = (int64_t)(mix64(key) & (uint64_t)tmask);
+  int32_t gid = -1;
+  for (;;) {
+    unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tkeys + h);
+    if (cur == kEmpty) {
+      cur = atomicCAS(tkeys + h, kEmpty, (unsigned long long)key);
+      if (cur == kEmpty) {   // this thread inserted the tuple: claim a group id
+        gid = atomicAdd(gcount, 1);
+        gkeys[gid] = key;
+        gslot[gid] = (int32_t)h;
+        __threadfence();
+        *reinterpret_cast<volatile int32_t*>(tgid + h) = gid;
+        break;
+      }
+    }
+    if (cur == key) {   // inserted by another thread: wait for its group id
+      int32_t g;
+      while ((g = *reinterpret_cast<volatile int32_t*>(tgid + h)) < 0) {}
+      gid = g;
+      break;
+    }
+    h = (h + 1) & tmask;
+  }
+  gid_out[i] = gid;
+  rank_out[i] = atomicAdd(gsize + gid, 1);
+}
+
+// one CTA: segment starts (prefix of group sizes), segment node tuples, chunk table (equal
+// chunks of <= kChunk points per segment), the counts for the pattern readback; re-empties the
+// hash slots and group sizes it used
+__global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t* gcount, const uint64_t* gkeys,
+                                                       const int32_t* gslot, int32_t* gsize, unsigned long long* tkeys,
+                                                       int32_t* tgid, int32_t* seg_start, int32_t* seg_nodes,
+                                                       int4* chunks, int64_t* info) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
+  __shared__ int32_t wsum[2][32];
+  __shared__ int32_t carry[2];
+  const int T = *gcount;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) { carry[0] = 0; carry[1] = 0; }
+  __syncthreads();
+  for (int base = 0; base < T; base += 1024) {
+    const int s = base + t;
+    const int len = s < T ? gsize[s] : 0, nc = (len + kChunk - 1) / kChunk;
+    int a = len, b = nc;   // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) { a += x; b += y; }
+    }
+    if (lane == 31) { wsum[0][w] = a; wsum[1][w] = b; }
+    __syncthreads();
+    if (w == 0) {
+      int x = wsum[0][lane], y = wsum[1][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o), v = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) { x += u; y += v; }
+      }
+      wsum[0][lane] = x;   // inclusive over warps
+      wsum[1][lane] = y;
+    }
+    __syncthreads();
+    const int pre0 = carry[0] + (w > 0 ? wsum[0][w - 1] : 0) + a - len;   // exclusive
+    const int pre1 = carry[1] + (w > 0 ? wsum[1][w - 1] : 0) + b - nc;
+    if (s < T) {
+      seg_start[s] = pre0;
+      const uint64_t key = gkeys[s];
+      for (int q = 0; q < K; ++q) seg_nodes[(int64_t)s * K + q] = (int32_t)((key >> (16 * q)) & 0xffffull);
+      for (int q = 0; q < nc; ++q)
+        chunks[pre1 + q] = make_int4(s, pre0 + (int32_t)((int64_t)len * q / nc), pre0 + (int32_t)((int64_t)len * (q + 1) / nc), 0);
+      const int32_t h = gslot[s];
+      tkeys[h] = kEmpty;
+      tgid[h] = -1;
+      gsize[s] = 0;
+    }
+    __syncthreads();
+    if (t == 0) { carry[0] += wsum[0][31]; carry[1] += wsum[1][31]; }
+    __syncthreads();
+  }
+  if (t == 0) {
+    seg_start[T] = (int32_t)n;
+    info[1] = T;
+    info[2] = carry[1];
+    *gcount = 0;
+  }
+}
+
+__global__ void k_group_perm(int64_t n, const int32_t* gid, const int32_t* rank, const int32_t* seg_start,
+                             uint32_t* perm) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  perm[seg_start[gid[i]] + rank[i]] = (uint32_t)i;
+}
+
+// the model grouped by tuple (replaces sort + segment scans when k <= 4 and m < 65535)
+static cudaError_t build_order_grouped(Ctx* c) {
+  const int64_t n = c->n;
+  const int K = c->K;
+  ModelBufs& A = c->mb[c->cur];
+  ModelBufs& B = c->mb[1 - c->cur];
+  int64_t slots = 1024;
+  while (slots < 2 * n) slots <<= 1;   // load factor <= 1/2 even if every point had its own tuple
+  if (c->gtab_slots < slots) {
+    CK(ensure(c, c->gtab, (size_t)slots * 12));
+    CK(cudaMemsetAsync(c->gtab.p, 0xff, (size_t)slots * 12, c->st));   // keys empty, group ids -1
+    c->gtab_slots = slots;
+  }
+  if (c->gcount.bytes < 64 || c->gsize_cap < n) {
+    CK(ensure(c, c->gkeys, (size_t)n * 8));
+    CK(ensure(c, c->gslot, (size_t)n * 4 + 64));
+    CK(ensure(c, c->gcount, (size_t)n * 4 + 64));   // [0]: group counter, [16..]: group sizes
+    CK(cudaMemsetAsync(c->gcount.p, 0, (size_t)n * 4 + 64, c->st));
+    c->gsize_cap = n;
+  }
+  CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4)); CK(ensure(c, c->keys, n * 8));
+  CK(ensure(c, c->seg_start, (n + 1) * 4));
+  CK(ensure(c, c->seg_nodes, (size_t)n * K * 4));
+  CK(ensure(c, c->chunks, (size_t)n * 16));
+  if (!c->nnz_dev.p) {
+    CK(ensure(c, c->nnz_dev, 64));
+    CK(cudaMemsetAsync(c->nnz_dev.p, 0, 64, c->st));
+  }
+  unsigned long long* tkeys = reinterpret_cast<unsigned long long*>(c->gtab.p);
+  int32_t* tgid = reinterpret_cast<int32_t*>(tkeys + c->gtab_slots);
+  int32_t* gcount = c->gcount.as<int32_t>();
+  int32_t* gsize = gcount + 16;
+  const int b = (int)((n + 255) / 256);
+  launch_pdl(k_group_insert, dim3(b), dim3(256), 0, c->st, n, c->cap, A.kidx.as<int32_t>(), K, tkeys, tgid,
+             c->gtab_slots - 1, gcount, c->gkeys.as<uint64_t>(), c->gslot.as<int32_t>(), gsize, c->vals.as<int32_t>(),
+             c->vals2.as<int32_t>());
+  launch_pdl(k_group_layout, dim3(1), dim3(1024), 0, c->st, n, K, gcount, c->gkeys.as<uint64_t>(),
+             c->gslot.as<int32_t>(), gsize, tkeys, tgid, c->seg_start.as<int32_t>(), c->seg_nodes.as<int32_t>(),
+             c->chunks.as<int4>(), c->nnz_dev.as<int64_t>());
+  uint32_t* perm = reinterpret_cast<uint32_t*>(c->keys.p);
+  launch_pdl(k_group_perm, dim3(b), dim3(256), 0, c->st, n, c->vals.as<int32_t>(), c->vals2.as<int32_t>(),
+             c->seg_start.as<int32_t>(), perm);
+  launch_pdl(k_gather_model, dim3(b), dim3(256), 0, c->st, n, perm, model_view(c), model_view_of(c, B), K);
+  count_launches(4);
+  CK(cudaGetLastError());
+  c->cur = 1 - c->cur;
+  c->nseg = -1;
+  c->nchunk = -1;
+  c->dirty = false;
+  c->pattern_valid = false;
+  return cudaSuccess;
+}
+
 template <class F>
 static cudaError_t cub_call(Ctx* c, F f) {
   size_t need = 0;
@@ -125,6 +302,7 @@ static cudaError_t cub_call(Ctx* c, F f) {
 cudaError_t build_order(Ctx* c) {
   const int64_t n = c->n;
   const int K = c->K;
+  if (n > 0 && K <= 4 && c->m < 65535 && !c->order_by_sort) return build_order_grouped(c);
   ModelBufs& A = c->mb[c->cur];
   ModelBufs& B = c->mb[1 - c->cur];
   if (n > 0) {
