@@ -131,39 +131,73 @@ __device__ __forceinline__ uint64_t tuple_key(const int32_t* kidx, int64_t cap, 
   return key;
 }
 
-__global__ void k_group_insert(int64_t n, int64_t cap, const int32_t* kidx, int K, unsigned long long* tkeys,
-                               int32_t* tgid, int64_t tmask, int32_t* gcount, uint64_t* gkeys, int32_t* gslot,
-                               int32_t* gsize, int32_t* gid_out, int32_t* rank_out) {
+__global__ void __launch_bounds__(256) k_group_insert(int64_t n, int64_t cap, const int32_t* kidx, int K,
+                                                      unsigned long long* tkeys, int32_t* tgid, int64_t tmask,
+                                                      int32_t* gcount, uint64_t* gkeys, int32_t* gslot, int32_t* gsize,
+                                                      int32_t* gid_out, int32_t* rank_out) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
+  __shared__ int32_t nwin, base;
+  if (threadIdx.x == 0) nwin = 0;
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t key = tuple_key(kidx, cap, i, K);
-  int64_t h = (int64_t)(mix64(key) & (uint64_t)tmask);
-  int32_t gid = -1;
-  for (;;) {
-    unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tkeys + h);
-    if (cur == kEmpty) {
-      cur = atomicCAS(tkeys + h, kEmpty, (unsigned long long)key);
-      if (cur == kEmpty) {   // this thread inserted the tuple: claim a group id
-        gid = atomicAdd(gcount, 1);
-        gkeys[gid] = key;
-        gslot[gid] = (int32_t)h;
-        __threadfence();
-        *reinterpret_cast<volatile int32_t*>(tgid + h) = gid;
-        break;
+  const int lane = threadIdx.x & 31;
+  const bool valid = i < n;
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  // lanes with the same tuple (a grouped model makes most of a warp one tuple) elect the lowest
+  // as their leader: only leaders touch the table and the group sizes
+  uint64_t key = 0;
+  unsigned mask = 0;
+  if (valid) {
+    key = tuple_key(kidx, cap, i, K);
+    mask = __match_any_sync(vmask, key);
+  }
+  const int leader = valid ? __ffs(mask) - 1 : lane;
+  const bool lead = valid && leader == lane;
+  // phase A (never waits): leaders find or insert the tuple's slot
+  int64_t h = -1;
+  bool won = false;
+  if (lead) {
+    h = (int64_t)(mix64(key) & (uint64_t)tmask);
+    for (;;) {
+      unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(tkeys + h);
+      if (cur == kEmpty) {
+        cur = atomicCAS(tkeys + h, kEmpty, (unsigned long long)key);
+        if (cur == kEmpty) { won = true; break; }
       }
+      if (cur == key) break;
+      h = (h + 1) & tmask;
     }
-    if (cur == key) {   // inserted by another thread: wait for its group id
+  }
+  // group ids for this block's new tuples: one counter atomic per block
+  int my = 0;
+  if (won) my = atomicAdd(&nwin, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && nwin > 0) base = atomicAdd(gcount, nwin);
+  __syncthreads();
+  int32_t gid = -1, r0 = 0;
+  if (won) {
+    gid = base + my;
+    gkeys[gid] = key;
+    gslot[gid] = (int32_t)h;
+    __threadfence();
+    *reinterpret_cast<volatile int32_t*>(tgid + h) = gid;
+  }
+  // phase B: tuples inserted elsewhere (their winner is resident and publishes without waiting)
+  if (lead) {
+    if (!won) {
       int32_t g;
       while ((g = *reinterpret_cast<volatile int32_t*>(tgid + h)) < 0) {}
       gid = g;
-      break;
     }
-    h = (h + 1) & tmask;
+    r0 = atomicAdd(gsize + gid, __popc(mask));
   }
-  gid_out[i] = gid;
-  rank_out[i] = atomicAdd(gsize + gid, 1);
+  if (valid) {
+    gid = __shfl_sync(vmask, gid, leader);
+    r0 = __shfl_sync(vmask, r0, leader);
+    gid_out[i] = gid;
+    rank_out[i] = r0 + __popc(mask & ((1u << lane) - 1u));
+  }
 }
 
 // one CTA: segment starts (prefix of group sizes), segment node tuples, chunk table (equal
@@ -183,8 +217,11 @@ __global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t
   __syncthreads();
   for (int base = 0; base < T; base += 1024) {
     const int s = base + t;
+    // every load of the pass first (one latency), then the scan, then the writes
     const int len = s < T ? gsize[s] : 0, nc = (len + kChunk - 1) / kChunk;
-    int a = len, b = nc;   // inclusive warp scans
+    const uint64_t key = s < T ? gkeys[s] : 0;
+    const int32_t hs = s < T ? gslot[s] : 0;
+    int a = len, b = nc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int x = __shfl_up_sync(0xffffffffu, a, o), y = __shfl_up_sync(0xffffffffu, b, o);
@@ -199,21 +236,19 @@ __global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t
         const int u = __shfl_up_sync(0xffffffffu, x, o), v = __shfl_up_sync(0xffffffffu, y, o);
         if (lane >= o) { x += u; y += v; }
       }
-      wsum[0][lane] = x;   // inclusive over warps
+      wsum[0][lane] = x;
       wsum[1][lane] = y;
     }
     __syncthreads();
-    const int pre0 = carry[0] + (w > 0 ? wsum[0][w - 1] : 0) + a - len;   // exclusive
+    const int pre0 = carry[0] + (w > 0 ? wsum[0][w - 1] : 0) + a - len;
     const int pre1 = carry[1] + (w > 0 ? wsum[1][w - 1] : 0) + b - nc;
     if (s < T) {
       seg_start[s] = pre0;
-      const uint64_t key = gkeys[s];
       for (int q = 0; q < K; ++q) seg_nodes[(int64_t)s * K + q] = (int32_t)((key >> (16 * q)) & 0xffffull);
       for (int q = 0; q < nc; ++q)
         chunks[pre1 + q] = make_int4(s, pre0 + (int32_t)((int64_t)len * q / nc), pre0 + (int32_t)((int64_t)len * (q + 1) / nc), 0);
-      const int32_t h = gslot[s];
-      tkeys[h] = kEmpty;
-      tgid[h] = -1;
+      tkeys[hs] = kEmpty;
+      tgid[hs] = -1;
       gsize[s] = 0;
     }
     __syncthreads();
