@@ -203,10 +203,8 @@ __global__ void __launch_bounds__(256) k_group_insert(int64_t n, int64_t cap, co
 // one CTA: segment starts (prefix of group sizes), segment node tuples, chunk table (equal
 // chunks of <= kChunk points per segment), the counts for the pattern readback; re-empties the
 // hash slots and group sizes it used
-__global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t* gcount, const uint64_t* gkeys,
-                                                       const int32_t* gslot, int32_t* gsize, unsigned long long* tkeys,
-                                                       int32_t* tgid, int32_t* seg_start, int32_t* seg_nodes,
-                                                       int4* chunks, int64_t* info) {
+__global__ void __launch_bounds__(1024) k_group_layout(int64_t n, const int32_t* gcount, const int32_t* gsize,
+                                                       int2* pre, int32_t* seg_start, int64_t* info) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   __shared__ int32_t wsum[2][32];
@@ -217,10 +215,7 @@ __global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t
   __syncthreads();
   for (int base = 0; base < T; base += 1024) {
     const int s = base + t;
-    // every load of the pass first (one latency), then the scan, then the writes
     const int len = s < T ? gsize[s] : 0, nc = (len + kChunk - 1) / kChunk;
-    const uint64_t key = s < T ? gkeys[s] : 0;
-    const int32_t hs = s < T ? gslot[s] : 0;
     int a = len, b = nc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -242,15 +237,7 @@ __global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t
     __syncthreads();
     const int pre0 = carry[0] + (w > 0 ? wsum[0][w - 1] : 0) + a - len;
     const int pre1 = carry[1] + (w > 0 ? wsum[1][w - 1] : 0) + b - nc;
-    if (s < T) {
-      seg_start[s] = pre0;
-      for (int q = 0; q < K; ++q) seg_nodes[(int64_t)s * K + q] = (int32_t)((key >> (16 * q)) & 0xffffull);
-      for (int q = 0; q < nc; ++q)
-        chunks[pre1 + q] = make_int4(s, pre0 + (int32_t)((int64_t)len * q / nc), pre0 + (int32_t)((int64_t)len * (q + 1) / nc), 0);
-      tkeys[hs] = kEmpty;
-      tgid[hs] = -1;
-      gsize[s] = 0;
-    }
+    if (s < T) pre[s] = make_int2(pre0, pre1);   // one coalesced store: the writes are spread by k_group_write
     __syncthreads();
     if (t == 0) { carry[0] += wsum[0][31]; carry[1] += wsum[1][31]; }
     __syncthreads();
@@ -259,15 +246,38 @@ __global__ void __launch_bounds__(1024) k_group_layout(int64_t n, int K, int32_t
     seg_start[T] = (int32_t)n;
     info[1] = T;
     info[2] = carry[1];
-    *gcount = 0;
   }
 }
 
+// one thread per group: segment start, node tuple, chunks; re-empties the hash slot and the size
+__global__ void k_group_write(int K, const int32_t* gcount, const uint64_t* gkeys, const int32_t* gslot,
+                              int32_t* gsize, const int2* pre, unsigned long long* tkeys, int32_t* tgid,
+                              int32_t* seg_start, int32_t* seg_nodes, int4* chunks) {
+  pdl_wait();   // programmatic dependent launch (common.cuh)
+  pdl_trigger();
+  const int T = *gcount;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= T) return;
+  const int len = gsize[s], nc = (len + kChunk - 1) / kChunk;
+  const int2 p = pre[s];
+  const uint64_t key = gkeys[s];
+  const int32_t hs = gslot[s];
+  seg_start[s] = p.x;
+  for (int q = 0; q < K; ++q) seg_nodes[s * K + q] = (int32_t)((key >> (16 * q)) & 0xffffull);
+  for (int q = 0; q < nc; ++q)
+    chunks[p.y + q] = make_int4((int)s, p.x + (int32_t)((int64_t)len * q / nc), p.x + (int32_t)((int64_t)len * (q + 1) / nc), 0);
+  tkeys[hs] = kEmpty;
+  tgid[hs] = -1;
+  gsize[s] = 0;
+}
+
+
 __global__ void k_group_perm(int64_t n, const int32_t* gid, const int32_t* rank, const int32_t* seg_start,
-                             uint32_t* perm) {
+                             uint32_t* perm, int32_t* gcount) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *gcount = 0;   // every reader of the group count (the layout kernels) has finished
   if (i >= n) return;
   perm[seg_start[gid[i]] + rank[i]] = (uint32_t)i;
 }
@@ -308,14 +318,17 @@ static cudaError_t build_order_grouped(Ctx* c) {
   launch_pdl(k_group_insert, dim3(b), dim3(256), 0, c->st, n, c->cap, A.kidx.as<int32_t>(), K, tkeys, tgid,
              c->gtab_slots - 1, gcount, c->gkeys.as<uint64_t>(), c->gslot.as<int32_t>(), gsize, c->vals.as<int32_t>(),
              c->vals2.as<int32_t>());
-  launch_pdl(k_group_layout, dim3(1), dim3(1024), 0, c->st, n, K, gcount, c->gkeys.as<uint64_t>(),
-             c->gslot.as<int32_t>(), gsize, tkeys, tgid, c->seg_start.as<int32_t>(), c->seg_nodes.as<int32_t>(),
-             c->chunks.as<int4>(), c->nnz_dev.as<int64_t>());
+  CK(ensure(c, c->scan, (size_t)n * 8));   // per-group (segment start, chunk start)
+  int2* pre = reinterpret_cast<int2*>(c->scan.p);
+  launch_pdl(k_group_layout, dim3(1), dim3(1024), 0, c->st, n, gcount, gsize, pre, c->seg_start.as<int32_t>(),
+             c->nnz_dev.as<int64_t>());
+  launch_pdl(k_group_write, dim3(b), dim3(256), 0, c->st, K, gcount, c->gkeys.as<uint64_t>(), c->gslot.as<int32_t>(),
+             gsize, pre, tkeys, tgid, c->seg_start.as<int32_t>(), c->seg_nodes.as<int32_t>(), c->chunks.as<int4>());
   uint32_t* perm = reinterpret_cast<uint32_t*>(c->keys.p);
   launch_pdl(k_group_perm, dim3(b), dim3(256), 0, c->st, n, c->vals.as<int32_t>(), c->vals2.as<int32_t>(),
-             c->seg_start.as<int32_t>(), perm);
+             c->seg_start.as<int32_t>(), perm, gcount);
   launch_pdl(k_gather_model, dim3(b), dim3(256), 0, c->st, n, perm, model_view(c), model_view_of(c, B), K);
-  count_launches(4);
+  count_launches(5);
   CK(cudaGetLastError());
   c->cur = 1 - c->cur;
   c->nseg = -1;
