@@ -64,7 +64,10 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
 
 /* Flags */
 #define MIS_F_FINAL_ENERGY 1u   /* mis_register also evaluates the energy after the last update */
-#define MIS_F_NO_GRAPH     2u   /* do not capture the GN loop in a CUDA graph                    */
+#define MIS_F_NO_GRAPH     2u   /* reserved, no effect: the GN loop is not captured in a CUDA
+                                   graph -- its kernels are chained by programmatic dependent
+                                   launch and the host stays ahead of the device there; the
+                                   per-frame shapes (pattern, chunks) change every frame        */
 #define MIS_F_GRID_SOLVER  4u   /* force the grid-wide PCG kernel (else the cluster-resident one
                                    whenever the system fits in one cluster's shared memory)       */
 #define MIS_F_STANDARD_PCG 8u   /* cluster kernel: textbook PCG recurrences (2 barriers/iteration)
