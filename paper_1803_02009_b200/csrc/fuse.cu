@@ -407,21 +407,38 @@ __global__ void __launch_bounds__(kTile * kTile) k_skin_tiles(int W, int H, cons
 #pragma unroll
     for (int r = 0; r <= K; ++r) sel[wid][r] = wsel[r];
   __syncthreads();
-  float U2 = INFINITY;
-  {   // block: the (k+1)-th smallest of the 8 warps' sorted lists (every thread, same order: identical)
-    float best[K + 1];
+  __shared__ float U2s;
+  if (wid == 0) {   // block: the (k+1)-th smallest of the 8 warps' k+1 smallest, k+1 rounds of (min, pop)
+    constexpr int NV = (kTile * kTile / 32) * (K + 1);   // 8 (k+1) values, <= 3 per lane (k <= 8)
+    static_assert(NV <= 96, "skin tile merge");
+    float v[3];
 #pragma unroll
-    for (int s = 0; s <= K; ++s) best[s] = INFINITY;
-    for (int w = 0; w < kTile * kTile / 32; ++w)
+    for (int z = 0; z < 3; ++z) {
+      const int q = lane + 32 * z;
+      v[z] = q < NV ? sel[q / (K + 1)][q % (K + 1)] : INFINITY;
+    }
+    float kth = INFINITY;
 #pragma unroll
-      for (int r = 0; r <= K; ++r) {
-        float cu = sel[w][r];
-        if (cu < best[K])
+    for (int r = 0; r <= K; ++r) {
+      float mn = fminf(v[0], fminf(v[1], v[2]));
 #pragma unroll
-          for (int s = 0; s <= K; ++s) if (cu < best[s]) { const float tt = best[s]; best[s] = cu; cu = tt; }
+      for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      kth = mn;
+      // pop exactly one copy of the minimum (lowest slot, then lowest lane holding it)
+      bool popped = false;
+#pragma unroll
+      for (int z = 0; z < 3; ++z) {
+        const unsigned hz = __ballot_sync(0xffffffffu, v[z] == mn);
+        if (!popped && hz) {
+          if (lane == __ffs(hz) - 1) v[z] = INFINITY;
+          popped = true;
+        }
       }
-    U2 = best[K] * (1.0f + 1e-5f) + 1e-6f;   // conservative against rounding
+    }
+    if (lane == 0) U2s = kth * (1.0f + 1e-5f) + 1e-6f;   // conservative against rounding
   }
+  __syncthreads();
+  const float U2 = U2s;
   // candidates: nodes whose squared distance to the box can be <= U^2
   for (int j = t; j < m; j += blockDim.x) {
     float l2 = 0.f;
