@@ -1164,26 +1164,33 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
     ProfScope ps(c, P_LIFT, 2);
     launch_lift_count(a, counts, nbk, ids_dev, cnt, do_lift, base, c->cap, c->st);
   }
-  int32_t hb[3];   // [lifted total, registered pixels (u64)]: one readback
-  TRY(c, cudaMemcpyAsync(hb, counts + 2 * nbk + 1, 12, cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaStreamSynchronize(c->st));
-  const int32_t n_lift = hb[0];
-  unsigned long long n_reg = 0;
-  memcpy(&n_reg, hb + 1, 8);
-  if (c->n + n_lift > c->cap) {
-    *n_out = c->n;
-    return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
-  }
-  if (n_lift > 0) {
+  // one readback of [lifted total, registered pixels (u64)] (pinned, asynchronous).  Lifting
+  // ranks queue the lifted points' writes (+ pixel-key reset) and their K2 behind it, so they
+  // run while the host waits for the count; they write only below the capacity, and points
+  // past an exceeded capacity are ignored (MIS_E_CAPACITY, model size unchanged)
+  TRY(c, cudaMemcpyAsync(c->hpin, counts + 2 * nbk + 1, 12, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaEventRecord(c->rb_ev, c->st));
+  if (do_lift) {
     ProfScope ps(c, P_LIFT, 2);
     ModelView md = model_view(c);
     TRY(c, ensure(c, c->lift_pos, px * 4));
     launch_lift_write(a, counts + nbk + 1, nbk, base, c->cap, ids_dev, c->lift_pos.as<int32_t>(), c->st);   // + key reset
     launch_skin_lifted(c->K, c->W, c->H, c->lift_pos.as<int32_t>(), md, c->g.as<float>(), c->m, c->st);
-    c->dirty = true;
   } else {
     TRY(c, cudaMemsetAsync(c->pixkey.p, 0xff, px * 8, c->st));
   }
+  TRY(c, cudaEventSynchronize(c->rb_ev));
+  int32_t hb[3];
+  memcpy(hb, c->hpin, 12);
+  const int32_t n_lift = hb[0];
+  unsigned long long n_reg = 0;
+  memcpy(&n_reg, hb + 1, 8);
+  if (c->n + n_lift > c->cap) {
+    c->pixkey_clean = true;
+    *n_out = c->n;
+    return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
+  }
+  if (n_lift > 0) c->dirty = true;
   c->pixkey_clean = true;
   if (rgb_staged) TRY(c, cudaEventRecord(c->ev_rgb_free, c->st));   // K11 / K12 have read the staged colours
   TRY(c, cudaGetLastError());
