@@ -225,7 +225,8 @@ cudaError_t launch_solve(const SolveArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s);
 // per frame, after the pattern: the cluster ranks' SpMV pieces and halo push lists
 void launch_pcg_prep(const int32_t* row_ptr, const int32_t* col, const int32_t* part, int cs, int max_rows, int max_nnz,
-                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s);
+                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s,
+                     bool marked = false);
 int pcg_max_pieces(int max_rows, int max_nnz);
 // cluster partition (row boundaries balancing nnz) computed on the device; cl_size 0 = does not fit
 struct PlanOut { int32_t cl_size, max_rows, max_nnz, pad; int64_t smem; };

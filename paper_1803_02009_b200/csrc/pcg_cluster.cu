@@ -948,9 +948,10 @@ __global__ void k_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, P
 }
 
 void launch_pcg_prep(const int32_t* row_ptr, const int32_t* col, const int32_t* part, int cs, int max_rows, int max_nnz,
-                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s) {
+                     int32_t* pptr, int32_t* pc, int32_t* push, int32_t* npush, uint32_t* mask, cudaStream_t s,
+                     bool marked) {
   PcgLists L{pptr, pc, push, npush, mask};
-  launch_pdl(k_pcg_mark, dim3(cs), dim3(256), 0, s, row_ptr, col, part, L);
+  if (!marked) launch_pdl(k_pcg_mark, dim3(cs), dim3(256), 0, s, row_ptr, col, part, L);
   launch_pdl(k_pcg_lists, dim3(cs), dim3(32), 0, s, row_ptr, part, cs, max_rows, max_pieces(max_rows, max_nnz), L);
 }
 int pcg_max_pieces(int max_rows, int max_nnz) { return max_pieces(max_rows, max_nnz); }

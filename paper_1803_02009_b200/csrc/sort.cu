@@ -540,51 +540,81 @@ __device__ __forceinline__ int find_entry(const int32_t* row_ptr, const int32_t*
   return (lo < row_ptr[a + 1] && col[lo] == b) ? lo : -1;
 }
 
-// upper_of: the (min, max) entry of each entry; lower_of[upper] = its mirror (-1 on the diagonal)
-__global__ void k_upper_lower(const int32_t* row_ptr, const int32_t* col, const int32_t* row_of, int m,
-                              int32_t* upper_of, int32_t* lower_of, int2* ulist, unsigned long long* ucount) {
+// After k_row_fill, three independent jobs in one launch (block ranges): the mirror / upper maps
+// and the finalisation's off-diagonal list (k_upper_lower), the cluster PCG's halo marks (each
+// rank marks, in the owner's mask, the rows its blocks read: as k_pcg_mark) and the slot tables
+// (k_slots).  One launch instead of three keeps the device fed while the host is still catching
+// up after the pattern readback.
+struct PostArgs {
+  const int32_t *row_ptr, *col, *row_of;
+  int m;
+  int32_t *upper_of, *lower_of;
+  int2* ulist;
+  unsigned long long* ucount;
+  int64_t nnz, ul_blocks;
+  // halo marks (cs = 0: none)
+  const int32_t* part;
+  int cs;
+  uint32_t* mask;
+  int32_t* nin;
+  // slots
+  int64_t nseg;
+  const int32_t* seg_nodes;
+  int K, n_nbr, nf;
+  const int32_t *nbr, *fidx;
+  int32_t *seg_slot, *edge_slot, *feat_slot;
+  int64_t total;
+};
+__device__ __forceinline__ void slot_item(const PostArgs& a, int64_t t);
+__global__ void k_pattern_post(PostArgs a) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
-  const int64_t nnz = row_ptr[m];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = row_of[e], cc = col[e];
-    if (r == cc) {
-      upper_of[e] = (int32_t)e;
-      lower_of[e] = -1;
-    } else if (r < cc) {
-      upper_of[e] = (int32_t)e;
-      const int lo = find_entry(row_ptr, col, cc, r);
-      lower_of[e] = lo;
-      ulist[atomicAdd(ucount, 1ull)] = make_int2((int)e, lo);   // the finalisation's off-diagonal work list
-    } else {
-      upper_of[e] = find_entry(row_ptr, col, cc, r);
+  const int64_t b = blockIdx.x;
+  if (b < a.ul_blocks) {
+    for (int64_t e = b * blockDim.x + threadIdx.x; e < a.nnz; e += a.ul_blocks * blockDim.x) {
+      const int r = a.row_of[e], cc = a.col[e];
+      if (r == cc) {
+        a.upper_of[e] = (int32_t)e;
+        a.lower_of[e] = -1;
+      } else if (r < cc) {
+        a.upper_of[e] = (int32_t)e;
+        const int lo = find_entry(a.row_ptr, a.col, cc, r);
+        a.lower_of[e] = lo;
+        a.ulist[atomicAdd(a.ucount, 1ull)] = make_int2((int)e, lo);
+      } else {
+        a.upper_of[e] = find_entry(a.row_ptr, a.col, cc, r);
+      }
     }
+    return;
   }
+  if (b < a.ul_blocks + a.cs) {
+    const int rank = (int)(b - a.ul_blocks), r0 = a.part[rank], r1 = a.part[rank + 1];
+    if (rank == 0 && threadIdx.x < 16) a.nin[threadIdx.x] = 0;   // summed by k_pcg_lists
+    for (int k = a.row_ptr[r0] + threadIdx.x; k < a.row_ptr[r1]; k += blockDim.x) {
+      const int j = a.col[k];
+      if (j < r0 || j >= r1) atomicOr(a.mask + j, 1u << rank);
+    }
+    return;
+  }
+  const int64_t t = (b - a.ul_blocks - a.cs) * blockDim.x + threadIdx.x;
+  if (t < a.total) slot_item(a, t);
 }
-
-// slot tables: (segment, pair), (node, edge), (feature, pair) -> upper BSR entry
-__global__ void k_slots(int64_t nseg, const int32_t* seg_nodes, int K, int m, int n_nbr, const int32_t* nbr, int nf,
-                        const int32_t* fidx, const int32_t* row_ptr, const int32_t* col, int32_t* seg_slot,
-                        int32_t* edge_slot, int32_t* feat_slot, int64_t total) {
-  pdl_wait();   // programmatic dependent launch (common.cuh)
-  pdl_trigger();
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= total) return;
-  const int P = K * (K + 1) / 2;
-  const int64_t ns = nseg * P, ne = (int64_t)m * n_nbr;
+__device__ __forceinline__ void slot_item(const PostArgs& a, int64_t t) {
+  const int K = a.K, P = K * (K + 1) / 2;
+  const int64_t ns = a.nseg * P, ne = (int64_t)a.m * a.n_nbr;
   int j, off;
   if (t < ns) {
     const int64_t sg = t / P;
     pair_of((int)(t % P), K, j, off);
-    seg_slot[t] = find_entry(row_ptr, col, seg_nodes[sg * K + j], seg_nodes[sg * K + j + off]);
+    a.seg_slot[t] = find_entry(a.row_ptr, a.col, a.seg_nodes[sg * K + j], a.seg_nodes[sg * K + j + off]);
   } else if (t < ns + ne) {
     const int64_t e = t - ns;
-    const int l = nbr[e], a = (int)(e / n_nbr);
-    edge_slot[e] = (l >= 0) ? find_entry(row_ptr, col, min(a, l), max(a, l)) : -1;
+    const int l = a.nbr[e], q = (int)(e / a.n_nbr);
+    a.edge_slot[e] = (l >= 0) ? find_entry(a.row_ptr, a.col, min(q, l), max(q, l)) : -1;
   } else {
     const int64_t e = t - ns - ne, f = e / P;
     pair_of((int)(e % P), K, j, off);
-    feat_slot[e] = find_entry(row_ptr, col, fidx[(int64_t)j * nf + f], fidx[(int64_t)(j + off) * nf + f]);
+    a.feat_slot[e] = find_entry(a.row_ptr, a.col, a.fidx[(int64_t)j * a.nf + f], a.fidx[(int64_t)(j + off) * a.nf + f]);
   }
 }
 
@@ -645,12 +675,12 @@ cudaError_t build_pattern(Ctx* c) {
   launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
              c->row_of.as<int32_t>(), c->diag_pos.as<int32_t>(), info);
   c->bitmap_clean = true;
-  count_launches(1 + (nnz > 0) + (c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P > 0));
-  if (nnz > 0)
-    launch_pdl(k_upper_lower, dim3((unsigned)std::min<int64_t>(grid, (nnz + 255) / 256)), dim3(256), 0, c->st,
-        c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->row_of.as<int32_t>(), m, c->upper_of.as<int32_t>(),
-        c->lower_of.as<int32_t>(), c->ulist.as<int2>(), reinterpret_cast<unsigned long long*>(info + 7));
-  if (c->cl_size > 0 && nnz > 0) {   // cluster PCG: per-rank SpMV pieces and halo lists for the frame
+  const int64_t total = c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P;
+  CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
+  CK(ensure(c, c->edge_slot, ((int64_t)m * c->prm.n_nbr + 1) * 4));
+  CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
+  const bool clu = c->cl_size > 0 && nnz > 0;   // cluster PCG: per-rank SpMV pieces and halo lists for the frame
+  if (clu) {
     const int cs = c->cl_size, mr = c->cl_max_rows, mp = pcg_max_pieces(c->cl_max_rows, c->cl_max_nnz);
     CK(ensure(c, c->pcg_pptr, (size_t)cs * (mr + 1) * 4));
     CK(ensure(c, c->pcg_pc, (size_t)cs * mp * 4));
@@ -660,22 +690,29 @@ cudaError_t build_pattern(Ctx* c) {
       CK(ensure(c, c->pcg_mask, (size_t)m * 4));
       CK(cudaMemsetAsync(c->pcg_mask.p, 0, (size_t)m * 4, c->st));   // kept zero by k_pcg_lists
     }
-    launch_pcg_prep(c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->part.as<int32_t>(), cs, mr, c->cl_max_nnz,
-                    c->pcg_pptr.as<int32_t>(), c->pcg_pc.as<int32_t>(), c->pcg_push.as<int32_t>(),
-                    c->pcg_npush.as<int32_t>(), c->pcg_mask.as<uint32_t>(), c->st);
-    count_launches(2);
   }
-  // slot tables (exact sizes now)
-  const int64_t total = c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P;
-  CK(ensure(c, c->seg_slot, (c->nseg * P + 1) * 4));
-  CK(ensure(c, c->edge_slot, ((int64_t)m * c->prm.n_nbr + 1) * 4));
-  CK(ensure(c, c->feat_slot, ((int64_t)c->nf * P + 1) * 4));
-  if (total > 0)
-    launch_pdl(k_slots, dim3((int)((total + 255) / 256)), dim3(256), 0, c->st, c->nseg, c->seg_nodes.as<int32_t>(), K, m, c->prm.n_nbr,
-                                                          c->nbr.as<int32_t>(), c->nf, c->fidx.as<int32_t>(),
-                                                          c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
-                                                          c->seg_slot.as<int32_t>(), c->edge_slot.as<int32_t>(),
-                                                          c->feat_slot.as<int32_t>(), total);
+  {
+    PostArgs pa;
+    pa.row_ptr = c->row_ptr.as<int32_t>(); pa.col = c->col.as<int32_t>(); pa.row_of = c->row_of.as<int32_t>();
+    pa.m = m; pa.upper_of = c->upper_of.as<int32_t>(); pa.lower_of = c->lower_of.as<int32_t>();
+    pa.ulist = c->ulist.as<int2>(); pa.ucount = reinterpret_cast<unsigned long long*>(info + 7);
+    pa.nnz = nnz; pa.ul_blocks = nnz > 0 ? std::min<int64_t>(grid, (nnz + 255) / 256) : 0;
+    pa.part = c->part.as<int32_t>(); pa.cs = clu ? c->cl_size : 0;
+    pa.mask = c->pcg_mask.as<uint32_t>(); pa.nin = c->pcg_npush.as<int32_t>() + 16;
+    pa.nseg = c->nseg; pa.seg_nodes = c->seg_nodes.as<int32_t>(); pa.K = K; pa.n_nbr = c->prm.n_nbr; pa.nf = c->nf;
+    pa.nbr = c->nbr.as<int32_t>(); pa.fidx = c->fidx.as<int32_t>();
+    pa.seg_slot = c->seg_slot.as<int32_t>(); pa.edge_slot = c->edge_slot.as<int32_t>();
+    pa.feat_slot = c->feat_slot.as<int32_t>(); pa.total = total;
+    const int64_t blocks = pa.ul_blocks + pa.cs + (total + 255) / 256;
+    if (blocks > 0) launch_pdl(k_pattern_post, dim3((unsigned)blocks), dim3(256), 0, c->st, pa);
+  }
+  count_launches(2);
+  if (clu) {
+    launch_pcg_prep(c->row_ptr.as<int32_t>(), c->col.as<int32_t>(), c->part.as<int32_t>(), c->cl_size, c->cl_max_rows,
+                    c->cl_max_nnz, c->pcg_pptr.as<int32_t>(), c->pcg_pc.as<int32_t>(), c->pcg_push.as<int32_t>(),
+                    c->pcg_npush.as<int32_t>(), c->pcg_mask.as<uint32_t>(), c->st, /*marked=*/true);
+    count_launches(1);
+  }
   CK(cudaGetLastError());
   // accumulators (K3 commits atomically into them) and solver buffers
   const size_t m6 = 6 * (size_t)m;
