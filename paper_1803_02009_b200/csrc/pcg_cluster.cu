@@ -105,11 +105,18 @@ __global__ void k_pcg_lists(const int32_t* row_ptr, const int32_t* part, int cs,
     }
     if (l == 31) pptr[nr] = inc;
   }
+  // the rows' reader masks, loaded once (registers for the first 128 rows): the d loop below
+  // would otherwise issue a dependent global load per (destination, 32 rows)
+  uint32_t mreg[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) mreg[q] = (32 * q + l < nr) ? L.mask[r0 + 32 * q + l] : 0u;
   int n = 0;
   for (int d = 0; d < cs; ++d)
     for (int b = 0; b < nr; b += 32) {
       const int i = b + l;
-      const bool on = i < nr && (d == rank || ((L.mask[r0 + i] >> d) & 1u));
+      const uint32_t mk = b < 128 ? (b == 0 ? mreg[0] : b == 32 ? mreg[1] : b == 64 ? mreg[2] : mreg[3])
+                                  : (i < nr ? L.mask[r0 + i] : 0u);
+      const bool on = i < nr && (d == rank || ((mk >> d) & 1u));
       const unsigned bal = __ballot_sync(0xffffffffu, on);
       if (on) push[n + __popc(bal & ((1u << l) - 1u))] = (d << 16) | i;
       n += __popc(bal);
