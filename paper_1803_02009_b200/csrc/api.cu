@@ -910,6 +910,9 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
   if (!c) return MIS_E_ARG;
   cudaSetDevice(c->device);
   mis_status s;
+  // the report block is zeroed first: enqueued while the device is still busy with earlier work,
+  // it is not a host-bound step between the pattern and the first assembly
+  TRY(c, cudaMemsetAsync(c->rep.p, 0, kRepBytes, c->st));
   if (depth_mm) {
     if ((s = set_frame_impl(c, mem, depth_mm, intr, pose, true)) != MIS_OK) return s;
   } else if (pose) {
@@ -931,7 +934,6 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
     TRY(c, ensure(c, c->rhs2, (size_t)c->m * 6 * 4));
     TRY(c, ensure(c, c->Rt_acc, (size_t)c->m * 96));
   }
-  TRY(c, cudaMemsetAsync(c->rep.p, 0, kRepBytes, c->st));
   for (int it = 0; it < G; ++it) {
     if ((s = assemble(c, false, it)) != MIS_OK) return s;
     ProfScope ps(c, P_SOLVE, 1);
