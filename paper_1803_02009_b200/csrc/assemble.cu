@@ -211,9 +211,9 @@ template <int K, bool DBG>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_blocks) {
   pdl_wait();   // node states from the previous solve
+  pdl_trigger();   // K3b's CTAs may start their table prologue on the SMs this grid's tail frees
   if (blockIdx.x >= point_blocks) {
     graph_item(ga, (int64_t)(blockIdx.x - point_blocks) * blockDim.x + threadIdx.x);
-    pdl_trigger();
     return;
   }
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -230,7 +230,6 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArg
     ps[(K + 1) * S + i] = st.nn;
   }
   commit_point_energies(a, ed, ep, as);
-  pdl_trigger();
 }
 
 // factor row of one point from its compact state (K3b: shared memory, FSP floats)
@@ -341,6 +340,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
   }
 
   pdl_wait();   // K3a's factor state (the tables above are independent of it)
+  pdl_trigger();   // the finalisation may launch early (it waits for this grid's completion)
   // dynamic chunk scheduling (segments are uneven): one atomic fetch per chunk per warp
   int64_t c = 0;
   if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
@@ -430,7 +430,6 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
-  pdl_trigger();
 }
 
 // ---------------------------------------------------------------- K3b on tensor cores (k <= 4)
@@ -590,6 +589,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
   }
 
   pdl_wait();   // K3a's factor state (the tables above are independent of it)
+  pdl_trigger();   // the finalisation may launch early (it waits for this grid's completion)
   int64_t c = 0;
   if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
   c = __shfl_sync(0xffffffffu, c, 0);
@@ -684,7 +684,6 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
-  pdl_trigger();
 }
 
 // ---- tensor-core K3b for 5 <= k <= 8 (C5): the same per-chunk Gram sums as k_accum_points_tc with
