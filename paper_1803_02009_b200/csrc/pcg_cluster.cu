@@ -576,8 +576,9 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
       for (int k = t; k < 3 * npush; k += kCT) {
         const int e = push[k / 3], qq = k - 3 * (k / 3), dst = e >> 16, i = e & 0xffff;
         const float2 v = reinterpret_cast<const float2*>(ms + 6 * i)[qq];
-        if (dst == rank) reinterpret_cast<float2*>(Zb + 6 * (r0 + i))[qq] = v;
-        else st_async_f2(map_rank_u32(zb_u + 4u * (uint32_t)(6 * (r0 + i) + 2 * qq), dst), v, map_rank_u32(bar_u, dst));
+        // own rows too: every value read after the wait arrives through the mbarrier, so no
+        // CTA barrier is needed after it
+        st_async_f2(map_rank_u32(zb_u + 4u * (uint32_t)(6 * (r0 + i) + 2 * qq), dst), v, map_rank_u32(bar_u, dst));
       }
     }
     if (st1) ts[10] = gtimer();
@@ -589,10 +590,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
       __syncthreads();
       if (wi == 0) {
         const double sg = warp_sum_all(l < kWarps ? red[l] : 0.0), sd = warp_sum_all(l < kWarps ? red[32 + l] : 0.0);
-        if (l == rank) {
-          gam[rank] = sg;
-          del[rank] = sd;
-        } else if (l < cs) {
+        if (l < cs) {
           const uint32_t rb = map_rank_u32(bar_u, l);
           st_async_f64(map_rank_u32(smem_u32(gam + rank), l), sg, rb);
           st_async_f64(map_rank_u32(smem_u32(del + rank), l), sd, rb);
@@ -604,7 +602,6 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     double inv_gprev = 1.0 / gprev, inv_aprev = aprev_den / gprev;
     asm volatile("" : "+d"(inv_gprev), "+d"(inv_aprev));
     mbar_wait_bounded(bar, (uint32_t)(it >> 1) & 1u);
-    __syncthreads();   // this CTA's own rows / dot slots, written by other threads, visible
     if (st1) ts[12] = gtimer();
     g = gather_sum16(gam);
     double d = gather_sum16(del);
@@ -796,7 +793,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
   if (stamp) ts[2] = gtimer();
   double rz = 0.0, rz0 = 0.0;
   if (a.pipelined && 6 * a.max_rows <= kCT) {
-    const uint32_t in_bytes = (uint32_t)(24 * a.npush[kMaxCluster + rank] + 16 * (cs - 1));
+    const uint32_t in_bytes = (uint32_t)(24 * (a.npush[kMaxCluster + rank] + nr) + 16 * cs);   // halo + own rows, dots
     pcg_pipelined_reg(a, cl, sm, L, rank, cs, r0, nr, col, H, Mi, &rz, &rz0, stamp ? ts : nullptr, pptr, pc, part, push,
                       npush, R, pcg_bar, in_bytes, lam_t);
     if (stamp) ts[3] = ts[2];
