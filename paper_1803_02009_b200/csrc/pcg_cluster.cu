@@ -742,9 +742,12 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
       else rt[q] = a.Rt_acc[12 * (int64_t)r0 + q];
     }
     // damped block-Jacobi inverses: (H_jj with its diagonal times (1 + mu) + (lambda + guard) I)^-1,
-    // fp64 Gauss-Jordan, one warp per node (lane rr < 6 holds row rr)
-    const int wi = t >> 5, l = t & 31, rr = l < 6 ? l : 0;
-    for (int i = wi; i < nr; i += kWarps) {
+    // fp64 Gauss-Jordan, one 8-lane group per node (lane rr < 6 of the group holds row rr), so the
+    // CTA's <= 64 nodes take one pass
+    const int wi = t >> 5, l = t & 31, gl = l & 7, rr = gl < 6 ? gl : 0;
+    for (int base = 4 * wi; base < nr; base += 4 * kWarps) {   // warp-uniform trip count (shuffles)
+      const bool act = base + (l >> 3) < nr;
+      const int i = act ? base + (l >> 3) : base;
       const int k0 = pc[pptr[i]] & 0xffffff, k1 = i + 1 < nr ? (pc[pptr[i + 1]] & 0xffffff) : ne;
       int kd = k0;
       for (int k = k0; k < k1; ++k)
@@ -763,16 +766,16 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
       bool pd = true;
 #pragma unroll
       for (int pv_i = 0; pv_i < 6; ++pv_i) {
-        const double pv = __shfl_sync(0xffffffffu, row[pv_i], pv_i);
+        const double pv = __shfl_sync(0xffffffffu, row[pv_i], pv_i, 8);
         if (!(pv > 0.0)) pd = false;
         const double ipv = 1.0 / pv, f = row[pv_i] * ipv;
 #pragma unroll
         for (int q = 0; q < 12; ++q) {
-          const double pq = __shfl_sync(0xffffffffu, row[q], pv_i);
+          const double pq = __shfl_sync(0xffffffffu, row[q], pv_i, 8);
           row[q] = rr == pv_i ? pq * ipv : row[q] - f * pq;
         }
       }
-      if (l < 6)
+      if (act && gl < 6)
 #pragma unroll
         for (int q = 0; q < 6; ++q) Mi[36 * i + 6 * rr + q] = pd ? (float)row[6 + q] : 0.f;
     }
