@@ -28,9 +28,12 @@
  *  - Layouts: xyz-like arrays are n x 3 row-major float32 (x, y, z), node
  *    states are m x 12 float32 (R row-major 9, t 3), pose[12] is the
  *    world->camera transform (R row-major 9, T 3) of Eq. 1.
- *  - Internal point order: points are kept sorted by their canonical kNN
- *    tuple (the K13 sort); every per-point output is in that internal order
- *    and mis_get_model returns the caller ids that map it back.
+ *  - Internal point order: points are kept grouped by their canonical kNN
+ *    tuple, every tuple's points contiguous (K13: exact-tuple hash grouping
+ *    for k <= 4 and m < 65535, where the order of the groups and within a
+ *    group is unspecified; else a stable radix sort of a tuple hash); every
+ *    per-point output is in that internal order and mis_get_model returns the
+ *    caller ids that map it back.
  */
 #ifndef MIS_H
 #define MIS_H
@@ -154,8 +157,8 @@ mis_status mis_set_model(mis_ctx* ctx, int64_t n, mis_mem mem, const float* xyz,
  * order (distinct ids per point, weights >= 0, normalised in the warp,
  * reading A6).  knn_idx == NULL: the skinning is computed on the device by
  * Eq. 2 (k+1 nearest nodes, ties to the lower id; requires m >= k+1).
- * Resets every node transform to the identity (R_j = I, t_j = 0).  Sorts the
- * points by their canonical kNN tuple (internal order).
+ * Resets every node transform to the identity (R_j = I, t_j = 0).  Groups the
+ * points by their canonical kNN tuple (internal order, see above).
  * Validation (MIS_E_ARG): with MIS_MEM_HOST inputs before returning; with
  * MIS_MEM_DEVICE inputs without a host synchronisation -- invalid ids are
  * clamped / dropped on the device and the next mis_register (or mis_dbg_*)
