@@ -92,6 +92,9 @@ def lib():
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p]
             L.or_fuse.restype = C.c_int64
+            L.or_filter.argtypes = [C.c_int64] + [C.c_void_p] * 6 + [C.c_float, C.c_int32, C.c_int32, C.c_float,
+                                                                      C.c_float] + [C.c_void_p] * 8
+            L.or_filter.restype = C.c_int64
             _lib = L
     return _lib
 
@@ -287,4 +290,23 @@ def fuse(prm: or_params, xyz, nrm, rgb, weight, stamp, fr: Frame, rgb_obs, frame
     for key in ("lift_idx", "lift_w", "lift_margin"):
         out[key] = out[key][:nl]
     out["n_lift"] = int(nl)
+    return out
+
+
+def filter_points(xyz, nrm, rgb, weight, stamp, ids, grid, frame_index, tau_time, tau_weight, omega_max):
+    """O7: Alg. 3 downsampling + deletion (readings A30-A34)."""
+    xyz, nrm, rgb, weight = _f32(xyz), _f32(nrm), _f32(rgb), _f32(weight)
+    stamp = _i32(stamp)
+    ids = None if ids is None else np.ascontiguousarray(ids, np.int64)
+    n = xyz.shape[0]
+    out = dict(xyz=np.zeros((n, 3)), nrm=np.zeros((n, 3)), rgb=np.zeros((n, 3)), weight=np.zeros(n),
+               stamp=np.zeros(n, np.int32), ids=np.zeros(n, np.int64), stable=np.zeros(n, np.uint8))
+    cells = C.c_int64(0)
+    no = lib().or_filter(n, _p(xyz), _p(nrm), _p(rgb), _p(weight), _p(stamp), _p(ids), float(grid), int(frame_index),
+                         int(tau_time), float(tau_weight), float(omega_max), _p(out["xyz"]), _p(out["nrm"]),
+                         _p(out["rgb"]), _p(out["weight"]), _p(out["stamp"]), _p(out["ids"]), _p(out["stable"]),
+                         C.addressof(cells))
+    for key in list(out):
+        out[key] = out[key][:no]
+    out["cells"] = int(cells.value)
     return out

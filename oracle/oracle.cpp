@@ -891,4 +891,60 @@ int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, co
   return nl;
 }
 
+// O7 (NEXT-1): Alg. 3, "Down sample point cloud according to grid size" read as
+// P:597 "setting a fixed box to average points fill inside each 3D box" with the averages of
+// S:369 (readings A30-A34), then the deletion test of Alg. 3 line 3 in the form of S:369.
+int64_t or_filter(int64_t n, const float* xyz, const float* nrm, const float* rgb, const float* weight,
+                  const int32_t* stamp, const int64_t* ids, float grid, int32_t frame_index, int32_t tau_time,
+                  float tau_weight, float omega_max, double* xyz_out, double* nrm_out, double* rgb_out,
+                  double* weight_out, int32_t* stamp_out, int64_t* ids_out, uint8_t* stable_out,
+                  int64_t* cells_out) {
+  // the fixed boxes: members of every cell in ascending input index (A30, A31)
+  std::map<std::array<int64_t, 3>, std::vector<int64_t>> cells;
+  for (int64_t i = 0; i < n; ++i) {
+    std::array<int64_t, 3> key;
+    for (int a = 0; a < 3; ++a) {
+      float q = xyz[3 * i + a] / grid;   // fp32 division and floor: the decision's precision (A30)
+      key[a] = (int64_t)floorf(q);
+    }
+    cells[key].push_back(i);
+  }
+  if (cells_out) *cells_out = (int64_t)cells.size();
+  int64_t o = 0;
+  for (const auto& cell : cells) {   // std::map: ascending (kx, ky, kz) (A33)
+    const std::vector<int64_t>& mem = cell.second;
+    double wsum = 0.0;
+    for (int64_t i : mem) wsum += (double)weight[i];
+    const bool weighted = wsum > 0.0;
+    V3 v = v3(0, 0, 0), nn = v3(0, 0, 0), c = v3(0, 0, 0);
+    double den = 0.0;
+    int32_t t = std::numeric_limits<int32_t>::min();
+    for (int64_t i : mem) {
+      const double wi = weighted ? (double)weight[i] : 1.0;
+      for (int a = 0; a < 3; ++a) {
+        v[a] += wi * (double)xyz[3 * i + a];
+        nn[a] += wi * (double)nrm[3 * i + a];
+        c[a] += wi * (double)rgb[3 * i + a];
+      }
+      den += wi;
+      t = std::max(t, stamp[i]);
+    }
+    const double len = std::sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+    const double om = std::min(wsum, (double)omega_max);            // Eq. 15 cap
+    // Alg. 3 line 3 as S:369: t_k < frame - tau_time and omega_k < tau_weight -> delete
+    if ((int64_t)t < (int64_t)frame_index - (int64_t)tau_time && om < (double)tau_weight) continue;
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * o + a] = v[a] / den;
+      nrm_out[3 * o + a] = len > 0.0 ? nn[a] / len : (double)nrm[3 * mem[0] + a];
+      rgb_out[3 * o + a] = c[a] / den;
+    }
+    weight_out[o] = om;
+    stamp_out[o] = t;                                                  // Alg. 3 keeps the max stamp
+    ids_out[o] = ids ? ids[mem[0]] : mem[0];
+    stable_out[o] = om >= (double)tau_weight ? 1 : 0;                  // S_i (A32)
+    ++o;
+  }
+  return o;
+}
+
 }  // extern "C"

@@ -121,6 +121,23 @@ int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, co
                 int32_t* lift_idx, double* lift_w, double* lift_margin,
                 int64_t* owner, double* key_margin, uint8_t* why, double* gate_margin);
 
+/* O7 (NEXT-1): Alg. 3 point filtering with the downsampling of
+ * P:597 and the reading of S:369 (A30-A34).  Cells: (floor(x/grid),
+ * floor(y/grid), floor(z/grid)), each quotient an IEEE fp32 division and floor
+ * (A30).  Per non-empty cell, members in ascending input index: position,
+ * normal and colour weighted by omega (unweighted if the cell's omega sum is
+ * 0), the normal renormalised (the first member's if the sum is 0), omega =
+ * min(sum omega, omega_max), stamp = max, id = the first member's (A31).
+ * Then Alg. 3: delete the merged point iff stamp < frame - tau_time and
+ * omega < tau_weight; stable = omega >= tau_weight (A32).  Survivors are
+ * written in ascending (kx, ky, kz) order (A33).  Outputs sized n.
+ * cells_out (nullable): the number of non-empty cells.  Returns survivors. */
+int64_t or_filter(int64_t n, const float* xyz, const float* nrm, const float* rgb, const float* weight,
+                  const int32_t* stamp, const int64_t* ids, float grid, int32_t frame_index, int32_t tau_time,
+                  float tau_weight, float omega_max, double* xyz_out, double* nrm_out, double* rgb_out,
+                  double* weight_out, int32_t* stamp_out, int64_t* ids_out, uint8_t* stable_out,
+                  int64_t* cells_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -720,3 +720,98 @@ def test_lm_accepted_energy_strictly_decreasing_and_final_is_best():
     Ef = O.system(prm, pb, fr, Rt)["energy"][4]
     assert abs(Ef - ea[-1]) < 1e-9 * ea[0]
     assert (E[acc == 0, 4] >= ea.min()).all()
+
+
+# ------------------------------------------------------------------ O7: Alg. 3 filtering (NEXT-1)
+def _flt(xyz, w, stamp, grid, frame=20, tau_time=10, tau_weight=3.0, omega_max=20.0, nrm=None, rgb=None, ids=None):
+    xyz = np.asarray(xyz, np.float64)
+    n = len(xyz)
+    nrm = np.tile([0.0, 0.0, 1.0], (n, 1)) if nrm is None else nrm
+    rgb = np.zeros((n, 3)) if rgb is None else rgb
+    return O.filter_points(xyz, nrm, rgb, np.asarray(w, np.float64), np.asarray(stamp), ids, grid, frame,
+                           tau_time, tau_weight, omega_max)
+
+
+def test_filter_spec_two_point_cell():
+    """one cell, weights 1 and 3, depths 10 and 20 -> weighted mean (10*1 + 20*3)/4 = 17.5, omega 4."""
+    o = _flt([[0.5, 0.5, 10.0], [0.5, 0.5, 20.0]], [1.0, 3.0], [20, 20], grid=100.0)
+    assert o["cells"] == 1 and len(o["weight"]) == 1
+    np.testing.assert_allclose(o["xyz"][0], [0.5, 0.5, 17.5], rtol=0, atol=1e-12)
+    assert o["weight"][0] == 4.0 and o["stable"][0] == 1
+
+
+def test_filter_spec_time_rule():
+    """S:373-374 ("time stamp threshold is set to 10"): delete iff t < frame - tau_time and omega < tau_weight."""
+    pts = [[0.5, 0.5, 0.5], [10.5, 0.5, 0.5], [20.5, 0.5, 0.5], [30.5, 0.5, 0.5]]
+    # fresh (t = frame), last seen tau_time ago (kept: boundary), tau_time+1 ago (deleted), old but heavy (kept)
+    o = _flt(pts, [1.0, 1.0, 1.0, 5.0], [20, 10, 9, 0], grid=1.0, frame=20, tau_time=10, tau_weight=3.0)
+    np.testing.assert_array_equal(o["xyz"][:, 0], [0.5, 10.5, 30.5])
+    np.testing.assert_array_equal(o["stable"], [0, 0, 1])
+    np.testing.assert_array_equal(o["ids"], [0, 1, 3])
+
+
+def test_filter_weight_cap_and_zero_weight_cell():
+    """Eq. 15 cap in the merge; a cell whose weights sum to 0 takes the plain mean."""
+    o = _flt([[0.2, 0.2, 0.2], [0.4, 0.4, 0.4], [5.1, 5.1, 5.1], [5.3, 5.1, 5.1]], [15.0, 9.0, 0.0, 0.0],
+             [20, 20, 20, 20], grid=1.0, omega_max=20.0)
+    assert o["weight"][0] == 20.0
+    np.testing.assert_allclose(o["xyz"][0], np.full(3, (15 * 0.2 + 9 * 0.4) / 24.0), atol=1e-7)
+    np.testing.assert_allclose(o["xyz"][1], [5.2, 5.1, 5.1], atol=1e-6)
+    assert o["weight"][1] == 0.0
+
+
+def test_filter_single_cell_is_weighted_centroid():
+    """A box holding every point: numpy's weighted average, renormalised mean normal, max stamp, first id."""
+    rng = np.random.default_rng(7)
+    n = 50
+    xyz = rng.uniform(1.0, 9.0, (n, 3))
+    nrm = rng.normal(size=(n, 3)); nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    nrm[:, 2] = np.abs(nrm[:, 2]) + 0.5
+    rgb = rng.uniform(0, 1, (n, 3))
+    w = rng.uniform(0.5, 2.0, n)
+    st = rng.integers(0, 20, n)
+    ids = rng.integers(1000, 2000, n)
+    o = _flt(xyz, w, st, grid=10.0, nrm=nrm, rgb=rgb, ids=ids, omega_max=1e9)
+    x32 = xyz.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(o["xyz"][0], np.average(x32, axis=0, weights=w.astype(np.float32)), rtol=1e-12)
+    np.testing.assert_allclose(o["rgb"][0], np.average(rgb.astype(np.float32).astype(np.float64), axis=0,
+                                                          weights=w.astype(np.float32)),
+                               rtol=1e-12)
+    nm = np.average(nrm.astype(np.float32).astype(np.float64), axis=0, weights=w.astype(np.float32))
+    np.testing.assert_allclose(o["nrm"][0], nm / np.linalg.norm(nm), rtol=1e-12)
+    assert o["stamp"][0] == st.max() and o["ids"][0] == ids[0]
+    np.testing.assert_allclose(o["weight"][0], w.astype(np.float32).astype(np.float64).sum(), rtol=1e-12)
+
+
+def test_filter_distinct_cells_is_a_sorted_identity():
+    """Grid finer than the spacing: every point alone -> values unchanged, order = lexsort of the cell keys."""
+    rng = np.random.default_rng(3)
+    lat = np.stack(np.meshgrid(np.arange(6), np.arange(5), np.arange(4), indexing="ij"), -1).reshape(-1, 3)
+    perm = rng.permutation(len(lat))
+    xyz = (lat[perm] * 2.0 + 0.5).astype(np.float32)
+    w = rng.uniform(1, 5, len(xyz)).astype(np.float32)
+    o = _flt(xyz, w, np.full(len(xyz), 20), grid=2.0, omega_max=100.0)
+    order = np.lexsort((lat[perm][:, 2], lat[perm][:, 1], lat[perm][:, 0]))
+    np.testing.assert_array_equal(o["xyz"], xyz[order].astype(np.float64))
+    np.testing.assert_array_equal(o["weight"], w[order].astype(np.float64))
+    np.testing.assert_array_equal(o["ids"], order)
+
+
+def test_filter_conserves_weighted_mass_and_stays_in_cell():
+    """Random cloud, no cap, no deletion: per-cell sum of omega*v conserved, merged points inside their box,
+    cell count = distinct floor keys (numpy), keys strictly ascending."""
+    rng = np.random.default_rng(11)
+    n = 4000
+    xyz = rng.normal(0, 20, (n, 3)).astype(np.float32)
+    w = rng.uniform(0.5, 3.0, n).astype(np.float32)
+    grid = np.float32(3.0)
+    o = _flt(xyz, w, np.zeros(n, int), grid=float(grid), frame=0, tau_time=10, omega_max=1e9)
+    keys = np.floor(xyz / grid).astype(np.int64)
+    uk, inv = np.unique(keys, axis=0, return_inverse=True)
+    assert o["cells"] == len(uk) == len(o["weight"])
+    mass = np.zeros((len(uk), 3)); np.add.at(mass, inv.ravel(), w[:, None].astype(np.float64) * xyz)
+    wsum = np.zeros(len(uk)); np.add.at(wsum, inv.ravel(), w.astype(np.float64))
+    np.testing.assert_allclose(o["weight"], wsum, rtol=1e-12)
+    np.testing.assert_allclose(o["xyz"] * o["weight"][:, None], mass, rtol=1e-9, atol=1e-9)
+    ok = np.floor(o["xyz"] / float(grid)).astype(np.int64)
+    np.testing.assert_array_equal(ok, uk)   # np.unique sorts lexicographically: the same ascending order
