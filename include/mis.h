@@ -212,6 +212,24 @@ mis_status mis_warp(mis_ctx* ctx, mis_mem mem, float* xyz_cam, float* nrm_cam);
 mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out,
                     int64_t stats[4]);
 
+/* NEXT-1: Alg. 3 point filtering with the grid-box downsampling of
+ * P:597 (readings A30-A34).  The model points are binned into the boxes
+ * (floor(x/grid_mm), floor(y/grid_mm), floor(z/grid_mm)) of the world frame (fp32
+ * division); each non-empty box becomes one point: omega-weighted average of
+ * position, colour and normal (renormalised), omega = min(sum omega, omega_max),
+ * stamp = max, id = the member's with the lowest internal index.  The merged
+ * point is deleted iff stamp < frame_index - tau_time and omega < tau_weight
+ * (Alg. 3 line 3); the stability flag S_i is omega >= tau_weight (not
+ * stored).  Survivors are written in ascending (kx, ky, kz) box order and
+ * re-skinned by Eq. 2 against the current nodes (requires m >= k+1); the node
+ * graph is unchanged (Step 5 regeneration is out of scope).  grid_mm > 0,
+ * tau_time >= 0.  n_out (host): new model size; stats (host, nullable):
+ * [boxes, deleted, stable survivors, model size].  One host synchronisation.
+ * MIS_E_ARG (model unchanged) if a box coordinate leaves [-2^20, 2^20) or a
+ * position is not finite. */
+mis_status mis_filter(mis_ctx* ctx, float grid_mm, int32_t frame_index, int32_t tau_time, float tau_weight,
+                      int64_t* n_out, int64_t stats[4]);
+
 /* Read the model (internal order).  Any output may be NULL.  knn_idx/knn_w:
  * n x k in the canonical per-point order (ids ascending). */
 mis_status mis_get_model(mis_ctx* ctx, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight,
@@ -242,11 +260,12 @@ mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* v
 mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
 
 /* ---- instrumentation (bench / profiling) ---- */
-#define MIS_PROF_NCAT 14
+#define MIS_PROF_NCAT 15
 /* Kernel groups: 0 frame_prep (K1), 1 skin (K2), 2 sort_order (K13), 3 pattern,
  * 4 assemble_points (K3), 5 assemble_graph (K4/K5), 6 solve (K6-K8),
  * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),
- * 11 io (uploads, layout conversion), 12 reduce_records (K3 chunk records -> blocks). */
+ * 11 io (uploads, layout conversion), 12 reduce_records (K3 chunk records -> blocks),
+ * 13 accum_points, 14 filter (K14 + the survivors' K2). */
 const char* mis_prof_name(int cat);
 /* on = 1: record a CUDA event pair on the context stream around every kernel
  * group launched by this context; on = 2: only around the K3 and solver groups

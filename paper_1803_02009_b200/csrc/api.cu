@@ -1208,6 +1208,46 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   return MIS_OK;
 }
 
+mis_status mis_filter(mis_ctx* c, float grid_mm, int32_t frame_index, int32_t tau_time, float tau_weight,
+                      int64_t* n_out, int64_t stats[4]) {
+  if (!c || !n_out || !(grid_mm > 0.f) || tau_time < 0 || !(tau_weight == tau_weight)) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  if (c->m < c->K + 1) return fail(c, MIS_E_ARG, "mis_filter: re-skinning needs m >= k+1");
+  TRY(c, flush_frame(c));
+  cudaSetDevice(c->device);
+  TRY(c, ensure(c, c->finfo, 64));
+  int64_t* info = c->finfo.as<int64_t>();
+  {
+    ProfScope ps(c, P_FILTER, c->n > 0 ? 3 : 0);
+    TRY(c, run_filter(c, grid_mm, frame_index, tau_time, tau_weight, info));
+  }
+  TRY(c, cudaMemcpyAsync(c->hpin, info, 32, cudaMemcpyDeviceToHost, c->st));
+  TRY(c, cudaStreamSynchronize(c->st));
+  int64_t h[4];
+  memcpy(h, c->hpin, 32);
+  if (h[3]) {
+    *n_out = c->n;   // K14b kept nothing and K14c wrote nothing: the model is unchanged
+    return fail(c, MIS_E_ARG, "mis_filter: a box coordinate is out of range or a position is not finite");
+  }
+  const int64_t n0 = c->n;
+  c->n = h[0];
+  if (c->n > 0) {
+    ProfScope ps(c, P_FILTER, 1);
+    run_filter_skin(c, c->n);
+    TRY(c, cudaGetLastError());
+  }
+  c->dirty = true;
+  c->pattern_valid = false;
+  *n_out = c->n;
+  if (stats) {
+    stats[0] = h[1];
+    stats[1] = n0 - h[0];
+    stats[2] = h[2];
+    stats[3] = c->n;
+  }
+  return MIS_OK;
+}
+
 mis_status mis_get_model(mis_ctx* c, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight, int32_t* stamp,
                          int64_t* ids, int32_t* knn_idx, float* knn_w, int64_t* n_host) {
   if (!c) return MIS_E_ARG;
@@ -1278,7 +1318,7 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
 const char* mis_prof_name(int cat) {
   static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assoc_points",
                                              "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
-                                             "lift", "io", "finalize", "accum_points"};
+                                             "lift", "io", "finalize", "accum_points", "filter"};
   return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
 }
 

@@ -104,6 +104,7 @@ struct Ctx {
   DBuf rep;   // report block (one memset / one readback per registration), layout below
 
   DBuf cub_tmp;
+  DBuf finfo;   // mis_filter: int64 [survivors, cells, stable, bad key]
 
   // ---- instrumentation
   bool prof = false, prof_light = false;   // light: only the K3 and solver groups
@@ -115,7 +116,7 @@ struct Ctx {
 };
 
 enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO,
-       P_REDUCE, P_ACCUM };
+       P_REDUCE, P_ACCUM, P_FILTER };
 void count_launches(int64_t k);
 
 // report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual
@@ -153,6 +154,9 @@ AccView acc_view(Ctx* c);
 cudaError_t build_order(Ctx* c);      // K13: tuple sort, gather, segments, chunks
 cudaError_t flush_frame(Ctx* c);      // a deferred frame prep (api.cu)
 cudaError_t build_pattern(Ctx* c);    // BSR pattern + slot tables (incl. features)
+// filter.cu (NEXT-1)
+cudaError_t run_filter(Ctx* c, float grid, int32_t frame, int32_t tau_time, float tau_weight, int64_t* info);
+void run_filter_skin(Ctx* c, int64_t ns);
 cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
 cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
 cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count);

@@ -75,6 +75,7 @@ _sig = {
     "mis_get_graph": ([_V, C.c_int, _V], C.c_int),
     "mis_warp": ([_V, C.c_int, _V, _V], C.c_int),
     "mis_fuse": ([_V, C.c_int, _V, C.c_int32, _P(C.c_int64), _V], C.c_int),
+    "mis_filter": ([_V, C.c_float, C.c_int32, C.c_int32, C.c_float, _P(C.c_int64), _V], C.c_int),
     "mis_get_model": ([_V, C.c_int, _V, _V, _V, _V, _V, _V, _V, _V, _P(C.c_int64)], C.c_int),
     "mis_skin": ([_V, C.c_int, C.c_int64, _V, _V, _V], C.c_int),
     "mis_dbg_set_nodes": ([_V, C.c_int, _V], C.c_int),
@@ -88,7 +89,7 @@ _sig = {
     "mis_launch_count": ([], C.c_int64),
     "mis_dbg_solver_phases": ([_V, _V], C.c_int),
 }
-MIS_PROF_NCAT = 14
+MIS_PROF_NCAT = 15
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -243,6 +244,14 @@ def mis_fuse(ctx, rgb=None, frame_index=0):
     n_out = C.c_int64()
     stats = np.zeros(4, np.int64)
     _check(ctx, _lib.mis_fuse(ctx, _mem_of(rgb), _ptr(rgb, np.float32), frame_index, C.byref(n_out), _ptr(stats)))
+    return int(n_out.value), stats
+
+
+def mis_filter(ctx, grid_mm, frame_index, tau_time=10, tau_weight=3.0):
+    """NEXT-1, Alg. 3 filtering.  Returns (n, [boxes, deleted, stable, n])."""
+    n_out = C.c_int64()
+    stats = np.zeros(4, np.int64)
+    _check(ctx, _lib.mis_filter(ctx, grid_mm, frame_index, tau_time, tau_weight, C.byref(n_out), _ptr(stats)))
     return int(n_out.value), stats
 
 
