@@ -289,6 +289,43 @@ def run_mis(args, rank, world, local_rank):
                   "E_first": float(rl["energy"][0, 4]), "E_final_trial": float(rl["energy"][cfg.gn_iters, 4])}
         ctx_lm.close()
 
+    # ---------------- NEXT-1: Alg. 3 filtering (mis_filter, K14) of the fused model, single GPU only.
+    # Each timed filter runs on the model a full step just produced (the step itself untimed); the
+    # box is the model's point spacing (the paper's "point cloud density"), L2 flushed.
+    filt_out = None
+    if world == 1 and not args.no_filter:
+        xy_ext = sc["xyz"].max(0) - sc["xyz"].min(0)
+        box = float(np.sqrt(xy_ext[0] * xy_ext[1] / n))
+        f_frame, f_tau_time, f_tau_weight = 1, 10, 3.0
+        fms, fstats, n_in = [], None, 0
+        for k in range(args.warmup + K):
+            n_in = step()[0]
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fstats = M.mis_filter(ctx.ptr, box, f_frame, f_tau_time, f_tau_weight)[1]
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                fms.append(e0.elapsed_time(e1))
+        f_ms = float(np.mean(fms))
+        ns_f = int(fstats[3])
+        # algorithmic bytes: every model record read once (xyz, normal, colour 36 B, omega, stamp 8 B,
+        # id 8 B) and every survivor written once with its Eq. 2 skinning (8k B)
+        f_algo = n_in * 52 + ns_f * (52 + 8 * cfg.k)
+        hbm_f, _, kind_f = peaks()
+        f_ach = f_algo / (f_ms * 1e-3) / 1e9
+        filt_out = {"ms_per_call": round(f_ms, 4), "points_in": int(n_in),
+                    "box_mm": round(box, 4), "frame": f_frame, "tau_time": f_tau_time, "tau_weight": f_tau_weight,
+                    "stats": [int(x) for x in fstats], "points_per_s": round(n_in / (f_ms * 1e-3), 1),
+                    "roofline": {"bound": "hbm", "achieved": round(f_ach, 2), "peak": hbm_f, "unit": "GB/s",
+                                 "frac": round(f_ach / hbm_f, 4), "peak_source": kind_f,
+                                 "algorithmic_bytes_per_call": int(f_algo),
+                                 "timing": "CUDA events around the whole mis_filter call (K14, CUB sort / scan, "
+                                           "the survivor-count readback, K2)"},
+                    "what": "Alg. 3 (P:244-262): box merge, omega cap, deletion test, compaction, Eq. 2 re-skinning; "
+                            "ms_per_call includes the one host readback of the survivor count"}
+
     # ---------------- roofline of the dominant kernel (timed region: events around K3a, K3b, solver)
     hbm, _, peak_kind = peaks()
     groups = {k: v for k, v in prof.items() if v[1] > 0 and v[0] > 0}
@@ -365,6 +402,7 @@ def run_mis(args, rank, world, local_rank):
         "ms_per_step_with_kernel_events": round(kev["dev_ms_max"] / K, 4),
         "pcg_phases_us_last_launch": pcg_phases,
         "lm": lm_out,
+        "filter": filt_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
@@ -458,6 +496,7 @@ def main():
     ap.add_argument("--impl", default="mis", choices=["mis", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-lm", action="store_true", help="skip the Levenberg-Marquardt (MIS_F_LM) timing")
+    ap.add_argument("--no-filter", action="store_true", help="skip the Alg. 3 filtering (mis_filter) timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one model over the ranks (else replicas)")
     args = ap.parse_args()

@@ -220,13 +220,15 @@ mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_i
  * stamp = max, id = the member's with the lowest internal index.  The merged
  * point is deleted iff stamp < frame_index - tau_time and omega < tau_weight
  * (Alg. 3 line 3); the stability flag S_i is omega >= tau_weight (not
- * stored).  Survivors are written in ascending (kx, ky, kz) box order and
- * re-skinned by Eq. 2 against the current nodes (requires m >= k+1); the node
+ * stored).  Survivors are written in ascending (kx, ky, kz) box order; merged
+ * boxes are re-skinned by Eq. 2 against the current nodes (requires m >= k+1),
+ * single-member boxes keep their point's position and skinning; the node
  * graph is unchanged (Step 5 regeneration is out of scope).  grid_mm > 0,
  * tau_time >= 0.  n_out (host): new model size; stats (host, nullable):
- * [boxes, deleted, stable survivors, model size].  One host synchronisation.
- * MIS_E_ARG (model unchanged) if a box coordinate leaves [-2^20, 2^20) or a
- * position is not finite. */
+ * [boxes, deleted, stable survivors, model size].  Two host synchronisations
+ * (the box range, the survivor count).  MIS_E_ARG (model unchanged) if a
+ * position is not finite, a box coordinate leaves (-2^30, 2^30) or the boxes'
+ * range needs more than 63 key bits. */
 mis_status mis_filter(mis_ctx* ctx, float grid_mm, int32_t frame_index, int32_t tau_time, float tau_weight,
                       int64_t* n_out, int64_t stats[4]);
 

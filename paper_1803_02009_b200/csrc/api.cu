@@ -1216,25 +1216,36 @@ mis_status mis_filter(mis_ctx* c, float grid_mm, int32_t frame_index, int32_t ta
   TRY(c, flush_frame(c));
   cudaSetDevice(c->device);
   TRY(c, ensure(c, c->finfo, 64));
-  int64_t* info = c->finfo.as<int64_t>();
-  {
-    ProfScope ps(c, P_FILTER, c->n > 0 ? 3 : 0);
-    TRY(c, run_filter(c, grid_mm, frame_index, tau_time, tau_weight, info));
+  const int64_t n0 = c->n;
+  if (n0 == 0) {
+    *n_out = 0;
+    if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+    return MIS_OK;
   }
-  TRY(c, cudaMemcpyAsync(c->hpin, info, 32, cudaMemcpyDeviceToHost, c->st));
+  // K14a + readback: validate the box coordinates before the model is touched, size the sort key
+  int32_t range[7];
+  {
+    ProfScope ps(c, P_FILTER, 1);
+    TRY(c, run_filter_range(c, grid_mm, range));
+  }
+  int sh_x = 0, sh_y = 0;
+  const int bits = range[6] ? -1 : filter_key_bits(range, &sh_x, &sh_y);
+  if (bits < 0) {
+    *n_out = n0;
+    return fail(c, MIS_E_ARG, "mis_filter: a position is not finite or the boxes span more than 63 key bits");
+  }
+  {
+    ProfScope ps(c, P_FILTER, 3);
+    TRY(c, run_filter(c, grid_mm, range, sh_x, sh_y, bits, frame_index, tau_time, tau_weight));
+  }
+  TRY(c, cudaMemcpyAsync(c->hpin, c->finfo.p, 32, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
   int64_t h[4];
   memcpy(h, c->hpin, 32);
-  if (h[3]) {
-    *n_out = c->n;   // K14b kept nothing and K14c wrote nothing: the model is unchanged
-    return fail(c, MIS_E_ARG, "mis_filter: a box coordinate is out of range or a position is not finite");
-  }
-  const int64_t n0 = c->n;
   c->n = h[0];
-  if (c->n > 0) {
-    ProfScope ps(c, P_FILTER, 1);
-    run_filter_skin(c, c->n);
-    TRY(c, cudaGetLastError());
+  {
+    ProfScope ps(c, P_FILTER, h[3] > 0 ? 2 : 0);
+    TRY(c, run_filter_skin(c, h[3]));
   }
   c->dirty = true;
   c->pattern_valid = false;

@@ -104,7 +104,8 @@ struct Ctx {
   DBuf rep;   // report block (one memset / one readback per registration), layout below
 
   DBuf cub_tmp;
-  DBuf finfo;   // mis_filter: int64 [survivors, cells, stable, bad key]
+  DBuf finfo;   // mis_filter: int64 [survivors, boxes, stable, boxes to re-skin] + int32 range [7]
+  DBuf fl_xyz, fl_idx, fl_kidx, fl_kw;   // mis_filter: re-skinning list (positions, model index, K2 output)
 
   // ---- instrumentation
   bool prof = false, prof_light = false;   // light: only the K3 and solver groups
@@ -155,8 +156,11 @@ cudaError_t build_order(Ctx* c);      // K13: tuple sort, gather, segments, chun
 cudaError_t flush_frame(Ctx* c);      // a deferred frame prep (api.cu)
 cudaError_t build_pattern(Ctx* c);    // BSR pattern + slot tables (incl. features)
 // filter.cu (NEXT-1)
-cudaError_t run_filter(Ctx* c, float grid, int32_t frame, int32_t tau_time, float tau_weight, int64_t* info);
-void run_filter_skin(Ctx* c, int64_t ns);
+cudaError_t run_filter_range(Ctx* c, float grid, int32_t* range_host);
+int filter_key_bits(const int32_t* range, int* sh_x, int* sh_y);
+cudaError_t run_filter(Ctx* c, float grid, const int32_t* range, int sh_x, int sh_y, int bits, int32_t frame,
+                       int32_t tau_time, float tau_weight);
+cudaError_t run_filter_skin(Ctx* c, int64_t nl);
 cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
 cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
 cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count);

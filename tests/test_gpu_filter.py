@@ -112,3 +112,30 @@ def test_fuse_filter_register_chain():
     assert fresh_boxes <= kept_boxes
     rep2 = M.mis_register(ctx.ptr)
     assert rep2.status == 0 and np.isfinite(rep2.energy[0][4])
+
+
+def test_filter_fullsize_c3():
+    """BASELINE's C3 workload in bench.py's launch configuration: model after a full step (register, warp,
+    fuse of the 640x480 frame), box = the point spacing, frame 1; every output compared with the oracle."""
+    import torch
+    from paper_1803_02009_b200 import synth
+
+    sc = synth.make_scene("c3", 1)
+    cfg = sc["cfg"]
+    n = sc["xyz"].shape[0]
+    prm = M.mis_default_params(k=cfg.k, n_nbr=cfg.n_nbr, gn_iters=cfg.gn_iters, pcg_iters=cfg.pcg_iters)
+    ctx = M.Context(prm, stream=torch.cuda.current_stream().cuda_stream)
+    M.mis_set_model(ctx.ptr, sc["xyz"], sc["nrm"], sc["rgb"], sc["weight"], sc["stamp"], capacity=n + cfg.H * cfg.W + 16)
+    M.mis_set_graph(ctx.ptr, sc["g"], sc["nbr"])
+    it = sc["intr"]
+    M.mis_register(ctx.ptr, sc["depth"], M.intrinsics(it["fx"], it["fy"], it["cx"], it["cy"], it["W"], it["H"]),
+                   sc["pose"], sc["feat_src"], sc["feat_dst"])
+    M.mis_warp(ctx.ptr)
+    n1, _ = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 1)
+    before = M.mis_get_model(ctx.ptr, cfg.k)
+    ext = sc["xyz"].max(0) - sc["xyz"].min(0)
+    box = float(np.sqrt(ext[0] * ext[1] / n))
+    n2, stats = M.mis_filter(ctx.ptr, box, 1, 10, 3.0)
+    o = _oracle_on(before, box, 1, 10, 3.0, prm.omega_max)
+    assert n2 < n1
+    _compare(M.mis_get_model(ctx.ptr, cfg.k), o, stats, n1)
