@@ -67,10 +67,6 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
 
 /* Flags */
 #define MIS_F_FINAL_ENERGY 1u   /* mis_register also evaluates the energy after the last update */
-#define MIS_F_NO_GRAPH     2u   /* reserved, no effect: the GN loop is not captured in a CUDA
-                                   graph -- its kernels are chained by programmatic dependent
-                                   launch and the host stays ahead of the device there; the
-                                   per-frame shapes (pattern, chunks) change every frame        */
 #define MIS_F_GRID_SOLVER  4u   /* force the grid-wide PCG kernel (else the cluster-resident one
                                    whenever the system fits in one cluster's shared memory)       */
 #define MIS_F_STANDARD_PCG 8u   /* cluster kernel: textbook PCG recurrences (2 barriers/iteration)
@@ -141,6 +137,21 @@ const char* mis_last_error(const mis_ctx* ctx);
 /* 128-byte NCCL unique id (rank 0 only).  MIS_E_NCCL if libnccl cannot be loaded. */
 mis_status mis_nccl_unique_id(void* out128);
 mis_status mis_set_params(mis_ctx* ctx, const mis_params* params);
+
+/* Caller-provided device memory (e.g. torch.empty(bytes, dtype=torch.uint8,
+ * device='cuda')).  mis_workspace_bytes: an upper bound of the device memory the context
+ * allocates for a model capacity n_cap, m nodes and H x W frames, assuming at most
+ * m (2 n_nbr + 1 + 4 k^2) nonzero 6x6 blocks (the node pairs sharing a kNN tuple or a
+ * regulariser edge; surface-like graphs have 14 m at k = 4, 32 m at k = 8) and at most
+ * max(4096, H W / 64) feature pairs.  mis_bind_workspace: from then on every buffer of the
+ * context is carved from [dev_ptr, dev_ptr + bytes) (first fit, 256-byte aligned) instead of
+ * cudaMalloc; must precede mis_set_model (MIS_E_STATE), dev_ptr must be 256-byte aligned device
+ * memory of the context's GPU (MIS_E_ARG).  The caller owns the region and frees it after
+ * mis_destroy.  A request the region cannot hold fails with MIS_E_NOMEM (the call's state is
+ * unchanged up to the failing allocation; mis_last_error names the size).  mis_create's own
+ * ~4 KB (report block, counters) stay cudaMalloc'ed. */
+mis_status mis_workspace_bytes(const mis_ctx* ctx, int64_t n_cap, int32_t m, int32_t H, int32_t W, size_t* bytes);
+mis_status mis_bind_workspace(mis_ctx* ctx, void* dev_ptr, size_t bytes);
 
 /* Model points, Sec. II-A "five domains" + normal.  n >= 0 points,
  * capacity >= n bounds Group-2 growth in mis_fuse.  xyz: world positions v_i;
@@ -223,7 +234,8 @@ mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_i
  * stored).  Survivors are written in ascending (kx, ky, kz) box order; merged
  * boxes are re-skinned by Eq. 2 against the current nodes (requires m >= k+1),
  * single-member boxes keep their point's position and skinning; the node
- * graph is unchanged (Step 5 regeneration is out of scope).  grid_mm > 0,
+ * graph is unchanged (Step 5 regeneration is a separate call).  Single GPU only
+ * (world > 1: MIS_E_ARG, a box may span several ranks' shards).  grid_mm > 0,
  * tau_time >= 0.  n_out (host): new model size; stats (host, nullable):
  * [boxes, deleted, stable survivors, model size].  Two host synchronisations
  * (the box range, the survivor count).  MIS_E_ARG (model unchanged) if a

@@ -2,7 +2,10 @@
 // uploads, orchestration of the kernels of one frame, NCCL plumbing.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
+#include <iterator>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -16,25 +19,67 @@ struct mis_ctx : public mis::Ctx {};
 namespace mis {
 
 // ------------------------------------------------------------ buffers
+static constexpr size_t kWsAlign = 256;
+
+// first-fit allocation from the bound workspace (mis_bind_workspace); nullptr when it is exhausted
+static void* ws_alloc(Ctx* c, size_t bytes) {
+  bytes = (bytes + kWsAlign - 1) & ~(kWsAlign - 1);
+  for (auto it = c->ws_free.begin(); it != c->ws_free.end(); ++it) {
+    if (it->second < bytes) continue;
+    const size_t off = it->first, left = it->second - bytes;
+    c->ws_free.erase(it);
+    if (left) c->ws_free[off + bytes] = left;
+    return c->ws_base + off;
+  }
+  return nullptr;
+}
+static void ws_release(Ctx* c, void* p, size_t bytes) {
+  bytes = (bytes + kWsAlign - 1) & ~(kWsAlign - 1);
+  size_t off = (size_t)(static_cast<char*>(p) - c->ws_base);
+  auto nx = c->ws_free.lower_bound(off);
+  if (nx != c->ws_free.end() && off + bytes == nx->first) {   // merge with the next extent
+    bytes += nx->second;
+    nx = c->ws_free.erase(nx);
+  }
+  if (nx != c->ws_free.begin()) {                              // and with the previous one
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == off) { pv->second += bytes; return; }
+  }
+  c->ws_free[off] = bytes;
+}
+static bool in_ws(const Ctx* c, const void* p) {
+  return c->ws_base && p >= c->ws_base && p < c->ws_base + c->ws_bytes;
+}
+
 cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.p && b.bytes >= bytes) return cudaSuccess;
   if (b.p) {
     cudaError_t e = cudaStreamSynchronize(c->st);   // the old buffer may still be in use
     if (e != cudaSuccess) return e;
-    cudaFree(b.p);
-    b.p = nullptr;
-    b.bytes = 0;
+    free_buf(c, b);
   }
   size_t alloc = bytes + bytes / 4 + 256;
-  cudaError_t e = cudaMalloc(&b.p, alloc);
-  if (e != cudaSuccess) { b.p = nullptr; return e; }
+  if (c->ws_base) {
+    b.p = ws_alloc(c, alloc);
+    if (!b.p) {
+      c->err = "workspace exhausted (" + std::to_string(alloc) + " more bytes needed; see mis_workspace_bytes)";
+      return cudaErrorMemoryAllocation;
+    }
+  } else {
+    cudaError_t e = cudaMalloc(&b.p, alloc);
+    if (e != cudaSuccess) { b.p = nullptr; return e; }
+  }
   b.bytes = alloc;
+  if (!b.reg) { b.reg = true; c->bufs.push_back(&b); }
   return cudaSuccess;
 }
 
-void free_buf(DBuf& b) {
-  if (b.p) cudaFree(b.p);
+void free_buf(Ctx* c, DBuf& b) {
+  if (b.p) {
+    if (in_ws(c, b.p)) ws_release(c, b.p, b.bytes);
+    else cudaFree(b.p);
+  }
   b.p = nullptr;
   b.bytes = 0;
 }
@@ -344,8 +389,8 @@ static mis_status fail(Ctx* c, mis_status s, const std::string& msg) {
   return s;
 }
 static mis_status cuda_fail(Ctx* c, cudaError_t e, const char* where) {
-  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e) + (c->err.empty() ? "" : "");
-  return MIS_E_CUDA;
+  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e) + (c->err.empty() ? "" : " (" + c->err + ")");
+  return e == cudaErrorMemoryAllocation ? MIS_E_NOMEM : MIS_E_CUDA;
 }
 #define TRY(c, call)                                              \
   do {                                                            \
@@ -365,7 +410,9 @@ static mis_status check_params(const mis_params* p) {
   if (!p) return MIS_E_ARG;
   if (p->k < 1 || p->k > MIS_MAX_K || p->n_nbr < 0 || p->gn_iters < 1 || p->gn_iters > MIS_MAX_GN ||
       p->pcg_iters < 0 || !(p->eps_d_mm > 0) || !(p->eps_n_deg > 0) || !(p->tau_z_mm > 0) || !(p->trunc_mm > 0) ||
-      !(p->omega_max >= 1) || !(p->lambda >= 0))
+      !(p->omega_max >= 1) || !(p->lambda >= 0) || !std::isfinite(p->tau_z_mm) || !std::isfinite(p->trunc_mm) ||
+      !std::isfinite(p->eps_d_mm) || !(p->delta_deg > 0) || !(p->delta_deg < 180) || !(p->eps_n_deg < 180) ||
+      !std::isfinite(p->omega_max) || !std::isfinite(p->lambda) || p->n_nbr > 64)
     return MIS_E_ARG;
   return MIS_OK;
 }
@@ -439,21 +486,8 @@ mis_status mis_destroy(mis_ctx* c) {
   if (!c) return MIS_E_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
-  DBuf* all[] = {&c->g, &c->nbr, &c->node32, &c->Rt64, &c->keys, &c->keys2, &c->vals, &c->vals2, &c->flags,
-                 &c->scan, &c->seg_start, &c->seg_nodes, &c->chunks, &c->chunk_off, &c->bitmap, &c->bitmap_all,
-                 &c->row_cnt, &c->row_ptr, &c->col, &c->row_of, &c->diag_pos, &c->upper_of, &c->lower_of,
-                 &c->seg_slot, &c->edge_slot, &c->feat_slot, &c->nnz_dev, &c->part, &c->tstamp, &c->acc, &c->energy,
-                 &c->Hval, &c->rhs, &c->Minv, &c->x, &c->r, &c->z, &c->p, &c->Ap, &c->dots,
-                 &c->depth, &c->nmap, &c->rgb_obs, &c->stage, &c->fsrc, &c->fdst, &c->fidx, &c->fw, &c->pixkey,
-                 &c->pix, &c->why, &c->lift_counts, &c->counter, &c->ids_dev, &c->rep, &c->pstate, &c->nmapd, &c->pcg_pptr, &c->pcg_pc, &c->pcg_push,
-                 &c->pcg_npush, &c->pcg_mask, &c->lift_pos, &c->ulist, &c->cub_tmp, &c->lm, &c->Hval2, &c->rhs2,
-                 &c->Rt_acc};
-  for (DBuf* b : all) free_buf(*b);
-  for (int s = 0; s < 2; ++s) {
-    ModelBufs& B = c->mb[s];
-    DBuf* mbv[] = {&B.px, &B.py, &B.pz, &B.nx, &B.ny, &B.nz, &B.cr, &B.cg, &B.cb, &B.w, &B.stamp, &B.ids, &B.kidx, &B.kw};
-    for (DBuf* b : mbv) free_buf(*b);
-  }
+  for (DBuf* b : c->bufs) free_buf(c, *b);   // every buffer ensure() ever allocated
+  c->bufs.clear();
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(c->nccl_comm);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->rb_ev) cudaEventDestroy(c->rb_ev);
@@ -463,6 +497,71 @@ mis_status mis_destroy(mis_ctx* c) {
   if (c->own_stream) cudaStreamDestroy(c->st);
 
   delete c;
+  return MIS_OK;
+}
+
+// Upper bound of the device memory the context's buffers take for a model capacity n_cap, m nodes
+// and H x W frames (mis.h).  Every buffer ensure() may allocate is listed at its largest size; the
+// pattern-dependent ones assume nnzb <= m (2 n_nbr + 1 + 4 k^2) blocks (measured: 14 m at C3, 32 m
+// at C5) and n_feat <= max(4096, H W / 64) feature pairs.
+static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int64_t W) {
+  const int64_t K = c->K, P = K * (K + 1) / 2, nn = std::max<int32_t>(c->prm.n_nbr, 1), px = H * W;
+  const int64_t nnz = std::min<int64_t>(m * m, m * (2 * nn + 1 + 4 * K * K));
+  const int64_t nf = std::max<int64_t>(4096, px / 64);
+  const int64_t mr = m, cs = 16, mp = nnz / 4 + mr + 1;   // cluster PCG lists (pcg_cluster.cu max_pieces)
+  int64_t slots = 1024;
+  while (slots < 2 * n) slots <<= 1;
+  std::vector<int64_t> b = {
+      // model, two buffer sets: 10 float planes, stamp, ids, skinning (MIS_MAX_K slots)
+      2 * 10 * 4 * n, 2 * 4 * n, 2 * 8 * n, 2 * 4 * n * MIS_MAX_K, 2 * 4 * n * MIS_MAX_K,
+      32, 64, 64, 64,                                                        // ids_dev, nnz_dev, finfo, lm
+      12 * m, 4 * m * nn, 64 * m, 96 * m,                                    // graph, node states
+      std::max(std::max(n * 64 + 64, n * (12 + 16 * K) + 64), m * 48),       // staging
+      slots * 12, 8 * n, 4 * n + 64, 4 * n + 64,                            // K13 grouping
+      4 * n, 4 * n, 8 * n, 8 * n, 4 * (n + 1), 4 * n * K, 16 * n, 8 * n, 4 * n, 4 * (n + 1),   // order
+      (int64_t)cub_tmp_bound(std::max<int64_t>(n, m + 1)) + 256,
+      m * ((m + 63) / 64) * 8 * (c->world > 1 ? 1 + c->world : 1),         // pattern bitmap(s)
+      4 * (m + 1), 4 * (m + 1), 4 * m, 128, 4 * nnz + 4, 4 * nnz + 4, 4 * nnz + 4, 4 * nnz + 4,
+      ((nnz - m) / 2 + 1) * 8, (n * P + 1) * 4, (m * nn + 1) * 4, (nf * P + 1) * 4,
+      cs * (mr + 1) * 4, cs * mp * 4, cs * mr * 64, 128, 4 * m,              // cluster PCG lists
+      nnz * 88 * 4 + (6 * m + 3) * 4 + 48 * m + 24 * m, kEnergyDoubles * 8,  // accumulators
+      144 * nnz, 24 * m, 144 * m, 5 * 24 * m, (2 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
+      144 * nnz, 24 * m, 96 * m,                                            // LM second system, kept nodes
+      (K + 2) * 16 * n,                                                     // K3a -> K3b state
+      4 * px, 16 * px, 32 * px, 12 * px, 8 * px, 4 * px, (2 * ((px + 255) / 256) + 4) * 4,   // frame, fusion
+      4 * n, n,                                                             // pix, why
+      12 * nf + 16, 12 * nf + 16, 4 * nf * K + 16, 4 * nf * K + 16,         // features
+      12 * n, 4 * n, 4 * n * K, 4 * n * K,                                  // filter re-skinning list
+  };
+  size_t total = 0;
+  for (int64_t x : b) {
+    const size_t bytes = (size_t)std::max<int64_t>(x, 16);
+    total += ((bytes + bytes / 4 + 256) + kWsAlign - 1) & ~(kWsAlign - 1);   // ensure()'s growth slack
+  }
+  return total + total / 8 + (1 << 20);   // first-fit fragmentation margin
+}
+
+mis_status mis_workspace_bytes(const mis_ctx* c, int64_t n_cap, int32_t m, int32_t H, int32_t W, size_t* bytes) {
+  if (!c || !bytes || n_cap < 0 || m < 1 || H < 0 || W < 0) return MIS_E_ARG;
+  *bytes = workspace_plan(c, std::max<int64_t>(n_cap, 1), m, H, W);
+  return MIS_OK;
+}
+
+mis_status mis_bind_workspace(mis_ctx* c, void* dev_ptr, size_t bytes) {
+  if (!c) return MIS_E_ARG;
+  if (!dev_ptr || bytes < (1 << 20) || ((uintptr_t)dev_ptr & (kWsAlign - 1)))
+    return fail(c, MIS_E_ARG, "bind_workspace: null, < 1 MiB or not 256-byte aligned");
+  if (c->ws_base) return fail(c, MIS_E_STATE, "bind_workspace: a workspace is already bound");
+  if (c->have_model) return fail(c, MIS_E_STATE, "bind_workspace must precede mis_set_model");
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, dev_ptr) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device) {
+    cudaGetLastError();
+    return fail(c, MIS_E_ARG, "bind_workspace: not device memory of the context's GPU");
+  }
+  c->ws_base = static_cast<char*>(dev_ptr);
+  c->ws_bytes = bytes & ~(kWsAlign - 1);
+  c->ws_free.clear();
+  c->ws_free[0] = c->ws_bytes;
   return MIS_OK;
 }
 
@@ -1073,6 +1172,7 @@ static FuseArgs fuse_args(Ctx* c, const float* rgb, int32_t frame) {
   a.md = model_view(c);
   a.fr = frame_view(c);
   a.tz = fmin((double)c->prm.tau_z_mm, (double)c->prm.trunc_mm);
+  a.key_scale = 4294967295.0 / a.tz;   // dz * key_scale < 2^32 - 1 for dz < tz
   a.cos_delta = cos(c->prm.delta_deg * M_PI / 180.0);
   a.omega_max = c->prm.omega_max;
   a.rgb_obs = rgb;
@@ -1082,6 +1182,7 @@ static FuseArgs fuse_args(Ctx* c, const float* rgb, int32_t frame) {
   a.why = c->why.as<uint8_t>();
   a.rank_tag = c->world > 1 ? ((uint32_t)c->rank << 27) : 0u;
   const int nbk = lift_blocks(c->W, c->H);   // lift counts: [nbk counts | nbk + 1 offsets | u64 n_reg]
+  a.fits = nullptr;
   a.n_reg = c->lift_counts.bytes >= (size_t)(2 * nbk + 4) * 4
                 ? reinterpret_cast<unsigned long long*>(c->lift_counts.as<int32_t>() + 2 * nbk + 2)
                 : nullptr;
@@ -1149,22 +1250,25 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   const bool rgb_staged = rgb && mem == MIS_MEM_HOST;
   if (rgb_staged) TRY(c, cudaStreamWaitEvent(c->st, c->ev_rgb_ready, 0));
   FuseArgs a = fuse_args(c, rgb_dev, frame_index);
-  {
-    ProfScope ps(c, P_FAPPLY, c->n > 0 ? 1 : 0);
-    launch_fuse_apply(a, c->st);
-  }
   const int nbk = lift_blocks(c->W, c->H);
   int32_t* counts = c->lift_counts.as<int32_t>();
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(counts + 2 * nbk + 2);   // zeroed by K10
   if (c->n == 0) TRY(c, cudaMemsetAsync(cnt, 0, 8, c->st));   // (K10 not launched)
-  // lift: count + offsets, one host readback (the API returns the new model size), then
-  // the writes and K2 of the new points run behind the return (overlapping the caller)
+  // lift count + offsets first: the scan decides on the device whether the lift fits the
+  // capacity, and K11 (Eq. 12-15) and the lift write apply nothing when it does not, so
+  // MIS_E_CAPACITY leaves the model unchanged.  One host readback (the API returns the new model
+  // size); the writes and K2 of the new points run behind it (overlapping the host's wait)
   const int64_t base = c->n;
   const int do_lift = (c->world == 1 || c->rank == 0) ? 1 : 0;   // sharded model: rank 0 owns the lifted points
   long long* ids_dev = c->ids_dev.as<long long>();
   {
     ProfScope ps(c, P_LIFT, 2);
     launch_lift_count(a, counts, nbk, ids_dev, cnt, do_lift, base, c->cap, c->st);
+  }
+  a.fits = ids_dev + 3;
+  {
+    ProfScope ps(c, P_FAPPLY, c->n > 0 ? 1 : 0);
+    launch_fuse_apply(a, c->st);
   }
   // one readback of [lifted total, registered pixels (u64)] (pinned, asynchronous).  Lifting
   // ranks queue the lifted points' writes (+ pixel-key reset) and their K2 behind it, so they
@@ -1187,14 +1291,13 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   const int32_t n_lift = hb[0];
   unsigned long long n_reg = 0;
   memcpy(&n_reg, hb + 1, 8);
+  if (rgb_staged) TRY(c, cudaEventRecord(c->ev_rgb_free, c->st));   // K11 / K12 have read the staged colours
+  c->pixkey_clean = true;
   if (c->n + n_lift > c->cap) {
-    c->pixkey_clean = true;
     *n_out = c->n;
-    return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity");
+    return fail(c, MIS_E_CAPACITY, "mis_fuse: lifted points exceed the model capacity (model unchanged)");
   }
   if (n_lift > 0) c->dirty = true;
-  c->pixkey_clean = true;
-  if (rgb_staged) TRY(c, cudaEventRecord(c->ev_rgb_free, c->st));   // K11 / K12 have read the staged colours
   TRY(c, cudaGetLastError());
   c->n += n_lift;
   *n_out = c->n;
@@ -1213,6 +1316,8 @@ mis_status mis_filter(mis_ctx* c, float grid_mm, int32_t frame_index, int32_t ta
   if (!c || !n_out || !(grid_mm > 0.f) || tau_time < 0 || !(tau_weight == tau_weight)) return MIS_E_ARG;
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
   if (c->m < c->K + 1) return fail(c, MIS_E_ARG, "mis_filter: re-skinning needs m >= k+1");
+  if (c->world > 1)   // a box may hold points of several ranks' shards: not merged across ranks (yet)
+    return fail(c, MIS_E_ARG, "mis_filter: single-GPU only (world > 1 would filter per-rank partial boxes)");
   TRY(c, flush_frame(c));
   cudaSetDevice(c->device);
   TRY(c, ensure(c, c->finfo, 64));

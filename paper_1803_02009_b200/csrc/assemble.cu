@@ -1249,28 +1249,34 @@ void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_
 // One thread per (edge, block row), (feature, node pair, block row) and
 // (feature, node): ~50k independent items at C3 instead of 4.5k serial
 // atomic chains (the regulariser and feature blocks are few: latency-bound).
-__device__ __forceinline__ void feature_warp(const AsmGraphArgs& a, int fi, float (*am)[3], float* wn, float* e,
+__device__ __forceinline__ void feature_warp(const AsmGraphArgs& a, int fi, float (*am)[3], float* wn, double* e,
                                              float* rp, bool* ok) {
+  // the residual in fp64 from the fp64 master node state (the feature term is O(n_f k): free), so
+  // E_corr carries no fp32 cancellation of ~50 mm positions; the Jacobian rows are fp32
   const int K = a.K;
-  const float V[3] = {a.fsrc[3 * fi], a.fsrc[3 * fi + 1], a.fsrc[3 * fi + 2]};
-  float W = 0.f;
+  const double V[3] = {a.fsrc[3 * fi], a.fsrc[3 * fi + 1], a.fsrc[3 * fi + 2]};
+  double W = 0.0;
   for (int s = 0; s < K; ++s) W += a.fw[(int64_t)s * a.nf + fi];
-  *ok = W > 0.f;
+  *ok = W > 0.0;
   if (!*ok) return;
-  float xh[3] = {0, 0, 0};
+  double xh[3] = {0, 0, 0};
   for (int s = 0; s < K; ++s) {
-    const float* Nd = a.nd.node32 + 16 * a.fidx[(int64_t)s * a.nf + fi];
-    wn[s] = a.fw[(int64_t)s * a.nf + fi] / W;
-    const float d[3] = {V[0] - Nd[12], V[1] - Nd[13], V[2] - Nd[14]};
+    const int j = a.fidx[(int64_t)s * a.nf + fi];
+    const double* Rt = a.nd.Rt64 + 12 * j;
+    const float* g = a.nd.g + 3 * j;
+    const double w = a.fw[(int64_t)s * a.nf + fi] / W;
+    wn[s] = (float)w;
+    const double d[3] = {V[0] - g[0], V[1] - g[1], V[2] - g[2]};
     for (int r = 0; r < 3; ++r) {
-      am[s][r] = Nd[3 * r] * d[0] + Nd[3 * r + 1] * d[1] + Nd[3 * r + 2] * d[2];
-      xh[r] += wn[s] * (am[s][r] + Nd[12 + r] + Nd[9 + r]);
+      const double ar = Rt[3 * r] * d[0] + Rt[3 * r + 1] * d[1] + Rt[3 * r + 2] * d[2];
+      am[s][r] = (float)ar;
+      xh[r] += w * (ar + g[r] + Rt[9 + r]);
     }
   }
-  const float* R = a.fr.R;
+  const double* R = a.fr.Rd;
   for (int r = 0; r < 3; ++r)
-    e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.T[r] - a.fdst[3 * fi + r];
-  for (int r = 0; r < 3; ++r) rp[r] = R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2];
+    e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.Td[r] - a.fdst[3 * fi + r];
+  for (int r = 0; r < 3; ++r) rp[r] = (float)(R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2]);
 }
 
 // row r of [ (a.b) I - b a^T , [a]x ; -[b]x , I ]
@@ -1306,7 +1312,7 @@ __device__ __forceinline__ int64_t graph_items(const AsmGraphArgs& a) {
 __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
   const int K = a.K, P = K * (K + 1) / 2;
   const int64_t n_edge = (int64_t)a.nd.m * a.n_nbr * 6, n_fp = (int64_t)a.nf * P * 6, n_fr = (int64_t)a.nf * K;
-  float eR = 0.f, eC = 0.f;
+  double eR = 0.0, eC = 0.0;
   if (tid < n_edge) {
     // Eq. 6, alpha = 1, directed edge j -> l (reading A14):
     // J_j = [-[b]x, I], J_l = [0, -I], b = R_j (g_l - g_j)
@@ -1314,13 +1320,19 @@ __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
     const int r = (int)(tid % 6);
     const int j = (int)(ei / a.n_nbr), l = a.nbr[ei];
     if (l >= 0) {
-      const float* Nj = a.nd.node32 + 16 * j;
-      const float* Nl = a.nd.node32 + 16 * l;
-      const float d[3] = {Nl[12] - Nj[12], Nl[13] - Nj[13], Nl[14] - Nj[14]};
+      // residual in fp64 from the master state: e = R_j d - d + t_j - t_l with d = g_l - g_j exact,
+      // so a rigid-consistent field gives E_reg = 0 like the oracle (no fp32 cancellation of g)
+      const double* Rj = a.nd.Rt64 + 12 * j;
+      const double* Rl = a.nd.Rt64 + 12 * l;
+      const float* gj = a.nd.g + 3 * j;
+      const float* gl = a.nd.g + 3 * l;
+      const double d[3] = {(double)gl[0] - gj[0], (double)gl[1] - gj[1], (double)gl[2] - gj[2]};
+      double bd[3], ed[3];
+      for (int q = 0; q < 3; ++q) bd[q] = Rj[3 * q] * d[0] + Rj[3 * q + 1] * d[1] + Rj[3 * q + 2] * d[2];
+      for (int q = 0; q < 3; ++q) ed[q] = (bd[q] - d[q]) + (Rj[9 + q] - Rl[9 + q]);
+      if (r == 0) eR = ed[0] * ed[0] + ed[1] * ed[1] + ed[2] * ed[2];
       float b[3], e[3], row[6];
-      for (int q = 0; q < 3; ++q) b[q] = Nj[3 * q] * d[0] + Nj[3 * q + 1] * d[1] + Nj[3 * q + 2] * d[2];
-      for (int q = 0; q < 3; ++q) e[q] = b[q] + Nj[12 + q] + Nj[9 + q] - Nl[12 + q] - Nl[9 + q];
-      if (r == 0) eR = e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
+      for (int q = 0; q < 3; ++q) { b[q] = (float)bd[q]; e[q] = (float)ed[q]; }
       pt_row(b, b, r, row);                                           // J_j^T J_j
       add_row(a.acc.graph + 36 * (int64_t)a.diag_slot[j], r, row, a.w_reg);
       if (r >= 3) atomicAdd(a.acc.graph + 36 * (int64_t)a.diag_slot[l] + 7 * r, a.w_reg);   // J_l^T J_l
@@ -1347,7 +1359,8 @@ __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
     const bool is_rhs = tid >= n_edge + n_fp;
     const int64_t t2 = is_rhs ? tid - n_edge - n_fp : tid - n_edge;
     const int fi = is_rhs ? (int)(t2 / K) : (int)(t2 / (6 * P));
-    float am[MIS_MAX_K][3], wn[MIS_MAX_K], e[3], rp[3];
+    float am[MIS_MAX_K][3], wn[MIS_MAX_K], rp[3];
+    double e[3];
     bool ok;
     feature_warp(a, fi, am, wn, e, rp, &ok);
     if (ok) {
@@ -1378,8 +1391,8 @@ __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
     eC += __shfl_xor_sync(0xffffffffu, eC, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    energy_add(a.acc.energy, 2, (double)eR);
-    energy_add(a.acc.energy, 3, (double)eC);
+    energy_add(a.acc.energy, 2, eR);
+    energy_add(a.acc.energy, 3, eC);
   }
 }
 

@@ -241,6 +241,7 @@ struct FuseArgs {
   ModelView md;
   FrameView fr;
   double tz, cos_delta, omega_max;
+  double key_scale;           // (2^32 - 1) / tz: |dz| < tz quantised to the key's 32 high bits
   const float* rgb_obs;       // H*W*3 or null
   int32_t frame_index;
   unsigned long long* pixkey; // H*W
@@ -248,6 +249,7 @@ struct FuseArgs {
   uint8_t* why;               // n (nullable)
   uint32_t rank_tag;          // rank << 27 in the key's index bits (0 on one GPU): keys unique across ranks
   unsigned long long* n_reg;  // registered-pixel counter (zeroed by K10, filled by the lift count)
+  const long long* fits;      // nullable: 0 when the frame's lift would exceed the capacity (K11 skips)
 };
 void launch_fuse_register(const FuseArgs& a, cudaStream_t s);
 void launch_fuse_apply(const FuseArgs& a, cudaStream_t s);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -14,6 +15,7 @@ namespace mis {
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool reg = false;   // in Ctx::bufs (freed by mis_destroy)
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
@@ -33,6 +35,14 @@ struct Ctx {
   int rank = 0, world = 1;
   void* nccl_comm = nullptr;
   std::string err;
+
+  // ---- memory: every device buffer of the context is registered here on its first allocation
+  // (mis_destroy frees exactly this list); with a bound workspace (mis_bind_workspace) buffers are
+  // carved first-fit from the caller's region instead of cudaMalloc
+  std::vector<DBuf*> bufs;
+  char* ws_base = nullptr;
+  size_t ws_bytes = 0;
+  std::map<size_t, size_t> ws_free;   // offset -> bytes of the free extents (coalesced)
 
   // ---- model (internal, tuple-sorted order); two buffer sets for the sort gather
   int64_t n = 0, cap = 0, next_id = 0;
@@ -142,7 +152,8 @@ struct ProfScope {
 
 // buffer management (api.cu)
 cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes);
-void free_buf(DBuf& b);
+void free_buf(Ctx* c, DBuf& b);
+size_t cub_tmp_bound(int64_t n);   // sort.cu: CUB temporary storage of the largest sort / scan over n items
 
 // views
 ModelView model_view(Ctx* c);

@@ -118,16 +118,16 @@ __global__ void __launch_bounds__(256) k_cell_decide(MergeArgs r) {
     head = (i == 0) || (r.keys[i - 1] != r.keys[i]);
     if (head) {
       const int64_t e = box_end(r, i, n);
-      float wsum = 0.f;
+      double wsum = 0.0;   // fp64 like the oracle: the deletion test must not flip on rounding
       int32_t t = INT_MIN;
       for (int64_t j = i; j < e; ++j) {
         const uint32_t p = r.vals[j];
-        wsum += r.a.w[p];
+        wsum += (double)r.a.w[p];
         t = max(t, r.a.stamp[p]);
       }
-      const float om = fminf(wsum, r.omega_max);                                  // Eq. 15 cap
-      kept = !(((int64_t)t < (int64_t)r.frame - (int64_t)r.tau_time) && (om < r.tau_weight));
-      stable = kept && om >= r.tau_weight;                                        // S_i (A32)
+      const double om = fmin(wsum, (double)r.omega_max);                          // Eq. 15 cap
+      kept = !(((int64_t)t < (int64_t)r.frame - (int64_t)r.tau_time) && (om < (double)r.tau_weight));
+      stable = kept && om >= (double)r.tau_weight;                                // S_i (A32)
     }
     r.keep[i] = kept ? 1 : 0;
   }
@@ -159,9 +159,9 @@ __global__ void __launch_bounds__(256) k_cell_merge(MergeArgs r) {
       const ModelView& b = r.b;
       const uint32_t p0 = r.vals[i];
       o = r.pos[i];
-      float wsum = 0.f;
-      for (int64_t j = i; j < e; ++j) wsum += a.w[r.vals[j]];
-      const bool weighted = wsum > 0.f;
+      double wsum = 0.0;
+      for (int64_t j = i; j < e; ++j) wsum += (double)a.w[r.vals[j]];
+      const bool weighted = wsum > 0.0;
       float nx = 0.f, ny = 0.f, nz = 0.f, cr = 0.f, cg = 0.f, cb = 0.f, den = 0.f;
       int32_t t = INT_MIN;
       for (int64_t j = i; j < e; ++j) {
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256) k_cell_merge(MergeArgs r) {
       } else {
         b.nx[o] = a.nx[p0]; b.ny[o] = a.ny[p0]; b.nz[o] = a.nz[p0];
       }
-      b.w[o] = fminf(wsum, r.omega_max);
+      b.w[o] = (float)fmin(wsum, (double)r.omega_max);
       b.stamp[o] = t;
       b.ids[o] = a.ids[p0];
     }

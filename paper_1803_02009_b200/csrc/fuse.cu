@@ -96,7 +96,8 @@ __device__ __forceinline__ bool normal_map64(const FrameView& f, int px, int py,
 
 
 // K10: Alg. 1 gates + exclusive registration by 64-bit atomicMin
-// of ((|dz| in 1e-8 mm units) << 32 | point index) per pixel (reading A19).
+// of ((|dz| / tz quantised to 32 bits) << 32 | point index) per pixel (reading A19).  The
+// quantum is tz / 2^32 (2.3e-9 mm at tz = 10 mm) for every gate width, no overflow since |dz| < tz.
 __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
               why |= 32;
               pix = py * f.W + px;
               const unsigned long long key =
-                  ((unsigned long long)(dz * 1e8) << 32) | (unsigned long long)(a.rank_tag | (uint32_t)i);
+                  ((unsigned long long)(dz * a.key_scale) << 32) | (unsigned long long)(a.rank_tag | (uint32_t)i);
               atomicMin(a.pixkey + pix, key);
             }
           }
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
   pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.md.n) return;
+  if (a.fits && !*a.fits) return;   // the lift would exceed the capacity: the model stays unchanged
   const int32_t pix = a.pix[i];
   if (pix < 0) return;
   if ((uint32_t)(a.pixkey[pix] & 0xffffffffull) != (a.rank_tag | (uint32_t)i)) return;
@@ -249,9 +251,11 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const int32_t* counts, int
     wtot[lane] = ti - t;   // exclusive warp offsets
     if (lane == 31) {
       offs[nb] = ti;
+      const bool fits = (int64_t)ti <= cap - base;
       ids_dev[1] = ids_dev[0];   // ids of the lifted points: ids_dev[1] + rank
-      ids_dev[0] += ti;
+      if (fits) ids_dev[0] += ti;   // an exceeded capacity consumes no ids (MIS_E_CAPACITY: unchanged)
       ids_dev[2] = ti < cap - base ? ti : cap - base;
+      ids_dev[3] = fits ? 1 : 0;  // read by K11 and the lift write: nothing is applied unless it fits
     }
   }
   __syncthreads();
@@ -276,9 +280,8 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   __syncthreads();
   int before = 0;
   for (int i = 0; i < w; ++i) before += wsum[i];
-  if (!on) return;
+  if (!on || !ids_dev[3]) return;   // over capacity: nothing written, reported by mis_fuse (MIS_E_CAPACITY)
   const int64_t o = base + offs[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
-  if (o >= cap) return;   // over capacity: reported by mis_fuse (MIS_E_CAPACITY)
   lift_pos[p] = (int32_t)o;
   const FrameView& f = a.fr;
   const int px = p % f.W, py = p / f.W;

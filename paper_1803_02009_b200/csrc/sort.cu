@@ -347,6 +347,15 @@ static cudaError_t cub_call(Ctx* c, F f) {
   return f(c->cub_tmp.p, have);
 }
 
+size_t cub_tmp_bound(int64_t n) {
+  size_t a = 0, b = 0, d = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)n, 0, 64);
+  cub::DeviceScan::InclusiveSum(nullptr, b, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  cub::DeviceScan::ExclusiveSum(nullptr, d, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return std::max(a, std::max(b, d));
+}
+
 cudaError_t build_order(Ctx* c) {
   const int64_t n = c->n;
   const int K = c->K;

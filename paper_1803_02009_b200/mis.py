@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("MIS_LIB_PATH", os.path.join(_HERE, "libmis.so"))   # 
 
 MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
-MIS_F_FINAL_ENERGY, MIS_F_NO_GRAPH, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 2, 4, 8
+MIS_F_FINAL_ENERGY, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 4, 8
 MIS_F_LM = 16   # Levenberg-Marquardt (include/mis.h)
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
@@ -65,6 +65,8 @@ _sig = {
     "mis_last_error": ([_V], C.c_char_p),
     "mis_nccl_unique_id": ([_V], C.c_int),
     "mis_set_params": ([_V, _P(mis_params)], C.c_int),
+    "mis_workspace_bytes": ([_V, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P(C.c_size_t)], C.c_int),
+    "mis_bind_workspace": ([_V, _V, C.c_size_t], C.c_int),
     "mis_set_model": ([_V, C.c_int64, C.c_int, _V, _V, _V, _V, _V, _V, C.c_int64], C.c_int),
     "mis_set_graph": ([_V, C.c_int32, C.c_int, _V, _V, _V, _V], C.c_int),
     "mis_set_frame": ([_V, C.c_int, _V, _P(mis_intrinsics), _V], C.c_int),
@@ -167,6 +169,17 @@ def mis_destroy(ctx):
 
 def mis_set_params(ctx, params):
     _check(ctx, _lib.mis_set_params(ctx, C.byref(params)))
+
+
+def mis_workspace_bytes(ctx, n_cap, m, H, W) -> int:
+    b = C.c_size_t()
+    _check(ctx, _lib.mis_workspace_bytes(ctx, int(n_cap), int(m), int(H), int(W), C.byref(b)))
+    return int(b.value)
+
+
+def mis_bind_workspace(ctx, buf):
+    """buf: a contiguous CUDA tensor (e.g. torch.empty(bytes, dtype=torch.uint8, device='cuda'))."""
+    _check(ctx, _lib.mis_bind_workspace(ctx, _ptr(buf), int(buf.numel() * buf.element_size())))
 
 
 def mis_set_model(ctx, xyz, nrm, rgb=None, weight=None, stamp=None, ids=None, capacity=None):

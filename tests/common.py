@@ -57,3 +57,66 @@ def apply_perturbation(Rt, j, comp, h):
 def state_f32(Rt):
     """The fp32 node state both sides receive in stage-wise parity (exact upcast)."""
     return np.asarray(Rt, np.float32).astype(np.float64)
+
+
+def check_fusion(M, ctx, k, o, fr, owner, why, ids, frame_index, n_out, stats, tie=1e-6):
+    """Alg. 1 + Eq. 12-15 + Alg. 2 Step 3 parity, exact outside ties.
+
+    owner / why: mis_dbg_fuse_register (GPU internal indices / order) taken before the
+    fusion; ids: the caller ids of the internal order then; o: oracle O.fuse on the same
+    model.  Excluded ("unsure") pixels: equal keys within `tie` (oracle key_margin) or an
+    owner -- on either side -- whose fp64 gate quantity lies within `tie` of a threshold
+    (oracle gate_margin).  Everything else is compared exactly: the owner map both ways,
+    why bits, weights and stamps; positions within 0.05 mm, normals 1e-4, colours 1e-5;
+    lifted points pixel by pixel (the row-major lift order of both sides)."""
+    n = ids.shape[0]
+    gown = np.where(owner >= 0, ids[np.maximum(owner, 0)], -1)
+    oown = o["owner"]
+    unsure_pt = o["gate_margin"] <= tie
+
+    def unsure_owner(own):
+        return (own >= 0) & unsure_pt[np.maximum(own, 0)]
+
+    excl = (o["key_margin"] <= tie) | unsure_owner(gown) | unsure_owner(oown)
+    assert excl.mean() < 1e-3, excl.mean()
+    bad = np.flatnonzero((gown != oown) & ~excl)
+    assert bad.size == 0, (bad[:10], gown[bad[:10]], oown[bad[:10]])
+    sure = ~unsure_pt[ids]
+    wbad = np.flatnonzero(sure & (why != o["why"][ids]))
+    assert wbad.size == 0, (wbad[:10], why[wbad[:10]], o["why"][ids][wbad[:10]])
+    assert stats[0] == int((gown >= 0).sum())
+    # the model after the fusion, matched by caller id
+    mod = M.mis_get_model(ctx.ptr, k)
+    gid = mod["ids"]
+    aff = np.unique(np.concatenate([gown[excl], oown[excl]]))
+    old = gid < n
+    ok = old & ~np.isin(gid, aff)
+    go = gid[ok]
+    assert (mod["weight"][ok] == o["weight"][go]).all()
+    assert (mod["stamp"][ok] == o["stamp"][go]).all()
+    assert np.abs(mod["xyz"][ok] - o["xyz"][go]).max() < 0.05
+    assert np.abs(mod["nrm"][ok] - o["nrm"][go]).max() < 1e-4
+    assert np.abs(mod["rgb"][ok] - o["rgb"][go]).max() < 1e-5
+    fused = ok & (mod["stamp"] == frame_index) & np.isin(gid, gown[gown >= 0])
+    assert fused.sum() > 0
+    # lifted points: GPU id n + r <-> the r-th lifted pixel of the GPU owner map (row-major)
+    _, _, dv, nv = O.frame_prep(fr)
+    valid = (dv & nv).ravel().astype(bool)
+    g_lift = np.flatnonzero(valid & (gown < 0))
+    o_lift = np.flatnonzero(valid & (oown < 0))
+    assert np.isin(np.setxor1d(g_lift, o_lift), np.flatnonzero(excl)).all()
+    assert n_out == n + g_lift.size and stats[1] == g_lift.size
+    new = ~old
+    r_g = gid[new] - n
+    pix_g = g_lift[r_g]
+    both = np.isin(pix_g, o_lift)
+    r_o = np.searchsorted(o_lift, pix_g[both])
+    sel = np.flatnonzero(new)[both]
+    assert np.abs(mod["xyz"][sel] - o["xyz"][n + r_o]).max() < 1e-3
+    assert np.abs(mod["nrm"][sel] - o["nrm"][n + r_o]).max() < 1e-5
+    assert (mod["rgb"][sel] == o["rgb"][n + r_o]).all()
+    assert (mod["weight"][new] == 1).all() and (mod["stamp"][new] == frame_index).all()
+    lm = o["lift_margin"][r_o] > 1e-5
+    oi = np.sort(o["lift_idx"][r_o], axis=1)
+    assert (mod["knn_idx"][sel][lm] == oi[lm]).all()
+    return mod

@@ -81,7 +81,7 @@ def test_filter_keeps_fresh_and_deletes_all_stale():
 
 
 def test_filter_bad_box_leaves_model_unchanged():
-    """Box coordinates outside [-2^20, 2^20): MIS_E_ARG and the model is untouched."""
+    """Box coordinates outside (-2^30, 2^30): MIS_E_ARG and the model is untouched."""
     sc, pb, fr, _ = scene_problem("c1")
     ctx = make_ctx(sc, pb)
     before = M.mis_get_model(ctx.ptr, pb.k)

@@ -20,7 +20,7 @@ import pytest
 
 import oracle as O
 from paper_1803_02009_b200 import synth
-from tests.common import scene_problem, state_f32
+from tests.common import check_fusion, scene_problem, state_f32
 from tests.test_gpu_parity import make_ctx, node_state, oracle_params, order_of, rot_err
 
 pytestmark = pytest.mark.gpu
@@ -72,9 +72,9 @@ def check_system_sparse(gs, osys, m, tol=1e-4):
     E = osys["energy"][4]
     bt = np.abs(gs["rhs"] - osys["rhs"]) / np.sqrt(dg.ravel() ** 2 * 2 * E)
     assert bt.max() < tol, bt.max()
-    p_ = osys["prm"]
-    w = np.array([p_.w_data, p_.w_pt, p_.w_reg, p_.w_corr])
-    assert (np.abs(gs["energy"][:4] - osys["energy"][:4]) * w <= tol * E + 1e-12).all(), (gs["energy"], osys["energy"])
+    # every energy term on its own, relative 1e-4 (test_gpu_parity.check_system)
+    assert (np.abs(gs["energy"][:4] - osys["energy"][:4]) <= tol * np.abs(osys["energy"][:4]) + 1e-9).all(), \
+        (gs["energy"], osys["energy"])
 
 
 # ------------------------------------------------------------------ c3: the bench workload, whole problem
@@ -152,17 +152,8 @@ def test_c3_warp_and_fuse_full():
     ids = order_of(ctx, pb.k)
     o = O.fuse(oracle_params(ctx.params), pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], fr,
                sc["rgb_obs"], 9, pb.g)
-    gown = np.where(owner >= 0, ids[np.maximum(owner, 0)], -1)
-    tie = o["key_margin"] <= 1e-6
-    bad = np.flatnonzero((gown != o["owner"]) & ~tie)
-    own_bad = o["owner"][bad]
-    assert bad.size == 0 or (o["gate_margin"][own_bad[own_bad >= 0]] <= 1e-6).all(), bad[:10]
-    assert (why == o["why"][ids]).mean() > 0.999
     n_out, stats = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 9)
-    assert n_out == n + o["n_lift"]
-    mod = M.mis_get_model(ctx.ptr, pb.k)
-    gid = mod["ids"]
-    assert np.abs(mod["xyz"] - o["xyz"][gid]).max() < 0.05  # 5e-5 m
+    check_fusion(M, ctx, pb.k, o, fr, owner, why, ids, 9, n_out, stats)
     # warp with a random field on a fresh context
     ctx = make_ctx(sc, pb)
     Rt = state_f32(node_state("random", pb.g, seed=41))

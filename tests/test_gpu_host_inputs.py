@@ -1,8 +1,10 @@
 """Host-memory frame inputs go through the context's copy stream (depth before the frame prep,
 colours before the fusion's update kernel; DESIGN.md §5 host synchronisation): two consecutive
-frames with pinned host inputs must give the same registration, fused model and lifted points
-as the same frames with device inputs (within fp32 atomic-order rounding), including the reuse
-of the staging buffers by the second frame."""
+frames with pinned host inputs must give the same registration (within fp32 atomic-order
+rounding) and, bit for bit, the same fused model and lifted points as the same frames with
+device inputs, including the reuse of the staging buffers by the second frame.  (The node state is
+reset to the identity after each registration, so the warp and the fusion -- fp64 decisions, no
+float atomics -- are deterministic and the two runs must agree exactly.)"""
 import numpy as np
 import pytest
 
@@ -33,6 +35,9 @@ def _run(sc, pb, host):
         rep = M.report_dict(M.mis_register(ctx.ptr, depth, intr, sc["pose"], fs, fd))
         assert rep["status"] == 0
         energies.append(rep["energy"][:, 4])
+        ident = np.zeros((pb.g.shape[0], 12), np.float32)
+        ident[:, [0, 4, 8]] = 1.0                       # R_j = I, t_j = 0
+        M.mis_dbg_set_nodes(ctx.ptr, ident)
         M.mis_warp(ctx.ptr)
         n_out, stats = M.mis_fuse(ctx.ptr, rgb, frame)
         sizes.append((n_out, stats.copy()))
@@ -48,14 +53,5 @@ def test_host_inputs_match_device_inputs():
     for a, b in zip(eh, ed):
         assert np.allclose(a, b, rtol=1e-3)
     for (na, sa), (nb, sb) in zip(sh, sd):
-        assert abs(na - nb) <= max(5, 1e-4 * nb)
-        assert np.abs(sa - sb).max() <= max(5, 1e-4 * nb)
-    # the caller's points (ids < n0): lifted points get ids in pixel order, so one pixel registered
-    # in one run and lifted in the other (atomic-order rounding deciding a |dz| tie) shifts every
-    # later id; two fusions in a row can also move an occasional winner, so the gate is on 99.9 %
-    n = pb.xyz.shape[0]
-    dx = np.abs(xh[:n] - xd[:n]).max(axis=1)
-    assert np.quantile(dx, 0.999) < 0.05, np.quantile(dx, 0.999)   # mm, the warped / fused gate
-    assert dx.max() < 1.0, dx.max()
-    dc = np.abs(ch[:n] - cd[:n]).max(axis=1)
-    assert np.quantile(dc, 0.999) < 1e-3
+        assert na == nb and (sa == sb).all()
+    assert (xh == xd).all() and (ch == cd).all()

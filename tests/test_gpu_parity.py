@@ -11,7 +11,7 @@ import pytest
 
 import oracle as O
 from paper_1803_02009_b200 import synth
-from tests.common import pose12, random_state, rot, scene_problem, state_f32
+from tests.common import check_fusion, pose12, random_state, rot, scene_problem, state_f32
 
 pytestmark = pytest.mark.gpu
 
@@ -135,9 +135,10 @@ def check_system(gs, osys, m, tol=1e-4):
     E = osys["energy"][4]
     bt = np.abs(gs["rhs"] - osys["rhs"]) / np.sqrt(np.diag(Ho) * 2 * E)
     assert bt.max() < tol, bt.max()
-    p_ = osys["prm"]
-    w = np.array([p_.w_data, p_.w_pt, p_.w_reg, p_.w_corr])
-    assert (np.abs(gs["energy"][:4] - osys["energy"][:4]) * w <= tol * E + 1e-12).all(), (gs["energy"], osys["energy"])
+    # every term on its own (E_data, E_pt, E_reg, E_corr), relative 1e-4; the 1e-9 mm^2 floor only
+    # matters for a term that is exactly zero on the oracle side (e.g. E_reg of a rigid-consistent field)
+    assert (np.abs(gs["energy"][:4] - osys["energy"][:4]) <= tol * np.abs(osys["energy"][:4]) + 1e-9).all(), \
+        (gs["energy"], osys["energy"])
     # structure: every oracle block present in the GPU pattern, symmetric
     assert np.abs(Hg - Hg.T).max() <= 1e-6 * np.abs(Hg).max()
 
@@ -217,8 +218,18 @@ def test_warp_parity(cfg):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
-def test_fuse_parity(cfg):
+@pytest.mark.parametrize("posed", [False, True])
+def test_fuse_parity(cfg, posed):
+    """Fusion registration, Eq. 12-15 and the lift, exact outside ties (common.check_fusion).
+    posed: a random world->camera pose and random model weights (Eq. 12-14 with omega != 1,
+    back-transform R^T(. - T) under a non-identity pose)."""
     sc, pb, fr, _ = scene_problem(cfg)
+    if posed:
+        rng = np.random.default_rng(17)
+        sc = dict(sc)
+        sc["pose"] = pose12(rot(rng.normal(size=3), 2.0), rng.normal(0, 0.8, 3))
+        sc["weight"] = rng.integers(1, 10, pb.xyz.shape[0]).astype(np.float32)
+        fr = O.Frame(sc["depth"], sc["intr"], sc["pose"])
     ctx = make_ctx(sc, pb)
     n = pb.xyz.shape[0]
     cfgo = sc["cfg"]
@@ -226,36 +237,24 @@ def test_fuse_parity(cfg):
     ids = order_of(ctx, pb.k)
     prm = oracle_params(ctx.params)
     o = O.fuse(prm, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], fr, sc["rgb_obs"], 7, pb.g)
-    # owner: GPU internal index -> caller id
-    gown = np.where(owner >= 0, ids[np.maximum(owner, 0)], -1)
-    gate_ok = np.ones(n, bool)
-    gate_ok[ids] = True
-    tie = o["key_margin"] <= 1e-6
-    # pixels whose candidate points all have clear gate decisions
-    assert ((gown == o["owner"]) | tie).mean() > 0.999
-    bad = np.flatnonzero((gown != o["owner"]) & ~tie)
-    near = o["gate_margin"][o["owner"][bad][o["owner"][bad] >= 0]] if bad.size else np.zeros(0)
-    assert bad.size == 0 or (near <= 1e-6).all(), bad[:10]
-    assert (why == o["why"][ids]).mean() > 0.999
-    # apply
     n_out, stats = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 7)
-    assert n_out == n + o["n_lift"]
-    assert stats[1] == o["n_lift"]
-    mod = M.mis_get_model(ctx.ptr, pb.k)
-    gid = mod["ids"]
-    old = gid < n
-    assert np.abs(mod["xyz"][old] - o["xyz"][gid[old]]).max() < 0.05
-    assert (mod["weight"][old] == o["weight"][gid[old]]).mean() > 0.999
-    assert (mod["stamp"][old] == o["stamp"][gid[old]]).mean() > 0.999
-    assert np.abs(mod["rgb"][old] - o["rgb"][gid[old]]).max() < 1e-3
-    # lifted points: ids n.. in row-major pixel order
-    new = ~old
-    assert np.abs(mod["xyz"][new] - o["xyz"][gid[new]]).max() < 0.05
-    assert (mod["weight"][new] == 1).all() and (mod["stamp"][new] == 7).all()
-    li = gid[new] - n
-    lm = o["lift_margin"][li] > 1e-5
-    oi = np.sort(o["lift_idx"][li], axis=1)
-    assert (mod["knn_idx"][new][lm] == oi[lm]).all()
+    check_fusion(M, ctx, pb.k, o, fr, owner, why, ids, 7, n_out, stats)
+
+
+@pytest.mark.parametrize("gate_mm", [45.0, 120.0])
+def test_fuse_parity_wide_gates(gate_mm):
+    """tau_z = trunc beyond 42.9 mm (where a 1e-8 mm fixed-point key would overflow 32 bits):
+    the key is |dz| / tz quantised to 32 bits, so the per-pixel winner stays exact."""
+    sc, pb, fr, _ = scene_problem("c1")
+    ctx = make_ctx(sc, pb, tau_z_mm=gate_mm, trunc_mm=gate_mm)
+    n = pb.xyz.shape[0]
+    cfgo = sc["cfg"]
+    owner, why = M.mis_dbg_fuse_register(ctx.ptr, cfgo.H, cfgo.W, n)
+    ids = order_of(ctx, pb.k)
+    o = O.fuse(oracle_params(ctx.params), pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], fr, sc["rgb_obs"], 3,
+               pb.g)
+    n_out, stats = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 3)
+    check_fusion(M, ctx, pb.k, o, fr, owner, why, ids, 3, n_out, stats)
 
 
 def test_device_memory_roundtrip():
@@ -336,3 +335,135 @@ def test_device_graph_validation_deferred():
     M.mis_set_graph(ctx.ptr, t(pb.g), t(pb.nbr))        # a valid graph binds again
     r = M.report_dict(M.mis_register(ctx.ptr, t(sc["depth"]), intr, sc["pose"]))
     assert r["status"] == 0
+
+
+# ------------------------------------------------------------------ C5-shaped registration at C2 size
+@pytest.mark.parametrize("solver", ["grid", "cluster"])
+def test_register_parity_c5_shape(solver):
+    """C5's method shape (k = 8, n_nbr = 8, G = 8, P = 20; BASELINE configs[4]) on the C2 scene,
+    against the oracle's MIRROR registration (same G and P): the grid-wide PCG is C5's solver."""
+    sc = synth.make_scene("c2", 1)
+    k = 8
+    nbr = synth.node_graph(sc["g"], 8)
+    idx, w, _ = O.skin(sc["xyz"], sc["g"], k)
+    _, _, fm = O.skin(sc["feat_src"], sc["g"], k)
+    keep = fm > 1e-4
+    pb = O.Problem(sc["xyz"], sc["nrm"], idx, w.astype(np.float32), sc["g"], nbr, sc["feat_src"][keep],
+                   sc["feat_dst"][keep])
+    fr = O.Frame(sc["depth"], sc["intr"], sc["pose"])
+    flags = M.MIS_F_FINAL_ENERGY | (M.MIS_F_GRID_SOLVER if solver == "grid" else 0)
+    ctx = make_ctx(sc, pb, gn_iters=8, pcg_iters=20, flags=flags)
+    rep = M.report_dict(M.mis_register(ctx.ptr))
+    assert rep["status"] == 0
+    assert (rep["solver_cluster"] > 0) == (solver == "cluster")
+    m = pb.g.shape[0]
+    Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+    Ro, Eo, nao = O.register(oracle_params(ctx.params), pb, fr)
+    terr = np.linalg.norm(Rg[:, 9:] - Ro[:, 9:], axis=1)
+    rerr = np.array([rot_err(Rg[j, :9].reshape(3, 3), Ro[j, :9].reshape(3, 3)) for j in range(m)])
+    assert terr.max() < 0.01, terr.max()
+    assert rerr.max() < 1e-4, rerr.max()
+    assert np.allclose(rep["energy"][:, 4], Eo[:, 4], rtol=1e-3)
+    assert np.abs(rep["n_assoc"] - nao).max() <= max(3, 1e-4 * pb.xyz.shape[0])
+
+
+# ------------------------------------------------------------------ error paths (mis.h)
+@pytest.mark.parametrize("solver", ["cluster", "grid"])
+def test_numeric_failure_rolls_back(solver):
+    """MIS_E_NUMERIC: a non-finite GN step (here: a NaN feature observation makes b non-finite)
+    rolls the node state back to before the failing iteration -- the identity, since it is the
+    first -- and the context stays usable: the next registration matches the oracle."""
+    sc, pb, fr, _ = scene_problem("c1")
+    flags = M.MIS_F_GRID_SOLVER if solver == "grid" else 0
+    ctx = make_ctx(sc, pb, flags=flags)
+    bad = pb.fdst.copy()
+    bad[0, 1] = np.nan
+    with pytest.raises(M.MisError) as e:
+        M.mis_register(ctx.ptr, None, None, None, pb.fsrc, bad)
+    assert e.value.status == 7
+    m = pb.g.shape[0]
+    assert (M.mis_get_nodes_f64(ctx.ptr, m) == O.identity_state(m)).all()
+    rep = M.report_dict(M.mis_register(ctx.ptr, None, None, None, pb.fsrc, pb.fdst))
+    assert rep["status"] == 0
+    Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+    Ro, _, _ = O.register(oracle_params(ctx.params), pb, fr)
+    assert np.abs(Rg[:, 9:] - Ro[:, 9:]).max() < 0.01 and np.abs(Rg[:, :9] - Ro[:, :9]).max() < 1e-4
+
+
+def test_capacity_exceeded_leaves_model_unchanged():
+    """MIS_E_CAPACITY: the frame's lift would exceed the capacity -> neither the Eq. 12-15 update
+    of the registered points nor any lifted point is applied, the size and ids are unchanged, and
+    a later fusion with room proceeds normally (no id consumed)."""
+    sc, pb, fr, _ = scene_problem("c1")
+    c = sc["cfg"]
+    prm = M.mis_default_params(k=pb.k, n_nbr=pb.n_nbr)
+    ctx = M.Context(prm)
+    n = pb.xyz.shape[0]
+    M.mis_set_model(ctx.ptr, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], None, capacity=n + 10)
+    M.mis_set_graph(ctx.ptr, pb.g, pb.nbr, pb.idx, np.ascontiguousarray(pb.w, np.float32))
+    it = sc["intr"]
+    M.mis_set_frame(ctx.ptr, sc["depth"], M.intrinsics(it["fx"], it["fy"], it["cx"], it["cy"], it["W"], it["H"]),
+                    sc["pose"])
+    before = M.mis_get_model(ctx.ptr, pb.k)
+    with pytest.raises(M.MisError) as e:
+        M.mis_fuse(ctx.ptr, sc["rgb_obs"], 5)
+    assert e.value.status == 6
+    after = M.mis_get_model(ctx.ptr, pb.k)
+    for key in before:
+        np.testing.assert_array_equal(after[key], before[key])
+    # same model into a context with room: the lifted ids start at n (nothing was consumed)
+    M.mis_set_model(ctx.ptr, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], None, capacity=n + c.H * c.W)
+    M.mis_set_graph(ctx.ptr, pb.g, pb.nbr, pb.idx, np.ascontiguousarray(pb.w, np.float32))
+    n_out, st = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 5)
+    ids = M.mis_get_model(ctx.ptr, pb.k)["ids"]
+    assert n_out == n + st[1] and np.array_equal(np.sort(ids), np.arange(n_out))
+
+
+def test_workspace_binding():
+    """§8(b) mis_workspace_bytes / mis_bind_workspace: a torch allocation backs every buffer of a
+    full frame (register, warp, fuse, filter) -- no device memory is taken outside it -- with the
+    same result as a cudaMalloc'ed context; order and size errors are reported."""
+    torch = pytest.importorskip("torch")
+    sc, pb, fr, _ = scene_problem("c2")
+    c = sc["cfg"]
+    n, m = pb.xyz.shape[0], pb.g.shape[0]
+    cap = n + 2 * c.H * c.W
+    it = sc["intr"]
+    intr = M.intrinsics(it["fx"], it["fy"], it["cx"], it["cy"], it["W"], it["H"])
+
+    def frame(ctx):
+        M.mis_set_model(ctx.ptr, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], None, capacity=cap)
+        M.mis_set_graph(ctx.ptr, pb.g, pb.nbr)
+        rep = M.report_dict(M.mis_register(ctx.ptr, sc["depth"], intr, sc["pose"], pb.fsrc, pb.fdst))
+        nodes = M.mis_get_nodes_f64(ctx.ptr, m)
+        M.mis_warp(ctx.ptr)
+        n1, _ = M.mis_fuse(ctx.ptr, sc["rgb_obs"], 1)
+        n2, _ = M.mis_filter(ctx.ptr, 0.5, 1, 10, 3.0)
+        return rep, nodes, n1, n2
+
+    ref = frame(M.Context(M.mis_default_params()))
+    ctx = M.Context(M.mis_default_params())
+    nb = M.mis_workspace_bytes(ctx.ptr, cap, m, c.H, c.W)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    M.mis_bind_workspace(ctx.ptr, ws)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    got = frame(ctx)
+    torch.cuda.synchronize()
+    assert free0 - torch.cuda.mem_get_info()[0] < 4 << 20      # nothing (beyond driver noise) outside the workspace
+    assert got[0]["status"] == 0 and np.abs(got[1] - ref[1]).max() < 1e-3   # fp32 atomic order only
+    assert abs(got[2] - ref[2]) <= 10 and abs(got[3] - ref[3]) <= 10
+    with pytest.raises(M.MisError) as e:
+        M.mis_bind_workspace(ctx.ptr, ws)                      # already bound
+    assert e.value.status == 2
+    small = M.Context(M.mis_default_params())
+    tiny = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    M.mis_bind_workspace(small.ptr, tiny)
+    with pytest.raises(M.MisError) as e:
+        M.mis_set_model(small.ptr, pb.xyz, pb.nrm, capacity=cap)
+    assert e.value.status == 5                                 # MIS_E_NOMEM, names the size
+    late = M.Context(M.mis_default_params())
+    M.mis_set_model(late.ptr, pb.xyz, pb.nrm, capacity=cap)
+    with pytest.raises(M.MisError) as e:
+        M.mis_bind_workspace(late.ptr, ws)
+    assert e.value.status == 2

@@ -815,3 +815,130 @@ def test_filter_conserves_weighted_mass_and_stays_in_cell():
     np.testing.assert_allclose(o["xyz"] * o["weight"][:, None], mass, rtol=1e-9, atol=1e-9)
     ok = np.floor(o["xyz"] / float(grid)).astype(np.int64)
     np.testing.assert_array_equal(ok, uk)   # np.unique sorts lexicographically: the same ascending order
+
+
+# ------------------------------------------------------------------ Eq. 12-14 and the world back-transform
+def test_eq14_unequal_normals_and_back_transform_under_pose():
+    """Eq. 12-14 with omega = 3 and unequal normals under a non-identity pose, against geometry
+    written in the camera-to-world parametrisation (rotation Rc, centre C; world->camera is then
+    R = Rc^T, T = -Rc^T C): a rigid map preserves affine combinations, so the fused world point is
+    (omega v + q_w) / (omega + 1) with q_w = C + Rc q; by the law of sines in the parallelogram of
+    omega n~ and N the fused normal makes tan(phi) = omega sin(theta) / (1 + omega cos(theta)) with
+    N, in their plane, on n~'s side; Eq. 13 colours; lifted pixels (Alg. 2 Step 3) land at
+    C + Rc q with normal Rc N.  An R / R^T slip, an unweighted or unnormalised blend or a dropped
+    T fails one of these."""
+    W, H, f, D = 64, 48, 40.0, 50.0
+    it = dict(fx=f, fy=f, cx=W / 2.0, cy=H / 2.0, W=W, H=H)
+    depth = np.full((H, W), D, np.float32)            # fronto-parallel in the camera frame: N = (0, 0, -1)
+    Rc = rot([1.0, 2.0, -0.5], 25.0)
+    C = np.array([3.0, -2.0, 5.0])
+    fr = O.Frame(depth, it, pose12(Rc.T, -Rc.T @ C))
+    px, py = 40, 30
+    q_cam = np.array([(px - it["cx"]) * D / f, (py - it["cy"]) * D / f, D])
+    v_cam = q_cam * (47.0 / D)                        # same pixel ray, |dz| = 3 mm < tau_z
+    theta = np.deg2rad(8.0)                           # < delta = 10 deg
+    n_cam = np.array([0.0, np.sin(theta), -np.cos(theta)])
+    omega = 3.0
+    xyz = (C + Rc @ v_cam)[None].astype(np.float32)
+    nrm = (Rc @ n_cam)[None].astype(np.float32)
+    rgb = np.array([[0.2, 0.4, 0.8]], np.float32)
+    obs = np.zeros((H, W, 3), np.float32)
+    obs[py, px] = [0.6, 0.0, 0.4]
+    obs[1, 1] = [0.25, 0.5, 0.75]
+    prm = O.params(k=1, n_nbr=1)
+    out = O.fuse(prm, xyz, nrm, rgb, np.array([omega], np.float32), np.zeros(1, np.int32), fr, obs, 6,
+                 np.array([[0, 0, 50.0], [99, 0, 50.0]], np.float32))
+    assert out["owner"][py * W + px] == 0
+    v_w = xyz[0].astype(np.float64)
+    q_w = C + Rc @ q_cam
+    assert np.abs(out["xyz"][0] - (omega * v_w + q_w) / (omega + 1)).max() < 1e-9
+    phi = np.arctan2(omega * np.sin(theta), 1 + omega * np.cos(theta))
+    assert 0 < phi < theta and abs(phi - theta * omega / (omega + 1)) > 2e-5   # not the angle-weighted mean (slerp)
+    n_exp = Rc @ np.array([0.0, np.sin(phi), -np.cos(phi)])
+    assert np.abs(out["nrm"][0] - n_exp).max() < 1e-6   # fp32 storage of the input normal
+    assert abs(np.linalg.norm(out["nrm"][0]) - 1) < 1e-12
+    assert np.allclose(out["rgb"][0], [0.3, 0.3, 0.7], atol=1e-7)
+    assert out["weight"][0] == 4.0 and out["stamp"][0] == 6
+    # lifted: every valid pixel except the registered one, row-major; the first is (1, 1)
+    assert out["n_lift"] == (W - 2) * (H - 2) - 1
+    q11 = np.array([(1 - it["cx"]) * D / f, (1 - it["cy"]) * D / f, D])
+    assert np.abs(out["xyz"][1] - (C + Rc @ q11)).max() < 1e-9
+    assert np.abs(out["nrm"][1] - Rc @ np.array([0, 0, -1.0])).max() < 1e-12
+    assert np.allclose(out["rgb"][1], [0.25, 0.5, 0.75]) and out["weight"][1] == 1.0 and out["stamp"][1] == 6
+    # the registered pixel is not lifted: no lifted point lies on its ray
+    lw = out["xyz"][1:]
+    lc = (lw - C) @ Rc                                 # back to the camera frame via Rc^T (x - C)
+    u = f * lc[:, 0] / lc[:, 2] + it["cx"]
+    v = f * lc[:, 1] / lc[:, 2] + it["cy"]
+    assert not np.any((np.abs(u - px) < 1e-6) & (np.abs(v - py) < 1e-6))
+
+
+# ------------------------------------------------------------------ MIRROR PCG at P = 10 (O3h)
+def _textbook_pcg(A, b, Minv, P):
+    """Preconditioned CG from x0 = 0, P iterations (Hestenes-Stiefel, Saad Alg. 9.1), dense numpy."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = Minv @ r
+    p = z.copy()
+    rz = r @ z
+    for _ in range(P):
+        Ap = A @ p
+        alpha = rz / (p @ Ap)
+        x += alpha * p
+        r -= alpha * Ap
+        z = Minv @ r
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x
+
+
+def _block_jacobi(Hd, m, lam):
+    Minv = np.zeros_like(Hd)
+    for j in range(m):
+        B = Hd[6 * j:6 * j + 6, 6 * j:6 * j + 6]
+        mu = 1e-9 * np.trace(B) / 6                      # R-A17
+        Minv[6 * j:6 * j + 6, 6 * j:6 * j + 6] = np.linalg.inv(B + (lam + mu) * np.eye(6))
+    return Minv
+
+
+def test_mirror_pcg_p10_is_textbook_pcg():
+    """O3h MIRROR with the GPU's P = 10 against textbook dense PCG with the block-Jacobi
+    preconditioner of R-A17, on the C2 system (P = 10 is far from convergence there, so a wrong
+    recurrence -- beta, the residual update, the preconditioner -- shows)."""
+    sc, pb, fr, _ = scene_problem("c2")
+    m = pb.g.shape[0]
+    prm = O.params()
+    s = O.system(prm, pb, fr, random_state(m, np.random.default_rng(8), 0.01, 0.3))
+    Hd = O.dense_H(s, m)
+    A = Hd + prm.lambda_ * np.eye(6 * m)
+    Minv = _block_jacobi(Hd, m, prm.lambda_)
+    for P in (2, 10):
+        x_ref = _textbook_pcg(A, s["rhs"], Minv, P)
+        x, it = O.solve(s, m, prm.lambda_, 1, P)
+        assert it == P
+        assert np.abs(x - x_ref).max() < 1e-8 * np.abs(x_ref).max(), P
+    x_exact = np.linalg.solve(A, s["rhs"])
+    assert np.abs(x - x_exact).max() > 1e-4 * np.abs(x_exact).max()   # P = 10 is not converged
+
+
+def test_mirror_register_trajectory_c1():
+    """O3 in MIRROR mode (G = 5, P = 10, the bench's GN shape) against a numpy loop: oracle
+    assembly, textbook PCG, Exp(dtheta) R_j / t_j + dt_j (R-A18) -- same energies, same state."""
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    prm = O.params(gn_iters=5, pcg_iters=10, solve_mode=1)
+    Rt = O.identity_state(m)
+    Es = []
+    for _ in range(prm.gn_iters):
+        s = O.system(prm, pb, fr, Rt)
+        Es.append(s["energy"][4])
+        Hd = O.dense_H(s, m)
+        x = _textbook_pcg(Hd + prm.lambda_ * np.eye(6 * m), s["rhs"], _block_jacobi(Hd, m, prm.lambda_), 10)
+        for j in range(m):
+            Rt[j, :9] = (O.exp_so3(x[6 * j:6 * j + 3]) @ Rt[j, :9].reshape(3, 3)).ravel()
+            Rt[j, 9:] += x[6 * j + 3:6 * j + 6]
+    Es.append(O.system(prm, pb, fr, Rt)["energy"][4])
+    Ro, Eo, _ = O.register(prm, pb, fr)
+    assert np.abs(Ro - Rt).max() < 1e-9
+    assert np.allclose(Eo[:, 4], Es, rtol=1e-10)
