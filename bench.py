@@ -9,14 +9,25 @@ k=4, sparse ORB feature term, 5 GN x 10 PCG): rebuild of the model order
 (mis_set_model + mis_set_graph: K13 tuple sort), frame prep, feature skinning,
 BSR pattern, 5 Gauss-Newton iterations (K3 + K4/K5 + K6-K8), final warp (K9)
 and fusion + lift (K10-K12).  Inputs are resident in HBM when the timed region
-starts (`value`); `e2e` repeats the step through the C-ABI with pinned HOST
-buffers (H2D of the model, graph, depth, features, colour and D2H of the
-report inside the timed region).  Metric: GN registrations per second
-(whole job, all ranks).  With N > 1 each rank runs an independent replica
-(the C3 path does not shard: DESIGN.md §7, "replicas only"), scaling "weak".
+starts (`value`); `e2e` repeats the step through the C-ABI with the frame's
+inputs in pinned HOST memory (H2D of the depth, colour, ORB matches and pose,
+D2H of the registration report and the new model size inside the timed
+region; the model and the node graph stay resident on the device, restored
+from a device snapshot as in the device-timed step).  Metric: GN registrations
+per second (whole job, all ranks).  With N > 1 each rank runs an independent
+replica (the C3 path does not shard: DESIGN.md §7, "replicas only"), scaling
+"weak"; --shard splits one model over the ranks instead.
+
+Roofline (`roofline`, `roofline_k3`): algorithmic work per launch in SURVEY
+§8(d)'s units: PCG nnzb x 168 B + m x 384 B per iteration; K3
+(24 + 8k) B per point + 16 B per associated pixel and 40k + 40 + 15k + 2 (6k)(6k+1)/2
++ 20 k(k+1)/2 + 25k flop per point (1,160 at k = 4, 3,752 at k = 8).  `traffic`
+is the ncu DRAM bytes per launch of the same configuration (profiles/
+r2_traffic_<config>.json, written by scripts/ncu_traffic.py from an
+`ncu --set full` capture of this bench), else null.
 
 --impl reference times the fp64 CPU oracle (oracle/, the reference arm of this
-tier) on the same workload, on rank 0 only.
+tier) on the same workload, on rank 0 only, on all host cores (OpenMP).
 """
 from __future__ import annotations
 
@@ -335,25 +346,35 @@ def run_mis(args, rank, world, local_rank):
     kk = cfg.k
     n_assoc = float(np.mean(rep["n_assoc"][:G]))
     nseg = int(rep["n_segments"])
-    # algorithmic bytes per launch
+    # algorithmic work per launch in SURVEY §8(d)'s units
     cluster = rep["solver_cluster"] > 0
+    k3_bytes = n * (24 + 8 * kk) + n_assoc * 16                  # point x GN iteration + associated pixel
+    k3_flop = n * (40 * kk + 40 + 15 * kk + (6 * kk) * (6 * kk + 1) + 10 * kk * (kk + 1) + 25 * kk)
     algo = {
-        # K3a: point (24 B), skinning (8k B), one normal-map gather (32 B), compact state written (16(k+2) B)
-        "assoc_points": n * (24 + 8 * kk + 32 + 16 * (kk + 2)),
-        # K3b: compact state read once, one vector atomic per 4 accumulated floats per chunk (>= segments)
-        "accum_points": n * 16 * (kk + 2) + nseg * (13 * kk * (kk + 1) // 2 + 6 * kk) * 16,
-        # cluster PCG: H (nnzb 6x6 blocks) and b read once, node state read/written once;
-        # grid PCG: H streamed every iteration
-        "solve": (nnzb * 144 + m * (24 + 96 + 64)) if cluster else (P * (nnzb * 144 + 6 * m * 4 * 11) + m * 160),
-        # accumulators read once, H (both triangles), b and the block inverses written
+        # K3a reads the point, its skinning and the associated normal-map texel; K3b re-reads nothing
+        # of the model (its input is K3a's compact state, an implementation intermediate)
+        "assoc_points": k3_bytes,
+        "accum_points": k3_bytes,
+        # PCG: per iteration every nnz block (144 B) + the gathered p (24 B), and per node the
+        # vectors / preconditioner (240 + 144 B)
+        "solve": P * (nnzb * 168 + m * 384),
+        # accumulators read once (88 floats per upper+lower slot), H, b and the block inverses written
         "finalize": nnzb * 88 * 4 + m * 24 * 4 + nnzb * 144 + m * (24 + 144),
     }
-    # K3b flops: the two upper-triangle SYRKs per associated point
-    flops_pt = 2 * ((6 * kk + 1) * (6 * kk + 2) // 2 + (4 * kk + 3) * (4 * kk + 4) // 2)
+    # K3b's share of the flops: the two per-chunk SYRKs (J^T J point-to-plane + point-to-point
+    # moments); at k <= 4 they run as mma.sync TF32 (3xTF32 split): scored against the TF32 tensor
+    # peak (dense bf16 measured x 1/2, the guide's nominal ratio), else against the FP32 FMA peak
+    syrk_flop = n_assoc * ((6 * kk) * (6 * kk + 1) + 10 * kk * (kk + 1))
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = sm_count * 128 * 2 * 1.965e9 / 1e12   # TFLOP/s at the max SM clock (guide: 148 SMs)
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    traffic_all = json.load(open(tp)) if os.path.exists(tp) else {}
+    _, bf16_peak, _ = peaks()
+    tf32_peak = bf16_peak / 2.0
+    tp = os.path.join(ROOT, "profiles", f"r2_traffic_{args.config}.json")
+    traffic_all = {}
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        if tj.get("config") == args.config:
+            traffic_all = tj.get("bytes_per_launch", {})
 
     def roofline_of(name):
         ms_k, n_k = groups[name]
@@ -361,20 +382,39 @@ def run_mis(args, rank, world, local_rank):
         base = {"kernel": name, "launch_ms": round(t * 1e3, 5), "share_of_step": round(ms_k / max(kev["dev_ms"], 1e-9), 3),
                 "timing": "CUDA events around every launch, second timed pass of the same K steps"}
         if name == "accum_points":
-            ach = n_assoc * flops_pt / t / 1e12
-            base.update({"bound": "alu", "achieved": round(ach, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
-                         "frac": round(ach / fp32_peak, 4), "flops_per_associated_point": flops_pt,
-                         "peak_source": "FP32 FMA: SMs x 128 lanes x 2 x max SM clock"})
+            tc = kk <= 4
+            pk = tf32_peak if tc else fp32_peak
+            ach = syrk_flop / t / 1e12
+            base.update({"bound": "tensor" if tc else "alu", "achieved": round(ach, 3), "peak": round(pk, 1),
+                         "unit": "TFLOP/s", "frac": round(ach / pk, 5), "algorithmic_flops_per_launch": int(syrk_flop),
+                         "peak_source": ("TF32 tensor: measured dense bf16 x 1/2 (mma.sync m16n8k8 TF32, 3xTF32 "
+                                         "split: 3 MMAs per algorithmic product)") if tc else
+                                        "FP32 FMA: SMs x 128 lanes x 2 x max SM clock",
+                         "hbm_view": {"achieved": round(algo[name] / t / 1e9, 2), "peak": hbm,
+                                      "frac": round(algo[name] / t / 1e9 / hbm, 4)}})
         else:
             ach = algo[name] / t / 1e9
             base.update({"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": int(algo[name])})
-        base["traffic"] = traffic_all.get(name)
+            if name == "assoc_points":
+                fl = k3_flop / t / 1e12
+                base["alu_view"] = {"achieved_tflops": round(fl, 3), "peak": round(fp32_peak, 1),
+                                    "frac": round(fl / fp32_peak, 4), "flops_per_launch": int(k3_flop)}
+        tr = traffic_all.get(name)
+        base["traffic"] = tr
+        if tr and name != "accum_points":
+            base["traffic_over_algorithmic"] = round(tr / max(1, algo[name]), 3)
         return base
 
     roof = roofline_of(dom)
     roof_k3 = {k: roofline_of(k) for k in ("assoc_points", "accum_points") if k in groups}
+    if "assoc_points" in groups and "accum_points" in groups:   # K3 as one GN-iteration unit (§8(d))
+        t3 = sum(groups[k][0] / max(1, groups[k][1]) for k in ("assoc_points", "accum_points")) * 1e-3
+        roof_k3["k3_total"] = {
+            "launch_ms": round(t3 * 1e3, 5), "bytes": int(k3_bytes), "flops": int(k3_flop),
+            "hbm_frac": round(k3_bytes / t3 / 1e9 / hbm, 4), "fp32_frac": round(k3_flop / t3 / 1e12 / fp32_peak, 4),
+            "floor_ms": round(max(k3_bytes / (hbm * 1e9), k3_flop / (fp32_peak * 1e12)) * 1e3, 5)}
 
     jobs = 1 if sharded else world   # registrations per step over the whole job
     value = jobs * K / (dev_ms_max / 1e3)
@@ -436,21 +476,38 @@ def oracle_setup(sc):
     return O, pb, fr, prm
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline(args, sc, steps=2):
+    """The oracle as it stands on the box's host cores: all cores (OpenMP over points, pixels and
+    skinning queries), plus the single-thread column (SURVEY §8(d) "Oracle timing")."""
     O, pb, fr, prm = oracle_setup(sc)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        oracle_step(O, sc, prm, pb, fr, sc["rgb_obs"])
-    dt = time.perf_counter() - t0
-    return {"value": round(steps / dt, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+    cores = host_cores()
+    res = {}
+    for T in (cores, 1):
+        O.set_threads(T)
+        t0 = time.perf_counter()
+        for _ in range(steps if T > 1 else 1):
+            oracle_step(O, sc, prm, pb, fr, sc["rgb_obs"])
+        res[T] = (steps if T > 1 else 1) / (time.perf_counter() - t0)
+    O.set_threads(1)
+    return {"value": round(res[cores], 5), "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{steps} full steps of the same {args.config} workload (register {sc['cfg'].gn_iters} GN x "
-                      f"{sc['cfg'].pcg_iters} PCG MIRROR + warp + fuse/lift), fp64 C++ oracle, single thread; "
-                      "initial skinning precomputed (as on the GPU)"}
+                      f"{sc['cfg'].pcg_iters} PCG MIRROR + warp + fuse/lift), fp64 C++ oracle on all {cores} host "
+                      "cores (OpenMP); initial skinning precomputed (as on the GPU)",
+            "single_thread": {"value": round(res[1], 5), "cores": 1, "sample": "1 full step, 1 thread"}}
 
 
 def run_reference(args, budget_s=150.0):
     sc = load_workload(args.config, 0)
     O, pb, fr, prm = oracle_setup(sc)
+    cores = host_cores()
+    O.set_threads(cores)
     # bounded sample: one full frame if (warmup + steps) frames fit the budget, else every step
     # registers a fixed random fraction f of the model points (all graph and feature terms kept)
     # and the rate is scaled by f (the oracle's cost is linear in the point count)
@@ -479,10 +536,11 @@ def run_reference(args, budget_s=150.0):
         "config": {"workload": f"{args.config}: {cfg.W}x{cfg.H} depth, {sc['xyz'].shape[0]} model points, "
                                f"{sc['g'].shape[0]} nodes, k={cfg.k}, {cfg.gn_iters} GN x {cfg.pcg_iters} PCG; "
                                "step = register + warp + fuse"},
-        "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": (f"each step = one frame of the workload with a random {f:.3f} fraction of the "
-                                    "model points (rate scaled by it), fp64 C++ oracle, 1 thread") if f < 1.0 else
-                         "each step = one full frame of the workload on the fp64 C++ oracle, 1 thread"},
+                                    f"model points (rate scaled by it), fp64 C++ oracle, {cores} threads (OpenMP)")
+                         if f < 1.0 else
+                         f"each step = one full frame of the workload on the fp64 C++ oracle, {cores} threads (OpenMP)"},
         "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -57,7 +57,9 @@ typedef enum {
   MIS_E_NCCL = 4,      /* NCCL error or NCCL unavailable with world > 1             */
   MIS_E_NOMEM = 5,     /* device allocation failed                                  */
   MIS_E_CAPACITY = 6,  /* Group-2 growth would exceed the model capacity            */
-  MIS_E_NUMERIC = 7    /* non-finite GN step; the node state is rolled back         */
+  MIS_E_NUMERIC = 7    /* non-finite GN step or PCG scalar (e.g. a NaN input): the node
+                          state is rolled back to before that GN iteration and no later
+                          iteration of the registration updates it                    */
 } mis_status;
 
 typedef enum { MIS_MEM_HOST = 0, MIS_MEM_DEVICE = 1 } mis_mem;

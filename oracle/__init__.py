@@ -27,7 +27,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with g++ (fp64, no -ffast-math)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC",
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-fopenmp",
                                _SRC, "-o", _SO + ".tmp"])
         os.replace(_SO + ".tmp", _SO)
     return _SO
@@ -71,6 +71,7 @@ def lib():
             L.or_skin.argtypes = [C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_exp.argtypes = [C.c_void_p, C.c_void_p]
+            L.or_set_threads.argtypes = [C.c_int32]
             L.or_warp.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_associate.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p,
@@ -115,6 +116,11 @@ def _i32(a):
 PAPER_DEFAULTS = dict(k=4, n_nbr=4, w_data=1.0, w_pt=1.0, w_reg=1e4, w_corr=10.0,
                       eps_d=15.0, eps_n_deg=10.0, tau_z=10.0, delta_deg=10.0, trunc=40.0, omega_max=10.0,
                       gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1, lm=0, lm_mu0=1e-3)
+
+
+def set_threads(n: int) -> None:
+    """Host threads of the oracle (bench.py's all-cores column; default 1)."""
+    lib().or_set_threads(int(n))
 
 
 def params(**kw) -> or_params:

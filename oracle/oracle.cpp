@@ -18,7 +18,15 @@
 #include <vector>
 #include <algorithm>
 
+#include <omp.h>
+
 namespace {
+
+// Host threads of the oracle (or_set_threads; default 1).  Only the loops over independent items
+// (points, pixels, queries) are split; the per-thread partial normal equations are merged in
+// thread order, so a fixed thread count gives a fixed summation order.  Used by bench.py's
+// all-cores timing column; the pins and parity tests run single-threaded.
+int g_threads = 1;
 
 typedef std::array<double, 3> V3;
 typedef std::array<double, 9> M3;     // row-major
@@ -307,13 +315,13 @@ void wraw_of(const or_problem* p, int k, int64_t i, double* wr) {
   for (int s = 0; s < k; ++s) wr[s] = (double)p->w[k * i + s];
 }
 
-void assemble(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
-              const int32_t* fidx, const double* fw, System* S) {
+// O3a-d, O3g for the points [i0, i1): data (Eq. 8) and dense point-to-point terms
+void assemble_points(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt, int64_t i0,
+                     int64_t i1, System* S) {
   const int k = prm->k;
   M3 R = pose_R(f->pose);
   double Jpl[8 * 6], Jpt[8 * 18], rpl, rpt[3];
-  // O3a-d, O3g: data (Eq. 8) and dense point-to-point terms
-  for (int64_t i = 0; i < p->n; ++i) {
+  for (int64_t i = i0; i < i1; ++i) {
     double wr[8];
     wraw_of(p, k, i, wr);
     Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
@@ -337,6 +345,28 @@ void assemble(const or_params* prm, const or_problem* p, const or_frame* f, cons
       }
       S->add_rhs(ja, Jpl + 6 * a, &rpl, 1, prm->w_data);
       S->add_rhs(ja, Jpt + 18 * a, rpt, 3, prm->w_pt);
+    }
+  }
+}
+
+void assemble(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+              const int32_t* fidx, const double* fw, System* S) {
+  const int k = prm->k;
+  if (g_threads <= 1) {
+    assemble_points(prm, p, f, Rt, 0, p->n, S);
+  } else {   // T contiguous point ranges, merged in range order
+    const int T = g_threads;
+    std::vector<System> part(T, System(p->m));
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; ++t) assemble_points(prm, p, f, Rt, p->n * t / T, p->n * (t + 1) / T, &part[t]);
+    for (int t = 0; t < T; ++t) {
+      for (const auto& kv : part[t].blk) {
+        B6& B = S->blk[kv.first];
+        for (int a = 0; a < 36; ++a) B[a] += kv.second[a];
+      }
+      for (int i = 0; i < 6 * p->m; ++i) S->rhs[i] += part[t].rhs[i];
+      for (int a = 0; a < 4; ++a) S->E[a] += part[t].E[a];
+      S->n_assoc += part[t].n_assoc;
     }
   }
   // O3e: regulariser
@@ -525,6 +555,7 @@ void update_nodes(int m, const std::vector<double>& x, double* Rt) {
 void feature_skin(const or_problem* p, int k, std::vector<int32_t>& fidx, std::vector<double>& fw) {
   fidx.assign((size_t)k * p->nf, 0);
   fw.assign((size_t)k * p->nf, 0.0);
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int q = 0; q < p->nf; ++q)
     skin_one(load3(p->fsrc + 3 * q), p->m, p->g, k, &fidx[k * q], &fw[k * q], nullptr);
 }
@@ -546,8 +577,11 @@ void or_frame_prep(const or_frame* f, double* q, double* N, uint8_t* dvalid, uin
     }
 }
 
+void or_set_threads(int32_t n) { g_threads = n < 1 ? 1 : n; }
+
 void or_skin(int64_t nq, const float* p, int32_t m, const float* g, int32_t k,
              int32_t* idx, double* w, double* margin) {
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int64_t i = 0; i < nq; ++i)
     skin_one(load3(p + 3 * i), m, g, k, idx + k * i, w + k * i, margin ? margin + i : nullptr);
 }
@@ -570,6 +604,7 @@ void or_exp(const double w[3], double R[9]) {
 
 void or_warp(const or_problem* p, int32_t k, const double* Rt, const double pose[12],
              double* x_hat, double* n_hat, double* vt, double* nt, uint8_t* ok) {
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int64_t i = 0; i < p->n; ++i) {
     double wr[8];
     wraw_of(p, k, i, wr);
@@ -587,6 +622,7 @@ void or_warp(const or_problem* p, int32_t k, const double* Rt, const double pose
 void or_associate(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
                   int32_t* pix, uint8_t* why, double* margin) {
   const int k = prm->k;
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int64_t i = 0; i < p->n; ++i) {
     double wr[8];
     wraw_of(p, k, i, wr);
@@ -762,6 +798,7 @@ void or_register(const or_params* prm, const or_problem* p, const or_frame* f, d
 void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
                    double* g_out) {
   double pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int64_t i = 0; i < p->n; ++i) {
     double wr[8];
     wraw_of(p, k, i, wr);
@@ -789,6 +826,7 @@ int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, co
   std::vector<int32_t> pix(mdl->n, -1);
   std::vector<double> dz(mdl->n, 0.0);
   // O5 / Alg. 1: v~ = R v + T, gates, exclusive per pixel with key (|dz|, i)
+#pragma omp parallel for num_threads(g_threads) schedule(static)
   for (int64_t i = 0; i < mdl->n; ++i) {
     V3 vt = add(mul(R, load3(mdl->xyz + 3 * i)), T);
     V3 nt = mul(R, load3(mdl->nrm + 3 * i));
@@ -884,9 +922,14 @@ int64_t or_fuse(const or_params* prm, const or_model* mdl, const or_frame* f, co
     }
     weight_out[o] = 1.0;
     stamp_out[o] = frame_index;
-    float pf[3] = {(float)vw[0], (float)vw[1], (float)vw[2]};   // skinning input as the GPU stores it
-    skin_one(load3(pf), m, g, k, lift_idx + k * nl, lift_w + k * nl, lift_margin + nl);
     ++nl;
+  }
+  // Eq. 2 skinning of the lifted points on the current g (each independent)
+#pragma omp parallel for num_threads(g_threads) schedule(static)
+  for (int64_t l = 0; l < nl; ++l) {
+    const int64_t o = mdl->n + l;
+    float pf[3] = {(float)xyz_out[3 * o], (float)xyz_out[3 * o + 1], (float)xyz_out[3 * o + 2]};   // as the GPU stores it
+    skin_one(load3(pf), m, g, k, lift_idx + k * l, lift_w + k * l, lift_margin + l);
   }
   return nl;
 }

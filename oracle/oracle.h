@@ -55,6 +55,10 @@ typedef struct {
  * short-circuited at the first failure. */
 enum { OR_Z = 1, OR_FRAME = 2, OR_DEPTH = 4, OR_NORMAL = 8, OR_DIST = 16, OR_ANGLE = 32, OR_ALL = 63 };
 
+/* Host threads of the oracle (default 1): independent points / pixels / queries are split over
+ * them; per-thread partial normal equations are merged in thread order.  bench.py's all-cores
+ * column only -- the pins and the parity tests run single-threaded. */
+void or_set_threads(int32_t n);
 /* O0: back-projection and central-difference normals of a depth map. */
 void or_frame_prep(const or_frame* f, double* q, double* N, uint8_t* dvalid, uint8_t* nvalid);
 /* O1: Eq. 2 skinning of nq query points against m nodes. idx/w: nq*k, nearest

@@ -476,6 +476,7 @@ __device__ __forceinline__ void pcg_pipelined(const SolveArgs& a, cg::cluster_gr
     g = gather_sum16(gam);
     double d = gather_sum16(del);
     asm volatile("" : "+d"(g), "+d"(d));   // both sums before the early-exit test
+    if (!isfinite(g) || !isfinite(d)) { g = NAN; break; }   // non-finite system: MIS_E_NUMERIC at the update
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
@@ -606,6 +607,7 @@ __device__ __forceinline__ void pcg_pipelined_reg(const SolveArgs& a, cg::cluste
     g = gather_sum16(gam);
     double d = gather_sum16(del);
     asm volatile("" : "+d"(g), "+d"(d));   // both sums before the early-exit test
+    if (!isfinite(g) || !isfinite(d)) { g = NAN; break; }   // non-finite system: MIS_E_NUMERIC at the update
     if (it == 0) g0 = g;
     if (g == 0.0) break;
     const double beta = it == 0 ? 0.0 : g * inv_gprev;
@@ -851,6 +853,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     cl.sync();   // (B) p.Ap known everywhere; every CTA is done reading z
     if (st1) ts[11] = gtimer();
     const double pAp = gather_sum(partB, cs);
+    if (!isfinite(pAp) || !isfinite(rz)) { rz = NAN; done = 1; break; }   // non-finite: MIS_E_NUMERIC below
     if (!(pAp > 0.0)) { done = 1; break; }
     const float alpha = (float)(rz / pAp);
     for (int q = t; q < 6 * nr; q += kCT) {
@@ -886,7 +889,7 @@ __global__ void __launch_bounds__(kCT, 1) k_pcg_cluster(SolveArgs a) {
     return;
   }
   // ---- node update; a non-finite step anywhere rolls the whole update back
-  bool bad = false;
+  bool bad = !isfinite(rz);   // a PCG scalar went non-finite (identical in every CTA)
   for (int q = t; q < 6 * nr; q += kCT)
     if (!isfinite(x[q])) bad = true;
   const int bad_cta = __syncthreads_or(bad);

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   if (threadIdx.x == 0) atomicAdd(a.dots + 0, s);
   grid.sync();
   double rz = a.dots[0], rz_prev = 1.0;
+  bool nonfin = false;
   const double rz0 = rz;
   for (int it = 0; it < a.pcg_iters; ++it) {
     if (rz == 0.0) break;
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
     if (threadIdx.x == 0) atomicAdd(a.dots + 1 + 2 * it, s);
     grid.sync();
     const double pAp = a.dots[1 + 2 * it];
+    if (!isfinite(pAp) || !isfinite(rz)) { nonfin = true; break; }   // MIS_E_NUMERIC below
     if (!(pAp > 0.0)) break;
     const float alpha = (float)(rz / pAp);
     my = 0.0;
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   if (!a.do_update) return;
 
   // ---- node update (fp64 master), rolled back as a whole on a non-finite step
+  if (nonfin && tid == 0) atomicOr(a.numeric_flag, 1);
   for (int64_t j = tid; j < m; j += nth)
     for (int c = 0; c < 6; ++c)
       if (!isfinite(a.x[6 * j + c])) atomicOr(a.numeric_flag, 1);

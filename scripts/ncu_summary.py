@@ -1,11 +1,11 @@
 """Summarise an ncu launch list + full capture into profiles/.
 
-    python scripts/ncu_summary.py <tag> [--round r1]
+    python scripts/ncu_summary.py <tag> [--round r2] [--config c3]
 
 Reads gpurun_out/launches_<tag>.csv and gpurun_out/full_<tag>.ncu-rep and writes
-profiles/<round>_launches.csv (per-kernel aggregate), profiles/<round>_ncu_summary.md
-and profiles/ncu_traffic.json (dram bytes per launch of each captured kernel group,
-read by bench.py for the roofline "traffic" field).
+profiles/<round>_launches_<config>.csv (per-kernel aggregate), profiles/<round>_ncu_summary_<config>.md
+and profiles/<round>_traffic_<config>.json (DRAM bytes per launch of each captured kernel group,
+averaged over the captured launches; read by bench.py --config <config> for the roofline "traffic").
 """
 import argparse
 import collections
@@ -81,19 +81,20 @@ def full(tag):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
-    ap.add_argument("--round", default="r1")
+    ap.add_argument("--round", default="r2")
+    ap.add_argument("--config", default="c3")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     agg = launches(a.tag)
     total = sum(v[0] for v in agg.values())
-    with open(os.path.join(ROOT, "profiles", f"{a.round}_launches.csv"), "w", newline="") as f:
+    with open(os.path.join(ROOT, "profiles", f"{a.round}_launches_{a.config}.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "total_us", "avg_us", "share_pct"])
         for n, (v, c) in sorted(agg.items(), key=lambda x: -x[1][0]):
             w.writerow([n, c, round(v / 1e3, 2), round(v / c / 1e3, 3), round(100 * v / total, 2)])
     fl = full(a.tag)
     traffic = {}
-    lines = [f"# ncu summary ({a.round}, capture tag {a.tag})", "",
+    lines = [f"# ncu summary ({a.round}, bench --config {a.config}, capture tag {a.tag})", "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` over "
              "`python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1` (cold-cache, serialised: "
              "shares, not absolute times). Full capture: `ncu --set full --clock-control none --import-source on`.",
@@ -108,10 +109,14 @@ def main():
                      f"{d.get('dram_write', 0) / 1e6:.2f} | {d.get('l2_bytes', 0) / 1e6:.1f} | {d.get('regs', 0):.0f} | "
                      f"{d.get('achieved_occupancy_pct', 0):.1f} | {d.get('sm_throughput_pct', 0):.1f} | {d['top_stalls']} |")
         g = next((v for k, v in GROUP.items() if d["kernel"].startswith(k)), None)
-        if g and g not in traffic:
-            traffic[g] = int(d.get("dram_read", 0) + d.get("dram_write", 0))
-    open(os.path.join(ROOT, "profiles", f"{a.round}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+        if g:
+            traffic.setdefault(g, []).append(d.get("dram_read", 0) + d.get("dram_write", 0))
+    open(os.path.join(ROOT, "profiles", f"{a.round}_ncu_summary_{a.config}.md"), "w").write("\n".join(lines) + "\n")
+    json.dump({"config": a.config, "source": f"gpurun_out/full_{a.tag}.ncu-rep (ncu --set full, dram__bytes_read.sum "
+                                             "+ dram__bytes_write.sum, mean over the captured launches)",
+               "bytes_per_launch": {g: int(sum(v) / len(v)) for g, v in traffic.items()},
+               "launches_captured": {g: len(v) for g, v in traffic.items()}},
+              open(os.path.join(ROOT, "profiles", f"{a.round}_traffic_{a.config}.json"), "w"), indent=1)
     print("\n".join(lines))
 
 

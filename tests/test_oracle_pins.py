@@ -942,3 +942,24 @@ def test_mirror_register_trajectory_c1():
     Ro, Eo, _ = O.register(prm, pb, fr)
     assert np.abs(Ro - Rt).max() < 1e-9
     assert np.allclose(Eo[:, 4], Es, rtol=1e-10)
+
+
+def test_oracle_threads_same_result():
+    """or_set_threads (bench.py's all-cores column) changes only the summation order."""
+    sc, pb, fr, _ = scene_problem("c2")
+    m = pb.g.shape[0]
+    prm = O.params()
+    Rt = random_state(m, np.random.default_rng(4), 0.01, 0.3)
+    s1 = O.system(prm, pb, fr, Rt)
+    try:
+        O.set_threads(4)
+        s4 = O.system(prm, pb, fr, Rt)
+        o4 = O.fuse(prm, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], fr, sc["rgb_obs"], 2, pb.g)
+    finally:
+        O.set_threads(1)
+    o1 = O.fuse(prm, pb.xyz, pb.nrm, sc["rgb"], sc["weight"], sc["stamp"], fr, sc["rgb_obs"], 2, pb.g)
+    H1, H4 = O.dense_H(s1, m), O.dense_H(s4, m)
+    assert np.abs(H1 - H4).max() <= 1e-12 * np.abs(H1).max()
+    assert np.allclose(s1["energy"], s4["energy"], rtol=1e-12) and s1["n_assoc"] == s4["n_assoc"]
+    for key in ("xyz", "nrm", "weight", "stamp", "owner", "lift_idx", "why"):
+        np.testing.assert_array_equal(o1[key], o4[key])
