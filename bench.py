@@ -337,6 +337,69 @@ def run_mis(args, rank, world, local_rank):
                     "what": "Alg. 3 (P:244-262): box merge, omega cap, deletion test, compaction, Eq. 2 re-skinning; "
                             "ms_per_call includes the one host readback of the survivor count"}
 
+    # ---------------- BASELINE configs[2] / NEXT-1: the C3 100-frame sequence, Alg. 2 per frame --
+    # register -> warp -> fuse -> Alg. 3 filter -> Step 5 node regeneration -- on a model that grows
+    # and is filtered / regrouped every frame (the steady state the per-step number above does not
+    # see: it restores the frame-1 model).  All frames' depth and colour resident on the device; CUDA
+    # events per frame (the API's host readbacks are inside); a first pass on a fresh context warms up.
+    seq_out = None
+    if world == 1 and args.seq_frames > 0:
+        from paper_1803_02009_b200 import synth
+        base, frames = synth.make_sequence_frames(args.config, args.seq_frames)
+        fdev = [(td(f["depth"]), td(f["rgb_obs"]), f["pose"], f["frame"]) for f in frames]
+        n0, m0 = base["xyz"].shape[0], base["g"].shape[0]
+        seq_cap = n0 + 4 * cfg.H * cfg.W
+        ext = base["xyz"].max(0) - base["xyz"].min(0)
+        seq_box = float(np.sqrt(ext[0] * ext[1] / n0))           # point density
+        seq_node = 1.3 * float(np.sqrt(ext[0] * ext[1] / m0))    # node density
+        ef0, ef1 = td(np.zeros((0, 3), np.float32)), td(np.zeros((0, 3), np.float32))
+
+        def run_sequence(prof_on):
+            cs = M.Context(params_for(cfg, M), device=local_rank, stream=stream.cuda_stream)
+            M.mis_set_model(cs.ptr, td(base["xyz"]), td(base["nrm"]), td(base["rgb"]), td(base["weight"]),
+                            td(base["stamp"]), capacity=seq_cap)
+            M.mis_set_graph(cs.ptr, td(base["g"]), td(base["nbr"]))
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in fdev]
+            sizes = []
+            if prof_on:
+                M.mis_prof_read(cs.ptr, reset=True)
+                M.mis_prof_enable(cs.ptr, True)
+            for q, (dd, rr, pz, fi) in enumerate(fdev):
+                evs[q][0].record(stream)
+                M.mis_register(cs.ptr, dd, intr, pz, ef0, ef1, report=False)
+                M.mis_warp(cs.ptr)
+                n_f, _ = M.mis_fuse(cs.ptr, rr, fi)
+                n_k, _ = M.mis_filter(cs.ptr, seq_box, fi, 10, 3.0)
+                m_k = M.mis_regenerate_nodes(cs.ptr, seq_node)
+                evs[q][1].record(stream)
+                sizes.append((n_f, n_k, m_k))
+            torch.cuda.synchronize()
+            ms = [a.elapsed_time(b) for a, b in evs]
+            prof_s = M.mis_prof_read(cs.ptr, reset=True) if prof_on else None
+            rep_s = M.report_dict(M.mis_register(cs.ptr, fdev[-1][0], intr, fdev[-1][2], ef0, ef1))
+            cs.close()
+            return ms, sizes, prof_s, rep_s
+
+        run_sequence(False)                                   # warm-up
+        ms_f, sizes, _, rep_s = run_sequence(False)           # timed (no kernel-group events)
+        prof_s = run_sequence(True)[2]                        # per-group breakdown (separate pass)
+        nf_ = len(ms_f)
+        half = ms_f[nf_ // 2:]
+        seq_out = {"frames": nf_, "fps": round(1e3 * nf_ / sum(ms_f), 2), "ms_per_frame": round(sum(ms_f) / nf_, 4),
+                   "ms_per_frame_steady": round(float(np.mean(half)), 4),
+                   "ms_per_frame_p90": round(float(np.quantile(ms_f, 0.9)), 4),
+                   "model_points": {"start": n0, "after_fuse_last": int(sizes[-1][0]), "end": int(sizes[-1][1]),
+                                    "max": int(max(x[0] for x in sizes))},
+                   "nodes": {"start": m0, "end": int(sizes[-1][2])},
+                   "box_mm": round(seq_box, 4), "node_grid_mm": round(seq_node, 4),
+                   "last_frame_E": [float(rep_s["energy"][0, 4]), float(rep_s["energy"][cfg.gn_iters - 1, 4])],
+                   "kernels_ms_per_frame": {k: round(v[0] / nf_, 5) for k, v in prof_s.items() if v[1] > 0},
+                   "what": "Alg. 2 per frame: register (G x P GN, no ORB term in this leg) + warp + fuse/lift + "
+                           "Alg. 3 filter (box = point spacing, tau_time 10, tau_weight 3) + Step 5 node "
+                           "regeneration (grid = 1.3 x node spacing) + Eq. 2 re-skinning; CUDA events per frame "
+                           "(host readbacks of the API inside); kernels_ms_per_frame from a third pass with kernel-group events"}
+
     # ---------------- roofline of the dominant kernel (timed region: events around K3a, K3b, solver)
     hbm, _, peak_kind = peaks()
     groups = {k: v for k, v in prof.items() if v[1] > 0 and v[0] > 0}
@@ -443,6 +506,7 @@ def run_mis(args, rank, world, local_rank):
         "pcg_phases_us_last_launch": pcg_phases,
         "lm": lm_out,
         "filter": filt_out,
+        "sequence": seq_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "wall_s_timed": round(wall, 4),
@@ -556,6 +620,7 @@ def main():
     ap.add_argument("--no-lm", action="store_true", help="skip the Levenberg-Marquardt (MIS_F_LM) timing")
     ap.add_argument("--no-filter", action="store_true", help="skip the Alg. 3 filtering (mis_filter) timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seq-frames", type=int, default=100, help="frames of the sequence leg (0: skip)")
     ap.add_argument("--shard", action="store_true", help="N>1: shard one model over the ranks (else replicas)")
     args = ap.parse_args()
     if args.warmup < 3:

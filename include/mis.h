@@ -206,6 +206,8 @@ mis_status mis_get_nodes(mis_ctx* ctx, mis_mem mem, float* R9_t3);
 mis_status mis_get_nodes_f64(mis_ctx* ctx, double* R9_t3_host);
 /* Current node positions g_j (m x 3). */
 mis_status mis_get_graph(mis_ctx* ctx, mis_mem mem, float* node_pos);
+/* Current regulariser neighbour lists N(j) (m x n_nbr, -1 padded). */
+mis_status mis_get_nbr(mis_ctx* ctx, mis_mem mem, int32_t* node_nbr);
 
 /* Alg. 2 Step 2: apply the converged field to every point and
  * normal; the model becomes the live world-frame state x_hat_i; the nodes
@@ -246,6 +248,19 @@ mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_i
 mis_status mis_filter(mis_ctx* ctx, float grid_mm, int32_t frame_index, int32_t tau_time, float tau_weight,
                       int64_t* n_out, int64_t stats[4]);
 
+/* NEXT-1: Alg. 2 Step 5 "Regenerate node and corresponding rotation and translation"
+ * in the form of S:102-104 (reading A36): the nodes become the centroids (fp64 mean,
+ * stored fp32) of the occupied cells (floor(x/g), floor(y/g), floor(z/g)) of the model points,
+ * g = node_grid_mm (the paper's node density: 4 mm / 10 mm), each quotient an IEEE fp32
+ * division (as mis_filter), in ascending (kx, ky, kz) order, with identity transforms (R_j = I,
+ * t_j = 0); N(j) = the n_nbr nearest other nodes (ties to the lower index, -1 padded); every
+ * point is re-skinned by Eq. 2 against the new nodes and the model regrouped -- i.e. exactly
+ * mis_set_graph with these nodes and device skinning.  *m_out (host): the node count.  Two host
+ * synchronisations (the cell range, the node count).  MIS_E_ARG (graph unchanged) for
+ * node_grid_mm <= 0, a non-finite position, cells spanning more than 63 key bits, fewer than k+1
+ * occupied cells or points, n_nbr > 16, or world > 1. */
+mis_status mis_regenerate_nodes(mis_ctx* ctx, float node_grid_mm, int32_t* m_out);
+
 /* Read the model (internal order).  Any output may be NULL.  knn_idx/knn_w:
  * n x k in the canonical per-point order (ids ascending). */
 mis_status mis_get_model(mis_ctx* ctx, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight,
@@ -276,12 +291,12 @@ mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* v
 mis_status mis_dbg_fuse_register(mis_ctx* ctx, int64_t* owner, uint8_t* why);
 
 /* ---- instrumentation (bench / profiling) ---- */
-#define MIS_PROF_NCAT 15
+#define MIS_PROF_NCAT 16
 /* Kernel groups: 0 frame_prep (K1), 1 skin (K2), 2 sort_order (K13), 3 pattern,
  * 4 assemble_points (K3), 5 assemble_graph (K4/K5), 6 solve (K6-K8),
  * 7 warp_model (K9), 8 fuse_register (K10), 9 fuse_apply (K11), 10 lift (K12),
  * 11 io (uploads, layout conversion), 12 reduce_records (K3 chunk records -> blocks),
- * 13 accum_points, 14 filter (K14 + the survivors' K2). */
+ * 13 accum_points, 14 filter (K14 + the survivors' K2), 15 regenerate (K15 node regeneration). */
 const char* mis_prof_name(int cat);
 /* on = 1: record a CUDA event pair on the context stream around every kernel
  * group launched by this context; on = 2: only around the K3 and solver groups

@@ -96,6 +96,9 @@ def lib():
             L.or_filter.argtypes = [C.c_int64] + [C.c_void_p] * 6 + [C.c_float, C.c_int32, C.c_int32, C.c_float,
                                                                       C.c_float] + [C.c_void_p] * 8
             L.or_filter.restype = C.c_int64
+            L.or_regenerate_nodes.argtypes = [C.c_int64, C.c_void_p, C.c_float, C.c_int32, C.c_void_p, C.c_void_p,
+                                              C.c_void_p]
+            L.or_regenerate_nodes.restype = C.c_int64
             _lib = L
     return _lib
 
@@ -316,3 +319,15 @@ def filter_points(xyz, nrm, rgb, weight, stamp, ids, grid, frame_index, tau_time
         out[key] = out[key][:no]
     out["cells"] = int(cells.value)
     return out
+
+
+def regenerate_nodes(xyz, grid, n_nbr):
+    """O8: Alg. 2 Step 5 node regeneration (reading A36).
+    Returns (g (m x 3, fp64 centroids), nbr (m x n_nbr), nbr_margin (m))."""
+    xyz = _f32(xyz)
+    n = xyz.shape[0]
+    g = np.zeros((max(n, 1), 3))
+    nbr = np.zeros((max(n, 1), max(n_nbr, 1)), np.int32)
+    mg = np.zeros(max(n, 1))
+    m = lib().or_regenerate_nodes(n, _p(xyz), float(grid), int(n_nbr), _p(g), _p(nbr), _p(mg))
+    return g[:m], nbr[:m, :n_nbr], mg[:m]

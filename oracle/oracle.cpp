@@ -990,4 +990,39 @@ int64_t or_filter(int64_t n, const float* xyz, const float* nrm, const float* rg
   return o;
 }
 
+// O8 (NEXT-1, Alg. 2 Step 5 "Regenerate node and corresponding rotation and translation"),
+// in the form of S:102-104 (reading A36): nodes = the centroids (plain fp64 mean) of the occupied
+// axis-aligned cells of size `grid` -- (floor(x/grid), floor(y/grid), floor(z/grid)), each quotient
+// an IEEE fp32 division and floor (as A30) -- in ascending (kx, ky, kz) order; R_j = I, t_j = 0;
+// N(j) = the n_nbr nearest other nodes by Euclidean distance, ties to the lower index, -1 padded.
+// nbr_margin[j]: relative gap between the n_nbr-th and the next distance (1 if none).
+int64_t or_regenerate_nodes(int64_t n, const float* xyz, float grid, int32_t n_nbr, double* g_out,
+                            int32_t* nbr_out, double* nbr_margin) {
+  std::map<std::array<int64_t, 3>, std::vector<int64_t>> cells;
+  for (int64_t i = 0; i < n; ++i) {
+    std::array<int64_t, 3> key;
+    for (int a = 0; a < 3; ++a) key[a] = (int64_t)floorf(xyz[3 * i + a] / grid);
+    cells[key].push_back(i);
+  }
+  int64_t m = 0;
+  for (const auto& cell : cells) {   // ascending (kx, ky, kz)
+    V3 c = v3(0, 0, 0);
+    for (int64_t i : cell.second) c = add(c, load3(xyz + 3 * i));
+    c = scale(c, 1.0 / (double)cell.second.size());
+    for (int a = 0; a < 3; ++a) g_out[3 * m + a] = c[a];
+    ++m;
+  }
+  for (int64_t j = 0; j < m; ++j) {
+    std::vector<std::pair<double, int64_t> > d;   // (distance, id) of every other node, sorted
+    const V3 gj = v3(g_out[3 * j], g_out[3 * j + 1], g_out[3 * j + 2]);
+    for (int64_t l = 0; l < m; ++l)
+      if (l != j) d.push_back(std::make_pair(norm(sub(v3(g_out[3 * l], g_out[3 * l + 1], g_out[3 * l + 2]), gj)), l));
+    std::sort(d.begin(), d.end());
+    for (int s = 0; s < n_nbr; ++s) nbr_out[(int64_t)n_nbr * j + s] = s < (int)d.size() ? (int32_t)d[s].second : -1;
+    nbr_margin[j] = ((int)d.size() > n_nbr && n_nbr > 0 && d[n_nbr].first > 0)
+                        ? (d[n_nbr].first - d[n_nbr - 1].first) / d[n_nbr].first : 1.0;
+  }
+  return m;
+}
+
 }  // extern "C"

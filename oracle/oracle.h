@@ -142,6 +142,14 @@ int64_t or_filter(int64_t n, const float* xyz, const float* nrm, const float* rg
                   double* weight_out, int32_t* stamp_out, int64_t* ids_out, uint8_t* stable_out,
                   int64_t* cells_out);
 
+/* O8 (NEXT-1): Alg. 2 Step 5 node regeneration as S:102-104 (reading A36): the
+ * centroids of the occupied grid cells (fp32 floor(x/grid) per axis, A30) in ascending (kx, ky, kz)
+ * order, identity transforms, N(j) = the n_nbr nearest other nodes (ties to the lower index, -1
+ * padded).  g_out: n*3 capacity; nbr_out: n*n_nbr; nbr_margin: n (relative gap at the n_nbr cut).
+ * Returns the node count. */
+int64_t or_regenerate_nodes(int64_t n, const float* xyz, float grid, int32_t n_nbr, double* g_out,
+                            int32_t* nbr_out, double* nbr_margin);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1086,6 +1086,16 @@ mis_status mis_get_graph(mis_ctx* c, mis_mem mem, float* node_pos) {
   return MIS_OK;
 }
 
+mis_status mis_get_nbr(mis_ctx* c, mis_mem mem, int32_t* node_nbr) {
+  if (!c || !node_nbr) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  if (c->prm.n_nbr == 0) return MIS_OK;
+  cudaSetDevice(c->device);
+  TRY(c, cudaMemcpyAsync(node_nbr, c->nbr.p, (size_t)c->m * c->prm.n_nbr * 4, kind_out(mem), c->st));
+  if (mem == MIS_MEM_HOST) TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
 mis_status mis_dbg_set_nodes(mis_ctx* c, mis_mem mem, const float* Rt) {
   if (!c || !Rt) return MIS_E_ARG;
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
@@ -1364,6 +1374,45 @@ mis_status mis_filter(mis_ctx* c, float grid_mm, int32_t frame_index, int32_t ta
   return MIS_OK;
 }
 
+mis_status mis_regenerate_nodes(mis_ctx* c, float node_grid_mm, int32_t* m_out) {
+  if (!c || !m_out || !(node_grid_mm > 0.f) || !std::isfinite(node_grid_mm)) return MIS_E_ARG;
+  if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph");
+  if (c->world > 1)   // the cells of a sharded model span ranks: not reduced across ranks (yet)
+    return fail(c, MIS_E_ARG, "mis_regenerate_nodes: single-GPU only");
+  if (c->prm.n_nbr > 16) return fail(c, MIS_E_ARG, "mis_regenerate_nodes: n_nbr <= 16");
+  if (c->n <= c->K) return fail(c, MIS_E_ARG, "mis_regenerate_nodes: fewer than k+1 points");
+  TRY(c, flush_frame(c));
+  cudaSetDevice(c->device);
+  TRY(c, ensure(c, c->finfo, 64));
+  int32_t range[7];
+  int64_t m = 0;
+  {
+    ProfScope ps(c, P_REGEN, 1);
+    TRY(c, run_filter_range(c, node_grid_mm, range));
+  }
+  int sh_x = 0, sh_y = 0;
+  const int bits = range[6] ? -1 : filter_key_bits(range, &sh_x, &sh_y);
+  if (bits < 0)
+    return fail(c, MIS_E_ARG, "mis_regenerate_nodes: a position is not finite or the cells span more than 63 key bits");
+  {
+    ProfScope ps(c, P_REGEN, 3);
+    TRY(c, run_regen_centroids(c, node_grid_mm, range, sh_x, sh_y, bits, &m));
+  }
+  if (m < c->K + 1 || m > 0x7fffffff)
+    return fail(c, MIS_E_ARG, "mis_regenerate_nodes: fewer than k+1 occupied cells (graph unchanged)");
+  {
+    ProfScope ps(c, P_REGEN, c->prm.n_nbr > 0 ? 1 : 0);
+    TRY(c, run_regen_knn(c, (int)m, c->prm.n_nbr));
+  }
+  // the new graph through the device-input path of mis_set_graph: identity transforms, Eq. 2
+  // skinning of every point against the new nodes (K2), K13 regrouping
+  mis_status s = mis_set_graph(c, (int32_t)m, MIS_MEM_DEVICE, c->fl_xyz.as<float>(), c->rg_nbr.as<int32_t>(), nullptr,
+                               nullptr);
+  if (s != MIS_OK) return s;
+  *m_out = (int32_t)m;
+  return MIS_OK;
+}
+
 mis_status mis_get_model(mis_ctx* c, mis_mem mem, float* xyz, float* nrm, float* rgb, float* weight, int32_t* stamp,
                          int64_t* ids, int32_t* knn_idx, float* knn_w, int64_t* n_host) {
   if (!c) return MIS_E_ARG;
@@ -1434,7 +1483,8 @@ mis_status mis_skin(mis_ctx* c, mis_mem mem, int64_t nq, const float* pts, int32
 const char* mis_prof_name(int cat) {
   static const char* names[MIS_PROF_NCAT] = {"frame_prep", "skin", "sort_order", "pattern", "assoc_points",
                                              "assemble_graph", "solve", "warp_model", "fuse_register", "fuse_apply",
-                                             "lift", "io", "finalize", "accum_points", "filter"};
+                                             "lift", "io", "finalize", "accum_points", "filter",
+                                             "regenerate"};
   return (cat >= 0 && cat < MIS_PROF_NCAT) ? names[cat] : "?";
 }
 

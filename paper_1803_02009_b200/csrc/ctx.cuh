@@ -116,6 +116,7 @@ struct Ctx {
   DBuf cub_tmp;
   DBuf finfo;   // mis_filter: int64 [survivors, boxes, stable, boxes to re-skin] + int32 range [7]
   DBuf fl_xyz, fl_idx, fl_kidx, fl_kw;   // mis_filter: re-skinning list (positions, model index, K2 output)
+  DBuf rg_nbr;   // mis_regenerate_nodes: N(j) of the new nodes (their positions: fl_xyz)
 
   // ---- instrumentation
   bool prof = false, prof_light = false;   // light: only the K3 and solver groups
@@ -127,7 +128,7 @@ struct Ctx {
 };
 
 enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WARP, P_FREG, P_FAPPLY, P_LIFT, P_IO,
-       P_REDUCE, P_ACCUM, P_FILTER };
+       P_REDUCE, P_ACCUM, P_FILTER, P_REGEN };
 void count_launches(int64_t k);
 
 // report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual
@@ -172,6 +173,8 @@ int filter_key_bits(const int32_t* range, int* sh_x, int* sh_y);
 cudaError_t run_filter(Ctx* c, float grid, const int32_t* range, int sh_x, int sh_y, int bits, int32_t frame,
                        int32_t tau_time, float tau_weight);
 cudaError_t run_filter_skin(Ctx* c, int64_t nl);
+cudaError_t run_regen_centroids(Ctx* c, float grid, const int32_t* range, int sh_x, int sh_y, int bits, int64_t* m_out);
+cudaError_t run_regen_knn(Ctx* c, int m, int nn);
 cudaError_t nccl_allreduce_sum_f32(Ctx* c, float* buf, size_t count);
 cudaError_t nccl_allreduce_sum_f64(Ctx* c, double* buf, size_t count);
 cudaError_t nccl_allreduce_max_i64(Ctx* c, int64_t* buf, size_t count);

@@ -319,4 +319,125 @@ cudaError_t run_filter_skin(Ctx* c, int64_t nl) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- K15: node regeneration
+// NEXT-1, Alg. 2 Step 5 as S:102-104, reading A36: the nodes become the centroids of the
+// occupied cells of size s (the same fp32 box coordinates as K14, A30), in ascending (kx, ky, kz)
+// order, with identity transforms; N(j) = the n_nbr nearest other nodes (ties to the lower index).
+//   K14a k_cell_range + readback   validation and key width (as the filter)
+//   K14b k_cell_keys + CUB sort    a cell's members contiguous, cells in ascending key order
+//   K15a k_cell_heads + CUB scan   cell id of every sorted position
+//   K15b k_cell_centroid           a cell's first position sums its members in fp64 (ascending internal
+//                                  index), writes the fp32 centroid; the node count is read back
+//   K15c k_node_knn                brute-force n_nbr nearest (fp64 distances of the fp32 centroids)
+// then mis_set_graph (device inputs): identity states, Eq. 2 skinning of every point (K2), K13 order.
+__global__ void __launch_bounds__(256) k_cell_heads(int64_t n, const uint64_t* __restrict__ keys,
+                                                    int32_t* __restrict__ head) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || keys[i - 1] != keys[i]) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(256) k_cell_centroid(int64_t n, const uint64_t* __restrict__ keys,
+                                                       const uint32_t* __restrict__ vals,
+                                                       const int32_t* __restrict__ cid, ModelView md,
+                                                       float* __restrict__ g, int64_t* __restrict__ info) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) info[0] = cid[n - 1];   // node count
+  if (i > 0 && keys[i - 1] == keys[i]) return;
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  int64_t e = i;
+  for (; e < n && keys[e] == keys[i]; ++e) {
+    const uint32_t p = vals[e];
+    sx += md.px[p]; sy += md.py[p]; sz += md.pz[p];
+  }
+  const double inv = 1.0 / (double)(e - i);
+  const int64_t j = cid[i] - 1;
+  g[3 * j] = (float)(sx * inv); g[3 * j + 1] = (float)(sy * inv); g[3 * j + 2] = (float)(sz * inv);
+}
+
+constexpr int kMaxRegenNbr = 16;
+__global__ void __launch_bounds__(256) k_node_knn(int m, int nn, const float* __restrict__ g,
+                                                  int32_t* __restrict__ nbr) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float4 tile[256];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double gj[3] = {0, 0, 0};
+  if (j < m) { gj[0] = g[3 * j]; gj[1] = g[3 * j + 1]; gj[2] = g[3 * j + 2]; }
+  double bd[kMaxRegenNbr];
+  int bi[kMaxRegenNbr];
+#pragma unroll
+  for (int s = 0; s < kMaxRegenNbr; ++s) { bd[s] = INFINITY; bi[s] = -1; }
+  for (int t0 = 0; t0 < m; t0 += 256) {
+    __syncthreads();
+    const int l = t0 + threadIdx.x;
+    if (l < m) tile[threadIdx.x] = make_float4(g[3 * l], g[3 * l + 1], g[3 * l + 2], 0.f);
+    __syncthreads();
+    const int tn = min(256, m - t0);
+    if (j >= m) continue;
+    for (int q = 0; q < tn; ++q) {
+      const int l2 = t0 + q;
+      if (l2 == j) continue;
+      const float4 p = tile[q];
+      const double dx = (double)p.x - gj[0], dy = (double)p.y - gj[1], dz = (double)p.z - gj[2];
+      double cd = dx * dx + dy * dy + dz * dz;
+      if (!(cd < bd[nn - 1])) continue;   // ids ascend within the scan: a tie keeps the lower id
+      int ci = l2;
+#pragma unroll
+      for (int s = 0; s < kMaxRegenNbr; ++s) {
+        if (s < nn && cd < bd[s]) {
+          const double td = bd[s];
+          const int ti = bi[s];
+          bd[s] = cd; bi[s] = ci; cd = td; ci = ti;
+        }
+      }
+    }
+  }
+  if (j >= m) return;
+  for (int s = 0; s < nn; ++s) nbr[(int64_t)nn * j + s] = bi[s];
+}
+
+// K14b + CUB + K15a/b: centroids into c->fl_xyz, node count read back into *m_out.
+cudaError_t run_regen_centroids(Ctx* c, float grid, const int32_t* range, int sh_x, int sh_y, int bits, int64_t* m_out) {
+  const int64_t n = c->n;
+  int64_t* info = c->finfo.as<int64_t>();
+  CK(ensure(c, c->keys, n * 8)); CK(ensure(c, c->keys2, n * 8));
+  CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
+  CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
+  CK(ensure(c, c->fl_xyz, n * 12));
+  const int b = (int)((n + 255) / 256);
+  ModelView A = model_view(c);
+  launch_pdl(k_cell_keys, dim3(b), dim3(256), 0, c->st, A, grid, make_int3(range[0], range[1], range[2]), sh_x, sh_y,
+             c->keys.as<uint64_t>(), c->vals.as<uint32_t>());
+  CK(cub_call(c, [&](void* t, size_t& s) {
+    return cub::DeviceRadixSort::SortPairs(t, s, c->keys.as<uint64_t>(), c->keys2.as<uint64_t>(), c->vals.as<uint32_t>(),
+                                           c->vals2.as<uint32_t>(), (int)n, 0, std::max(bits, 1), c->st);
+  }));
+  launch_pdl(k_cell_heads, dim3(b), dim3(256), 0, c->st, n, (const uint64_t*)c->keys2.as<uint64_t>(), c->flags.as<int32_t>());
+  CK(cub_call(c, [&](void* t, size_t& s) {
+    return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->scan.as<int32_t>(), (int)n, c->st);
+  }));
+  launch_pdl(k_cell_centroid, dim3(b), dim3(256), 0, c->st, n, (const uint64_t*)c->keys2.as<uint64_t>(),
+             (const uint32_t*)c->vals2.as<uint32_t>(), (const int32_t*)c->scan.as<int32_t>(), A, c->fl_xyz.as<float>(),
+             info);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->hpin, info, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  memcpy(m_out, c->hpin, 8);
+  return cudaSuccess;
+}
+
+// K15c: N(j) of the m regenerated nodes (in c->fl_xyz) into c->rg_nbr.
+cudaError_t run_regen_knn(Ctx* c, int m, int nn) {
+  CK(ensure(c, c->rg_nbr, (size_t)m * (nn > 0 ? nn : 1) * 4));
+  if (nn > 0)
+    launch_pdl(k_node_knn, dim3((unsigned)((m + 255) / 256)), dim3(256), 0, c->st, m, nn,
+               (const float*)c->fl_xyz.as<float>(), c->rg_nbr.as<int32_t>());
+  return cudaGetLastError();
+}
+
 }  // namespace mis

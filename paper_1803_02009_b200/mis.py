@@ -75,9 +75,11 @@ _sig = {
     "mis_get_nodes": ([_V, C.c_int, _V], C.c_int),
     "mis_get_nodes_f64": ([_V, _V], C.c_int),
     "mis_get_graph": ([_V, C.c_int, _V], C.c_int),
+    "mis_get_nbr": ([_V, C.c_int, _V], C.c_int),
     "mis_warp": ([_V, C.c_int, _V, _V], C.c_int),
     "mis_fuse": ([_V, C.c_int, _V, C.c_int32, _P(C.c_int64), _V], C.c_int),
     "mis_filter": ([_V, C.c_float, C.c_int32, C.c_int32, C.c_float, _P(C.c_int64), _V], C.c_int),
+    "mis_regenerate_nodes": ([_V, C.c_float, _P(C.c_int32)], C.c_int),
     "mis_get_model": ([_V, C.c_int, _V, _V, _V, _V, _V, _V, _V, _V, _P(C.c_int64)], C.c_int),
     "mis_skin": ([_V, C.c_int, C.c_int64, _V, _V, _V], C.c_int),
     "mis_dbg_set_nodes": ([_V, C.c_int, _V], C.c_int),
@@ -91,7 +93,7 @@ _sig = {
     "mis_launch_count": ([], C.c_int64),
     "mis_dbg_solver_phases": ([_V, _V], C.c_int),
 }
-MIS_PROF_NCAT = 15
+MIS_PROF_NCAT = 16
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -249,6 +251,11 @@ def mis_get_graph(ctx, out):
     return out
 
 
+def mis_get_nbr(ctx, out):
+    _check(ctx, _lib.mis_get_nbr(ctx, _mem_of(out), _ptr(out, np.int32)))
+    return out
+
+
 def mis_warp(ctx, xyz_cam=None, nrm_cam=None):
     _check(ctx, _lib.mis_warp(ctx, _mem_of(xyz_cam, nrm_cam), _ptr(xyz_cam, np.float32), _ptr(nrm_cam, np.float32)))
 
@@ -266,6 +273,13 @@ def mis_filter(ctx, grid_mm, frame_index, tau_time=10, tau_weight=3.0):
     stats = np.zeros(4, np.int64)
     _check(ctx, _lib.mis_filter(ctx, grid_mm, frame_index, tau_time, tau_weight, C.byref(n_out), _ptr(stats)))
     return int(n_out.value), stats
+
+
+def mis_regenerate_nodes(ctx, node_grid_mm):
+    """NEXT-1, Alg. 2 Step 5 (reading A36).  Returns the new node count."""
+    m = C.c_int32()
+    _check(ctx, _lib.mis_regenerate_nodes(ctx, float(node_grid_mm), C.byref(m)))
+    return int(m.value)
 
 
 def mis_get_model(ctx, k, device=False):

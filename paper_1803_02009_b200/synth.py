@@ -103,6 +103,19 @@ class Surface:
             hy = hy - e * (y - by) / (s * s)
         return hx, hy
 
+    def h_grad(self, x, y):
+        """h and its gradient with one exponential per bump (the ray caster's Newton step)."""
+        z = Z0 + (x * x + y * y) / CURV + RESP_AMP * math.sin(2 * math.pi * RESP_HZ * self.t_s)
+        hx = 2 * x / CURV
+        hy = 2 * y / CURV
+        for bx, by, a, s in self.bumps:
+            dx, dy = x - bx, y - by
+            e = a * np.exp(-(dx * dx + dy * dy) / (2 * s * s))
+            z = z + e
+            hx = hx - e * dx / (s * s)
+            hy = hy - e * dy / (s * s)
+        return z, hx, hy
+
     def normal(self, x, y):
         """Unit normal facing the camera (negative z side)."""
         hx, hy = self.grad(x, y)
@@ -148,14 +161,17 @@ def render_depth(cfg, surf: Surface, R, T, rng, noise=True, holes=True):
     dw = dc @ R          # R^T d  (row vectors)
     o = -R.T @ T         # camera centre in world
     s = np.full(u.shape, Z0 - o[2])
-    for _ in range(30):
+    for _ in range(30):   # Newton on z(s) - h(x(s), y(s)) = 0, to convergence (quadratic: ~5 steps)
         x = o[0] + s * dw[..., 0]
         y = o[1] + s * dw[..., 1]
         z = o[2] + s * dw[..., 2]
-        hx, hy = surf.grad(x, y)
-        f = z - surf.h(x, y)
+        hz, hx, hy = surf.h_grad(x, y)
+        f = z - hz
         fp = dw[..., 2] - (hx * dw[..., 0] + hy * dw[..., 1])
-        s = s - f / fp
+        step = f / fp
+        s = s - step
+        if np.abs(step).max() < 1e-11:
+            break
     # the camera-frame z of o + s*dw equals s (dc has unit z)
     depth = s.copy()
     if noise:

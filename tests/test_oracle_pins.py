@@ -963,3 +963,44 @@ def test_oracle_threads_same_result():
     assert np.allclose(s1["energy"], s4["energy"], rtol=1e-12) and s1["n_assoc"] == s4["n_assoc"]
     for key in ("xyz", "nrm", "weight", "stamp", "owner", "lift_idx", "why"):
         np.testing.assert_array_equal(o1[key], o4[key])
+
+
+# ------------------------------------------------------------------ O8: Alg. 2 Step 5 node regeneration (A36)
+def test_regen_spec_cube_and_clusters():
+    gr = GOLD["node_regen"]
+    lo, e = np.array(gr["cube_corner_min"]), gr["cube_edge"]
+    corners = np.array([[lo[0] + e * (i & 1), lo[1] + e * ((i >> 1) & 1), lo[2] + e * (i >> 2)] for i in range(8)])
+    g, nbr, _ = O.regenerate_nodes(corners, gr["cube_grid"], 4)
+    assert g.shape == (1, 3) and np.allclose(g[0], gr["cube_centroid"], atol=1e-12)
+    assert (nbr == -1).all()                                    # no other node
+    rng = np.random.default_rng(2)
+    pts = np.concatenate([c + rng.uniform(-2, 2, (20, 3)) for c in gr["clusters"]])
+    g, nbr, _ = O.regenerate_nodes(pts, gr["cluster_grid"], 1)
+    assert g.shape == (2, 3) and nbr[0, 0] == 1 and nbr[1, 0] == 0
+    assert np.allclose(g, [pts[:20].astype(np.float32).astype(np.float64).mean(0),
+                           pts[20:].astype(np.float32).astype(np.float64).mean(0)], atol=1e-12)
+    g4, nbr4, _ = O.regenerate_nodes(pts, gr["cluster_grid"], 4)
+    assert (nbr4[:, 1:] == -1).all() and (nbr4[:, 0] == [1, 0]).all()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_regen_uniform_cube_brute_force(seed):
+    """node count = occupied cells; centroids = per-cell means; N(j) = the n_nbr nearest by a
+    brute-force distance table with (distance, index) ties; ascending (kx, ky, kz) node order."""
+    gr = GOLD["node_regen"]
+    rng = np.random.default_rng(20 + seed)
+    pts = rng.uniform(0, gr["uniform_edge"], (gr["uniform_n"], 3)).astype(np.float32)
+    s = np.float32(gr["uniform_grid"])
+    g, nbr, mg = O.regenerate_nodes(pts, s, 6)
+    cells = np.floor(pts / s).astype(np.int64)                      # fp32 division, as A30
+    uc, inv = np.unique(cells, axis=0, return_inverse=True)          # lexicographic = (kx, ky, kz)
+    assert g.shape[0] == uc.shape[0]
+    cnt = np.bincount(inv)
+    mean = np.stack([np.bincount(inv, pts[:, a].astype(np.float64)) / cnt for a in range(3)], -1)
+    assert np.abs(g - mean).max() < 1e-12
+    D = np.linalg.norm(g[:, None] - g[None], axis=-1)
+    np.fill_diagonal(D, np.inf)
+    for j in range(g.shape[0]):
+        order = np.lexsort((np.arange(g.shape[0]), D[j]))[:6]
+        assert (nbr[j] == order).all()
+    assert (mg >= 0).all()
