@@ -532,6 +532,7 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
       4 * n, n,                                                             // pix, why
       12 * nf + 16, 12 * nf + 16, 4 * nf * K + 16, 4 * nf * K + 16,         // features
       12 * n, 4 * n, 4 * n * K, 4 * n * K,                                  // filter re-skinning list
+      32 * n, 4 * m * nn,                                                   // node regeneration: cell sums, N(j)
   };
   size_t total = 0;
   for (int64_t x : b) {
@@ -644,8 +645,18 @@ static std::string graph_flag_message(int f) {
          ((f & 4) ? " weight" : "") + ((f & 8) ? " neighbour list" : "");
 }
 
+// skin_order (internal, mis_regenerate_nodes): the points in a spatially coherent order (sorted by node
+// cell), skinned by the boxed K2 instead of the brute-force one
+static mis_status set_graph_impl(mis_ctx* c, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
+                                 const int32_t* knn_idx, const float* knn_w, const uint32_t* skin_order);
+
 mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
                          const int32_t* knn_idx, const float* knn_w) {
+  return set_graph_impl(c, m, mem, node_pos, node_nbr, knn_idx, knn_w, nullptr);
+}
+
+static mis_status set_graph_impl(mis_ctx* c, int32_t m, mis_mem mem, const float* node_pos, const int32_t* node_nbr,
+                                 const int32_t* knn_idx, const float* knn_w, const uint32_t* skin_order) {
   if (!c) return MIS_E_ARG;
   if (!c->have_model) return fail(c, MIS_E_STATE, "set_graph before set_model");
   const int K = c->K, nn = c->prm.n_nbr;
@@ -694,6 +705,10 @@ mis_status mis_set_graph(mis_ctx* c, int32_t m, mis_mem mem, const float* node_p
         sw = dw;
       }
       launch_pdl(k_canon_knn, dim3(nb(n)), dim3(256), 0, c->st, n, K, m, si, sw, c->cap, md.kidx, md.kw, flag);
+    } else if (skin_order) {
+      launch_skin_boxed(n, skin_order, 1, md.px, md.py, md.pz, 1, c->g.as<float>(), m, K, md.kidx, md.kw, c->cap,
+                        c->st);
+      TRY(c, cudaGetLastError());
     } else {
       TRY(c, skin(c, n, md.px, md.py, md.pz, 1, md.kidx, md.kw, c->cap));
     }
@@ -1395,7 +1410,7 @@ mis_status mis_regenerate_nodes(mis_ctx* c, float node_grid_mm, int32_t* m_out) 
   if (bits < 0)
     return fail(c, MIS_E_ARG, "mis_regenerate_nodes: a position is not finite or the cells span more than 63 key bits");
   {
-    ProfScope ps(c, P_REGEN, 3);
+    ProfScope ps(c, P_REGEN, 4);
     TRY(c, run_regen_centroids(c, node_grid_mm, range, sh_x, sh_y, bits, &m));
   }
   if (m < c->K + 1 || m > 0x7fffffff)
@@ -1406,8 +1421,8 @@ mis_status mis_regenerate_nodes(mis_ctx* c, float node_grid_mm, int32_t* m_out) 
   }
   // the new graph through the device-input path of mis_set_graph: identity transforms, Eq. 2
   // skinning of every point against the new nodes (K2), K13 regrouping
-  mis_status s = mis_set_graph(c, (int32_t)m, MIS_MEM_DEVICE, c->fl_xyz.as<float>(), c->rg_nbr.as<int32_t>(), nullptr,
-                               nullptr);
+  mis_status s = set_graph_impl(c, (int32_t)m, MIS_MEM_DEVICE, c->fl_xyz.as<float>(), c->rg_nbr.as<int32_t>(), nullptr,
+                                nullptr, c->vals2.as<uint32_t>());   // points in node-cell order (K15's sort)
   if (s != MIS_OK) return s;
   *m_out = (int32_t)m;
   return MIS_OK;

@@ -97,6 +97,10 @@ struct Ctx;   // defined in api.cu
 void launch_frame_prep(const FrameView& f, float4* nmap, double4* nmapd, cudaStream_t s);
 void launch_skin(int64_t nq, const float* px, const float* py, const float* pz, int64_t stride_xyz,
                  const float* g, int m, int K, int32_t* idx, float* w, int64_t out_stride, cudaStream_t s);
+// K2 over spatially coherent 256-query blocks with a per-block candidate-node bound (exact Eq. 2)
+void launch_skin_boxed(int64_t nq, const uint32_t* order, int out_at_q, const float* px, const float* py,
+                       const float* pz, int64_t sxyz, const float* g, int m, int K, int32_t* idx, float* w, int64_t os,
+                       cudaStream_t s);
 
 struct AsmPointsArgs {
   ModelView md;

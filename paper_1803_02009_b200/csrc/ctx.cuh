@@ -116,7 +116,7 @@ struct Ctx {
   DBuf cub_tmp;
   DBuf finfo;   // mis_filter: int64 [survivors, boxes, stable, boxes to re-skin] + int32 range [7]
   DBuf fl_xyz, fl_idx, fl_kidx, fl_kw;   // mis_filter: re-skinning list (positions, model index, K2 output)
-  DBuf rg_nbr;   // mis_regenerate_nodes: N(j) of the new nodes (their positions: fl_xyz)
+  DBuf rg_nbr, rg_sums;   // mis_regenerate_nodes: N(j) of the new nodes (positions: fl_xyz), fp64 cell sums
 
   // ---- instrumentation
   bool prof = false, prof_light = false;   // light: only the K3 and solver groups

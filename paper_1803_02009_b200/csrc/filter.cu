@@ -312,8 +312,8 @@ cudaError_t run_filter_skin(Ctx* c, int64_t nl) {
   if (nl <= 0) return cudaSuccess;
   CK(ensure(c, c->fl_kidx, (size_t)nl * 4 * c->K)); CK(ensure(c, c->fl_kw, (size_t)nl * 4 * c->K));
   const float* x = c->fl_xyz.as<float>();
-  launch_skin(nl, x, x + 1, x + 2, 3, c->g.as<float>(), c->m, c->K, c->fl_kidx.as<int32_t>(), c->fl_kw.as<float>(), nl,
-              c->st);
+  launch_skin_boxed(nl, nullptr, 0, x, x + 1, x + 2, 3, c->g.as<float>(), c->m, c->K, c->fl_kidx.as<int32_t>(),
+                    c->fl_kw.as<float>(), nl, c->st);   // the list is in box order: spatially coherent blocks
   launch_pdl(k_cell_skin_scatter, dim3((unsigned)((nl + 255) / 256)), dim3(256), 0, c->st, nl, c->K,
              c->fl_idx.as<int32_t>(), c->fl_kidx.as<int32_t>(), c->fl_kw.as<float>(), model_view(c));
   return cudaGetLastError();
@@ -326,8 +326,8 @@ cudaError_t run_filter_skin(Ctx* c, int64_t nl) {
 //   K14a k_cell_range + readback   validation and key width (as the filter)
 //   K14b k_cell_keys + CUB sort    a cell's members contiguous, cells in ascending key order
 //   K15a k_cell_heads + CUB scan   cell id of every sorted position
-//   K15b k_cell_centroid           a cell's first position sums its members in fp64 (ascending internal
-//                                  index), writes the fp32 centroid; the node count is read back
+//   K15b k_cell_accum              segmented warp sums of the members' positions (fp64) + one atomic per
+//                                  (warp, cell); k_cell_centroid: fp32 centroids, the node count read back
 //   K15c k_node_knn                brute-force n_nbr nearest (fp64 distances of the fp32 centroids)
 // then mis_set_graph (device inputs): identity states, Eq. 2 skinning of every point (K2), K13 order.
 __global__ void __launch_bounds__(256) k_cell_heads(int64_t n, const uint64_t* __restrict__ keys,
@@ -338,25 +338,51 @@ __global__ void __launch_bounds__(256) k_cell_heads(int64_t n, const uint64_t* _
   if (i < n) head[i] = (i == 0 || keys[i - 1] != keys[i]) ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(256) k_cell_centroid(int64_t n, const uint64_t* __restrict__ keys,
-                                                       const uint32_t* __restrict__ vals,
-                                                       const int32_t* __restrict__ cid, ModelView md,
-                                                       float* __restrict__ g, int64_t* __restrict__ info) {
+// K15b: every sorted position adds its point to its cell's fp64 sums (x, y, z, count): a segmented
+// warp scan over the (non-decreasing) cell ids, then one atomic per (warp, cell) segment -- fully
+// parallel whatever the cell sizes (a cell of a 3 mm node grid holds ~500 points at C3).
+__global__ void __launch_bounds__(256) k_cell_accum(int64_t n, const uint32_t* __restrict__ vals,
+                                                    const int32_t* __restrict__ cid_incl, ModelView md,
+                                                    double4* __restrict__ sums) {
   pdl_wait();
   pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (i == n - 1) info[0] = cid[n - 1];   // node count
-  if (i > 0 && keys[i - 1] == keys[i]) return;
-  double sx = 0.0, sy = 0.0, sz = 0.0;
-  int64_t e = i;
-  for (; e < n && keys[e] == keys[i]; ++e) {
-    const uint32_t p = vals[e];
-    sx += md.px[p]; sy += md.py[p]; sz += md.pz[p];
+  const int lane = threadIdx.x & 31;
+  int cid = -1;
+  double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (i < n) {
+    const uint32_t p = vals[i];
+    cid = cid_incl[i] - 1;
+    v = make_double4(md.px[p], md.py[p], md.pz[p], 1.0);
   }
-  const double inv = 1.0 / (double)(e - i);
-  const int64_t j = cid[i] - 1;
-  g[3 * j] = (float)(sx * inv); g[3 * j + 1] = (float)(sy * inv); g[3 * j + 2] = (float)(sz * inv);
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int cu = __shfl_up_sync(full, cid, off);
+    const double ux = __shfl_up_sync(full, v.x, off), uy = __shfl_up_sync(full, v.y, off);
+    const double uz = __shfl_up_sync(full, v.z, off), uw = __shfl_up_sync(full, v.w, off);
+    if (lane >= off && cu == cid) { v.x += ux; v.y += uy; v.z += uz; v.w += uw; }
+  }
+  const int cn = __shfl_down_sync(full, cid, 1);
+  if (cid >= 0 && (lane == 31 || cn != cid)) {   // the last lane of its segment in this warp
+    double* s = reinterpret_cast<double*>(sums + cid);
+    atomicAdd(s, v.x); atomicAdd(s + 1, v.y); atomicAdd(s + 2, v.z); atomicAdd(s + 3, v.w);
+  }
+}
+
+// K15b': the fp32 centroids of the m cells (m = the last inclusive cell id), node count to info[0].
+__global__ void __launch_bounds__(256) k_cell_centroid(int64_t n, const int32_t* __restrict__ cid_incl,
+                                                       const double4* __restrict__ sums, float* __restrict__ g,
+                                                       int64_t* __restrict__ info) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t m = cid_incl[n - 1];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0) info[0] = m;
+  if (j >= m) return;
+  const double4 s = sums[j];
+  const double inv = 1.0 / s.w;
+  g[3 * j] = (float)(s.x * inv); g[3 * j + 1] = (float)(s.y * inv); g[3 * j + 2] = (float)(s.z * inv);
 }
 
 constexpr int kMaxRegenNbr = 16;
@@ -409,6 +435,8 @@ cudaError_t run_regen_centroids(Ctx* c, float grid, const int32_t* range, int sh
   CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
   CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
   CK(ensure(c, c->fl_xyz, n * 12));
+  CK(ensure(c, c->rg_sums, n * 32));
+  CK(cudaMemsetAsync(c->rg_sums.p, 0, n * 32, c->st));
   const int b = (int)((n + 255) / 256);
   ModelView A = model_view(c);
   launch_pdl(k_cell_keys, dim3(b), dim3(256), 0, c->st, A, grid, make_int3(range[0], range[1], range[2]), sh_x, sh_y,
@@ -421,9 +449,10 @@ cudaError_t run_regen_centroids(Ctx* c, float grid, const int32_t* range, int sh
   CK(cub_call(c, [&](void* t, size_t& s) {
     return cub::DeviceScan::InclusiveSum(t, s, c->flags.as<int32_t>(), c->scan.as<int32_t>(), (int)n, c->st);
   }));
-  launch_pdl(k_cell_centroid, dim3(b), dim3(256), 0, c->st, n, (const uint64_t*)c->keys2.as<uint64_t>(),
-             (const uint32_t*)c->vals2.as<uint32_t>(), (const int32_t*)c->scan.as<int32_t>(), A, c->fl_xyz.as<float>(),
-             info);
+  launch_pdl(k_cell_accum, dim3(b), dim3(256), 0, c->st, n, (const uint32_t*)c->vals2.as<uint32_t>(),
+             (const int32_t*)c->scan.as<int32_t>(), A, c->rg_sums.as<double4>());
+  launch_pdl(k_cell_centroid, dim3(b), dim3(256), 0, c->st, n, (const int32_t*)c->scan.as<int32_t>(),
+             (const double4*)c->rg_sums.as<double4>(), c->fl_xyz.as<float>(), info);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c->hpin, info, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
