@@ -39,7 +39,8 @@ class or_params(C.Structure):
                 ("eps_d", C.c_double), ("eps_n_deg", C.c_double),
                 ("tau_z", C.c_double), ("delta_deg", C.c_double), ("trunc", C.c_double), ("omega_max", C.c_double),
                 ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_double),
-                ("solve_mode", C.c_int32), ("lm", C.c_int32), ("lm_mu0", C.c_double)]
+                ("solve_mode", C.c_int32), ("lm", C.c_int32), ("lm_mu0", C.c_double),
+                ("joint_pose", C.c_int32), ("w_r", C.c_double), ("w_p", C.c_double)]
 
 
 class or_frame(C.Structure):
@@ -87,6 +88,18 @@ def lib():
                                    C.c_double, C.c_int32, C.c_int32, C.c_void_p]
             L.or_solve.restype = C.c_int32
             L.or_register.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_system_pose.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_int64,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_system_pose.restype = C.c_int64
+            L.or_residuals_pose.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+            L.or_residuals_pose.restype = C.c_int64
+            L.or_register_pose.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_euler_zyx.argtypes = [C.c_void_p, C.c_void_p]
+            L.or_pose_prior.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_pose_prior.restype = C.c_int32
             L.or_warp_model.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_fuse.argtypes = [P(or_params), P(or_model), P(or_frame), C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -118,7 +131,8 @@ def _i32(a):
 
 PAPER_DEFAULTS = dict(k=4, n_nbr=4, w_data=1.0, w_pt=1.0, w_reg=1e4, w_corr=10.0,
                       eps_d=15.0, eps_n_deg=10.0, tau_z=10.0, delta_deg=10.0, trunc=40.0, omega_max=10.0,
-                      gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1, lm=0, lm_mu0=1e-3)
+                      gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1, lm=0, lm_mu0=1e-3,
+                      joint_pose=0, w_r=1e6, w_p=1000.0)
 
 
 def set_threads(n: int) -> None:
@@ -266,6 +280,68 @@ def register(prm: or_params, pb: Problem, fr: Frame, Rt0=None, with_accepted=Fal
     if with_accepted:
         return Rt, E, na, acc
     return Rt, E, na
+
+
+# ---------------------------------------------------------------- NEXT-2: joint global pose
+def euler_zyx(O):
+    """ZYX Euler angles (yaw, pitch, roll) of a rotation matrix O = Rz Ry Rx."""
+    e = np.zeros(3)
+    lib().or_euler_zyx(_p(np.ascontiguousarray(O, np.float64).reshape(9)), _p(e))
+    return e
+
+
+def pose_prior(prior, cur):
+    """Eq. 10 residuals r (6) and Jacobian J (6x6) w.r.t. [dphi, dtau] (A37-A39); flag 1 = gimbal lock."""
+    r = np.zeros(6); J = np.zeros(36)
+    fl = lib().or_pose_prior(_p(np.ascontiguousarray(prior, np.float64)), _p(np.ascontiguousarray(cur, np.float64)),
+                             _p(r), _p(J))
+    return r, J.reshape(6, 6), int(fl)
+
+
+def system_pose(prm: or_params, pb: Problem, fr: Frame, Rt, pose_cur, fskin=None):
+    """Joint system over m + 1 unknowns (the pose last); energy[7]."""
+    m = pb.g.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    pc = np.ascontiguousarray(pose_cur, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    rhs = np.zeros(6 * (m + 1)); E = np.zeros(7); na = np.zeros(1, np.int64)
+    z = np.zeros(1, np.int32); zd = np.zeros(36)
+    nb = lib().or_system_pose(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pc), _p(fidx), _p(fw), 0,
+                              _p(z), _p(z), _p(zd), _p(rhs), _p(E), _p(na))
+    rows = np.zeros(nb, np.int32); cols = np.zeros(nb, np.int32); vals = np.zeros((nb, 36))
+    lib().or_system_pose(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pc), _p(fidx), _p(fw), nb,
+                         _p(rows), _p(cols), _p(vals), _p(rhs), _p(E), _p(na))
+    return dict(rows=rows, cols=cols, vals=vals.reshape(nb, 6, 6), rhs=rhs, energy=E, n_assoc=int(na[0]))
+
+
+def residuals_pose(prm: or_params, pb: Problem, fr: Frame, Rt, pose_cur, pix_frozen, fskin=None):
+    m = pb.g.shape[0]
+    Rt = np.ascontiguousarray(Rt, np.float64)
+    pc = np.ascontiguousarray(pose_cur, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    pix_frozen = _i32(pix_frozen)
+    cap = 4 * pb.xyz.shape[0] + 3 * m * pb.n_nbr + 3 * pb.fsrc.shape[0] + 6
+    r = np.zeros(cap); J = np.zeros((cap, 6 * (m + 1)))
+    nr = lib().or_residuals_pose(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pc), _p(pix_frozen),
+                                 _p(fidx), _p(fw), cap, _p(r), _p(J))
+    assert nr >= 0
+    return r[:nr], J[:nr]
+
+
+def register_pose(prm: or_params, pb: Problem, fr: Frame, Rt0=None, pose0=None, with_accepted=False):
+    """Joint registration: returns (Rt, pose, E (G+1 x 7), n_assoc[, accepted]); pose0 defaults to the prior."""
+    m = pb.g.shape[0]
+    Rt = identity_state(m) if Rt0 is None else np.array(Rt0, np.float64, copy=True)
+    pose = np.array(fr.s.pose[:] if pose0 is None else pose0, np.float64)
+    G = prm.gn_iters
+    E = np.zeros((G + 1, 7)); na = np.zeros(G + 1, np.int64)
+    acc = np.zeros(G + 1, np.int32)
+    lib().or_register_pose(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(Rt), _p(pose), _p(E), _p(na), _p(acc))
+    if with_accepted:
+        return Rt, pose, E, na, acc
+    return Rt, pose, E, na
 
 
 def warp_model(pb: Problem, Rt):

@@ -213,9 +213,9 @@ struct System {
   int m;
   std::map<std::pair<int, int>, B6> blk;
   std::vector<double> rhs;
-  double E[4];
+  double E[6];       // E_data, E_pt, E_reg, E_corr, E_r, E_p (the last two: NEXT-2 only)
   int64_t n_assoc;
-  explicit System(int m_) : m(m_), rhs(6 * m_, 0.0), n_assoc(0) { E[0] = E[1] = E[2] = E[3] = 0; }
+  explicit System(int m_) : m(m_), rhs(6 * m_, 0.0), n_assoc(0) { for (int a = 0; a < 6; ++a) E[a] = 0; }
   // H += w * Ja^T Jb for rows r (Ja: rows x 6 for node a, Jb for node b)
   void add_pair(int a, const double* Ja, int b, const double* Jb, int rows, double w) {
     if (a <= b) {
@@ -316,25 +316,97 @@ void wraw_of(const or_problem* p, int k, int64_t i, double* wr) {
 }
 
 // O3a-d, O3g for the points [i0, i1): data (Eq. 8) and dense point-to-point terms
-void assemble_points(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt, int64_t i0,
-                     int64_t i1, System* S) {
+// ---- NEXT-2 (Eq. 10): pose priors.  Scope orientation O = R^T (R world->camera)
+// as ZYX Euler angles O = Rz(psi) Ry(theta) Rx(phi) ("ZYX", A38); scope position
+// c = -R^T T, the camera centre in the world frame (A39).
+V3 euler_zyx(const M3& O) {
+  double s = -O[6];
+  s = s > 1.0 ? 1.0 : (s < -1.0 ? -1.0 : s);
+  return v3(std::atan2(O[3], O[0]), std::asin(s), std::atan2(O[7], O[8]));
+}
+double wrap_pi(double a) {   // to (-pi, pi]
+  while (a > M_PI) a -= 2.0 * M_PI;
+  while (a <= -M_PI) a += 2.0 * M_PI;
+  return a;
+}
+M3 transpose(const M3& A) {
+  M3 T;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) T[3 * i + j] = A[3 * j + i];
+  return T;
+}
+// r = [wrap(e(O) - e(O0)); c - c0], J = d r / d[dphi, dtau] (6x6 row-major) under A37's increment:
+//  O' = Exp(dphi)^T O = Exp(-dphi) O, a left (spatial) rotation by -dphi, and d e = E_s^-1 omega
+//  with E_s = [e_z, Rz(psi) e_y, Rz(psi) Ry(theta) e_x] (the Euler rates -> angular velocity map);
+//  c' = -Exp(-dphi)(R^T T + dtau) = c - dtau + [c]x dphi to first order.
+// Returns 1 (E_r rows zeroed) at gimbal lock |cos theta| < 1e-6.
+int pose_prior(const double* prior, const double* cur, double* r, double* J) {
+  const M3 O = transpose(pose_R(cur)), O0 = transpose(pose_R(prior));
+  const V3 e = euler_zyx(O), e0 = euler_zyx(O0);
+  const V3 c = scale(mulT(pose_R(cur), pose_T(cur)), -1.0), c0 = scale(mulT(pose_R(prior), pose_T(prior)), -1.0);
+  for (int a = 0; a < 36; ++a) J[a] = 0.0;
+  for (int a = 0; a < 3; ++a) { r[a] = wrap_pi(e[a] - e0[a]); r[3 + a] = c[a] - c0[a]; }
+  // E_p rows: [ [c]x , -I ]
+  const double C[9] = {0, -c[2], c[1], c[2], 0, -c[0], -c[1], c[0], 0};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      J[6 * (3 + i) + j] = C[3 * i + j];
+      J[6 * (3 + i) + 3 + j] = (i == j) ? -1.0 : 0.0;
+    }
+  const double cps = std::cos(e[0]), sps = std::sin(e[0]), cth = std::cos(e[1]), sth = std::sin(e[1]);
+  if (std::fabs(cth) < 1e-6) { r[0] = r[1] = r[2] = 0.0; return 1; }
+  // E_s (columns e_z, Rz e_y, Rz Ry e_x), inverted by the 3x3 adjugate
+  const double Es[9] = {0.0, -sps, cps * cth,
+                        0.0, cps, sps * cth,
+                        1.0, 0.0, -sth};
+  double inv[9];
+  const double det = Es[0] * (Es[4] * Es[8] - Es[5] * Es[7]) - Es[1] * (Es[3] * Es[8] - Es[5] * Es[6]) +
+                     Es[2] * (Es[3] * Es[7] - Es[4] * Es[6]);
+  inv[0] = (Es[4] * Es[8] - Es[5] * Es[7]) / det; inv[1] = (Es[2] * Es[7] - Es[1] * Es[8]) / det;
+  inv[2] = (Es[1] * Es[5] - Es[2] * Es[4]) / det; inv[3] = (Es[5] * Es[6] - Es[3] * Es[8]) / det;
+  inv[4] = (Es[0] * Es[8] - Es[2] * Es[6]) / det; inv[5] = (Es[2] * Es[3] - Es[0] * Es[5]) / det;
+  inv[6] = (Es[3] * Es[7] - Es[4] * Es[6]) / det; inv[7] = (Es[1] * Es[6] - Es[0] * Es[7]) / det;
+  inv[8] = (Es[0] * Es[4] - Es[1] * Es[3]) / det;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) J[6 * i + j] = -inv[3 * i + j];   // omega = -dphi
+  return 0;
+}
+
+// NEXT-2 (A37): with the pose unknown, v~ = R (Exp(dphi) x_hat + dtau) + T, so
+// dv~/d[dphi, dtau] = R [-[x_hat]x, I]: the pose enters every point / feature row like a node
+// of weight 1 with a = x_hat; its rows are appended as slot k with unknown id m.
+void pose_slot_rows(const M3& R, const Warped& w, const Assoc* as, double* Jpl, double* Jpt) {
+  if (as) {
+    V3 np = mulT(R, as->N);
+    V3 c = cross(w.x_hat, np);
+    for (int i = 0; i < 3; ++i) { Jpl[i] = c[i]; Jpl[3 + i] = np[i]; }
+  }
+  jac_point(R, 1.0, w.x_hat, Jpt);
+}
+
+void assemble_points(const or_params* prm, const or_problem* p, const or_frame* f, const double* pose,
+                     const double* Rt, int64_t i0, int64_t i1, System* S) {
   const int k = prm->k;
-  M3 R = pose_R(f->pose);
-  double Jpl[8 * 6], Jpt[8 * 18], rpl, rpt[3];
+  const int ks = k + (prm->joint_pose ? 1 : 0);   // slots incl. the pose (unknown m)
+  M3 R = pose_R(pose);
+  double Jpl[9 * 6], Jpt[9 * 18], rpl, rpt[3];
+  int32_t ids[9];
   for (int64_t i = i0; i < i1; ++i) {
     double wr[8];
     wraw_of(p, k, i, wr);
-    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, pose);
     Assoc as = associate_point(prm, f, w);
     if (as.pix < 0) continue;
     S->n_assoc++;
     point_rows(R, w, as, k, Jpl, Jpt, &rpl, rpt);
+    for (int a = 0; a < k; ++a) ids[a] = p->idx[k * i + a];
+    if (ks > k) { pose_slot_rows(R, w, &as, Jpl + 6 * k, Jpt + 18 * k); ids[k] = p->m; }
     S->E[0] += rpl * rpl;
     S->E[1] += rpt[0] * rpt[0] + rpt[1] * rpt[1] + rpt[2] * rpt[2];
-    for (int a = 0; a < k; ++a) {
-      int ja = p->idx[k * i + a];
-      for (int b = 0; b < k; ++b) {
-        int jb = p->idx[k * i + b];
+    for (int a = 0; a < ks; ++a) {
+      int ja = ids[a];
+      for (int b = 0; b < ks; ++b) {
+        int jb = ids[b];
         if (ja > jb || (ja == jb && a > b)) continue;   // each unordered slot pair once
         S->add_pair(ja, Jpl + 6 * a, jb, Jpl + 6 * b, 1, prm->w_data);
         S->add_pair(ja, Jpt + 18 * a, jb, Jpt + 18 * b, 3, prm->w_pt);
@@ -349,22 +421,22 @@ void assemble_points(const or_params* prm, const or_problem* p, const or_frame* 
   }
 }
 
-void assemble(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+void assemble(const or_params* prm, const or_problem* p, const or_frame* f, const double* pose, const double* Rt,
               const int32_t* fidx, const double* fw, System* S) {
   const int k = prm->k;
   if (g_threads <= 1) {
-    assemble_points(prm, p, f, Rt, 0, p->n, S);
+    assemble_points(prm, p, f, pose, Rt, 0, p->n, S);
   } else {   // T contiguous point ranges, merged in range order
     const int T = g_threads;
-    std::vector<System> part(T, System(p->m));
+    std::vector<System> part(T, System(S->m));
 #pragma omp parallel for num_threads(T) schedule(static, 1)
-    for (int t = 0; t < T; ++t) assemble_points(prm, p, f, Rt, p->n * t / T, p->n * (t + 1) / T, &part[t]);
+    for (int t = 0; t < T; ++t) assemble_points(prm, p, f, pose, Rt, p->n * t / T, p->n * (t + 1) / T, &part[t]);
     for (int t = 0; t < T; ++t) {
       for (const auto& kv : part[t].blk) {
         B6& B = S->blk[kv.first];
         for (int a = 0; a < 36; ++a) B[a] += kv.second[a];
       }
-      for (int i = 0; i < 6 * p->m; ++i) S->rhs[i] += part[t].rhs[i];
+      for (int i = 0; i < 6 * S->m; ++i) S->rhs[i] += part[t].rhs[i];
       for (int a = 0; a < 4; ++a) S->E[a] += part[t].E[a];
       S->n_assoc += part[t].n_assoc;
     }
@@ -383,16 +455,20 @@ void assemble(const or_params* prm, const or_problem* p, const or_frame* f, cons
       S->add_rhs(j, Jj, e, 3, prm->w_reg);
       S->add_rhs(l, Jl, e, 3, prm->w_reg);
     }
-  // O3f: features
-  double Jf[8 * 18];
+  // O3f: features (NEXT-2: plus the pose slot, A37)
+  const int ks = k + (prm->joint_pose ? 1 : 0);
+  double Jf[9 * 18];
+  int32_t ids[9];
   for (int q = 0; q < p->nf; ++q) {
     Warped w;
-    if (!feature_rows(p, k, Rt, f->pose, q, fidx, fw, &w, e, Jf)) continue;
+    if (!feature_rows(p, k, Rt, pose, q, fidx, fw, &w, e, Jf)) continue;
+    for (int a = 0; a < k; ++a) ids[a] = fidx[k * q + a];
+    if (ks > k) { pose_slot_rows(pose_R(pose), w, nullptr, nullptr, Jf + 18 * k); ids[k] = p->m; }
     S->E[3] += e[0] * e[0] + e[1] * e[1] + e[2] * e[2];
-    for (int a = 0; a < k; ++a) {
-      int ja = fidx[k * q + a];
-      for (int b = 0; b < k; ++b) {
-        int jb = fidx[k * q + b];
+    for (int a = 0; a < ks; ++a) {
+      int ja = ids[a];
+      for (int b = 0; b < ks; ++b) {
+        int jb = ids[b];
         if (ja > jb || (ja == jb && a > b)) continue;
         S->add_pair(ja, Jf + 18 * a, jb, Jf + 18 * b, 3, prm->w_corr);
         if (ja == jb && a != b) S->add_pair(jb, Jf + 18 * b, ja, Jf + 18 * a, 3, prm->w_corr);
@@ -400,10 +476,23 @@ void assemble(const or_params* prm, const or_problem* p, const or_frame* f, cons
       S->add_rhs(ja, Jf + 18 * a, e, 3, prm->w_corr);
     }
   }
+  // NEXT-2: the pose priors of Eq. 10 on unknown m (A38-A39)
+  if (prm->joint_pose) {
+    double r[6], J[36];
+    pose_prior(f->pose, pose, r, J);
+    S->E[4] = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+    S->E[5] = r[3] * r[3] + r[4] * r[4] + r[5] * r[5];
+    S->add_pair(p->m, J, p->m, J, 3, prm->w_r);
+    S->add_pair(p->m, J + 18, p->m, J + 18, 3, prm->w_p);
+    S->add_rhs(p->m, J, r, 3, prm->w_r);
+    S->add_rhs(p->m, J + 18, r + 3, 3, prm->w_p);
+  }
 }
 
 double total_energy(const or_params* prm, const double* E) {
-  return prm->w_data * E[0] + prm->w_pt * E[1] + prm->w_reg * E[2] + prm->w_corr * E[3];
+  double s = prm->w_data * E[0] + prm->w_pt * E[1] + prm->w_reg * E[2] + prm->w_corr * E[3];
+  if (prm->joint_pose) s += prm->w_r * E[4] + prm->w_p * E[5];
+  return s;
 }
 
 // ---- linear algebra for O3h
@@ -552,6 +641,29 @@ void update_nodes(int m, const std::vector<double>& x, double* Rt) {
   }
 }
 
+// NEXT-2, A37: R <- R Exp(dphi), T <- T + R dtau (x[0..6) = [dphi, dtau])
+void update_pose(const double* x, double* pose) {
+  double w[3] = {x[0], x[1], x[2]}, E[9];
+  or_exp(w, E);
+  M3 Em, R = pose_R(pose);
+  for (int a = 0; a < 9; ++a) Em[a] = E[a];
+  const V3 dT = mul(R, v3(x[3], x[4], x[5]));
+  M3 Rn = matmul(R, Em);
+  for (int a = 0; a < 9; ++a) pose[a] = Rn[a];
+  for (int a = 0; a < 3; ++a) pose[9 + a] += dT[a];
+}
+
+int n_unknown_blocks(const or_params* prm, const or_problem* p) { return p->m + (prm->joint_pose ? 1 : 0); }
+
+int64_t system_impl(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                    const double* pose, const int32_t* fidx, const double* fw, int64_t cap, int32_t* brow,
+                    int32_t* bcol, double* bval, double* rhs, double* energy, int64_t* n_assoc);
+int64_t residuals_impl(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                       const double* pose, const int32_t* pix_frozen, const int32_t* fidx, const double* fw,
+                       int64_t cap_rows, double* r, double* J);
+void register_impl(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt, double* pose,
+                   double* energy, int64_t* n_assoc, int32_t* accepted);
+
 void feature_skin(const or_problem* p, int k, std::vector<int32_t>& fidx, std::vector<double>& fw) {
   fidx.assign((size_t)k * p->nf, 0);
   fw.assign((size_t)k * p->nf, 0.0);
@@ -638,8 +750,32 @@ int64_t or_system(const or_params* prm, const or_problem* p, const or_frame* f, 
                   const int32_t* fidx, const double* fw, int64_t cap,
                   int32_t* brow, int32_t* bcol, double* bval, double* rhs, double energy[5],
                   int64_t* n_assoc) {
-  System S(p->m);
-  assemble(prm, p, f, Rt, fidx, fw, &S);
+  or_params q = *prm;
+  q.joint_pose = 0;
+  double E7[7];
+  const int64_t nb = system_impl(&q, p, f, Rt, f->pose, fidx, fw, cap, brow, bcol, bval, rhs, E7, n_assoc);
+  for (int a = 0; a < 4; ++a) energy[a] = E7[a];
+  energy[4] = E7[6];
+  return nb;
+}
+
+int64_t or_system_pose(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                       const double pose_cur[12], const int32_t* fidx, const double* fw, int64_t cap,
+                       int32_t* brow, int32_t* bcol, double* bval, double* rhs, double energy[7],
+                       int64_t* n_assoc) {
+  or_params q = *prm;
+  q.joint_pose = 1;
+  return system_impl(&q, p, f, Rt, pose_cur, fidx, fw, cap, brow, bcol, bval, rhs, energy, n_assoc);
+}
+
+}  // extern "C"
+
+namespace {
+int64_t system_impl(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                    const double* pose, const int32_t* fidx, const double* fw, int64_t cap, int32_t* brow,
+                    int32_t* bcol, double* bval, double* rhs, double* energy, int64_t* n_assoc) {
+  System S(n_unknown_blocks(prm, p));
+  assemble(prm, p, f, pose, Rt, fidx, fw, &S);
   int64_t nb = 0;
   for (std::map<std::pair<int, int>, B6>::const_iterator it = S.blk.begin(); it != S.blk.end(); ++it, ++nb) {
     if (nb >= cap) continue;
@@ -647,18 +783,39 @@ int64_t or_system(const or_params* prm, const or_problem* p, const or_frame* f, 
     bcol[nb] = it->first.second;
     for (int a = 0; a < 36; ++a) bval[36 * nb + a] = it->second[a];
   }
-  for (int i = 0; i < 6 * p->m; ++i) rhs[i] = S.rhs[i];
-  for (int a = 0; a < 4; ++a) energy[a] = S.E[a];
-  energy[4] = total_energy(prm, S.E);
+  for (int i = 0; i < 6 * S.m; ++i) rhs[i] = S.rhs[i];
+  for (int a = 0; a < 6; ++a) energy[a] = S.E[a];
+  energy[6] = total_energy(prm, S.E);
   *n_assoc = S.n_assoc;
   return nb;
 }
+}  // namespace
 
+extern "C" {
 int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
                      const int32_t* pix_frozen, const int32_t* fidx, const double* fw,
                      int64_t cap_rows, double* r, double* J) {
-  const int k = prm->k, ncol = 6 * p->m;
-  M3 R = pose_R(f->pose);
+  or_params q = *prm;
+  q.joint_pose = 0;
+  return residuals_impl(&q, p, f, Rt, f->pose, pix_frozen, fidx, fw, cap_rows, r, J);
+}
+
+int64_t or_residuals_pose(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                          const double pose_cur[12], const int32_t* pix_frozen, const int32_t* fidx,
+                          const double* fw, int64_t cap_rows, double* r, double* J) {
+  or_params q = *prm;
+  q.joint_pose = 1;
+  return residuals_impl(&q, p, f, Rt, pose_cur, pix_frozen, fidx, fw, cap_rows, r, J);
+}
+}  // extern "C"
+
+namespace {
+int64_t residuals_impl(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                       const double* pose, const int32_t* pix_frozen, const int32_t* fidx, const double* fw,
+                       int64_t cap_rows, double* r, double* J) {
+  const int k = prm->k, ncol = 6 * n_unknown_blocks(prm, p);
+  const bool joint = prm->joint_pose != 0;
+  M3 R = pose_R(pose);
   int64_t row = 0;
   double Jpl[8 * 6], Jpt[8 * 18], rpl, rpt[3];
   const double sd = std::sqrt(prm->w_data), sp = std::sqrt(prm->w_pt);
@@ -667,7 +824,7 @@ int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* 
     if (pix_frozen[i] < 0) continue;
     double wr[8];
     wraw_of(p, k, i, wr);
-    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, f->pose);
+    Warped w = warp_point(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, Rt, pose);
     if (!w.ok) continue;
     Assoc as;
     int px = pix_frozen[i] % f->W, py = pix_frozen[i] / f->W;
@@ -684,6 +841,15 @@ int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* 
       for (int c = 0; c < 6; ++c) {
         J0[6 * j + c] += sd * Jpl[6 * s + c];
         for (int q = 0; q < 3; ++q) J0[(size_t)(1 + q) * ncol + 6 * j + c] += sp * Jpt[18 * s + 6 * q + c];
+      }
+    }
+    if (joint) {   // pose columns (A37)
+      double Jplp[6], Jptp[18];
+      pose_slot_rows(R, w, &as, Jplp, Jptp);
+      const int j = p->m;
+      for (int c = 0; c < 6; ++c) {
+        J0[6 * j + c] += sd * Jplp[c];
+        for (int q = 0; q < 3; ++q) J0[(size_t)(1 + q) * ncol + 6 * j + c] += sp * Jptp[6 * q + c];
       }
     }
     row += 4;
@@ -709,21 +875,41 @@ int64_t or_residuals(const or_params* prm, const or_problem* p, const or_frame* 
   double Jf[8 * 18];
   for (int q = 0; q < p->nf; ++q) {
     Warped w;
-    if (!feature_rows(p, k, Rt, f->pose, q, fidx, fw, &w, e, Jf)) continue;
+    if (!feature_rows(p, k, Rt, pose, q, fidx, fw, &w, e, Jf)) continue;
     if (row + 3 > cap_rows) return -1;
     double* J0 = J + (size_t)row * ncol;
     std::memset(J0, 0, sizeof(double) * 3 * ncol);
+    double Jfp[18];
+    if (joint) pose_slot_rows(R, w, nullptr, nullptr, Jfp);
     for (int a = 0; a < 3; ++a) {
       r[row + a] = sc * e[a];
       for (int s = 0; s < k; ++s) {
         int j = fidx[k * q + s];
         for (int c = 0; c < 6; ++c) J0[(size_t)a * ncol + 6 * j + c] += sc * Jf[18 * s + 6 * a + c];
       }
+      if (joint)
+        for (int c = 0; c < 6; ++c) J0[(size_t)a * ncol + 6 * p->m + c] += sc * Jfp[6 * a + c];
     }
     row += 3;
   }
+  if (joint) {   // Eq. 10 prior rows (A38-A39), last
+    double rr[6], Jp[36];
+    pose_prior(f->pose, pose, rr, Jp);
+    if (row + 6 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 6 * ncol);
+    for (int a = 0; a < 6; ++a) {
+      const double sw = std::sqrt(a < 3 ? prm->w_r : prm->w_p);
+      r[row + a] = sw * rr[a];
+      for (int c = 0; c < 6; ++c) J0[(size_t)a * ncol + 6 * p->m + c] = sw * Jp[6 * a + c];
+    }
+    row += 6;
+  }
   return row;
 }
+}  // namespace
+
+extern "C" {
 
 int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
                  const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x) {
@@ -741,60 +927,107 @@ int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bc
 
 void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
                  double* energy, int64_t* n_assoc, int32_t* accepted) {
+  or_params q = *prm;
+  q.joint_pose = 0;
+  double pose[12];
+  for (int a = 0; a < 12; ++a) pose[a] = f->pose[a];
+  std::vector<double> E7(7 * (size_t)(prm->gn_iters + 1));
+  register_impl(&q, p, f, Rt, pose, E7.data(), n_assoc, accepted);
+  for (int it = 0; it <= prm->gn_iters; ++it) {
+    for (int a = 0; a < 4; ++a) energy[5 * it + a] = E7[7 * it + a];
+    energy[5 * it + 4] = E7[7 * it + 6];
+  }
+}
+
+void or_register_pose(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt, double* pose_io,
+                      double* energy, int64_t* n_assoc, int32_t* accepted) {
+  or_params q = *prm;
+  q.joint_pose = 1;
+  register_impl(&q, p, f, Rt, pose_io, energy, n_assoc, accepted);
+}
+
+void or_euler_zyx(const double O[9], double e[3]) {
+  M3 M;
+  for (int a = 0; a < 9; ++a) M[a] = O[a];
+  V3 v = euler_zyx(M);
+  for (int a = 0; a < 3; ++a) e[a] = v[a];
+}
+
+int32_t or_pose_prior(const double prior[12], const double cur[12], double r[6], double J[36]) {
+  return pose_prior(prior, cur, r, J);
+}
+}  // extern "C"
+
+namespace {
+// O3 (+ NEXT-2 when prm->joint_pose): fixed-G Gauss-Newton or LM over the nodes and, jointly,
+// the pose (unknown m); energy rows of 7 (E_data, E_pt, E_reg, E_corr, E_r, E_p, total).
+void register_impl(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt, double* pose,
+                   double* energy, int64_t* n_assoc, int32_t* accepted) {
   std::vector<int32_t> fidx;
   std::vector<double> fw;
   feature_skin(p, prm->k, fidx, fw);   // O1 on the (fixed) node positions
+  const int nu = n_unknown_blocks(prm, p);
+  auto step = [&](const std::vector<double>& x) {
+    update_nodes(p->m, x, Rt);
+    if (prm->joint_pose) update_pose(x.data() + 6 * p->m, pose);
+  };
+  auto record = [&](int it, const System& S) {
+    for (int a = 0; a < 6; ++a) energy[7 * it + a] = S.E[a];
+    energy[7 * it + 6] = total_energy(prm, S.E);
+    n_assoc[it] = S.n_assoc;
+  };
   if (!prm->lm) {
     for (int it = 0; it <= prm->gn_iters; ++it) {
-      System S(p->m);
-      assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);
-      for (int a = 0; a < 4; ++a) energy[5 * it + a] = S.E[a];
-      energy[5 * it + 4] = total_energy(prm, S.E);
-      n_assoc[it] = S.n_assoc;
+      System S(nu);
+      assemble(prm, p, f, pose, Rt, fidx.data(), fw.data(), &S);
+      record(it, S);
       if (accepted) accepted[it] = 1;
       if (it == prm->gn_iters) break;   // final energy only
       std::vector<double> x;
       solve_system(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
-      update_nodes(p->m, x, Rt);
+      step(x);
     }
     return;
   }
   // Levenberg-Marquardt, Marquardt damping H + mu diag(H) (R-A29)
   const size_t ns = 12 * (size_t)p->m;
   std::vector<double> base(Rt, Rt + ns);   // last accepted state
-  System acc(p->m);                        // its normal equations
+  std::vector<double> base_pose(pose, pose + 12);
+  System acc(nu);                          // its normal equations
   double E_acc = 0.0, mu = prm->lm_mu0;
   for (int it = 0; it <= prm->gn_iters; ++it) {
-    System S(p->m);
-    assemble(prm, p, f, Rt, fidx.data(), fw.data(), &S);   // at the trial state
-    for (int a = 0; a < 4; ++a) energy[5 * it + a] = S.E[a];
+    System S(nu);
+    assemble(prm, p, f, pose, Rt, fidx.data(), fw.data(), &S);   // at the trial state
+    record(it, S);
     const double E = total_energy(prm, S.E);
-    energy[5 * it + 4] = E;
-    n_assoc[it] = S.n_assoc;
     const bool ok = it == 0 || E < E_acc;
     if (accepted) accepted[it] = ok ? 1 : 0;
     if (ok) {
       std::copy(Rt, Rt + ns, base.begin());
+      std::copy(pose, pose + 12, base_pose.begin());
       acc = S;
       E_acc = E;
       if (it > 0) mu *= 0.5;
     } else {
       std::copy(base.begin(), base.end(), Rt);
+      std::copy(base_pose.begin(), base_pose.end(), pose);
       mu *= 10.0;
     }
     if (it == prm->gn_iters) break;   // the final trial is only evaluated
     System D = acc;                   // damped copy: diagonal entries of H times (1 + mu)
-    for (int j = 0; j < p->m; ++j) {
+    for (int j = 0; j < nu; ++j) {
       std::map<std::pair<int, int>, B6>::iterator d = D.blk.find(std::make_pair(j, j));
       if (d != D.blk.end())
         for (int a = 0; a < 6; ++a) d->second[7 * a] *= 1.0 + mu;
     }
     std::vector<double> x;
     solve_system(D, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
-    update_nodes(p->m, x, Rt);   // Rt == base here: the step starts from the accepted state
+    step(x);   // Rt == base here: the step starts from the accepted state
   }
 }
+}  // namespace
 
+extern "C" {
 void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
                    double* g_out) {
   double pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};

@@ -28,7 +28,16 @@ typedef struct {
   int32_t solve_mode;                   /* 0 = EXACT, 1 = MIRROR (same P as GPU)     */
   int32_t lm;                           /* 1: Levenberg-Marquardt, R-A29 */
   double lm_mu0;                        /* initial Marquardt damping (1e-3)    */
+  int32_t joint_pose;                   /* 1: joint global-pose refinement (NEXT-2, below) */
+  double w_r, w_p;                      /* Eq. 10 prior weights, P:598 (1e6, 1000)    */
 } or_params;
+/* joint_pose (NEXT-2, readings A37-A40): the pose of Eq. 1 becomes unknown
+ * number m (after the m nodes; "only 6 more variables") with the local increment
+ * R <- R Exp(dphi), T <- T + R dtau (A37); or_frame.pose is both its start value and the
+ * ORB-SLAM prior of Eq. 10: E_r = |wrap(euler_zyx(R^T) - euler_zyx(R0^T))|^2 (scope
+ * orientation as yaw-pitch-roll, A38), E_p = |c - c0|^2 with the scope position
+ * c = -R^T T (A39).  Energy rows then have 7 entries: E_data, E_pt, E_reg, E_corr, E_r,
+ * E_p, weighted total. */
 
 typedef struct {
   int32_t W, H;
@@ -105,6 +114,27 @@ int32_t or_solve(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bc
  * accepted (G+1) may be NULL. */
 void or_register(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt,
                  double* energy, int64_t* n_assoc, int32_t* accepted);
+/* ---- NEXT-2: joint global pose (see or_params.joint_pose) ---- */
+/* ZYX Euler angles (yaw psi, pitch theta, roll phi) of a rotation O = Rz(psi) Ry(theta) Rx(phi). */
+void or_euler_zyx(const double O[9], double e[3]);
+/* Eq. 10 prior residuals at the current pose cur (world->camera R row-major 9, T 3) against
+ * prior: r[0..3) = wrap(euler_zyx(R^T) - euler_zyx(R0^T)), r[3..6) = c - c0, c = -R^T T;
+ * J (6x6 row-major) w.r.t. [dphi, dtau] of A37.  Returns 0, or 1 at gimbal lock
+ * (|cos theta| < 1e-6: the E_r rows are zero). */
+int32_t or_pose_prior(const double prior[12], const double cur[12], double r[6], double J[36]);
+/* or_system / or_residuals / or_register with the pose: pose_cur (12) is the current pose
+ * (or_frame.pose the prior); blocks over m + 1 unknowns (the pose is unknown m), rhs 6(m+1),
+ * energy[7]; J: rows x 6(m+1) incl. the 6 sqrt-weighted prior rows (last).  or_register_pose:
+ * pose_io = start pose on entry (normally the prior), the refined pose on exit; energy (G+1)*7. */
+int64_t or_system_pose(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                       const double pose_cur[12], const int32_t* fidx, const double* fw, int64_t cap,
+                       int32_t* brow, int32_t* bcol, double* bval, double* rhs, double energy[7],
+                       int64_t* n_assoc);
+int64_t or_residuals_pose(const or_params* prm, const or_problem* p, const or_frame* f, const double* Rt,
+                          const double pose_cur[12], const int32_t* pix_frozen, const int32_t* fidx,
+                          const double* fw, int64_t cap_rows, double* r, double* J);
+void or_register_pose(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt, double* pose_io,
+                      double* energy, int64_t* n_assoc, int32_t* accepted);
 /* O4: apply the field: live world state x_hat, unit normals; advanced nodes g+t. */
 void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
                    double* g_out);

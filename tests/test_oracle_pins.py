@@ -1004,3 +1004,179 @@ def test_regen_uniform_cube_brute_force(seed):
         order = np.lexsort((np.arange(g.shape[0]), D[j]))[:6]
         assert (nbr[j] == order).all()
     assert (mg >= 0).all()
+
+
+# ------------------------------------------------------------------ NEXT-2: joint global pose (Eq. 10, A37-A39)
+def _Rz(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, -s, 0], [s, c, 0], [0, 0, 1.0]])
+
+
+def _Ry(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, 0, s], [0, 1.0, 0], [-s, 0, c]])
+
+
+def _Rx(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[1.0, 0, 0], [0, c, -s], [0, s, c]])
+
+
+def _scope(yaw, pitch, roll):
+    """Textbook ZYX composition O = Rz(yaw) Ry(pitch) Rx(roll) (radians)."""
+    return _Rz(yaw) @ _Ry(pitch) @ _Rx(roll)
+
+
+def _pose_increment(pose, x):
+    """A37's increment, written out: R <- R Exp(dphi), T <- T + R dtau."""
+    R = pose[:9].reshape(3, 3)
+    return np.concatenate([(R @ O.exp_so3(x[:3])).ravel(), pose[9:] + R @ x[3:6]])
+
+
+def _random_pose(rng, rot_deg=8.0, trans=5.0):
+    O_ = _scope(*np.deg2rad(rng.uniform(-rot_deg, rot_deg, 3)))
+    return np.concatenate([O_.T.ravel(), rng.normal(0, trans, 3)])
+
+
+def test_pose_euler_zyx_textbook():
+    rng = np.random.default_rng(2001)
+    for _ in range(50):
+        e = np.array([rng.uniform(-np.pi, np.pi), rng.uniform(-1.5, 1.5), rng.uniform(-np.pi, np.pi)])
+        assert np.abs(O.euler_zyx(_scope(*e)) - e).max() < 1e-12
+    assert np.abs(O.euler_zyx(_Rz(0.3))).max() - 0.3 < 1e-15
+
+
+def test_pose_prior_golden():
+    for c in GOLD["pose_prior"]["cases"]:
+        pri = np.concatenate([_scope(*np.deg2rad(c["prior_R_deg_zyx"])).T.ravel(), c["prior_T"]])
+        cur = np.concatenate([_scope(*np.deg2rad(c["cur_R_deg_zyx"])).T.ravel(), c["cur_T"]])
+        r, J, fl = O.pose_prior(pri, cur)
+        assert fl == 0 and np.abs(r - np.array(c["r"])).max() < 1e-12, (c["what"], r)
+
+
+def test_pose_prior_jacobian_finite_differences():
+    rng = np.random.default_rng(2002)
+    h = 1e-6
+    for _ in range(20):
+        pri, cur = _random_pose(rng), _random_pose(rng)
+        r, J, fl = O.pose_prior(pri, cur)
+        Jfd = np.zeros((6, 6))
+        for c in range(6):
+            e = np.zeros(6); e[c] = h
+            Jfd[:, c] = (O.pose_prior(pri, _pose_increment(cur, e))[0] - O.pose_prior(pri, _pose_increment(cur, -e))[0]) / (2 * h)
+        assert np.abs(J - Jfd).max() < 1e-6 * max(1.0, np.abs(J).max()), np.abs(J - Jfd).max()
+
+
+def test_pose_prior_gimbal_lock_flag():
+    cur = np.concatenate([_scope(0.2, np.pi / 2, 0.1).T.ravel(), np.zeros(3)])
+    r, J, fl = O.pose_prior(pose12(), cur)
+    assert fl == 1 and np.abs(r[:3]).max() == 0 and np.abs(J[:3]).max() == 0
+
+
+def _joint_fd(prm, pb, fr, Rt, pose, h=1e-5):
+    pix, _, _ = O.associate(prm, pb, fr, Rt)   # frozen at the prior's association (a smooth function)
+    fsk = O.feature_skin(pb)[:2]
+    r0, J = O.residuals_pose(prm, pb, fr, Rt, pose, pix, fsk)
+    m = pb.g.shape[0]
+    Jfd = np.zeros_like(J)
+    for j in range(m):
+        for c in range(6):
+            rp, _ = O.residuals_pose(prm, pb, fr, apply_perturbation(Rt, j, c, h), pose, pix, fsk)
+            rm, _ = O.residuals_pose(prm, pb, fr, apply_perturbation(Rt, j, c, -h), pose, pix, fsk)
+            Jfd[:, 6 * j + c] = (rp - rm) / (2 * h)
+    for c in range(6):
+        e = np.zeros(6); e[c] = h
+        rp, _ = O.residuals_pose(prm, pb, fr, Rt, _pose_increment(pose, e), pix, fsk)
+        rm, _ = O.residuals_pose(prm, pb, fr, Rt, _pose_increment(pose, -e), pix, fsk)
+        Jfd[:, 6 * m + c] = (rp - rm) / (2 * h)
+    return J, Jfd, pix
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_pose_joint_finite_difference_jacobians_small(seed):
+    prm, pb, fr, Rt = _small_problem(seed)
+    prm.joint_pose = 1
+    prm.w_r, prm.w_p = 3.0, 2.0   # O(1) weights so that every block of J is visible in the max-norm
+    pose = _pose_increment(np.array(fr.s.pose[:]), np.random.default_rng(700 + seed).normal(0, [0.003] * 3 + [0.2] * 3))
+    J, Jfd, pix = _joint_fd(prm, pb, fr, Rt, pose)
+    m = pb.g.shape[0]
+    assert (pix >= 0).sum() >= 5
+    assert np.abs(J[:, 6 * m:]).max() > 0
+    rel = np.abs(J - Jfd).max() / np.abs(J).max()
+    assert rel < 1e-4, rel
+    relp = np.abs(J[:, 6 * m:] - Jfd[:, 6 * m:]).max() / np.abs(J[:, 6 * m:]).max()
+    assert relp < 1e-4, relp
+
+
+def test_pose_joint_assembly_equals_dense_jtj_c1():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    rng = np.random.default_rng(2003)
+    Rt = random_state(m, rng, 0.01, 0.3)
+    prm = O.params(joint_pose=1)
+    pose = _pose_increment(np.array(fr.s.pose[:]), rng.normal(0, [0.002] * 3 + [0.1] * 3))
+    s = O.system_pose(prm, pb, fr, Rt, pose)
+    pix, _, _ = O.associate(prm, pb, fr, Rt)
+    # the association of the system is taken at the current pose: freeze the same one
+    frc = O.Frame(sc["depth"], sc["intr"], pose)
+    pix, _, _ = O.associate(prm, pb, frc, Rt)
+    r, J = O.residuals_pose(prm, pb, fr, Rt, pose, pix)
+    H = O.dense_H(s, m + 1)
+    Hd = J.T @ J
+    assert np.abs(H - Hd).max() < 1e-9 * np.abs(Hd).max()
+    assert np.abs(s["rhs"] + J.T @ r).max() < 1e-9 * np.abs(J.T @ r).max()
+    assert abs(s["energy"][6] - r @ r) < 1e-10 * (r @ r)
+    assert s["energy"][4] > 0 and s["energy"][5] > 0
+    # the node-node part is the fixed-pose system at the same pose (the pose only adds a row / column)
+    s0 = O.system(O.params(), pb, frc, Rt)
+    H0 = O.dense_H(s0, m)
+    assert np.abs(H[:6 * m, :6 * m] - H0).max() < 1e-10 * np.abs(H0).max()
+    assert np.abs(s["rhs"][:6 * m] - s0["rhs"]).max() < 1e-10 * np.abs(s0["rhs"]).max()
+
+
+def test_pose_joint_gn_step_is_dense_solve_and_increment():
+    """One joint GN iteration (EXACT) = numpy solve of (J^T J + lambda I) x = -J^T r on the
+    oracle's residual stack, then the node (A18) and pose (A37) increments written out."""
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    prm = O.params(joint_pose=1, gn_iters=1, solve_mode=0)
+    Rt0 = O.identity_state(m)
+    pose0 = np.array(fr.s.pose[:])
+    pix, _, _ = O.associate(prm, pb, fr, Rt0)
+    r, J = O.residuals_pose(prm, pb, fr, Rt0, pose0, pix)
+    x = np.linalg.solve(J.T @ J + prm.lambda_ * np.eye(6 * (m + 1)), -J.T @ r)
+    Rt, pose, E, na = O.register_pose(prm, pb, fr)
+    Rd = Rt0.copy()
+    for j in range(m):
+        Rd[j, :9] = (O.exp_so3(x[6 * j:6 * j + 3]) @ Rt0[j, :9].reshape(3, 3)).ravel()
+        Rd[j, 9:] += x[6 * j + 3:6 * j + 6]
+    assert np.abs(Rt - Rd).max() < 1e-8
+    assert np.abs(pose - _pose_increment(pose0, x[6 * m:])).max() < 1e-9
+    assert abs(E[0, 6] - r @ r) < 1e-10 * (r @ r) and E[0, 4] == 0 and E[0, 5] == 0
+
+
+def test_pose_prior_anchoring_and_energy():
+    """with w_r, w_p -> 1e12 the refined pose stays at the prior (1e-6) and the nodes
+    match the fixed-pose registration; with the paper's weights the joint GN energy falls,
+    ends no higher than the fixed-pose one (6 more unknowns, EXACT solves) and the pose
+    moves off the prior (E_r + E_p > 0: the stiff priors hold it within ~1e-7)."""
+    sc, pb, fr, _ = scene_problem("c1")
+    base = dict(gn_iters=3, solve_mode=0)
+    Rt_f, E_f, _ = O.register(O.params(**base), pb, fr)
+    Rt_a, pose_a, E_a, _ = O.register_pose(O.params(joint_pose=1, w_r=1e12, w_p=1e12, **base), pb, fr)
+    pose0 = np.array(fr.s.pose[:])
+    assert np.abs(pose_a - pose0).max() < 1e-6
+    assert np.abs(Rt_a - Rt_f).max() < 1e-4
+    Rt_j, pose_j, E_j, _ = O.register_pose(O.params(joint_pose=1, **base), pb, fr)
+    assert (np.diff(E_j[:, 6]) < 0).all() and E_j[-1, 6] <= E_f[-1, 4] * (1 + 1e-9)
+    assert E_j[-1, 4] + E_j[-1, 5] > 0 and 0 < np.abs(pose_j - pose0).max() < 1e-6
+
+
+def test_pose_joint_lm_accepted_energy_decreasing():
+    sc, pb, fr, _ = scene_problem("c1")
+    prm = O.params(joint_pose=1, gn_iters=8, solve_mode=1, lm=1, lm_mu0=1e-3)
+    Rt, pose, E, na, acc = O.register_pose(prm, pb, fr, with_accepted=True)
+    ea = E[acc == 1, 6]
+    assert (np.diff(ea) < 0).all(), ea
+    Ef = O.system_pose(prm, pb, fr, Rt, pose)["energy"][6]
+    assert abs(Ef - ea[-1]) < 1e-9 * ea[0]
