@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define MIS_ABI_VERSION 1
+#define MIS_ABI_VERSION 2
 #define MIS_MAX_GN 32
 #define MIS_MAX_K 8
 
@@ -84,6 +84,20 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    only if accepted.  Per-iteration decisions in report n_guard.
                                    Needs the register-resident cluster PCG (systems of C1-C3
                                    size, pipelined recurrence): else MIS_E_ARG                      */
+#define MIS_F_JOINT_POSE  32u   /* NEXT-2 (readings A37-A40): the global pose (R, T) of
+                                   Eq. 1 is refined jointly with the nodes as unknown number m
+                                   ("only 6 more variables"): increment R <- R Exp(dphi),
+                                   T <- T + R dtau; the pose given to mis_register / mis_set_frame
+                                   is the start value and the ORB-SLAM prior of Eq. 10:
+                                   E_r = |wrap(euler_zyx(R^T) - euler_zyx(R0^T))|^2 (scope
+                                   orientation as yaw, pitch, roll), E_p = |c - c0|^2 with the
+                                   scope position c = -R^T T, weights w_r, w_p.  The pose enters
+                                   every point / feature row (Jacobian R [-[x_hat]x, I]), the
+                                   block-Jacobi preconditioner and lambda like a node.  The refined
+                                   pose is used by mis_warp / mis_fuse of the frame and read with
+                                   mis_get_pose.  Solved by the grid-wide PCG (the pose row is
+                                   dense).  Requires k <= 7 and world == 1; not with MIS_F_LM
+                                   (MIS_E_ARG)                                                      */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {
@@ -103,6 +117,8 @@ typedef struct {
   int32_t pcg_iters;    /* PCG iterations P per GN iteration, >= 1                         */
   float lambda;         /* GN damping, 1e-4 (reading A16)                                  */
   uint32_t flags;       /* MIS_F_*                                                         */
+  float w_r;            /* Eq. 10 orientation prior weight, 1e6, MIS_F_JOINT_POSE  */
+  float w_p;            /* Eq. 10 position prior weight, 1000, MIS_F_JOINT_POSE    */
 } mis_params;
 
 /* Per-registration report (all host memory). */
@@ -120,6 +136,8 @@ typedef struct {
   int32_t reserved;
   int64_t n_guard[MIS_MAX_GN + 1];     /* MIS_F_LM: 1 if the trial of iteration i (row [iters]: the
                                           final one) was accepted, else 0; Gauss-Newton: 0        */
+  double energy_pose[MIS_MAX_GN + 1][2]; /* MIS_F_JOINT_POSE: E_r, E_p per iteration (unweighted;
+                                          their weighted sum is part of energy[i][4]); else 0     */
 } mis_report;
 
 int32_t mis_abi_version(void);
@@ -204,6 +222,9 @@ mis_status mis_register(mis_ctx* ctx, mis_mem mem, const float* depth_mm, const 
 /* Node transforms: R9_t3 m x 12 float32 (mem) or fp64 master copy (host). */
 mis_status mis_get_nodes(mis_ctx* ctx, mis_mem mem, float* R9_t3);
 mis_status mis_get_nodes_f64(mis_ctx* ctx, double* R9_t3_host);
+/* The pose of the last registration (host, 12 doubles: R row-major, T; world -> camera):
+ * with MIS_F_JOINT_POSE the refined pose, else the frame's input pose. */
+mis_status mis_get_pose(mis_ctx* ctx, double pose[12]);
 /* Current node positions g_j (m x 3). */
 mis_status mis_get_graph(mis_ctx* ctx, mis_mem mem, float* node_pos);
 /* Current regulariser neighbour lists N(j) (m x n_nbr, -1 padded). */
@@ -273,6 +294,10 @@ mis_status mis_skin(mis_ctx* ctx, mis_mem mem, int64_t nq, const float* pts, int
 /* ---- stage outputs for parity tests (same kernels as the hot path) ---- */
 /* Inject a node state (m x 12 float32: R row-major, t); fp64 master = upcast. */
 mis_status mis_dbg_set_nodes(mis_ctx* ctx, mis_mem mem, const float* R9_t3);
+/* NEXT-2: inject the current pose (host, 12 doubles, R row-major + T) of a joint registration; the
+ * prior stays the frame's input pose.  The next mis_dbg_system / mis_dbg_associate with
+ * MIS_F_JOINT_POSE and mis_warp / mis_fuse use it (mis_register restarts from the prior). */
+mis_status mis_dbg_set_pose(mis_ctx* ctx, const double pose[12]);
 /* Normal map of the current frame: H x W x 4 (nx, ny, nz, D); n = 0 when the
  * normal is invalid, D = 0 when the depth is invalid. */
 mis_status mis_dbg_frame(mis_ctx* ctx, mis_mem mem, float* nmap);
@@ -283,6 +308,8 @@ mis_status mis_dbg_associate(mis_ctx* ctx, mis_mem mem, int32_t* pix, uint8_t* w
 /* The normal equations at the current state: full BSR (both triangles,
  * rows sorted by column): row_ptr (m+1), col (nnzb), val (nnzb x 36,
  * row-major 6x6, unknowns [dtheta, dt] per node), rhs (6m) = -J^T r, energy[5].
+ * With MIS_F_JOINT_POSE the pose is unknown m: row_ptr (m+2), rhs 6(m+1), and
+ * energy[4] includes w_r E_r + w_p E_p.
  * With val == NULL only *nnzb is returned.  Host memory only. */
 mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* val, float* rhs,
                           double energy[5], int64_t* nnzb);

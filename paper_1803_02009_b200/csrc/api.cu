@@ -114,13 +114,14 @@ FrameView frame_view(Ctx* c) {
   f.nmapd = c->nmapd.as<double4>();
   for (int i = 0; i < 9; ++i) { f.R[i] = c->pose[i]; f.Rd[i] = c->pose[i]; }
   for (int i = 0; i < 3; ++i) { f.T[i] = c->pose[9 + i]; f.Td[i] = c->pose[9 + i]; }
+  f.pose_dev = c->pose_valid ? c->posebuf.as<double>() : nullptr;   // NEXT-2: the refined pose
   return f;
 }
 
 AccView acc_view(Ctx* c) {
   AccView a;
   float* base = c->acc.as<float>();
-  const size_t nz = (size_t)c->nnzb, m = (size_t)c->m;
+  const size_t nz = (size_t)c->nnzb, m = (size_t)sys_m(c);
   // all accumulated atomically (K3 float4 / float2 adds, K4 / K5), zeroed every iteration:
   // data | mom | rhs_data (padded to 4 floats: 16-byte aligned node moments) | node_mom | graph | rhs_graph
   a.data = base;
@@ -412,8 +413,10 @@ static mis_status check_params(const mis_params* p) {
       p->pcg_iters < 0 || !(p->eps_d_mm > 0) || !(p->eps_n_deg > 0) || !(p->tau_z_mm > 0) || !(p->trunc_mm > 0) ||
       !(p->omega_max >= 1) || !(p->lambda >= 0) || !std::isfinite(p->tau_z_mm) || !std::isfinite(p->trunc_mm) ||
       !std::isfinite(p->eps_d_mm) || !(p->delta_deg > 0) || !(p->delta_deg < 180) || !(p->eps_n_deg < 180) ||
-      !std::isfinite(p->omega_max) || !std::isfinite(p->lambda) || p->n_nbr > 64)
+      !std::isfinite(p->omega_max) || !std::isfinite(p->lambda) || p->n_nbr > 64 || !(p->w_r >= 0) ||
+      !(p->w_p >= 0) || !std::isfinite(p->w_r) || !std::isfinite(p->w_p))
     return MIS_E_ARG;
+  if ((p->flags & MIS_F_JOINT_POSE) && (p->k > MIS_MAX_K - 1 || (p->flags & MIS_F_LM))) return MIS_E_ARG;
   return MIS_OK;
 }
 
@@ -429,6 +432,7 @@ void mis_default_params(mis_params* o) {
   o->eps_d_mm = 15.0f; o->eps_n_deg = 10.0f;
   o->tau_z_mm = 10.0f; o->delta_deg = 10.0f; o->trunc_mm = 40.0f; o->omega_max = 10.0f;
   o->gn_iters = 5; o->pcg_iters = 10; o->lambda = 1e-4f; o->flags = 0;
+  o->w_r = 1e6f; o->w_p = 1000.0f;   // Eq. 10 prior weights, MIS_F_JOINT_POSE
 }
 
 const char* mis_last_error(const mis_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -505,8 +509,10 @@ mis_status mis_destroy(mis_ctx* c) {
 // pattern-dependent ones assume nnzb <= m (2 n_nbr + 1 + 4 k^2) blocks (measured: 14 m at C3, 32 m
 // at C5) and n_feat <= max(4096, H W / 64) feature pairs.
 static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int64_t W) {
-  const int64_t K = c->K, P = K * (K + 1) / 2, nn = std::max<int32_t>(c->prm.n_nbr, 1), px = H * W;
-  const int64_t nnz = std::min<int64_t>(m * m, m * (2 * nn + 1 + 4 * K * K));
+  const int64_t K = c->K + 1, P = K * (K + 1) / 2, nn = std::max<int32_t>(c->prm.n_nbr, 1), px = H * W;
+  // sized for a joint-pose pattern (NEXT-2): k + 1 factor slots, m + 1 unknowns, 2m + 1 more blocks
+  const int64_t nnz = std::min<int64_t>(m * m, m * (2 * nn + 1 + 4 * K * K)) + 2 * m + 1;
+  m += 1;
   const int64_t nf = std::max<int64_t>(4096, px / 64);
   const int64_t mr = m, cs = 16, mp = nnz / 4 + mr + 1;   // cluster PCG lists (pcg_cluster.cu max_pieces)
   int64_t slots = 1024;
@@ -533,6 +539,7 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
       12 * nf + 16, 12 * nf + 16, 4 * nf * K + 16, 4 * nf * K + 16,         // features
       12 * n, 4 * n, 4 * n * K, 4 * n * K,                                  // filter re-skinning list
       32 * n, 4 * m * nn,                                                   // node regeneration: cell sums, N(j)
+      24 * 8, 4 * n * K,                                                    // joint pose: state, tuples
   };
   size_t total = 0;
   for (int64_t x : b) {
@@ -759,6 +766,7 @@ static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm,
   c->W = it->width;
   c->H = it->height;
   memcpy(c->pose, pose, 48);   // pose is host memory (12 floats) in every mode
+  c->pose_valid = false;       // a new input pose (NEXT-2: the next joint registration refines it)
   const size_t px = (size_t)c->W * c->H;
   const float* dsrc = depth_mm;   // device depth is read in place by K1 (stream order)
   if (mem == MIS_MEM_HOST) {
@@ -794,7 +802,7 @@ mis_status mis_set_features(mis_ctx* c, mis_mem mem, int32_t n_feat, const float
   const int K = c->K;
   TRY(c, ensure(c, c->fsrc, (size_t)n_feat * 12 + 16));
   TRY(c, ensure(c, c->fdst, (size_t)n_feat * 12 + 16));
-  TRY(c, ensure(c, c->fidx, (size_t)n_feat * K * 4 + 16));
+  TRY(c, ensure(c, c->fidx, (size_t)n_feat * (K + 1) * 4 + 16));   // + the pose row of a joint pattern
   TRY(c, ensure(c, c->fw, (size_t)n_feat * K * 4 + 16));
   if (n_feat > 0) {
     if (mem == MIS_MEM_HOST) {
@@ -833,7 +841,11 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.cos_eps_nd = cos(c->prm.eps_n_deg * d2r);
   a.cos_eps_n = (float)a.cos_eps_nd;
   a.acc = acc;
-  TRY(c, ensure(c, c->pstate, (size_t)(c->K + 2) * 16 * (size_t)std::max<int64_t>(c->n, 1)));
+  const bool joint = c->pattern_joint;   // NEXT-2: the pose as factor slot k / unknown m
+  const int KS = c->K + (joint ? 1 : 0);
+  a.pose_cur = joint ? c->posebuf.as<double>() : nullptr;
+  if (joint) a.seg_nodes = c->seg_nodes_j.as<int32_t>();
+  TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(c->n, 1)));
   a.pstate = c->pstate.as<float4>();
   a.pstride = std::max<int64_t>(c->n, 1);
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
@@ -858,6 +870,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     gA.w_corr = c->prm.w_corr;
     gA.acc = acc;
     gA.K = c->K;
+    gA.KS = KS;
+    gA.pose_cur = a.pose_cur;
   }
   if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch
     ProfScope ps(c, P_POINTS, 1);
@@ -865,7 +879,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   }
   if (a.nchunk > 0) {
     ProfScope ps(c, P_ACCUM, 1);
-    launch_accum_points(c->K, a, c->num_sms, c->st);
+    launch_accum_points(KS, a, c->num_sms, c->st);
   }
   TRY(c, cudaGetLastError());
   if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
@@ -876,9 +890,15 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     ProfScope ps(c, P_REDUCE, 1);
     FinalArgs r;
     r.nnzb = c->nnzb;
-    r.nup = (c->nnzb - c->m) / 2;
+    r.nup = (c->nnzb - sys_m(c)) / 2;
     r.ulist = c->ulist.as<int2>();
-    r.m = c->m;
+    r.m = sys_m(c);
+    r.pose_node = joint ? c->m : -1;
+    r.pose_cur = joint ? c->posebuf.as<double>() : nullptr;
+    r.pose_prior = joint ? c->posebuf.as<double>() + 12 : nullptr;
+    r.w_r = c->prm.w_r;
+    r.w_p = c->prm.w_p;
+    r.rep_pose = rep_pose(c);
     r.upper_of = c->upper_of.as<int32_t>();
     r.lower_of = c->lower_of.as<int32_t>();
     r.diag_pos = c->diag_pos.as<int32_t>();
@@ -908,8 +928,10 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
 
 static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   SolveArgs s;
-  s.m = c->m;
+  s.m = sys_m(c);
   s.K = c->K;
+  s.pose_node = c->pattern_joint ? c->m : -1;   // NEXT-2
+  s.pose = c->pattern_joint ? c->posebuf.as<double>() : nullptr;
   s.nnzb = c->nnzb;
   s.row_ptr = c->row_ptr.as<int32_t>();
   s.col = c->col.as<int32_t>();
@@ -972,9 +994,32 @@ static cudaError_t run_solve(Ctx* c, const SolveArgs& s) {
   return e;
 }
 
+// NEXT-2: posebuf = [current pose | prior]; the prior is the frame's input pose, the current one
+// `cur` (fp64, host) or the prior.  One tiny launch (by-value arguments, no host buffer to keep).
+struct Pose24 { double v[24]; };
+__global__ void k_pose_init(Pose24 p, double* out) {
+  if (threadIdx.x < 24) out[threadIdx.x] = p.v[threadIdx.x];
+}
+static cudaError_t pose_init(Ctx* c, const double* cur) {
+  cudaError_t e = ensure(c, c->posebuf, 24 * 8);
+  if (e != cudaSuccess) return e;
+  Pose24 p;
+  for (int i = 0; i < 12; ++i) {
+    p.v[12 + i] = (double)c->pose[i];
+    p.v[i] = cur ? cur[i] : (double)c->pose[i];
+  }
+  launch_pdl(k_pose_init, dim3(1), dim3(32), 0, c->st, p, c->posebuf.as<double>());
+  count_launches(1);
+  c->pose_valid = true;
+  return cudaGetLastError();
+}
+
 static mis_status prepare(Ctx* c) {
   if (!c->have_graph) return fail(c, MIS_E_STATE, "no graph (mis_set_graph)");
   if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame (mis_set_frame / depth)");
+  c->joint = (c->prm.flags & MIS_F_JOINT_POSE) != 0;
+  if (c->joint && c->world > 1) return fail(c, MIS_E_ARG, "MIS_F_JOINT_POSE: single GPU only");
+  if (c->joint != c->pattern_joint) c->pattern_valid = false;   // the pose row / column come or go
   if (c->dirty) TRY(c, run_build_order(c));
   if (!c->pattern_valid) {
     {
@@ -992,6 +1037,7 @@ static mis_status prepare(Ctx* c) {
   }
   TRY(c, flush_frame(c));   // if the pattern was still valid (no readback to hide it behind)
   if (c->nf > 0 && !c->fidx.p) return fail(c, MIS_E_STATE, "features not set");
+  if (c->joint && !c->pose_valid) TRY(c, pose_init(c, nullptr));
   return MIS_OK;
 }
 
@@ -1011,6 +1057,8 @@ static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
     for (int q = 0; q < 5; ++q) rep->energy[i][q] = e[5 * i + q];
     rep->n_assoc[i] = (int64_t)llround(na[i]);
     rep->n_guard[i] = (int64_t)llround(na[MIS_MAX_GN + 1 + i]);
+    rep->energy_pose[i][0] = blk[kRepP + 2 * i];
+    rep->energy_pose[i][1] = blk[kRepP + 2 * i + 1];
   }
   rep->nnzb = c->nnzb;
   rep->n_segments = c->nseg;
@@ -1031,9 +1079,11 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
     if ((s = set_frame_impl(c, mem, depth_mm, intr, pose, true)) != MIS_OK) return s;
   } else if (pose) {
     memcpy(c->pose, pose, 48);
+    c->pose_valid = false;
   }
   if (n_feat >= 0)
     if ((s = mis_set_features(c, mem, n_feat, feat_src, feat_dst)) != MIS_OK) return s;
+  if ((c->prm.flags & MIS_F_JOINT_POSE) && c->pose_valid) TRY(c, pose_init(c, nullptr));   // start at the prior
   if ((s = prepare(c)) != MIS_OK) return s;
   const int G = c->prm.gn_iters;
   const bool lm = c->prm.flags & MIS_F_LM;
@@ -1089,6 +1139,26 @@ mis_status mis_get_nodes_f64(mis_ctx* c, double* out) {
   cudaSetDevice(c->device);
   TRY(c, cudaMemcpyAsync(out, c->Rt64.p, (size_t)c->m * 96, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
+  return MIS_OK;
+}
+
+mis_status mis_get_pose(mis_ctx* c, double pose[12]) {
+  if (!c || !pose) return MIS_E_ARG;
+  cudaSetDevice(c->device);
+  if (c->pose_valid) {
+    TRY(c, cudaMemcpyAsync(pose, c->posebuf.p, 96, cudaMemcpyDeviceToHost, c->st));
+    TRY(c, cudaStreamSynchronize(c->st));
+  } else {
+    for (int i = 0; i < 12; ++i) pose[i] = (double)c->pose[i];
+  }
+  return MIS_OK;
+}
+
+mis_status mis_dbg_set_pose(mis_ctx* c, const double pose[12]) {
+  if (!c || !pose) return MIS_E_ARG;
+  if (!c->have_frame) return fail(c, MIS_E_STATE, "no frame");
+  cudaSetDevice(c->device);
+  TRY(c, pose_init(c, pose));
   return MIS_OK;
 }
 
@@ -1157,10 +1227,10 @@ mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val
   *nnzb = c->nnzb;
   if (!val) return MIS_OK;
   if ((s = assemble(c, false, 0)) != MIS_OK) return s;
-  if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(c->m + 1) * 4, cudaMemcpyDeviceToHost, c->st));
+  if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(sys_m(c) + 1) * 4, cudaMemcpyDeviceToHost, c->st));
   if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
-  if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)c->m * 24, cudaMemcpyDeviceToHost, c->st));
+  if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)sys_m(c) * 24, cudaMemcpyDeviceToHost, c->st));
   if (energy) TRY(c, cudaMemcpyAsync(energy, rep_energy(c), 40, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
   return MIS_OK;

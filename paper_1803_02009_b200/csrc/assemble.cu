@@ -78,9 +78,11 @@ struct PState {   // a point's compact factor state (zeros: not associated)
   float4 nn;      // (n', 0)
 };
 
-template <int K, bool DBG>
-__device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, PState<K>& st, double& ed, double& ep,
-                                            int& as) {
+// JOINT (NEXT-2, A37): the pose comes from a.pose_cur and is written as factor slot K: (x_hat, 1),
+// the form of a node of weight 1 with a = x_hat (Jacobian R [-[x_hat]x, I])
+template <int K, bool DBG, bool JOINT>
+__device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, PState<K + (JOINT ? 1 : 0)>& st,
+                                            double& ed, double& ep, int& as) {
   const ModelView& md = a.md;
   const FrameView& fr = a.fr;
   const double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
@@ -95,6 +97,9 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
   int pix = -1;
   uint8_t why = 0;
   double vt[3] = {0, 0, 0}, q[3] = {0, 0, 0}, N[3] = {0, 0, 0};
+  double xh[3] = {0, 0, 0};
+  const double* Rd = JOINT ? a.pose_cur : fr.Rd;
+  const double* Td = JOINT ? a.pose_cur + 9 : fr.Td;
   float af[K][3];
 #pragma unroll
   for (int s = 0; s < K; ++s) af[s][0] = af[s][1] = af[s][2] = 0.f;
@@ -103,7 +108,7 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
     // each and squared comparisons: the results differ from the oracle's only in the
     // last bits, so only exact ties could decide differently
     const double iW = 1.0 / W;
-    double xh[3] = {0, 0, 0}, mh[3] = {0, 0, 0};
+    double mh[3] = {0, 0, 0};
 #pragma unroll
     for (int s = 0; s < K; ++s) {
       const double2* rt = reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nid[s]);   // R (9), t (3)
@@ -123,11 +128,10 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
       mh[1] += wn[s] * (R23.y * n[0] + R45.x * n[1] + R45.y * n[2]);
       mh[2] += wn[s] * (R67.x * n[0] + R67.y * n[1] + R8t0.x * n[2]);
     }
-    const double* Rd = fr.Rd;
     double nt[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      vt[r] = Rd[3 * r] * xh[0] + Rd[3 * r + 1] * xh[1] + Rd[3 * r + 2] * xh[2] + fr.Td[r];
+      vt[r] = Rd[3 * r] * xh[0] + Rd[3 * r + 1] * xh[1] + Rd[3 * r + 2] * xh[2] + Td[r];
       nt[r] = Rd[3 * r] * mh[0] + Rd[3 * r + 1] * mh[1] + Rd[3 * r + 2] * mh[2];
     }
     const double ml2 = mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2];
@@ -163,7 +167,6 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
   if (DBG) { a.dbg_pix[i] = pix; a.dbg_why[i] = why; }
   if (pix >= 0) {
     as = 1;
-    const double* Rd = fr.Rd;
     const double e0 = vt[0] - q[0], e1 = vt[1] - q[1], e2 = vt[2] - q[2];
     const double rpl = N[0] * e0 + N[1] * e1 + N[2] * e2;                        // Eq. 8
     const float np0 = (float)(Rd[0] * N[0] + Rd[3] * N[1] + Rd[6] * N[2]);      // n' = R^T N
@@ -177,13 +180,14 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
       const float w = (float)wn[s];
       st.wa[s] = make_float4(w * af[s][0], w * af[s][1], w * af[s][2], w);
     }
+    if constexpr (JOINT) st.wa[K] = make_float4((float)xh[0], (float)xh[1], (float)xh[2], 1.f);
     st.rr = make_float4((float)rp0, (float)rp1, (float)rp2, (float)rpl);
     st.nn = make_float4(np0, np1, np2, 0.f);
     ed += rpl * rpl;
     ep += rp0 * rp0 + rp1 * rp1 + rp2 * rp2;
   } else {
 #pragma unroll
-    for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < K + (JOINT ? 1 : 0); ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
     st.rr = st.nn = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
@@ -207,7 +211,7 @@ __device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, do
 __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid);
 
 // K3a; the blocks after the points' run the K4/K5 items (independent of K3a, same launch)
-template <int K, bool DBG>
+template <int K, bool DBG, bool JOINT>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_blocks) {
   pdl_wait();   // node states from the previous solve
@@ -220,14 +224,15 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArg
   double ed = 0.0, ep = 0.0;
   int as = 0;
   if (i < a.md.n) {
-    PState<K> st;
-    assoc_point<K, DBG>(a, i, st, ed, ep, as);
+    constexpr int KS = K + (JOINT ? 1 : 0);   // factor slots (the pose last, NEXT-2)
+    PState<KS> st;
+    assoc_point<K, DBG, JOINT>(a, i, st, ed, ep, as);
     float4* ps = a.pstate;
     const int64_t S = a.pstride;
 #pragma unroll
-    for (int s = 0; s < K; ++s) ps[s * S + i] = st.wa[s];
-    ps[K * S + i] = st.rr;
-    ps[(K + 1) * S + i] = st.nn;
+    for (int s = 0; s < KS; ++s) ps[s * S + i] = st.wa[s];
+    ps[KS * S + i] = st.rr;
+    ps[(KS + 1) * S + i] = st.nn;
   }
   commit_point_energies(a, ed, ep, as);
 }
@@ -1022,6 +1027,20 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     r.acc.graph[36 * e + lane] = 0.f;
     if (lane < 4) r.acc.graph[36 * e + 32 + lane] = 0.f;
     __syncwarp();
+    if (gw == r.pose_node) {   // NEXT-2: + w_r J_r^T J_r + w_p J_p^T J_p of Eq. 10 (A38-A39), into G
+      double pr[6], pJ[36];
+      pose_prior_dev(r.pose_prior, r.pose_cur, pr, pJ);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int l = lane + 32 * k, i = l / 6, j = l - 6 * (l / 6);
+        if (l < 36) {
+          double h = 0.0;
+          for (int q = 0; q < 6; ++q) h += (q < 3 ? (double)r.w_r : (double)r.w_p) * pJ[6 * q + i] * pJ[6 * q + j];
+          st[52 + l] += (float)h;
+        }
+      }
+      __syncwarp();
+    }
     const Recipe rc[2] = {rtab[0][lane], rtab[0][lane < 4 ? lane + 32 : 0]};
     final_block(r, st, st + 88, e, -1, lane, rc);
     if (r.Minv) {   // block-Jacobi inverse of this node (K7), off the solver's critical path:
@@ -1140,7 +1159,14 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
       } else {
         pt = Nm[9 + (lane - 3)];
       }
-      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + gv[q];
+      float prior = 0.f;
+      if (n == r.pose_node) {   // NEXT-2: -(w_r J_r^T r_r + w_p J_p^T r_p)
+        double pr[6], pJ[36], b = 0.0;
+        pose_prior_dev(r.pose_prior, r.pose_cur, pr, pJ);
+        for (int k = 0; k < 6; ++k) b += (k < 3 ? (double)r.w_r : (double)r.w_p) * pJ[6 * k + lane] * pr[k];
+        prior = (float)(-b);
+      }
+      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + gv[q] + prior;
     }
     return;
   }
@@ -1160,9 +1186,17 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
     if (lane == 0) {
       if (r.slot >= 0) {
         double* rep = r.rep_energy + 5 * r.slot;
+        double Er = 0.0, Ep = 0.0;
+        if (r.pose_node >= 0) {   // NEXT-2: E_r, E_p (Eq. 10) at the assembled pose
+          double pr[6], pJ[36];
+          pose_prior_dev(r.pose_prior, r.pose_cur, pr, pJ);
+          Er = pr[0] * pr[0] + pr[1] * pr[1] + pr[2] * pr[2];
+          Ep = pr[3] * pr[3] + pr[4] * pr[4] + pr[5] * pr[5];
+          if (r.rep_pose) { r.rep_pose[2 * r.slot] = Er; r.rep_pose[2 * r.slot + 1] = Ep; }
+        }
         rep[0] = tot[0]; rep[1] = tot[1]; rep[2] = tot[2]; rep[3] = tot[3];
         rep[4] = (double)r.w_data * tot[0] + (double)r.w_pt * tot[1] + (double)r.w_reg * tot[2] +
-                 (double)r.w_corr * tot[3];
+                 (double)r.w_corr * tot[3] + (double)r.w_r * Er + (double)r.w_p * Ep;
         r.rep_nassoc[r.slot] = tot[4];
         r.rep_nassoc[MIS_MAX_GN + 1 + r.slot] = 0.0;   // (no fp32 guard band: the association runs in fp64)
       }
@@ -1185,13 +1219,21 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
   int64_t ng = 0;
   if (ga) {
     gz = *ga;
-    const int P = K * (K + 1) / 2;
-    ng = (int64_t)gz.nd.m * gz.n_nbr * 6 + (int64_t)gz.nf * P * 6 + (int64_t)gz.nf * K;
+    const int PS = gz.KS * (gz.KS + 1) / 2;
+    ng = (int64_t)gz.nd.m * gz.n_nbr * 6 + (int64_t)gz.nf * PS * 6 + (int64_t)gz.nf * gz.KS;
   }
   const unsigned gg = (unsigned)((ng + 255) / 256);
   if (g + gg == 0) return;
-  if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
-  else launch_pdl(k_assoc_points<K, false>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+  const bool joint = a.pose_cur != nullptr;
+  if constexpr (K < MIS_MAX_K) {
+    if (joint) {
+      if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+      else launch_pdl(k_assoc_points<K, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+      return;
+    }
+  }
+  if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, false>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+  else launch_pdl(k_assoc_points<K, false, false>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
 }
 
 #ifndef MIS_K3B_TC
@@ -1273,9 +1315,14 @@ __device__ __forceinline__ void feature_warp(const AsmGraphArgs& a, int fi, floa
       xh[r] += w * (ar + g[r] + Rt[9 + r]);
     }
   }
-  const double* R = a.fr.Rd;
+  const double* R = a.pose_cur ? a.pose_cur : a.fr.Rd;
+  const double* T = a.pose_cur ? a.pose_cur + 9 : a.fr.Td;
+  if (a.KS > K) {   // NEXT-2: the pose as slot K, a = x_hat, weight 1 (A37)
+    for (int r = 0; r < 3; ++r) am[K][r] = (float)xh[r];
+    wn[K] = 1.f;
+  }
   for (int r = 0; r < 3; ++r)
-    e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + a.fr.Td[r] - a.fdst[3 * fi + r];
+    e[r] = R[3 * r] * xh[0] + R[3 * r + 1] * xh[1] + R[3 * r + 2] * xh[2] + T[r] - a.fdst[3 * fi + r];
   for (int r = 0; r < 3; ++r) rp[r] = (float)(R[r] * e[0] + R[3 + r] * e[1] + R[6 + r] * e[2]);
 }
 
@@ -1304,13 +1351,13 @@ __device__ __forceinline__ void add_row(float* B, int r, const float* row, float
 }
 
 __device__ __forceinline__ int64_t graph_items(const AsmGraphArgs& a) {
-  const int P = a.K * (a.K + 1) / 2;
-  return (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.K;
+  const int P = a.KS * (a.KS + 1) / 2;
+  return (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.KS;
 }
 
 // one K4/K5 item per thread (whole warps call this; tid >= graph_items: no work)
 __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid) {
-  const int K = a.K, P = K * (K + 1) / 2;
+  const int K = a.KS, P = K * (K + 1) / 2;   // feature slots (incl. the pose, NEXT-2)
   const int64_t n_edge = (int64_t)a.nd.m * a.n_nbr * 6, n_fp = (int64_t)a.nf * P * 6, n_fr = (int64_t)a.nf * K;
   double eR = 0.0, eC = 0.0;
   if (tid < n_edge) {
@@ -1401,8 +1448,8 @@ __global__ void __launch_bounds__(256) k_assemble_graph(AsmGraphArgs a) {
 }
 
 void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s) {
-  const int P = a.K * (a.K + 1) / 2;
-  const int64_t n = (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.K;
+  const int P = a.KS * (a.KS + 1) / 2;
+  const int64_t n = (int64_t)a.nd.m * a.n_nbr * 6 + (int64_t)a.nf * P * 6 + (int64_t)a.nf * a.KS;
   if (n <= 0) return;
   k_assemble_graph<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
 }

@@ -45,7 +45,24 @@ struct FrameView {
   const double4* nmapd;  // H*W: the same in fp64 (the association's precision)
   float R[9], T[3];      // world -> camera (fp32 copy)
   double Rd[9], Td[3];   // fp64 copy (the association and fusion decisions)
+  const double* pose_dev;   // NEXT-2: the refined pose on the device (R row-major 9, T 3), else null
 };
+
+// The frame's world -> camera pose in fp64: the device copy refined by a joint registration
+// (MIS_F_JOINT_POSE) when there is one, else the input pose passed by value.
+__device__ __forceinline__ void frame_pose(const FrameView& f, double* R, double* T) {
+  if (f.pose_dev) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = f.pose_dev[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) T[i] = f.pose_dev[9 + i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = f.Rd[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) T[i] = f.Td[i];
+  }
+}
 
 struct ModelView {
   int64_t n, cap;
@@ -118,6 +135,10 @@ struct AsmPointsArgs {
   unsigned long long* work_counter;   // zeroed before the launch (dynamic chunk scheduling)
   int32_t* dbg_pix;           // nullable: per point association outputs
   uint8_t* dbg_why;
+  // NEXT-2 (MIS_F_JOINT_POSE): the current pose (12 doubles) -- K3a warps with it and writes the
+  // pose as one more factor slot (x_hat, 1) after the K node slots; K3b then runs with K + 1 slots
+  // whose last node id is m (seg_nodes / seg_slot of the joint pattern).  null: fixed pose
+  const double* pose_cur;
 };
 // K3a (per point), then K3b (per chunk)
 struct AsmGraphArgs;
@@ -154,6 +175,12 @@ struct FinalArgs {
   float* Minv;                // m*36 block-Jacobi inverses
   float lambda, w_reg, w_corr;
   int slot;                   // report slot of this assembly (-1: none)
+  // NEXT-2: unknown pose_node (= m; -1: none) is the pose; its diagonal block and rhs get the
+  // Eq. 10 priors at pose_cur against pose_prior (w_r, w_p), its energies go to rep_pose
+  int pose_node;
+  const double *pose_cur, *pose_prior;
+  float w_r, w_p;
+  double* rep_pose;           // (MIS_MAX_GN+1)*2
   double* rep_energy;         // (MIS_MAX_GN+1)*5
   double* rep_nassoc;         // 2*(MIS_MAX_GN+1): association counts, fp64 guard counts
   const LmDev* lm;            // LM: write the system into the buffer not holding the accepted one
@@ -175,6 +202,8 @@ struct AsmGraphArgs {
   float w_reg, w_corr;
   AccView acc;
   int K;
+  int KS;                     // feature slots: K, or K + 1 with the pose (fidx row K = m, NEXT-2)
+  const double* pose_cur;     // NEXT-2: the current pose (null: fr's)
 };
 void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s);
 
@@ -214,6 +243,8 @@ struct SolveArgs {
   float lm_mu0;
   const float *Hval_alt, *rhs_alt;
   double* Rt_acc;             // m x 12: last accepted state
+  int pose_node;              // NEXT-2: unknown index of the pose (m), -1: none
+  double* pose;               // its state (R row-major 9, T 3): R <- R Exp(dphi), T <- T + R dtau
   const double* rep_energy;   // (MIS_MAX_GN+1) x 5, the trial energies
   double* rep_flags;          // MIS_MAX_GN+1: 1 = trial accepted
 };

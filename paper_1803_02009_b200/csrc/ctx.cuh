@@ -57,6 +57,13 @@ struct Ctx {
   int m = 0;
   DBuf g, nbr, node32, Rt64;
 
+  // ---- NEXT-2 joint global pose (MIS_F_JOINT_POSE): unknown number m of the system
+  bool joint = false;           // the flag, as of the last prepare()
+  bool pattern_joint = false;   // the current pattern / accumulator layout includes the pose
+  bool pose_valid = false;      // posebuf holds this frame's pose (registered jointly or injected)
+  DBuf posebuf;                 // 24 doubles: current pose (R 9, T 3) | prior (the frame's input pose)
+  DBuf seg_nodes_j;             // nseg x (k + 1): segment tuples + the pose id m
+
   // ---- order: segments and chunks (K13)
   int64_t nseg = 0, nchunk = 0;
   DBuf keys, keys2, vals, vals2, flags, scan, seg_start, seg_nodes, chunks, chunk_off;
@@ -132,13 +139,16 @@ enum { P_FRAME = 0, P_SKIN, P_ORDER, P_PATTERN, P_POINTS, P_GRAPH, P_SOLVE, P_WA
 void count_launches(int64_t k);
 
 // report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual
-// MIS_MAX_GN floats | numeric flag], doubles
+// MIS_MAX_GN floats | numeric flag | E_r, E_p (MIS_MAX_GN+1) x 2], doubles
 constexpr size_t kRepN = 5 * (MIS_MAX_GN + 1), kRepR = kRepN + 2 * (MIS_MAX_GN + 1), kRepF = kRepR + MIS_MAX_GN / 2,
-                 kRepBytes = (kRepF + 1) * 8;
+                 kRepP = kRepF + 1, kRepBytes = (kRepP + 2 * (MIS_MAX_GN + 1)) * 8;
+// unknown blocks of the current system: the m nodes, plus the pose with the joint pattern (NEXT-2)
+inline int sys_m(const Ctx* c) { return c->m + (c->pattern_joint ? 1 : 0); }
 inline double* rep_energy(Ctx* c) { return c->rep.as<double>(); }
 inline double* rep_nassoc(Ctx* c) { return c->rep.as<double>() + kRepN; }
 inline float* rep_res(Ctx* c) { return reinterpret_cast<float*>(c->rep.as<double>() + kRepR); }
 inline int* numeric_flag(Ctx* c) { return reinterpret_cast<int*>(c->rep.as<double>() + kRepF); }
+inline double* rep_pose(Ctx* c) { return c->rep.as<double>() + kRepP; }
 
 // Records an event pair around a group of `nk` kernel launches on the context
 // stream when profiling is on; always adds nk to the launch counter.

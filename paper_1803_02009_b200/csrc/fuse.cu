@@ -40,12 +40,16 @@ __global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, F
       md.nx[i] = n[0]; md.ny[i] = n[1]; md.nz[i] = n[2];
     }
   }
-  if (xyz_cam) {
-    for (int r = 0; r < 3; ++r)
-      xyz_cam[3 * i + r] = fr.R[3 * r] * v[0] + fr.R[3 * r + 1] * v[1] + fr.R[3 * r + 2] * v[2] + fr.T[r];
-  }
-  if (nrm_cam) {
-    for (int r = 0; r < 3; ++r) nrm_cam[3 * i + r] = fr.R[3 * r] * n[0] + fr.R[3 * r + 1] * n[1] + fr.R[3 * r + 2] * n[2];
+  if (xyz_cam || nrm_cam) {
+    double Rd[9], Td[3];
+    frame_pose(fr, Rd, Td);   // the refined pose after a joint registration (NEXT-2)
+    float R[9], T[3];
+    for (int q = 0; q < 9; ++q) R[q] = (float)Rd[q];
+    for (int q = 0; q < 3; ++q) T[q] = (float)Td[q];
+    if (xyz_cam)
+      for (int r = 0; r < 3; ++r) xyz_cam[3 * i + r] = R[3 * r] * v[0] + R[3 * r + 1] * v[1] + R[3 * r + 2] * v[2] + T[r];
+    if (nrm_cam)
+      for (int r = 0; r < 3; ++r) nrm_cam[3 * i + r] = R[3 * r] * n[0] + R[3 * r + 1] * n[1] + R[3 * r + 2] * n[2];
   }
 }
 
@@ -105,11 +109,13 @@ __global__ void __launch_bounds__(256) k_fuse_register(FuseArgs a) {
   if (i == 0 && a.n_reg) *a.n_reg = 0;   // counted later by the lift count
   if (i >= a.md.n) return;
   const FrameView& f = a.fr;
+  double Rd[9], Td[3];
+  frame_pose(f, Rd, Td);   // the refined pose after a joint registration (NEXT-2)
   const double v[3] = {a.md.px[i], a.md.py[i], a.md.pz[i]}, n[3] = {a.md.nx[i], a.md.ny[i], a.md.nz[i]};
   double vt[3], nt[3];
   for (int r = 0; r < 3; ++r) {
-    vt[r] = f.Rd[3 * r] * v[0] + f.Rd[3 * r + 1] * v[1] + f.Rd[3 * r + 2] * v[2] + f.Td[r];
-    nt[r] = f.Rd[3 * r] * n[0] + f.Rd[3 * r + 1] * n[1] + f.Rd[3 * r + 2] * n[2];
+    vt[r] = Rd[3 * r] * v[0] + Rd[3 * r + 1] * v[1] + Rd[3 * r + 2] * v[2] + Td[r];
+    nt[r] = Rd[3 * r] * n[0] + Rd[3 * r + 1] * n[1] + Rd[3 * r + 2] * n[2];
   }
   uint8_t why = 0;
   int32_t pix = -1;
@@ -160,6 +166,8 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
   if (pix < 0) return;
   if ((uint32_t)(a.pixkey[pix] & 0xffffffffull) != (a.rank_tag | (uint32_t)i)) return;
   const FrameView& f = a.fr;
+  double Rd[9], Td[3];
+  frame_pose(f, Rd, Td);   // the refined pose after a joint registration (NEXT-2)
   const int px = pix % f.W, py = pix / f.W;
   double N[3], q[3];
   normal_map64(f, px, py, N, q);
@@ -167,17 +175,17 @@ __global__ void __launch_bounds__(256) k_fuse_apply(FuseArgs a) {
   const double om = a.md.w[i];
   double pf[3], nf[3];
   for (int r = 0; r < 3; ++r) {
-    const double vt = f.Rd[3 * r] * v[0] + f.Rd[3 * r + 1] * v[1] + f.Rd[3 * r + 2] * v[2] + f.Td[r];
-    const double nt = f.Rd[3 * r] * n[0] + f.Rd[3 * r + 1] * n[1] + f.Rd[3 * r + 2] * n[2];
+    const double vt = Rd[3 * r] * v[0] + Rd[3 * r + 1] * v[1] + Rd[3 * r + 2] * v[2] + Td[r];
+    const double nt = Rd[3 * r] * n[0] + Rd[3 * r + 1] * n[1] + Rd[3 * r + 2] * n[2];
     pf[r] = (om * vt + q[r]) / (om + 1.0);      // Eq. 12 (its z) lifted to 3-D
     nf[r] = (om * nt + N[r]) / (om + 1.0);      // Eq. 14
   }
   const double nl = sqrt(nf[0] * nf[0] + nf[1] * nf[1] + nf[2] * nf[2]);
-  for (int r = 0; r < 3; ++r) { nf[r] /= nl; pf[r] -= f.Td[r]; }
+  for (int r = 0; r < 3; ++r) { nf[r] /= nl; pf[r] -= Td[r]; }
   float vo[3], no[3];
   for (int c = 0; c < 3; ++c) {   // back to world: R^T (p - T), R^T n
-    vo[c] = (float)(f.Rd[c] * pf[0] + f.Rd[3 + c] * pf[1] + f.Rd[6 + c] * pf[2]);
-    no[c] = (float)(f.Rd[c] * nf[0] + f.Rd[3 + c] * nf[1] + f.Rd[6 + c] * nf[2]);
+    vo[c] = (float)(Rd[c] * pf[0] + Rd[3 + c] * pf[1] + Rd[6 + c] * pf[2]);
+    no[c] = (float)(Rd[c] * nf[0] + Rd[3 + c] * nf[1] + Rd[6 + c] * nf[2]);
   }
   a.md.px[i] = vo[0]; a.md.py[i] = vo[1]; a.md.pz[i] = vo[2];
   a.md.nx[i] = no[0]; a.md.ny[i] = no[1]; a.md.nz[i] = no[2];
@@ -202,6 +210,8 @@ int lift_blocks(int W, int H) { return (W * H + kLiftBlock - 1) / kLiftBlock; }
 
 __device__ __forceinline__ bool lift_pixel(const FuseArgs& a, int p) {
   const FrameView& f = a.fr;
+  double Rd[9], Td[3];
+  frame_pose(f, Rd, Td);   // the refined pose after a joint registration (NEXT-2)
   if (p >= f.W * f.H) return false;
   const float4 nm = f.nmap[p];
   return nm.w > 0.f && (nm.x != 0.f || nm.y != 0.f || nm.z != 0.f) && a.pixkey[p] == ~0ull;
@@ -284,14 +294,16 @@ __global__ void __launch_bounds__(kLiftBlock) k_lift_write(FuseArgs a, const int
   const int64_t o = base + offs[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
   lift_pos[p] = (int32_t)o;
   const FrameView& f = a.fr;
+  double Rd[9], Td[3];
+  frame_pose(f, Rd, Td);   // the refined pose after a joint registration (NEXT-2)
   const int px = p % f.W, py = p / f.W;
   double N[3], q[3];
   normal_map64(f, px, py, N, q);
-  for (int c = 0; c < 3; ++c) q[c] -= f.Td[c];
+  for (int c = 0; c < 3; ++c) q[c] -= Td[c];
   float vo[3], no[3];
   for (int c = 0; c < 3; ++c) {
-    vo[c] = (float)(f.Rd[c] * q[0] + f.Rd[3 + c] * q[1] + f.Rd[6 + c] * q[2]);
-    no[c] = (float)(f.Rd[c] * N[0] + f.Rd[3 + c] * N[1] + f.Rd[6 + c] * N[2]);
+    vo[c] = (float)(Rd[c] * q[0] + Rd[3 + c] * q[1] + Rd[6 + c] * q[2]);
+    no[c] = (float)(Rd[c] * N[0] + Rd[3 + c] * N[1] + Rd[6 + c] * N[2]);
   }
   ModelView md = a.md;
   md.px[o] = vo[0]; md.py[o] = vo[1]; md.pz[o] = vo[2];

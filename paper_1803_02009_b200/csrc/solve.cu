@@ -35,6 +35,10 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int m = a.m, n6 = 6 * m;
+  // NEXT-2: the pose row (unknown pose_node = m - 1, ~m blocks) is summed by warps, not one thread
+  const int64_t n6s = a.pose_node >= 0 ? 6 * (int64_t)a.pose_node : n6;
+  const int64_t gwarp = tid >> 5;
+  const int lane = threadIdx.x & 31;
 
   // ---- phase 0: H (both triangles) and b are final (record reduction); clear the dot slots
   if (tid < 2 * a.pcg_iters + 4) a.dots[tid] = 0.0;
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
     const float beta = it == 0 ? 0.f : (float)(rz / rz_prev);
     // Az, p = z + beta p, Ap = Az + beta Ap, p.Ap
     my = 0.0;
-    for (int64_t q = tid; q < n6; q += nth) {
+    for (int64_t q = tid; q < n6s; q += nth) {
       const int row = (int)(q / 6), c = (int)(q % 6);
       float az = a.lambda * a.z[q];
       for (int e = a.row_ptr[row]; e < a.row_ptr[row + 1]; ++e) {
@@ -79,6 +83,27 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
       a.p[q] = pn;
       a.Ap[q] = apn;
       my += (double)pn * (double)apn;
+    }
+    if (a.pose_node >= 0 && gwarp < 6) {   // NEXT-2: the dense pose row, one warp per component
+      const int row = a.pose_node, c = (int)gwarp;
+      const int64_t q = 6 * (int64_t)row + c;
+      float az = 0.f;
+      for (int e = a.row_ptr[row] + lane; e < a.row_ptr[row + 1]; e += 32) {
+        const float* Hb = a.Hval + 36 * (int64_t)e + 6 * c;
+        const float* zz = a.z + 6 * a.col[e];
+#pragma unroll
+        for (int b = 0; b < 6; ++b) az = fmaf(Hb[b], zz[b], az);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) az += __shfl_xor_sync(0xffffffffu, az, o);
+      if (lane == 0) {
+        az = fmaf(a.lambda, a.z[q], az);
+        const float pn = fmaf(beta, a.p[q], a.z[q]);
+        const float apn = fmaf(beta, a.Ap[q], az);
+        a.p[q] = pn;
+        a.Ap[q] = apn;
+        my += (double)pn * (double)apn;
+      }
     }
     s = block_sum(my, sh);
     if (threadIdx.x == 0) atomicAdd(a.dots + 1 + 2 * it, s);
@@ -120,7 +145,10 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
       if (!isfinite(a.x[6 * j + c])) atomicOr(a.numeric_flag, 1);
   grid.sync();
   if (*a.numeric_flag) return;
-  for (int64_t j = tid; j < m; j += nth) node_update(a.x + 6 * j, a.nd.Rt64 + 12 * j, a.nd.node32 + 16 * j);
+  for (int64_t j = tid; j < m; j += nth) {
+    if (j == a.pose_node) pose_update(a.x + 6 * j, a.pose);   // A37
+    else node_update(a.x + 6 * j, a.nd.Rt64 + 12 * j, a.nd.node32 + 16 * j);
+  }
 }
 
 cudaError_t launch_solve_grid(const SolveArgs& a, int num_sms, cudaStream_t s) {

@@ -222,4 +222,71 @@ __device__ inline void node_update(const float* dx, double* Rt, float* n32) {
   }
 }
 
+// ---- NEXT-2 (MIS_F_JOINT_POSE, readings A37-A40)
+// A37: R <- R Exp(dphi), T <- T + R dtau (fp64, in place; dx = [dphi, dtau])
+__device__ inline void pose_update(const float* dx, double* P) {
+  const double w0 = dx[0], w1 = dx[1], w2 = dx[2];
+  const double t2 = w0 * w0 + w1 * w1 + w2 * w2, th = sqrt(t2);
+  double A, Bc;
+  if (th < 0.05) {
+    A = 1.0 + t2 * (-1.0 / 6 + t2 * (1.0 / 120 + t2 * (-1.0 / 5040 + t2 * (1.0 / 362880))));
+    Bc = 0.5 + t2 * (-1.0 / 24 + t2 * (1.0 / 720 + t2 * (-1.0 / 40320 + t2 * (1.0 / 3628800))));
+  } else {
+    A = sin(th) / th;
+    Bc = (1.0 - cos(th)) / t2;
+  }
+  const double K[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+  double E[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double k2 = K[3 * i] * K[j] + K[3 * i + 1] * K[3 + j] + K[3 * i + 2] * K[6 + j];
+      E[3 * i + j] = (i == j ? 1.0 : 0.0) + A * K[3 * i + j] + Bc * k2;
+    }
+  double Rn[9], dT[3];
+  for (int i = 0; i < 3; ++i) {
+    dT[i] = P[3 * i] * dx[3] + P[3 * i + 1] * dx[4] + P[3 * i + 2] * dx[5];
+    for (int j = 0; j < 3; ++j) Rn[3 * i + j] = P[3 * i] * E[j] + P[3 * i + 1] * E[3 + j] + P[3 * i + 2] * E[6 + j];
+  }
+  for (int i = 0; i < 9; ++i) P[i] = Rn[i];
+  for (int i = 0; i < 3; ++i) P[9 + i] += dT[i];
+}
+
+// Eq. 10 at the current pose P against the prior P0 (R row-major 9, T 3, world -> camera):
+//  r[0..3) = wrap(e(O) - e(O0)), e = ZYX Euler angles (yaw, pitch, roll) of the scope orientation
+//  O = R^T (A38); r[3..6) = c - c0, c = -R^T T the scope position (A39); J = dr/d[dphi, dtau]
+//  under A37's increment: O' = Exp(-dphi) O, so the Euler rows are -E_s^-1 with E_s^-1 written out
+//  row by row (yaw: [tan(th) cos(psi), tan(th) sin(psi), 1], pitch: [-sin(psi), cos(psi), 0],
+//  roll: [cos(psi), sin(psi), 0] / cos(th)); c' = c - dtau + [c]x dphi.  Returns false at gimbal
+//  lock (|cos th| < 1e-6), where the orientation rows are zero.
+__device__ inline bool pose_prior_dev(const double* P0, const double* P, double* r, double* J) {
+  // O = R^T: O[i][j] = R[j][i]; yaw = atan2(O10, O00), pitch = asin(-O20), roll = atan2(O21, O22)
+  const double yaw = atan2(P[1], P[0]), pitch = asin(fmin(1.0, fmax(-1.0, -P[2]))), roll = atan2(P[5], P[8]);
+  const double yaw0 = atan2(P0[1], P0[0]), pitch0 = asin(fmin(1.0, fmax(-1.0, -P0[2]))), roll0 = atan2(P0[5], P0[8]);
+  const double d[3] = {yaw - yaw0, pitch - pitch0, roll - roll0};
+  for (int q = 0; q < 3; ++q) {
+    double v = d[q];
+    while (v > M_PI) v -= 2.0 * M_PI;
+    while (v <= -M_PI) v += 2.0 * M_PI;
+    r[q] = v;
+  }
+  double c[3], c0[3];
+  for (int q = 0; q < 3; ++q) {
+    c[q] = -(P[q] * P[9] + P[3 + q] * P[10] + P[6 + q] * P[11]);
+    c0[q] = -(P0[q] * P0[9] + P0[3 + q] * P0[10] + P0[6 + q] * P0[11]);
+    r[3 + q] = c[q] - c0[q];
+  }
+  for (int q = 0; q < 36; ++q) J[q] = 0.0;
+  J[18 + 1] = -c[2]; J[18 + 2] = c[1];     // [c]x
+  J[24 + 0] = c[2];  J[24 + 2] = -c[0];
+  J[30 + 0] = -c[1]; J[30 + 1] = c[0];
+  J[18 + 3] = J[24 + 4] = J[30 + 5] = -1.0;
+  const double cp = cos(yaw), sp = sin(yaw), ct = cos(pitch), st = sin(pitch);
+  if (fabs(ct) < 1e-6) { r[0] = r[1] = r[2] = 0.0; return false; }
+  const double tt = st / ct;
+  J[0] = -tt * cp; J[1] = -tt * sp; J[2] = -1.0;
+  J[6] = sp;       J[7] = -cp;      J[8] = 0.0;
+  J[12] = -cp / ct; J[13] = -sp / ct; J[14] = 0.0;
+  return true;
+}
+
 }  // namespace mis

@@ -440,15 +440,16 @@ __device__ __forceinline__ void mark(unsigned long long* bm, int64_t W, int a, i
   if (!(*w & bit)) atomicOr(w, bit);
 }
 
-// candidates: [tuples ntup*P][edges m*n_nbr][feature pairs nf*P][diagonal m]; tuples with a
-// negative first id are padding (gathered shards)
-__global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup_host, int K, int m, int n_nbr,
+// candidates: [tuples ntup*P][edges m*n_nbr][feature pairs nf*P][diagonal mu]; tuples with a
+// negative first id are padding (gathered shards).  mu = m unknown blocks, or m + 1 with the pose
+// (NEXT-2: tuples and feature slots then carry the pose id m as their last entry)
+__global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup_host, int K, int m, int mu, int n_nbr,
                        const int32_t* nbr, int nf, const int32_t* fidx, unsigned long long* bm, int64_t W) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int P = K * (K + 1) / 2;
   const int64_t ntup = ntup_dev ? *ntup_dev : ntup_host;
-  const int64_t ns = ntup * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P, total = ns + ne + nfp + m;
+  const int64_t ns = ntup * P, ne = (int64_t)m * n_nbr, nfp = (int64_t)nf * P, total = ns + ne + nfp + mu;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int a, b;
     if (t < ns) {
@@ -470,7 +471,7 @@ __global__ void k_mark(const int32_t* tup, const int64_t* ntup_dev, int64_t ntup
     } else {
       a = b = (int)(t - ns - ne - nfp);
     }
-    if (a < 0 || b < 0 || a >= m || b >= m) continue;
+    if (a < 0 || b < 0 || a >= mu || b >= mu) continue;
     mark(bm, W, a, b);
     if (a != b) mark(bm, W, b, a);
   }
@@ -627,9 +628,29 @@ __device__ __forceinline__ void slot_item(const PostArgs& a, int64_t t) {
   }
 }
 
+// NEXT-2 (joint pose): the tuples of the joint pattern -- every segment's K nodes, then the pose
+// id m -- and the pose row K (= m) of the feature skinning ids (slot-major, row stride nf)
+__global__ void k_joint_tuples(const int64_t* nseg_dev, int K, const int32_t* seg_nodes, int m, int32_t* out, int nf,
+                               int32_t* fidx) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t nseg = *nseg_dev, total = nseg * (K + 1) + nf;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nseg * (K + 1)) {
+      const int64_t sg = t / (K + 1);
+      const int j = (int)(t - sg * (K + 1));
+      out[t] = j < K ? seg_nodes[sg * K + j] : m;
+    } else {
+      fidx[(int64_t)K * nf + (t - nseg * (K + 1))] = m;
+    }
+  }
+}
+
 cudaError_t build_pattern(Ctx* c) {
-  const int K = c->K, P = K * (K + 1) / 2, m = c->m;
-  const int64_t W = (m + 63) / 64, words = (int64_t)m * W;
+  const bool joint = c->joint;
+  const int K = c->K + (joint ? 1 : 0), P = K * (K + 1) / 2, m = c->m, mu = m + (joint ? 1 : 0);
+  c->pattern_joint = joint;
+  const int64_t W = (mu + 63) / 64, words = (int64_t)mu * W;
   int64_t* info = c->nnz_dev.as<int64_t>();
   if (c->bitmap.bytes < (size_t)words * 8 || c->bitmap_words != words) c->bitmap_clean = false;
   CK(ensure(c, c->bitmap, words * 8));
@@ -638,7 +659,15 @@ cudaError_t build_pattern(Ctx* c) {
   c->bitmap_words = words;
   unsigned long long* bm = c->bitmap.as<unsigned long long>();
   const int grid = c->num_sms * 8;
-  launch_pdl(k_mark, dim3(grid), dim3(256), 0, c->st, c->seg_nodes.as<int32_t>(), info + 1, 0, K, m, c->prm.n_nbr, c->nbr.as<int32_t>(),
+  const int32_t* tup = c->seg_nodes.as<int32_t>();
+  if (joint) {   // tuples + pose id, pose row of the feature ids (K = k + 1 slots from here on)
+    CK(ensure(c, c->seg_nodes_j, (size_t)std::max<int64_t>(c->n, 1) * K * 4));
+    launch_pdl(k_joint_tuples, dim3(grid), dim3(256), 0, c->st, (const int64_t*)(info + 1), c->K, tup, m,
+               c->seg_nodes_j.as<int32_t>(), c->nf, c->fidx.as<int32_t>());
+    count_launches(1);
+    tup = c->seg_nodes_j.as<int32_t>();
+  }
+  launch_pdl(k_mark, dim3(grid), dim3(256), 0, c->st, tup, info + 1, 0, K, m, mu, c->prm.n_nbr, c->nbr.as<int32_t>(),
                                   c->nf, c->fidx.as<int32_t>(), bm, W);
   if (c->world > 1) {   // union over the ranks: all-gather the bitmaps and OR them (same pattern everywhere)
     CK(ensure(c, c->bitmap_all, (size_t)words * 8 * c->world));
@@ -646,16 +675,16 @@ cudaError_t build_pattern(Ctx* c) {
     launch_pdl(k_bitmap_or, dim3(grid), dim3(256), 0, c->st, words, c->world, c->bitmap_all.as<unsigned long long>(), bm);
   }
   count_launches(c->world > 1 ? 2 : 1);
-  CK(ensure(c, c->row_cnt, (size_t)(m + 1) * 4));
-  CK(ensure(c, c->row_ptr, (size_t)(m + 1) * 4));
-  CK(ensure(c, c->diag_pos, (size_t)m * 4));
+  CK(ensure(c, c->row_cnt, (size_t)(mu + 1) * 4));
+  CK(ensure(c, c->row_ptr, (size_t)(mu + 1) * 4));
+  CK(ensure(c, c->diag_pos, (size_t)mu * 4));
   CK(ensure(c, c->part, 32 * 4));
-  const int wb = (int)(((int64_t)(m + 1) * 32 + 255) / 256);
-  launch_pdl(k_row_count, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_cnt.as<int32_t>());
+  const int wb = (int)(((int64_t)(mu + 1) * 32 + 255) / 256);
+  launch_pdl(k_row_count, dim3(wb), dim3(256), 0, c->st, bm, W, mu, c->row_cnt.as<int32_t>());
   CK(cub_call(c, [&](void* t, size_t& s) {
-    return cub::DeviceScan::ExclusiveSum(t, s, c->row_cnt.as<int32_t>(), c->row_ptr.as<int32_t>(), m + 1, c->st);
+    return cub::DeviceScan::ExclusiveSum(t, s, c->row_cnt.as<int32_t>(), c->row_ptr.as<int32_t>(), mu + 1, c->st);
   }));
-  launch_plan_cluster(c->row_ptr.as<int32_t>(), m, 16, reinterpret_cast<PlanOut*>(info + 4), c->part.as<int32_t>(),
+  launch_plan_cluster(c->row_ptr.as<int32_t>(), mu, 16, reinterpret_cast<PlanOut*>(info + 4), c->part.as<int32_t>(),
                       info, c->st);
   count_launches(2);   // row count, plan (+ the CUB scan)
   CK(cudaGetLastError());
@@ -678,10 +707,11 @@ cudaError_t build_pattern(Ctx* c) {
   c->cl_max_rows = plan->max_rows;
   c->cl_max_nnz = plan->max_nnz;
   c->cl_smem = (size_t)plan->smem;
+  if (joint) c->cl_size = 0;   // the dense pose row: the grid-wide PCG (NEXT-2)
   CK(ensure(c, c->col, nnz * 4 + 4)); CK(ensure(c, c->row_of, nnz * 4 + 4));
   CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
-  CK(ensure(c, c->ulist, ((nnz - m) / 2 + 1) * 8));
-  launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, m, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
+  CK(ensure(c, c->ulist, ((nnz - mu) / 2 + 1) * 8));
+  launch_pdl(k_row_fill, dim3(wb), dim3(256), 0, c->st, bm, W, mu, c->row_ptr.as<int32_t>(), c->col.as<int32_t>(),
              c->row_of.as<int32_t>(), c->diag_pos.as<int32_t>(), info);
   c->bitmap_clean = true;
   const int64_t total = c->nseg * P + (int64_t)m * c->prm.n_nbr + (int64_t)c->nf * P;
@@ -695,9 +725,9 @@ cudaError_t build_pattern(Ctx* c) {
     CK(ensure(c, c->pcg_pc, (size_t)cs * mp * 4));
     CK(ensure(c, c->pcg_push, (size_t)cs * mr * 16 * 4));
     CK(ensure(c, c->pcg_npush, 32 * 4));   // npush[16] | incoming halo rows nin[16]
-    if (c->pcg_mask.bytes < (size_t)m * 4) {
-      CK(ensure(c, c->pcg_mask, (size_t)m * 4));
-      CK(cudaMemsetAsync(c->pcg_mask.p, 0, (size_t)m * 4, c->st));   // kept zero by k_pcg_lists
+    if (c->pcg_mask.bytes < (size_t)mu * 4) {
+      CK(ensure(c, c->pcg_mask, (size_t)mu * 4));
+      CK(cudaMemsetAsync(c->pcg_mask.p, 0, (size_t)mu * 4, c->st));   // kept zero by k_pcg_lists
     }
   }
   {
@@ -708,7 +738,7 @@ cudaError_t build_pattern(Ctx* c) {
     pa.nnz = nnz; pa.ul_blocks = nnz > 0 ? std::min<int64_t>(grid, (nnz + 255) / 256) : 0;
     pa.part = c->part.as<int32_t>(); pa.cs = clu ? c->cl_size : 0;
     pa.mask = c->pcg_mask.as<uint32_t>(); pa.nin = c->pcg_npush.as<int32_t>() + 16;
-    pa.nseg = c->nseg; pa.seg_nodes = c->seg_nodes.as<int32_t>(); pa.K = K; pa.n_nbr = c->prm.n_nbr; pa.nf = c->nf;
+    pa.nseg = c->nseg; pa.seg_nodes = tup; pa.K = K; pa.n_nbr = c->prm.n_nbr; pa.nf = c->nf;
     pa.nbr = c->nbr.as<int32_t>(); pa.fidx = c->fidx.as<int32_t>();
     pa.seg_slot = c->seg_slot.as<int32_t>(); pa.edge_slot = c->edge_slot.as<int32_t>();
     pa.feat_slot = c->feat_slot.as<int32_t>(); pa.total = total;
@@ -724,8 +754,8 @@ cudaError_t build_pattern(Ctx* c) {
   }
   CK(cudaGetLastError());
   // accumulators (K3 commits atomically into them) and solver buffers
-  const size_t m6 = 6 * (size_t)m;
-  c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)m + m6;
+  const size_t m6 = 6 * (size_t)mu;
+  c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)mu + m6;
   // accumulators: every finalisation re-zeroes what it read, so they need a memset only when
   // (re)allocated or after an assembly that did not reach its finalisation
   if (c->acc.bytes < c->acc_floats * 4 || c->energy.bytes < (size_t)kEnergyDoubles * 8) c->acc_dirty = true;
@@ -737,7 +767,7 @@ cudaError_t build_pattern(Ctx* c) {
     c->acc_dirty = false;
   }
   CK(ensure(c, c->Hval, (size_t)nnz * 36 * 4));
-  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)m * 36 * 4));
+  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)mu * 36 * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
   CK(ensure(c, c->p, m6 * 4)); CK(ensure(c, c->Ap, m6 * 4));
   CK(ensure(c, c->dots, (2 * (size_t)c->prm.pcg_iters + 8) * 8));

@@ -20,6 +20,7 @@ MIS_MEM_HOST, MIS_MEM_DEVICE = 0, 1
 MIS_MAX_GN, MIS_MAX_K = 32, 8
 MIS_F_FINAL_ENERGY, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 4, 8
 MIS_F_LM = 16   # Levenberg-Marquardt (include/mis.h)
+MIS_F_JOINT_POSE = 32   # NEXT-2 joint global pose (include/mis.h)
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
 
@@ -35,7 +36,8 @@ class mis_params(C.Structure):
                 ("w_data", C.c_float), ("w_point", C.c_float), ("w_reg", C.c_float), ("w_corr", C.c_float),
                 ("eps_d_mm", C.c_float), ("eps_n_deg", C.c_float),
                 ("tau_z_mm", C.c_float), ("delta_deg", C.c_float), ("trunc_mm", C.c_float), ("omega_max", C.c_float),
-                ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_float), ("flags", C.c_uint32)]
+                ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_float), ("flags", C.c_uint32),
+                ("w_r", C.c_float), ("w_p", C.c_float)]
 
 
 class mis_intrinsics(C.Structure):
@@ -49,7 +51,8 @@ class mis_report(C.Structure):
                 ("n_assoc", C.c_int64 * (MIS_MAX_GN + 1)),
                 ("pcg_rel_res", C.c_float * MIS_MAX_GN),
                 ("nnzb", C.c_int64), ("n_segments", C.c_int64), ("solver_cluster", C.c_int32),
-                ("reserved", C.c_int32), ("n_guard", C.c_int64 * (MIS_MAX_GN + 1))]
+                ("reserved", C.c_int32), ("n_guard", C.c_int64 * (MIS_MAX_GN + 1)),
+                ("energy_pose", (C.c_double * 2) * (MIS_MAX_GN + 1))]
 
 
 if not os.path.exists(LIB_PATH):
@@ -75,6 +78,8 @@ _sig = {
     "mis_get_nodes": ([_V, C.c_int, _V], C.c_int),
     "mis_get_nodes_f64": ([_V, _V], C.c_int),
     "mis_get_graph": ([_V, C.c_int, _V], C.c_int),
+    "mis_get_pose": ([_V, _V], C.c_int),
+    "mis_dbg_set_pose": ([_V, _V], C.c_int),
     "mis_get_nbr": ([_V, C.c_int, _V], C.c_int),
     "mis_warp": ([_V, C.c_int, _V, _V], C.c_int),
     "mis_fuse": ([_V, C.c_int, _V, C.c_int32, _P(C.c_int64), _V], C.c_int),
@@ -232,7 +237,8 @@ def report_dict(rep: mis_report):
                 pcg_rel_res=np.array([rep.pcg_rel_res[i] for i in range(it)]),
                 nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster,
                 n_guard=np.array([rep.n_guard[i] for i in range(it + 1)]),
-                accepted=np.array([rep.n_guard[i] for i in range(it + 1)]))   # MIS_F_LM decisions
+                accepted=np.array([rep.n_guard[i] for i in range(it + 1)]),   # MIS_F_LM decisions
+                energy_pose=np.array([[rep.energy_pose[i][q] for q in range(2)] for i in range(it + 1)]))
 
 
 def mis_get_nodes(ctx, out):
@@ -244,6 +250,16 @@ def mis_get_nodes_f64(ctx, m):
     out = np.zeros((m, 12), np.float64)
     _check(ctx, _lib.mis_get_nodes_f64(ctx, _ptr(out)))
     return out
+
+
+def mis_get_pose(ctx):
+    out = np.zeros(12, np.float64)
+    _check(ctx, _lib.mis_get_pose(ctx, _ptr(out)))
+    return out
+
+
+def mis_dbg_set_pose(ctx, pose):
+    _check(ctx, _lib.mis_dbg_set_pose(ctx, _ptr(np.ascontiguousarray(pose, np.float64))))
 
 
 def mis_get_graph(ctx, out):

@@ -39,10 +39,11 @@ def test_library_exports_every_declared_symbol(lib_built):
 
 def test_binding_loads_and_matches_header(lib_built):
     from paper_1803_02009_b200 import mis as M
-    assert M.mis_abi_version() == 1
+    assert M.mis_abi_version() == 2
     assert sorted(M.EXPORTED) == declared()
     p = M.mis_default_params()
     assert (p.k, p.n_nbr, p.w_reg, p.w_corr, p.eps_d_mm, p.eps_n_deg) == (4, 4, 1e4, 10.0, 15.0, 10.0)
+    assert (p.w_r, p.w_p) == (1e6, 1000.0)   # Eq. 10 priors, P:598 (struct layout matches the header)
 
 
 def test_sm100a_sass_present(lib_built):
