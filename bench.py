@@ -263,42 +263,60 @@ def run_mis(args, rank, world, local_rank):
     M.mis_prof_enable(ctx.ptr, False)
     breakdown = M.mis_prof_read(ctx.ptr, reset=True)
 
-    # ---------------- NEXT-3: the same step with Levenberg-Marquardt registration (MIS_F_LM),
-    # device-timed the same way (events at step boundaries, L2 flushed), single GPU only
-    lm_out = None
-    if world == 1 and not args.no_lm:
-        plm = params_for(cfg, M)
-        plm.flags |= M.MIS_F_LM
-        ctx_lm = M.Context(plm, device=local_rank, stream=stream.cuda_stream)
+    # ---------------- NEXT-3 / NEXT-2: the same step with Levenberg-Marquardt registration (MIS_F_LM)
+    # and with the joint global-pose refinement (MIS_F_JOINT_POSE), device-timed the same way (events at
+    # step boundaries, L2 flushed), single GPU only
+    def variant_leg(flag):
+        pv = params_for(cfg, M)
+        pv.flags |= flag
+        cv = M.Context(pv, device=local_rank, stream=stream.cuda_stream)
 
-        def step_lm():
-            M.mis_set_model(ctx_lm.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"],
+        def step_v():
+            M.mis_set_model(cv.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"],
                             capacity=cap)
-            M.mis_set_graph(ctx_lm.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
-            M.mis_register(ctx_lm.ptr, depth_d, intr, pose, fs_d, fd_d, report=False)
-            M.mis_warp(ctx_lm.ptr)
-            return M.mis_fuse(ctx_lm.ptr, rgb_d, 1)
+            M.mis_set_graph(cv.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+            M.mis_register(cv.ptr, depth_d, intr, pose, fs_d, fd_d, report=False)
+            M.mis_warp(cv.ptr)
+            return M.mis_fuse(cv.ptr, rgb_d, 1)
 
         for _ in range(args.warmup):
-            step_lm()
+            step_v()
         torch.cuda.synchronize()
         evl = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         for k in range(K):
             flush.zero_()
             evl[k][0].record(stream)
-            step_lm()
+            step_v()
             evl[k][1].record(stream)
         torch.cuda.synchronize()
-        lm_ms = sum(a.elapsed_time(b) for a, b in evl) / K
-        M.mis_set_model(ctx_lm.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
-        M.mis_set_graph(ctx_lm.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
-        rl = M.report_dict(M.mis_register(ctx_lm.ptr, depth_d, intr, pose, fs_d, fd_d, report=True))
+        v_ms = sum(a.elapsed_time(b) for a, b in evl) / K
+        M.mis_set_model(cv.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
+        M.mis_set_graph(cv.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+        rv = M.report_dict(M.mis_register(cv.ptr, depth_d, intr, pose, fs_d, fd_d, report=True))
+        pose_v = M.mis_get_pose(cv.ptr)
+        cv.close()
+        return v_ms, rv, pose_v
+
+    lm_out = None
+    if world == 1 and not args.no_lm:
+        lm_ms, rl, _ = variant_leg(M.MIS_F_LM)
         lm_out = {"ms_per_step": round(lm_ms, 4), "value": round(1e3 / lm_ms, 3), "unit": UNIT,
                   "what": "same step with Levenberg-Marquardt registration (MIS_F_LM: G trials + final evaluation, "
                           "accept / reject and Marquardt damping on the device)",
                   "accepted": [int(v) for v in rl["accepted"]],
                   "E_first": float(rl["energy"][0, 4]), "E_final_trial": float(rl["energy"][cfg.gn_iters, 4])}
-        ctx_lm.close()
+    joint_out = None
+    if world == 1 and not args.no_lm:
+        jp_ms, rj, pose_j = variant_leg(M.MIS_F_JOINT_POSE)
+        p0 = np.asarray(pose, np.float64)
+        joint_out = {"ms_per_step": round(jp_ms, 4), "value": round(1e3 / jp_ms, 3), "unit": UNIT,
+                     "what": "same step with the joint global-pose refinement (MIS_F_JOINT_POSE, NEXT-2: the pose as "
+                             "unknown m with the Eq. 10 priors w_r = 1e6, w_p = 1000; grid-wide PCG for the dense pose "
+                             "row)",
+                     "solver_cluster": int(rj["solver_cluster"]), "nnzb": int(rj["nnzb"]),
+                     "E_first": float(rj["energy"][0, 4]), "E_last_iter": float(rj["energy"][cfg.gn_iters - 1, 4]),
+                     "E_r_E_p_last": [float(x) for x in rj["energy_pose"][cfg.gn_iters - 1]],
+                     "pose_change_mm": float(np.linalg.norm(pose_j[9:] - p0[9:]))}
 
     # ---------------- NEXT-1: Alg. 3 filtering (mis_filter, K14) of the fused model, single GPU only.
     # Each timed filter runs on the model a full step just produced (the step itself untimed); the
@@ -505,6 +523,7 @@ def run_mis(args, rank, world, local_rank):
         "ms_per_step_with_kernel_events": round(kev["dev_ms_max"] / K, 4),
         "pcg_phases_us_last_launch": pcg_phases,
         "lm": lm_out,
+        "joint_pose": joint_out,
         "filter": filt_out,
         "sequence": seq_out,
         "gpu_launches": int(launches),

@@ -111,3 +111,24 @@ def test_pose_errors():
         M.Context(M.mis_default_params(k=8, flags=M.MIS_F_JOINT_POSE))
     with pytest.raises(M.MisError):
         M.Context(M.mis_default_params(w_r=-1.0))
+
+
+def test_pose_register_full_c3():
+    """NEXT-2 at the bench configuration (C3: 300k points, 999 nodes, 5 GN x 10 PCG, ORB features)
+    with the paper's prior weights and a wrong ORB-SLAM pose: nodes and pose against the oracle."""
+    from tests.test_gpu_fullsize import problem
+    sc, pb, fr, _ = problem("c3")
+    prior = perturbed_pose(np.array(fr.s.pose[:]))
+    ctx, sc2 = joint_ctx(sc, pb, prior)
+    rep = M.report_dict(M.mis_register(ctx.ptr))
+    assert rep["status"] == 0
+    m = pb.g.shape[0]
+    Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+    pg = M.mis_get_pose(ctx.ptr)
+    prm = oracle_params(ctx.params, joint_pose=1, w_r=ctx.params.w_r, w_p=ctx.params.w_p)
+    Ro, po, Eo, nao = O.register_pose(prm, pb, ofr(sc2))
+    terr = np.linalg.norm(Rg[:, 9:] - Ro[:, 9:], axis=1)
+    rerr = np.array([rot_err(Rg[j, :9].reshape(3, 3), Ro[j, :9].reshape(3, 3)) for j in range(m)])
+    assert terr.max() < 0.01 and rerr.max() < 1e-4, (terr.max(), rerr.max())
+    assert np.linalg.norm(pg[9:] - po[9:]) < 0.01 and np.abs(pg[:9] - po[:9]).max() < 1e-4
+    assert np.allclose(rep["energy"][:, 4], Eo[:, 6], rtol=1e-3)
