@@ -40,7 +40,7 @@ class or_params(C.Structure):
                 ("tau_z", C.c_double), ("delta_deg", C.c_double), ("trunc", C.c_double), ("omega_max", C.c_double),
                 ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_double),
                 ("solve_mode", C.c_int32), ("lm", C.c_int32), ("lm_mu0", C.c_double),
-                ("joint_pose", C.c_int32), ("w_r", C.c_double), ("w_p", C.c_double)]
+                ("joint_pose", C.c_int32), ("w_r", C.c_double), ("w_p", C.c_double), ("w_rot", C.c_double)]
 
 
 class or_frame(C.Structure):
@@ -100,6 +100,24 @@ def lib():
             L.or_euler_zyx.argtypes = [C.c_void_p, C.c_void_p]
             L.or_pose_prior.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_pose_prior.restype = C.c_int32
+            L.or_warp_aff.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_associate_aff.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_rot.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.or_system_aff.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]
+            L.or_system_aff.restype = C.c_int64
+            L.or_residuals_aff.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+            L.or_residuals_aff.restype = C.c_int64
+            L.or_solve_aff.argtypes = [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_double, C.c_int32, C.c_int32, C.c_void_p]
+            L.or_solve_aff.restype = C.c_int32
+            L.or_register_aff.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
+            L.or_warp_model_aff.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_warp_model.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_fuse.argtypes = [P(or_params), P(or_model), P(or_frame), C.c_void_p, C.c_int32, C.c_int32,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -132,7 +150,7 @@ def _i32(a):
 PAPER_DEFAULTS = dict(k=4, n_nbr=4, w_data=1.0, w_pt=1.0, w_reg=1e4, w_corr=10.0,
                       eps_d=15.0, eps_n_deg=10.0, tau_z=10.0, delta_deg=10.0, trunc=40.0, omega_max=10.0,
                       gn_iters=5, pcg_iters=10, lambda_=1e-4, solve_mode=1, lm=0, lm_mu0=1e-3,
-                      joint_pose=0, w_r=1e6, w_p=1000.0)
+                      joint_pose=0, w_r=1e6, w_p=1000.0, w_rot=1000.0)
 
 
 def set_threads(n: int) -> None:
@@ -342,6 +360,102 @@ def register_pose(prm: or_params, pb: Problem, fr: Frame, Rt0=None, pose0=None, 
     if with_accepted:
         return Rt, pose, E, na, acc
     return Rt, pose, E, na
+
+
+# ---------------------------------------------------------------- NEXT-4: affine nodes + E_rot
+def identity_affine(m):
+    """m x 12 affine state: A_j = I (row-major), t_j = 0."""
+    return identity_state(m)
+
+
+def rot_terms(A):
+    """Eq. 5 residuals (6) and their Jacobian (6 x 9, A row-major)."""
+    r = np.zeros(6); J = np.zeros(54)
+    lib().or_rot(_p(np.ascontiguousarray(A, np.float64).reshape(9)), _p(r), _p(J))
+    return r, J.reshape(6, 9)
+
+
+def warp_aff(pb: Problem, At, pose):
+    n = pb.xyz.shape[0]
+    At = np.ascontiguousarray(At, np.float64)
+    out = [np.zeros((n, 3)) for _ in range(4)]
+    ok = np.zeros(n, np.uint8)
+    lib().or_warp_aff(C.byref(pb.s), pb.k, _p(At), _p(np.ascontiguousarray(pose, np.float64)),
+                      *[_p(o) for o in out], _p(ok))
+    return (*out, ok)
+
+
+def associate_aff(prm: or_params, pb: Problem, fr: Frame, At):
+    n = pb.xyz.shape[0]
+    At = np.ascontiguousarray(At, np.float64)
+    pix = np.zeros(n, np.int32); why = np.zeros(n, np.uint8); mg = np.zeros(n)
+    lib().or_associate_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(pix), _p(why), _p(mg))
+    return pix, why, mg
+
+
+def system_aff(prm: or_params, pb: Problem, fr: Frame, At, fskin=None):
+    """12 x 12 block normal equations of the affine model; energy[6]."""
+    m = pb.g.shape[0]
+    At = np.ascontiguousarray(At, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    rhs = np.zeros(12 * m); E = np.zeros(6); na = np.zeros(1, np.int64)
+    z = np.zeros(1, np.int32); zd = np.zeros(144)
+    nb = lib().or_system_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(fidx), _p(fw), 0,
+                             _p(z), _p(z), _p(zd), _p(rhs), _p(E), _p(na))
+    rows = np.zeros(nb, np.int32); cols = np.zeros(nb, np.int32); vals = np.zeros((nb, 144))
+    lib().or_system_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(fidx), _p(fw), nb,
+                        _p(rows), _p(cols), _p(vals), _p(rhs), _p(E), _p(na))
+    return dict(rows=rows, cols=cols, vals=vals.reshape(nb, 12, 12), rhs=rhs, energy=E, n_assoc=int(na[0]))
+
+
+def dense_H_aff(sysd, m):
+    H = np.zeros((12 * m, 12 * m))
+    for r, c, B in zip(sysd["rows"], sysd["cols"], sysd["vals"]):
+        H[12 * r:12 * r + 12, 12 * c:12 * c + 12] += B
+        if r != c:
+            H[12 * c:12 * c + 12, 12 * r:12 * r + 12] += B.T
+    return H
+
+
+def residuals_aff(prm: or_params, pb: Problem, fr: Frame, At, pix_frozen, fskin=None):
+    m = pb.g.shape[0]
+    At = np.ascontiguousarray(At, np.float64)
+    fidx, fw = (fskin if fskin is not None else feature_skin(pb)[:2])
+    fidx = _i32(fidx.reshape(-1, pb.k)); fw = np.ascontiguousarray(fw, np.float64)
+    cap = 4 * pb.xyz.shape[0] + 3 * m * pb.n_nbr + 3 * pb.fsrc.shape[0] + 6 * m
+    r = np.zeros(cap); J = np.zeros((cap, 12 * m))
+    nr = lib().or_residuals_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(_i32(pix_frozen)), _p(fidx),
+                                _p(fw), cap, _p(r), _p(J))
+    assert nr >= 0
+    return r[:nr], J[:nr]
+
+
+def solve_aff(sysd, m, lam, mode, pcg_iters):
+    x = np.zeros(12 * m)
+    nb = len(sysd["rows"])
+    vals = np.ascontiguousarray(sysd["vals"].reshape(nb, 144), np.float64)
+    it = lib().or_solve_aff(m, nb, _p(_i32(sysd["rows"])), _p(_i32(sysd["cols"])), _p(vals),
+                            _p(np.ascontiguousarray(sysd["rhs"], np.float64)), lam, mode, pcg_iters, _p(x))
+    return x, it
+
+
+def register_aff(prm: or_params, pb: Problem, fr: Frame, At0=None):
+    """Affine-node Gauss-Newton: returns (At, E (G+1 x 6), n_assoc)."""
+    m = pb.g.shape[0]
+    At = identity_affine(m) if At0 is None else np.array(At0, np.float64, copy=True)
+    G = prm.gn_iters
+    E = np.zeros((G + 1, 6)); na = np.zeros(G + 1, np.int64)
+    lib().or_register_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(E), _p(na))
+    return At, E, na
+
+
+def warp_model_aff(pb: Problem, At):
+    n, m = pb.xyz.shape[0], pb.g.shape[0]
+    At = np.ascontiguousarray(At, np.float64)
+    xyz = np.zeros((n, 3)); nrm = np.zeros((n, 3)); g = np.zeros((m, 3))
+    lib().or_warp_model_aff(C.byref(pb.s), pb.k, _p(At), _p(xyz), _p(nrm), _p(g))
+    return xyz, nrm, g
 
 
 def warp_model(pb: Problem, Rt):

@@ -1259,3 +1259,496 @@ int64_t or_regenerate_nodes(int64_t n, const float* xyz, float grid, int32_t n_n
 }
 
 }  // extern "C"
+
+// =====================================================================================
+// O9 (NEXT-4): affine nodes A_j + E_rot ("affine matrix A_j", Eq. 1 with A_j, Eq. 4-5
+// E_rot, Eq. 6 with A_j; readings A41-A45).  Node state At (m x 12): A_j row-major (9), t_j (3);
+// 12 unknowns per node [dA_j row-major, dt_j] with the additive update A_j += dA_j, t_j += dt_j
+// (A41).  Normals warp by the inverse transpose, n~ = normalize(R sum_j w_j A_j^-T n), A_j itself
+// if |det A_j| < 1e-9 (A43).  Written out separately from the SE(3) path above (12 x 12
+// blocks); the same Gauss-Newton loop (fixed G, P), the same solve modes.
+// =====================================================================================
+namespace {
+
+typedef std::array<double, 144> B12;
+
+M3 aff_A(const double* At, int j) { M3 A; for (int a = 0; a < 9; ++a) A[a] = At[12 * j + a]; return A; }
+V3 aff_t(const double* At, int j) { return v3(At[12 * j + 9], At[12 * j + 10], At[12 * j + 11]); }
+
+// inverse transpose of A (cofactor matrix / det); A itself when |det| < 1e-9 (A43)
+M3 inv_transpose(const M3& A) {
+  M3 C;   // cofactors C[i][j] = (-1)^(i+j) minor(i, j)
+  C[0] = A[4] * A[8] - A[5] * A[7]; C[1] = A[5] * A[6] - A[3] * A[8]; C[2] = A[3] * A[7] - A[4] * A[6];
+  C[3] = A[2] * A[7] - A[1] * A[8]; C[4] = A[0] * A[8] - A[2] * A[6]; C[5] = A[1] * A[6] - A[0] * A[7];
+  C[6] = A[1] * A[5] - A[2] * A[4]; C[7] = A[2] * A[3] - A[0] * A[5]; C[8] = A[0] * A[4] - A[1] * A[3];
+  const double det = A[0] * C[0] + A[1] * C[1] + A[2] * C[2];
+  if (std::fabs(det) < 1e-9) return A;
+  for (int a = 0; a < 9; ++a) C[a] /= det;   // (A^-1)^T = cof(A) / det
+  return C;
+}
+
+struct WarpedA {
+  bool ok;
+  double wn[8];
+  V3 d[8];          // d_j = v - g_j
+  V3 x_hat, m_hat, vt, nt;
+};
+
+// Eq. 1 with affine A_j, weights normalised (R-A6); normal by A_j^-T (A43)
+WarpedA warp_point_aff(const V3& v, const V3& n, int k, const int32_t* idx, const double* wraw, const float* g,
+                       const double* At, const double* pose) {
+  WarpedA o;
+  o.ok = false;
+  double W = 0;
+  for (int s = 0; s < k; ++s) W += wraw[s];
+  if (!(W > 0)) return o;
+  o.x_hat = v3(0, 0, 0);
+  o.m_hat = v3(0, 0, 0);
+  for (int s = 0; s < k; ++s) {
+    const int j = idx[s];
+    o.wn[s] = wraw[s] / W;
+    const V3 gj = load3(g + 3 * j);
+    o.d[s] = sub(v, gj);
+    o.x_hat = add(o.x_hat, scale(add(add(mul(aff_A(At, j), o.d[s]), gj), aff_t(At, j)), o.wn[s]));
+    o.m_hat = add(o.m_hat, scale(mul(inv_transpose(aff_A(At, j)), n), o.wn[s]));
+  }
+  const M3 R = pose_R(pose);
+  o.vt = add(mul(R, o.x_hat), pose_T(pose));
+  const double ml = norm(o.m_hat);
+  if (ml < 1e-12) return o;
+  o.nt = mul(R, scale(o.m_hat, 1.0 / ml));
+  o.ok = true;
+  return o;
+}
+
+// the Eq. 7 gates on an affine-warped point (same gates as associate_point)
+Assoc associate_aff(const or_params* prm, const or_frame* f, const WarpedA& w) {
+  Warped s;
+  s.ok = w.ok;
+  s.vt = w.vt;
+  s.nt = w.nt;
+  return associate_point(prm, f, s);
+}
+
+// Jacobian of the warped camera-frame point w.r.t. node slot s (3 x 12): columns (r, c) of dA
+// (row-major) = w_j d_c R e_r; columns of dt = w_j R
+void jac_point_aff(const M3& R, double wj, const V3& d, double* J /*3 x 12*/) {
+  for (int q = 0; q < 3; ++q) {
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) J[12 * q + 3 * r + c] = wj * d[c] * R[3 * q + r];
+    for (int c = 0; c < 3; ++c) J[12 * q + 9 + c] = wj * R[3 * q + c];
+  }
+}
+
+// Eq. 5: r = [c1.c2, c1.c3, c2.c3, c1.c1 - 1, c2.c2 - 1, c3.c3 - 1] of the columns
+// c_i of A; J (6 x 9) w.r.t. A row-major (A[r][c] is entry r of column c)
+void rot_rows(const M3& A, double* r, double* J) {
+  V3 c[3];
+  for (int i = 0; i < 3; ++i) c[i] = v3(A[i], A[3 + i], A[6 + i]);
+  const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {1, 2, 2, 0, 1, 2};
+  for (int q = 0; q < 6; ++q) {
+    const int a = pa[q], b = pb[q];
+    r[q] = dot(c[a], c[b]) - (a == b ? 1.0 : 0.0);
+    for (int e = 0; e < 9; ++e) J[9 * q + e] = 0.0;
+    for (int row = 0; row < 3; ++row) {   // d(c_a . c_b) / dA[row][a] = c_b[row], / dA[row][b] = c_a[row]
+      J[9 * q + 3 * row + a] += c[b][row];
+      J[9 * q + 3 * row + b] += c[a][row];
+    }
+  }
+}
+
+struct SystemA {
+  int m;
+  std::map<std::pair<int, int>, B12> blk;   // upper blocks (j <= l)
+  std::vector<double> rhs;
+  double E[5];   // E_data, E_pt, E_reg, E_corr, E_rot
+  int64_t n_assoc;
+  explicit SystemA(int m_) : m(m_), rhs(12 * m_, 0.0), n_assoc(0) { for (int a = 0; a < 5; ++a) E[a] = 0; }
+  // H(a, b) += w Ja^T Jb over `rows` rows (Ja, Jb: rows x 12)
+  void add_pair(int a, const double* Ja, int b, const double* Jb, int rows, double w) {
+    const bool sw = a > b;
+    B12& B = blk[sw ? std::make_pair(b, a) : std::make_pair(a, b)];
+    const double* X = sw ? Jb : Ja;
+    const double* Y = sw ? Ja : Jb;
+    for (int i = 0; i < 12; ++i)
+      for (int j = 0; j < 12; ++j) {
+        double s = 0;
+        for (int q = 0; q < rows; ++q) s += X[12 * q + i] * Y[12 * q + j];
+        B[12 * i + j] += w * s;
+      }
+  }
+  void add_rhs(int a, const double* Ja, const double* r, int rows, double w) {
+    for (int i = 0; i < 12; ++i) {
+      double s = 0;
+      for (int q = 0; q < rows; ++q) s += Ja[12 * q + i] * r[q];
+      rhs[12 * a + i] -= w * s;
+    }
+  }
+  // every slot pair of one residual group (ids may repeat: both orders then)
+  void add_group(const int32_t* ids, const double* J, int ks, int rows, const double* r, double w) {
+    for (int a = 0; a < ks; ++a) {
+      for (int b = 0; b < ks; ++b) {
+        if (ids[a] > ids[b] || (ids[a] == ids[b] && a > b)) continue;
+        add_pair(ids[a], J + 12 * rows * a, ids[b], J + 12 * rows * b, rows, w);
+        if (ids[a] == ids[b] && a != b) add_pair(ids[b], J + 12 * rows * b, ids[a], J + 12 * rows * a, rows, w);
+      }
+      add_rhs(ids[a], J + 12 * rows * a, r, rows, w);
+    }
+  }
+};
+
+double total_energy_aff(const or_params* prm, const double* E) {
+  return prm->w_data * E[0] + prm->w_pt * E[1] + prm->w_reg * E[2] + prm->w_corr * E[3] + prm->w_rot * E[4];
+}
+
+void assemble_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At, const int32_t* fidx,
+                  const double* fw, SystemA* S) {
+  const int k = prm->k;
+  const M3 R = pose_R(f->pose);
+  double Jpl[8 * 12], Jpt[8 * 36];
+  for (int64_t i = 0; i < p->n; ++i) {   // O9a: data (Eq. 8) and point-to-point terms
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    WarpedA w = warp_point_aff(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, At, f->pose);
+    Assoc as = associate_aff(prm, f, w);
+    if (as.pix < 0) continue;
+    S->n_assoc++;
+    const V3 dd = sub(w.vt, as.q);
+    const double rpl = dot(as.N, dd), rpt[3] = {dd[0], dd[1], dd[2]};
+    for (int s = 0; s < k; ++s) {
+      jac_point_aff(R, w.wn[s], w.d[s], Jpt + 36 * s);
+      for (int c = 0; c < 12; ++c)   // plane row = N^T (point rows)
+        Jpl[12 * s + c] = as.N[0] * Jpt[36 * s + c] + as.N[1] * Jpt[36 * s + 12 + c] + as.N[2] * Jpt[36 * s + 24 + c];
+    }
+    S->E[0] += rpl * rpl;
+    S->E[1] += rpt[0] * rpt[0] + rpt[1] * rpt[1] + rpt[2] * rpt[2];
+    S->add_group(p->idx + k * i, Jpl, k, 1, &rpl, prm->w_data);
+    S->add_group(p->idx + k * i, Jpt, k, 3, rpt, prm->w_pt);
+  }
+  // O9b: Eq. 6 with A_j: e = A_j (g_l - g_j) + g_j + t_j - g_l - t_l
+  for (int j = 0; j < p->m; ++j)
+    for (int s = 0; s < prm->n_nbr; ++s) {
+      const int l = p->nbr[prm->n_nbr * j + s];
+      if (l < 0) continue;
+      const V3 gj = load3(p->g + 3 * j), gl = load3(p->g + 3 * l), d = sub(gl, gj);
+      const V3 e = sub(add(add(mul(aff_A(At, j), d), gj), aff_t(At, j)), add(gl, aff_t(At, l)));
+      double Jj[36], Jl[36];
+      for (int a = 0; a < 36; ++a) Jj[a] = Jl[a] = 0.0;
+      for (int q = 0; q < 3; ++q) {
+        for (int c = 0; c < 3; ++c) Jj[12 * q + 3 * q + c] = d[c];   // de_q / dA_j[q][c]
+        Jj[12 * q + 9 + q] = 1.0;
+        Jl[12 * q + 9 + q] = -1.0;
+      }
+      const double ev[3] = {e[0], e[1], e[2]};
+      S->E[2] += dot(e, e);
+      S->add_pair(j, Jj, j, Jj, 3, prm->w_reg);
+      S->add_pair(l, Jl, l, Jl, 3, prm->w_reg);
+      S->add_pair(j, Jj, l, Jl, 3, prm->w_reg);
+      S->add_rhs(j, Jj, ev, 3, prm->w_reg);
+      S->add_rhs(l, Jl, ev, 3, prm->w_reg);
+    }
+  // O9c: Eq. 9 features
+  for (int q = 0; q < p->nf; ++q) {
+    double W = 0;
+    for (int s = 0; s < k; ++s) W += fw[k * q + s];
+    if (!(W > 0)) continue;
+    WarpedA w = warp_point_aff(load3(p->fsrc + 3 * q), v3(0, 0, 1), k, fidx + k * q, fw + k * q, p->g, At, f->pose);
+    const V3 e = sub(w.vt, load3(p->fdst + 3 * q));
+    const double ev[3] = {e[0], e[1], e[2]};
+    double Jf[8 * 36];
+    for (int s = 0; s < k; ++s) jac_point_aff(R, w.wn[s], w.d[s], Jf + 36 * s);
+    S->E[3] += dot(e, e);
+    S->add_group(fidx + k * q, Jf, k, 3, ev, prm->w_corr);
+  }
+  // O9d: Eq. 4-5 E_rot on every node (A42)
+  for (int j = 0; j < p->m; ++j) {
+    double r[6], J9[54], J[72];
+    rot_rows(aff_A(At, j), r, J9);
+    for (int q = 0; q < 6; ++q) {
+      for (int c = 0; c < 12; ++c) J[12 * q + c] = c < 9 ? J9[9 * q + c] : 0.0;
+      S->E[4] += r[q] * r[q];
+    }
+    S->add_pair(j, J, j, J, 6, prm->w_rot);
+    S->add_rhs(j, J, r, 6, prm->w_rot);
+  }
+}
+
+// O9e: solve (H + lambda I) x = rhs: EXACT (dense Cholesky, or PCG to 1e-12) or MIRROR (block-Jacobi
+// PCG with the GPU's P; M_j = (H_jj + lambda I + mu_j I)^-1, mu_j = 1e-9 tr(H_jj)/12, A17)
+void spmv_aff(const SystemA& S, double lambda, const std::vector<double>& x, std::vector<double>& y) {
+  std::fill(y.begin(), y.end(), 0.0);
+  for (const auto& kv : S.blk) {
+    const int j = kv.first.first, l = kv.first.second;
+    const B12& B = kv.second;
+    for (int a = 0; a < 12; ++a)
+      for (int b = 0; b < 12; ++b) {
+        y[12 * j + a] += B[12 * a + b] * x[12 * l + b];
+        if (j != l) y[12 * l + b] += B[12 * a + b] * x[12 * j + a];
+      }
+  }
+  for (size_t i = 0; i < y.size(); ++i) y[i] += lambda * x[i];
+}
+
+int solve_aff(const SystemA& S, double lambda, int mode, int pcg_iters, std::vector<double>& x) {
+  const int n = 12 * S.m;
+  if (mode == 0 && n <= 1200) {
+    std::vector<double> A((size_t)n * n, 0.0);
+    for (const auto& kv : S.blk) {
+      const int j = kv.first.first, l = kv.first.second;
+      for (int a = 0; a < 12; ++a)
+        for (int b = 0; b < 12; ++b) {
+          A[(size_t)(12 * j + a) * n + 12 * l + b] += kv.second[12 * a + b];
+          if (j != l) A[(size_t)(12 * l + b) * n + 12 * j + a] += kv.second[12 * a + b];
+        }
+    }
+    for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += lambda;
+    x.assign(n, 0.0);
+    if (!cholesky(A, n)) return -1;
+    chol_solve(A, n, S.rhs.data(), x.data());
+    return 0;
+  }
+  std::vector<double> Minv(144 * (size_t)S.m, 0.0);
+  for (int j = 0; j < S.m; ++j) {
+    std::vector<double> A(144, 0.0);
+    auto it = S.blk.find(std::make_pair(j, j));
+    if (it != S.blk.end()) for (int a = 0; a < 144; ++a) A[a] = it->second[a];
+    double tr = 0;
+    for (int a = 0; a < 12; ++a) tr += A[13 * a];
+    for (int a = 0; a < 12; ++a) A[13 * a] += lambda + 1e-9 * tr / 12.0;
+    if (!cholesky(A, 12)) continue;
+    for (int c = 0; c < 12; ++c) {
+      double e[12] = {0}, col[12];
+      e[c] = 1.0;
+      chol_solve(A, 12, e, col);
+      for (int r = 0; r < 12; ++r) Minv[144 * j + 12 * r + c] = col[r];
+    }
+  }
+  auto applyM = [&](const std::vector<double>& r, std::vector<double>& z) {
+    for (int j = 0; j < S.m; ++j)
+      for (int a = 0; a < 12; ++a) {
+        double s = 0;
+        for (int b = 0; b < 12; ++b) s += Minv[144 * j + 12 * a + b] * r[12 * j + b];
+        z[12 * j + a] = s;
+      }
+  };
+  const int max_it = mode == 1 ? pcg_iters : 20 * n;
+  const double rel_tol = mode == 1 ? 0.0 : 1e-12;
+  std::vector<double> r(S.rhs), z(n), p(n), Ap(n);
+  x.assign(n, 0.0);
+  applyM(r, z);
+  p = z;
+  double rz = vdot(r, z), b2 = vdot(S.rhs, S.rhs);
+  int it = 0;
+  for (; it < max_it; ++it) {
+    if (rel_tol > 0 && vdot(r, r) <= rel_tol * rel_tol * b2) break;
+    if (rz == 0) break;
+    spmv_aff(S, lambda, p, Ap);
+    const double pAp = vdot(p, Ap);
+    if (!(pAp > 0)) break;
+    const double alpha = rz / pAp;
+    for (int i = 0; i < n; ++i) { x[i] += alpha * p[i]; r[i] -= alpha * Ap[i]; }
+    applyM(r, z);
+    const double rz_new = vdot(r, z), beta = rz_new / rz;
+    rz = rz_new;
+    for (int i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+  }
+  return it;
+}
+
+}  // namespace
+
+extern "C" {
+
+void or_warp_aff(const or_problem* p, int32_t k, const double* At, const double pose[12], double* x_hat,
+                 double* n_hat, double* vt, double* nt, uint8_t* ok) {
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    WarpedA w = warp_point_aff(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, At, pose);
+    ok[i] = w.ok ? 1 : 0;
+    for (int a = 0; a < 3; ++a) {
+      x_hat[3 * i + a] = w.ok ? w.x_hat[a] : 0.0;
+      n_hat[3 * i + a] = w.ok ? w.m_hat[a] / norm(w.m_hat) : 0.0;
+      vt[3 * i + a] = w.ok ? w.vt[a] : 0.0;
+      nt[3 * i + a] = w.ok ? w.nt[a] : 0.0;
+    }
+  }
+}
+
+void or_associate_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At, int32_t* pix,
+                      uint8_t* why, double* margin) {
+  const int k = prm->k;
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    WarpedA w = warp_point_aff(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, At, f->pose);
+    Assoc a = associate_aff(prm, f, w);
+    pix[i] = a.pix;
+    why[i] = a.why;
+    margin[i] = a.margin;
+  }
+}
+
+void or_rot(const double A[9], double r[6], double J[54]) {
+  M3 M;
+  for (int a = 0; a < 9; ++a) M[a] = A[a];
+  rot_rows(M, r, J);
+}
+
+int64_t or_system_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At,
+                      const int32_t* fidx, const double* fw, int64_t cap, int32_t* brow, int32_t* bcol, double* bval,
+                      double* rhs, double energy[6], int64_t* n_assoc) {
+  SystemA S(p->m);
+  assemble_aff(prm, p, f, At, fidx, fw, &S);
+  int64_t nb = 0;
+  for (auto it = S.blk.begin(); it != S.blk.end(); ++it, ++nb) {
+    if (nb >= cap) continue;
+    brow[nb] = it->first.first;
+    bcol[nb] = it->first.second;
+    for (int a = 0; a < 144; ++a) bval[144 * nb + a] = it->second[a];
+  }
+  for (int i = 0; i < 12 * p->m; ++i) rhs[i] = S.rhs[i];
+  for (int a = 0; a < 5; ++a) energy[a] = S.E[a];
+  energy[5] = total_energy_aff(prm, S.E);
+  *n_assoc = S.n_assoc;
+  return nb;
+}
+
+int64_t or_residuals_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At,
+                         const int32_t* pix_frozen, const int32_t* fidx, const double* fw, int64_t cap_rows, double* r,
+                         double* J) {
+  const int k = prm->k, ncol = 12 * p->m;
+  const M3 R = pose_R(f->pose);
+  const double sd = std::sqrt(prm->w_data), sp = std::sqrt(prm->w_pt), sr = std::sqrt(prm->w_reg),
+               sc = std::sqrt(prm->w_corr), so = std::sqrt(prm->w_rot);
+  int64_t row = 0;
+  double Jp[36];
+  for (int64_t i = 0; i < p->n; ++i) {
+    if (pix_frozen[i] < 0) continue;
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    WarpedA w = warp_point_aff(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, At, f->pose);
+    if (!w.ok) continue;
+    const int px = pix_frozen[i] % f->W, py = pix_frozen[i] / f->W;
+    V3 N;
+    if (!pixel_normal(f, px, py, &N)) continue;
+    const V3 q = back_project(f, px, py, (double)f->depth[pix_frozen[i]]);
+    if (row + 4 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 4 * ncol);
+    const V3 dd = sub(w.vt, q);
+    r[row] = sd * dot(N, dd);
+    for (int c = 0; c < 3; ++c) r[row + 1 + c] = sp * dd[c];
+    for (int s = 0; s < k; ++s) {
+      const int j = p->idx[k * i + s];
+      jac_point_aff(R, w.wn[s], w.d[s], Jp);
+      for (int c = 0; c < 12; ++c) {
+        J0[12 * j + c] += sd * (N[0] * Jp[c] + N[1] * Jp[12 + c] + N[2] * Jp[24 + c]);
+        for (int qq = 0; qq < 3; ++qq) J0[(size_t)(1 + qq) * ncol + 12 * j + c] += sp * Jp[12 * qq + c];
+      }
+    }
+    row += 4;
+  }
+  for (int j = 0; j < p->m; ++j)
+    for (int s = 0; s < prm->n_nbr; ++s) {
+      const int l = p->nbr[prm->n_nbr * j + s];
+      if (l < 0) continue;
+      const V3 gj = load3(p->g + 3 * j), gl = load3(p->g + 3 * l), d = sub(gl, gj);
+      const V3 e = sub(add(add(mul(aff_A(At, j), d), gj), aff_t(At, j)), add(gl, aff_t(At, l)));
+      if (row + 3 > cap_rows) return -1;
+      double* J0 = J + (size_t)row * ncol;
+      std::memset(J0, 0, sizeof(double) * 3 * ncol);
+      for (int qq = 0; qq < 3; ++qq) {
+        r[row + qq] = sr * e[qq];
+        for (int c = 0; c < 3; ++c) J0[(size_t)qq * ncol + 12 * j + 3 * qq + c] += sr * d[c];
+        J0[(size_t)qq * ncol + 12 * j + 9 + qq] += sr;
+        J0[(size_t)qq * ncol + 12 * l + 9 + qq] -= sr;
+      }
+      row += 3;
+    }
+  for (int q = 0; q < p->nf; ++q) {
+    double W = 0;
+    for (int s = 0; s < k; ++s) W += fw[k * q + s];
+    if (!(W > 0)) continue;
+    WarpedA w = warp_point_aff(load3(p->fsrc + 3 * q), v3(0, 0, 1), k, fidx + k * q, fw + k * q, p->g, At, f->pose);
+    const V3 e = sub(w.vt, load3(p->fdst + 3 * q));
+    if (row + 3 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 3 * ncol);
+    for (int a = 0; a < 3; ++a) r[row + a] = sc * e[a];
+    for (int s = 0; s < k; ++s) {
+      const int j = fidx[k * q + s];
+      jac_point_aff(R, w.wn[s], w.d[s], Jp);
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 12; ++c) J0[(size_t)a * ncol + 12 * j + c] += sc * Jp[12 * a + c];
+    }
+    row += 3;
+  }
+  for (int j = 0; j < p->m; ++j) {
+    double rr[6], J9[54];
+    rot_rows(aff_A(At, j), rr, J9);
+    if (row + 6 > cap_rows) return -1;
+    double* J0 = J + (size_t)row * ncol;
+    std::memset(J0, 0, sizeof(double) * 6 * ncol);
+    for (int q = 0; q < 6; ++q) {
+      r[row + q] = so * rr[q];
+      for (int c = 0; c < 9; ++c) J0[(size_t)q * ncol + 12 * j + c] = so * J9[9 * q + c];
+    }
+    row += 6;
+  }
+  return row;
+}
+
+int32_t or_solve_aff(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
+                     const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x) {
+  SystemA S(m);
+  for (int64_t b = 0; b < nblk; ++b) {
+    B12& B = S.blk[std::make_pair(brow[b], bcol[b])];
+    for (int a = 0; a < 144; ++a) B[a] = bval[144 * b + a];
+  }
+  for (int i = 0; i < 12 * m; ++i) S.rhs[i] = rhs[i];
+  std::vector<double> xs;
+  const int32_t it = solve_aff(S, lambda, mode, pcg_iters, xs);
+  for (int i = 0; i < 12 * m; ++i) x[i] = xs[i];
+  return it;
+}
+
+// O9f: fixed-G Gauss-Newton over the affine nodes; energy (G+1) x 6 (E_data, E_pt, E_reg, E_corr,
+// E_rot, weighted total); At (m x 12) initial state on entry, result on exit
+void or_register_aff(const or_params* prm, const or_problem* p, const or_frame* f, double* At, double* energy,
+                     int64_t* n_assoc) {
+  std::vector<int32_t> fidx;
+  std::vector<double> fw;
+  feature_skin(p, prm->k, fidx, fw);
+  for (int it = 0; it <= prm->gn_iters; ++it) {
+    SystemA S(p->m);
+    assemble_aff(prm, p, f, At, fidx.data(), fw.data(), &S);
+    for (int a = 0; a < 5; ++a) energy[6 * it + a] = S.E[a];
+    energy[6 * it + 5] = total_energy_aff(prm, S.E);
+    n_assoc[it] = S.n_assoc;
+    if (it == prm->gn_iters) break;
+    std::vector<double> x;
+    solve_aff(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+    for (int j = 0; j < p->m; ++j)   // A41: additive update
+      for (int a = 0; a < 12; ++a) At[12 * j + a] += x[12 * j + a];
+  }
+}
+
+// O9g: the converged affine field applied (live world state), normals by A^-T, nodes g + t (A45)
+void or_warp_model_aff(const or_problem* p, int32_t k, const double* At, double* xyz_out, double* nrm_out,
+                       double* g_out) {
+  const double pose[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+  for (int64_t i = 0; i < p->n; ++i) {
+    double wr[8];
+    wraw_of(p, k, i, wr);
+    WarpedA w = warp_point_aff(load3(p->xyz + 3 * i), load3(p->nrm + 3 * i), k, p->idx + k * i, wr, p->g, At, pose);
+    for (int a = 0; a < 3; ++a) {
+      xyz_out[3 * i + a] = w.ok ? w.x_hat[a] : (double)p->xyz[3 * i + a];
+      nrm_out[3 * i + a] = w.ok ? w.nt[a] : (double)p->nrm[3 * i + a];
+    }
+  }
+  for (int j = 0; j < p->m; ++j)
+    for (int a = 0; a < 3; ++a) g_out[3 * j + a] = (double)p->g[3 * j + a] + At[12 * j + 9 + a];
+}
+
+}  // extern "C"

@@ -30,6 +30,7 @@ typedef struct {
   double lm_mu0;                        /* initial Marquardt damping (1e-3)    */
   int32_t joint_pose;                   /* 1: joint global-pose refinement (NEXT-2, below) */
   double w_r, w_p;                      /* Eq. 10 prior weights, P:598 (1e6, 1000)    */
+  double w_rot;                         /* Eq. 4 weight, P:598 (1000); the _aff functions */
 } or_params;
 /* joint_pose (NEXT-2, readings A37-A40): the pose of Eq. 1 becomes unknown
  * number m (after the m nodes; "only 6 more variables") with the local increment
@@ -135,6 +136,28 @@ int64_t or_residuals_pose(const or_params* prm, const or_problem* p, const or_fr
                           const double* fw, int64_t cap_rows, double* r, double* J);
 void or_register_pose(const or_params* prm, const or_problem* p, const or_frame* f, double* Rt, double* pose_io,
                       double* energy, int64_t* n_assoc, int32_t* accepted);
+/* ---- NEXT-4: affine nodes A_j + E_rot (Eq. 1, Eq. 4-6; readings A41-A45) ----
+ * At: m x 12 (A_j row-major 9, t_j 3); 12 unknowns per node [dA_j row-major, dt_j], additive
+ * update; normals warp by A_j^-T (A itself if |det| < 1e-9).  Blocks 12 x 12 (144 doubles),
+ * rhs 12m, energy[6] = E_data, E_pt, E_reg, E_corr, E_rot, weighted total (w_rot). */
+void or_warp_aff(const or_problem* p, int32_t k, const double* At, const double pose[12], double* x_hat,
+                 double* n_hat, double* vt, double* nt, uint8_t* ok);
+void or_associate_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At, int32_t* pix,
+                      uint8_t* why, double* margin);
+/* Eq. 5 residuals r[6] (c1.c2, c1.c3, c2.c3, |c1|^2-1, |c2|^2-1, |c3|^2-1) and J (6 x 9, A row-major) */
+void or_rot(const double A[9], double r[6], double J[54]);
+int64_t or_system_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At,
+                      const int32_t* fidx, const double* fw, int64_t cap, int32_t* brow, int32_t* bcol, double* bval,
+                      double* rhs, double energy[6], int64_t* n_assoc);
+int64_t or_residuals_aff(const or_params* prm, const or_problem* p, const or_frame* f, const double* At,
+                         const int32_t* pix_frozen, const int32_t* fidx, const double* fw, int64_t cap_rows, double* r,
+                         double* J);
+int32_t or_solve_aff(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
+                     const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x);
+void or_register_aff(const or_params* prm, const or_problem* p, const or_frame* f, double* At, double* energy,
+                     int64_t* n_assoc);
+void or_warp_model_aff(const or_problem* p, int32_t k, const double* At, double* xyz_out, double* nrm_out,
+                       double* g_out);
 /* O4: apply the field: live world state x_hat, unit normals; advanced nodes g+t. */
 void or_warp_model(const or_problem* p, int32_t k, const double* Rt, double* xyz_out, double* nrm_out,
                    double* g_out);

@@ -1180,3 +1180,176 @@ def test_pose_joint_lm_accepted_energy_decreasing():
     assert (np.diff(ea) < 0).all(), ea
     Ef = O.system_pose(prm, pb, fr, Rt, pose)["energy"][6]
     assert abs(Ef - ea[-1]) < 1e-9 * ea[0]
+
+
+# ------------------------------------------------------------------ NEXT-4: affine nodes + E_rot (A41-A45)
+def random_affine(m, rng, rot_rad=0.02, shear=0.02, trans_mm=0.3):
+    """A_j = rotation x (I + small general matrix), t_j random: a non-orthonormal state."""
+    At = np.zeros((m, 12))
+    for j in range(m):
+        At[j, :9] = (O.exp_so3(rng.normal(0, rot_rad, 3)) @ (np.eye(3) + rng.normal(0, shear, (3, 3)))).ravel()
+        At[j, 9:] = rng.normal(0, trans_mm, 3)
+    return At
+
+
+def test_rot_spec_examples_and_jacobian():
+    """Rot(I) = 0, Rot(2I) = 27 ((4-1)^2 x 3), Rot(30 deg about z) = 0; E_rot = 0 iff
+    orthonormal; the Jacobian against central differences."""
+    assert np.abs(O.rot_terms(np.eye(3))[0]).max() == 0
+    assert abs((O.rot_terms(2 * np.eye(3))[0] ** 2).sum() - 27.0) < 1e-12
+    assert (O.rot_terms(rot([0, 0, 1], 30.0))[0] ** 2).sum() < 1e-24
+    rng = np.random.default_rng(4001)
+    for _ in range(10):
+        A = rng.normal(0, 1, (3, 3))
+        r, J = O.rot_terms(A)
+        # textbook: the Gram matrix of the columns minus I
+        G = A.T @ A - np.eye(3)
+        assert np.allclose(r, [G[0, 1], G[0, 2], G[1, 2], G[0, 0], G[1, 1], G[2, 2]], atol=1e-12)
+        Jfd = np.zeros((6, 9))
+        for e in range(9):
+            d = np.zeros(9); d[e] = 1e-6
+            Jfd[:, e] = (O.rot_terms(A.ravel() + d)[0] - O.rot_terms(A.ravel() - d)[0]) / 2e-6
+        assert np.abs(J - Jfd).max() < 1e-8
+        assert (r ** 2).sum() > 0   # a random matrix is not orthonormal
+
+
+def test_aff_normal_warp_golden_and_tangent_invariant():
+    """A = diag(2,1,1), n = (1,0,0) -> (1,0,0); the inverse transpose keeps warped tangents
+    orthogonal to warped normals: (A u).(A^-T n) = u.n = 0 for random A."""
+    pb = single_node_problem([[0.5, 0.2, 50.0]], [[1, 0, 0]])
+    At = O.identity_affine(2)
+    At[0, :9] = np.diag([2.0, 1.0, 1.0]).ravel()
+    _, nh, _, nt, ok = O.warp_aff(pb, At, pose12())
+    assert ok[0] and np.allclose(nt[0], [1, 0, 0], atol=1e-15)
+    rng = np.random.default_rng(4002)
+    for _ in range(20):
+        A = np.eye(3) + rng.normal(0, 0.3, (3, 3))
+        n = rng.normal(0, 1, 3); n /= np.linalg.norm(n)
+        n = n.astype(np.float32).astype(np.float64)   # what the problem stores
+        u = np.cross(n, rng.normal(0, 1, 3))
+        pb = single_node_problem([[1.0, 2.0, 3.0]], [n])
+        At = O.identity_affine(2)
+        At[0, :9] = A.ravel()
+        _, nh, _, _, ok = O.warp_aff(pb, At, pose12())
+        assert ok[0] and abs((A @ u) @ nh[0]) < 1e-12 * np.linalg.norm(A @ u)
+
+
+def test_aff_reduces_to_se3_on_rotations():
+    """With every A_j a rotation the affine model is the SE(3) model: same warp, association,
+    data / point / regulariser / feature energies, and E_rot = 0 (two separate code paths)."""
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    Rt = random_state(m, np.random.default_rng(4003), 0.02, 0.3)
+    prm = O.params()
+    x1 = O.warp(pb, Rt, np.array(fr.s.pose[:]))
+    x2 = O.warp_aff(pb, Rt, np.array(fr.s.pose[:]))
+    for a, b in zip(x1[:4], x2[:4]):
+        assert np.abs(a - b).max() < 1e-12
+    p1, w1, _ = O.associate(prm, pb, fr, Rt)
+    p2, w2, _ = O.associate_aff(prm, pb, fr, Rt)
+    assert (p1 == p2).all() and (w1 == w2).all()
+    e1 = O.system(prm, pb, fr, Rt)["energy"]
+    e2 = O.system_aff(prm, pb, fr, Rt)["energy"]
+    assert np.allclose(e1[:4], e2[:4], rtol=1e-12, atol=1e-12) and e2[4] < 1e-20
+
+
+def _aff_fd(prm, pb, fr, At, h=1e-6):
+    pix, _, _ = O.associate_aff(prm, pb, fr, At)
+    fsk = O.feature_skin(pb)[:2]
+    r0, J = O.residuals_aff(prm, pb, fr, At, pix, fsk)
+    Jfd = np.zeros_like(J)
+    for j in range(pb.g.shape[0]):
+        for c in range(12):
+            Ap = At.copy(); Ap[j, c] += h
+            Am = At.copy(); Am[j, c] -= h
+            Jfd[:, 12 * j + c] = (O.residuals_aff(prm, pb, fr, Ap, pix, fsk)[0] -
+                                  O.residuals_aff(prm, pb, fr, Am, pix, fsk)[0]) / (2 * h)
+    return J, Jfd, pix
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_aff_finite_difference_jacobians_small(seed):
+    prm, pb, fr, _ = _small_problem(seed)
+    prm.w_rot = 3.0
+    At = random_affine(pb.g.shape[0], np.random.default_rng(4100 + seed))
+    J, Jfd, pix = _aff_fd(prm, pb, fr, At)
+    assert (pix >= 0).sum() >= 5
+    rel = np.abs(J - Jfd).max() / np.abs(J).max()
+    assert rel < 1e-6, rel
+
+
+def test_aff_assembly_equals_dense_jtj_c1():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    At = random_affine(m, np.random.default_rng(4004))
+    prm = O.params()
+    s = O.system_aff(prm, pb, fr, At)
+    pix, _, _ = O.associate_aff(prm, pb, fr, At)
+    r, J = O.residuals_aff(prm, pb, fr, At, pix)
+    H = O.dense_H_aff(s, m)
+    Hd = J.T @ J
+    assert np.abs(H - Hd).max() < 1e-10 * np.abs(Hd).max()
+    assert np.abs(s["rhs"] + J.T @ r).max() < 1e-10 * np.abs(J.T @ r).max()
+    assert abs(s["energy"][5] - r @ r) < 1e-10 * (r @ r)
+    assert s["energy"][4] > 0 and s["n_assoc"] == int((pix >= 0).sum())
+    # with the features' rows and E_rot's the system is symmetric PSD
+    ev = np.linalg.eigvalsh(0.5 * (H + H.T))
+    assert ev.min() > -1e-10 * ev.max()
+
+
+def test_aff_gn_step_is_dense_solve_and_additive_update():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    prm = O.params(gn_iters=1, solve_mode=0)
+    At0 = random_affine(m, np.random.default_rng(4005))
+    pix, _, _ = O.associate_aff(prm, pb, fr, At0)
+    r, J = O.residuals_aff(prm, pb, fr, At0, pix)
+    x = np.linalg.solve(J.T @ J + prm.lambda_ * np.eye(12 * m), -J.T @ r)
+    At, E, na = O.register_aff(prm, pb, fr, At0)
+    assert np.abs(At - (At0 + x.reshape(m, 12))).max() < 1e-8
+    assert abs(E[0, 5] - r @ r) < 1e-10 * (r @ r)
+
+
+def test_aff_mirror_pcg_is_textbook_pcg():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    prm = O.params()
+    s = O.system_aff(prm, pb, fr, random_affine(m, np.random.default_rng(4006)))
+    Hd = O.dense_H_aff(s, m)
+    A = Hd + prm.lambda_ * np.eye(12 * m)
+    Minv = np.zeros_like(Hd)
+    for j in range(m):
+        B = Hd[12 * j:12 * j + 12, 12 * j:12 * j + 12]
+        Minv[12 * j:12 * j + 12, 12 * j:12 * j + 12] = np.linalg.inv(B + (prm.lambda_ + 1e-9 * np.trace(B) / 12) *
+                                                                     np.eye(12))
+    for P in (1, 10):
+        x_ref = _textbook_pcg(A, s["rhs"], Minv, P)
+        x, it = O.solve_aff(s, m, prm.lambda_, 1, P)
+        assert it == P and np.abs(x - x_ref).max() < 1e-8 * np.abs(x_ref).max()
+    x, _ = O.solve_aff(s, m, prm.lambda_, 0, 0)
+    assert np.abs(A @ x - s["rhs"]).max() < 1e-9 * np.abs(s["rhs"]).max()
+
+
+def test_aff_rigid_motion_recovered():
+    """P2 for the affine model: a noise-free rigid tissue motion (Q, c) is recovered with
+    A_j = Q (E_rot = 0 there) and t_j = (Q - I) g_j + c."""
+    Q, c = rot([1, -2, 0.5], 1.5), np.array([0.8, -0.5, 0.6])
+    pb, fr = _rigid_scene(Q, c)
+    prm = O.params(w_pt=0.0, gn_iters=10, solve_mode=0)
+    At, E, _ = O.register_aff(prm, pb, fr)
+    g = pb.g.astype(np.float64)
+    assert np.abs(At[:, :9] - Q.ravel()).max() < 1e-4
+    assert np.linalg.norm(At[:, 9:] - (g @ (Q - np.eye(3)).T + c), axis=1).max() < 0.01
+    assert E[-1, 5] < 1e-3 * E[0, 5]
+
+
+def test_aff_warp_model_closed_forms():
+    sc, pb, fr, _ = scene_problem("c1")
+    m = pb.g.shape[0]
+    xyz, nrm, g = O.warp_model_aff(pb, O.identity_affine(m))
+    assert np.abs(xyz - pb.xyz).max() < 1e-5 and np.abs(g - pb.g).max() == 0
+    At = O.identity_affine(m)
+    At[:, 9:] = [1.0, -2.0, 0.5]       # common translation: every point moves by it, nodes advance
+    xyz, nrm, g = O.warp_model_aff(pb, At)
+    assert np.abs(xyz - (pb.xyz.astype(np.float64) + [1.0, -2.0, 0.5])).max() < 1e-9
+    assert np.abs(g - (pb.g.astype(np.float64) + [1.0, -2.0, 0.5])).max() < 1e-12
