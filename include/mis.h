@@ -98,6 +98,16 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    mis_get_pose.  Solved by the grid-wide PCG (the pose row is
                                    dense).  Requires k <= 7 and world == 1; not with MIS_F_LM
                                    (MIS_E_ARG)                                                      */
+#define MIS_F_AFFINE      64u   /* NEXT-4 (Eq. 1, Eq. 4-6; readings A41-A45): every node carries
+                                   the paper's general 3x3 matrix A_j instead of a rotation -- 12
+                                   unknowns per node [dA_j row-major, dt_j], additive update,
+                                   12 x 12 blocks -- with E_rot (Eq. 4-5: the columns' Gram matrix
+                                   minus I, weight w_rot) and Eq. 6 with A_j; normals warp by
+                                   A_j^-T (A_j itself if |det A_j| < 1e-9).  Node states in the
+                                   R9_t3 arrays of mis_get_nodes / mis_dbg_set_nodes are then
+                                   A (row-major 9), t.  Gauss-Newton with the grid-wide PCG;
+                                   requires k <= 4 and world == 1; not with MIS_F_LM or
+                                   MIS_F_JOINT_POSE (MIS_E_ARG)                                     */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {
@@ -119,6 +129,7 @@ typedef struct {
   uint32_t flags;       /* MIS_F_*                                                         */
   float w_r;            /* Eq. 10 orientation prior weight, 1e6, MIS_F_JOINT_POSE  */
   float w_p;            /* Eq. 10 position prior weight, 1000, MIS_F_JOINT_POSE    */
+  float w_rot;          /* Eq. 4 E_rot weight, 1000, MIS_F_AFFINE                  */
 } mis_params;
 
 /* Per-registration report (all host memory). */
@@ -138,6 +149,8 @@ typedef struct {
                                           final one) was accepted, else 0; Gauss-Newton: 0        */
   double energy_pose[MIS_MAX_GN + 1][2]; /* MIS_F_JOINT_POSE: E_r, E_p per iteration (unweighted;
                                           their weighted sum is part of energy[i][4]); else 0     */
+  double energy_rot[MIS_MAX_GN + 1];   /* MIS_F_AFFINE: E_rot per iteration (unweighted; w_rot E_rot
+                                          is part of energy[i][4]); else 0                        */
 } mis_report;
 
 int32_t mis_abi_version(void);
@@ -309,7 +322,9 @@ mis_status mis_dbg_associate(mis_ctx* ctx, mis_mem mem, int32_t* pix, uint8_t* w
  * rows sorted by column): row_ptr (m+1), col (nnzb), val (nnzb x 36,
  * row-major 6x6, unknowns [dtheta, dt] per node), rhs (6m) = -J^T r, energy[5].
  * With MIS_F_JOINT_POSE the pose is unknown m: row_ptr (m+2), rhs 6(m+1), and
- * energy[4] includes w_r E_r + w_p E_p.
+ * energy[4] includes w_r E_r + w_p E_p.  With MIS_F_AFFINE the blocks are 12 x 12
+ * (val nnzb x 144, unknowns [dA row-major, dt] per node), rhs 12m, energy[4]
+ * includes w_rot E_rot.
  * With val == NULL only *nnzb is returned.  Host memory only. */
 mis_status mis_dbg_system(mis_ctx* ctx, int32_t* row_ptr, int32_t* col, float* val, float* rhs,
                           double energy[5], int64_t* nnzb);

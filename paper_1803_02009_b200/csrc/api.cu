@@ -121,15 +121,16 @@ FrameView frame_view(Ctx* c) {
 AccView acc_view(Ctx* c) {
   AccView a;
   float* base = c->acc.as<float>();
-  const size_t nz = (size_t)c->nnzb, m = (size_t)sys_m(c);
+  const size_t nz = (size_t)c->nnzb, m = (size_t)sys_m(c), B = (size_t)sys_b(c);
   // all accumulated atomically (K3 float4 / float2 adds, K4 / K5), zeroed every iteration:
   // data | mom | rhs_data (padded to 4 floats: 16-byte aligned node moments) | node_mom | graph | rhs_graph
+  // (B x B blocks, B = 6, or 12 for the affine nodes of NEXT-4)
   a.data = base;
-  a.mom = a.data + nz * 36;
+  a.mom = a.data + nz * B * B;
   a.rhs_data = a.mom + nz * 16;
-  a.node_mom = a.rhs_data + ((6 * m + 3) & ~(size_t)3);
+  a.node_mom = a.rhs_data + ((B * m + 3) & ~(size_t)3);
   a.graph = a.node_mom + 12 * m;
-  a.rhs_graph = a.graph + nz * 36;
+  a.rhs_graph = a.graph + nz * B * B;
   a.energy = c->energy.as<double>();
   return a;
 }
@@ -414,8 +415,10 @@ static mis_status check_params(const mis_params* p) {
       !(p->omega_max >= 1) || !(p->lambda >= 0) || !std::isfinite(p->tau_z_mm) || !std::isfinite(p->trunc_mm) ||
       !std::isfinite(p->eps_d_mm) || !(p->delta_deg > 0) || !(p->delta_deg < 180) || !(p->eps_n_deg < 180) ||
       !std::isfinite(p->omega_max) || !std::isfinite(p->lambda) || p->n_nbr > 64 || !(p->w_r >= 0) ||
-      !(p->w_p >= 0) || !std::isfinite(p->w_r) || !std::isfinite(p->w_p))
+      !(p->w_p >= 0) || !std::isfinite(p->w_r) || !std::isfinite(p->w_p) || !(p->w_rot >= 0) ||
+      !std::isfinite(p->w_rot))
     return MIS_E_ARG;
+  if ((p->flags & MIS_F_AFFINE) && (p->k > 4 || (p->flags & (MIS_F_LM | MIS_F_JOINT_POSE)))) return MIS_E_ARG;
   if ((p->flags & MIS_F_JOINT_POSE) && (p->k > MIS_MAX_K - 1 || (p->flags & MIS_F_LM))) return MIS_E_ARG;
   return MIS_OK;
 }
@@ -433,6 +436,7 @@ void mis_default_params(mis_params* o) {
   o->tau_z_mm = 10.0f; o->delta_deg = 10.0f; o->trunc_mm = 40.0f; o->omega_max = 10.0f;
   o->gn_iters = 5; o->pcg_iters = 10; o->lambda = 1e-4f; o->flags = 0;
   o->w_r = 1e6f; o->w_p = 1000.0f;   // Eq. 10 prior weights, MIS_F_JOINT_POSE
+  o->w_rot = 1000.0f;                 // Eq. 4 weight, MIS_F_AFFINE
 }
 
 const char* mis_last_error(const mis_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -530,8 +534,9 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
       4 * (m + 1), 4 * (m + 1), 4 * m, 128, 4 * nnz + 4, 4 * nnz + 4, 4 * nnz + 4, 4 * nnz + 4,
       ((nnz - m) / 2 + 1) * 8, (n * P + 1) * 4, (m * nn + 1) * 4, (nf * P + 1) * 4,
       cs * (mr + 1) * 4, cs * mp * 4, cs * mr * 64, 128, 4 * m,              // cluster PCG lists
-      nnz * 88 * 4 + (6 * m + 3) * 4 + 48 * m + 24 * m, kEnergyDoubles * 8,  // accumulators
-      144 * nnz, 24 * m, 144 * m, 5 * 24 * m, (2 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
+      // accumulators, system and PCG sized for 12 x 12 blocks (the affine nodes of NEXT-4)
+      nnz * 304 * 4 + (12 * m + 3) * 4 + 48 * m + 48 * m, kEnergyDoubles * 8,  // accumulators
+      576 * nnz, 48 * m, 576 * m, 5 * 48 * m, (2 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
       144 * nnz, 24 * m, 96 * m,                                            // LM second system, kept nodes
       (K + 2) * 16 * n,                                                     // K3a -> K3b state
       4 * px, 16 * px, 32 * px, 12 * px, 8 * px, 4 * px, (2 * ((px + 255) / 256) + 4) * 4,   // frame, fusion
@@ -844,6 +849,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   const bool joint = c->pattern_joint;   // NEXT-2: the pose as factor slot k / unknown m
   const int KS = c->K + (joint ? 1 : 0);
   a.pose_cur = joint ? c->posebuf.as<double>() : nullptr;
+  const bool aff = c->pattern_affine;   // NEXT-4
+  a.affine = aff ? 1 : 0;
   if (joint) a.seg_nodes = c->seg_nodes_j.as<int32_t>();
   TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(c->n, 1)));
   a.pstate = c->pstate.as<float4>();
@@ -853,7 +860,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
   const bool graph_terms = c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0;   // K4/K5 on rank 0
   AsmGraphArgs gA;
-  if (graph_terms) {
+  {   // (filled always: the affine model's E_rot terms need it without edges or features)
     gA.nd = node_view(c);
     gA.n_nbr = c->prm.n_nbr;
     gA.nbr = c->nbr.as<int32_t>();
@@ -872,14 +879,20 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     gA.K = c->K;
     gA.KS = KS;
     gA.pose_cur = a.pose_cur;
+    gA.w_rot = c->prm.w_rot;
   }
-  if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch
+  if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch (affine: K4/K5/E_rot in their own)
     ProfScope ps(c, P_POINTS, 1);
     launch_assoc_points(c->K, a, graph_terms ? &gA : nullptr, c->st);
   }
+  if (aff) {   // the affine graph terms include E_rot on every node: always (rank 0)
+    ProfScope ps(c, P_GRAPH, 1);
+    if (c->rank == 0) launch_assemble_graph_aff(gA, c->st);
+  }
   if (a.nchunk > 0) {
     ProfScope ps(c, P_ACCUM, 1);
-    launch_accum_points(KS, a, c->num_sms, c->st);
+    if (aff) launch_accum_points_aff(c->K, a, c->num_sms, c->st);
+    else launch_accum_points(KS, a, c->num_sms, c->st);
   }
   TRY(c, cudaGetLastError());
   if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
@@ -899,6 +912,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     r.w_r = c->prm.w_r;
     r.w_p = c->prm.w_p;
     r.rep_pose = rep_pose(c);
+    r.w_rot = c->prm.w_rot;
+    r.rep_rot = rep_rot(c);
     r.upper_of = c->upper_of.as<int32_t>();
     r.lower_of = c->lower_of.as<int32_t>();
     r.diag_pos = c->diag_pos.as<int32_t>();
@@ -919,7 +934,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     r.Hval_alt = lm ? c->Hval2.as<float>() : nullptr;
     r.rhs_alt = lm ? c->rhs2.as<float>() : nullptr;
     if (lm) r.Minv = nullptr;   // the damped inverses are built by the solver once it has decided
-    launch_finalize(r, c->st);
+    if (aff) launch_finalize_aff(r, c->st);
+    else launch_finalize(r, c->st);
   }
   c->acc_dirty = false;
   TRY(c, cudaGetLastError());
@@ -932,6 +948,7 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.K = c->K;
   s.pose_node = c->pattern_joint ? c->m : -1;   // NEXT-2
   s.pose = c->pattern_joint ? c->posebuf.as<double>() : nullptr;
+  s.block = sys_b(c);   // NEXT-4: 12 x 12 blocks
   s.nnzb = c->nnzb;
   s.row_ptr = c->row_ptr.as<int32_t>();
   s.col = c->col.as<int32_t>();
@@ -1020,6 +1037,9 @@ static mis_status prepare(Ctx* c) {
   c->joint = (c->prm.flags & MIS_F_JOINT_POSE) != 0;
   if (c->joint && c->world > 1) return fail(c, MIS_E_ARG, "MIS_F_JOINT_POSE: single GPU only");
   if (c->joint != c->pattern_joint) c->pattern_valid = false;   // the pose row / column come or go
+  c->affine = (c->prm.flags & MIS_F_AFFINE) != 0;
+  if (c->affine && c->world > 1) return fail(c, MIS_E_ARG, "MIS_F_AFFINE: single GPU only");
+  if (c->affine != c->pattern_affine) c->pattern_valid = false;   // 12 x 12 blocks come or go
   if (c->dirty) TRY(c, run_build_order(c));
   if (!c->pattern_valid) {
     {
@@ -1059,6 +1079,7 @@ static mis_status fill_report(Ctx* c, mis_report* rep, int iters) {
     rep->n_guard[i] = (int64_t)llround(na[MIS_MAX_GN + 1 + i]);
     rep->energy_pose[i][0] = blk[kRepP + 2 * i];
     rep->energy_pose[i][1] = blk[kRepP + 2 * i + 1];
+    rep->energy_rot[i] = blk[kRepO + i];
   }
   rep->nnzb = c->nnzb;
   rep->n_segments = c->nseg;
@@ -1229,8 +1250,9 @@ mis_status mis_dbg_system(mis_ctx* c, int32_t* row_ptr, int32_t* col, float* val
   if ((s = assemble(c, false, 0)) != MIS_OK) return s;
   if (row_ptr) TRY(c, cudaMemcpyAsync(row_ptr, c->row_ptr.p, (size_t)(sys_m(c) + 1) * 4, cudaMemcpyDeviceToHost, c->st));
   if (col) TRY(c, cudaMemcpyAsync(col, c->col.p, (size_t)c->nnzb * 4, cudaMemcpyDeviceToHost, c->st));
-  TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * 144, cudaMemcpyDeviceToHost, c->st));
-  if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)sys_m(c) * 24, cudaMemcpyDeviceToHost, c->st));
+  const size_t B = (size_t)sys_b(c);
+  TRY(c, cudaMemcpyAsync(val, c->Hval.p, (size_t)c->nnzb * B * B * 4, cudaMemcpyDeviceToHost, c->st));
+  if (rhs) TRY(c, cudaMemcpyAsync(rhs, c->rhs.p, (size_t)sys_m(c) * B * 4, cudaMemcpyDeviceToHost, c->st));
   if (energy) TRY(c, cudaMemcpyAsync(energy, rep_energy(c), 40, cudaMemcpyDeviceToHost, c->st));
   TRY(c, cudaStreamSynchronize(c->st));
   return MIS_OK;
@@ -1251,7 +1273,7 @@ mis_status mis_warp(mis_ctx* c, mis_mem mem, float* xyz_cam, float* nrm_cam) {
   {
     ProfScope ps(c, P_WARP, (c->n > 0) + 1);
     launch_warp_model(c->K, model_view(c), node_view(c), frame_view(c), xyz_cam ? xc : nullptr,
-                      nrm_cam ? nc : nullptr, c->st);
+                      nrm_cam ? nc : nullptr, c->st, (c->prm.flags & MIS_F_AFFINE) != 0);
     launch_advance_nodes(node_view(c), c->g.as<float>(), c->st);
   }
   TRY(c, cudaGetLastError());

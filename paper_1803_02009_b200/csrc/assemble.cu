@@ -80,7 +80,10 @@ struct PState {   // a point's compact factor state (zeros: not associated)
 
 // JOINT (NEXT-2, A37): the pose comes from a.pose_cur and is written as factor slot K: (x_hat, 1),
 // the form of a node of weight 1 with a = x_hat (Jacobian R [-[x_hat]x, I])
-template <int K, bool DBG, bool JOINT>
+// AFF (NEXT-4, A41-A43): the node matrices are general A_j (same R9 t3 layout); normals warp by
+// A_j^-T (cofactors / det; A_j itself if |det| < 1e-9) and the state's slot s holds (w_s d_s, w_s),
+// d_s = v - g_s, the factor of the 12-unknown Jacobian rows
+template <int K, bool DBG, bool JOINT, bool AFF = false>
 __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, PState<K + (JOINT ? 1 : 0)>& st,
                                             double& ed, double& ep, int& as) {
   const ModelView& md = a.md;
@@ -120,13 +123,36 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
       const double a0 = R01.x * d0 + R01.y * d1 + R23.x * d2;
       const double a1 = R23.y * d0 + R45.x * d1 + R45.y * d2;
       const double a2 = R67.x * d0 + R67.y * d1 + R8t0.x * d2;
-      af[s][0] = (float)a0; af[s][1] = (float)a1; af[s][2] = (float)a2;
+      if constexpr (AFF) {
+        af[s][0] = (float)d0; af[s][1] = (float)d1; af[s][2] = (float)d2;
+      } else {
+        af[s][0] = (float)a0; af[s][1] = (float)a1; af[s][2] = (float)a2;
+      }
       xh[0] += wn[s] * (a0 + (double)g[0] + R8t0.y);
       xh[1] += wn[s] * (a1 + (double)g[1] + t12.x);
       xh[2] += wn[s] * (a2 + (double)g[2] + t12.y);
-      mh[0] += wn[s] * (R01.x * n[0] + R01.y * n[1] + R23.x * n[2]);
-      mh[1] += wn[s] * (R23.y * n[0] + R45.x * n[1] + R45.y * n[2]);
-      mh[2] += wn[s] * (R67.x * n[0] + R67.y * n[1] + R8t0.x * n[2]);
+      if constexpr (AFF) {   // A^-T = cof(A) / det(A)
+        const double A0 = R01.x, A1 = R01.y, A2 = R23.x, A3 = R23.y, A4 = R45.x, A5 = R45.y, A6 = R67.x,
+                     A7 = R67.y, A8 = R8t0.x;
+        double C[9] = {A4 * A8 - A5 * A7, A5 * A6 - A3 * A8, A3 * A7 - A4 * A6,
+                       A2 * A7 - A1 * A8, A0 * A8 - A2 * A6, A1 * A6 - A0 * A7,
+                       A1 * A5 - A2 * A4, A2 * A3 - A0 * A5, A0 * A4 - A1 * A3};
+        const double det = A0 * C[0] + A1 * C[1] + A2 * C[2];
+        if (fabs(det) < 1e-9) {
+          C[0] = A0; C[1] = A1; C[2] = A2; C[3] = A3; C[4] = A4; C[5] = A5; C[6] = A6; C[7] = A7; C[8] = A8;
+        } else {
+          const double id = 1.0 / det;
+#pragma unroll
+          for (int q = 0; q < 9; ++q) C[q] *= id;
+        }
+        mh[0] += wn[s] * (C[0] * n[0] + C[1] * n[1] + C[2] * n[2]);
+        mh[1] += wn[s] * (C[3] * n[0] + C[4] * n[1] + C[5] * n[2]);
+        mh[2] += wn[s] * (C[6] * n[0] + C[7] * n[1] + C[8] * n[2]);
+      } else {
+        mh[0] += wn[s] * (R01.x * n[0] + R01.y * n[1] + R23.x * n[2]);
+        mh[1] += wn[s] * (R23.y * n[0] + R45.x * n[1] + R45.y * n[2]);
+        mh[2] += wn[s] * (R67.x * n[0] + R67.y * n[1] + R8t0.x * n[2]);
+      }
     }
     double nt[3];
 #pragma unroll
@@ -211,13 +237,13 @@ __device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, do
 __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid);
 
 // K3a; the blocks after the points' run the K4/K5 items (independent of K3a, same launch)
-template <int K, bool DBG, bool JOINT>
+template <int K, bool DBG, bool JOINT, bool AFF = false>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_blocks) {
   pdl_wait();   // node states from the previous solve
   pdl_trigger();   // K3b's CTAs may start their table prologue on the SMs this grid's tail frees
   if (blockIdx.x >= point_blocks) {
-    graph_item(ga, (int64_t)(blockIdx.x - point_blocks) * blockDim.x + threadIdx.x);
+    if constexpr (!AFF) graph_item(ga, (int64_t)(blockIdx.x - point_blocks) * blockDim.x + threadIdx.x);
     return;
   }
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -226,7 +252,7 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArg
   if (i < a.md.n) {
     constexpr int KS = K + (JOINT ? 1 : 0);   // factor slots (the pose last, NEXT-2)
     PState<KS> st;
-    assoc_point<K, DBG, JOINT>(a, i, st, ed, ep, as);
+    assoc_point<K, DBG, JOINT, AFF>(a, i, st, ed, ep, as);
     float4* ps = a.pstate;
     const int64_t S = a.pstride;
 #pragma unroll
@@ -1225,6 +1251,14 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
   const unsigned gg = (unsigned)((ng + 255) / 256);
   if (g + gg == 0) return;
   const bool joint = a.pose_cur != nullptr;
+  if constexpr (K <= 4) {
+    if (a.affine) {   // NEXT-4: the graph terms run in their own kernel (affine.cu)
+      if (g == 0) return;
+      if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, false, true>, dim3(g), dim3(256), 0, s, a, gz, g);
+      else launch_pdl(k_assoc_points<K, false, false, true>, dim3(g), dim3(256), 0, s, a, gz, g);
+      return;
+    }
+  }
   if constexpr (K < MIS_MAX_K) {
     if (joint) {
       if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);

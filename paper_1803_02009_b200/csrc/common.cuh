@@ -98,10 +98,11 @@ struct AccView {
   float* rhs_graph;
   double* energy;              // [0..3] energies, [4] n_assoc, [6] K3b work counter (u64);
                                // [8 + 64 q + s]: striped partials of quantity q (0 E_data, 1 E_pt, 2 E_reg,
-                               // 3 E_corr, 4 n_assoc), summed by the finalisation
+                               // 3 E_corr, 4 n_assoc, 5 E_rot), summed by the finalisation
 };
 constexpr int kEnergyStripes = 64;
-constexpr int kEnergyDoubles = 8 + 5 * kEnergyStripes;
+constexpr int kEnergyQ = 6;
+constexpr int kEnergyDoubles = 8 + kEnergyQ * kEnergyStripes;
 // one fp64 atomic per warp into a stripe picked by the warp index: no same-address serialisation
 __device__ __forceinline__ void energy_add(double* energy, int q, double v) {
   const unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -139,6 +140,8 @@ struct AsmPointsArgs {
   // pose as one more factor slot (x_hat, 1) after the K node slots; K3b then runs with K + 1 slots
   // whose last node id is m (seg_nodes / seg_slot of the joint pattern).  null: fixed pose
   const double* pose_cur;
+  int affine;                 // NEXT-4 (MIS_F_AFFINE): the node matrices are general A_j; K3a writes
+                              // (w_j d_j, w_j), d_j = v - g_j, and warps normals by A_j^-T
 };
 // K3a (per point), then K3b (per chunk)
 struct AsmGraphArgs;
@@ -181,12 +184,19 @@ struct FinalArgs {
   const double *pose_cur, *pose_prior;
   float w_r, w_p;
   double* rep_pose;           // (MIS_MAX_GN+1)*2
+  float w_rot;                // NEXT-4: E_rot weight (its energy goes to rep_rot)
+  double* rep_rot;            // (MIS_MAX_GN+1)
   double* rep_energy;         // (MIS_MAX_GN+1)*5
   double* rep_nassoc;         // 2*(MIS_MAX_GN+1): association counts, fp64 guard counts
   const LmDev* lm;            // LM: write the system into the buffer not holding the accepted one
   float *Hval_alt, *rhs_alt;
 };
 void launch_finalize(const FinalArgs& r, cudaStream_t s);
+// NEXT-4 (affine.cu): K3b over the 12-unknown node blocks, the graph terms (Eq. 6 with A_j, Eq. 9,
+// Eq. 4-5 E_rot) and the 12 x 12 finalisation
+void launch_accum_points_aff(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
+void launch_assemble_graph_aff(const struct AsmGraphArgs& a, cudaStream_t s);
+void launch_finalize_aff(const FinalArgs& r, cudaStream_t s);
 
 struct AsmGraphArgs {
   NodeView nd;
@@ -204,6 +214,7 @@ struct AsmGraphArgs {
   int K;
   int KS;                     // feature slots: K, or K + 1 with the pose (fidx row K = m, NEXT-2)
   const double* pose_cur;     // NEXT-2: the current pose (null: fr's)
+  float w_rot;                // NEXT-4 (affine kernels): E_rot weight
 };
 void launch_assemble_graph(const AsmGraphArgs& a, cudaStream_t s);
 
@@ -244,6 +255,7 @@ struct SolveArgs {
   const float *Hval_alt, *rhs_alt;
   double* Rt_acc;             // m x 12: last accepted state
   int pose_node;              // NEXT-2: unknown index of the pose (m), -1: none
+  int block;                  // unknowns per node: 6 (SE(3)), 12 (NEXT-4 affine; additive update)
   double* pose;               // its state (R row-major 9, T 3): R <- R Exp(dphi), T <- T + R dtau
   const double* rep_energy;   // (MIS_MAX_GN+1) x 5, the trial energies
   double* rep_flags;          // MIS_MAX_GN+1: 1 = trial accepted
@@ -270,7 +282,7 @@ void launch_plan_cluster(const int32_t* row_ptr, int m, int max_cluster, PlanOut
 
 // ---- fusion (fuse.cu)
 void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const FrameView& fr, float* xyz_cam,
-                       float* nrm_cam, cudaStream_t s);
+                       float* nrm_cam, cudaStream_t s, bool affine = false);
 void launch_advance_nodes(const NodeView& nd, float* g_mut, cudaStream_t s);
 struct FuseArgs {
   ModelView md;

@@ -64,6 +64,10 @@ struct Ctx {
   DBuf posebuf;                 // 24 doubles: current pose (R 9, T 3) | prior (the frame's input pose)
   DBuf seg_nodes_j;             // nseg x (k + 1): segment tuples + the pose id m
 
+  // ---- NEXT-4 affine nodes (MIS_F_AFFINE): 12 unknowns per node
+  bool affine = false;          // the flag, as of the last prepare()
+  bool pattern_affine = false;  // the accumulator / system layout has 12 x 12 blocks
+
   // ---- order: segments and chunks (K13)
   int64_t nseg = 0, nchunk = 0;
   DBuf keys, keys2, vals, vals2, flags, scan, seg_start, seg_nodes, chunks, chunk_off;
@@ -141,14 +145,17 @@ void count_launches(int64_t k);
 // report block: [energy (MIS_MAX_GN+1) x 5 | n_assoc, n_guard 2 x (MIS_MAX_GN+1) | PCG residual
 // MIS_MAX_GN floats | numeric flag | E_r, E_p (MIS_MAX_GN+1) x 2], doubles
 constexpr size_t kRepN = 5 * (MIS_MAX_GN + 1), kRepR = kRepN + 2 * (MIS_MAX_GN + 1), kRepF = kRepR + MIS_MAX_GN / 2,
-                 kRepP = kRepF + 1, kRepBytes = (kRepP + 2 * (MIS_MAX_GN + 1)) * 8;
+                 kRepP = kRepF + 1, kRepO = kRepP + 2 * (MIS_MAX_GN + 1), kRepBytes = (kRepO + MIS_MAX_GN + 1) * 8;
 // unknown blocks of the current system: the m nodes, plus the pose with the joint pattern (NEXT-2)
 inline int sys_m(const Ctx* c) { return c->m + (c->pattern_joint ? 1 : 0); }
+// unknowns per node block of the current system: 6 (SE(3)), 12 (affine, NEXT-4)
+inline int sys_b(const Ctx* c) { return c->pattern_affine ? 12 : 6; }
 inline double* rep_energy(Ctx* c) { return c->rep.as<double>(); }
 inline double* rep_nassoc(Ctx* c) { return c->rep.as<double>() + kRepN; }
 inline float* rep_res(Ctx* c) { return reinterpret_cast<float*>(c->rep.as<double>() + kRepR); }
 inline int* numeric_flag(Ctx* c) { return reinterpret_cast<int*>(c->rep.as<double>() + kRepF); }
 inline double* rep_pose(Ctx* c) { return c->rep.as<double>() + kRepP; }
+inline double* rep_rot(Ctx* c) { return c->rep.as<double>() + kRepO; }
 
 // Records an event pair around a group of `nk` kernel launches on the context
 // stream when profiling is on; always adds nk to the launch counter.

@@ -9,7 +9,8 @@ namespace mis {
 __device__ __forceinline__ bool dok(float d) { return isfinite(d) && d > 0.0f; }
 
 // K9: x_hat = sum_j w_j (R_j (v - g_j) + g_j + t_j), n = normalize(sum_j w_j R_j n) (Eq. 1, A_j = R_j)
-template <int K>
+// AFF (NEXT-4, A43): the node matrices are general A_j, normals warp by A_j^-T (A_j if |det| < 1e-9)
+template <int K, bool AFF = false>
 __global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, FrameView fr, float* xyz_cam,
                                                    float* nrm_cam) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
@@ -28,10 +29,27 @@ __global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, F
       const float wn = w[s] / W;
       const float d[3] = {v[0] - N[12], v[1] - N[13], v[2] - N[14]};
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
+      for (int r = 0; r < 3; ++r)
         xh[r] += wn * (N[3 * r] * d[0] + N[3 * r + 1] * d[1] + N[3 * r + 2] * d[2] + N[12 + r] + N[9 + r]);
-        mh[r] += wn * (N[3 * r] * n[0] + N[3 * r + 1] * n[1] + N[3 * r + 2] * n[2]);
+      float C[9];
+      if constexpr (AFF) {   // cofactors / det
+        C[0] = N[4] * N[8] - N[5] * N[7]; C[1] = N[5] * N[6] - N[3] * N[8]; C[2] = N[3] * N[7] - N[4] * N[6];
+        C[3] = N[2] * N[7] - N[1] * N[8]; C[4] = N[0] * N[8] - N[2] * N[6]; C[5] = N[1] * N[6] - N[0] * N[7];
+        C[6] = N[1] * N[5] - N[2] * N[4]; C[7] = N[2] * N[3] - N[0] * N[5]; C[8] = N[0] * N[4] - N[1] * N[3];
+        const float det = N[0] * C[0] + N[1] * C[1] + N[2] * C[2];
+        if (fabsf(det) < 1e-9f) {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) C[q] = N[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) C[q] /= det;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) C[q] = N[q];
       }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) mh[r] += wn * (C[3 * r] * n[0] + C[3 * r + 1] * n[1] + C[3 * r + 2] * n[2]);
     }
     const float ml = sqrtf(mh[0] * mh[0] + mh[1] * mh[1] + mh[2] * mh[2]);
     if (ml >= 1e-12f) {
@@ -54,9 +72,18 @@ __global__ void __launch_bounds__(256) k_warp_model(ModelView md, NodeView nd, F
 }
 
 void launch_warp_model(int K, const ModelView& md, const NodeView& nd, const FrameView& fr, float* xyz_cam,
-                       float* nrm_cam, cudaStream_t s) {
+                       float* nrm_cam, cudaStream_t s, bool affine) {
   if (md.n <= 0) return;
   const int b = (int)((md.n + 255) / 256);
+  if (affine) {
+    switch (K) {
+#define WA(KK) case KK: launch_pdl(k_warp_model<KK, true>, dim3(b), dim3(256), 0, s, md, nd, fr, xyz_cam, nrm_cam); break;
+      WA(1) WA(2) WA(3) WA(4)
+#undef WA
+      default: break;
+    }
+    return;
+  }
   switch (K) {
 #define WK(KK) case KK: launch_pdl(k_warp_model<KK>, dim3(b), dim3(256), 0, s, md, nd, fr, xyz_cam, nrm_cam); break;
     WK(1) WK(2) WK(3) WK(4) WK(5) WK(6) WK(7) WK(8)

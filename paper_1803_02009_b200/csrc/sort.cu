@@ -650,6 +650,8 @@ cudaError_t build_pattern(Ctx* c) {
   const bool joint = c->joint;
   const int K = c->K + (joint ? 1 : 0), P = K * (K + 1) / 2, m = c->m, mu = m + (joint ? 1 : 0);
   c->pattern_joint = joint;
+  c->pattern_affine = c->affine;
+  const size_t B = c->affine ? 12 : 6, BB = B * B;   // unknowns per node block (NEXT-4: 12)
   const int64_t W = (mu + 63) / 64, words = (int64_t)mu * W;
   int64_t* info = c->nnz_dev.as<int64_t>();
   if (c->bitmap.bytes < (size_t)words * 8 || c->bitmap_words != words) c->bitmap_clean = false;
@@ -707,7 +709,7 @@ cudaError_t build_pattern(Ctx* c) {
   c->cl_max_rows = plan->max_rows;
   c->cl_max_nnz = plan->max_nnz;
   c->cl_smem = (size_t)plan->smem;
-  if (joint) c->cl_size = 0;   // the dense pose row: the grid-wide PCG (NEXT-2)
+  if (joint || c->affine) c->cl_size = 0;   // the dense pose row / 12 x 12 blocks: the grid-wide PCG
   CK(ensure(c, c->col, nnz * 4 + 4)); CK(ensure(c, c->row_of, nnz * 4 + 4));
   CK(ensure(c, c->upper_of, nnz * 4 + 4)); CK(ensure(c, c->lower_of, nnz * 4 + 4));
   CK(ensure(c, c->ulist, ((nnz - mu) / 2 + 1) * 8));
@@ -754,8 +756,8 @@ cudaError_t build_pattern(Ctx* c) {
   }
   CK(cudaGetLastError());
   // accumulators (K3 commits atomically into them) and solver buffers
-  const size_t m6 = 6 * (size_t)mu;
-  c->acc_floats = (size_t)nnz * (36 + 16 + 36) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)mu + m6;
+  const size_t m6 = B * (size_t)mu;
+  c->acc_floats = (size_t)nnz * (BB + 16 + BB) + ((m6 + 3) & ~(size_t)3) + 12 * (size_t)mu + m6;
   // accumulators: every finalisation re-zeroes what it read, so they need a memset only when
   // (re)allocated or after an assembly that did not reach its finalisation
   if (c->acc.bytes < c->acc_floats * 4 || c->energy.bytes < (size_t)kEnergyDoubles * 8) c->acc_dirty = true;
@@ -766,8 +768,8 @@ cudaError_t build_pattern(Ctx* c) {
     CK(cudaMemsetAsync(c->energy.p, 0, kEnergyDoubles * 8, c->st));
     c->acc_dirty = false;
   }
-  CK(ensure(c, c->Hval, (size_t)nnz * 36 * 4));
-  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)mu * 36 * 4));
+  CK(ensure(c, c->Hval, (size_t)nnz * BB * 4));
+  CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)mu * BB * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
   CK(ensure(c, c->p, m6 * 4)); CK(ensure(c, c->Ap, m6 * 4));
   CK(ensure(c, c->dots, (2 * (size_t)c->prm.pcg_iters + 8) * 8));

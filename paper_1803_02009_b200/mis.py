@@ -21,6 +21,7 @@ MIS_MAX_GN, MIS_MAX_K = 32, 8
 MIS_F_FINAL_ENERGY, MIS_F_GRID_SOLVER, MIS_F_STANDARD_PCG = 1, 4, 8
 MIS_F_LM = 16   # Levenberg-Marquardt (include/mis.h)
 MIS_F_JOINT_POSE = 32   # NEXT-2 joint global pose (include/mis.h)
+MIS_F_AFFINE = 64   # NEXT-4 affine nodes + E_rot (include/mis.h)
 STATUS = {0: "MIS_OK", 1: "MIS_E_ARG", 2: "MIS_E_STATE", 3: "MIS_E_CUDA", 4: "MIS_E_NCCL",
           5: "MIS_E_NOMEM", 6: "MIS_E_CAPACITY", 7: "MIS_E_NUMERIC"}
 
@@ -37,7 +38,7 @@ class mis_params(C.Structure):
                 ("eps_d_mm", C.c_float), ("eps_n_deg", C.c_float),
                 ("tau_z_mm", C.c_float), ("delta_deg", C.c_float), ("trunc_mm", C.c_float), ("omega_max", C.c_float),
                 ("gn_iters", C.c_int32), ("pcg_iters", C.c_int32), ("lambda_", C.c_float), ("flags", C.c_uint32),
-                ("w_r", C.c_float), ("w_p", C.c_float)]
+                ("w_r", C.c_float), ("w_p", C.c_float), ("w_rot", C.c_float)]
 
 
 class mis_intrinsics(C.Structure):
@@ -52,7 +53,8 @@ class mis_report(C.Structure):
                 ("pcg_rel_res", C.c_float * MIS_MAX_GN),
                 ("nnzb", C.c_int64), ("n_segments", C.c_int64), ("solver_cluster", C.c_int32),
                 ("reserved", C.c_int32), ("n_guard", C.c_int64 * (MIS_MAX_GN + 1)),
-                ("energy_pose", (C.c_double * 2) * (MIS_MAX_GN + 1))]
+                ("energy_pose", (C.c_double * 2) * (MIS_MAX_GN + 1)),
+                ("energy_rot", C.c_double * (MIS_MAX_GN + 1))]
 
 
 if not os.path.exists(LIB_PATH):
@@ -238,7 +240,8 @@ def report_dict(rep: mis_report):
                 nnzb=rep.nnzb, n_segments=rep.n_segments, solver_cluster=rep.solver_cluster,
                 n_guard=np.array([rep.n_guard[i] for i in range(it + 1)]),
                 accepted=np.array([rep.n_guard[i] for i in range(it + 1)]),   # MIS_F_LM decisions
-                energy_pose=np.array([[rep.energy_pose[i][q] for q in range(2)] for i in range(it + 1)]))
+                energy_pose=np.array([[rep.energy_pose[i][q] for q in range(2)] for i in range(it + 1)]),
+                energy_rot=np.array([rep.energy_rot[i] for i in range(it + 1)]))
 
 
 def mis_get_nodes(ctx, out):
@@ -351,14 +354,14 @@ def mis_dbg_associate(ctx, n):
     return pix, why
 
 
-def mis_dbg_system(ctx, m):
+def mis_dbg_system(ctx, m, block=6):
     nnz = C.c_int64()
     _check(ctx, _lib.mis_dbg_system(ctx, None, None, None, None, None, C.byref(nnz)))
     nz = nnz.value
     row_ptr = np.zeros(m + 1, np.int32)
     col = np.zeros(nz, np.int32)
-    val = np.zeros((nz, 6, 6), np.float32)
-    rhs = np.zeros(6 * m, np.float32)
+    val = np.zeros((nz, block, block), np.float32)
+    rhs = np.zeros(block * m, np.float32)
     E = np.zeros(5, np.float64)
     _check(ctx, _lib.mis_dbg_system(ctx, _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(rhs), _ptr(E), C.byref(nnz)))
     return dict(row_ptr=row_ptr, col=col, val=val, rhs=rhs, energy=E, nnzb=nz)

@@ -1,0 +1,126 @@
+"""GPU parity of NEXT-4, the affine node model (MIS_F_AFFINE; Eq. 1 with A_j, Eq. 4-6,
+readings A41-A45): 12 unknowns per node, E_rot, normals by A^-T.  Gates as DESIGN.md §6:
+association bit-exact outside ties, the 12 x 12 block system within relative 1e-4 (Cauchy-Schwarz
+scaled), converged node states within 0.01 mm (t) / 1e-4 (A entries) of the oracle's MIRROR
+run, warped points within 0.05 mm."""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.common import scene_problem, state_f32
+from tests.test_gpu_parity import M, make_ctx, oracle_params, order_of
+from tests.test_oracle_pins import random_affine
+
+pytestmark = pytest.mark.gpu
+
+
+def aff_ctx(sc, pb, **kw):
+    flags = kw.pop("flags", 0) | M.MIS_F_AFFINE | M.MIS_F_FINAL_ENERGY
+    return make_ctx(sc, pb, flags=flags, **kw)
+
+
+def aff_state(kind, m, seed):
+    if kind == "identity":
+        return O.identity_affine(m)
+    return state_f32(random_affine(m, np.random.default_rng(seed)))
+
+
+def oprm(ctx):
+    return oracle_params(ctx.params, w_rot=ctx.params.w_rot)
+
+
+def dense_bsr(s, m, B):
+    H = np.zeros((B * m, B * m))
+    for r in range(m):
+        for e in range(s["row_ptr"][r], s["row_ptr"][r + 1]):
+            c = s["col"][e]
+            H[B * r:B * r + B, B * c:B * c + B] = s["val"][e]
+    return H
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_affine_association_parity(cfg):
+    sc, pb, fr, _ = scene_problem(cfg)
+    ctx = aff_ctx(sc, pb)
+    At = aff_state("random", pb.g.shape[0], 5001)
+    M.mis_dbg_set_nodes(ctx.ptr, At.astype(np.float32))
+    pix, why = M.mis_dbg_associate(ctx.ptr, pb.xyz.shape[0])
+    ids = order_of(ctx, pb.k)
+    opix, owhy, omg = O.associate_aff(oprm(ctx), pb, fr, At)
+    opix, owhy, omg = opix[ids], owhy[ids], omg[ids]
+    keep = omg > 1e-6
+    assert keep.mean() > 0.99
+    bad = np.flatnonzero(keep & ((pix != opix) | (why != owhy)))
+    assert bad.size == 0, (bad[:10], pix[bad[:10]], opix[bad[:10]])
+    # the A^-T normal warp decides gates: a plain A n warp would differ
+    assert (opix >= 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+@pytest.mark.parametrize("state", ["identity", "random"])
+def test_affine_system_parity(cfg, state):
+    sc, pb, fr, _ = scene_problem(cfg)
+    ctx = aff_ctx(sc, pb)
+    m = pb.g.shape[0]
+    At = aff_state(state, m, 5002)
+    M.mis_dbg_set_nodes(ctx.ptr, At.astype(np.float32))
+    gs = M.mis_dbg_system(ctx.ptr, m, block=12)
+    osys = O.system_aff(oprm(ctx), pb, fr, At)
+    Hg = dense_bsr(gs, m, 12)
+    Ho = O.dense_H_aff(osys, m)
+    d = np.sqrt(np.maximum(np.diag(Ho), 1e-30))
+    err = np.abs(Hg - Ho) / np.outer(d, d)
+    assert err.max() < 1e-4, err.max()
+    E = osys["energy"][5]
+    bt = np.abs(gs["rhs"] - osys["rhs"]) / np.sqrt(np.diag(Ho) * 2 * E)
+    assert bt.max() < 1e-4, bt.max()
+    eo = osys["energy"]
+    assert (np.abs(gs["energy"][:4] - eo[:4]) <= 1e-4 * np.abs(eo[:4]) + 1e-9).all(), (gs["energy"], eo)
+    assert abs(gs["energy"][4] - eo[5]) <= 1e-4 * eo[5]
+    assert np.abs(Hg - Hg.T).max() <= 1e-6 * np.abs(Hg).max()
+    if state == "random":
+        assert eo[4] > 0   # E_rot is active
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_affine_register_parity_mirror(cfg):
+    sc, pb, fr, _ = scene_problem(cfg)
+    ctx = aff_ctx(sc, pb)
+    rep = M.report_dict(M.mis_register(ctx.ptr))
+    assert rep["status"] == 0 and rep["solver_cluster"] == 0
+    m = pb.g.shape[0]
+    Ag = M.mis_get_nodes_f64(ctx.ptr, m)
+    Ao, Eo, nao = O.register_aff(oprm(ctx), pb, fr)
+    terr = np.linalg.norm(Ag[:, 9:] - Ao[:, 9:], axis=1)
+    assert terr.max() < 0.01, terr.max()
+    assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < 1e-4, np.abs(Ag[:, :9] - Ao[:, :9]).max()
+    assert np.abs(Ao[:, :9] - np.eye(3).ravel()).max() > 1e-4   # the matrices left the rotations
+    assert np.allclose(rep["energy"][:, 4], Eo[:, 5], rtol=1e-3)
+    assert np.allclose(rep["energy_rot"], Eo[:, 4], rtol=2e-2, atol=1e-12)
+    assert np.abs(rep["n_assoc"] - nao).max() <= max(3, 1e-4 * pb.xyz.shape[0])
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_affine_warp_parity(cfg):
+    sc, pb, fr, _ = scene_problem(cfg)
+    ctx = aff_ctx(sc, pb)
+    m = pb.g.shape[0]
+    At = aff_state("random", m, 5003)
+    M.mis_dbg_set_nodes(ctx.ptr, At.astype(np.float32))
+    M.mis_warp(ctx.ptr)
+    mod = M.mis_get_model(ctx.ptr, pb.k)
+    xo, no, go = O.warp_model_aff(pb, At)
+    ids = mod["ids"]
+    assert np.abs(mod["xyz"] - xo[ids]).max() < 0.05
+    assert np.abs(mod["nrm"] - no[ids]).max() < 1e-4
+    g = M.mis_get_graph(ctx.ptr, np.zeros((m, 3), np.float32))
+    assert np.abs(g - go).max() < 1e-4
+    assert np.abs(M.mis_get_nodes_f64(ctx.ptr, m) - O.identity_affine(m)).max() == 0   # A45: reset
+
+
+def test_affine_errors():
+    for flags, k in [(M.MIS_F_AFFINE | M.MIS_F_LM, 4), (M.MIS_F_AFFINE | M.MIS_F_JOINT_POSE, 4), (M.MIS_F_AFFINE, 8)]:
+        with pytest.raises(M.MisError):
+            M.Context(M.mis_default_params(k=k, flags=flags))
+    with pytest.raises(M.MisError):
+        M.Context(M.mis_default_params(w_rot=float("nan")))
