@@ -317,6 +317,15 @@ def run_mis(args, rank, world, local_rank):
                      "E_first": float(rj["energy"][0, 4]), "E_last_iter": float(rj["energy"][cfg.gn_iters - 1, 4]),
                      "E_r_E_p_last": [float(x) for x in rj["energy_pose"][cfg.gn_iters - 1]],
                      "pose_change_mm": float(np.linalg.norm(pose_j[9:] - p0[9:]))}
+    affine_out = None
+    if world == 1 and not args.no_lm and cfg.k <= 4:
+        af_ms, ra, _ = variant_leg(M.MIS_F_AFFINE)
+        affine_out = {"ms_per_step": round(af_ms, 4), "value": round(1e3 / af_ms, 3), "unit": UNIT,
+                      "what": "same step with affine nodes A_j + E_rot (MIS_F_AFFINE, NEXT-4: 12 x 12 node blocks, "
+                              "w_rot = 1000, grid-wide PCG)",
+                      "solver_cluster": int(ra["solver_cluster"]),
+                      "E_first": float(ra["energy"][0, 4]), "E_last_iter": float(ra["energy"][cfg.gn_iters - 1, 4]),
+                      "E_rot_last": float(ra["energy_rot"][cfg.gn_iters - 1])}
 
     # ---------------- NEXT-1: Alg. 3 filtering (mis_filter, K14) of the fused model, single GPU only.
     # Each timed filter runs on the model a full step just produced (the step itself untimed); the
@@ -524,6 +533,7 @@ def run_mis(args, rank, world, local_rank):
         "pcg_phases_us_last_launch": pcg_phases,
         "lm": lm_out,
         "joint_pose": joint_out,
+        "affine": affine_out,
         "filter": filt_out,
         "sequence": seq_out,
         "gpu_launches": int(launches),

@@ -124,3 +124,18 @@ def test_affine_errors():
             M.Context(M.mis_default_params(k=k, flags=flags))
     with pytest.raises(M.MisError):
         M.Context(M.mis_default_params(w_rot=float("nan")))
+
+
+def test_affine_register_full_c3():
+    """NEXT-4 at the bench configuration (C3: 300k points, 999 nodes, 5 GN x 10 PCG, features)."""
+    from tests.test_gpu_fullsize import problem
+    sc, pb, fr, _ = problem("c3")
+    ctx = aff_ctx(sc, pb)
+    rep = M.report_dict(M.mis_register(ctx.ptr))
+    assert rep["status"] == 0
+    m = pb.g.shape[0]
+    Ag = M.mis_get_nodes_f64(ctx.ptr, m)
+    Ao, Eo, nao = O.register_aff(oprm(ctx), pb, fr)
+    assert np.linalg.norm(Ag[:, 9:] - Ao[:, 9:], axis=1).max() < 0.01
+    assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < 1e-4
+    assert np.allclose(rep["energy"][:, 4], Eo[:, 5], rtol=1e-3)
