@@ -470,6 +470,7 @@ mis_status mis_create(const mis_params* params, int device, void* cuda_stream, i
     c->own_stream = true;
   }
   if (const char* e = getenv("MIS_ORDER_BY_SORT")) c->order_by_sort = atoi(e) != 0;
+  if (const char* e = getenv("MIS_K3_SPLIT")) c->k3_split = atoi(e) != 0;
 
   if (world > 1) {
     NcclApi& api = nccl();
@@ -881,18 +882,28 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     gA.pose_cur = a.pose_cur;
     gA.w_rot = c->prm.w_rot;
   }
-  if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch (affine: K4/K5/E_rot in their own)
-    ProfScope ps(c, P_POINTS, 1);
-    launch_assoc_points(c->K, a, graph_terms ? &gA : nullptr, c->st);
-  }
-  if (aff) {   // the affine graph terms include E_rot on every node: always (rank 0)
-    ProfScope ps(c, P_GRAPH, 1);
-    if (c->rank == 0) launch_assemble_graph_aff(gA, c->st);
-  }
-  if (a.nchunk > 0) {
-    ProfScope ps(c, P_ACCUM, 1);
-    if (aff) launch_accum_points_aff(c->K, a, c->num_sms, c->st);
-    else launch_accum_points(KS, a, c->num_sms, c->st);
+  // K3a + K3b fused into one kernel (k <= 4 SE(3), no debug outputs; MIS_K3_SPLIT=1 in the
+  // environment keeps the two-kernel path for comparison), the K4/K5 items in its extra CTAs
+  const bool fused = !dbg && !joint && !aff && c->K <= 4 && !c->k3_split;
+  if (fused) {
+    if (a.nchunk > 0 || graph_terms) {
+      ProfScope ps(c, P_ACCUM, 1);
+      launch_accum_points(KS, a, c->num_sms, c->st, true, graph_terms ? &gA : nullptr);
+    }
+  } else {
+    if (c->n > 0 || graph_terms) {   // K3a + K4/K5 in one launch (affine: K4/K5/E_rot in their own)
+      ProfScope ps(c, P_POINTS, 1);
+      launch_assoc_points(c->K, a, graph_terms ? &gA : nullptr, c->st);
+    }
+    if (aff) {   // the affine graph terms include E_rot on every node: always (rank 0)
+      ProfScope ps(c, P_GRAPH, 1);
+      if (c->rank == 0) launch_assemble_graph_aff(gA, c->st);
+    }
+    if (a.nchunk > 0) {
+      ProfScope ps(c, P_ACCUM, 1);
+      if (aff) launch_accum_points_aff(c->K, a, c->num_sms, c->st);
+      else launch_accum_points(KS, a, c->num_sms, c->st);
+    }
   }
   TRY(c, cudaGetLastError());
   if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them

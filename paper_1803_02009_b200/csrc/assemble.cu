@@ -83,9 +83,33 @@ struct PState {   // a point's compact factor state (zeros: not associated)
 // AFF (NEXT-4, A41-A43): the node matrices are general A_j (same R9 t3 layout); normals warp by
 // A_j^-T (cofactors / det; A_j itself if |det| < 1e-9) and the state's slot s holds (w_s d_s, w_s),
 // d_s = v - g_s, the factor of the 12-unknown Jacobian rows
-template <int K, bool DBG, bool JOINT, bool AFF = false>
+// Where a point's K node states come from: the per-point skinning ids (K3a), or the chunk's
+// tuple staged in shared memory (the fused K3, every point of a chunk shares its K nodes)
+struct NodesGlobal {
+  __device__ __forceinline__ int id(const AsmPointsArgs& a, int64_t i, int s) const {
+    return a.md.kidx[s * a.md.cap + i];
+  }
+  __device__ __forceinline__ void get(const AsmPointsArgs& a, int id, int, double2 (&r)[6], const float*& g) const {
+    const double2* p = reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)id);   // R (9), t (3)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) r[q] = __ldg(p + q);
+    g = a.nd.g + 3 * (int64_t)id;
+  }
+};
+struct NodesChunk {
+  const double2* rt;   // K x 6 double2 (R, t) of the chunk's nodes, shared memory
+  const float* g;      // K x 4 (g, pad)
+  __device__ __forceinline__ int id(const AsmPointsArgs&, int64_t, int) const { return 0; }
+  __device__ __forceinline__ void get(const AsmPointsArgs&, int, int s, double2 (&r)[6], const float*& gp) const {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) r[q] = rt[6 * s + q];
+    gp = g + 4 * s;
+  }
+};
+
+template <int K, bool DBG, bool JOINT, bool AFF = false, class NS = NodesGlobal>
 __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, PState<K + (JOINT ? 1 : 0)>& st,
-                                            double& ed, double& ep, int& as) {
+                                            double& ed, double& ep, int& as, const NS& ns = NS()) {
   const ModelView& md = a.md;
   const FrameView& fr = a.fr;
   const double v[3] = {md.px[i], md.py[i], md.pz[i]}, n[3] = {md.nx[i], md.ny[i], md.nz[i]};
@@ -94,7 +118,7 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     wn[s] = md.kw[s * md.cap + i];
-    nid[s] = md.kidx[s * md.cap + i];
+    nid[s] = ns.id(a, i, s);
     W += wn[s];
   }
   int pix = -1;
@@ -114,10 +138,10 @@ __device__ __forceinline__ void assoc_point(const AsmPointsArgs& a, int64_t i, P
     double mh[3] = {0, 0, 0};
 #pragma unroll
     for (int s = 0; s < K; ++s) {
-      const double2* rt = reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nid[s]);   // R (9), t (3)
-      const double2 R01 = __ldg(rt), R23 = __ldg(rt + 1), R45 = __ldg(rt + 2), R67 = __ldg(rt + 3),
-                    R8t0 = __ldg(rt + 4), t12 = __ldg(rt + 5);
-      const float* g = a.nd.g + 3 * (int64_t)nid[s];
+      double2 rq[6];
+      const float* g;
+      ns.get(a, nid[s], s, rq, g);
+      const double2 R01 = rq[0], R23 = rq[1], R45 = rq[2], R67 = rq[3], R8t0 = rq[4], t12 = rq[5];
       wn[s] *= iW;
       const double d0 = v[0] - g[0], d1 = v[1] - g[1], d2 = v[2] - g[2];
       const double a0 = R01.x * d0 + R01.y * d1 + R23.x * d2;
@@ -548,9 +572,23 @@ __device__ __forceinline__ void mma3(float (&d)[4], const FragT& f, int mi, int 
   mma_tf32(d, f.l[mi][0], f.l[mi][1], f.l[mi][2], f.l[mi][3], f.bh[ni][0], f.bh[ni][1]);
 }
 
-template <int K>
-__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(AsmPointsArgs a) {
+// FUSED: K3a and K3b in one kernel -- every point of a chunk shares the chunk's k nodes, so the
+// warp stages their fp64 states in shared memory once per chunk and each lane computes its
+// point's association, residuals and factor state (assoc_point, the K3a arithmetic) straight
+// into its factor row: no per-point node loads, no factor-state round trip through memory.
+// The CTAs past point_grid run the K4 / K5 items (as K3a's extra blocks do).
+template <int K, bool FUSED = false>
+__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(AsmPointsArgs a, AsmGraphArgs ga,
+                                                                              unsigned point_grid) {
   static_assert(6 * K + 1 <= 32 && 4 * K + 3 <= 24, "tensor-core K3b: k <= 4");
+  if constexpr (FUSED) {
+    if (blockIdx.x >= point_grid) {
+      pdl_wait();   // node states of the previous solve
+      pdl_trigger();
+      graph_item(ga, (int64_t)(blockIdx.x - point_grid) * blockDim.x + threadIdx.x);
+      return;
+    }
+  }
   constexpr int P = K * (K + 1) / 2;
   constexpr int RT = tc_rec_floats(K);
   extern __shared__ float4 smem4[];
@@ -559,6 +597,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
   float* Rec = reinterpret_cast<float*>(smem4) + kWarps * 32 * kTcFSP + warp * RT;
   __shared__ int32_t slot_sm[kWarps][P + K];   // the chunk's BSR slots, then its K node ids
   int32_t* slots = slot_sm[warp];
+  __shared__ double2 nrt_sm[FUSED ? kWarps : 1][6 * K];   // FUSED: the chunk's node states (R, t)
+  __shared__ float4 ng_sm[FUSED ? kWarps : 1][K];          // and positions
+  double ed = 0.0, ep = 0.0;
+  int n_as = 0;
   // where each summed entry goes: inv[q] = record index of position q of the dumped sums
   // (c' 32 x 32 at 0, e' 24 x 24 at 1024; upper triangles), -1: not part of the system
   __shared__ int16_t inv[32 * 32 + 24 * 24];
@@ -633,6 +675,17 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     __syncwarp();
     if (lane < P) slots[lane] = a.seg_slot[(int64_t)seg * P + lane];
     else if (lane < P + K) slots[lane] = nodes[lane - P];
+    if constexpr (FUSED) {   // stage the chunk's node states (fp64 master) and positions
+      if (lane < 6 * K) {
+        const int nid = nodes[lane / 6];
+        nrt_sm[warp][lane] = __ldg(reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nid) + lane % 6);
+      } else if (lane < 7 * K) {
+        const int nid = nodes[lane - 6 * K];
+        const float* g = a.nd.g + 3 * (int64_t)nid;
+        ng_sm[warp][lane - 6 * K] = make_float4(g[0], g[1], g[2], 0.f);
+      }
+      __syncwarp();
+    }
     // c' tiles (0,0..3),(1,2),(1,3); e' tiles (0,0..2) -- the e' rows >= 4k (r') pair only with
     // each other there, which the system does not use
     float dc[6][4], de[3][4];
@@ -645,10 +698,17 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
       float* row = F + lane * kTcFSP;
       PState<K> st;
       if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point or past the chunk)
+        if constexpr (FUSED) {
+          int as1 = 0;
+          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
+          n_as += as1;
+        } else {
 #pragma unroll
-        for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
-        st.rr = ps[K * S + i];
-        st.nn = ps[(K + 1) * S + i];
+          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+          st.rr = ps[K * S + i];
+          st.nn = ps[(K + 1) * S + i];
+        }
       } else {
 #pragma unroll
         for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -715,6 +775,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
+  if constexpr (FUSED) commit_point_energies(a, ed, ep, n_as);
 }
 
 // ---- tensor-core K3b for 5 <= k <= 8 (C5): the same per-chunk Gram sums as k_accum_points_tc with
@@ -1274,9 +1335,8 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
 #define MIS_K3B_TC 1   // 0: the FP32 FMA path for every k
 #endif
 template <int K>
-static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s, bool fused, const AsmGraphArgs* ga) {
   using L = Lay<K>;
-  if (a.nchunk <= 0) return;
   constexpr bool tc = MIS_K3B_TC && K <= 4;   // tensor-core SYRK: k <= 4 (8 warps x 2 CTAs / SM),
   // 5 <= k <= 8 on tensor cores (one 8-warp CTA / SM at 167 registers) measured slower than the FP32
   // tiles at 16 warps / SM (C5: 2.9 vs 2.5 ms per launch, latency-bound), so it is opt-in
@@ -1284,9 +1344,36 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s) 
   const size_t smem = tc    ? sizeof(float) * kWarps * (32 * kTcFSP + tc_rec_floats(K <= 4 ? K : 4))
                       : tcw ? tcw_smem(K)
                             : sizeof(float) * kWarps * 32 * L::FSP;
+  if constexpr (tc) {   // K3b, or K3a + K3b fused (with the K4 / K5 items in extra CTAs)
+    auto kern = fused ? k_accum_points_tc<(K <= 4 ? K : 4), true> : k_accum_points_tc<(K <= 4 ? K : 4), false>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[fused]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set[fused] = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (a.nchunk + kWarps - 1) / kWarps;
+    int64_t grid = (int64_t)num_sms * per_sm;
+    if (want < grid) grid = want;
+    if (grid < 1) grid = 1;
+    AsmGraphArgs gz{};
+    int64_t gg = 0;
+    if (fused && ga) {
+      gz = *ga;
+      const int PS = gz.KS * (gz.KS + 1) / 2;
+      const int64_t ng = (int64_t)gz.nd.m * gz.n_nbr * 6 + (int64_t)gz.nf * PS * 6 + (int64_t)gz.nf * gz.KS;
+      gg = (ng + kWarps * 32 - 1) / (kWarps * 32);
+    }
+    if (a.nchunk <= 0) grid = 0;
+    if (grid + gg == 0) return;
+    launch_pdl(kern, dim3((unsigned)(grid + gg)), dim3(kWarps * 32), smem, s, a, gz, (unsigned)grid);
+    return;
+  }
+  if (a.nchunk <= 0) return;
   void (*kern)(AsmPointsArgs);
-  if constexpr (tc) kern = k_accum_points_tc<(K <= 4 ? K : 4)>;
-  else if constexpr (tcw) kern = k_accum_points_tcw<(K > 4 ? K : 5)>;
+  if constexpr (tcw) kern = k_accum_points_tcw<(K > 4 ? K : 5)>;
   else kern = k_accum_points<K>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1312,9 +1399,10 @@ void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, 
   }
 }
 
-void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s) {
+void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s, bool fused,
+                         const AsmGraphArgs* ga) {
   switch (K) {
-#define LP(KK) case KK: launch_accum_k<KK>(a, num_sms, s); break;
+#define LP(KK) case KK: launch_accum_k<KK>(a, num_sms, s, fused, ga); break;
     LP(1) LP(2) LP(3) LP(4) LP(5) LP(6) LP(7) LP(8)
 #undef LP
     default: break;

@@ -147,7 +147,9 @@ struct AsmPointsArgs {
 struct AsmGraphArgs;
 // K3a (per point; with K4/K5 items in the same launch when ga != null), then K3b (per chunk)
 void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s);
-void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
+// fused (k <= 4, no debug outputs): K3a + K3b in one kernel, the K4 / K5 items (ga) in extra CTAs
+void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s, bool fused = false,
+                         const AsmGraphArgs* ga = nullptr);
 
 // Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator
 // addresses at commit): P pairs x [36 data (6x6, upper for the diagonal pair) |

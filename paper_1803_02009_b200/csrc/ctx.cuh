@@ -76,6 +76,7 @@ struct Ctx {
   DBuf gtab, gkeys, gslot, gcount;
   int64_t gtab_slots = 0, gsize_cap = 0;
   bool order_by_sort = false;   // MIS_ORDER_BY_SORT=1 in the environment: the radix-sort path
+  bool k3_split = false;        // MIS_K3_SPLIT=1 in the environment: K3a + K3b as two kernels
 
   // ---- pattern
   int64_t nnzb = 0;
