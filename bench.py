@@ -297,9 +297,18 @@ def run_mis(args, rank, world, local_rank):
         cv.close()
         return v_ms, rv, pose_v
 
+    def variant_or_reason(flag):
+        try:
+            return variant_leg(flag)
+        except M.MisError as e:   # e.g. LM needs the cluster-resident PCG (C1-C3 sizes)
+            return None, str(e), None
+
     lm_out = None
     if world == 1 and not args.no_lm:
-        lm_ms, rl, _ = variant_leg(M.MIS_F_LM)
+        lm_ms, rl, _ = variant_or_reason(M.MIS_F_LM)
+    if world == 1 and not args.no_lm and lm_ms is None:
+        lm_out = {"unavailable": rl}
+    elif world == 1 and not args.no_lm:
         lm_out = {"ms_per_step": round(lm_ms, 4), "value": round(1e3 / lm_ms, 3), "unit": UNIT,
                   "what": "same step with Levenberg-Marquardt registration (MIS_F_LM: G trials + final evaluation, "
                           "accept / reject and Marquardt damping on the device)",
@@ -307,8 +316,11 @@ def run_mis(args, rank, world, local_rank):
                   "E_first": float(rl["energy"][0, 4]), "E_final_trial": float(rl["energy"][cfg.gn_iters, 4])}
     joint_out = None
     if world == 1 and not args.no_lm:
-        jp_ms, rj, pose_j = variant_leg(M.MIS_F_JOINT_POSE)
+        jp_ms, rj, pose_j = variant_or_reason(M.MIS_F_JOINT_POSE)
         p0 = np.asarray(pose, np.float64)
+    if world == 1 and not args.no_lm and jp_ms is None:
+        joint_out = {"unavailable": rj}
+    elif world == 1 and not args.no_lm:
         joint_out = {"ms_per_step": round(jp_ms, 4), "value": round(1e3 / jp_ms, 3), "unit": UNIT,
                      "what": "same step with the joint global-pose refinement (MIS_F_JOINT_POSE, NEXT-2: the pose as "
                              "unknown m with the Eq. 10 priors w_r = 1e6, w_p = 1000; grid-wide PCG for the dense pose "
@@ -319,7 +331,10 @@ def run_mis(args, rank, world, local_rank):
                      "pose_change_mm": float(np.linalg.norm(pose_j[9:] - p0[9:]))}
     affine_out = None
     if world == 1 and not args.no_lm and cfg.k <= 4:
-        af_ms, ra, _ = variant_leg(M.MIS_F_AFFINE)
+        af_ms, ra, _ = variant_or_reason(M.MIS_F_AFFINE)
+    if world == 1 and not args.no_lm and cfg.k <= 4 and af_ms is None:
+        affine_out = {"unavailable": ra}
+    elif world == 1 and not args.no_lm and cfg.k <= 4:
         affine_out = {"ms_per_step": round(af_ms, 4), "value": round(1e3 / af_ms, 3), "unit": UNIT,
                       "what": "same step with affine nodes A_j + E_rot (MIS_F_AFFINE, NEXT-4: 12 x 12 node blocks, "
                               "w_rot = 1000, grid-wide PCG)",

@@ -537,7 +537,7 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
       cs * (mr + 1) * 4, cs * mp * 4, cs * mr * 64, 128, 4 * m,              // cluster PCG lists
       // accumulators, system and PCG sized for 12 x 12 blocks (the affine nodes of NEXT-4)
       nnz * 304 * 4 + (12 * m + 3) * 4 + 48 * m + 48 * m, kEnergyDoubles * 8,  // accumulators
-      576 * nnz, 48 * m, 576 * m, 5 * 48 * m, (2 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
+      576 * nnz, 48 * m, 576 * m, 5 * 48 * m, (8 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
       144 * nnz, 24 * m, 96 * m,                                            // LM second system, kept nodes
       (K + 2) * 16 * n,                                                     // K3a -> K3b state
       4 * px, 16 * px, 32 * px, 12 * px, 8 * px, 4 * px, (2 * ((px + 255) / 256) + 4) * 4,   // frame, fusion
