@@ -481,12 +481,30 @@ def run_mis(args, rank, world, local_rank):
         if tj.get("config") == args.config:
             traffic_all = tj.get("bytes_per_launch", {})
 
+    fused_k3 = "assoc_points" not in groups and kk <= 4   # the fused K3 kernel ran (api.cu)
+
     def roofline_of(name):
         ms_k, n_k = groups[name]
         t = ms_k / max(1, n_k) * 1e-3
         base = {"kernel": name, "launch_ms": round(t * 1e3, 5), "share_of_step": round(ms_k / max(kev["dev_ms"], 1e-9), 3),
                 "timing": "CUDA events around every launch, second timed pass of the same K steps"}
-        if name == "accum_points":
+        if name == "accum_points" and fused_k3:
+            # K3a + K3b in one kernel (k <= 4): SURVEY §8(d)'s K3 unit -- (24 + 8k) B per point + 16 B per
+            # associated pixel, 40k + 40 + 15k + 2 (6k)(6k+1)/2 + 20 k(k+1)/2 + 25k flop per point -- bound by
+            # its arithmetic (FP32 FMA pipe; the SYRK part runs as 3xTF32 mma.sync, tensor view below)
+            ach = k3_flop / t / 1e12
+            base.update({"bound": "alu", "achieved": round(ach, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
+                         "frac": round(ach / fp32_peak, 4), "algorithmic_flops_per_launch": int(k3_flop),
+                         "peak_source": "FP32 FMA: SMs x 128 lanes x 2 x max SM clock (B200_PROFILING.md)",
+                         "what": "fused K3 (association + residuals + tensor-core SYRK + commit), one launch per GN "
+                                 "iteration",
+                         "hbm_view": {"achieved": round(k3_bytes / t / 1e9, 2), "peak": hbm,
+                                      "frac": round(k3_bytes / t / 1e9 / hbm, 4),
+                                      "algorithmic_bytes_per_launch": int(k3_bytes)},
+                         "tensor_view": {"achieved": round(syrk_flop / t / 1e12, 3), "peak": round(tf32_peak, 1),
+                                         "frac": round(syrk_flop / t / 1e12 / tf32_peak, 5),
+                                         "flops_per_launch": int(syrk_flop)}})
+        elif name == "accum_points":
             tc = kk <= 4
             pk = tf32_peak if tc else fp32_peak
             ach = syrk_flop / t / 1e12
@@ -508,8 +526,8 @@ def run_mis(args, rank, world, local_rank):
                                     "frac": round(fl / fp32_peak, 4), "flops_per_launch": int(k3_flop)}
         tr = traffic_all.get(name)
         base["traffic"] = tr
-        if tr and name != "accum_points":
-            base["traffic_over_algorithmic"] = round(tr / max(1, algo[name]), 3)
+        if tr and (name != "accum_points" or fused_k3):
+            base["traffic_over_algorithmic"] = round(tr / max(1, k3_bytes if name == "accum_points" else algo[name]), 3)
         return base
 
     roof = roofline_of(dom)

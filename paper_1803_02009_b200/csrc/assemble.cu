@@ -54,6 +54,9 @@ struct Lay {
 };
 
 constexpr int kWarps = 8;
+#ifndef MIS_K3_STATIC
+#define MIS_K3_STATIC 0   // 1: static round-robin chunk schedule (measured ~1.5% slower at C3: tail imbalance)
+#endif
 #ifndef MIS_K3_MINB
 #define MIS_K3_MINB 2   // resident blocks per SM the register budget is sized for
 #endif
@@ -663,13 +666,24 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
 
   pdl_wait();   // K3a's factor state (the tables above are independent of it)
   pdl_trigger();   // the finalisation may launch early (it waits for this grid's completion)
+  // chunk schedule: dynamic through one global counter (default), or static round robin over the
+  // grid's warps with the next chunk's header loaded one chunk ahead (MIS_K3_STATIC=1): ~12% of
+  // the fused kernel's stall samples sit on the counter's atomics, but the static schedule's tail
+  // imbalance costs more (C3: 0.647 vs 0.637 ms/step)
+  const int64_t cstride = (int64_t)point_grid * kWarps;
   int64_t c = 0;
-  if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
-  c = __shfl_sync(0xffffffffu, c, 0);
+  if (MIS_K3_STATIC) {
+    c = (int64_t)blockIdx.x * kWarps + warp;
+  } else {
+    if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+  }
   const float4* ps = a.pstate;
   const int64_t S = a.pstride;
+  int4 ch_next = c < a.nchunk ? a.chunks[c] : make_int4(0, 0, 0, 0);
   for (; c < a.nchunk;) {
-    const int4 ch = a.chunks[c];
+    const int4 ch = ch_next;
+    if (MIS_K3_STATIC && c + cstride < a.nchunk) ch_next = a.chunks[c + cstride];   // in flight meanwhile
     const int seg = ch.x;
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
     __syncwarp();
@@ -752,8 +766,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
       }
     }
     __syncwarp();
-    int64_t next_chunk = 0;
-    if (lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next chunk id
+    int64_t next_chunk = c + cstride;
+    if (!MIS_K3_STATIC && lane == 0) next_chunk = (int64_t)atomicAdd(a.work_counter, 1ull);   // prefetch the next id
 #pragma unroll
     for (int k = 0; k < NIT; ++k) {
       const uint32_t d = cdesc[k][lane];
@@ -774,6 +788,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     }
     __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
+    if (!MIS_K3_STATIC && c < a.nchunk) ch_next = a.chunks[c];
   }
   if constexpr (FUSED) commit_point_energies(a, ed, ep, n_as);
 }
