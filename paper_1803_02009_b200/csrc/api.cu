@@ -19,6 +19,9 @@ struct mis_ctx : public mis::Ctx {};
 namespace mis {
 
 // ------------------------------------------------------------ buffers
+#ifndef MIS_ENSURE_SLACK_DIV
+#define MIS_ENSURE_SLACK_DIV 4   // a (re)allocation takes 1 + 1/DIV times the request
+#endif
 static constexpr size_t kWsAlign = 256;
 
 // first-fit allocation from the bound workspace (mis_bind_workspace); nullptr when it is exhausted
@@ -59,7 +62,7 @@ cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes) {
     if (e != cudaSuccess) return e;
     free_buf(c, b);
   }
-  size_t alloc = bytes + bytes / 4 + 256;
+  size_t alloc = bytes + bytes / MIS_ENSURE_SLACK_DIV + 256;
   if (c->ws_base) {
     b.p = ws_alloc(c, alloc);
     if (!b.p) {
@@ -537,7 +540,7 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
       cs * (mr + 1) * 4, cs * mp * 4, cs * mr * 64, 128, 4 * m,              // cluster PCG lists
       // accumulators, system and PCG sized for 12 x 12 blocks (the affine nodes of NEXT-4)
       nnz * 304 * 4 + (12 * m + 3) * 4 + 48 * m + 48 * m, kEnergyDoubles * 8,  // accumulators
-      576 * nnz, 48 * m, 576 * m, 5 * 48 * m, (8 * (int64_t)c->prm.pcg_iters + 8) * 8,   // system, PCG
+      576 * nnz, 48 * m, 576 * m, 14 * 48 * m, (8 * (int64_t)c->prm.pcg_iters + 16) * 8,   // system, PCG
       144 * nnz, 24 * m, 96 * m,                                            // LM second system, kept nodes
       (K + 2) * 16 * n,                                                     // K3a -> K3b state
       4 * px, 16 * px, 32 * px, 12 * px, 8 * px, 4 * px, (2 * ((px + 255) / 256) + 4) * 4,   // frame, fusion
@@ -974,6 +977,7 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.rhs = c->rhs.as<float>();
   s.Minv = c->Minv.as<float>();
   s.x = c->x.as<float>(); s.r = c->r.as<float>(); s.z = c->z.as<float>(); s.p = c->p.as<float>(); s.Ap = c->Ap.as<float>();
+  s.pv = c->pvec.as<float>();
   s.dots = c->dots.as<double>();
   s.nd = node_view(c);
   s.do_update = update ? 1 : 0;

@@ -234,6 +234,7 @@ struct SolveArgs {
   float* rhs;                 // 6m
   float* Minv;                // m*36
   float *x, *r, *z, *p, *Ap;  // 6m
+  float* pv;                  // grid pipelined PCG: 9 planes of B m floats (r u w z q s p m m)
   double* dots;               // 2*pcg_iters + 4
   NodeView nd;
   int do_update;              // 0: only build the system (debug)

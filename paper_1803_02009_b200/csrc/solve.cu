@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   double* pose_y = a.dots + 2 * a.pcg_iters + 8;   // 6 per iteration
 
   // ---- phase 0: H (both triangles) and b are final (record reduction); clear the dot slots
-  if (tid < 8 * a.pcg_iters + 8) a.dots[tid] = 0.0;
+  if (tid < 8 * a.pcg_iters + 16) a.dots[tid] = 0.0;
   grid.sync();
   if (a.pcg_iters <= 0 && !a.do_update) return;
 
@@ -291,9 +291,343 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   }
 }
 
+// ---- pipelined grid PCG (Ghysels & Vanroose 2014, as the cluster kernel): ONE grid barrier per
+// iteration.  Per iteration every lane group of kG lanes owns a block row j: n_j = (A m)_j, then
+//   z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p,
+//   x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z,
+// then m'_j = M_j w_j (the node's whole block in the group) and the partials of the next dots
+// gamma = (r, u), delta = (w, u); the barrier completes the dots (fp64 atomics), alpha and beta follow
+// on every thread (same values everywhere).  m is double-buffered by iteration parity.  The same
+// Krylov iterates as the standard recurrence in exact arithmetic; the MIRROR early stops are
+// gamma == r.z == 0 and delta - beta gamma / alpha_prev == p.A p <= 0.
+// NEXT-2: the dense pose row (unknown pose_node) as an arrowhead: every thread keeps the pose's
+// vector entries in registers and uses them for the pose column of every block row; the pose row's
+// products n_pose are partial sums over all threads (fp64 slots per iteration), finished after
+// the barrier identically by every thread.
+// Planes of a.pv (B m floats each): 0 r, 1 u, 2 w, 3 z, 4 q, 5 s, 6 p, 7 m (even), 8 m (odd).
+template <int B>
+__global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
+  constexpr int BB = B * B, kG = 8, H2 = (B + kG - 1) / kG;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[32];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int m = a.m;
+  const bool has_pose = B == 6 && a.pose_node >= 0;
+  const int pose = has_pose ? a.pose_node : -1;
+  const int64_t nrows = has_pose ? pose : m;   // block rows of the row loop
+  const int64_t BM = (int64_t)B * m;
+  float* const R = a.pv;
+  float* const U = a.pv + BM;
+  float* const Wv = a.pv + 2 * BM;
+  float* const Z = a.pv + 3 * BM;
+  float* const Q = a.pv + 4 * BM;
+  float* const S = a.pv + 5 * BM;
+  float* const P = a.pv + 6 * BM;
+  float* const Mb[2] = {a.pv + 7 * BM, a.pv + 8 * BM};
+  double* const dots = a.dots;                        // [0, 2]: init gamma, delta; 2 + 2 it (+1): iteration it
+  double* const pose_y = a.dots + 2 * a.pcg_iters + 8;   // 6 per pass (init: slot 0, iteration it: slot it + 1)
+  const int lg = threadIdx.x & (kG - 1);
+  const unsigned gm = ((1u << kG) - 1u) << (threadIdx.x & 31 & ~(kG - 1));
+  const int lane = threadIdx.x & 31;
+
+  if (tid < 8 * a.pcg_iters + 16) dots[tid] = 0.0;
+  grid.sync();
+  if (a.pcg_iters <= 0 && !a.do_update) return;
+
+  // pose registers (NEXT-2)
+  float xp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, rp[6], up[6], wp[6], zp[6], qp[6], sp[6], pp[6], mp[6];
+  float Mp[36];
+  if (has_pose) {
+    for (int q = 0; q < 36; ++q) Mp[q] = __ldg(a.Minv + 36 * (int64_t)pose + q);
+    for (int c = 0; c < 6; ++c) rp[c] = a.rhs[6 * (int64_t)pose + c];
+    for (int r = 0; r < 6; ++r) {
+      float v = 0.f;
+      for (int c = 0; c < 6; ++c) v = fmaf(Mp[6 * r + c], rp[c], v);
+      up[r] = v;
+      zp[r] = qp[r] = sp[r] = pp[r] = 0.f;
+    }
+  }
+
+  // ---- init 1: x = 0, r = b, u = M r (lane groups per node)
+  for (int64_t j = tid / kG; j < nrows; j += nth / kG) {
+    float rr[H2];
+#pragma unroll
+    for (int h = 0; h < H2; ++h) {
+      const int c = lg + kG * h;
+      rr[h] = 0.f;
+      if (c < B) {
+        const int64_t q = B * j + c;
+        rr[h] = a.rhs[q];
+        a.x[q] = 0.f;
+        R[q] = rr[h];
+        Z[q] = 0.f; Q[q] = 0.f; S[q] = 0.f; P[q] = 0.f;
+      }
+    }
+    float rv[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) rv[c] = __shfl_sync(gm, rr[c / kG], c % kG, kG);
+#pragma unroll
+    for (int h = 0; h < H2; ++h) {
+      const int r = lg + kG * h;
+      if (r < B) {
+        const float2* Mi = reinterpret_cast<const float2*>(a.Minv + BB * j + B * r);
+        float v = 0.f;
+#pragma unroll
+        for (int c = 0; c < B; c += 2) {
+          const float2 mv = __ldg(Mi + c / 2);
+          v = fmaf(mv.x, rv[c], v);
+          v = fmaf(mv.y, rv[c + 1], v);
+        }
+        U[B * j + r] = v;
+      }
+    }
+  }
+  grid.sync();
+
+  // block row j of (A v): the kG lanes' strided blocks, summed by shuffles (all lanes get all B);
+  // the pose column from the registers pv_pose
+  auto row_product = [&](int64_t j, const float* vsrc, const float* pv_pose, float (&y)[B]) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) y[i] = 0.f;
+    for (int e = a.row_ptr[j] + lg; e < a.row_ptr[j + 1]; e += kG) {
+      const float4* H4 = reinterpret_cast<const float4*>(a.Hval + BB * (int64_t)e);
+      const int cl = a.col[e];
+      float zv[B];
+      if (B == 6 && cl == pose) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) zv[b] = pv_pose[b % 6];
+      } else {
+        const float* zz = vsrc + B * (int64_t)cl;
+#pragma unroll
+        for (int b = 0; b < B; b += 2) {
+          const float2 t = *reinterpret_cast<const float2*>(zz + b);
+          zv[b] = t.x;
+          zv[b + 1] = t.y;
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < BB / 4; ++f) {
+        const float4 h = __ldg(H4 + f);
+        const int i0 = (4 * f) / B, c0 = (4 * f) % B;
+        const float hv[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + (c0 + u) / B, c = (c0 + u) % B;
+          y[i] = fmaf(hv[u], zv[c], y[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = kG / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < B; ++i) y[i] += __shfl_xor_sync(gm, y[i], o, kG);
+  };
+  // the pose row's products over all threads -> slot (6 fp64)
+  auto pose_row = [&](const float* vsrc, const float* pv_pose, double* slot) {
+    if (!has_pose) return;
+    const int e0 = a.row_ptr[pose], e1 = a.row_ptr[pose + 1];
+    float yp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int64_t e = e0 + tid; e < e1; e += nth) {
+      const float4* H4 = reinterpret_cast<const float4*>(a.Hval + 36 * e);
+      const int cl = a.col[e];
+      float zv[6];
+      for (int b = 0; b < 6; ++b) zv[b] = cl == pose ? pv_pose[b] : vsrc[6 * (int64_t)cl + b];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) {
+        const float4 h = __ldg(H4 + f);
+        const float hv[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) yp[(4 * f + u) / 6] = fmaf(hv[u], zv[(4 * f + u) % 6], yp[(4 * f + u) / 6]);
+      }
+    }
+    if (e0 + (tid & ~31ll) < e1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 6; ++i) yp[i] += __shfl_xor_sync(0xffffffffu, yp[i], o);
+      if (lane < 6) {
+        float v = 0.f;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) v = (i == lane) ? yp[i] : v;
+        atomicAdd(slot + lane, (double)v);
+      }
+    }
+  };
+  // m'_j = M_j w_j for the group's node (w components wv[h] of this lane) -> dst; returns nothing
+  auto precond_row = [&](int64_t j, const float (&wv)[H2], float* dst) {
+    float wa[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) wa[c] = __shfl_sync(gm, wv[c / kG], c % kG, kG);
+#pragma unroll
+    for (int h = 0; h < H2; ++h) {
+      const int r = lg + kG * h;
+      if (r < B) {
+        const float2* Mi = reinterpret_cast<const float2*>(a.Minv + BB * j + B * r);
+        float v = 0.f;
+#pragma unroll
+        for (int c = 0; c < B; c += 2) {
+          const float2 mv = __ldg(Mi + c / 2);
+          v = fmaf(mv.x, wa[c], v);
+          v = fmaf(mv.y, wa[c + 1], v);
+        }
+        dst[B * j + r] = v;
+      }
+    }
+  };
+
+  // ---- init 2: w = A u, m = M w (parity 0), gamma0 = (r, u), delta0 = (w, u)
+  double dg = 0.0, dd = 0.0;
+  for (int64_t j = tid / kG; j < nrows; j += nth / kG) {
+    float y[B];
+    row_product(j, U, up, y);
+    float wv[H2];
+#pragma unroll
+    for (int h = 0; h < H2; ++h) {
+      const int c = lg + kG * h;
+      wv[h] = 0.f;
+      if (c < B) {
+        float yc = 0.f;
+#pragma unroll
+        for (int i = 0; i < B; ++i) yc = (i == c) ? y[i] : yc;
+        const int64_t q = B * j + c;
+        const float uq = U[q];
+        wv[h] = fmaf(a.lambda, uq, yc);
+        Wv[q] = wv[h];
+        dg += (double)R[q] * (double)uq;
+        dd += (double)wv[h] * (double)uq;
+      }
+    }
+    precond_row(j, wv, Mb[0]);
+  }
+  pose_row(U, up, pose_y);
+  {
+    const double s1 = block_sum(dg, sh), s2 = block_sum(dd, sh);
+    if (threadIdx.x == 0) { atomicAdd(dots + 0, s1); atomicAdd(dots + 1, s2); }
+  }
+  grid.sync();
+  double g = dots[0], d = dots[1];
+  if (has_pose) {
+    for (int c = 0; c < 6; ++c) wp[c] = fmaf(a.lambda, up[c], (float)pose_y[c]);
+    for (int r = 0; r < 6; ++r) {
+      float v = 0.f;
+      for (int c = 0; c < 6; ++c) v = fmaf(Mp[6 * r + c], wp[c], v);
+      mp[r] = v;
+    }
+    for (int c = 0; c < 6; ++c) {
+      g += (double)rp[c] * (double)up[c];
+      d += (double)wp[c] * (double)up[c];
+    }
+  }
+  const double g0 = g;
+  double gprev = 1.0, aprev_den = 1.0;
+  bool nonfin = false;
+  for (int it = 0; it < a.pcg_iters; ++it) {
+    if (!isfinite(g) || !isfinite(d)) { nonfin = true; break; }   // MIS_E_NUMERIC below
+    if (g == 0.0) break;
+    const double beta = it == 0 ? 0.0 : g / gprev;
+    const double den = it == 0 ? d : d - beta * g * (aprev_den / gprev);
+    if (!(den > 0.0)) break;
+    const float fa = (float)(g / den), fb = (float)beta;
+    const float* Mc = Mb[it & 1];
+    float* Mn = Mb[(it + 1) & 1];
+    double* slot = pose_y + 6 * (it + 1);
+    dg = 0.0;
+    dd = 0.0;
+    for (int64_t j = tid / kG; j < nrows; j += nth / kG) {
+      float y[B];
+      row_product(j, Mc, mp, y);
+      float wv[H2];
+#pragma unroll
+      for (int h = 0; h < H2; ++h) {
+        const int c = lg + kG * h;
+        wv[h] = 0.f;
+        if (c < B) {
+          float yc = 0.f;
+#pragma unroll
+          for (int i = 0; i < B; ++i) yc = (i == c) ? y[i] : yc;
+          const int64_t q = B * j + c;
+          const float mq = Mc[q];
+          const float n = fmaf(a.lambda, mq, yc);
+          const float zn = fmaf(fb, Z[q], n), qn = fmaf(fb, Q[q], mq), sn = fmaf(fb, S[q], Wv[q]);
+          const float pn = fmaf(fb, P[q], U[q]);
+          const float xn = fmaf(fa, pn, a.x[q]), rn = fmaf(-fa, sn, R[q]), un = fmaf(-fa, qn, U[q]);
+          const float wn = fmaf(-fa, zn, Wv[q]);
+          Z[q] = zn; Q[q] = qn; S[q] = sn; P[q] = pn; a.x[q] = xn; R[q] = rn; U[q] = un; Wv[q] = wn;
+          wv[h] = wn;
+          dg += (double)rn * (double)un;
+          dd += (double)wn * (double)un;
+        }
+      }
+      precond_row(j, wv, Mn);
+    }
+    pose_row(Mc, mp, slot);
+    {
+      const double s1 = block_sum(dg, sh), s2 = block_sum(dd, sh);
+      if (threadIdx.x == 0) { atomicAdd(dots + 2 + 2 * it, s1); atomicAdd(dots + 3 + 2 * it, s2); }
+    }
+    grid.sync();
+    double gn = dots[2 + 2 * it], dn = dots[3 + 2 * it];
+    if (has_pose) {   // the pose's entries, identically in every thread
+      for (int c = 0; c < 6; ++c) {
+        const float n = fmaf(a.lambda, mp[c], (float)slot[c]);
+        zp[c] = fmaf(fb, zp[c], n);
+        qp[c] = fmaf(fb, qp[c], mp[c]);
+        sp[c] = fmaf(fb, sp[c], wp[c]);
+        pp[c] = fmaf(fb, pp[c], up[c]);
+        xp[c] = fmaf(fa, pp[c], xp[c]);
+        rp[c] = fmaf(-fa, sp[c], rp[c]);
+        up[c] = fmaf(-fa, qp[c], up[c]);
+        wp[c] = fmaf(-fa, zp[c], wp[c]);
+      }
+      for (int r = 0; r < 6; ++r) {
+        float v = 0.f;
+        for (int c = 0; c < 6; ++c) v = fmaf(Mp[6 * r + c], wp[c], v);
+        mp[r] = v;
+      }
+      for (int c = 0; c < 6; ++c) {
+        gn += (double)rp[c] * (double)up[c];
+        dn += (double)wp[c] * (double)up[c];
+      }
+    }
+    gprev = g;
+    aprev_den = den;
+    g = gn;
+    d = dn;
+  }
+  if (tid == 0) a.rep_res[a.gn_it] = (float)(g0 > 0 ? sqrt(fabs(g / g0)) : 0.0);
+  if (has_pose && tid == 0)
+    for (int c = 0; c < 6; ++c) {
+      a.x[6 * (int64_t)pose + c] = xp[c];
+      if (a.do_update && !isfinite(xp[c])) atomicOr(a.numeric_flag, 1);
+    }
+  if (!a.do_update) return;
+  if (nonfin && tid == 0) atomicOr(a.numeric_flag, 1);
+  for (int64_t j = tid; j < nrows; j += nth)
+    for (int c = 0; c < B; ++c)
+      if (!isfinite(a.x[B * j + c])) atomicOr(a.numeric_flag, 1);
+  grid.sync();
+  if (*a.numeric_flag) return;
+  for (int64_t j = tid; j < m; j += nth) {
+    if constexpr (B == 12) {   // NEXT-4 (A41): A_j += dA_j, t_j += dt_j
+      for (int c = 0; c < 12; ++c) {
+        const double v = a.nd.Rt64[12 * j + c] + (double)a.x[12 * j + c];
+        a.nd.Rt64[12 * j + c] = v;
+        a.nd.node32[16 * j + c] = (float)v;
+      }
+    } else {
+      if (j == pose) pose_update(a.x + 6 * j, a.pose);   // A37
+      else node_update(a.x + 6 * j, a.nd.Rt64 + 12 * j, a.nd.node32 + 16 * j);
+    }
+  }
+}
+
 cudaError_t launch_solve_grid(const SolveArgs& a, int num_sms, cudaStream_t s) {
   int per_sm = 1;
-  const void* kern = a.block == 12 ? (const void*)k_solve<12> : (const void*)k_solve<6>;
+  // the pipelined recurrence (one grid barrier per iteration) unless MIS_F_STANDARD_PCG asks for
+  // the textbook one (two barriers)
+  const void* kern = a.pipelined ? (a.block == 12 ? (const void*)k_solve_pipe<12> : (const void*)k_solve_pipe<6>)
+                                 : (a.block == 12 ? (const void*)k_solve<12> : (const void*)k_solve<6>);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (void (*)(SolveArgs))kern, 256, 0);
   int64_t work = (int64_t)a.block * a.m;
   if (a.nnzb > work) work = a.nnzb;

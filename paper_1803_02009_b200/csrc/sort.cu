@@ -772,7 +772,8 @@ cudaError_t build_pattern(Ctx* c) {
   CK(ensure(c, c->rhs, m6 * 4)); CK(ensure(c, c->Minv, (size_t)mu * BB * 4));
   CK(ensure(c, c->x, m6 * 4)); CK(ensure(c, c->r, m6 * 4)); CK(ensure(c, c->z, m6 * 4));
   CK(ensure(c, c->p, m6 * 4)); CK(ensure(c, c->Ap, m6 * 4));
-  CK(ensure(c, c->dots, (8 * (size_t)c->prm.pcg_iters + 8) * 8));   // dots | pose_y (grid PCG)
+  CK(ensure(c, c->pvec, 9 * m6 * 4));   // the grid PCG's pipelined vectors (also a fallback of the cluster one)
+  CK(ensure(c, c->dots, (8 * (size_t)c->prm.pcg_iters + 16) * 8));   // dots | pose_y (grid PCG)
   c->pattern_valid = true;
   return cudaSuccess;
 }

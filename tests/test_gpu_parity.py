@@ -179,14 +179,15 @@ def rot_err(Ra, Rb):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
-@pytest.mark.parametrize("solver", ["cluster", "cluster_standard", "grid"])
+@pytest.mark.parametrize("solver", ["cluster", "cluster_standard", "grid", "grid_standard"])
 def test_register_parity_mirror(cfg, solver):
     sc, pb, fr, _ = scene_problem(cfg)
     flags = M.MIS_F_FINAL_ENERGY | {"cluster": 0, "cluster_standard": M.MIS_F_STANDARD_PCG,
-                                    "grid": M.MIS_F_GRID_SOLVER}[solver]
+                                    "grid": M.MIS_F_GRID_SOLVER,
+                                    "grid_standard": M.MIS_F_GRID_SOLVER | M.MIS_F_STANDARD_PCG}[solver]
     ctx = make_ctx(sc, pb, flags=flags)
     rep = M.report_dict(M.mis_register(ctx.ptr))
-    assert (rep["solver_cluster"] > 0) == (solver != "grid")
+    assert (rep["solver_cluster"] > 0) == (not solver.startswith("grid"))
     m = pb.g.shape[0]
     Rg = M.mis_get_nodes_f64(ctx.ptr, m)
     Ro, Eo, nao = O.register(oracle_params(ctx.params), pb, fr)
