@@ -82,8 +82,10 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    with its diagonal entries times (1 + mu), from that state.
                                    The last trial is evaluated too (energy row [iters]) and kept
                                    only if accepted.  Per-iteration decisions in report n_guard.
-                                   Needs the register-resident cluster PCG (systems of C1-C3
-                                   size, pipelined recurrence): else MIS_E_ARG                      */
+                                   Runs in the register-resident pipelined cluster PCG (systems
+                                   of C1-C3 size) or else the pipelined grid PCG (the damped
+                                   block-Jacobi inverses built there); combines with
+                                   MIS_F_JOINT_POSE and MIS_F_AFFINE; single GPU (MIS_E_ARG)        */
 #define MIS_F_JOINT_POSE  32u   /* NEXT-2 (readings A37-A40): the global pose (R, T) of
                                    Eq. 1 is refined jointly with the nodes as unknown number m
                                    ("only 6 more variables"): increment R <- R Exp(dphi),
@@ -96,8 +98,7 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    block-Jacobi preconditioner and lambda like a node.  The refined
                                    pose is used by mis_warp / mis_fuse of the frame and read with
                                    mis_get_pose.  Solved by the grid-wide PCG (the pose row is
-                                   dense).  Requires k <= 7 and world == 1; not with MIS_F_LM
-                                   (MIS_E_ARG)                                                      */
+                                   dense).  Requires k <= 7 and world == 1 (MIS_E_ARG)              */
 #define MIS_F_AFFINE      64u   /* NEXT-4 (Eq. 1, Eq. 4-6; readings A41-A45): every node carries
                                    the paper's general 3x3 matrix A_j instead of a rotation -- 12
                                    unknowns per node [dA_j row-major, dt_j], additive update,
@@ -106,8 +107,8 @@ typedef struct { float fx, fy, cx, cy; int32_t width, height; } mis_intrinsics;
                                    A_j^-T (A_j itself if |det A_j| < 1e-9).  Node states in the
                                    R9_t3 arrays of mis_get_nodes / mis_dbg_set_nodes are then
                                    A (row-major 9), t.  Gauss-Newton with the grid-wide PCG;
-                                   requires k <= 4 and world == 1; not with MIS_F_LM or
-                                   MIS_F_JOINT_POSE (MIS_E_ARG)                                     */
+                                   requires k <= 4 and world == 1; not with MIS_F_JOINT_POSE
+                                   (MIS_E_ARG)                                                      */
 
 /* Method parameters; defaults (mis_default_params) are the paper's. */
 typedef struct {

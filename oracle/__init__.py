@@ -116,7 +116,7 @@ def lib():
                                        C.c_double, C.c_int32, C.c_int32, C.c_void_p]
             L.or_solve_aff.restype = C.c_int32
             L.or_register_aff.argtypes = [P(or_params), P(or_problem), P(or_frame), C.c_void_p, C.c_void_p,
-                                          C.c_void_p]
+                                          C.c_void_p, C.c_void_p]
             L.or_warp_model_aff.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_warp_model.argtypes = [P(or_problem), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.or_fuse.argtypes = [P(or_params), P(or_model), P(or_frame), C.c_void_p, C.c_int32, C.c_int32,
@@ -440,13 +440,15 @@ def solve_aff(sysd, m, lam, mode, pcg_iters):
     return x, it
 
 
-def register_aff(prm: or_params, pb: Problem, fr: Frame, At0=None):
-    """Affine-node Gauss-Newton: returns (At, E (G+1 x 6), n_assoc)."""
+def register_aff(prm: or_params, pb: Problem, fr: Frame, At0=None, with_accepted=False):
+    """Affine-node Gauss-Newton (or LM with prm.lm): returns (At, E (G+1 x 6), n_assoc[, accepted])."""
     m = pb.g.shape[0]
     At = identity_affine(m) if At0 is None else np.array(At0, np.float64, copy=True)
     G = prm.gn_iters
-    E = np.zeros((G + 1, 6)); na = np.zeros(G + 1, np.int64)
-    lib().or_register_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(E), _p(na))
+    E = np.zeros((G + 1, 6)); na = np.zeros(G + 1, np.int64); acc = np.zeros(G + 1, np.int32)
+    lib().or_register_aff(C.byref(prm), C.byref(pb.s), C.byref(fr.s), _p(At), _p(E), _p(na), _p(acc))
+    if with_accepted:
+        return At, E, na, acc
     return At, E, na
 
 

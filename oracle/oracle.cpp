@@ -1716,21 +1716,63 @@ int32_t or_solve_aff(int32_t m, int64_t nblk, const int32_t* brow, const int32_t
 // O9f: fixed-G Gauss-Newton over the affine nodes; energy (G+1) x 6 (E_data, E_pt, E_reg, E_corr,
 // E_rot, weighted total); At (m x 12) initial state on entry, result on exit
 void or_register_aff(const or_params* prm, const or_problem* p, const or_frame* f, double* At, double* energy,
-                     int64_t* n_assoc) {
+                     int64_t* n_assoc, int32_t* accepted) {
   std::vector<int32_t> fidx;
   std::vector<double> fw;
   feature_skin(p, prm->k, fidx, fw);
-  for (int it = 0; it <= prm->gn_iters; ++it) {
-    SystemA S(p->m);
-    assemble_aff(prm, p, f, At, fidx.data(), fw.data(), &S);
+  auto record = [&](int it, const SystemA& S) {
     for (int a = 0; a < 5; ++a) energy[6 * it + a] = S.E[a];
     energy[6 * it + 5] = total_energy_aff(prm, S.E);
     n_assoc[it] = S.n_assoc;
-    if (it == prm->gn_iters) break;
-    std::vector<double> x;
-    solve_aff(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+  };
+  auto step = [&](const std::vector<double>& x) {
     for (int j = 0; j < p->m; ++j)   // A41: additive update
       for (int a = 0; a < 12; ++a) At[12 * j + a] += x[12 * j + a];
+  };
+  if (!prm->lm) {
+    for (int it = 0; it <= prm->gn_iters; ++it) {
+      SystemA S(p->m);
+      assemble_aff(prm, p, f, At, fidx.data(), fw.data(), &S);
+      record(it, S);
+      if (accepted) accepted[it] = 1;
+      if (it == prm->gn_iters) break;
+      std::vector<double> x;
+      solve_aff(S, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+      step(x);
+    }
+    return;
+  }
+  // Levenberg-Marquardt with the schedule of R-A29, as register_impl
+  const size_t ns = 12 * (size_t)p->m;
+  std::vector<double> base(At, At + ns);
+  SystemA acc(p->m);
+  double E_acc = 0.0, mu = prm->lm_mu0;
+  for (int it = 0; it <= prm->gn_iters; ++it) {
+    SystemA S(p->m);
+    assemble_aff(prm, p, f, At, fidx.data(), fw.data(), &S);
+    record(it, S);
+    const double E = total_energy_aff(prm, S.E);
+    const bool ok = it == 0 || E < E_acc;
+    if (accepted) accepted[it] = ok ? 1 : 0;
+    if (ok) {
+      std::copy(At, At + ns, base.begin());
+      acc = S;
+      E_acc = E;
+      if (it > 0) mu *= 0.5;
+    } else {
+      std::copy(base.begin(), base.end(), At);
+      mu *= 10.0;
+    }
+    if (it == prm->gn_iters) break;
+    SystemA D = acc;   // damped copy: diagonal entries of H times (1 + mu)
+    for (int j = 0; j < p->m; ++j) {
+      auto d = D.blk.find(std::make_pair(j, j));
+      if (d != D.blk.end())
+        for (int a = 0; a < 12; ++a) d->second[13 * a] *= 1.0 + mu;
+    }
+    std::vector<double> x;
+    solve_aff(D, prm->lambda, prm->solve_mode, prm->pcg_iters, x);
+    step(x);
   }
 }
 

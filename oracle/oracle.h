@@ -154,8 +154,9 @@ int64_t or_residuals_aff(const or_params* prm, const or_problem* p, const or_fra
                          double* J);
 int32_t or_solve_aff(int32_t m, int64_t nblk, const int32_t* brow, const int32_t* bcol, const double* bval,
                      const double* rhs, double lambda, int32_t mode, int32_t pcg_iters, double* x);
+/* prm->lm: Levenberg-Marquardt with the schedule of or_register (R-A29); accepted (G+1) nullable */
 void or_register_aff(const or_params* prm, const or_problem* p, const or_frame* f, double* At, double* energy,
-                     int64_t* n_assoc);
+                     int64_t* n_assoc, int32_t* accepted);
 void or_warp_model_aff(const or_problem* p, int32_t k, const double* At, double* xyz_out, double* nrm_out,
                        double* g_out);
 /* O4: apply the field: live world state x_hat, unit normals; advanced nodes g+t. */

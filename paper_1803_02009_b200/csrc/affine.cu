@@ -386,6 +386,10 @@ __device__ __forceinline__ float pt_aff(const float* Mo, bool diag, int i, int j
 __global__ void __launch_bounds__(256) k_finalize_aff(FinalArgs r) {
   __shared__ float hst[8][144];
   pdl_wait();
+  if (r.lm && r.lm->acc_buf == 0) {   // LM: keep the accepted system, write the trial's into the other buffer
+    r.Hval = r.Hval_alt;
+    r.rhs = r.rhs_alt;
+  }
   pdl_trigger();
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

@@ -20,7 +20,7 @@ namespace mis {
 
 // ------------------------------------------------------------ buffers
 #ifndef MIS_ENSURE_SLACK_DIV
-#define MIS_ENSURE_SLACK_DIV 4   // a (re)allocation takes 1 + 1/DIV times the request
+#define MIS_ENSURE_SLACK_DIV 2   // a (re)allocation takes 1 + 1/DIV times the request (growing sequences: fewer reallocations)
 #endif
 static constexpr size_t kWsAlign = 256;
 
@@ -421,8 +421,8 @@ static mis_status check_params(const mis_params* p) {
       !(p->w_p >= 0) || !std::isfinite(p->w_r) || !std::isfinite(p->w_p) || !(p->w_rot >= 0) ||
       !std::isfinite(p->w_rot))
     return MIS_E_ARG;
-  if ((p->flags & MIS_F_AFFINE) && (p->k > 4 || (p->flags & (MIS_F_LM | MIS_F_JOINT_POSE)))) return MIS_E_ARG;
-  if ((p->flags & MIS_F_JOINT_POSE) && (p->k > MIS_MAX_K - 1 || (p->flags & MIS_F_LM))) return MIS_E_ARG;
+  if ((p->flags & MIS_F_AFFINE) && (p->k > 4 || (p->flags & MIS_F_JOINT_POSE))) return MIS_E_ARG;
+  if ((p->flags & MIS_F_JOINT_POSE) && p->k > MIS_MAX_K - 1) return MIS_E_ARG;
   return MIS_OK;
 }
 
@@ -553,7 +553,7 @@ static size_t workspace_plan(const Ctx* c, int64_t n, int64_t m, int64_t H, int6
   size_t total = 0;
   for (int64_t x : b) {
     const size_t bytes = (size_t)std::max<int64_t>(x, 16);
-    total += ((bytes + bytes / 4 + 256) + kWsAlign - 1) & ~(kWsAlign - 1);   // ensure()'s growth slack
+    total += ((bytes + bytes / MIS_ENSURE_SLACK_DIV + 256) + kWsAlign - 1) & ~(kWsAlign - 1);   // ensure()'s slack
   }
   return total + total / 8 + (1 << 20);   // first-fit fragmentation margin
 }
@@ -984,14 +984,17 @@ static SolveArgs solve_args(Ctx* c, int it, bool update, int pcg_iters) {
   s.gn_it = it;
   s.rep_res = rep_res(c);
   s.numeric_flag = numeric_flag(c);
-  const bool cl = c->cl_size > 0 && c->cluster_ok && !(c->prm.flags & MIS_F_GRID_SOLVER);
+  const bool lm_flag = (c->prm.flags & MIS_F_LM) != 0;
+  // LM runs in the register-resident pipelined cluster kernel or in the pipelined grid kernel
+  const bool cl_lm_ok = 6 * c->cl_max_rows <= 512 && !(c->prm.flags & MIS_F_STANDARD_PCG);
+  const bool cl = c->cl_size > 0 && c->cluster_ok && !(c->prm.flags & MIS_F_GRID_SOLVER) && (!lm_flag || cl_lm_ok);
   s.cluster_size = cl ? c->cl_size : 0;
   s.part = c->part.as<int32_t>();
   s.max_rows = c->cl_max_rows;
   s.max_nnz = c->cl_max_nnz;
   s.smem_bytes = c->cl_smem;
   s.write_global = update ? 0 : 1;
-  s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) ? 0 : 1;
+  s.pipelined = (c->prm.flags & MIS_F_STANDARD_PCG) && !lm_flag ? 0 : 1;
   s.minv_ready = 1;   // built by the finalisation (after the all-reduce when sharded)
   s.tstamp = c->tstamp.as<unsigned long long>();
   s.pptr = c->pcg_pptr.as<int32_t>();
@@ -1123,34 +1126,30 @@ mis_status mis_register(mis_ctx* c, mis_mem mem, const float* depth_mm, const mi
   if ((s = prepare(c)) != MIS_OK) return s;
   const int G = c->prm.gn_iters;
   const bool lm = c->prm.flags & MIS_F_LM;
-  if (lm) {   // the register-resident pipelined cluster PCG carries the LM decisions
-    const bool ok = c->cl_size > 0 && c->cluster_ok && 6 * c->cl_max_rows <= 512 &&
-                    !(c->prm.flags & (MIS_F_GRID_SOLVER | MIS_F_STANDARD_PCG)) && c->world == 1;
-    if (!ok) return fail(c, MIS_E_ARG, "MIS_F_LM needs the register-resident cluster PCG (single GPU)");
+  if (lm) {   // the LM decisions live in the register-resident pipelined cluster PCG and in the
+              // pipelined grid PCG (solve_args picks one of them)
+    if (c->world != 1) return fail(c, MIS_E_ARG, "MIS_F_LM: single GPU only");
     const bool fresh = !c->lm.p;
+    const size_t B = (size_t)sys_b(c), mu = (size_t)sys_m(c);
     TRY(c, ensure(c, c->lm, 64));
     if (fresh) TRY(c, cudaMemsetAsync(c->lm.p, 0, 64, c->st));
-    TRY(c, ensure(c, c->Hval2, (size_t)c->nnzb * 36 * 4));
-    TRY(c, ensure(c, c->rhs2, (size_t)c->m * 6 * 4));
-    TRY(c, ensure(c, c->Rt_acc, (size_t)c->m * 96));
+    TRY(c, ensure(c, c->Hval2, (size_t)c->nnzb * B * B * 4));
+    TRY(c, ensure(c, c->rhs2, mu * B * 4));
+    TRY(c, ensure(c, c->Rt_acc, mu * 96));   // the kept node states (+ the pose, NEXT-2)
   }
   for (int it = 0; it < G; ++it) {
     if ((s = assemble(c, false, it)) != MIS_OK) return s;
     ProfScope ps(c, P_SOLVE, 1);
     const SolveArgs sa = solve_args(c, it, true, c->prm.pcg_iters);
-    if (lm) {   // no grid fallback: it has no LM logic
-      TRY(c, launch_solve(sa, c->num_sms, c->st));
-      c->last_solver = sa.cluster_size;
-    } else {
-      TRY(c, run_solve(c, sa));
-    }
+    TRY(c, run_solve(c, sa));
   }
   if ((c->prm.flags & MIS_F_FINAL_ENERGY) || lm)
     if ((s = assemble(c, false, G)) != MIS_OK) return s;
   if (lm) {   // the last trial is kept only if accepted
     ProfScope ps(c, P_SOLVE, 1);
     launch_lm_finish(c->m, G, reinterpret_cast<const LmDev*>(c->lm.p), rep_energy(c), rep_nassoc(c) + MIS_MAX_GN + 1,
-                     c->Rt64.as<double>(), c->Rt_acc.as<double>(), c->node32.as<float>(), c->st);
+                     c->Rt64.as<double>(), c->Rt_acc.as<double>(), c->node32.as<float>(), c->st,
+                     c->pattern_joint ? c->posebuf.as<double>() : nullptr);
   }
   TRY(c, cudaGetLastError());
   if (rep) return fill_report(c, rep, G);

@@ -264,7 +264,7 @@ struct SolveArgs {
   double* rep_flags;          // MIS_MAX_GN+1: 1 = trial accepted
 };
 void launch_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags, double* Rt64,
-                      const double* Rt_acc, float* node32, cudaStream_t s);
+                      const double* Rt_acc, float* node32, cudaStream_t s, double* pose = nullptr);
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;

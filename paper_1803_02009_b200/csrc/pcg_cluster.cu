@@ -1006,21 +1006,22 @@ cudaError_t launch_solve_cluster(const SolveArgs& a, cudaStream_t s) {
 // LM: the last trial (its energy in report slot `slot`) is kept only if accepted; otherwise
 // the kept state is restored (fp64 master and its fp32 copy)
 __global__ void k_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags,
-                            double* Rt64, const double* Rt_acc, float* node32) {
+                            double* Rt64, const double* Rt_acc, float* node32, double* pose) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const bool accept = rep_energy[5 * slot + 4] < lm->E_acc;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q == 0) rep_flags[slot] = accept ? 1.0 : 0.0;
+  if (!accept && pose && q < 12) pose[q] = Rt_acc[12 * (int64_t)m + q];   // NEXT-2: the kept pose (after the nodes)
   if (accept || q >= 12 * (int64_t)m) return;
   const double v = Rt_acc[q];
   Rt64[q] = v;
   node32[16 * (q / 12) + q % 12] = (float)v;
 }
 void launch_lm_finish(int m, int slot, const LmDev* lm, const double* rep_energy, double* rep_flags, double* Rt64,
-                      const double* Rt_acc, float* node32, cudaStream_t s) {
+                      const double* Rt_acc, float* node32, cudaStream_t s, double* pose) {
   launch_pdl(k_lm_finish, dim3((unsigned)((12 * (int64_t)m + 255) / 256)), dim3(256), 0, s, m, slot, lm, rep_energy,
-             rep_flags, Rt64, Rt_acc, node32);
+             rep_flags, Rt64, Rt_acc, node32, pose);
 }
 
 }  // namespace mis

@@ -291,6 +291,37 @@ __global__ void __launch_bounds__(256) k_solve(SolveArgs a) {
   }
 }
 
+// LM (MIS_F_LM) block-Jacobi inverse of the damped diagonal block: (H_jj with its diagonal times
+// (1 + mu) + (lambda + guard) I)^-1, guard = 1e-9 tr / B of the damped block (A17), fp64 Gauss-Jordan
+// (one thread per node; zeros if not positive definite)
+template <int B>
+__device__ void precond_block_lm(const float* Hjj, float lambda, double mu, float* Mi) {
+  double A[B][2 * B];
+  double tr = 0.0;
+  for (int i = 0; i < B; ++i) tr += (double)Hjj[(B + 1) * i] * (1.0 + mu);
+  const double guard = 1e-9 * tr / B;
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < B; ++j) {
+      const double h = (double)Hjj[B * i + j];
+      A[i][j] = i == j ? h * (1.0 + mu) + (double)lambda + guard : h;
+      A[i][B + j] = i == j ? 1.0 : 0.0;
+    }
+  bool pd = true;
+  for (int p = 0; p < B; ++p) {
+    const double pv = A[p][p];
+    if (!(pv > 0.0)) { pd = false; break; }
+    const double ipv = 1.0 / pv;
+    for (int q = 0; q < 2 * B; ++q) A[p][q] *= ipv;
+    for (int i = 0; i < B; ++i) {
+      if (i == p) continue;
+      const double f = A[i][p];
+      for (int q = 0; q < 2 * B; ++q) A[i][q] -= f * A[p][q];
+    }
+  }
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < B; ++j) Mi[B * i + j] = pd ? (float)A[i][B + j] : 0.f;
+}
+
 // ---- pipelined grid PCG (Ghysels & Vanroose 2014, as the cluster kernel): ONE grid barrier per
 // iteration.  Per iteration every lane group of kG lanes owns a block row j: n_j = (A m)_j, then
 //   z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p,
@@ -331,16 +362,65 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
   const unsigned gm = ((1u << kG) - 1u) << (threadIdx.x & 31 & ~(kG - 1));
   const int lane = threadIdx.x & 31;
 
+  // ---- Levenberg-Marquardt (MIS_F_LM, reading A29): every thread takes the same decision on the
+  // trial whose energy the finalisation reported -- accept if first or strictly lower than the last
+  // accepted -- then solves the trial's (accept) or the kept (reject) system, damped by mu H_cc on
+  // every diagonal entry, from the trial or the restored kept state (the pose included, NEXT-2)
+  const bool lm = a.lm != nullptr;
+  bool lm_accept = true;
+  double lm_mu = 0.0, lm_E = 0.0;
+  int lm_src = 0;
+  if (lm) {
+    const double Et = a.rep_energy[5 * a.gn_it + 4];
+    const LmDev st = *a.lm;
+    lm_accept = a.gn_it == 0 || Et < st.E_acc;
+    lm_mu = a.gn_it == 0 ? (double)a.lm_mu0 : (lm_accept ? 0.5 * st.mu : 10.0 * st.mu);
+    lm_E = lm_accept ? Et : st.E_acc;
+    lm_src = lm_accept ? 1 - st.acc_buf : st.acc_buf;
+  }
+  const float* const Hs = lm && lm_src == 1 ? a.Hval_alt : a.Hval;
+  const float* const bs = lm && lm_src == 1 ? a.rhs_alt : a.rhs;
   if (tid < 8 * a.pcg_iters + 16) dots[tid] = 0.0;
+  if (lm) {
+    for (int64_t q = tid; q < 12 * (int64_t)m; q += nth) {   // the step's base state; Rt_acc: the kept one
+      const int64_t j = q / 12;
+      if (j == pose) {   // the pose (A37) is kept after the nodes' rows of Rt_acc
+        const int c = (int)(q % 12);
+        if (lm_accept) a.Rt_acc[12 * (int64_t)pose + c] = a.pose[c];
+        else a.pose[c] = a.Rt_acc[12 * (int64_t)pose + c];
+        continue;
+      }
+      if (lm_accept) {
+        a.Rt_acc[q] = a.nd.Rt64[q];
+      } else {
+        const double v = a.Rt_acc[q];
+        a.nd.Rt64[q] = v;
+        a.nd.node32[16 * j + q % 12] = (float)v;
+      }
+    }
+    for (int64_t j = tid; j < m; j += nth)
+      precond_block_lm<B>(Hs + BB * (int64_t)a.diag_pos[j], a.lambda, lm_mu, a.Minv + BB * j);
+  }
   grid.sync();
+  if (lm && tid == 0) {   // every thread has read the LM state
+    a.lm->mu = lm_mu;
+    a.lm->E_acc = lm_E;
+    a.lm->acc_buf = lm_src;
+    a.rep_flags[a.gn_it] = lm_accept ? 1.0 : 0.0;
+  }
   if (a.pcg_iters <= 0 && !a.do_update) return;
+  const float mu_f = (float)lm_mu;   // the Marquardt term of element (j, c): mu H_jj[c][c] (0 without LM)
 
   // pose registers (NEXT-2)
   float xp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, rp[6], up[6], wp[6], zp[6], qp[6], sp[6], pp[6], mp[6];
   float Mp[36];
+  float lamp[6] = {a.lambda, a.lambda, a.lambda, a.lambda, a.lambda, a.lambda};   // LM: lambda + mu H_pp[c][c]
   if (has_pose) {
-    for (int q = 0; q < 36; ++q) Mp[q] = __ldg(a.Minv + 36 * (int64_t)pose + q);
-    for (int c = 0; c < 6; ++c) rp[c] = a.rhs[6 * (int64_t)pose + c];
+    for (int q = 0; q < 36; ++q) Mp[q] = a.Minv[36 * (int64_t)pose + q];
+    for (int c = 0; c < 6; ++c) rp[c] = bs[6 * (int64_t)pose + c];
+    if (lm)
+      for (int c = 0; c < 6; ++c)
+        lamp[c] = (float)((double)a.lambda + lm_mu * (double)Hs[36 * (int64_t)a.diag_pos[pose] + 7 * c]);
     for (int r = 0; r < 6; ++r) {
       float v = 0.f;
       for (int c = 0; c < 6; ++c) v = fmaf(Mp[6 * r + c], rp[c], v);
@@ -358,7 +438,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
       rr[h] = 0.f;
       if (c < B) {
         const int64_t q = B * j + c;
-        rr[h] = a.rhs[q];
+        rr[h] = bs[q];
         a.x[q] = 0.f;
         R[q] = rr[h];
         Z[q] = 0.f; Q[q] = 0.f; S[q] = 0.f; P[q] = 0.f;
@@ -375,7 +455,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
         float v = 0.f;
 #pragma unroll
         for (int c = 0; c < B; c += 2) {
-          const float2 mv = __ldg(Mi + c / 2);
+          const float2 mv = Mi[c / 2];
           v = fmaf(mv.x, rv[c], v);
           v = fmaf(mv.y, rv[c + 1], v);
         }
@@ -391,7 +471,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
 #pragma unroll
     for (int i = 0; i < B; ++i) y[i] = 0.f;
     for (int e = a.row_ptr[j] + lg; e < a.row_ptr[j + 1]; e += kG) {
-      const float4* H4 = reinterpret_cast<const float4*>(a.Hval + BB * (int64_t)e);
+      const float4* H4 = reinterpret_cast<const float4*>(Hs + BB * (int64_t)e);
       const int cl = a.col[e];
       float zv[B];
       if (B == 6 && cl == pose) {
@@ -429,7 +509,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
     const int e0 = a.row_ptr[pose], e1 = a.row_ptr[pose + 1];
     float yp[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int64_t e = e0 + tid; e < e1; e += nth) {
-      const float4* H4 = reinterpret_cast<const float4*>(a.Hval + 36 * e);
+      const float4* H4 = reinterpret_cast<const float4*>(Hs + 36 * e);
       const int cl = a.col[e];
       float zv[6];
       for (int b = 0; b < 6; ++b) zv[b] = cl == pose ? pv_pose[b] : vsrc[6 * (int64_t)cl + b];
@@ -467,7 +547,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
         float v = 0.f;
 #pragma unroll
         for (int c = 0; c < B; c += 2) {
-          const float2 mv = __ldg(Mi + c / 2);
+          const float2 mv = Mi[c / 2];
           v = fmaf(mv.x, wa[c], v);
           v = fmaf(mv.y, wa[c + 1], v);
         }
@@ -492,7 +572,9 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
         for (int i = 0; i < B; ++i) yc = (i == c) ? y[i] : yc;
         const int64_t q = B * j + c;
         const float uq = U[q];
-        wv[h] = fmaf(a.lambda, uq, yc);
+        const float lamc = lm ? (float)((double)a.lambda + lm_mu * (double)Hs[BB * (int64_t)a.diag_pos[j] + (B + 1) * c])
+                              : a.lambda;
+        wv[h] = fmaf(lamc, uq, yc);
         Wv[q] = wv[h];
         dg += (double)R[q] * (double)uq;
         dd += (double)wv[h] * (double)uq;
@@ -508,7 +590,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
   grid.sync();
   double g = dots[0], d = dots[1];
   if (has_pose) {
-    for (int c = 0; c < 6; ++c) wp[c] = fmaf(a.lambda, up[c], (float)pose_y[c]);
+    for (int c = 0; c < 6; ++c) wp[c] = fmaf(lamp[c], up[c], (float)pose_y[c]);
     for (int r = 0; r < 6; ++r) {
       float v = 0.f;
       for (int c = 0; c < 6; ++c) v = fmaf(Mp[6 * r + c], wp[c], v);
@@ -548,7 +630,9 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
           for (int i = 0; i < B; ++i) yc = (i == c) ? y[i] : yc;
           const int64_t q = B * j + c;
           const float mq = Mc[q];
-          const float n = fmaf(a.lambda, mq, yc);
+          const float lamc = lm ? (float)((double)a.lambda + lm_mu * (double)Hs[BB * (int64_t)a.diag_pos[j] + (B + 1) * c])
+                                : a.lambda;
+          const float n = fmaf(lamc, mq, yc);
           const float zn = fmaf(fb, Z[q], n), qn = fmaf(fb, Q[q], mq), sn = fmaf(fb, S[q], Wv[q]);
           const float pn = fmaf(fb, P[q], U[q]);
           const float xn = fmaf(fa, pn, a.x[q]), rn = fmaf(-fa, sn, R[q]), un = fmaf(-fa, qn, U[q]);
@@ -570,7 +654,7 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
     double gn = dots[2 + 2 * it], dn = dots[3 + 2 * it];
     if (has_pose) {   // the pose's entries, identically in every thread
       for (int c = 0; c < 6; ++c) {
-        const float n = fmaf(a.lambda, mp[c], (float)slot[c]);
+        const float n = fmaf(lamp[c], mp[c], (float)slot[c]);
         zp[c] = fmaf(fb, zp[c], n);
         qp[c] = fmaf(fb, qp[c], mp[c]);
         sp[c] = fmaf(fb, sp[c], wp[c]);

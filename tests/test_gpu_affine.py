@@ -119,7 +119,7 @@ def test_affine_warp_parity(cfg):
 
 
 def test_affine_errors():
-    for flags, k in [(M.MIS_F_AFFINE | M.MIS_F_LM, 4), (M.MIS_F_AFFINE | M.MIS_F_JOINT_POSE, 4), (M.MIS_F_AFFINE, 8)]:
+    for flags, k in [(M.MIS_F_AFFINE | M.MIS_F_JOINT_POSE, 4), (M.MIS_F_AFFINE, 8)]:
         with pytest.raises(M.MisError):
             M.Context(M.mis_default_params(k=k, flags=flags))
     with pytest.raises(M.MisError):

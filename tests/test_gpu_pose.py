@@ -21,7 +21,8 @@ def perturbed_pose(P, deg=0.5, dt=(0.8, -0.5, 0.3)):
 def joint_ctx(sc, pb, prior, **kw):
     sc = dict(sc)
     sc["pose"] = prior.astype(np.float32)   # the caller's pose is fp32 (mis_set_frame)
-    return make_ctx(sc, pb, flags=M.MIS_F_FINAL_ENERGY | M.MIS_F_JOINT_POSE, **kw), sc
+    flags = kw.pop("flags", 0) | M.MIS_F_FINAL_ENERGY | M.MIS_F_JOINT_POSE
+    return make_ctx(sc, pb, flags=flags, **kw), sc
 
 
 def ofr(sc):
@@ -106,7 +107,7 @@ def test_pose_warp_and_fuse_use_refined_pose():
 def test_pose_errors():
     sc, pb, fr, _ = scene_problem("c1")
     with pytest.raises(M.MisError):
-        M.Context(M.mis_default_params(flags=M.MIS_F_JOINT_POSE | M.MIS_F_LM))
+        M.Context(M.mis_default_params(flags=M.MIS_F_JOINT_POSE | M.MIS_F_AFFINE))
     with pytest.raises(M.MisError):
         M.Context(M.mis_default_params(k=8, flags=M.MIS_F_JOINT_POSE))
     with pytest.raises(M.MisError):

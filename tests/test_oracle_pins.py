@@ -1353,3 +1353,17 @@ def test_aff_warp_model_closed_forms():
     xyz, nrm, g = O.warp_model_aff(pb, At)
     assert np.abs(xyz - (pb.xyz.astype(np.float64) + [1.0, -2.0, 0.5])).max() < 1e-9
     assert np.abs(g - (pb.g.astype(np.float64) + [1.0, -2.0, 0.5])).max() < 1e-12
+
+
+def test_aff_lm_accepted_energy_decreasing_and_mu0_is_gn():
+    """The affine oracle's LM: accepted energies strictly decrease, the returned state is the last
+    accepted one; with mu0 = 0 and every trial accepted it is the affine GN."""
+    sc, pb, fr, _ = scene_problem("c1")
+    prm = O.params(gn_iters=8, solve_mode=1, lm=1, lm_mu0=1e-3)
+    At, E, na, acc = O.register_aff(prm, pb, fr, with_accepted=True)
+    ea = E[acc == 1, 5]
+    assert (np.diff(ea) < 0).all(), ea
+    assert abs(O.system_aff(prm, pb, fr, At)["energy"][5] - ea[-1]) < 1e-9 * ea[0]
+    g = O.register_aff(O.params(gn_iters=2, solve_mode=1), pb, fr)
+    l = O.register_aff(O.params(gn_iters=2, solve_mode=1, lm=1, lm_mu0=0.0), pb, fr, with_accepted=True)
+    assert (l[3] == 1).all() and np.array_equal(g[0], l[0])
