@@ -58,6 +58,8 @@ cudaError_t ensure(Ctx* c, DBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.p && b.bytes >= bytes) return cudaSuccess;
   if (b.p) {
+    static const bool dbg = getenv("MIS_DEBUG_ALLOC") != nullptr;
+    if (dbg) fprintf(stderr, "mis: realloc %zu -> %zu bytes (buffer %p)\n", b.bytes, bytes, (void*)&b);
     cudaError_t e = cudaStreamSynchronize(c->st);   // the old buffer may still be in use
     if (e != cudaSuccess) return e;
     free_buf(c, b);
@@ -856,7 +858,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   const bool aff = c->pattern_affine;   // NEXT-4
   a.affine = aff ? 1 : 0;
   if (joint) a.seg_nodes = c->seg_nodes_j.as<int32_t>();
-  TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(c->n, 1)));
+  TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(ncap(c, c->n), 1)));
   a.pstate = c->pstate.as<float4>();
   a.pstride = std::max<int64_t>(c->n, 1);
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies

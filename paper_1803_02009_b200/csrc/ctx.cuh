@@ -147,6 +147,9 @@ void count_launches(int64_t k);
 // MIS_MAX_GN floats | numeric flag | E_r, E_p (MIS_MAX_GN+1) x 2], doubles
 constexpr size_t kRepN = 5 * (MIS_MAX_GN + 1), kRepR = kRepN + 2 * (MIS_MAX_GN + 1), kRepF = kRepR + MIS_MAX_GN / 2,
                  kRepP = kRepF + 1, kRepO = kRepP + 2 * (MIS_MAX_GN + 1), kRepBytes = (kRepO + MIS_MAX_GN + 1) * 8;
+// per-point scratch is sized for the model capacity (fixed at mis_set_model), not the current size:
+// a growing sequence (fuse / filter / regenerate every frame) then allocates it once
+inline int64_t ncap(const Ctx* c, int64_t n) { return n > c->cap ? n : c->cap; }
 // unknown blocks of the current system: the m nodes, plus the pose with the joint pattern (NEXT-2)
 inline int sys_m(const Ctx* c) { return c->m + (c->pattern_joint ? 1 : 0); }
 // unknowns per node block of the current system: 6 (SE(3)), 12 (affine, NEXT-4)

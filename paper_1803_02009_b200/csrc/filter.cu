@@ -233,7 +233,7 @@ template <class F>
 cudaError_t cub_call(Ctx* c, F f) {
   size_t need = 0;
   CK(f(nullptr, need));
-  CK(ensure(c, c->cub_tmp, need + 256));
+  CK(ensure(c, c->cub_tmp, std::max(need, cub_tmp_bound(c->cap)) + 256));
   size_t have = c->cub_tmp.bytes;
   return f(c->cub_tmp.p, have);
 }
@@ -280,10 +280,10 @@ cudaError_t run_filter(Ctx* c, float grid, const int32_t* range, int sh_x, int s
   const int64_t n = c->n;
   int64_t* info = c->finfo.as<int64_t>();
   CK(cudaMemsetAsync(info, 0, 32, c->st));
-  CK(ensure(c, c->keys, n * 8)); CK(ensure(c, c->keys2, n * 8));
-  CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
-  CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
-  CK(ensure(c, c->fl_xyz, n * 12)); CK(ensure(c, c->fl_idx, n * 4));
+  CK(ensure(c, c->keys, ncap(c, n) * 8)); CK(ensure(c, c->keys2, ncap(c, n) * 8));
+  CK(ensure(c, c->vals, ncap(c, n) * 4)); CK(ensure(c, c->vals2, ncap(c, n) * 4));
+  CK(ensure(c, c->flags, ncap(c, n) * 4)); CK(ensure(c, c->scan, ncap(c, n) * 4));
+  CK(ensure(c, c->fl_xyz, ncap(c, n) * 12)); CK(ensure(c, c->fl_idx, ncap(c, n) * 4));
   const int b = (int)((n + 255) / 256);
   ModelView A = model_view(c);
   ModelView B = model_view_of(c, c->mb[1 - c->cur]);
@@ -431,11 +431,11 @@ __global__ void __launch_bounds__(256) k_node_knn(int m, int nn, const float* __
 cudaError_t run_regen_centroids(Ctx* c, float grid, const int32_t* range, int sh_x, int sh_y, int bits, int64_t* m_out) {
   const int64_t n = c->n;
   int64_t* info = c->finfo.as<int64_t>();
-  CK(ensure(c, c->keys, n * 8)); CK(ensure(c, c->keys2, n * 8));
-  CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
-  CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
-  CK(ensure(c, c->fl_xyz, n * 12));
-  CK(ensure(c, c->rg_sums, n * 32));
+  CK(ensure(c, c->keys, ncap(c, n) * 8)); CK(ensure(c, c->keys2, ncap(c, n) * 8));
+  CK(ensure(c, c->vals, ncap(c, n) * 4)); CK(ensure(c, c->vals2, ncap(c, n) * 4));
+  CK(ensure(c, c->flags, ncap(c, n) * 4)); CK(ensure(c, c->scan, ncap(c, n) * 4));
+  CK(ensure(c, c->fl_xyz, ncap(c, n) * 12));
+  CK(ensure(c, c->rg_sums, ncap(c, n) * 32));
   CK(cudaMemsetAsync(c->rg_sums.p, 0, n * 32, c->st));
   const int b = (int)((n + 255) / 256);
   ModelView A = model_view(c);

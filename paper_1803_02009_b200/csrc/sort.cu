@@ -289,23 +289,23 @@ static cudaError_t build_order_grouped(Ctx* c) {
   ModelBufs& A = c->mb[c->cur];
   ModelBufs& B = c->mb[1 - c->cur];
   int64_t slots = 1024;
-  while (slots < 2 * n) slots <<= 1;   // load factor <= 1/2 even if every point had its own tuple
+  while (slots < 2 * ncap(c, n)) slots <<= 1;   // load factor <= 1/2 even if every point had its own tuple
   if (c->gtab_slots < slots) {
     CK(ensure(c, c->gtab, (size_t)slots * 12));
     CK(cudaMemsetAsync(c->gtab.p, 0xff, (size_t)slots * 12, c->st));   // keys empty, group ids -1
     c->gtab_slots = slots;
   }
-  if (c->gcount.bytes < 64 || c->gsize_cap < n) {
-    CK(ensure(c, c->gkeys, (size_t)n * 8));
-    CK(ensure(c, c->gslot, (size_t)n * 4 + 64));
-    CK(ensure(c, c->gcount, (size_t)n * 4 + 64));   // [0]: group counter, [16..]: group sizes
-    CK(cudaMemsetAsync(c->gcount.p, 0, (size_t)n * 4 + 64, c->st));
-    c->gsize_cap = n;
+  if (c->gcount.bytes < 64 || c->gsize_cap < n) {   // (sized for the capacity: see ncap)
+    CK(ensure(c, c->gkeys, (size_t)ncap(c, n) * 8));
+    CK(ensure(c, c->gslot, (size_t)ncap(c, n) * 4 + 64));
+    CK(ensure(c, c->gcount, (size_t)ncap(c, n) * 4 + 64));   // [0]: group counter, [16..]: group sizes
+    CK(cudaMemsetAsync(c->gcount.p, 0, (size_t)ncap(c, n) * 4 + 64, c->st));
+    c->gsize_cap = ncap(c, n);
   }
-  CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4)); CK(ensure(c, c->keys, n * 8));
-  CK(ensure(c, c->seg_start, (n + 1) * 4));
-  CK(ensure(c, c->seg_nodes, (size_t)n * K * 4));
-  CK(ensure(c, c->chunks, (size_t)n * 16));
+  CK(ensure(c, c->vals, ncap(c, n) * 4)); CK(ensure(c, c->vals2, ncap(c, n) * 4)); CK(ensure(c, c->keys, ncap(c, n) * 8));
+  CK(ensure(c, c->seg_start, (ncap(c, n) + 1) * 4));
+  CK(ensure(c, c->seg_nodes, (size_t)ncap(c, n) * K * 4));
+  CK(ensure(c, c->chunks, (size_t)ncap(c, n) * 16));
   if (!c->nnz_dev.p) {
     CK(ensure(c, c->nnz_dev, 64));
     CK(cudaMemsetAsync(c->nnz_dev.p, 0, 64, c->st));
@@ -318,7 +318,7 @@ static cudaError_t build_order_grouped(Ctx* c) {
   launch_pdl(k_group_insert, dim3(b), dim3(256), 0, c->st, n, c->cap, A.kidx.as<int32_t>(), K, tkeys, tgid,
              c->gtab_slots - 1, gcount, c->gkeys.as<uint64_t>(), c->gslot.as<int32_t>(), gsize, c->vals.as<int32_t>(),
              c->vals2.as<int32_t>());
-  CK(ensure(c, c->scan, (size_t)n * 8));   // per-group (segment start, chunk start)
+  CK(ensure(c, c->scan, (size_t)ncap(c, n) * 8));   // per-group (segment start, chunk start)
   int2* pre = reinterpret_cast<int2*>(c->scan.p);
   launch_pdl(k_group_layout, dim3(1), dim3(1024), 0, c->st, n, gcount, gsize, pre, c->seg_start.as<int32_t>(),
              c->nnz_dev.as<int64_t>());
@@ -342,7 +342,7 @@ template <class F>
 static cudaError_t cub_call(Ctx* c, F f) {
   size_t need = 0;
   CK(f(nullptr, need));
-  CK(ensure(c, c->cub_tmp, need + 256));
+  CK(ensure(c, c->cub_tmp, std::max(need, cub_tmp_bound(c->cap)) + 256));
   size_t have = c->cub_tmp.bytes;
   return f(c->cub_tmp.p, have);
 }
@@ -363,8 +363,8 @@ cudaError_t build_order(Ctx* c) {
   ModelBufs& A = c->mb[c->cur];
   ModelBufs& B = c->mb[1 - c->cur];
   if (n > 0) {
-    CK(ensure(c, c->keys, n * 8)); CK(ensure(c, c->keys2, n * 8));
-    CK(ensure(c, c->vals, n * 4)); CK(ensure(c, c->vals2, n * 4));
+    CK(ensure(c, c->keys, ncap(c, n) * 8)); CK(ensure(c, c->keys2, ncap(c, n) * 8));
+    CK(ensure(c, c->vals, ncap(c, n) * 4)); CK(ensure(c, c->vals2, ncap(c, n) * 4));
     // tuples expected: the last pattern's segment count (the model changes little between
     // frames), else n / 8; key bits = log2 of that + 7, rounded up to whole 8-bit passes
     const int64_t t_est = c->nseg > 0 ? c->nseg : std::max<int64_t>(n / 8, 1);
@@ -391,11 +391,11 @@ cudaError_t build_order(Ctx* c) {
   c->nseg = -1;
   c->nchunk = -1;
   if (n > 0) {
-    CK(ensure(c, c->flags, n * 4)); CK(ensure(c, c->scan, n * 4));
-    CK(ensure(c, c->seg_start, (n + 1) * 4));
-    CK(ensure(c, c->seg_nodes, (size_t)n * K * 4));
-    CK(ensure(c, c->chunk_off, (n + 1) * 4));
-    CK(ensure(c, c->chunks, (size_t)n * 16));
+    CK(ensure(c, c->flags, ncap(c, n) * 4)); CK(ensure(c, c->scan, ncap(c, n) * 4));
+    CK(ensure(c, c->seg_start, (ncap(c, n) + 1) * 4));
+    CK(ensure(c, c->seg_nodes, (size_t)ncap(c, n) * K * 4));
+    CK(ensure(c, c->chunk_off, (ncap(c, n) + 1) * 4));
+    CK(ensure(c, c->chunks, (size_t)ncap(c, n) * 16));
     const int b = (int)((n + 255) / 256);
     launch_pdl(k_seg_flags, dim3(b), dim3(256), 0, c->st, n, c->cap, S.kidx.as<int32_t>(), K, c->flags.as<int32_t>());
     CK(cub_call(c, [&](void* t, size_t& s) {
@@ -663,7 +663,7 @@ cudaError_t build_pattern(Ctx* c) {
   const int grid = c->num_sms * 8;
   const int32_t* tup = c->seg_nodes.as<int32_t>();
   if (joint) {   // tuples + pose id, pose row of the feature ids (K = k + 1 slots from here on)
-    CK(ensure(c, c->seg_nodes_j, (size_t)std::max<int64_t>(c->n, 1) * K * 4));
+    CK(ensure(c, c->seg_nodes_j, (size_t)std::max<int64_t>(ncap(c, c->n), 1) * K * 4));
     launch_pdl(k_joint_tuples, dim3(grid), dim3(256), 0, c->st, (const int64_t*)(info + 1), c->K, tup, m,
                c->seg_nodes_j.as<int32_t>(), c->nf, c->fidx.as<int32_t>());
     count_launches(1);
