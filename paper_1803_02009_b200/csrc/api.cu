@@ -889,6 +889,8 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   }
   // K3a + K3b fused into one kernel (k <= 4 SE(3), no debug outputs; MIS_K3_SPLIT=1 in the
   // environment keeps the two-kernel path for comparison), the K4/K5 items in its extra CTAs
+  // (k > 4 fused into the FP32 register-tile SYRK spills ~1.3 KB per thread and measured slower at C5:
+  // 39.2 vs 30.1 ms per step of K3, so k > 4 keeps the two kernels)
   const bool fused = !dbg && !joint && !aff && c->K <= 4 && !c->k3_split;
   if (fused) {
     if (a.nchunk > 0 || graph_terms) {

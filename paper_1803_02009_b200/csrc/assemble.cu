@@ -322,8 +322,21 @@ __device__ __forceinline__ void build_row(const PState<K>& st, float* row) {
 // in shared memory; lanes own 4x4 tiles of the upper triangles of sum c'c'^T and
 // sum e'e'^T and accumulate them in registers (16 FFMA per 2 LDS.128); the
 // chunk's sums are committed with float4 / float2 atomic adds into its BSR slots.
-template <int K>
-__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPointsArgs a) {
+// FUSED (k > 4: C5): K3a's association computed per lane into the factor row, the chunk's node
+// states staged in shared memory (as k_accum_points_tc<K, true>); the CTAs past point_grid run the
+// K4 / K5 items.  Saves the 16 (k + 2) B per point factor-state round trip through HBM.
+__device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, double ed, double ep, int as);
+template <int K, bool FUSED = false>
+__global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPointsArgs a, AsmGraphArgs ga,
+                                                                           unsigned point_grid) {
+  if constexpr (FUSED) {
+    if (blockIdx.x >= point_grid) {
+      pdl_wait();
+      pdl_trigger();
+      graph_item(ga, (int64_t)(blockIdx.x - point_grid) * blockDim.x + threadIdx.x);
+      return;
+    }
+  }
   using L = Lay<K>;
   constexpr int P = L::P;
   constexpr int RT = 52 * P + 20 * K;   // commit record (aliases the warp's row buffer at commit)
@@ -335,6 +348,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
   float* Rec = F;
   __shared__ int32_t slot_sm[kWarps][P + K];   // the chunk's BSR slots, then its K node ids
   int32_t* slots = slot_sm[warp];
+  __shared__ double2 nrt_sm[FUSED ? kWarps : 1][6 * K];   // FUSED: the chunk's node states (R, t)
+  __shared__ float4 ng_sm[FUSED ? kWarps : 1][K];          // and positions
+  double ed = 0.0, ep = 0.0;
+  int n_as = 0;
 
   // tile table of the two upper triangles: (I, J) in units of 4 entries
   __shared__ uint8_t tabI[L::NT], tabJ[L::NT];
@@ -411,6 +428,17 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     const int32_t* nodes = a.seg_nodes + (int64_t)seg * K;
     __syncwarp();
     for (int q = lane; q < P + K; q += 32) slots[q] = q < P ? a.seg_slot[(int64_t)seg * P + q] : nodes[q - P];
+    if constexpr (FUSED) {   // stage the chunk's node states (fp64 master) and positions
+      for (int q = lane; q < 7 * K; q += 32) {
+        if (q < 6 * K) {
+          nrt_sm[warp][q] = __ldg(reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nodes[q / 6]) + q % 6);
+        } else {
+          const float* g = a.nd.g + 3 * (int64_t)nodes[q - 6 * K];
+          ng_sm[warp][q - 6 * K] = make_float4(g[0], g[1], g[2], 0.f);
+        }
+      }
+      __syncwarp();
+    }
     float acc[L::RI][16];
 #pragma unroll
     for (int r = 0; r < L::RI; ++r)
@@ -421,10 +449,17 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
       float* row = F + lane * L::FSP;
       if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point)
         PState<K> st;
+        if constexpr (FUSED) {
+          int as1 = 0;
+          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
+          n_as += as1;
+        } else {
 #pragma unroll
-        for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
-        st.rr = ps[K * S + i];
-        st.nn = ps[(K + 1) * S + i];
+          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+          st.rr = ps[K * S + i];
+          st.nn = ps[(K + 1) * S + i];
+        }
         build_row<K>(st, row);
       }
       __syncwarp();
@@ -488,6 +523,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     __syncwarp();
     c = __shfl_sync(0xffffffffu, next_chunk, 0);
   }
+  if constexpr (FUSED) commit_point_energies(a, ed, ep, n_as);
 }
 
 // ---------------------------------------------------------------- K3b on tensor cores (k <= 4)
@@ -1386,14 +1422,30 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s, 
     launch_pdl(kern, dim3((unsigned)(grid + gg)), dim3(kWarps * 32), smem, s, a, gz, (unsigned)grid);
     return;
   }
-  if (a.nchunk <= 0) return;
-  void (*kern)(AsmPointsArgs);
-  if constexpr (tcw) kern = k_accum_points_tcw<(K > 4 ? K : 5)>;
-  else kern = k_accum_points<K>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  if constexpr (tcw) {
+    if (a.nchunk <= 0) return;
+    void (*kern)(AsmPointsArgs) = k_accum_points_tcw<(K > 4 ? K : 5)>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (a.nchunk + kWarps - 1) / kWarps;
+    int64_t grid = (int64_t)num_sms * per_sm;
+    if (want < grid) grid = want;
+    if (grid < 1) grid = 1;
+    launch_pdl(kern, dim3((unsigned)grid), dim3(kWarps * 32), smem, s, a);
+    return;
+  }
+  // FP32 register-tile SYRK (k > 4), K3a fused into it when `fused`
+  auto kern = fused ? k_accum_points<K, true> : k_accum_points<K, false>;
+  static bool attr_set2[2] = {false, false};
+  if (!attr_set2[fused]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+    attr_set2[fused] = true;
   }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem);
@@ -1401,8 +1453,17 @@ static void launch_accum_k(const AsmPointsArgs& a, int num_sms, cudaStream_t s, 
   int64_t want = (a.nchunk + kWarps - 1) / kWarps;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (want < grid) grid = want;
-  if (grid < 1) grid = 1;
-  launch_pdl(kern, dim3((unsigned)grid), dim3(kWarps * 32), smem, s, a);
+  if (a.nchunk <= 0) grid = 0;
+  AsmGraphArgs gz{};
+  int64_t gg = 0;
+  if (fused && ga) {
+    gz = *ga;
+    const int PS = gz.KS * (gz.KS + 1) / 2;
+    const int64_t ng = (int64_t)gz.nd.m * gz.n_nbr * 6 + (int64_t)gz.nf * PS * 6 + (int64_t)gz.nf * gz.KS;
+    gg = (ng + kWarps * 32 - 1) / (kWarps * 32);
+  }
+  if (grid + gg == 0) return;
+  launch_pdl(kern, dim3((unsigned)(grid + gg)), dim3(kWarps * 32), smem, s, a, gz, (unsigned)grid);
 }
 
 void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s) {
