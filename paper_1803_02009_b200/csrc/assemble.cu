@@ -358,13 +358,26 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
   // per lane: record index of each of its items' 16 tile entries (-1: not part of the system)
   __shared__ int16_t dm[L::RI * 16][32];
   __shared__ uint32_t cdesc[NIT][32];   // commit items, as in k_accum_points_tc
-  for (int t = threadIdx.x; t < L::NT; t += blockDim.x) {
-    const bool e = t >= L::TD;
-    const int nb = e ? L::NE : L::ND;
-    int u = e ? t - L::TD : t, I = 0;
-    while (u >= nb - I) { u -= nb - I; ++I; }
-    tabI[t] = (uint8_t)I;
-    tabJ[t] = (uint8_t)(I + u);
+  // tiles in blocks of 4 rows x 8 columns of the tile grid (each triangle separately), so the 32
+  // lanes of one round read <= 4 distinct A and <= 8 distinct B float4 of a point's row: two
+  // shared-memory wavefronts per point and round instead of three (row-major order: up to 13 B's)
+  if (threadIdx.x == 0) {
+    int t = 0;
+#pragma unroll 1
+    for (int e = 0; e < 2; ++e) {
+      const int nb = e ? L::NE : L::ND;
+      for (int I0 = 0; I0 < nb; I0 += 4)
+        for (int J0 = I0; J0 < nb; J0 += 8)
+          for (int dI = 0; dI < 4; ++dI)
+            for (int dJ = 0; dJ < 8; ++dJ) {
+              const int I = I0 + dI, J = J0 + dJ;
+              if (I < nb && J < nb && I <= J) {
+                tabI[t] = (uint8_t)I;
+                tabJ[t] = (uint8_t)J;
+                ++t;
+              }
+            }
+    }
   }
   __syncthreads();
   for (int q = threadIdx.x; q < L::RI * 16 * 32; q += blockDim.x) {
