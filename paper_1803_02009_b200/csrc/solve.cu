@@ -336,15 +336,19 @@ __device__ void precond_block_lm(const float* Hjj, float lambda, double mu, floa
 // products n_pose are partial sums over all threads (fp64 slots per iteration), finished after
 // the barrier identically by every thread.
 // Planes of a.pv (B m floats each): 0 r, 1 u, 2 w, 3 z, 4 q, 5 s, 6 p, 7 m (even), 8 m (odd).
-template <int B>
-__global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
+// POSE: compiled with the NEXT-2 arrowhead (its ~90 registers of replicated pose state are not
+// carried by the plain kernel).  MINB: resident 256-thread CTAs per SM the registers are sized for --
+// 2 (128 registers, a few spills, twice the loads in flight) for HBM-bound systems (C5: 3.4 vs
+// 3.9 ms of PCG per step), else 1 (C4: 0.42 vs 0.51 ms)
+template <int B, bool POSE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_solve_pipe(SolveArgs a) {
   constexpr int BB = B * B, kG = 8, H2 = (B + kG - 1) / kG;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[32];
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int m = a.m;
-  const bool has_pose = B == 6 && a.pose_node >= 0;
+  constexpr bool has_pose = B == 6 && POSE;
   const int pose = has_pose ? a.pose_node : -1;
   const int64_t nrows = has_pose ? pose : m;   // block rows of the row loop
   const int64_t BM = (int64_t)B * m;
@@ -467,10 +471,53 @@ __global__ void __launch_bounds__(256) k_solve_pipe(SolveArgs a) {
 
   // block row j of (A v): the kG lanes' strided blocks, summed by shuffles (all lanes get all B);
   // the pose column from the registers pv_pose
+  auto block_fma = [&](const float4 (&hb)[BB / 4], const float (&zv)[B], float (&y)[B]) {
+#pragma unroll
+    for (int f = 0; f < BB / 4; ++f) {
+      const int i0 = (4 * f) / B, c0 = (4 * f) % B;
+      const float hv[4] = {hb[f].x, hb[f].y, hb[f].z, hb[f].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + (c0 + u) / B, c = (c0 + u) % B;
+        y[i] = fmaf(hv[u], zv[c], y[i]);
+      }
+    }
+  };
+  auto load_z = [&](const float* vsrc, const float* pv_pose, int cl, float (&zv)[B]) {
+    if (B == 6 && cl == pose) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) zv[b] = pv_pose[b % 6];
+    } else {
+      const float* zz = vsrc + B * (int64_t)cl;
+#pragma unroll
+      for (int b = 0; b < B; b += 2) {
+        const float2 t = *reinterpret_cast<const float2*>(zz + b);
+        zv[b] = t.x;
+        zv[b + 1] = t.y;
+      }
+    }
+  };
   auto row_product = [&](int64_t j, const float* vsrc, const float* pv_pose, float (&y)[B]) {
 #pragma unroll
     for (int i = 0; i < B; ++i) y[i] = 0.f;
-    for (int e = a.row_ptr[j] + lg; e < a.row_ptr[j + 1]; e += kG) {
+    int e = a.row_ptr[j] + lg;
+    const int e_end = a.row_ptr[j + 1];
+    if constexpr (B == 6) {   // two blocks per step: 18 float4 of H in flight per lane (HBM-bound sizes)
+      for (; e + kG < e_end; e += 2 * kG) {
+        const int c0 = a.col[e], c1 = a.col[e + kG];
+        float4 h0[9], h1[9];
+        const float4* H0 = reinterpret_cast<const float4*>(Hs + 36 * (int64_t)e);
+        const float4* H1 = reinterpret_cast<const float4*>(Hs + 36 * (int64_t)(e + kG));
+#pragma unroll
+        for (int f = 0; f < 9; ++f) { h0[f] = __ldg(H0 + f); h1[f] = __ldg(H1 + f); }
+        float z0[B], z1[B];
+        load_z(vsrc, pv_pose, c0, z0);
+        load_z(vsrc, pv_pose, c1, z1);
+        block_fma(h0, z0, y);
+        block_fma(h1, z1, y);
+      }
+    }
+    for (; e < e_end; e += kG) {
       const float4* H4 = reinterpret_cast<const float4*>(Hs + BB * (int64_t)e);
       const int cl = a.col[e];
       float zv[B];
@@ -710,7 +757,11 @@ cudaError_t launch_solve_grid(const SolveArgs& a, int num_sms, cudaStream_t s) {
   int per_sm = 1;
   // the pipelined recurrence (one grid barrier per iteration) unless MIS_F_STANDARD_PCG asks for
   // the textbook one (two barriers)
-  const void* kern = a.pipelined ? (a.block == 12 ? (const void*)k_solve_pipe<12> : (const void*)k_solve_pipe<6>)
+  const bool big = a.nnzb > 200000;   // H beyond ~30 MB: HBM-bound SpMV, more loads in flight pay
+  const void* kern = a.pipelined ? (a.block == 12 ? (const void*)k_solve_pipe<12, false, 1>
+                                    : a.pose_node >= 0 ? (const void*)k_solve_pipe<6, true, 1>
+                                    : big ? (const void*)k_solve_pipe<6, false, 2>
+                                          : (const void*)k_solve_pipe<6, false, 1>)
                                  : (a.block == 12 ? (const void*)k_solve<12> : (const void*)k_solve<6>);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (void (*)(SolveArgs))kern, 256, 0);
   int64_t work = (int64_t)a.block * a.m;
