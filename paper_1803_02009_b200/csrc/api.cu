@@ -864,7 +864,9 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.work_counter = reinterpret_cast<unsigned long long*>(c->energy.as<double>() + 6);   // zeroed with the energies
   a.dbg_pix = dbg ? c->pix.as<int32_t>() : nullptr;
   a.dbg_why = dbg ? c->why.as<uint8_t>() : nullptr;
-  const bool graph_terms = c->rank == 0 && (int64_t)c->m * c->prm.n_nbr + c->nf > 0;   // K4/K5 on rank 0
+  // K4/K5 (regulariser, features) on every rank: they are O(m n_nbr + n_f), identical everywhere, and
+  // stay out of the cross-rank reduction (only the point terms are summed over the shards)
+  const bool graph_terms = (int64_t)c->m * c->prm.n_nbr + c->nf > 0;
   AsmGraphArgs gA;
   {   // (filled always: the affine model's E_rot terms need it without edges or features)
     gA.nd = node_view(c);
@@ -904,7 +906,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     }
     if (aff) {   // the affine graph terms include E_rot on every node: always (rank 0)
       ProfScope ps(c, P_GRAPH, 1);
-      if (c->rank == 0) launch_assemble_graph_aff(gA, c->st);
+      launch_assemble_graph_aff(gA, c->st);
     }
     if (a.nchunk > 0) {
       ProfScope ps(c, P_ACCUM, 1);
@@ -913,13 +915,39 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     }
   }
   TRY(c, cudaGetLastError());
-  if (c->world > 1) {   // the accumulators and energies are linear in the per-rank sums: all-reduce them
-    if (nccl_allreduce_sum_f32(c, c->acc.as<float>(), c->acc_floats) != cudaSuccess) return MIS_E_NCCL;
-    if (nccl_allreduce_sum_f64(c, c->energy.as<double>(), kEnergyDoubles) != cudaSuccess) return MIS_E_NCCL;
+  // multi-GPU: the point part of H (upper 6x6 blocks) and b is formed on every rank,
+  // all-reduced (36 (m + nup) + 6 m floats) with the point energies, and scattered back as pre-weighted
+  // accumulators; the graph terms are every rank's own.  MIS_SHARD_PROTOCOL=1 runs the same kernels on
+  // one GPU (without the NCCL call), so the parity tests check the payload path.
+  static const bool shard_protocol = getenv("MIS_SHARD_PROTOCOL") != nullptr;
+  const bool sharded = (c->world > 1 || shard_protocol) && !c->pattern_affine && !c->pattern_joint &&
+                       !(c->prm.flags & MIS_F_LM);
+  if (sharded) {
+    FinalArgs rp{};
+    rp.m = sys_m(c);
+    rp.nup = (c->nnzb - sys_m(c)) / 2;
+    rp.ulist = c->ulist.as<int2>();
+    rp.diag_pos = c->diag_pos.as<int32_t>();
+    rp.w_data = c->prm.w_data;
+    rp.w_pt = c->prm.w_point;
+    rp.acc = acc;
+    const size_t nh = 36 * (size_t)(rp.m + rp.nup), nr = 6 * (size_t)rp.m;
+    TRY(c, ensure(c, c->shard_buf, (nh + nr) * 4));
+    float* HU = c->shard_buf.as<float>();
+    launch_shard_partial(rp, HU, HU + nh, c->st);
+    if (c->world > 1) {
+      if (nccl_allreduce_sum_f32(c, HU, nh + nr) != cudaSuccess) return MIS_E_NCCL;
+      double* E = c->energy.as<double>();
+      if (nccl_allreduce_sum_f64(c, E + 8, 2 * kEnergyStripes) != cudaSuccess) return MIS_E_NCCL;   // E_data, E_pt
+      if (nccl_allreduce_sum_f64(c, E + 8 + 4 * kEnergyStripes, kEnergyStripes) != cudaSuccess) return MIS_E_NCCL;
+    }
+    launch_shard_scatter(rp, HU, HU + nh, c->st);
+    count_launches(2);
   }
   {   // accumulators -> final H (both triangles), b, block-Jacobi inverses
     ProfScope ps(c, P_REDUCE, 1);
     FinalArgs r;
+    r.pre_weighted = sharded ? 1 : 0;
     r.nnzb = c->nnzb;
     r.nup = (c->nnzb - sys_m(c)) / 2;
     r.ulist = c->ulist.as<int2>();

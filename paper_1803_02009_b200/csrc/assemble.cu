@@ -1142,7 +1142,7 @@ __device__ __forceinline__ void final_block(const FinalArgs& r, const float* st,
   for (int k = 0; k < 2; ++k) {
     const int l = lane + 32 * k;
     if (l < 36) {
-      const float h = apply_recipe(rc[k], st, l, r.w_data, r.w_pt);
+      const float h = r.pre_weighted ? apply_recipe(rc[k], st, l, 1.f, 0.f) : apply_recipe(rc[k], st, l, r.w_data, r.w_pt);
       r.Hval[36 * e + l] = h;
       if (!diag) r.Hval[36 * (int64_t)lo + rc[k].tr] = h;
       if (hst) hst[l] = h;
@@ -1317,7 +1317,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs r) {
         for (int k = 0; k < 6; ++k) b += (k < 3 ? (double)r.w_r : (double)r.w_p) * pJ[6 * k + lane] * pr[k];
         prior = (float)(-b);
       }
-      r.rhs[6 * n + lane] = -r.w_data * st[lane] - r.w_pt * pt + gv[q] + prior;
+      r.rhs[6 * n + lane] = (r.pre_weighted ? -st[lane] : -r.w_data * st[lane] - r.w_pt * pt) + gv[q] + prior;
     }
     return;
   }
@@ -1360,6 +1360,98 @@ void launch_finalize(const FinalArgs& r, cudaStream_t s) {
   const int64_t warps = (int64_t)r.m + (r.nup + kFB - 1) / kFB + (r.m + kFB - 1) / kFB + 1;
   const int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 0) launch_pdl(k_finalize, dim3((unsigned)blocks), dim3(256), 0, s, r);
+}
+
+// ---- multi-GPU reduction payload: before the cross-rank sum, each rank turns its point
+// accumulators (data | mom per upper block, rhs_data | node_mom per node) into the point part of the
+// final system -- the 6x6 upper blocks (36 floats) and the 6-vector b per node -- so the all-reduce moves
+// 36 (m + nup) + 6 m floats (C5: ~39 MB per GN iteration) instead of the raw accumulators (52 floats per
+// BSR entry, both triangles).  H is linear in the accumulators, so this commutes with the sum.  After the
+// reduce k_shard_scatter puts the point part back as "data" (mom = 0, rhs_data = -b) and the regular
+// finalisation runs with w_data = 1, w_pt = 0, adding each rank's own (identical) graph terms.
+// HU: [m diagonal blocks | nup off-diagonal upper blocks in the finalisation's list order] x 36, RU: 6 m.
+__global__ void __launch_bounds__(256) k_shard_partial(FinalArgs r, float* HU, float* RU) {
+  __shared__ float stage[8][52];
+  __shared__ Recipe rtab[2][36];
+  if (threadIdx.x < 72) rtab[threadIdx.x / 36][threadIdx.x % 36] = make_recipe(threadIdx.x % 36, threadIdx.x < 36);
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nblk = r.m + r.nup;
+  float* st = stage[wib];
+  if (gw < nblk) {
+    const bool diag = gw < r.m;
+    const int64_t e = diag ? (int64_t)r.diag_pos[gw] : (int64_t)r.ulist[gw - r.m].x;
+    st[lane] = r.acc.data[36 * e + lane];
+    if (lane < 4) st[32 + lane] = r.acc.data[36 * e + 32 + lane];
+    if (lane < 16) st[36 + lane] = r.acc.mom[16 * e + lane];
+    __syncwarp();
+    float g0[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {   // the recipes read G at st[52 + l]: evaluate with G = 0 by hand
+      const int l = lane + 32 * k;
+      g0[k] = 0.f;
+      if (l < 36) {
+        const Recipe rc = rtab[diag ? 0 : 1][l];
+        const float* Mo = st + 36;
+        const float pt = rc.coef.x * Mo[rc.idx & 0xff] + rc.coef.y * Mo[(rc.idx >> 8) & 0xff] +
+                         rc.coef.z * Mo[(rc.idx >> 16) & 0xff] + rc.coef.w * Mo[rc.idx >> 24];
+        g0[k] = r.w_data * st[rc.d] + r.w_pt * pt;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int l = lane + 32 * k;
+      if (l < 36) HU[36 * gw + l] = g0[k];
+    }
+    r.acc.data[36 * e + lane] = 0.f;
+    if (lane < 4) r.acc.data[36 * e + 32 + lane] = 0.f;
+    if (lane < 16) r.acc.mom[16 * e + lane] = 0.f;
+    return;
+  }
+  const int64_t n = gw - nblk;
+  if (n < r.m && lane < 6) {   // b's point part of node n (as k_finalize, without the graph rhs)
+    const float* Nm = r.acc.node_mom + 12 * n;
+    float pt;
+    if (lane < 3) {
+      const int c1 = (lane + 1) % 3, c2 = (lane + 2) % 3;
+      pt = Nm[3 * c1 + c2] - Nm[3 * c2 + c1];
+    } else {
+      pt = Nm[9 + (lane - 3)];
+    }
+    RU[6 * n + lane] = -r.w_data * r.acc.rhs_data[6 * n + lane] - r.w_pt * pt;
+    __syncwarp(0x3fu);
+    r.acc.rhs_data[6 * n + lane] = 0.f;
+    r.acc.node_mom[12 * n + lane] = 0.f;
+    r.acc.node_mom[12 * n + 6 + lane] = 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shard_scatter(FinalArgs r, const float* HU, const float* RU) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk = r.m + r.nup;
+  if (gw < nblk) {
+    const int64_t e = gw < r.m ? (int64_t)r.diag_pos[gw] : (int64_t)r.ulist[gw - r.m].x;
+    r.acc.data[36 * e + lane] = HU[36 * gw + lane];   // mom stays zero (zeroed by k_shard_partial)
+    if (lane < 4) r.acc.data[36 * e + 32 + lane] = HU[36 * gw + 32 + lane];
+    return;
+  }
+  const int64_t n = gw - nblk;
+  if (n < r.m && lane < 6) r.acc.rhs_data[6 * n + lane] = -RU[6 * n + lane];
+}
+
+void launch_shard_partial(const FinalArgs& r, float* HU, float* RU, cudaStream_t s) {
+  const int64_t warps = (int64_t)r.m + r.nup + r.m;
+  launch_pdl(k_shard_partial, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, s, r, HU, RU);
+}
+void launch_shard_scatter(const FinalArgs& r, const float* HU, const float* RU, cudaStream_t s) {
+  const int64_t warps = (int64_t)r.m + r.nup + r.m;
+  launch_pdl(k_shard_scatter, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, s, r, HU, RU);
 }
 
 template <int K>

@@ -174,6 +174,8 @@ struct FinalArgs {
   const int32_t* lower_of;    // upper entry -> its mirror (-1 on the diagonal)
   const int32_t* diag_pos;    // m: BSR entry of each diagonal block
   float w_data, w_pt;
+  int pre_weighted;           // data holds the weighted point part of H (rhs_data: -b), mom / node_mom zero
+                              // (the multi-GPU payload, k_shard_scatter): H = data + graph, b = -rhs_data + graph
   AccView acc;                // K3 / K4 / K5 sums in
   float* Hval;                // nnzb*36 final blocks (both triangles)
   float* rhs;                 // 6m final right-hand side
@@ -194,6 +196,10 @@ struct FinalArgs {
   float *Hval_alt, *rhs_alt;
 };
 void launch_finalize(const FinalArgs& r, cudaStream_t s);
+// multi-GPU reduction payload (assemble.cu): point part of H (upper blocks) and b before the all-reduce,
+// scattered back as accumulators after it
+void launch_shard_partial(const FinalArgs& r, float* HU, float* RU, cudaStream_t s);
+void launch_shard_scatter(const FinalArgs& r, const float* HU, const float* RU, cudaStream_t s);
 // NEXT-4 (affine.cu): K3b over the 12-unknown node blocks, the graph terms (Eq. 6 with A_j, Eq. 9,
 // Eq. 4-5 E_rot) and the 12 x 12 finalisation
 void launch_accum_points_aff(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);

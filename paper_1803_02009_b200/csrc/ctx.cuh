@@ -99,6 +99,7 @@ struct Ctx {
   DBuf pstate;   // K3a -> K3b per-point factor state
   bool acc_dirty = true;   // accumulators may be nonzero (set while an assembly is in flight)
   DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots, pvec;   // pvec: grid pipelined PCG vectors
+  DBuf shard_buf;   // multi-GPU reduction payload: point part of H (upper blocks) and b
   DBuf lm, Hval2, rhs2, Rt_acc;   // Levenberg-Marquardt (MIS_F_LM): state, second system buffer, kept nodes
 
   // ---- frame

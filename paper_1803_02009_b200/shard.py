@@ -5,9 +5,9 @@ their kNN tuple) falls in its node-row range; the ranges are contiguous and
 balanced by point count, so a rank's points are spatially coherent (node ids
 follow the node grid) and the per-rank block systems overlap only on the node
 rows at range boundaries.  Each rank passes its shard to mis_set_model /
-mis_set_graph with *global* node ids; the library all-reduces H, b and the
-energies (they are linear in the per-rank sums) and adds the regulariser and
-feature terms on rank 0 only.
+mis_set_graph with *global* node ids; the library all-reduces the point-term
+accumulators and energies (they are linear in the per-rank sums); the
+regulariser and feature terms are computed by every rank alike and not reduced.
 """
 from __future__ import annotations
 
@@ -32,5 +32,7 @@ def shard_indices(knn_idx: np.ndarray, m: int, world: int, rank: int) -> np.ndar
 
 
 def graph_terms_on(rank: int) -> bool:
-    """The regulariser (Eq. 6) and feature (Eq. 9) terms are added once, on rank 0."""
+    """In a sum of per-shard systems (P15) the regulariser (Eq. 6) and feature (Eq. 9) terms count
+    once: shard 0 carries them.  (libmis itself computes them on every rank and reduces only the
+    point terms, which gives the same total.)"""
     return rank == 0

@@ -76,3 +76,20 @@ def test_virtual_shards_sum_to_full_system(S):
             val[e] = H[6 * r:6 * r + 6, 6 * col[e]:6 * col[e] + 6]
     gsum["val"] = val
     check_system(gsum, osys, m)
+
+
+def test_multi_gpu_payload_path_parity():
+    """The multi-GPU reduction path (point part of H and b formed before the cross-rank sum,
+    scattered back as pre-weighted accumulators, graph terms per rank) on one GPU:
+    MIS_SHARD_PROTOCOL=1 runs its kernels in every assembly (without the NCCL call, a sum over one
+    rank), and the system / registration parity suites must pass unchanged through it."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MIS_SHARD_PROTOCOL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "system_parity or register_parity_mirror or association_parity"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -1,7 +1,8 @@
 """World-size-2 CPU tests (gloo) of the data-parallel host logic:
-shards are disjoint and complete, and the all-reduced per-rank normal
-equations equal the full system (what the NCCL all-reduce in libmis relies on:
-H, b and E are linear in the per-rank sums; graph terms on rank 0 only)."""
+shards are disjoint and complete, and the reduction protocol libmis uses gives the
+full system: every rank assembles the point terms of its shard and the graph terms
+(regulariser, features) of the whole graph; only the point terms (H, b, E_data, E_pt,
+the association count) are all-reduced, then each rank adds its own graph terms."""
 import os
 import socket
 
@@ -41,18 +42,25 @@ def _worker(rank, world, port, q):
         dist.all_gather(bufs, pad)
         merged = np.concatenate([b.numpy()[b.numpy() >= 0] for b in bufs])
         ok_part = len(merged) == pb.xyz.shape[0] and len(np.unique(merged)) == pb.xyz.shape[0]
-        # per-rank system, graph terms only on rank 0, then all-reduce (sum)
+        # per-rank point terms (the shard, no graph terms) all-reduced; graph terms local on every rank
         Rt = random_state(m, np.random.default_rng(7), 0.01, 0.2)
         prm = O.params()
-        nbr = pb.nbr if shard.graph_terms_on(rank) else np.full_like(pb.nbr, -1)
-        feats = (pb.fsrc, pb.fdst) if shard.graph_terms_on(rank) else (None, None)
-        sub = O.Problem(pb.xyz[idx], pb.nrm[idx], pb.idx[idx], pb.w[idx], pb.g, nbr, *feats)
+        no_nbr = np.full_like(pb.nbr, -1)
+        sub = O.Problem(pb.xyz[idx], pb.nrm[idx], pb.idx[idx], pb.w[idx], pb.g, no_nbr)
         s = O.system(prm, sub, fr, Rt)
         H = torch.from_numpy(O.dense_H(s, m))
         b = torch.from_numpy(s["rhs"].copy())
-        E = torch.from_numpy(s["energy"].copy())
+        E = torch.from_numpy(s["energy"][:2].copy())   # E_data, E_pt
         for t in (H, b, E):
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        none = np.zeros(0, np.int64)
+        gsub = O.Problem(pb.xyz[none], pb.nrm[none], pb.idx[none], pb.w[none], pb.g, pb.nbr, pb.fsrc, pb.fdst)
+        gs = O.system(prm, gsub, fr, Rt)   # the graph terms, identical on every rank
+        H = H + torch.from_numpy(O.dense_H(gs, m))
+        b = b + torch.from_numpy(gs["rhs"])
+        E = torch.from_numpy(np.concatenate([E.numpy(), gs["energy"][2:4]]))
+        E = torch.cat([E, torch.tensor([prm.w_data * E[0] + prm.w_pt * E[1] + prm.w_reg * E[2] + prm.w_corr * E[3]],
+                                       dtype=E.dtype)])
         if rank == 0:
             full = O.system(prm, pb, fr, Rt)
             Hf = O.dense_H(full, m)
