@@ -457,26 +457,8 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
     for (int r = 0; r < L::RI; ++r)
 #pragma unroll
       for (int e = 0; e < 16; ++e) acc[r][e] = 0.f;
-    for (int base = ch.y; base < ch.z; base += 32) {
-      const int64_t i = base + lane;
-      float* row = F + lane * L::FSP;
-      if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point)
-        PState<K> st;
-        if constexpr (FUSED) {
-          int as1 = 0;
-          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
-          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
-          n_as += as1;
-        } else {
-#pragma unroll
-          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
-          st.rr = ps[K * S + i];
-          st.nn = ps[(K + 1) * S + i];
-        }
-        build_row<K>(st, row);
-      }
-      __syncwarp();
-      const int np = min(32, ch.z - base);
+    // the Gram sums over the rows F[0, np)
+    auto gram = [&](int np) {
 #pragma unroll
       for (int r = 0; r < L::RI; ++r) {
         if (!tV[r]) continue;
@@ -494,7 +476,57 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points(AsmPo
             for (int y = 0; y < 4; ++y) acc[r][4 * x + y] = fmaf(Av[x], Bv[y], acc[r][4 * x + y]);
         }
       }
-      __syncwarp();
+    };
+    // Only associated points enter the sums (an unassociated point's state is all zeros, its rows
+    // add nothing): their rows are compacted into F across the chunk's 32-point loads and the Gram
+    // pass runs once per 32 rows (C5: ~53% of the points are associated)
+    int fill = 0, nlive = 0;
+    for (int base = ch.y; base < ch.z || fill > 0; base += 32) {
+      const int64_t i = base + lane;
+      PState<K> st;
+      bool live = false;
+      if (i < ch.z) {
+        if constexpr (FUSED) {
+          int as1 = 0;
+          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
+          n_as += as1;
+        } else {
+#pragma unroll
+          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+          st.rr = ps[K * S + i];
+          st.nn = ps[(K + 1) * S + i];
+        }
+#pragma unroll
+        for (int s = 0; s < K; ++s) live |= st.wa[s].w != 0.f;   // sum w = 1 when associated
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+      const int slot = live ? fill + __popc(bal & ((1u << lane) - 1u)) : -1;   // compacted row
+      if (slot >= 0 && slot < 32) build_row<K>(st, F + slot * L::FSP);
+      fill += __popc(bal);
+      nlive += __popc(bal);
+      if (fill >= 32 || (base + 32 >= ch.z && fill > 0)) {   // one call site of the pass
+        const int np = min(fill, 32);
+        __syncwarp();
+        gram(np);
+        __syncwarp();
+        fill -= np;
+        if (slot >= 32) {
+          if constexpr (!FUSED) {   // reload (L1) rather than keep the state live across the pass
+            const int64_t i2 = base + lane;
+#pragma unroll
+            for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i2];
+            st.rr = ps[K * S + i2];
+            st.nn = ps[(K + 1) * S + i2];
+          }
+          build_row<K>(st, F + (slot - 32) * L::FSP);   // (an overflowing last load: one more trip)
+        }
+      }
+    }
+    if (nlive == 0) {   // no associated point in the chunk (e.g. outside the view): nothing to commit
+      if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      continue;
     }
     // ---- commit: tiles scattered into the warp's record (aliasing the row buffer; a second batch
     // half adds to the first's entries), then one aligned shared load + vector atomic per item
@@ -756,30 +788,7 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
     for (int t = 0; t < 6; ++t) dc[t][0] = dc[t][1] = dc[t][2] = dc[t][3] = 0.f;
 #pragma unroll
     for (int t = 0; t < 3; ++t) de[t][0] = de[t][1] = de[t][2] = de[t][3] = 0.f;
-    for (int base = ch.y; base < ch.z; base += 32) {
-      const int64_t i = base + lane;
-      float* row = F + lane * kTcFSP;
-      PState<K> st;
-      if (i < ch.z) {   // rebuild the factor row (zeros for an unassociated point or past the chunk)
-        if constexpr (FUSED) {
-          int as1 = 0;
-          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
-          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
-          n_as += as1;
-        } else {
-#pragma unroll
-          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
-          st.rr = ps[K * S + i];
-          st.nn = ps[(K + 1) * S + i];
-        }
-      } else {
-#pragma unroll
-        for (int s = 0; s < K; ++s) st.wa[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-        st.rr = st.nn = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      build_row_tc<K>(st, row);
-      __syncwarp();
-      const int np = min(32, ch.z - base);
+    auto gram = [&](int np) {   // rows F[0, np), np rounded up to the k-step (the rows past np are zero)
       for (int k0 = 0; k0 < np; k0 += 8) {
         FragT f;
         load_frag(F, k0, 0, g, tig, f);   // c'
@@ -794,7 +803,58 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
         mma3(de[1], f, 0, 1);
         mma3(de[2], f, 0, 2);
       }
+    };
+    // associated points' rows compacted across the chunk's loads (as in k_accum_points): the
+    // mma passes skip the unassociated points' zero rows
+    int fill = 0, nlive = 0;
+    for (int base = ch.y; base < ch.z; base += 32) {
+      const int64_t i = base + lane;
+      PState<K> st;
+      bool live = false;
+      if (i < ch.z) {
+        if constexpr (FUSED) {
+          int as1 = 0;
+          const NodesChunk nc{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+          assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nc);
+          n_as += as1;
+        } else {
+#pragma unroll
+          for (int s = 0; s < K; ++s) st.wa[s] = ps[s * S + i];
+          st.rr = ps[K * S + i];
+          st.nn = ps[(K + 1) * S + i];
+        }
+#pragma unroll
+        for (int s = 0; s < K; ++s) live |= st.wa[s].w != 0.f;   // sum w = 1 when associated
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, live);
+      const int pos = fill + __popc(bal & ((1u << lane) - 1u));
+      if (live && pos < 32) build_row_tc<K>(st, F + pos * kTcFSP);
+      fill += __popc(bal);
+      nlive += __popc(bal);
+      if (fill >= 32) {
+        __syncwarp();
+        gram(32);
+        __syncwarp();
+        fill -= 32;
+        if (live && pos >= 32) build_row_tc<K>(st, F + (pos - 32) * kTcFSP);
+      }
+    }
+    if (fill > 0) {   // zero rows up to the next k-step, then the last pass
+      const int np = (fill + 7) & ~7;
+      if (lane >= fill && lane < np) {
+        float4* z = reinterpret_cast<float4*>(F + lane * kTcFSP);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       __syncwarp();
+      gram(np);
+    }
+    __syncwarp();
+    if (nlive == 0) {   // no associated point in the chunk: nothing to commit
+      if (!MIS_K3_STATIC && lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+      c = MIS_K3_STATIC ? c + cstride : __shfl_sync(0xffffffffu, c, 0);
+      if (!MIS_K3_STATIC && c < a.nchunk) ch_next = a.chunks[c];
+      continue;
     }
     // ---- commit: fragments -> the warp's record (scattered by the per-lane map) -> atomic adds
     {
