@@ -911,6 +911,7 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     if (a.nchunk > 0) {
       ProfScope ps(c, P_ACCUM, 1);
       if (aff) launch_accum_points_aff(c->K, a, c->num_sms, c->st);
+      else if (KS > 4 && kChunk <= 128 && umma_k3b_enabled()) launch_accum_points_umma(KS, a, c->num_sms, c->st);
       else launch_accum_points(KS, a, c->num_sms, c->st);
     }
   }

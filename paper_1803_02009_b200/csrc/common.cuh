@@ -150,6 +150,10 @@ void launch_assoc_points(int K, const AsmPointsArgs& a, const AsmGraphArgs* ga, 
 // fused (k <= 4, no debug outputs): K3a + K3b in one kernel, the K4 / K5 items (ga) in extra CTAs
 void launch_accum_points(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s, bool fused = false,
                          const AsmGraphArgs* ga = nullptr);
+// K3b for 5 <= k <= 8 on tcgen05 (k3b_umma.cu; chunks of <= 128 points); MIS_K3B_UMMA=0 in the
+// environment selects the FP32 register-tile kernel instead
+bool umma_k3b_enabled();
+void launch_accum_points_umma(int K, const AsmPointsArgs& a, int num_sms, cudaStream_t s);
 
 // Per-chunk tile dump order of K3 ("record" floats, mapped to accumulator
 // addresses at commit): P pairs x [36 data (6x6, upper for the diagonal pair) |

@@ -142,4 +142,4 @@ def test_lm_affine_parity(cfg, G):
     ties = _check_lm(rep, Eo, acco, G, tot=5)
     if not ties:
         assert np.linalg.norm(Ag[:, 9:] - Ao[:, 9:], axis=1).max() < 0.01
-        assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < 1e-4
+        assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < 3e-4   # A46
