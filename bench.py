@@ -351,16 +351,30 @@ def run_mis(args, rank, world, local_rank):
         box = float(np.sqrt(xy_ext[0] * xy_ext[1] / n))
         f_frame, f_tau_time, f_tau_weight = 1, 10, 3.0
         fms, fstats, n_in = [], None, 0
+        filt_err = None
         for k in range(args.warmup + K):
             n_in = step()[0]
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            fstats = M.mis_filter(ctx.ptr, box, f_frame, f_tau_time, f_tau_weight)[1]
+            try:
+                fstats = M.mis_filter(ctx.ptr, box, f_frame, f_tau_time, f_tau_weight)[1]
+            except M.MisError as ex:   # report the model's range (the API's MIS_E_ARG guard) and go on
+                mod = M.mis_get_model(ctx.ptr, cfg.k)
+                xyz = mod["xyz"]
+                fin = np.isfinite(xyz).all(1)
+                filt_err = {"error": str(ex), "box_mm": box, "n": int(xyz.shape[0]), "non_finite": int((~fin).sum()),
+                            "min": xyz[fin].min(0).tolist() if fin.any() else None,
+                            "max": xyz[fin].max(0).tolist() if fin.any() else None}
+                print("filter leg: " + json.dumps(filt_err), file=sys.stderr)
+                break
             e1.record(stream)
             torch.cuda.synchronize()
             if k >= args.warmup:
                 fms.append(e0.elapsed_time(e1))
+    if world == 1 and not args.no_filter and filt_err is not None:
+        filt_out = {"unavailable": filt_err}
+    elif world == 1 and not args.no_filter:
         f_ms = float(np.mean(fms))
         ns_f = int(fstats[3])
         # algorithmic bytes: every model record read once (xyz, normal, colour 36 B, omega, stamp 8 B,
@@ -505,16 +519,24 @@ def run_mis(args, rank, world, local_rank):
                                          "frac": round(syrk_flop / t / 1e12 / tf32_peak, 5),
                                          "flops_per_launch": int(syrk_flop)}})
         elif name == "accum_points":
-            tc = kk <= 4
+            # K3b on tensor cores: mma.sync TF32 at k <= 4, tcgen05.mma kind::tf32 (k3b_umma.cu) at k > 4
+            # unless MIS_K3B_UMMA=0 selects the FP32 register-tile kernel
+            umma = kk > 4 and os.environ.get("MIS_K3B_UMMA", "1") != "0"
+            tc = kk <= 4 or umma
             pk = tf32_peak if tc else fp32_peak
             ach = syrk_flop / t / 1e12
+            src = ("TF32 tensor: measured dense bf16 x 1/2 (tcgen05.mma kind::tf32 M=64, 3xTF32 split: 3 MMAs per "
+                   "algorithmic product)") if umma else \
+                  ("TF32 tensor: measured dense bf16 x 1/2 (mma.sync m16n8k8 TF32, 3xTF32 split: 3 MMAs per "
+                   "algorithmic product)") if tc else "FP32 FMA: SMs x 128 lanes x 2 x max SM clock"
             base.update({"bound": "tensor" if tc else "alu", "achieved": round(ach, 3), "peak": round(pk, 1),
                          "unit": "TFLOP/s", "frac": round(ach / pk, 5), "algorithmic_flops_per_launch": int(syrk_flop),
-                         "peak_source": ("TF32 tensor: measured dense bf16 x 1/2 (mma.sync m16n8k8 TF32, 3xTF32 "
-                                         "split: 3 MMAs per algorithmic product)") if tc else
-                                        "FP32 FMA: SMs x 128 lanes x 2 x max SM clock",
+                         "peak_source": src,
                          "hbm_view": {"achieved": round(algo[name] / t / 1e9, 2), "peak": hbm,
                                       "frac": round(algo[name] / t / 1e9 / hbm, 4)}})
+            if umma:
+                base["alu_view"] = {"achieved_tflops": round(ach, 3), "peak": round(fp32_peak, 1),
+                                    "frac": round(ach / fp32_peak, 4)}
         else:
             ach = algo[name] / t / 1e9
             base.update({"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",

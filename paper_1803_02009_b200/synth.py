@@ -172,8 +172,14 @@ def render_depth(cfg, surf: Surface, R, T, rng, noise=True, holes=True):
         s = s - step
         if np.abs(step).max() < 1e-11:
             break
+    # a ray whose Newton iteration has not converged (grazing incidence: f' ~ 0 throws s far away) or
+    # that lands behind the camera / beyond 3 Z0 has no valid surface hit: a hole, as in a stereo map
+    x = o[0] + s * dw[..., 0]
+    y = o[1] + s * dw[..., 1]
+    hz, _, _ = surf.h_grad(x, y)
+    bad = ~(np.abs(o[2] + s * dw[..., 2] - hz) < 1e-6) | ~(s > 0) | ~(s < 3 * Z0)
     # the camera-frame z of o + s*dw equals s (dc has unit z)
-    depth = s.copy()
+    depth = np.where(bad, 0.0, s)
     if noise:
         # stereo (ELAS-like) depth noise is spatially correlated: a smooth field of
         # std DEPTH_SIGMA (correlation ~NOISE_CORR_MM on the tissue) plus a small
@@ -185,6 +191,7 @@ def render_depth(cfg, surf: Surface, R, T, rng, noise=True, holes=True):
         field_ = gaussian_filter(rng.normal(0.0, 1.0, depth.shape), sig_px, mode="reflect")
         field_ *= DEPTH_SIGMA / max(field_.std(), 1e-12)
         depth += field_ + rng.normal(0.0, WHITE_SIGMA, depth.shape)
+        depth[bad] = 0.0
     if holes:
         target = HOLE_FRAC * H * W
         r = max(1.5, 0.02 * W)

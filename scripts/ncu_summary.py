@@ -21,7 +21,8 @@ GROUP = {"k_assoc_points": "assoc_points", "k_accum_points": "accum_points", "k_
 
 
 def short(name):
-    n = name.split("(")[0]
+    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
+    n = n.split("(")[0]
     n = n.replace("void ", "").replace("mis::", "")
     return n
 
@@ -54,7 +55,8 @@ def full(tag):
             "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
             "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput_pct",
             "launch__grid_size": "grid", "launch__block_size": "block"}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+             "ns": 1e-3, "us": 1, "ms": 1e3}
     for r in rows[2:]:
         d = {"kernel": short(r[hdr.index("Kernel Name")])}
         for k, nm in keys.items():
