@@ -172,6 +172,37 @@ def test_system_parity_k8_point_weight(w_pt):
     check_system(gs, osys, m)
 
 
+@pytest.mark.parametrize("k", [5, 6, 7])
+def test_system_parity_k5_to_k7(k):
+    """Every k > 4 instantiation of the tcgen05 K3b (k3b_umma.cu; the k = 8 one runs above and at C5):
+    the system of a random node state within the J^T J gate."""
+    sc, pb, fr, _ = scene_problem("c2", k=k)
+    ctx = make_ctx(sc, pb, n_nbr=pb.n_nbr)
+    Rt = state_f32(node_state("random", pb.g, seed=7 + k))
+    M.mis_dbg_set_nodes(ctx.ptr, Rt.astype(np.float32))
+    m = pb.g.shape[0]
+    gs = M.mis_dbg_system(ctx.ptr, m)
+    prm = oracle_params(ctx.params)
+    osys = O.system(prm, pb, fr, Rt)
+    osys["prm"] = prm
+    check_system(gs, osys, m)
+
+
+def test_k_gt4_fp32_k3b_path():
+    """The FP32 register-tile K3b (MIS_K3B_UMMA=0, the alternative to the tcgen05 kernel for k > 4)
+    through the same k > 4 system and registration gates, in a subprocess (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MIS_K3B_UMMA="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "k8_point_weight or k5_to_k7 or c5_shape"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 # ------------------------------------------------------------------ full registration (MIRROR)
 def rot_err(Ra, Rb):
     c = np.clip((np.trace(Ra @ Rb.T) - 1) / 2, -1, 1)
