@@ -857,6 +857,13 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
   a.pose_cur = joint ? c->posebuf.as<double>() : nullptr;
   const bool aff = c->pattern_affine;   // NEXT-4
   a.affine = aff ? 1 : 0;
+  // the tcgen05 K3b (k > 4) reads the factor state of associated points only (MIS_K3B_SPARSE=0 writes
+  // every point's planes, for comparison)
+  static const bool sparse_env = [] {
+    const char* e = getenv("MIS_K3B_SPARSE");
+    return e ? atoi(e) != 0 : true;
+  }();
+  a.sparse_state = (KS > 4 && !aff && kChunk <= 128 && umma_k3b_enabled() && sparse_env) ? 1 : 0;
   if (joint) a.seg_nodes = c->seg_nodes_j.as<int32_t>();
   TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(ncap(c, c->n), 1)));
   a.pstate = c->pstate.as<float4>();

@@ -264,7 +264,10 @@ __device__ __forceinline__ void commit_point_energies(const AsmPointsArgs& a, do
 __device__ __forceinline__ void graph_item(const AsmGraphArgs& a, int64_t tid);
 
 // K3a; the blocks after the points' run the K4/K5 items (independent of K3a, same launch)
-template <int K, bool DBG, bool JOINT, bool AFF = false>
+// SP (sparse state, read by the tcgen05 K3b only): plane K + 1 = (n', associated ? 1 : 0) for every point,
+// the other planes only for associated points (~47 % of the points at C5 are not: their planes are
+// never read -- K3b builds rows for associated points only)
+template <int K, bool DBG, bool JOINT, bool AFF = false, bool SP = false>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_blocks) {
   pdl_wait();   // node states from the previous solve
@@ -282,10 +285,12 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_points(AsmPointsArg
     assoc_point<K, DBG, JOINT, AFF>(a, i, st, ed, ep, as);
     float4* ps = a.pstate;
     const int64_t S = a.pstride;
+    if (!SP || as) {
 #pragma unroll
-    for (int s = 0; s < KS; ++s) ps[s * S + i] = st.wa[s];
-    ps[KS * S + i] = st.rr;
-    ps[(KS + 1) * S + i] = st.nn;
+      for (int s = 0; s < KS; ++s) ps[s * S + i] = st.wa[s];
+      ps[KS * S + i] = st.rr;
+    }
+    ps[(KS + 1) * S + i] = SP ? make_float4(st.nn.x, st.nn.y, st.nn.z, as ? 1.f : 0.f) : st.nn;
   }
   commit_point_energies(a, ed, ep, as);
 }
@@ -1538,8 +1543,20 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
   }
   if constexpr (K < MIS_MAX_K) {
     if (joint) {
+      if (a.sparse_state) {   // the joint slots K + 1 >= 5 run through the tcgen05 K3b
+        if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, true, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+        else launch_pdl(k_assoc_points<K, false, true, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+        return;
+      }
       if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
       else launch_pdl(k_assoc_points<K, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+      return;
+    }
+  }
+  if constexpr (K > 4) {
+    if (a.sparse_state) {
+      if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
+      else launch_pdl(k_assoc_points<K, false, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
       return;
     }
   }

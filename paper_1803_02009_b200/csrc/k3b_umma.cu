@@ -377,8 +377,12 @@ __global__ void __launch_bounds__(320, 2) k_accum_points_umma(AsmPointsArgs a) {
       const float4* sg = reinterpret_cast<const float4*>(sm + U::O_STG + st * U::STG);
       bool live = false;
       if (bt < n) {
+        if (a.sparse_state) {   // plane K + 1 = (n', associated); the other planes are stale when not
+          live = reinterpret_cast<const float*>(sg + (K + 1) * 128 + bt)[3] != 0.f;
+        } else {
 #pragma unroll
-        for (int q = 0; q < K; ++q) live |= reinterpret_cast<const float*>(sg + q * 128 + bt)[3] != 0.f;   // w_q
+          for (int q = 0; q < K; ++q) live |= reinterpret_cast<const float*>(sg + q * 128 + bt)[3] != 0.f;   // w_q
+        }
       }
       const unsigned bal = __ballot_sync(0xffffffffu, live);
       if (lane == 0) wcnt[warp] = __popc(bal);
