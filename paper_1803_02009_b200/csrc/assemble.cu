@@ -731,8 +731,10 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
   }
   __syncthreads();
   // this lane's 36 fragment positions -> record indices, packed in pairs (0xffff: dropped)
-  uint32_t dmap[18];
-  {
+  // (in shared memory, the same for every warp, read once per chunk at the commit: 18 registers fewer
+  // live across the chunk loop, whose spills sat on the per-chunk path)
+  __shared__ uint32_t dmap_sm[18][32];
+  if (warp == 0) {
     const int tmi[6] = {0, 0, 0, 0, 1, 1}, tni[6] = {0, 1, 2, 3, 2, 3};
     const int emi[3] = {0, 0, 0}, eni[3] = {0, 1, 2};
 #pragma unroll
@@ -745,10 +747,11 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
         const int rr = r0 + 8 * (h >> 1), cc = c0 + (h & 1);
         d4[h] = e ? (rr < 24 ? inv[1024 + rr * 24 + cc] : -1) : inv[rr * 32 + cc];
       }
-      dmap[2 * t] = (uint32_t)(d4[0] & 0xffff) | ((uint32_t)(d4[1] & 0xffff) << 16);
-      dmap[2 * t + 1] = (uint32_t)(d4[2] & 0xffff) | ((uint32_t)(d4[3] & 0xffff) << 16);
+      dmap_sm[2 * t][lane] = (uint32_t)(d4[0] & 0xffff) | ((uint32_t)(d4[1] & 0xffff) << 16);
+      dmap_sm[2 * t + 1][lane] = (uint32_t)(d4[2] & 0xffff) | ((uint32_t)(d4[3] & 0xffff) << 16);
     }
   }
+  __syncthreads();
 
   pdl_wait();   // K3a's factor state (the tables above are independent of it)
   pdl_trigger();   // the finalisation may launch early (it waits for this grid's completion)
@@ -870,13 +873,13 @@ __global__ void __launch_bounds__(kWarps * 32, MIS_K3_MINB) k_accum_points_tc(As
       };
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        put(dmap[2 * t], dc[t][0], dc[t][1]);
-        put(dmap[2 * t + 1], dc[t][2], dc[t][3]);
+        put(dmap_sm[2 * t][lane], dc[t][0], dc[t][1]);
+        put(dmap_sm[2 * t + 1][lane], dc[t][2], dc[t][3]);
       }
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
-        put(dmap[12 + 2 * t], de[t][0], de[t][1]);
-        put(dmap[12 + 2 * t + 1], de[t][2], de[t][3]);
+        put(dmap_sm[12 + 2 * t][lane], de[t][0], de[t][1]);
+        put(dmap_sm[12 + 2 * t + 1][lane], de[t][2], de[t][3]);
       }
     }
     __syncwarp();
