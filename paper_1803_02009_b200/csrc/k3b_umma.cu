@@ -16,9 +16,10 @@
 //   warp 8  (issuer):  per chunk, TMA bulk copies (cp.async.bulk, mbarrier tx counts) of its K + 2
 //                      factor-state planes and of 16-byte-aligned windows around its BSR slots and
 //                      node ids into a 2-stage shared staging ring
-//   warps 0-3 (build): compact the chunk's associated points (an unassociated point's state is all
-//                      zeros), then write their hi / lo factor rows (lane = row, warp = every 4th
-//                      feature group) into one of two 32-row operand buffers, UMMA K-major layout
+//   warps 0-3 (build): compact the chunk's associated points (K3a's (n', associated) plane; K3a
+//                      writes the other planes of associated points only), then write their hi / lo
+//                      factor rows (lane = row, warp = every 4th feature group) into one of two
+//                      32-row operand buffers, UMMA K-major layout
 //   warp 9  (MMA):     one thread issues a round's tcgen05.mma into one of two TMEM stages (128
 //                      columns each); tcgen05.commit frees the operand buffer and, at the chunk's
 //                      last round, signals the epilogue
