@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "solve_common.cuh"
 
@@ -1522,6 +1523,67 @@ void launch_shard_scatter(const FinalArgs& r, const float* HU, const float* RU, 
   launch_pdl(k_shard_scatter, dim3((unsigned)((warps * 32 + 255) / 256)), dim3(256), 0, s, r, HU, RU);
 }
 
+// K3a by chunk (k > 4 with the tcgen05 K3b; MIS_K3A_CHUNKED=0 selects the per-point K3a): one warp per
+// chunk (dynamic schedule), the chunk's k fp64 node states staged in shared memory once (as the fused
+// k <= 4 kernel), so a point reads neither its k node ids nor 6k node-state vectors from memory; the
+// sparse state out.  C5: 8.8 -> 6.6 ms per step.
+template <int K>
+__global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArgs a, AsmGraphArgs ga,
+                                                                   unsigned point_grid) {
+  if (blockIdx.x >= point_grid) {
+    pdl_wait();
+    pdl_trigger();
+    graph_item(ga, (int64_t)(blockIdx.x - point_grid) * blockDim.x + threadIdx.x);
+    return;
+  }
+  __shared__ double2 nrt_sm[kWarps][6 * K];
+  __shared__ float4 ng_sm[kWarps][K];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
+  double ed = 0.0, ep = 0.0;
+  int n_as = 0;
+  float4* ps = a.pstate;
+  const int64_t S = a.pstride;
+  int64_t c = 0;
+  if (lane == 0) c = (int64_t)atomicAdd(a.work_counter, 1ull);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  while (c < a.nchunk) {
+    const int4 ch = a.chunks[c];
+    const int32_t* nodes = a.seg_nodes + (int64_t)ch.x * K;
+    __syncwarp();
+    for (int q = lane; q < 7 * K; q += 32) {
+      if (q < 6 * K) {
+        nrt_sm[warp][q] = __ldg(reinterpret_cast<const double2*>(a.nd.Rt64 + 12 * (int64_t)nodes[q / 6]) + q % 6);
+      } else {
+        const float* g = a.nd.g + 3 * (int64_t)nodes[q - 6 * K];
+        ng_sm[warp][q - 6 * K] = make_float4(g[0], g[1], g[2], 0.f);
+      }
+    }
+    int64_t nc = 0;
+    if (lane == 0) nc = (int64_t)atomicAdd(a.work_counter, 1ull);   // the next chunk id in flight
+    __syncwarp();
+    const NodesChunk nch{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+    for (int base = ch.y; base < ch.z; base += 32) {
+      const int64_t i = base + lane;
+      if (i < ch.z) {
+        PState<K> st;
+        int as1 = 0;
+        assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nch);
+        n_as += as1;
+        if (as1) {
+#pragma unroll
+          for (int q = 0; q < K; ++q) ps[q * S + i] = st.wa[q];
+          ps[K * S + i] = st.rr;
+        }
+        ps[(K + 1) * S + i] = make_float4(st.nn.x, st.nn.y, st.nn.z, as1 ? 1.f : 0.f);
+      }
+    }
+    c = __shfl_sync(0xffffffffu, nc, 0);
+  }
+  commit_point_energies(a, ed, ep, n_as);
+}
+
 template <int K>
 static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaStream_t s) {
   const int64_t n = a.md.n;
@@ -1557,6 +1619,18 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
     }
   }
   if constexpr (K > 4) {
+    static const bool chunked = [] {
+      const char* e = getenv("MIS_K3A_CHUNKED");
+      return e ? atoi(e) != 0 : true;
+    }();
+    if (a.sparse_state && chunked && a.dbg_pix == nullptr && !joint && a.nchunk > 0) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const unsigned pg = (unsigned)std::min<int64_t>((a.nchunk + kWarps - 1) / kWarps, 2 * (int64_t)sms);
+      launch_pdl(k_assoc_chunks<K>, dim3(pg + gg), dim3(256), 0, s, a, gz, pg);
+      return;
+    }
     if (a.sparse_state) {
       if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
       else launch_pdl(k_assoc_points<K, false, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
