@@ -1527,9 +1527,10 @@ void launch_shard_scatter(const FinalArgs& r, const float* HU, const float* RU, 
 // chunk (dynamic schedule), the chunk's k fp64 node states staged in shared memory once (as the fused
 // k <= 4 kernel), so a point reads neither its k node ids nor 6k node-state vectors from memory; the
 // sparse state out.  C5: 8.8 -> 6.6 ms per step.
-template <int K>
+template <int K, bool JOINT = false>
 __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArgs a, AsmGraphArgs ga,
                                                                    unsigned point_grid) {
+  constexpr int KS = K + (JOINT ? 1 : 0);   // NEXT-2: the pose as the last factor slot (not staged)
   if (blockIdx.x >= point_grid) {
     pdl_wait();
     pdl_trigger();
@@ -1550,7 +1551,7 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArg
   c = __shfl_sync(0xffffffffu, c, 0);
   while (c < a.nchunk) {
     const int4 ch = a.chunks[c];
-    const int32_t* nodes = a.seg_nodes + (int64_t)ch.x * K;
+    const int32_t* nodes = a.seg_nodes + (int64_t)ch.x * KS;
     __syncwarp();
     for (int q = lane; q < 7 * K; q += 32) {
       if (q < 6 * K) {
@@ -1567,16 +1568,16 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArg
     for (int base = ch.y; base < ch.z; base += 32) {
       const int64_t i = base + lane;
       if (i < ch.z) {
-        PState<K> st;
+        PState<KS> st;
         int as1 = 0;
-        assoc_point<K, false, false, false, NodesChunk>(a, i, st, ed, ep, as1, nch);
+        assoc_point<K, false, JOINT, false, NodesChunk>(a, i, st, ed, ep, as1, nch);
         n_as += as1;
         if (as1) {
 #pragma unroll
-          for (int q = 0; q < K; ++q) ps[q * S + i] = st.wa[q];
-          ps[K * S + i] = st.rr;
+          for (int q = 0; q < KS; ++q) ps[q * S + i] = st.wa[q];
+          ps[KS * S + i] = st.rr;
         }
-        ps[(K + 1) * S + i] = make_float4(st.nn.x, st.nn.y, st.nn.z, as1 ? 1.f : 0.f);
+        ps[(KS + 1) * S + i] = make_float4(st.nn.x, st.nn.y, st.nn.z, as1 ? 1.f : 0.f);
       }
     }
     c = __shfl_sync(0xffffffffu, nc, 0);
@@ -1606,6 +1607,23 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
       return;
     }
   }
+  static const bool chunked = [] {
+    const char* e = getenv("MIS_K3A_CHUNKED");
+    return e ? atoi(e) != 0 : true;
+  }();
+  // k > 4 (or the joint pose's k + 1 > 4 slots) with the tcgen05 K3b: K3a by chunk
+  if (a.sparse_state && chunked && a.dbg_pix == nullptr && a.nchunk > 0 && (joint ? K < MIS_MAX_K : K > 4)) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned pg = (unsigned)std::min<int64_t>((a.nchunk + kWarps - 1) / kWarps, 2 * (int64_t)sms);
+    if (joint) {
+      if constexpr (K < MIS_MAX_K) launch_pdl(k_assoc_chunks<K, true>, dim3(pg + gg), dim3(256), 0, s, a, gz, pg);
+    } else {
+      if constexpr (K > 4) launch_pdl(k_assoc_chunks<K, false>, dim3(pg + gg), dim3(256), 0, s, a, gz, pg);
+    }
+    return;
+  }
   if constexpr (K < MIS_MAX_K) {
     if (joint) {
       if (a.sparse_state) {   // the joint slots K + 1 >= 5 run through the tcgen05 K3b
@@ -1619,18 +1637,6 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
     }
   }
   if constexpr (K > 4) {
-    static const bool chunked = [] {
-      const char* e = getenv("MIS_K3A_CHUNKED");
-      return e ? atoi(e) != 0 : true;
-    }();
-    if (a.sparse_state && chunked && a.dbg_pix == nullptr && !joint && a.nchunk > 0) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const unsigned pg = (unsigned)std::min<int64_t>((a.nchunk + kWarps - 1) / kWarps, 2 * (int64_t)sms);
-      launch_pdl(k_assoc_chunks<K>, dim3(pg + gg), dim3(256), 0, s, a, gz, pg);
-      return;
-    }
     if (a.sparse_state) {
       if (a.dbg_pix != nullptr) launch_pdl(k_assoc_points<K, true, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
       else launch_pdl(k_assoc_points<K, false, false, false, true>, dim3(g + gg), dim3(256), 0, s, a, gz, g);
