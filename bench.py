@@ -298,9 +298,14 @@ def run_mis(args, rank, world, local_rank):
         return v_ms, rv, pose_v
 
     def variant_or_reason(flag):
+        # the API's own limits first (mis.h: the joint pose needs k <= 7, affine nodes k <= 4)
+        if flag == M.MIS_F_JOINT_POSE and cfg.k > 7:
+            return None, f"MIS_F_JOINT_POSE needs k <= 7 (k + 1 factor slots <= 8); this config has k = {cfg.k}", None
+        if flag == M.MIS_F_AFFINE and cfg.k > 4:
+            return None, f"MIS_F_AFFINE needs k <= 4; this config has k = {cfg.k}", None
         try:
             return variant_leg(flag)
-        except M.MisError as e:   # e.g. LM needs the cluster-resident PCG (C1-C3 sizes)
+        except M.MisError as e:
             return None, str(e), None
 
     lm_out = None
@@ -330,11 +335,11 @@ def run_mis(args, rank, world, local_rank):
                      "E_r_E_p_last": [float(x) for x in rj["energy_pose"][cfg.gn_iters - 1]],
                      "pose_change_mm": float(np.linalg.norm(pose_j[9:] - p0[9:]))}
     affine_out = None
-    if world == 1 and not args.no_lm and cfg.k <= 4:
+    if world == 1 and not args.no_lm:
         af_ms, ra, _ = variant_or_reason(M.MIS_F_AFFINE)
-    if world == 1 and not args.no_lm and cfg.k <= 4 and af_ms is None:
+    if world == 1 and not args.no_lm and af_ms is None:
         affine_out = {"unavailable": ra}
-    elif world == 1 and not args.no_lm and cfg.k <= 4:
+    elif world == 1 and not args.no_lm:
         affine_out = {"ms_per_step": round(af_ms, 4), "value": round(1e3 / af_ms, 3), "unit": UNIT,
                       "what": "same step with affine nodes A_j + E_rot (MIS_F_AFFINE, NEXT-4: 12 x 12 node blocks, "
                               "w_rot = 1000, grid-wide PCG)",

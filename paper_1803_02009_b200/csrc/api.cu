@@ -864,6 +864,16 @@ static mis_status assemble(Ctx* c, bool dbg, int slot) {
     return e ? atoi(e) != 0 : true;
   }();
   a.sparse_state = (KS > 4 && !aff && kChunk <= 128 && umma_k3b_enabled() && sparse_env) ? 1 : 0;
+  // K3a by chunk (MIS_K3A_CHUNKED=0: per point) for the tcgen05 K3b's k > 4 (joint: k + 1 > 4) slots
+  static const bool chunked_env = [] {
+    const char* e = getenv("MIS_K3A_CHUNKED");
+    return e ? atoi(e) != 0 : true;
+  }();
+  a.chunk_live = nullptr;
+  if (a.sparse_state && chunked_env && !dbg && c->nchunk > 0 && (joint ? c->K < MIS_MAX_K : c->K > 4)) {
+    TRY(c, ensure(c, c->chunk_live, (size_t)c->nchunk * 4));
+    a.chunk_live = c->chunk_live.as<int32_t>();
+  }
   if (joint) a.seg_nodes = c->seg_nodes_j.as<int32_t>();
   TRY(c, ensure(c, c->pstate, (size_t)(KS + 2) * 16 * (size_t)std::max<int64_t>(ncap(c, c->n), 1)));
   a.pstate = c->pstate.as<float4>();

@@ -1565,6 +1565,7 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArg
     if (lane == 0) nc = (int64_t)atomicAdd(a.work_counter, 1ull);   // the next chunk id in flight
     __syncwarp();
     const NodesChunk nch{nrt_sm[warp], reinterpret_cast<const float*>(ng_sm[warp])};
+    int anylive = 0;
     for (int base = ch.y; base < ch.z; base += 32) {
       const int64_t i = base + lane;
       if (i < ch.z) {
@@ -1578,8 +1579,11 @@ __global__ void __launch_bounds__(256, MIS_K3A_MINB) k_assoc_chunks(AsmPointsArg
           ps[KS * S + i] = st.rr;
         }
         ps[(KS + 1) * S + i] = make_float4(st.nn.x, st.nn.y, st.nn.z, as1 ? 1.f : 0.f);
+        anylive |= as1;
       }
     }
+    anylive = __any_sync(0xffffffffu, anylive);
+    if (lane == 0) a.chunk_live[c] = anylive;
     c = __shfl_sync(0xffffffffu, nc, 0);
   }
   commit_point_energies(a, ed, ep, n_as);
@@ -1607,12 +1611,8 @@ static void launch_assoc_k(const AsmPointsArgs& a, const AsmGraphArgs* ga, cudaS
       return;
     }
   }
-  static const bool chunked = [] {
-    const char* e = getenv("MIS_K3A_CHUNKED");
-    return e ? atoi(e) != 0 : true;
-  }();
-  // k > 4 (or the joint pose's k + 1 > 4 slots) with the tcgen05 K3b: K3a by chunk
-  if (a.sparse_state && chunked && a.dbg_pix == nullptr && a.nchunk > 0 && (joint ? K < MIS_MAX_K : K > 4)) {
+  // k > 4 (or the joint pose's k + 1 > 4 slots) with the tcgen05 K3b: K3a by chunk (api.cu decides)
+  if (a.chunk_live != nullptr) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

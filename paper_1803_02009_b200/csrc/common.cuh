@@ -140,6 +140,8 @@ struct AsmPointsArgs {
   // pose as one more factor slot (x_hat, 1) after the K node slots; K3b then runs with K + 1 slots
   // whose last node id is m (seg_nodes / seg_slot of the joint pattern).  null: fixed pose
   const double* pose_cur;
+  int32_t* chunk_live;        // non-null: K3a runs by chunk and flags the chunks with an associated point
+                              // (the tcgen05 K3b skips the others: no staging, no commit)
   int sparse_state;           // the tcgen05 K3b consumes the factor state: K3a writes the (n', associated)
                               // plane for every point and the other K + 1 planes only for associated points
   int affine;                 // NEXT-4 (MIS_F_AFFINE): the node matrices are general A_j; K3a writes

@@ -97,6 +97,7 @@ struct Ctx {
   DBuf pcg_pptr, pcg_pc, pcg_push, pcg_npush, pcg_mask;   // cluster PCG lists (per frame)
   size_t acc_floats = 0;
   DBuf pstate;   // K3a -> K3b per-point factor state
+  DBuf chunk_live;   // per chunk: any point associated (K3a by chunk -> the tcgen05 K3b skips the rest)
   bool acc_dirty = true;   // accumulators may be nonzero (set while an assembly is in flight)
   DBuf acc, energy, Hval, rhs, Minv, x, r, z, p, Ap, dots, pvec;   // pvec: grid pipelined PCG vectors
   DBuf shard_buf;   // multi-GPU reduction payload: point part of H (upper blocks) and b

@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(320, 2) k_accum_points_umma(AsmPointsArgs a) {
       const bool valid = j0 + lane < J && cl < a.nchunk;
       int4 h = make_int4(0, 0, 0, 0);
       if (valid) h = a.chunks[cl];
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      // chunks without an associated point (K3a by chunk flags them) add nothing: never staged
+      const bool live = valid && (a.chunk_live == nullptr || a.chunk_live[cl] != 0);
+      const unsigned vmask = __ballot_sync(0xffffffffu, live);
       for (int k = 0; k < 32; ++k) {
         if (!((vmask >> k) & 1u)) continue;
         const int seg = __shfl_sync(0xffffffffu, h.x, k);

@@ -15,7 +15,7 @@ import os
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-GROUP = {"k_assoc_points": "assoc_points", "k_accum_points": "accum_points", "k_pcg_cluster": "solve", "k_solve": "solve",
+GROUP = {"k_assoc_points": "assoc_points", "k_assoc_chunks": "assoc_points", "k_accum_points": "accum_points", "k_pcg_cluster": "solve", "k_solve": "solve",
          "k_finalize": "finalize", "k_assemble_graph": "assemble_graph", "k_frame_prep": "frame_prep",
          "k_warp_model": "warp_model", "k_fuse_register": "fuse_register", "k_fuse_apply": "fuse_apply"}
 
