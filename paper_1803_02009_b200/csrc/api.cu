@@ -270,13 +270,20 @@ __global__ void k_copy2(int64_t n, const float* a, const float* b, float* a_out,
 }
 
 // mis_set_graph's inputs in one pass: node positions copied, neighbour lists copied and
-// validated (an invalid entry is flagged and neutralised so later kernels stay in bounds)
+// validated (an invalid entry is flagged and neutralised so later kernels stay in bounds), and the
+// node states initialised to the identity (from the source positions; one launch, not two)
 __global__ void k_graph_in(int m, int n_nbr, const float* g_src, const int32_t* nbr_src, float* g, int32_t* nbr,
-                           int* flag) {
+                           int* flag, double* Rt64, float* node32) {
   pdl_wait();   // programmatic dependent launch (common.cuh)
   pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < 3 * m) g[t] = g_src[t];
+  if (t < m) {
+    for (int i = 0; i < 12; ++i) Rt64[12 * t + i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
+    for (int i = 0; i < 12; ++i) node32[16 * t + i] = (i == 0 || i == 4 || i == 8) ? 1.f : 0.f;
+    for (int c = 0; c < 3; ++c) node32[16 * t + 12 + c] = g_src[3 * t + c];
+    node32[16 * t + 15] = 0.f;
+  }
   if (t >= m * n_nbr) return;
   int l = nbr_src[t];
   if (l < -1 || l >= m || l == t / n_nbr) {
@@ -284,16 +291,6 @@ __global__ void k_graph_in(int m, int n_nbr, const float* g_src, const int32_t* 
     l = -1;
   }
   nbr[t] = l;
-}
-__global__ void k_init_nodes(int m, const float* g, double* Rt64, float* node32) {
-  pdl_wait();   // programmatic dependent launch (common.cuh)
-  pdl_trigger();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  for (int i = 0; i < 12; ++i) Rt64[12 * j + i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
-  for (int i = 0; i < 12; ++i) node32[16 * j + i] = (float)Rt64[12 * j + i];
-  for (int c = 0; c < 3; ++c) node32[16 * j + 12 + c] = g[3 * j + c];
-  node32[16 * j + 15] = 0.f;
 }
 __global__ void k_set_nodes(int m, const float* Rt, double* Rt64, float* node32) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -704,7 +701,8 @@ static mis_status set_graph_impl(mis_ctx* c, int32_t m, mis_mem mem, const float
   {
     ProfScope ps(c, P_IO, 1);
     launch_pdl(k_graph_in, dim3(nb(std::max<int64_t>((int64_t)m * nn, 3 * (int64_t)m))), dim3(256), 0, c->st, m, nn,
-               g_src, nbr_src, c->g.as<float>(), c->nbr.as<int32_t>(), flag);
+               g_src, nbr_src, c->g.as<float>(), c->nbr.as<int32_t>(), flag, c->Rt64.as<double>(),
+               c->node32.as<float>());
   }
   ModelView md = model_view(c);
   const int64_t n = c->n;
@@ -747,11 +745,7 @@ static mis_status set_graph_impl(mis_ctx* c, int32_t m, mis_mem mem, const float
     // fails with MIS_E_ARG)
     c->graph_check = true;
   }
-  {
-    ProfScope ps(c, P_IO, 1);
-    launch_pdl(k_init_nodes, dim3(nb(m)), dim3(256), 0, c->st, m, c->g.as<float>(), c->Rt64.as<double>(), c->node32.as<float>());
-  }
-  TRY(c, cudaGetLastError());
+  TRY(c, cudaGetLastError());   // (the identity node states were written by k_graph_in)
   TRY(c, run_build_order(c));
   c->have_graph = true;
   return MIS_OK;
