@@ -43,6 +43,12 @@
 namespace mis {
 namespace {
 
+#ifndef MIS_UMMA_ROWS
+#define MIS_UMMA_ROWS 32   // operand rows per round (multiple of 8)
+#endif
+#ifndef MIS_UMMA_NS
+#define MIS_UMMA_NS 2      // staging stages
+#endif
 template <int K>
 struct UM {
   static constexpr int P = K * (K + 1) / 2;
@@ -53,12 +59,15 @@ struct UM {
   static constexpr int NC = 64, NE = 48;                                   // MMA N: the hi features
   static constexpr int NT = 2;                                             // TMEM stages of 128 columns
   static_assert(8 * GC <= NC && 8 * GE <= NE, "accumulator columns");
-  static constexpr int ROWS = 32, KSTEPS = ROWS / 8;
-  static constexpr int OB = KSTEPS * BLK + 16 * 288;                       // + slack: A reads 16 groups
+  static constexpr int ROWS = MIS_UMMA_ROWS, KSTEPS = ROWS / 8;
+  // + slack after the last K-step block: an M = 64 A operand reads 8 groups from its start (at most
+  // group 2 GC + GE), an N = 64 / 48 B operand 8 / 6: at most 2 GC + GE + 8 - NG groups past the block
+  static constexpr int SLACK = 2 * GC + GE + 8 - NG;                       // = 8 - GE groups
+  static constexpr int OB = KSTEPS * BLK + SLACK * 288;
   static constexpr int NPL = K + 2;                                         // staging: K + 2 planes x 128
   static constexpr int SLW = (4 * P + 31 + 15) & ~15, NDW = (4 * K + 31 + 15) & ~15;   // slot / node windows
   static constexpr int STG = NPL * 128 * 16 + SLW + NDW;
-  static constexpr int NS = 2;                                             // staging stages
+  static constexpr int NS = MIS_UMMA_NS;                                   // staging stages
   static constexpr int RT = 52 * P + 20 * K, NITEM = 13 * P + 6 * K;
   static constexpr int NMETA = P + K;
   // dynamic shared memory map (bytes)
