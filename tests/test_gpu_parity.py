@@ -188,14 +188,16 @@ def test_system_parity_k5_to_k7(k):
     check_system(gs, osys, m)
 
 
-def test_k_gt4_fp32_k3b_path():
-    """The FP32 register-tile K3b (MIS_K3B_UMMA=0, the alternative to the tcgen05 kernel for k > 4)
-    through the same k > 4 system and registration gates, in a subprocess (the switch is read once)."""
+@pytest.mark.parametrize("switch", ["MIS_K3B_UMMA", "MIS_K3A_CHUNKED"])
+def test_k_gt4_alternative_paths(switch):
+    """The k > 4 alternatives through the same k > 4 system and registration gates, in a subprocess
+    (the switches are read once): MIS_K3B_UMMA=0, the FP32 register-tile K3b instead of the tcgen05
+    one; MIS_K3A_CHUNKED=0, the per-point K3a (sparse factor state) feeding the tcgen05 K3b."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MIS_K3B_UMMA="0")
+    env = dict(os.environ, **{switch: "0"})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
                         "k8_point_weight or k5_to_k7 or c5_shape"],
