@@ -178,9 +178,13 @@ def run_mis(args, rank, world, local_rank):
     h2d_bytes = sum(int(t.numel() * t.element_size()) for t in [depth_h, rgb_h, fs_h, fd_h]) + 48
     rep_bytes = M.C.sizeof(M.mis_report)
 
+    stage_colour = os.environ.get("MIS_BENCH_STAGE_COLOUR", "1") != "0"
+
     def step_e2e():
         M.mis_set_model(ctx.ptr, st["xyz"], st["nrm"], st["rgb"], st["weight"], st["stamp"], st["ids"], capacity=cap)
         M.mis_set_graph(ctx.ptr, g_d, nbr_d, st["knn_idx"], st["knn_w"])
+        if stage_colour:
+            M.mis_stage_colour(ctx.ptr, rgb_h)   # the colour upload overlaps the registration
         rep = M.mis_register(ctx.ptr, depth_h, intr, pose, fs_h, fd_h, report=True)   # D2H of the report
         M.mis_warp(ctx.ptr)
         n_out, _ = M.mis_fuse(ctx.ptr, rgb_h, 1)

@@ -262,6 +262,13 @@ mis_status mis_warp(mis_ctx* ctx, mis_mem mem, float* xyz_cam, float* nrm_cam);
 mis_status mis_fuse(mis_ctx* ctx, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out,
                     int64_t stats[4]);
 
+/* Start the upload of the next mis_fuse's host colour (H x W x 3 float, the current camera's H x W)
+ * now, on the context's copy stream, so it overlaps whatever is issued before the fusion (e.g. the
+ * registration); a following mis_fuse with the same host pointer uses the staged copy.  The buffer
+ * must stay unchanged until that mis_fuse returns.  MIS_E_ARG: rgb NULL, a device pointer (device
+ * colours are read in place anyway) or no frame size known yet (before the first frame). */
+mis_status mis_stage_colour(mis_ctx* ctx, const float* rgb);
+
 /* NEXT-1: Alg. 3 point filtering with the grid-box downsampling of
  * P:597 (readings A30-A34).  The model points are binned into the boxes
  * (floor(x/grid_mm), floor(y/grid_mm), floor(z/grid_mm)) of the world frame (fp32

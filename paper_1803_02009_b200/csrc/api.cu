@@ -754,6 +754,7 @@ static mis_status set_graph_impl(mis_ctx* c, int32_t m, mis_mem mem, const float
 
 // defer: mis_register only -- K1 is queued behind the frame's pattern readback so it runs
 // while the host waits for it (the depth is still read within the same API call)
+static cudaError_t issue_colour_copy(Ctx* c, const float* rgb);
 static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it,
                                  const float pose[12], bool defer);
 mis_status mis_set_frame(mis_ctx* c, mis_mem mem, const float* depth_mm, const mis_intrinsics* it, const float pose[12]) {
@@ -789,6 +790,10 @@ static mis_status set_frame_impl(mis_ctx* c, mis_mem mem, const float* depth_mm,
     TRY(c, cudaMemcpyAsync(c->depth.p, depth_mm, px * 4, cudaMemcpyHostToDevice, c->st_copy));
     TRY(c, cudaEventRecord(c->ev_depth_ready, c->st_copy));
     TRY(c, cudaStreamWaitEvent(c->st, c->ev_depth_ready, 0));
+  }
+  if (c->rgb_pending) {   // a staged colour (mis_stage_colour): its upload right behind the depth's
+    TRY(c, issue_colour_copy(c, c->rgb_pending));
+    c->rgb_pending = nullptr;
   }
   c->frame_src = dsrc;
   c->frame_pending = true;
@@ -1402,6 +1407,34 @@ mis_status mis_dbg_fuse_register(mis_ctx* c, int64_t* owner, uint8_t* why) {
   return MIS_OK;
 }
 
+// the host colour's upload on the copy stream, after the previous fusion has read the buffer
+static cudaError_t issue_colour_copy(Ctx* c, const float* rgb) {
+  const size_t px = (size_t)c->W * c->H;
+  cudaError_t e;
+  if ((e = ensure(c, c->rgb_obs, px * 12)) != cudaSuccess) return e;
+  if ((e = copy_stream(c)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(c->st_copy, c->ev_rgb_free, 0)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, cudaMemcpyHostToDevice, c->st_copy)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(c->ev_rgb_ready, c->st_copy)) != cudaSuccess) return e;
+  c->rgb_staged = rgb;
+  return cudaSuccess;
+}
+
+mis_status mis_stage_colour(mis_ctx* c, const float* rgb) {
+  if (!c) return MIS_E_ARG;
+  if (!rgb) return fail(c, MIS_E_ARG, "stage_colour: rgb is NULL");
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, rgb) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+    return fail(c, MIS_E_ARG, "stage_colour: a device pointer (device colours are read in place)");
+  cudaGetLastError();   // (a pageable host pointer may leave an error on older drivers)
+  if ((size_t)c->W * c->H == 0) return fail(c, MIS_E_ARG, "stage_colour: no frame size known yet");
+  // issued by the next frame upload right behind its depth (the registration needs the depth first),
+  // or by mis_fuse if no frame comes in between
+  c->rgb_pending = rgb;
+  c->rgb_staged = nullptr;
+  return MIS_OK;
+}
+
 mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_index, int64_t* n_out, int64_t stats[4]) {
   if (!c || !n_out) return MIS_E_ARG;
   if (!c->have_graph || !c->have_frame) return fail(c, MIS_E_STATE, "no graph or frame");
@@ -1412,14 +1445,13 @@ mis_status mis_fuse(mis_ctx* c, mis_mem mem, const float* rgb, int32_t frame_ind
   const float* rgb_dev = rgb;   // device colours are read in place by K11 / K12 (stream order)
   if (rgb && mem == MIS_MEM_HOST) {
     // on the copy stream, after the previous fusion read the buffer: the transfer overlaps the
-    // registration of the model points (K10); the colours are first read by K11
-    TRY(c, ensure(c, c->rgb_obs, px * 12));
-    TRY(c, copy_stream(c));
-    TRY(c, cudaStreamWaitEvent(c->st_copy, c->ev_rgb_free, 0));
-    TRY(c, cudaMemcpyAsync(c->rgb_obs.p, rgb, px * 12, cudaMemcpyHostToDevice, c->st_copy));
-    TRY(c, cudaEventRecord(c->ev_rgb_ready, c->st_copy));
+    // registration of the model points (K10); the colours are first read by K11.  Already issued
+    // by mis_stage_colour for this pointer: nothing to do
+    if (c->rgb_staged != rgb || c->rgb_obs.bytes < px * 12) TRY(c, issue_colour_copy(c, rgb));
     rgb_dev = c->rgb_obs.as<float>();
   }
+  c->rgb_staged = nullptr;
+  c->rgb_pending = nullptr;
   mis_status s;
   if ((s = fuse_register(c, rgb_dev, frame_index)) != MIS_OK) return s;
   const bool rgb_staged = rgb && mem == MIS_MEM_HOST;

@@ -32,6 +32,8 @@ struct Ctx {
   bool own_stream = false;
   cudaStream_t st_copy = nullptr;      // host->device copies of frame inputs (overlap the model ordering)
   cudaEvent_t ev_depth_free = nullptr, ev_depth_ready = nullptr, ev_rgb_free = nullptr, ev_rgb_ready = nullptr;
+  const float* rgb_staged = nullptr;    // host colour already on its way into rgb_obs (mis_stage_colour)
+  const float* rgb_pending = nullptr;   // staged colour whose upload the next frame upload issues
   int rank = 0, world = 1;
   void* nccl_comm = nullptr;
   std::string err;

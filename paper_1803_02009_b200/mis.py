@@ -85,6 +85,7 @@ _sig = {
     "mis_get_nbr": ([_V, C.c_int, _V], C.c_int),
     "mis_warp": ([_V, C.c_int, _V, _V], C.c_int),
     "mis_fuse": ([_V, C.c_int, _V, C.c_int32, _P(C.c_int64), _V], C.c_int),
+    "mis_stage_colour": ([_V, _V], C.c_int),
     "mis_filter": ([_V, C.c_float, C.c_int32, C.c_int32, C.c_float, _P(C.c_int64), _V], C.c_int),
     "mis_regenerate_nodes": ([_V, C.c_float, _P(C.c_int32)], C.c_int),
     "mis_get_model": ([_V, C.c_int, _V, _V, _V, _V, _V, _V, _V, _V, _P(C.c_int64)], C.c_int),
@@ -284,6 +285,14 @@ def mis_fuse(ctx, rgb=None, frame_index=0):
     stats = np.zeros(4, np.int64)
     _check(ctx, _lib.mis_fuse(ctx, _mem_of(rgb), _ptr(rgb, np.float32), frame_index, C.byref(n_out), _ptr(stats)))
     return int(n_out.value), stats
+
+
+def mis_stage_colour(ctx, rgb):
+    """Start the upload of the next mis_fuse's host colour now (overlapping the registration); a
+    following mis_fuse(ctx, rgb) with the same host array uses the staged copy.  Host arrays only."""
+    if _mem_of(rgb) != MIS_MEM_HOST:
+        raise ValueError("mis_stage_colour takes a host array (device colours are read in place)")
+    _check(ctx, _lib.mis_stage_colour(ctx, _ptr(rgb, np.float32)))
 
 
 def mis_filter(ctx, grid_mm, frame_index, tau_time=10, tau_weight=3.0):

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 M = pytest.importorskip("paper_1803_02009_b200.mis")
 
 
-def _run(sc, pb, host):
+def _run(sc, pb, host, stage=False):
     torch = pytest.importorskip("torch")
     prm = M.mis_default_params(k=pb.k, n_nbr=pb.n_nbr)
     ctx = M.Context(prm)
@@ -32,6 +32,8 @@ def _run(sc, pb, host):
     depth, rgb, fs, fd = cv(sc["depth"]), cv(sc["rgb_obs"]), cv(pb.fsrc), cv(pb.fdst)
     energies, sizes = [], []
     for frame in (1, 2):
+        if stage and frame == 2:   # the colour upload issued before the registration (mis_stage_colour)
+            M.mis_stage_colour(ctx.ptr, rgb)
         rep = M.report_dict(M.mis_register(ctx.ptr, depth, intr, sc["pose"], fs, fd))
         assert rep["status"] == 0
         energies.append(rep["energy"][:, 4])
@@ -55,3 +57,20 @@ def test_host_inputs_match_device_inputs():
     for (na, sa), (nb, sb) in zip(sh, sd):
         assert na == nb and (sa == sb).all()
     assert (xh == xd).all() and (ch == cd).all()
+
+
+def test_staged_colour_matches_device_inputs():
+    """mis_stage_colour (the next fusion's host colour uploaded while the registration runs) gives the
+    same fused model, bit for bit, as device colours; its argument errors."""
+    torch = pytest.importorskip("torch")
+    sc, pb, fr, _ = scene_problem("c2")
+    es, ss, xs, cs = _run(sc, pb, True, stage=True)
+    ed, sd, xd, cd = _run(sc, pb, False)
+    for (na, sa), (nb, sb) in zip(ss, sd):
+        assert na == nb and (sa == sb).all()
+    assert (xs == xd).all() and (cs == cd).all()
+    ctx = M.Context(M.mis_default_params())
+    with pytest.raises(M.MisError):   # no frame size known yet
+        M.mis_stage_colour(ctx.ptr, np.zeros((4, 4, 3), np.float32))
+    with pytest.raises(ValueError):   # device colours are read in place, not staged
+        M.mis_stage_colour(ctx.ptr, torch.zeros((4, 4, 3), device="cuda"))
