@@ -7,11 +7,11 @@ c4 (2M points, ~4000 nodes, 1280x1024): whole-problem association and normal
 equations (block-by-block, sparse), and MIRROR registration on the solver the
 library picks at that size (the grid-cooperative PCG: the system does not fit one
 16-CTA cluster).
-c5 (10M points, ~16k nodes, k=8): the oracle's brute-force skinning of the whole
-model takes ~10 min on one core, so the oracle runs on a seeded sample of 20k
-points one by one (skinning, association -- a point's association depends only on
-its own inputs) and the whole-problem registration is checked through properties
-that hold at any size (monotone energy, finite state, symmetric system).
+c5 (10M points, ~16k nodes, k=8): the device skinning and association on a seeded
+sample of 20k points one by one (a point's association depends only on its own
+inputs), properties that hold at any size (monotone energy, finite state, symmetric
+system), and -- with the oracle on every host core (~75 s on the GPU box) -- the
+whole-problem normal equations block by block and the MIRROR registration.
 
 Gates as in test_gpu_parity.py.
 """
@@ -235,3 +235,39 @@ def test_c5_register_properties(c5):
     assert np.isfinite(Rg).all()
     R = Rg[:, :9].reshape(-1, 3, 3)
     assert np.abs(R @ R.transpose(0, 2, 1) - np.eye(3)).max() < 1e-6     # SE(3) state stays on the manifold
+
+
+# ------------------------------------------------------------------ c5: the whole problem on all host cores
+def test_c5_system_and_register_full():
+    """BASELINE's largest config (10M points, k = 8: the tcgen05 K3b, chunked sparse K3a, grid PCG) against
+    the oracle on the WHOLE problem: the oracle skins all 10M points and assembles / registers in fp64 on
+    every host core (or_set_threads changes only its summation order, tests/test_oracle_pins.py).  The
+    normal equations block by block under a random field (gates of test_system_full), then the MIRROR
+    registration in bench.py's launch configuration (gates of test_register_full_mirror)."""
+    import os
+    O.set_threads(os.cpu_count() or 1)
+    try:
+        sc, pb, fr, _ = scene_problem("c5")
+        ctx = make_ctx(sc, pb)
+        m = pb.g.shape[0]
+        Rt = state_f32(node_state("random", pb.g, seed=61))
+        M.mis_dbg_set_nodes(ctx.ptr, Rt.astype(np.float32))
+        gs = M.mis_dbg_system(ctx.ptr, m)
+        prm = oracle_params(ctx.params)
+        osys = O.system(prm, pb, fr, Rt)
+        osys["prm"] = prm
+        check_system_sparse(gs, osys, m)
+        del gs, osys
+        ctx = make_ctx(sc, pb, flags=M.MIS_F_FINAL_ENERGY)
+        rep = M.report_dict(M.mis_register(ctx.ptr))
+        assert rep["status"] == 0
+        Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+        Ro, Eo, nao = O.register(oracle_params(ctx.params), pb, fr)
+    finally:
+        O.set_threads(1)
+    terr = np.linalg.norm(Rg[:, 9:] - Ro[:, 9:], axis=1)
+    rerr = np.array([rot_err(Rg[j, :9].reshape(3, 3), Ro[j, :9].reshape(3, 3)) for j in range(m)])
+    assert terr.max() < 0.01, terr.max()                   # 1e-5 m
+    assert rerr.max() < 1e-4, rerr.max()
+    assert np.allclose(rep["energy"][:, 4], Eo[:, 4], rtol=1e-3)
+    assert np.abs(rep["n_assoc"] - nao).max() <= max(3, 1e-4 * pb.xyz.shape[0])
