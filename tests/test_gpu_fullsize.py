@@ -21,6 +21,7 @@ import pytest
 import oracle as O
 from paper_1803_02009_b200 import synth
 from tests.common import check_fusion, scene_problem, state_f32
+from tests.test_gpu_lm import _check_lm
 from tests.test_gpu_parity import make_ctx, node_state, oracle_params, order_of, rot_err
 
 pytestmark = pytest.mark.gpu
@@ -247,7 +248,7 @@ def test_c5_system_and_register_full():
     import os
     O.set_threads(os.cpu_count() or 1)
     try:
-        sc, pb, fr, _ = scene_problem("c5")
+        sc, pb, fr, _ = problem("c5")
         ctx = make_ctx(sc, pb)
         m = pb.g.shape[0]
         Rt = state_f32(node_state("random", pb.g, seed=61))
@@ -271,3 +272,29 @@ def test_c5_system_and_register_full():
     assert rerr.max() < 1e-4, rerr.max()
     assert np.allclose(rep["energy"][:, 4], Eo[:, 4], rtol=1e-3)
     assert np.abs(rep["n_assoc"] - nao).max() <= max(3, 1e-4 * pb.xyz.shape[0])
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_lm_full(cfg):
+    """MIS_F_LM in bench.py's `lm` leg configuration at C4 and C5 (the grid PCG carries the accept /
+    reject decisions; C5 with the tcgen05 K3b) against the oracle's LM on every host core: decisions up
+    to the first near tie, trial energies, and the nodes when no tie occurs (test_gpu_lm.py gates)."""
+    import os
+    O.set_threads(os.cpu_count() or 1)
+    try:
+        sc, pb, fr, _ = problem(cfg)
+        G = sc["cfg"].gn_iters
+        ctx = make_ctx(sc, pb, flags=M.MIS_F_LM)
+        rep = M.report_dict(M.mis_register(ctx.ptr))
+        assert rep["status"] == 0 and rep["solver_cluster"] == 0
+        m = pb.g.shape[0]
+        Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+        Ro, Eo, _, acco = O.register(oracle_params(ctx.params, lm=1, lm_mu0=1e-3, gn_iters=G), pb, fr,
+                                     with_accepted=True)
+    finally:
+        O.set_threads(1)
+    ties = _check_lm(rep, Eo, acco, G)
+    if not ties:
+        terr = np.linalg.norm(Rg[:, 9:] - Ro[:, 9:], axis=1)
+        rerr = np.array([rot_err(Rg[j, :9].reshape(3, 3), Ro[j, :9].reshape(3, 3)) for j in range(m)])
+        assert terr.max() < 0.01 and rerr.max() < 1e-4, (terr.max(), rerr.max())
