@@ -127,16 +127,24 @@ def test_affine_errors():
         M.Context(M.mis_default_params(w_rot=float("nan")))
 
 
-def test_affine_register_full_c3():
-    """NEXT-4 at the bench configuration (C3: 300k points, 999 nodes, 5 GN x 10 PCG, features)."""
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_affine_register_full(cfg):
+    """NEXT-4 at the bench configurations (C3: 300k points, 999 nodes, 5 GN x 10 PCG; C4: 2M points,
+    ~4000 nodes, 5 GN x 10 PCG; features); the oracle on every host core.  A entries: 1e-4 at C3, the
+    module's 3e-4 (reading A46) at C4."""
+    import os
     from tests.test_gpu_fullsize import problem
-    sc, pb, fr, _ = problem("c3")
-    ctx = aff_ctx(sc, pb)
-    rep = M.report_dict(M.mis_register(ctx.ptr))
-    assert rep["status"] == 0
-    m = pb.g.shape[0]
-    Ag = M.mis_get_nodes_f64(ctx.ptr, m)
-    Ao, Eo, nao = O.register_aff(oprm(ctx), pb, fr)
+    O.set_threads(os.cpu_count() or 1)
+    try:
+        sc, pb, fr, _ = problem(cfg)
+        ctx = aff_ctx(sc, pb)
+        rep = M.report_dict(M.mis_register(ctx.ptr))
+        assert rep["status"] == 0
+        m = pb.g.shape[0]
+        Ag = M.mis_get_nodes_f64(ctx.ptr, m)
+        Ao, Eo, nao = O.register_aff(oprm(ctx), pb, fr)
+    finally:
+        O.set_threads(1)
     assert np.linalg.norm(Ag[:, 9:] - Ao[:, 9:], axis=1).max() < 0.01
-    assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < 1e-4
+    assert np.abs(Ag[:, :9] - Ao[:, :9]).max() < (1e-4 if cfg == "c3" else 3e-4)
     assert np.allclose(rep["energy"][:, 4], Eo[:, 5], rtol=1e-3)

@@ -114,20 +114,27 @@ def test_pose_errors():
         M.Context(M.mis_default_params(w_r=-1.0))
 
 
-def test_pose_register_full_c3():
-    """NEXT-2 at the bench configuration (C3: 300k points, 999 nodes, 5 GN x 10 PCG, ORB features)
-    with the paper's prior weights and a wrong ORB-SLAM pose: nodes and pose against the oracle."""
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_pose_register_full(cfg):
+    """NEXT-2 at the bench configurations (C3: 300k points, 999 nodes, 5 GN x 10 PCG; C4: 2M points,
+    ~4000 nodes, 5 GN x 10 PCG; ORB features) with the paper's prior weights and a wrong ORB-SLAM pose:
+    nodes and pose against the oracle (on every host core: only its summation order changes)."""
+    import os
     from tests.test_gpu_fullsize import problem
-    sc, pb, fr, _ = problem("c3")
-    prior = perturbed_pose(np.array(fr.s.pose[:]))
-    ctx, sc2 = joint_ctx(sc, pb, prior)
-    rep = M.report_dict(M.mis_register(ctx.ptr))
-    assert rep["status"] == 0
-    m = pb.g.shape[0]
-    Rg = M.mis_get_nodes_f64(ctx.ptr, m)
-    pg = M.mis_get_pose(ctx.ptr)
-    prm = oracle_params(ctx.params, joint_pose=1, w_r=ctx.params.w_r, w_p=ctx.params.w_p)
-    Ro, po, Eo, nao = O.register_pose(prm, pb, ofr(sc2))
+    O.set_threads(os.cpu_count() or 1)
+    try:
+        sc, pb, fr, _ = problem(cfg)
+        prior = perturbed_pose(np.array(fr.s.pose[:]))
+        ctx, sc2 = joint_ctx(sc, pb, prior)
+        rep = M.report_dict(M.mis_register(ctx.ptr))
+        assert rep["status"] == 0
+        m = pb.g.shape[0]
+        Rg = M.mis_get_nodes_f64(ctx.ptr, m)
+        pg = M.mis_get_pose(ctx.ptr)
+        prm = oracle_params(ctx.params, joint_pose=1, w_r=ctx.params.w_r, w_p=ctx.params.w_p)
+        Ro, po, Eo, nao = O.register_pose(prm, pb, ofr(sc2))
+    finally:
+        O.set_threads(1)
     terr = np.linalg.norm(Rg[:, 9:] - Ro[:, 9:], axis=1)
     rerr = np.array([rot_err(Rg[j, :9].reshape(3, 3), Ro[j, :9].reshape(3, 3)) for j in range(m)])
     assert terr.max() < 0.01 and rerr.max() < 1e-4, (terr.max(), rerr.max())
